@@ -1,0 +1,372 @@
+"""Benchmark: RAC-ADMM sweeps/sec (and time to 1e-6) on one B200, vs the CPU reference path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config C]
+
+A "step" is one RAC sweep (one pass of the Gauss-Seidel chain over all p
+blocks, including that sweep's block assembly, block Grams and factorizations).
+The headline workload is BASELINE.json configs[1] (LASSO, D 10000x2000, s=100);
+`--config` selects another BASELINE config.  Multi-GPU: the sweep is a
+sequential Gauss-Seidel chain, so N>1 runs N independent replicas (one per GPU,
+`scaling: weak`) — see DESIGN.md "Multi-GPU".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK_GBS = 6650.0
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sms, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sms.append(float(parts[1]))
+                maxes.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None,
+                "sm_max_mhz": max(maxes) if maxes else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ------------------------------------------------------------------ distributed
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def dist_max(value: float, world: int, device=None) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ workloads
+def en_case(cfg: int):
+    from paper_1907_01995_b200 import configs
+    return configs.GENERATORS[cfg]()
+
+
+def en_flops_bytes(m, n, s):
+    """Algorithmic work per sweep: Gram m*n*(s+1) flop, D read 8*m*n bytes."""
+    return float(m) * n * (s + 1), 8.0 * m * n
+
+
+def fp64_peak_tflops(torch) -> float:
+    """Measured cuBLAS DGEMM (8192^3 fp64) on this device, best of 5 — FP64 roofline denominator."""
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn_like(a)
+    torch.matmul(a, b)
+    torch.cuda.synchronize()
+    best = math.inf
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2.0 * 8192 ** 3 / (best * 1e-3) / 1e12
+
+
+def cpu_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        blas = [i["num_threads"] for i in info if i.get("internal_api") in ("openblas", "mkl", "blis")]
+        if blas:
+            return int(max(blas))
+    except Exception:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
+def cpu_en_rate(case, sweeps: int) -> tuple[float, float]:
+    """Oracle (numpy restatement of racml fit) sweeps/s over `sweeps` fixed sweeps."""
+    from oracle import rac_oracle as ro
+    t0 = time.perf_counter()
+    ro.en_fit(case.X, case.y, case.lam, case.alpha, case.gamma, case.block_size, sweeps,
+              seed=case.seed, tol=None)
+    dt = time.perf_counter() - t0
+    return sweeps / dt, dt
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference algorithm on the host cores (oracle port)."""
+    case = en_case(args.config)
+    if rank != 0:
+        return 0
+    m, n = case.X.shape
+    cpu_en_rate(case, max(1, args.warmup // 3))
+    total = 0.0
+    for _ in range(args.steps):
+        _, dt = cpu_en_rate(case, 1)
+        total += dt
+    rate = args.steps / total
+    line = {
+        "impl": "reference", "metric": "rac_admm_sweeps_per_sec", "value": rate,
+        "unit": "sweeps/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) seed-0 recipe)",
+        "config": {"workload": case.name, "m": m, "n": n, "block_size": case.block_size},
+        "cpu_baseline": {"value": rate, "unit": "sweeps/s", "cores": cpu_threads(), "kind": "port",
+                         "sample": f"{args.steps} single sweeps of {case.name} (oracle/rac_oracle.en_fit)"},
+        "e2e": {"value": rate, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args, world, rank, local):
+    import torch
+    from paper_1907_01995_b200 import _device, elastic_net as en
+    from paper_1907_01995_b200.problems import Mode
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    case = en_case(args.config)
+    m, n = case.X.shape
+    s = min(case.block_size, n)
+    p = -(-n // s)
+    flops, bytes_ = en_flops_bytes(m, n, s)
+
+    # ---------------- device-resident throughput (fixed sweeps, every sweep does full work)
+    solver = en.EnSolver(m, n, s, Mode.RAC, case.lam, case.alpha, case.gamma, device=local)
+    solver.set_data(case.X, case.y)
+    rng = np.random.default_rng(case.seed)
+    K, W = args.steps, args.warmup
+    perms = _device.PermutationFeeder(rng, n, dev).draw(W + K)
+    torch.cuda.synchronize()
+    solver.run(perms[:W], None)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    dist_barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    solver.run(perms[W:W + K], None)
+    e1.record()
+    torch.cuda.synchronize()
+    dist_barrier(world)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    ms = dist_max(ms, world, dev)
+    value = world * K / (ms * 1e-3)
+
+    # ---------------- per-stage breakdown (separate sweeps, CUDA events between stages)
+    lib = solver.lib
+    lib.rac_en_set_timing(solver.h, 1)
+    more = _device.PermutationFeeder(rng, n, dev).draw(K)
+    solver.run(more, None)
+    stage = (np.ctypeslib.ctypes.c_double * 4)()
+    nt = np.ctypeslib.ctypes.c_int32()
+    lib.rac_en_timing(solver.h, stage, nt)
+    stages = {k: float(v) / max(nt.value, 1) for k, v in zip(("assembly", "gram", "factor", "chain"), stage)}
+    # chain phase trace (CTA 0 %globaltimer at each phase boundary of one sweep)
+    lib.rac_en_set_timing(solver.h, 2)
+    solver.run(_device.PermutationFeeder(rng, n, dev).draw(1), None)
+    torch.cuda.synchronize()
+    tbuf = (np.ctypeslib.ctypes.c_int64 * (2 + 7 * p))()
+    lib.rac_en_trace(solver.h, tbuf, 2 + 7 * p)
+    tv = np.array(tbuf[:2 + 6 * p], dtype=np.float64) / 1e3   # us
+    ph = np.diff(tv[1:]).reshape(p, 6) if p > 0 else np.zeros((0, 6))
+    chain_trace = {"first_row_phase_us": float(tv[1] - tv[0]),
+                   "per_block_us": {k: float(v) for k, v in zip(
+                       ("barrier1", "S1_reduce", "barrier2", "S2_solve", "barrier3", "row_phase"),
+                       ph.mean(axis=0))}}
+    lib.rac_en_set_timing(solver.h, 0)
+    solver.close()
+    del perms, more
+
+    # ---------------- time to tolerance (device-resident inputs, host PCG64 stream as in fit)
+    ttt = None
+    if case.tol is not None:
+        sol2 = en.EnSolver(m, n, s, Mode.RAC, case.lam, case.alpha, case.gamma, device=local)
+        sol2.set_data(case.X, case.y)
+        rng2 = np.random.default_rng(case.seed)
+        feeder = _device.PermutationFeeder(rng2, n, dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        done = 0
+        while done < case.iters:
+            k = min(8, case.iters - done)
+            sol2.run(feeder.draw(k), case.tol)
+            done += k
+            it, conv, res, _ = sol2.progress()
+            if conv:
+                break
+        t_tol = time.perf_counter() - t0
+        ttt = {"seconds": t_tol, "sweeps": it, "residual": res, "converged": bool(conv),
+               "tol": case.tol}
+        sol2.close()
+
+    # ---------------- end to end through the public API (host arrays, H2D/D2H inside)
+    spec = en.ElasticNetSpec(lam=case.lam, alpha=case.alpha, gamma=case.gamma,
+                             block_size=case.block_size, iters=K, seed=case.seed, tol=None)
+    en.fit(case.X[:64], case.y[:64], en.ElasticNetSpec(lam=case.lam, alpha=case.alpha, gamma=case.gamma,
+                                                       block_size=case.block_size, iters=1))
+    torch.cuda.synchronize()
+    dist_barrier(world)
+    t0 = time.perf_counter()
+    en.fit(case.X, case.y, spec)
+    t_e2e = time.perf_counter() - t0
+    t_e2e = dist_max(t_e2e, world, dev)
+    e2e = {"value": world * K / t_e2e, "unit": "sweeps/s",
+           "h2d_bytes_per_step": int((8 * m * n + 8 * m) / K + 8 * n),
+           "d2h_bytes_per_step": int((3 * 8 * n + 8 * 2 * K + 16) / K)}
+
+    # ---------------- roofline of the dominant kernel
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
+    fp64 = fp64_peak_tflops(torch)
+    dom = max(stages, key=stages.get)
+    if dom == "chain":
+        achieved = 2.0 * bytes_ / (stages["chain"] * 1e-3) / 1e9
+        roof = {"kernel": "en_chain_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm,
+                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                "algorithmic": "2 passes over D (8*m*n bytes each) per launch"}
+    else:
+        achieved = flops / (stages["gram"] * 1e-3) / 1e12
+        roof = {"kernel": "gram_kernel", "bound": "tensor", "achieved": achieved, "peak": fp64,
+                "unit": "TFLOP/s", "frac": achieved / fp64, "traffic": None,
+                "algorithmic": "m*n*(s+1) flop per launch (symmetric SYRK of all p blocks)"}
+
+    # ---------------- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r1, dt1 = cpu_en_rate(case, 1)
+        sweeps = int(max(1, min(60, 15.0 / max(dt1, 1e-3))))
+        rate, dt = cpu_en_rate(case, sweeps)
+        cpu = {"value": rate, "unit": "sweeps/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"{sweeps} sweeps of {case.name} via oracle/rac_oracle.en_fit ({dt:.1f} s)"}
+
+    line = {
+        "metric": "rac_admm_sweeps_per_sec", "value": value, "unit": "sweeps/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) seed-0 recipe)",
+        "config": {"workload": case.name, "m": m, "n": n, "block_size": s, "blocks": p,
+                   "mode": "rac", "l2": "inputs larger than L2 (D = %.0f MB)" % (8 * m * n / 1e6)
+                   if 8 * m * n > 126e6 else "D fits in L2 (no flush)",
+                   "parallelism": f"replicas x{world}"},
+        "stage_ms_per_sweep": stages,
+        "chain_trace": chain_trace,
+        "time_to_tol": ttt,
+        "e2e": e2e,
+        "roofline": roof,
+        "fp64_dgemm_tflops_measured": fp64,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "gpu_launches": 4 * K,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        rc = run_reference(args, world, rank)
+    else:
+        rc = run_b200(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

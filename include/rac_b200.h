@@ -1,0 +1,164 @@
+/*
+ * rac_b200.h — C ABI of the B200-native RAC-MBADMM sweep (arXiv 1907.01995).
+ *
+ * The reference (`racml` 0.1.0, pure Python over numpy/scipy) has no
+ * FFI/plugin layer: its boundary is three Python entry points.  This ABI sits
+ * *underneath* their drop-in replacements (paper_1907_01995_b200.{elastic_net,
+ * svm,engine}) and replaces the numpy/LAPACK calls each of them makes.  Every
+ * entry point cites the reference code it replaces.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers unless the name ends in `_host`.
+ *   - All arithmetic is IEEE FP64; indices are int64 on input, int32 inside.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *   - Every function returns RAC_OK (0) or an error code; no exceptions cross
+ *     the ABI.  rac_last_error() returns a thread-local message.
+ *   - Work is enqueued asynchronously on `stream` unless stated otherwise.
+ */
+#ifndef RAC_B200_H
+#define RAC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RAC_OK 0
+#define RAC_ERR_ARG 1          /* invalid argument (reference: ValueError)               */
+#define RAC_ERR_CUDA 2         /* CUDA runtime error / no sm_100 device                   */
+#define RAC_ERR_NOT_PD 3       /* block not positive definite (BlockDefinitenessError)    */
+#define RAC_ERR_UNSUPPORTED 4  /* shape outside what this build supports                  */
+
+/* sweep modes (problems.py:318-323 Mode) */
+#define RAC_MODE_RAC 0
+#define RAC_MODE_RP 1
+#define RAC_MODE_CYCLIC 2
+
+/* solve status (problems.py:326-329 Status) */
+#define RAC_STATUS_MAX_ITERS 0
+#define RAC_STATUS_CONVERGED 1
+#define RAC_STATUS_DIVERGED 2
+
+/* kernel kinds (svm.py:37-48 KernelSpec.kind) */
+#define RAC_KERNEL_LINEAR 0
+#define RAC_KERNEL_GAUSSIAN 1
+
+/* design-matrix layouts accepted by rac_en_set_data */
+#define RAC_LAYOUT_ROW_MAJOR 0 /* numpy C order, X[i*n + j]                                */
+#define RAC_LAYOUT_COL_MAJOR 1 /* Fortran order with leading dim m, X[i + j*m]             */
+
+const char* rac_version(void);
+const char* rac_last_error(void);
+/* 0 if `device` is an sm_100 part this library was built for. */
+int rac_device_check(int device);
+
+/* ------------------------------------------------------------------ K1
+ * Random without-replacement block assembly.
+ * Replaces problems.py:234-243 chunk_indices(rng.permutation(n), s) as used at
+ * elastic_net.py:195, svm.py:231, engine.py:318-319.  `perms` holds `count`
+ * permutations of 0..n-1 (int64, the host PCG64 stream); `idx_out` receives,
+ * per permutation, p = ceil(n/s) rows of s int32 indices, each row sorted
+ * ascending (the last row holds n - (p-1)s valid entries, the rest are -1). */
+int rac_chunk_sort(const int64_t* perms, int64_t n, int32_t s, int32_t count,
+                   int32_t* idx_out, void* stream);
+
+/* ------------------------------------------------------------------ K2/K3
+ * Batched block systems for one partition (p blocks of s indices):
+ *   sys_b = scale * V_b' V_b + shift * I         (elastic_net.py:210-212)
+ * where V_b gathers vectors idx[b*s + j] of V (vector k = V[k*ldv .. +len]).
+ * Then L_b = chol(sys_b) and inv_b = sys_b^{-1}, written to `inv`
+ * (p x s x s, row-major).  `info[b]` = 0, or k+1 if the k-th leading minor of
+ * block b is not positive (np.linalg.cholesky failure, elastic_net.py:213-219).
+ * `ws` must hold rac_gram_workspace_bytes(...) bytes. */
+size_t rac_gram_workspace_bytes(int64_t len, int32_t s, int32_t p);
+int rac_gram_inverse(const double* V, int64_t ldv, int64_t len, const int32_t* idx,
+                     int32_t s, int32_t p, int64_t n_valid, double scale, double shift,
+                     double* ws, double* inv, int32_t* info, void* stream);
+
+/* Elementwise z-prox (elastic_net.py:102-131, z_update): z = S(xi - g*beta, thr)/den. */
+int rac_z_prox(const double* beta, const double* xi, int64_t n, double gamma, double thr,
+               double den, double* z, void* stream);
+
+/* ------------------------------------------------------------------ fit()
+ * Elastic-net / LASSO / ridge sweep engine behind elastic_net.fit
+ * (elastic_net.py:150-232).  One context per solve. */
+typedef struct rac_en_ctx rac_en_ctx;
+
+int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t block_size, int32_t mode,
+                  double lam, double alpha, double gamma, void* stream);
+/* X: m x n design (layout RAC_LAYOUT_*), y: m.  Copies X into the context's
+ * column-major HBM layout and computes c = -X'y/m (elastic_net.py:177). */
+int rac_en_set_data(rac_en_ctx* ctx, const double* X, int32_t layout, const double* y);
+/* RP mode only: the fixed partition from one permutation of n
+ * (elastic_net.py:187-189); block systems are factored once. */
+int rac_en_set_partition(rac_en_ctx* ctx, const int64_t* perm);
+/* Enqueue `count` sweeps.  RAC: `perms` = count permutations of n.  RP: count
+ * permutations of p (block visit orders, elastic_net.py:197-198).  tol < 0
+ * means fixed sweeps (spec.tol None).  Sweeps after convergence are no-ops. */
+int rac_en_run(rac_en_ctx* ctx, const int64_t* perms, int32_t count, double tol);
+/* Synchronizes the stream.  iterations = sweeps executed so far. */
+int rac_en_progress(rac_en_ctx* ctx, int32_t* iterations_host, int32_t* converged_host,
+                    double* residual_host, int32_t* failed_block_host);
+/* Device-to-device copies of the iterate (any pointer may be NULL). */
+int rac_en_get(rac_en_ctx* ctx, double* beta, double* z, double* xi, double* r);
+/* per-sweep ||beta - z||_1 history (count = iterations) and gamma*||dz||_inf */
+int rac_en_history(rac_en_ctx* ctx, double* primal, double* dual, int32_t capacity);
+/* Optional per-stage CUDA-event timing of subsequent sweeps; rac_en_timing
+ * synchronizes and returns the summed milliseconds of [assembly, gram,
+ * factor, chain] over the timed sweeps, then resets. */
+int rac_en_set_timing(rac_en_ctx* ctx, int32_t enable);
+int rac_en_timing(rac_en_ctx* ctx, double* stage_ms_host4, int32_t* sweeps_host);
+/* enable >= 2 in rac_en_set_timing also records %globaltimer at every chain
+ * phase boundary of each sweep (CTA 0): [start, R0, then per block: bar, S1,
+ * bar, S2, bar, R] = 2 + 7p stamps (the last sweep's are kept). */
+int rac_en_trace(rac_en_ctx* ctx, int64_t* host, int32_t capacity);
+int rac_en_destroy(rac_en_ctx* ctx);
+
+/* ------------------------------------------------------------------ train()/solve()
+ * Dense box-QP sweep engine behind engine.solve (engine.py:322-405) and
+ * svm.train (svm.py:181-284): min 1/2 x'Hx + c'x  s.t. Ax = b, lo <= x <= hi. */
+typedef struct rac_qp_ctx rac_qp_ctx;
+
+/* ridge_rel > 0 adds ridge_rel * max(diag(M_b)) to every block matrix
+ * (svm.py:242-246 uses 1e-9).  running_residual != 0 reports the primal
+ * residual from the running Ax (svm.py:256,260) instead of recomputing. */
+int rac_qp_create(rac_qp_ctx** out, int64_t n, int64_t m, int32_t block_size, int32_t mode,
+                  double beta, double ridge_rel, void* stream);
+/* H: n x n row-major symmetric (may be NULL), A: m x n row-major (NULL iff m == 0),
+ * b: m, c: n, lower/upper: n (+-inf allowed).  Copies into context storage. */
+int rac_qp_set_problem(rac_qp_ctx* ctx, const double* H, const double* A, const double* b,
+                       const double* c, const double* lower, const double* upper);
+/* Use an externally owned H (e.g. the SVM Q built by rac_svm_build_q) without copying. */
+int rac_qp_borrow_h(rac_qp_ctx* ctx, const double* H);
+/* Divergence bar (engine.py:361-362): set_problem uses 1e8*max(primal0, 1);
+ * svm.train has no guard and passes +inf. */
+int rac_qp_set_divergence_bar(rac_qp_ctx* ctx, double bar);
+int rac_qp_set_partition(rac_qp_ctx* ctx, const int64_t* perm);   /* RP / CYCLIC */
+int rac_qp_run(rac_qp_ctx* ctx, const int64_t* perms, int32_t count, double tol_primal,
+               double tol_dual, int32_t fixed_iterations);
+int rac_qp_progress(rac_qp_ctx* ctx, int32_t* iterations_host, int32_t* status_host,
+                    int32_t* failed_block_host);
+int rac_qp_get(rac_qp_ctx* ctx, double* x, double* y, double* hx, double* ax);
+int rac_qp_history(rac_qp_ctx* ctx, double* primal, double* primal_l1, double* dual,
+                   int32_t capacity);
+int rac_qp_destroy(rac_qp_ctx* ctx);
+
+/* Label-weighted kernel matrix Q_ij = y_i y_j K(x_i, x_j) (svm.py:82-93,139),
+ * X: N x d row-major.  Built once with FP64 tensor-core tiles. */
+int rac_svm_build_q(const double* X, int64_t N, int64_t d, const double* labels, int32_t kind,
+                    double sigma, double* Q, void* stream);
+/* out_i = sum_j Q_ij * w_j (one HBM pass; used for the SVM bias, svm.py:287-305). */
+int rac_gemv(const double* Q, int64_t rows, int64_t cols, const double* w, double* out,
+             void* stream);
+
+/* Exact box-QP minimizer for ONE block on the device (engine.py:189-245),
+ * exposed for testing: M s x s row-major SPD, r, lo, hi -> x.  info as above. */
+int rac_box_block_min(const double* M, const double* r, const double* lo, const double* hi,
+                      int32_t s, double* x, int32_t* info, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAC_B200_H */

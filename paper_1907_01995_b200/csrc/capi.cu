@@ -1,0 +1,115 @@
+// C ABI plumbing: error reporting, version, device checks, small kernels.
+#include <stdarg.h>
+#include <algorithm>
+#include <stdio.h>
+
+#include "rac_internal.h"
+
+namespace rac {
+
+static thread_local char g_err[512] = {0};
+
+void clear_error() { g_err[0] = 0; }
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_cuda(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return RAC_OK;
+  return set_error(RAC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what); }
+
+int num_sms() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cached = v;
+  }
+  return cached;
+}
+
+// out = Q w  (rows x cols row-major): one warp per row, fixed-order reduction.
+__global__ void gemv_rows_kernel(const double* __restrict__ Q, int64_t rows, int64_t cols,
+                                 const double* __restrict__ w, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < rows; i += nw) {
+    const double* q = Q + i * cols;
+    double acc = 0.0;
+    for (int64_t j = lane; j < cols; j += 32) acc += q[j] * w[j];
+    acc = warp_sum(acc);
+    if (lane == 0) out[i] = acc;
+  }
+}
+
+int launch_gemv_rows(const double* Q, int64_t rows, int64_t cols, const double* w, double* out,
+                     cudaStream_t st) {
+  int blocks = (int)std::min<int64_t>((rows + 7) / 8, (int64_t)num_sms() * 8);
+  if (blocks < 1) blocks = 1;
+  gemv_rows_kernel<<<blocks, 256, 0, st>>>(Q, rows, cols, w, out);
+  return check_launch("gemv_rows");
+}
+
+__global__ void z_prox_kernel(const double* __restrict__ beta, const double* __restrict__ xi,
+                              int64_t n, double gamma, double thr, double den,
+                              double* __restrict__ z) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double a = sub(xi[i], mul(gamma, beta[i]));
+    z[i] = __ddiv_rn(neg_shrink(a, thr), den);
+  }
+}
+
+}  // namespace rac
+
+extern "C" const char* rac_version(void) { return "rac_b200 0.1.0 (sm_100a, fp64)"; }
+
+extern "C" const char* rac_last_error(void) { return rac::g_err; }
+
+extern "C" int rac_device_check(int device) {
+  using namespace rac;
+  clear_error();
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count <= device || device < 0)
+    return set_error(RAC_ERR_CUDA, "no CUDA device %d (%s)", device, cudaGetErrorString(e));
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return check_cuda(e, "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return set_error(RAC_ERR_CUDA, "device %d is sm_%d%d; this library is built for sm_100a",
+                     device, prop.major, prop.minor);
+  return RAC_OK;
+}
+
+extern "C" int rac_z_prox(const double* beta, const double* xi, int64_t n, double gamma,
+                          double thr, double den, double* z, void* stream) {
+  using namespace rac;
+  clear_error();
+  if (!beta || !xi || !z || n < 0) return set_error(RAC_ERR_ARG, "rac_z_prox: bad arguments");
+  if (n == 0) return RAC_OK;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+  z_prox_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(beta, xi, n, gamma, thr, den, z);
+  return check_launch("z_prox");
+}
+
+extern "C" int rac_gemv(const double* Q, int64_t rows, int64_t cols, const double* w, double* out,
+                        void* stream) {
+  using namespace rac;
+  clear_error();
+  if (!Q || !w || !out || rows < 0 || cols < 0) return set_error(RAC_ERR_ARG, "rac_gemv: bad arguments");
+  if (rows == 0) return RAC_OK;
+  return launch_gemv_rows(Q, rows, cols, w, out, (cudaStream_t)stream);
+}

@@ -1,0 +1,611 @@
+// Elastic-net / LASSO / ridge sweep engine behind elastic_net.fit
+// (elastic_net.py:150-232), sm_100a, FP64, everything HBM-resident.
+//
+// Per sweep (RAC):  K1 chunk-sort the host permutation -> K2 batched DMMA
+// block Grams -> K3 batched Cholesky/inverse -> K4 one cooperative launch
+// that runs the whole Gauss-Seidel chain over the p blocks:
+//
+//   R  (row phase, all CTAs, rows split across CTAs)
+//        r_i += X[i, blk_prev] . delta_prev            (elastic_net.py:223)
+//        t_i  = r_i - X[i, blk_next] . beta[blk_next]
+//        partial_cta[j] = sum_i X[i, blk_next[j]] t_i  (elastic_net.py:205)
+//   -- grid barrier --
+//   S1 rhs_j = -(c + (sum_cta partial)/m - xi - gamma z)   (elastic_net.py:206)
+//   -- grid barrier --
+//   S2 beta_new = inv_b rhs (elastic_net.py:222); delta = beta_new - beta;
+//      fused z-prox / dual / residual for the block's coordinates
+//      (elastic_net.py:225-228; bitwise-equivalent since every coordinate
+//      belongs to exactly one block and z/xi of other blocks are untouched)
+//   -- grid barrier --
+//
+// X is stored column-major with a leading dimension padded to 32 rows (zero
+// rows), so a block's column gather is a set of contiguous, coalesced reads.
+#include <algorithm>
+#include <vector>
+
+#include "rac_internal.h"
+#include "rac_rowphase.cuh"
+
+namespace rac {
+
+constexpr int ENT = RP_THREADS;   // threads per chain CTA
+constexpr int EN_QMAX = RP_QMAX;   // block_size <= EN_QMAX * ENT
+
+struct EnChainArgs {
+  const double* Xc;
+  int64_t ld, m;
+  int s, p, nrc;        // block size, blocks, row chunks
+  const int32_t* idx;   // [p][s] block table of this sweep
+  const int32_t* order; // [p] visit order (nullptr: identity)
+  const double* inv;    // [p][s][s]
+  const int32_t* info;  // [p]
+  const double* c;
+  double *beta, *z, *xi, *r;
+  double *partial, *rhs, *delta;
+  double *wsum, *wmax;  // per global warp
+  unsigned* bar;
+  int32_t* ctrl;        // [0] done, [1] iterations, [2] failed block + 1, [3] converged
+  double gamma, thr, den, mdiv, tol;
+  int sweep;
+  double *hist_p, *hist_d;
+  long long* trace;     // optional: %globaltimer at every phase boundary (CTA 0)
+};
+
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int RC>
+__global__ void __launch_bounds__(ENT) en_chain_kernel(EnChainArgs a) {
+  if (a.ctrl[0]) return;
+  extern __shared__ __align__(16) double esm[];
+  const int s = a.s;
+  const RowPhaseSmem w = carve_rowphase<RC>(esm, s);
+  __shared__ int bad;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int P = gridDim.x;
+  const int gw = blockIdx.x * (ENT / 32) + warp, GW = P * (ENT / 32);
+  unsigned target = 0;
+
+  if (tid == 0) {
+    bad = 0;
+    for (int t = 0; t < a.p; ++t) {
+      int b = a.order ? a.order[t] : t;
+      if (a.info[b]) { bad = b + 1; break; }
+    }
+  }
+  __syncthreads();
+  if (bad) {
+    if (blockIdx.x == 0 && tid == 0) { a.ctrl[2] = bad; a.ctrl[0] = 1; }
+    return;
+  }
+
+  double my_sum = 0.0, my_max = 0.0;
+  const double m = a.mdiv, gamma = a.gamma;
+
+  auto tfn = [&](int64_t, double r_i, double u) { return r_i - u; };
+  const bool tr = a.trace && blockIdx.x == 0 && tid == 0;
+  int tp = 0;
+  if (tr) a.trace[tp++] = gtimer();
+  int bnext = a.order ? a.order[0] : 0;
+  row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, -1, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
+  if (tr) a.trace[tp++] = gtimer();
+  for (int t = 0; t < a.p; ++t) {
+    const int b = bnext;
+    grid_barrier(a.bar, target, P);
+    if (tr) a.trace[tp++] = gtimer();
+    // ---- S1: reduce the per-CTA partials -> block right-hand side
+    for (int j = gw; j < s; j += GW) {
+      double acc = 0.0;
+      for (int q = lane; q < P; q += 32) acc += ldcg(a.partial + (int64_t)q * s + j);
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        int g = a.idx[(int64_t)b * s + j];
+        double rhs = 0.0;
+        if (g >= 0) {
+          double cross = acc / m;
+          rhs = -(sub(sub(add(a.c[g], cross), ldcg(a.xi + g)), mul(gamma, ldcg(a.z + g))));
+        }
+        a.rhs[j] = rhs;
+      }
+    }
+    if (tr) a.trace[tp++] = gtimer();
+    grid_barrier(a.bar, target, P);
+    if (tr) a.trace[tp++] = gtimer();
+    // ---- S2: beta_b = inv_b rhs, fused prox/dual/residual per coordinate
+    const double* Ib = a.inv + (int64_t)b * s * s;
+    for (int i = gw; i < s; i += GW) {
+      int g = a.idx[(int64_t)b * s + i];
+      const double* row = Ib + (int64_t)i * s;
+      double acc = 0.0;
+      for (int j = lane; j < s; j += 32) acc += row[j] * ldcg(a.rhs + j);
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        if (g >= 0) {
+          const double bn = acc;
+          const double bo = ldcg(a.beta + g);
+          a.delta[i] = bn - bo;
+          a.beta[g] = bn;
+          const double zo = ldcg(a.z + g), x0 = ldcg(a.xi + g);
+          const double av = sub(x0, mul(gamma, bn));
+          const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
+          a.z[g] = zn;
+          a.xi[g] = sub(x0, mul(gamma, sub(bn, zn)));
+          my_sum += fabs(sub(bn, zn));
+          my_max = fmax(my_max, fabs(sub(zn, zo)));
+        } else {
+          a.delta[i] = 0.0;
+        }
+      }
+    }
+    if (tr) a.trace[tp++] = gtimer();
+    grid_barrier(a.bar, target, P);
+    if (tr) a.trace[tp++] = gtimer();
+    bnext = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
+    row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
+    if (tr) a.trace[tp++] = gtimer();
+  }
+  if (lane == 0) {
+    a.wsum[gw] = my_sum;
+    a.wmax[gw] = my_max;
+  }
+  grid_barrier(a.bar, target, P);
+  if (blockIdx.x == 0 && warp == 0) {
+    double tot = 0.0, mx = 0.0;
+    for (int q = lane; q < GW; q += 32) {
+      tot += ldcg(a.wsum + q);
+      mx = fmax(mx, ldcg(a.wmax + q));
+    }
+    tot = warp_sum(tot);
+    mx = warp_max(mx);
+    if (lane == 0) {
+      a.hist_p[a.sweep] = tot;
+      a.hist_d[a.sweep] = gamma * mx;
+      a.ctrl[1] = a.sweep + 1;
+      if (a.tol >= 0.0 && tot <= a.tol) {
+        a.ctrl[0] = 1;
+        a.ctrl[3] = 1;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// prologue kernels
+// ---------------------------------------------------------------------------
+// row-major X (m x n) -> column-major Xc (ld x n), rows m..ld-1 zero
+__global__ void transpose_pad_kernel(const double* __restrict__ X, int64_t m, int64_t n, int64_t ld,
+                                     double* __restrict__ Xc) {
+  __shared__ double t[32][33];
+  const int64_t i0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    int64_t i = i0 + r, j = j0 + threadIdx.x;
+    t[r][threadIdx.x] = (i < m && j < n) ? X[i * n + j] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    int64_t j = j0 + r, i = i0 + threadIdx.x;
+    if (j < n && i < ld) Xc[j * ld + i] = t[threadIdx.x][r];
+  }
+}
+
+int launch_transpose_pad(const double* X, int64_t m, int64_t n, int64_t ld, double* Xc, cudaStream_t st) {
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((ld + 31) / 32));
+  if (grid.y > 65535) return set_error(RAC_ERR_UNSUPPORTED, "transpose: too many rows (%lld)", (long long)m);
+  transpose_pad_kernel<<<grid, dim3(32, 8), 0, st>>>(X, m, n, ld, Xc);
+  return check_launch("transpose_pad");
+}
+
+// c_j = -(X[:, j] . y) / m      (elastic_net.py:177)
+__global__ void neg_xty_kernel(const double* __restrict__ Xc, int64_t ld, int64_t m, int64_t n,
+                               const double* __restrict__ y, double mdiv, double* __restrict__ c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = w; j < n; j += nw) {
+    const double* col = Xc + j * ld;
+    double acc = 0.0;
+    for (int64_t i = lane; i < m; i += 32) acc += col[i] * y[i];
+    acc = warp_sum(acc);
+    if (lane == 0) c[j] = (-acc) / mdiv;
+  }
+}
+
+}  // namespace rac
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct rac_en_ctx {
+  int64_t m = 0, n = 0, ld = 0;
+  int s = 0, p = 0, mode = 0;
+  double lam = 0, alpha = 0, gamma = 1;
+  cudaStream_t st = nullptr;
+  int P = 0, RC = 32, nrc = 0;
+  rac::GramPlan gp{};
+  bool have_data = false, have_partition = false;
+  int sweeps = 0;        // sweeps enqueued so far
+  int hist_cap = 0;
+  // device buffers
+  double *Xc = nullptr, *y = nullptr, *c = nullptr, *beta = nullptr, *z = nullptr, *xi = nullptr,
+         *r = nullptr;
+  int32_t* idx = nullptr;     // [p][s]
+  int32_t* order = nullptr;   // [p] (RP)
+  double *gram_ws = nullptr, *scratch = nullptr, *inv = nullptr;
+  int32_t* info = nullptr;
+  double *partial = nullptr, *rhs = nullptr, *delta = nullptr, *wsum = nullptr, *wmax = nullptr;
+  unsigned* bar = nullptr;
+  int32_t* ctrl = nullptr;
+  double *hist_p = nullptr, *hist_d = nullptr;
+  std::vector<void*> allocs;
+  // optional per-stage CUDA-event timing: [assembly, gram, factor, chain]
+  bool timing = false;
+  std::vector<cudaEvent_t> events;  // 5 per timed sweep
+  long long* trace = nullptr;       // 2 + 7p phase timestamps of the last traced sweep
+};
+
+namespace {
+
+template <typename T>
+int dalloc(rac_en_ctx* c, T** p, size_t count) {
+  if (count == 0) count = 1;
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, count * sizeof(T));
+  if (e != cudaSuccess) return rac::check_cuda(e, "cudaMalloc");
+  c->allocs.push_back(q);
+  *p = (T*)q;
+  return RAC_OK;
+}
+
+size_t en_chain_smem(int s, int RC) {
+  size_t d = RC == 32 ? rac::RowPhase<32>::smem_doubles(s)
+                      : (RC == 16 ? rac::RowPhase<16>::smem_doubles(s) : rac::RowPhase<8>::smem_doubles(s));
+  return d * sizeof(double) + 2 * s * sizeof(int32_t);
+}
+
+int en_grow_history(rac_en_ctx* c, int need) {
+  if (need <= c->hist_cap) return RAC_OK;
+  int cap = std::max(need, std::max(64, 2 * c->hist_cap));
+  double *hp = nullptr, *hd = nullptr;
+  int rc = dalloc(c, &hp, cap);
+  if (rc) return rc;
+  rc = dalloc(c, &hd, cap);
+  if (rc) return rc;
+  if (c->hist_cap) {
+    cudaMemcpyAsync(hp, c->hist_p, c->hist_cap * sizeof(double), cudaMemcpyDeviceToDevice, c->st);
+    cudaMemcpyAsync(hd, c->hist_d, c->hist_cap * sizeof(double), cudaMemcpyDeviceToDevice, c->st);
+  }
+  c->hist_p = hp;
+  c->hist_d = hd;
+  c->hist_cap = cap;
+  return RAC_OK;
+}
+
+int en_factor(rac_en_ctx* c) {
+  using namespace rac;
+  SysArgs a{};
+  a.ws = c->gram_ws;
+  a.splits = c->gp.splits;
+  a.div = (double)c->m;
+  a.mul = 1.0;
+  a.shift = c->gamma;
+  a.s = c->s;
+  a.inv = c->inv;
+  a.scratch = c->scratch;
+  a.info = c->info;
+  a.done = c->ctrl;
+  return launch_chol_system(a, c->p, c->st);
+}
+
+int en_block_systems(rac_en_ctx* c) {
+  int rc = rac::launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->st,
+                            c->ctrl);
+  if (rc) return rc;
+  return en_factor(c);
+}
+
+int en_chain(rac_en_ctx* c, double tol) {
+  using namespace rac;
+  cudaMemsetAsync(c->bar, 0, sizeof(unsigned), c->st);
+  EnChainArgs a{};
+  a.Xc = c->Xc;
+  a.ld = c->ld;
+  a.m = c->m;
+  a.s = c->s;
+  a.p = c->p;
+  a.nrc = c->nrc;
+  a.idx = c->idx;
+  a.order = (c->mode == RAC_MODE_RP) ? c->order : nullptr;
+  a.inv = c->inv;
+  a.info = c->info;
+  a.c = c->c;
+  a.beta = c->beta;
+  a.z = c->z;
+  a.xi = c->xi;
+  a.r = c->r;
+  a.partial = c->partial;
+  a.rhs = c->rhs;
+  a.delta = c->delta;
+  a.wsum = c->wsum;
+  a.wmax = c->wmax;
+  a.bar = c->bar;
+  a.ctrl = c->ctrl;
+  a.gamma = c->gamma;
+  a.thr = c->lam * c->alpha;
+  a.den = (1.0 - c->alpha) * c->lam + c->gamma;
+  a.mdiv = (double)c->m;
+  a.tol = tol;
+  a.sweep = c->sweeps;
+  a.hist_p = c->hist_p;
+  a.hist_d = c->hist_d;
+  a.trace = c->trace;
+  void* args[] = {&a};
+  size_t smem = en_chain_smem(c->s, c->RC);
+  cudaError_t e;
+  if (c->RC == 32)
+    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<32>, dim3(c->P), dim3(ENT), args, smem, c->st);
+  else if (c->RC == 16)
+    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<16>, dim3(c->P), dim3(ENT), args, smem, c->st);
+  else
+    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<8>, dim3(c->P), dim3(ENT), args, smem, c->st);
+  return check_cuda(e, "en_chain (cooperative launch)");
+}
+
+}  // namespace
+
+extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t block_size,
+                             int32_t mode, double lam, double alpha, double gamma, void* stream) {
+  using namespace rac;
+  clear_error();
+  if (!out || m < 1 || n < 1 || block_size < 1 || !(gamma > 0) || lam < 0 || alpha < 0 || alpha > 1)
+    return set_error(RAC_ERR_ARG, "rac_en_create: bad arguments");
+  if (mode != RAC_MODE_RAC && mode != RAC_MODE_RP)
+    return set_error(RAC_ERR_ARG, "rac_en_create: mode must be rac or rp");
+  const int s = (int)std::min<int64_t>(block_size, n);
+  if (s > EN_QMAX * ENT) return set_error(RAC_ERR_UNSUPPORTED, "block_size %d > %d", s, EN_QMAX * ENT);
+  rac_en_ctx* c = new rac_en_ctx();
+  c->m = m;
+  c->n = n;
+  c->ld = (m + 31) / 32 * 32;
+  c->s = s;
+  c->p = (int)((n + s - 1) / s);
+  c->mode = mode;
+  c->lam = lam;
+  c->alpha = alpha;
+  c->gamma = gamma;
+  c->st = (cudaStream_t)stream;
+  // rows per chunk: biggest that keeps the tile within ~110 KB of shared memory
+  c->RC = (en_chain_smem(s, 32) <= 150 * 1024) ? 32 : (en_chain_smem(s, 16) <= 150 * 1024 ? 16 : 8);
+  c->nrc = (int)((m + c->RC - 1) / c->RC);
+  c->gp = plan_gram(m, s, c->p);
+  int rc = RAC_OK;
+  size_t smem = en_chain_smem(s, c->RC);
+  void* kfn = (c->RC == 32) ? (void*)en_chain_kernel<32>
+                            : (c->RC == 16 ? (void*)en_chain_kernel<16> : (void*)en_chain_kernel<8>);
+  if ((rc = check_cuda(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                       "chain smem attribute"))) {
+    delete c;
+    return rc;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, ENT, smem);
+  if (per_sm < 1) {
+    delete c;
+    return set_error(RAC_ERR_UNSUPPORTED, "chain kernel does not fit (smem %zu)", smem);
+  }
+  c->P = std::max(1, std::min(num_sms(), c->nrc));
+  const int GW = c->P * (ENT / 32);
+  const size_t sqs = (size_t)c->p * s * s;
+  if ((rc = dalloc(c, &c->Xc, (size_t)c->ld * n)) || (rc = dalloc(c, &c->c, n)) ||
+      (rc = dalloc(c, &c->beta, n)) || (rc = dalloc(c, &c->z, n)) || (rc = dalloc(c, &c->xi, n)) ||
+      (rc = dalloc(c, &c->r, c->ld)) || (rc = dalloc(c, &c->idx, (size_t)c->p * s)) ||
+      (rc = dalloc(c, &c->order, c->p)) ||
+      (rc = dalloc(c, &c->gram_ws, gram_ws_bytes(m, s, c->p) / sizeof(double))) ||
+      (rc = dalloc(c, &c->inv, sqs)) || (rc = dalloc(c, &c->info, c->p)) ||
+      (rc = dalloc(c, &c->partial, (size_t)c->P * s)) || (rc = dalloc(c, &c->rhs, s)) ||
+      (rc = dalloc(c, &c->delta, s)) || (rc = dalloc(c, &c->wsum, GW)) ||
+      (rc = dalloc(c, &c->wmax, GW)) || (rc = dalloc(c, &c->bar, 1)) || (rc = dalloc(c, &c->ctrl, 4))) {
+    rac_en_destroy(c);
+    return rc;
+  }
+  size_t scr = chol_scratch_bytes(s, c->p);
+  if (scr && (rc = dalloc(c, &c->scratch, scr / sizeof(double)))) {
+    rac_en_destroy(c);
+    return rc;
+  }
+  if ((rc = en_grow_history(c, 256))) {
+    rac_en_destroy(c);
+    return rc;
+  }
+  cudaMemsetAsync(c->beta, 0, n * sizeof(double), c->st);
+  cudaMemsetAsync(c->z, 0, n * sizeof(double), c->st);
+  cudaMemsetAsync(c->xi, 0, n * sizeof(double), c->st);
+  cudaMemsetAsync(c->r, 0, c->ld * sizeof(double), c->st);
+  cudaMemsetAsync(c->ctrl, 0, 4 * sizeof(int32_t), c->st);
+  cudaMemsetAsync(c->info, 0, c->p * sizeof(int32_t), c->st);
+  rc = check_launch("rac_en_create");
+  if (rc) {
+    rac_en_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return RAC_OK;
+}
+
+extern "C" int rac_en_set_data(rac_en_ctx* c, const double* X, int32_t layout, const double* y) {
+  using namespace rac;
+  clear_error();
+  if (!c || !X || !y) return set_error(RAC_ERR_ARG, "rac_en_set_data: null pointer");
+  if (layout == RAC_LAYOUT_ROW_MAJOR) {
+    int rc = launch_transpose_pad(X, c->m, c->n, c->ld, c->Xc, c->st);
+    if (rc) return rc;
+  } else if (layout == RAC_LAYOUT_COL_MAJOR) {
+    cudaMemcpy2DAsync(c->Xc, c->ld * sizeof(double), X, c->m * sizeof(double), c->m * sizeof(double),
+                      c->n, cudaMemcpyDeviceToDevice, c->st);
+    if (c->ld > c->m)
+      cudaMemset2DAsync(c->Xc + c->m, c->ld * sizeof(double), 0, (c->ld - c->m) * sizeof(double), c->n,
+                        c->st);
+  } else {
+    return set_error(RAC_ERR_ARG, "rac_en_set_data: unknown layout %d", layout);
+  }
+  int blocks = (int)std::min<int64_t>((c->n + 7) / 8, (int64_t)num_sms() * 16);
+  neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
+  c->have_data = true;
+  return check_launch("rac_en_set_data");
+}
+
+extern "C" int rac_en_set_partition(rac_en_ctx* c, const int64_t* perm) {
+  using namespace rac;
+  clear_error();
+  if (!c || !perm) return set_error(RAC_ERR_ARG, "rac_en_set_partition: null pointer");
+  if (c->mode != RAC_MODE_RP) return set_error(RAC_ERR_ARG, "rac_en_set_partition: mode is not rp");
+  if (!c->have_data) return set_error(RAC_ERR_ARG, "rac_en_set_partition: call rac_en_set_data first");
+  int rc = launch_chunk_sort(perm, c->n, c->s, 1, c->idx, c->st);
+  if (rc) return rc;
+  rc = en_block_systems(c);
+  if (rc) return rc;
+  c->have_partition = true;
+  return RAC_OK;
+}
+
+extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, double tol) {
+  using namespace rac;
+  clear_error();
+  if (!c || (!perms && count > 0) || count < 0) return set_error(RAC_ERR_ARG, "rac_en_run: bad arguments");
+  if (!c->have_data) return set_error(RAC_ERR_ARG, "rac_en_run: call rac_en_set_data first");
+  if (c->mode == RAC_MODE_RP && !c->have_partition)
+    return set_error(RAC_ERR_ARG, "rac_en_run: rp mode needs rac_en_set_partition");
+  int rc = en_grow_history(c, c->sweeps + count);
+  if (rc) return rc;
+  for (int k = 0; k < count; ++k) {
+    cudaEvent_t ev[5] = {};
+    if (c->timing) {
+      for (auto& e : ev) cudaEventCreate(&e);
+      cudaEventRecord(ev[0], c->st);
+    }
+    if (c->mode == RAC_MODE_RAC) {
+      rc = launch_chunk_sort(perms + (int64_t)k * c->n, c->n, c->s, 1, c->idx, c->st);
+      if (rc) return rc;
+      if (c->timing) cudaEventRecord(ev[1], c->st);
+      rc = launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->st, c->ctrl);
+      if (rc) return rc;
+      if (c->timing) cudaEventRecord(ev[2], c->st);
+      rc = en_factor(c);
+      if (rc) return rc;
+    } else {
+      rc = launch_order_cast(perms + (int64_t)k * c->p, c->p, c->order, c->st);
+      if (rc) return rc;
+      if (c->timing) { cudaEventRecord(ev[1], c->st); cudaEventRecord(ev[2], c->st); }
+    }
+    if (c->timing) cudaEventRecord(ev[3], c->st);
+    rc = en_chain(c, tol);
+    if (rc) return rc;
+    if (c->timing) {
+      cudaEventRecord(ev[4], c->st);
+      c->events.insert(c->events.end(), ev, ev + 5);
+    }
+    c->sweeps++;
+  }
+  return RAC_OK;
+}
+
+extern "C" int rac_en_progress(rac_en_ctx* c, int32_t* iterations, int32_t* converged,
+                               double* residual, int32_t* failed_block) {
+  using namespace rac;
+  clear_error();
+  if (!c) return set_error(RAC_ERR_ARG, "rac_en_progress: null context");
+  int32_t h[4];
+  int rc = check_cuda(cudaMemcpyAsync(h, c->ctrl, sizeof(h), cudaMemcpyDeviceToHost, c->st), "progress");
+  if (rc) return rc;
+  rc = check_cuda(cudaStreamSynchronize(c->st), "progress sync");
+  if (rc) return rc;
+  if (iterations) *iterations = h[1];
+  if (converged) *converged = h[3];
+  if (failed_block) *failed_block = h[2] - 1;
+  if (residual) {
+    *residual = INFINITY;
+    if (h[1] > 0) {
+      rc = check_cuda(cudaMemcpy(residual, c->hist_p + (h[1] - 1), sizeof(double), cudaMemcpyDeviceToHost),
+                      "progress residual");
+      if (rc) return rc;
+    }
+  }
+  return RAC_OK;
+}
+
+extern "C" int rac_en_get(rac_en_ctx* c, double* beta, double* z, double* xi, double* r) {
+  using namespace rac;
+  clear_error();
+  if (!c) return set_error(RAC_ERR_ARG, "rac_en_get: null context");
+  const size_t nb = c->n * sizeof(double);
+  if (beta) cudaMemcpyAsync(beta, c->beta, nb, cudaMemcpyDeviceToDevice, c->st);
+  if (z) cudaMemcpyAsync(z, c->z, nb, cudaMemcpyDeviceToDevice, c->st);
+  if (xi) cudaMemcpyAsync(xi, c->xi, nb, cudaMemcpyDeviceToDevice, c->st);
+  if (r) cudaMemcpyAsync(r, c->r, c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->st);
+  return check_launch("rac_en_get");
+}
+
+extern "C" int rac_en_history(rac_en_ctx* c, double* primal, double* dual, int32_t capacity) {
+  using namespace rac;
+  clear_error();
+  if (!c || capacity < 0) return set_error(RAC_ERR_ARG, "rac_en_history: bad arguments");
+  int k = std::min(capacity, c->hist_cap);
+  if (k <= 0) return RAC_OK;
+  if (primal) cudaMemcpyAsync(primal, c->hist_p, k * sizeof(double), cudaMemcpyDeviceToDevice, c->st);
+  if (dual) cudaMemcpyAsync(dual, c->hist_d, k * sizeof(double), cudaMemcpyDeviceToDevice, c->st);
+  return check_launch("rac_en_history");
+}
+
+extern "C" int rac_en_set_timing(rac_en_ctx* c, int32_t enable) {
+  using namespace rac;
+  clear_error();
+  if (!c) return set_error(RAC_ERR_ARG, "rac_en_set_timing: null context");
+  c->timing = enable != 0;
+  if (enable >= 2 && !c->trace) {
+    int rc = dalloc(c, &c->trace, 2 + 7 * (size_t)c->p);
+    if (rc) return rc;
+  }
+  if (enable < 2) c->trace = nullptr;
+  return RAC_OK;
+}
+
+extern "C" int rac_en_trace(rac_en_ctx* c, int64_t* host, int32_t capacity) {
+  using namespace rac;
+  clear_error();
+  if (!c || !host || !c->trace) return set_error(RAC_ERR_ARG, "rac_en_trace: tracing not enabled");
+  int k = std::min<int>(capacity, 2 + 7 * c->p);
+  return check_cuda(cudaMemcpy(host, c->trace, k * sizeof(int64_t), cudaMemcpyDeviceToHost), "trace copy");
+}
+
+extern "C" int rac_en_timing(rac_en_ctx* c, double* stage_ms, int32_t* sweeps) {
+  using namespace rac;
+  clear_error();
+  if (!c || !stage_ms) return set_error(RAC_ERR_ARG, "rac_en_timing: bad arguments");
+  int rc = check_cuda(cudaStreamSynchronize(c->st), "timing sync");
+  if (rc) return rc;
+  for (int q = 0; q < 4; ++q) stage_ms[q] = 0.0;
+  const size_t k = c->events.size() / 5;
+  for (size_t i = 0; i < k; ++i) {
+    for (int q = 0; q < 4; ++q) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->events[5 * i + q], c->events[5 * i + q + 1]);
+      stage_ms[q] += ms;
+    }
+  }
+  for (auto e : c->events) cudaEventDestroy(e);
+  c->events.clear();
+  if (sweeps) *sweeps = (int32_t)k;
+  return RAC_OK;
+}
+
+extern "C" int rac_en_destroy(rac_en_ctx* c) {
+  if (!c) return RAC_OK;
+  if (c->st) cudaStreamSynchronize(c->st);
+  for (auto e : c->events) cudaEventDestroy(e);
+  for (void* q : c->allocs) cudaFree(q);
+  delete c;
+  return RAC_OK;
+}

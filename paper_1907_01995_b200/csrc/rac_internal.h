@@ -1,0 +1,64 @@
+// Internal declarations shared by the .cu translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rac_b200.h"
+#include "rac_common.cuh"
+
+namespace rac {
+
+// thread-local error reporting (rac_last_error)
+void clear_error();
+int set_error(int code, const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* what);
+int check_launch(const char* what);
+
+int num_sms();
+int launch_gemv_rows(const double* Q, int64_t rows, int64_t cols, const double* w, double* out,
+                     cudaStream_t st);
+
+// K1
+int launch_chunk_sort(const int64_t* perms, int64_t n, int s, int count, int32_t* out,
+                      cudaStream_t st);
+int launch_order_cast(const int64_t* src, int64_t total, int32_t* dst, cudaStream_t st);
+
+// K2/K3: batched Gram (DMMA) and Cholesky/inverse of the block systems.
+struct GramPlan {
+  int tiles;      // 64-wide tiles per block side
+  int pairs;      // lower-triangular tile pairs
+  int splits;     // split-K factor
+  int64_t chunk;  // rows per split (multiple of 32)
+};
+GramPlan plan_gram(int64_t len, int s, int p);
+size_t gram_ws_bytes(int64_t len, int s, int p);
+// ws receives `splits` partial Grams per block ([p][splits][s][s], lower part valid)
+int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx, const int32_t* blk_list,
+                int s, int p, double* ws, const GramPlan& plan, cudaStream_t st,
+                const int32_t* done);
+// K3: assemble block systems, Cholesky, explicit inverse.
+struct SysArgs {
+  const double* ws;   // [p][splits][s][s] partial Grams (lower), may be null
+  int splits;
+  double div, mul;    // val = (sum / div) * mul  (div==1/mul==1 skip the op)
+  const double* H;    // optional dense H (row-major, ldh) -> + H[idx_i][idx_j]
+  int64_t ldh;
+  const int32_t* idx;  // block indices (-1 = padding of the short last block -> identity row)
+  const int32_t* blk_list;
+  double shift, ridge_rel;
+  int s;
+  double* inv;        // [p][s][s] out
+  double* mat_out;    // optional [p][s][s] copy of the assembled block matrix
+  double* hbb_out;    // optional [p][s][s] copy of H_bb (gathered H block)
+  double* scratch;    // [p][s][s] global scratch for the large-s path
+  int32_t* info;
+  const int32_t* done;  // skip when *done (converged / failed)
+};
+int launch_chol_system(const SysArgs& a, int p, cudaStream_t st);
+size_t chol_scratch_bytes(int s, int p);
+
+// row-major X (m x n) -> column-major (ld x n), rows m..ld-1 zero
+int launch_transpose_pad(const double* X, int64_t m, int64_t n, int64_t ld, double* Xc, cudaStream_t st);
+
+}  // namespace rac

@@ -1,0 +1,146 @@
+// Row phase of the Gauss-Seidel chain (shared by the EN and QP engines).
+//
+// Rows of a column-major matrix V (m x n, leading dim ld, zero rows past m)
+// are split into chunks of RC rows; chunk ch belongs to CTA ch % gridDim.x
+// for the whole launch, so the running row vector `acc` (EN: r = X beta,
+// QP: ax = A x) is only ever touched by its owner CTA.
+//
+//   acc_i += V[i, blk_prev] . delta                    (running residual update)
+//   t_i    = T(i, acc_i, V[i, blk_next] . x_next)      (engine-specific)
+//   partial[cta][j] = sum_i V[i, blk_next[j]] t_i      (coupling term, reduced later)
+#pragma once
+
+#include "rac_common.cuh"
+
+namespace rac {
+
+constexpr int RP_THREADS = 256;
+constexpr int RP_QMAX = 4;  // s <= RP_QMAX * RP_THREADS
+
+template <int RC>
+struct RowPhase {
+  static constexpr int NG = (RP_THREADS / 32) * (32 / RC);  // row groups of the tile reduction
+  // shared-memory doubles needed (tile + reductions), plus 2*s int32 of indices
+  // two tiles (prev + next block) + delta + x_next + reduction scratch
+  static __host__ __device__ size_t smem_doubles(int s) { return 2 * (size_t)s * (RC + 1) + 2 * (size_t)s + NG * RC + RC; }
+};
+
+struct RowPhaseSmem {
+  double* tile;
+  double* tile2;
+  double* sDel;
+  double* sXn;
+  double* red;
+  double* sT;
+  int32_t* sIdxP;
+  int32_t* sIdxN;
+};
+
+template <int RC>
+__device__ __forceinline__ RowPhaseSmem carve_rowphase(double* base, int s) {
+  RowPhaseSmem w;
+  w.tile = base;
+  w.tile2 = w.tile + (size_t)s * (RC + 1);
+  w.sDel = w.tile2 + (size_t)s * (RC + 1);
+  w.sXn = w.sDel + s;
+  w.red = w.sXn + s;
+  w.sT = w.red + RowPhase<RC>::NG * RC;
+  w.sIdxP = (int32_t*)(w.sT + RC);
+  w.sIdxN = w.sIdxP + s;
+  return w;
+}
+
+// T(i, acc_i, u_i) -> t_i
+template <int RC, class TFn>
+__device__ void row_phase(const double* __restrict__ V, int64_t ld, int64_t m, int nrc,
+                          const int32_t* __restrict__ idx, int s, int bprev, int bnext,
+                          const double* delta, const double* xsrc, double* acc,
+                          double* partial, const RowPhaseSmem& w, TFn tfn) {
+  constexpr int NG = RowPhase<RC>::NG;
+  const int tid = threadIdx.x;
+  const int P = gridDim.x;
+  if (bprev >= 0)
+    for (int j = tid; j < s; j += RP_THREADS) {
+      w.sIdxP[j] = idx[(int64_t)bprev * s + j];
+      w.sDel[j] = ldcg(delta + j);
+    }
+  if (bnext >= 0)
+    for (int j = tid; j < s; j += RP_THREADS) {
+      int g = idx[(int64_t)bnext * s + j];
+      w.sIdxN[j] = g;
+      w.sXn[j] = (g >= 0) ? ldcg(xsrc + g) : 0.0;
+    }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  const int grp = warp * (32 / RC) + lane / RC;
+  const int ri = lane % RC;
+  double part[RP_QMAX];
+#pragma unroll
+  for (int q = 0; q < RP_QMAX; ++q) part[q] = 0.0;
+
+  // Both tiles of a row chunk are fetched with asynchronous 8-byte copies
+  // (LDGSTS): every thread has ~s*RC/256 loads in flight instead of one.
+  auto issue = [&](double* dst, const int32_t* sIdx, int64_t i0) {
+    for (int e = tid; e < s * RC; e += RP_THREADS) {
+      int j = e / RC, i = e - j * RC;
+      int g = sIdx[j];
+      double* d = dst + j * (RC + 1) + i;
+      if (g >= 0) cp_async8(d, V + (int64_t)g * ld + i0 + i);
+      else *d = 0.0;
+    }
+  };
+  for (int ch = blockIdx.x; ch < nrc; ch += P) {
+    const int64_t i0 = (int64_t)ch * RC;
+    const int rows = (int)min64(RC, m - i0);
+    if (bprev >= 0) issue(w.tile, w.sIdxP, i0);
+    if (bnext >= 0) issue(w.tile2, w.sIdxN, i0);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    if (bprev >= 0) {
+      double u = 0.0;
+      for (int j = grp; j < s; j += NG) u += w.tile[j * (RC + 1) + ri] * w.sDel[j];
+      w.red[grp * RC + ri] = u;
+      __syncthreads();
+      if (tid < rows) {
+        double tot = w.red[tid];
+        for (int q = 1; q < NG; ++q) tot += w.red[q * RC + tid];
+        acc[i0 + tid] += tot;
+      }
+      __syncthreads();
+    }
+    if (bnext >= 0) {
+      double u = 0.0;
+      for (int j = grp; j < s; j += NG) u += w.tile2[j * (RC + 1) + ri] * w.sXn[j];
+      w.red[grp * RC + ri] = u;
+      __syncthreads();
+      if (tid < RC) {
+        double tot = w.red[tid];
+        for (int q = 1; q < NG; ++q) tot += w.red[q * RC + tid];
+        w.sT[tid] = (tid < rows) ? tfn(i0 + tid, acc[i0 + tid], tot) : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < RP_QMAX; ++q) {
+        int j = tid + q * RP_THREADS;
+        if (j < s) {
+          const double* col = w.tile2 + j * (RC + 1);
+          double a = part[q];
+#pragma unroll 8
+          for (int i = 0; i < RC; ++i) a += col[i] * w.sT[i];
+          part[q] = a;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (bnext >= 0) {
+#pragma unroll
+    for (int q = 0; q < RP_QMAX; ++q) {
+      int j = tid + q * RP_THREADS;
+      if (j < s) partial[(int64_t)blockIdx.x * s + j] = part[q];
+    }
+  }
+}
+
+}  // namespace rac

@@ -1,0 +1,274 @@
+"""Elastic-net / LASSO / ridge by RAC block sweeps on one B200.
+
+Drop-in for racml.elastic_net (elastic_net.py:51-232): same ElasticNetSpec,
+same ElasticNetModel fields, same fit(X, y, spec) signature, validation
+messages and BlockDefinitenessError.  The sweep itself runs in the native
+sm_100a engine (`rac_en_*`, include/rac_b200.h); the host only draws the
+reference's PCG64 permutations and streams them to the device.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _device, _native
+from .engine import BlockDefinitenessError
+from .problems import Matrix, Mode
+
+AUTO_GAMMA_DENSITY = 0.005   # elastic_net.py:48
+
+
+@dataclass(frozen=True)
+class ElasticNetSpec:
+    """Regression hyperparameters and sweep settings (elastic_net.py:51-76)."""
+
+    lam: float
+    alpha: float
+    gamma: Optional[float] = None
+    block_size: int = 100
+    iters: int = 10
+    mode: Mode = Mode.RAC
+    seed: int = 0
+    tol: Optional[float] = None
+
+    def validate(self) -> None:
+        if self.lam < 0:
+            raise ValueError(f"lam must be >= 0, got {self.lam}")
+        if not (0.0 <= self.alpha <= 1.0):
+            raise ValueError(f"alpha must be in [0, 1], got {self.alpha}")
+        if self.gamma is not None and self.gamma <= 0:
+            raise ValueError(f"gamma must be > 0, got {self.gamma}")
+        if self.block_size < 1:
+            raise ValueError("block_size must be >= 1")
+        if self.iters < 1:
+            raise ValueError("iters must be >= 1")
+        if Mode(self.mode) not in (Mode.RAC, Mode.RP):
+            raise ValueError(f"mode must be rac or rp, got {self.mode}")
+
+
+@dataclass
+class ElasticNetModel:
+    """Fitted coefficients and splitting state (elastic_net.py:79-89).
+
+    Extra (drop-in compatible) fields: per-sweep ||beta - z||_1 history and
+    gamma * ||z_k - z_{k-1}||_inf (a dual residual the reference does not
+    define; reported, never used for stopping).
+    """
+
+    beta: np.ndarray
+    z: np.ndarray
+    xi: np.ndarray
+    spec: ElasticNetSpec
+    gamma: float
+    iterations: int
+    residual: float
+    residual_history: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    dual_residual_history: np.ndarray = field(default_factory=lambda: np.zeros(0))
+
+
+def density(X) -> float:
+    """Stored-nonzero fraction (data_io.py:213-220)."""
+    total = X.shape[0] * X.shape[1]
+    if total == 0:
+        return 0.0
+    if sp.issparse(X):
+        return X.count_nonzero() / total
+    if isinstance(X, torch.Tensor):
+        return float(torch.count_nonzero(X).item()) / total
+    return float(np.count_nonzero(X)) / total
+
+
+def resolve_gamma(spec: ElasticNetSpec, X) -> float:
+    """elastic_net.py:92-99."""
+    if spec.gamma is not None:
+        return spec.gamma
+    if spec.lam == 0.0:
+        return 1.0
+    return 0.1 * spec.lam if density(X) >= AUTO_GAMMA_DENSITY else spec.lam
+
+
+def soft_threshold(a, b):
+    """Negated shrinkage -sign(a) max(|a| - b, 0) (elastic_net.py:102-115); API twin."""
+    a = np.asarray(a, dtype=float)
+    if np.any(np.asarray(b) < 0):
+        raise ValueError("threshold b must be >= 0")
+    out = -np.sign(a) * np.maximum(np.abs(a) - b, 0.0) + 0.0
+    return float(out) if out.ndim == 0 else out
+
+
+def z_update(beta_i, xi_i, gamma: float, lam: float, alpha: float):
+    """Closed-form z minimizer (elastic_net.py:118-131).
+
+    torch CUDA tensors run the device kernel (`rac_z_prox`, the same code the
+    fused sweep uses); numpy inputs keep the reference's host semantics.
+    """
+    if gamma <= 0:
+        raise ValueError(f"gamma must be > 0, got {gamma}")
+    denom = (1.0 - alpha) * lam + gamma
+    if isinstance(beta_i, torch.Tensor) and beta_i.is_cuda:
+        b = beta_i.contiguous().to(torch.float64)
+        x = torch.as_tensor(xi_i, device=b.device, dtype=torch.float64).contiguous()
+        z = torch.empty_like(b)
+        lib = _native.load()
+        _native.check(lib.rac_z_prox(b.data_ptr(), x.data_ptr(), b.numel(), gamma, lam * alpha,
+                                     denom, z.data_ptr(), _device.stream_handle()))
+        return z
+    a = np.asarray(xi_i, dtype=float) - gamma * np.asarray(beta_i, dtype=float)
+    out = soft_threshold(a, lam * alpha) / denom
+    return float(out) if np.ndim(out) == 0 else out
+
+
+def objective(X: Matrix, y: np.ndarray, beta: np.ndarray, lam: float, alpha: float) -> float:
+    """(1/2n)||y - X beta||^2 + lam(alpha||beta||_1 + (1-alpha)/2||beta||^2) (elastic_net.py:134-141)."""
+    n = X.shape[0]
+    r = X @ beta - y
+    penalty = lam * (alpha * np.sum(np.abs(beta)) + 0.5 * (1.0 - alpha) * float(beta @ beta))
+    return 0.5 * float(r @ r) / n + penalty
+
+
+class EnSolver:
+    """One native elastic-net sweep context (rac_en_ctx) on the current stream."""
+
+    def __init__(self, m: int, n: int, block_size: int, mode: Mode, lam: float, alpha: float,
+                 gamma: float, device: int = 0):
+        self.dev = _device.require_cuda(device)
+        self.lib = _native.load()
+        self.m, self.n = int(m), int(n)
+        self.s = min(int(block_size), self.n)
+        self.p = -(-self.n // self.s)
+        self.mode = Mode(mode)
+        self.stream = _device.stream_handle()
+        h = _native._p()
+        _native.check(self.lib.rac_en_create(
+            h, self.m, self.n, self.s,
+            _native.MODE_RP if self.mode == Mode.RP else _native.MODE_RAC,
+            float(lam), float(alpha), float(gamma), self.stream))
+        self.h = h
+        self._keep = []
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.rac_en_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_data(self, X, y) -> None:
+        """X: numpy (C or F order) / scipy sparse / torch tensor; y: length m."""
+        layout = _native.LAYOUT_ROW_MAJOR
+        if sp.issparse(X):
+            X = np.asarray(X.todense(), dtype=float)
+        if isinstance(X, torch.Tensor):
+            Xd = X.to(self.dev, torch.float64)
+            if not Xd.is_contiguous() and Xd.t().is_contiguous():
+                layout = _native.LAYOUT_COL_MAJOR
+            else:
+                Xd = Xd.contiguous()
+        else:
+            X = np.asarray(X, dtype=float)
+            if X.flags.f_contiguous and not X.flags.c_contiguous:
+                Xd = _device.upload(X.T, device=self.dev)   # (n, m) C-order == column-major X
+                layout = _native.LAYOUT_COL_MAJOR
+            else:
+                Xd = _device.upload(X, device=self.dev)
+        yd = _device.upload(y, device=self.dev)
+        _native.check(self.lib.rac_en_set_data(self.h, Xd.data_ptr(), layout, yd.data_ptr()))
+        self._keep = [Xd, yd]   # alive until the stream consumed them
+
+    def set_partition(self, perm_dev: torch.Tensor) -> None:
+        _native.check(self.lib.rac_en_set_partition(self.h, perm_dev.data_ptr()))
+
+    def run(self, perms_dev: torch.Tensor, tol: Optional[float]) -> None:
+        count = perms_dev.shape[0]
+        _native.check(self.lib.rac_en_run(self.h, perms_dev.data_ptr(), count,
+                                          -1.0 if tol is None else float(tol)))
+
+    def progress(self):
+        it, conv, fb = _native._i32(), _native._i32(), _native._i32()
+        res = _native._f64()
+        _native.check(self.lib.rac_en_progress(self.h, it, conv, res, fb))
+        return it.value, bool(conv.value), res.value, fb.value
+
+    def state(self):
+        b = torch.empty(self.n, dtype=torch.float64, device=self.dev)
+        z, xi = torch.empty_like(b), torch.empty_like(b)
+        _native.check(self.lib.rac_en_get(self.h, b.data_ptr(), z.data_ptr(), xi.data_ptr(), None))
+        return b, z, xi
+
+    def history(self, count: int):
+        hp = torch.empty(max(count, 1), dtype=torch.float64, device=self.dev)
+        hd = torch.empty_like(hp)
+        _native.check(self.lib.rac_en_history(self.h, hp.data_ptr(), hd.data_ptr(), count))
+        return hp[:count], hd[:count]
+
+
+def fit(X: Matrix, y: np.ndarray, spec: ElasticNetSpec, *, sweep_hook=None,
+        batch: int = 16, device: int = 0) -> ElasticNetModel:
+    """Randomized block-sweep fit of the elastic-net objective (elastic_net.py:150-232).
+
+    Same arguments, results and errors as the reference.  `sweep_hook(k, beta,
+    z, xi)` (optional, not in the reference) observes every sweep; it forces a
+    device->host copy per sweep and is meant for parity capture.
+    """
+    spec.validate()
+    m, n = X.shape
+    if m < 1 or n < 1:
+        raise ValueError("X must be non-empty")
+    if isinstance(y, torch.Tensor):
+        y = y.detach().cpu().numpy()
+    y = np.asarray(y, dtype=float)
+    if y.size != m:
+        raise ValueError(f"y has length {y.size}, expected {m}")
+    gamma = resolve_gamma(spec, X)
+    mode = Mode(spec.mode)
+    rng = np.random.default_rng(spec.seed)
+    solver = EnSolver(m, n, spec.block_size, mode, spec.lam, spec.alpha, gamma, device=device)
+    try:
+        solver.set_data(X, y)
+        if mode == Mode.RP:
+            solver.set_partition(_device.PermutationFeeder(rng, n, solver.dev).draw(1))
+            feeder = _device.PermutationFeeder(rng, solver.p, solver.dev)
+        else:
+            feeder = _device.PermutationFeeder(rng, n, solver.dev)
+        step = 1 if sweep_hook is not None else max(1, int(batch))
+        done = 0
+        iterations, converged, failed = 0, False, -1
+        while done < spec.iters:
+            k = min(step, spec.iters - done)
+            solver.run(feeder.draw(k), spec.tol)
+            done += k
+            if sweep_hook is not None or spec.tol is not None or done >= spec.iters:
+                iterations, converged, _, failed = solver.progress()
+                if failed >= 0:
+                    raise BlockDefinitenessError(
+                        "sub-block Gram matrix plus gamma*I is not positive definite; the "
+                        "sub-block positive-definiteness requirement is violated")
+                if sweep_hook is not None and iterations == done:
+                    b, z, xi = solver.state()
+                    sweep_hook(iterations, b.cpu().numpy(), z.cpu().numpy(), xi.cpu().numpy())
+                if converged:
+                    break
+        iterations, converged, residual, failed = solver.progress()
+        if failed >= 0:
+            raise BlockDefinitenessError(
+                "sub-block Gram matrix plus gamma*I is not positive definite; the "
+                "sub-block positive-definiteness requirement is violated")
+        b, z, xi = solver.state()
+        hp, hd = solver.history(iterations)
+        return ElasticNetModel(beta=b.cpu().numpy(), z=z.cpu().numpy(), xi=xi.cpu().numpy(),
+                               spec=spec, gamma=gamma, iterations=iterations,
+                               residual=residual if iterations else math.inf,
+                               residual_history=hp.cpu().numpy(),
+                               dual_residual_history=hd.cpu().numpy())
+    finally:
+        solver.close()

@@ -1,0 +1,193 @@
+"""GPU parity: elastic-net engine (fit) vs the reference's golden fixtures and the oracle.
+
+Bars (BASELINE.json north_star): block indices bit-exact; iterates <= 1e-9
+relative L2 after every sweep for the first 50 sweeps; final objective
+<= 1e-8 relative.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ITER_TOL = 1e-9      # relative L2, per sweep (north_star)
+OBJ_TOL = 1e-8       # relative, final objective (north_star)
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    d = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (d if d > 0 else 1.0))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1907_01995_b200 import _device, _native
+    _device.require_cuda(0)
+    return _native.load()
+
+
+def test_library_loaded_from_tree(lib):
+    from paper_1907_01995_b200 import _native
+    assert _native.MISSING == []
+    with open("/proc/self/maps") as f:
+        assert "librac_b200.so" in f.read()
+
+
+def test_chunk_sort_bit_exact(lib, golden):
+    from paper_1907_01995_b200 import _device, _native
+    g = golden("chunks")
+    for key in [k for k in g if k.startswith("perm_")]:
+        tag = key[len("perm_"):]
+        n, s = int(tag.split("_")[0]), int(tag.split("_")[1])
+        perm = torch.from_numpy(g[key]).cuda()
+        p = -(-n // s)
+        out = torch.empty(p * s, dtype=torch.int32, device="cuda")
+        _native.check(lib.rac_chunk_sort(perm.data_ptr(), n, s, 1, out.data_ptr(),
+                                         _device.stream_handle()))
+        got = out.cpu().numpy()
+        got = got[got >= 0].astype(np.int64)
+        assert np.array_equal(got, g["flat_" + tag])
+
+
+def test_chunk_sort_config_sizes_bit_exact(lib):
+    """Device chunk-sort vs the oracle's sorted chunks at every BASELINE (n, s), 3 sweeps each."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import _device, _native
+    for n, s in [(500, 50), (2000, 100), (5000, 200), (20000, 100), (100000, 500), (1001, 7)]:
+        rng = np.random.default_rng(0)
+        perms = np.stack([rng.permutation(n) for _ in range(3)])
+        p = -(-n // s)
+        out = torch.empty(3 * p * s, dtype=torch.int32, device="cuda")
+        _native.check(lib.rac_chunk_sort(torch.from_numpy(perms).cuda().data_ptr(), n, s, 3,
+                                         out.data_ptr(), _device.stream_handle()))
+        got = out.cpu().numpy().reshape(3, p * s)
+        for k in range(3):
+            want = np.concatenate(ro.sorted_chunks(perms[k], s))
+            row = got[k]
+            assert np.array_equal(row[row >= 0], want)
+
+
+def test_z_prox_bit_exact(lib, golden):
+    from paper_1907_01995_b200 import elastic_net as en
+    g = golden("block_prox")
+    z = en.z_update(torch.from_numpy(g["prox_beta"]).cuda(), torch.from_numpy(g["prox_xi"]).cuda(),
+                    0.7, 0.4, 0.3)
+    assert np.array_equal(z.cpu().numpy(), g["prox_z"])
+
+
+def _spec_from(g, tag):
+    from paper_1907_01995_b200.elastic_net import ElasticNetSpec
+    from paper_1907_01995_b200.problems import Mode
+    lam, alpha, gamma, bs, iters, seed, tol = g[f"{tag}_params"]
+    return ElasticNetSpec(lam=float(lam), alpha=float(alpha),
+                          gamma=None if np.isnan(gamma) else float(gamma),
+                          block_size=int(bs), iters=int(iters), mode=Mode(str(g[f"{tag}_mode"])),
+                          seed=int(seed), tol=None if np.isnan(tol) else float(tol))
+
+
+def _check_fit(g, tag, X, y, check_all_sweeps=True):
+    from paper_1907_01995_b200 import elastic_net as en
+    spec = _spec_from(g, tag)
+    caps = {}
+    hook = (lambda k, b, z, xi: caps.__setitem__(k, (b, z, xi))) if check_all_sweeps else None
+    model = en.fit(X, y, spec, sweep_hook=hook)
+    gamma, iters, resid, obj_b, obj_z = g[f"{tag}_final"]
+    if check_all_sweeps:
+        for k in g[f"{tag}_sweeps_kept"]:
+            k = int(k)
+            if k > 50:
+                continue
+            b, z, xi = caps[k]
+            assert rel(b, g[f"{tag}_beta_{k}"]) <= ITER_TOL, (tag, k)
+            assert rel(z, g[f"{tag}_z_{k}"]) <= ITER_TOL, (tag, k)
+            assert rel(xi, g[f"{tag}_xi_{k}"]) <= ITER_TOL, (tag, k)
+    assert abs(model.iterations - int(iters)) <= 1, (model.iterations, iters)
+    assert model.gamma == gamma
+    got_obj = en.objective(X, y, model.beta, spec.lam, spec.alpha)
+    assert abs(got_obj - obj_b) <= OBJ_TOL * abs(obj_b), (got_obj, obj_b)
+    return model
+
+
+@pytest.mark.parametrize("tag", ["lasso_rac", "ridge_rp", "enet_tol", "ls_lam0", "clamp_bs"])
+def test_fit_small_matches_reference(lib, golden, tag):
+    g = golden("en_small")
+    _check_fit(g, tag, g[f"{tag}_X"], g[f"{tag}_y"])
+
+
+def test_fit_config1_matches_reference(lib, golden):
+    from paper_1907_01995_b200 import configs
+    g = golden("en_config1")
+    c = configs.config1()
+    _check_fit(g, "cfg1", c.X, c.y)
+    # norms of every one of the first 50 sweeps
+    from paper_1907_01995_b200 import elastic_net as en
+    caps = []
+    en.fit(c.X, c.y, _spec_from(g, "cfg1"), sweep_hook=lambda k, b, z, xi: caps.append(
+        (np.linalg.norm(b), np.linalg.norm(z), np.linalg.norm(xi))) if k <= 50 else None)
+    got = np.asarray(caps)
+    want = g["cfg1_norms"][:50]
+    assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)) <= ITER_TOL
+
+
+def test_fit_config2_small_matches_reference(lib, golden):
+    from paper_1907_01995_b200 import configs
+    g = golden("en_config2_small")
+    c = configs.config2(scale=0.1)
+    _check_fit(g, "cfg2s", c.X, c.y)
+
+
+def test_fit_vs_oracle_random_shapes(lib):
+    """Ragged shapes (n % s != 0, m not a multiple of 32, s > 256) against the oracle."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import elastic_net as en
+    from paper_1907_01995_b200.problems import Mode
+    rng = np.random.default_rng(7)
+    for (m, n, s, mode, alpha) in [(33, 70, 9, "rac", 1.0), (257, 600, 300, "rac", 0.5),
+                                   (100, 513, 64, "rp", 0.2), (1, 5, 2, "rac", 1.0),
+                                   (70, 20, 20, "rp", 0.0)]:
+        X = rng.standard_normal((m, n))
+        y = rng.standard_normal(m)
+        kw = dict(lam=0.05, alpha=alpha, gamma=0.7, block_size=s, iters=12, seed=3)
+        caps = {}
+        ro.en_fit(X, y, mode=mode, **kw,
+                  on_sweep=lambda k, bl, b, z, xi: caps.__setitem__(k, (b.copy(), z.copy(), xi.copy())))
+        got = {}
+        en.fit(X, y, en.ElasticNetSpec(mode=Mode(mode), **kw),
+               sweep_hook=lambda k, b, z, xi: got.__setitem__(k, (b, z, xi)))
+        for k in caps:
+            for a_, b_ in zip(got[k], caps[k]):
+                assert rel(a_, b_) <= ITER_TOL, (m, n, s, mode, k)
+
+
+def test_fit_determinism(lib):
+    from paper_1907_01995_b200 import elastic_net as en
+    rng = np.random.default_rng(14)
+    X = rng.standard_normal((250, 120))
+    y = rng.standard_normal(250)
+    spec = en.ElasticNetSpec(lam=0.1, alpha=0.8, block_size=25, iters=20, seed=21)
+    a, b = en.fit(X, y, spec), en.fit(X, y, spec)
+    assert np.array_equal(a.beta, b.beta) and np.array_equal(a.z, b.z) and np.array_equal(a.xi, b.xi)
+
+
+def test_fit_validation_errors(lib):
+    from paper_1907_01995_b200 import elastic_net as en
+    from paper_1907_01995_b200.problems import Mode
+    with pytest.raises(ValueError):
+        en.fit(np.eye(2), np.zeros(2), en.ElasticNetSpec(lam=-1.0, alpha=0.5))
+    with pytest.raises(ValueError):
+        en.fit(np.eye(2), np.zeros(2), en.ElasticNetSpec(lam=1.0, alpha=2.0))
+    with pytest.raises(ValueError):
+        en.fit(np.eye(2), np.zeros(2), en.ElasticNetSpec(lam=1.0, alpha=0.5, mode=Mode.CYCLIC))
+    with pytest.raises(ValueError):
+        en.fit(np.eye(2), np.zeros(3), en.ElasticNetSpec(lam=1.0, alpha=0.5))
+
+
+def test_identity_design_recovers_targets(lib):
+    from paper_1907_01995_b200 import elastic_net as en
+    n = 8
+    y = np.arange(1.0, n + 1)
+    model = en.fit(np.eye(n), y, en.ElasticNetSpec(lam=0.0, alpha=1.0, gamma=1.0, block_size=3,
+                                                   iters=300, seed=1))
+    np.testing.assert_allclose(model.beta, y, atol=1e-10)

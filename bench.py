@@ -200,6 +200,12 @@ def run_reference(args, world, rank):
 
 
 def run_b200(args, world, rank, local):
+    if args.config == 4:
+        return run_b200_svm(args, world, rank, local)
+    return run_b200_en(args, world, rank, local)
+
+
+def run_b200_en(args, world, rank, local):
     import torch
     from paper_1907_01995_b200 import _device, elastic_net as en
     from paper_1907_01995_b200.problems import Mode
@@ -254,10 +260,15 @@ def run_b200(args, world, rank, local):
     lib.rac_en_trace(solver.h, tbuf, 2 + 7 * p)
     tv = np.array(tbuf[:2 + 6 * p], dtype=np.float64) / 1e3   # us
     ph = np.diff(tv[1:]).reshape(p, 6) if p > 0 else np.zeros((0, 6))
-    chain_trace = {"first_row_phase_us": float(tv[1] - tv[0]),
-                   "per_block_us": {k: float(v) for k, v in zip(
-                       ("barrier1", "S1_reduce", "barrier2", "S2_solve", "barrier3", "row_phase"),
-                       ph.mean(axis=0))}}
+    info = (np.ctypeslib.ctypes.c_int32 * 4)()
+    lib.rac_en_info(solver.h, info)
+    labels = (("cluster_sync", "cluster_reduce", "grid_barrier", "rhs", "delta+cluster_sync", "row_phase")
+              if info[0] == 1 else
+              ("barrier1", "S1_reduce", "barrier2", "S2_solve", "barrier3", "row_phase"))
+    chain_trace = {"variant": "resident-cluster" if info[0] == 1 else "streaming",
+                   "ctas": int(info[1]), "rows_per_chunk": int(info[2]), "chunks_per_cta": int(info[3]),
+                   "first_row_phase_us": float(tv[1] - tv[0]),
+                   "per_block_us": {k: float(v) for k, v in zip(labels, ph.mean(axis=0))}}
     lib.rac_en_set_timing(solver.h, 0)
     solver.close()
     del perms, more
@@ -347,13 +358,88 @@ def run_b200(args, world, rank, local):
     return 0
 
 
+def run_b200_svm(args, world, rank, local):
+    """Config 4: linear-SVM dual, N=20000, s=100, dense Q resident in HBM (3.2 GB)."""
+    import torch
+    from paper_1907_01995_b200 import _device, svm
+    from paper_1907_01995_b200.engine import QpSolver
+    from paper_1907_01995_b200.problems import Mode, SolverConfig
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    from paper_1907_01995_b200 import configs
+    case = configs.config4()
+    X, y = case.X, case.labels
+    N, d = X.shape
+    s = case.block_size
+    p = -(-N // s)
+    t0 = time.perf_counter()
+    Q = svm.build_q(X, y, svm.KernelSpec("linear"), dev)
+    t_q = time.perf_counter() - t0
+    solver = QpSolver(N, 1, s, Mode.RAC, case.beta, svm.RIDGE_REL, device=local)
+    solver.set_problem(np.full(N, -1.0), np.zeros(N), np.full(N, case.C), A=y.reshape(1, N),
+                       b=np.zeros(1), borrowed_h=Q)
+    solver.set_divergence_bar(math.inf)
+    rng = np.random.default_rng(case.seed)
+    K, W = args.steps, args.warmup
+    perms = _device.PermutationFeeder(rng, N, dev).draw(W + K)
+    solver.run(perms[:W], W, case.tol_primal, case.tol_dual, True)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    dist_barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    solver.run(perms[W:W + K], K, case.tol_primal, case.tol_dual, True)
+    e1.record()
+    torch.cuda.synchronize()
+    dist_barrier(world)
+    clk = clocks.stop()
+    ms = dist_max(e0.elapsed_time(e1), world, dev)
+    value = world * K / (ms * 1e-3)
+    it, status, _ = solver.progress()
+    hp, _, hd = (h.cpu().numpy() for h in solver.history(it))
+    solver.close()
+    peaks = measured_peaks()
+    hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
+    strip_bytes = 8.0 * N * N
+    achieved = strip_bytes / (ms * 1e-3 / K) / 1e9
+    roof = {"kernel": "qp_chain_kernel (whole sweep)", "bound": "hbm", "achieved": achieved, "peak": hbm,
+            "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+            "algorithmic": "one strip pass over Q (8*N^2 bytes) per sweep"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import rac_oracle as ro
+        t0 = time.perf_counter()
+        ro.svm_train(X, y, case.C, "linear", block_size=s, beta=case.beta, max_iters=1, seed=0)
+        dt = time.perf_counter() - t0
+        cpu = {"value": 1.0 / dt, "unit": "sweeps/s", "cores": cpu_threads(), "kind": "port",
+               "sample": f"1 sweep of {case.name} via oracle/rac_oracle.svm_train ({dt:.1f} s)"}
+    line = {
+        "metric": "rac_admm_sweeps_per_sec", "value": value, "unit": "sweeps/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) seed-0 recipe)",
+        "config": {"workload": case.name, "N": N, "d": d, "block_size": s, "blocks": p, "mode": "rac",
+                   "l2": "inputs larger than L2 (Q = %.1f GB)" % (8 * N * N / 1e9),
+                   "parallelism": f"replicas x{world}"},
+        "q_build_seconds": t_q,
+        "residuals_at_last_sweep": {"primal": float(hp[-1]), "dual": float(hd[-1]), "sweeps": it},
+        "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": 4 * K,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

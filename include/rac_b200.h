@@ -114,6 +114,8 @@ int rac_en_timing(rac_en_ctx* ctx, double* stage_ms_host4, int32_t* sweeps_host)
  * phase boundary of each sweep (CTA 0): [start, R0, then per block: bar, S1,
  * bar, S2, bar, R] = 2 + 7p stamps (the last sweep's are kept). */
 int rac_en_trace(rac_en_ctx* ctx, int64_t* host, int32_t capacity);
+/* [chain variant (0 streaming, 1 resident-tile cluster), CTAs, rows per chunk, chunks per CTA] */
+int rac_en_info(rac_en_ctx* ctx, int32_t* info_host4);
 int rac_en_destroy(rac_en_ctx* ctx);
 
 /* ------------------------------------------------------------------ train()/solve()

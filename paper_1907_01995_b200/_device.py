@@ -39,9 +39,10 @@ def upload(arr, dtype=torch.float64, device=None, pinned: bool = True) -> torch.
     else:
         np_dtype = np.float64 if dtype == torch.float64 else np.int64
         src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np_dtype))
-    if pinned:
-        src = src.pin_memory()
-    return src.to(device or "cuda", non_blocking=pinned)
+    if pinned and src.numel() * src.element_size() <= (64 << 20):
+        return src.pin_memory().to(device or "cuda", non_blocking=True)
+    # large one-shot uploads: pinning would cost more than it saves
+    return src.to(device or "cuda")
 
 
 class PermutationFeeder:

@@ -21,6 +21,7 @@
 // X is stored column-major with a leading dimension padded to 32 rows (zero
 // rows), so a block's column gather is a set of contiguous, coalesced reads.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "rac_internal.h"
@@ -30,6 +31,7 @@ namespace rac {
 
 constexpr int ENT = RP_THREADS;   // threads per chain CTA
 constexpr int EN_QMAX = RP_QMAX;   // block_size <= EN_QMAX * ENT
+constexpr int kResCS = 2;          // cluster size of the resident chain (148 SMs = 74 pairs)
 
 struct EnChainArgs {
   const double* Xc;
@@ -173,6 +175,12 @@ __global__ void __launch_bounds__(ENT) en_chain_kernel(EnChainArgs a) {
   }
 }
 
+}  // namespace rac
+
+#include "en_res.cuh"
+
+namespace rac {
+
 // ---------------------------------------------------------------------------
 // prologue kernels
 // ---------------------------------------------------------------------------
@@ -225,6 +233,7 @@ struct rac_en_ctx {
   double lam = 0, alpha = 0, gamma = 1;
   cudaStream_t st = nullptr;
   int P = 0, RC = 32, nrc = 0;
+  int variant = 0, nch = 0;   // 1: resident-tile cluster chain (en_chain_res_kernel)
   rac::GramPlan gp{};
   bool have_data = false, have_partition = false;
   int sweeps = 0;        // sweeps enqueued so far
@@ -343,6 +352,26 @@ int en_chain(rac_en_ctx* c, double tol) {
   a.hist_d = c->hist_d;
   a.trace = c->trace;
   void* args[] = {&a};
+  if (c->variant == 1) {
+    int nch = c->nch;
+    void* rargs[] = {&a, &nch};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(c->P);
+    cfg.blockDim = dim3(ENT);
+    cfg.dynamicSmemBytes = res_smem_bytes<32, kResCS>(c->s, c->nch);
+    cfg.stream = c->st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kResCS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    return check_cuda(cudaLaunchKernelExC(&cfg, (const void*)en_chain_res_kernel<32, kResCS>, rargs),
+                      "en_chain_res (cluster cooperative launch)");
+  }
   size_t smem = en_chain_smem(c->s, c->RC);
   cudaError_t e;
   if (c->RC == 32)
@@ -397,6 +426,41 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
     return set_error(RAC_ERR_UNSUPPORTED, "chain kernel does not fit (smem %zu)", smem);
   }
   c->P = std::max(1, std::min(num_sms(), c->nrc));
+  // resident-tile cluster chain when the row tiles of every CTA fit in shared memory
+  {
+    const char* env = getenv("RAC_EN_VARIANT");
+    const int want = env ? atoi(env) : 1;
+    const int nrc32 = (int)((m + 31) / 32);
+    int Pc = std::max(kResCS, std::min(num_sms(), (nrc32 + kResCS - 1) / kResCS * kResCS) / kResCS * kResCS);
+    const int nch = (nrc32 + Pc - 1) / Pc;
+    const size_t rs = res_smem_bytes<32, kResCS>(s, nch);
+    if (want == 1 && s <= ENT && rs <= 226 * 1024) {
+      void* rk = (void*)en_chain_res_kernel<32, kResCS>;
+      if (cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs) == cudaSuccess &&
+          cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(Pc);
+        cfg.blockDim = dim3(ENT);
+        cfg.dynamicSmemBytes = rs;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = kResCS;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, rk, &cfg) == cudaSuccess && clusters * kResCS >= Pc) {
+          c->variant = 1;
+          c->RC = 32;
+          c->nrc = nrc32;
+          c->nch = nch;
+          c->P = Pc;
+        }
+      }
+      cudaGetLastError();
+    }
+  }
   const int GW = c->P * (ENT / 32);
   const size_t sqs = (size_t)c->p * s * s;
   if ((rc = dalloc(c, &c->Xc, (size_t)c->ld * n)) || (rc = dalloc(c, &c->c, n)) ||
@@ -569,6 +633,17 @@ extern "C" int rac_en_set_timing(rac_en_ctx* c, int32_t enable) {
     if (rc) return rc;
   }
   if (enable < 2) c->trace = nullptr;
+  return RAC_OK;
+}
+
+extern "C" int rac_en_info(rac_en_ctx* c, int32_t* info4) {
+  using namespace rac;
+  clear_error();
+  if (!c || !info4) return set_error(RAC_ERR_ARG, "rac_en_info: bad arguments");
+  info4[0] = c->variant;
+  info4[1] = c->P;
+  info4[2] = c->RC;
+  info4[3] = c->nch;
   return RAC_OK;
 }
 

@@ -1,0 +1,335 @@
+// Resident-tile cluster chain for the elastic-net sweep (included by en.cu).
+//
+// Every CTA owns a fixed set of RC-row chunks of X.  The columns of the
+// current block stay RESIDENT in shared memory from the row phase that used
+// them as "next" to the one that applies their update, and everything the
+// next block needs — its X tile, its rows of inv_b, and c/xi/z/beta at its
+// indices — is prefetched with cp.async while the current block is solved.
+// CTAs form clusters of CS that pre-reduce partials through DSMEM and split
+// the s x s mat-vec.  Per block: two cluster barriers + one grid barrier.
+//
+//   R(t)   r += X[rows, b_t] delta_t ;  partial_{t+1} = X[rows, b_{t+1}]'(r - X beta)
+//   cl.sync; rank slice of the cluster sum -> global (double-buffered by parity)
+//   grid barrier
+//   every CTA: full rhs (elastic_net.py:205-206) from the C cluster partials
+//   rank: delta rows of its slice = inv_b rhs - beta (smem-resident inv rows)
+//   cl.sync; gather delta from the cluster
+// Cluster 0 commits beta/z/xi of block t after the grid barrier of block t+1
+// (nobody reads block t's coordinates after that point in the sweep).
+#pragma once
+
+#include <cooperative_groups.h>
+
+namespace rac {
+
+namespace cg = cooperative_groups;
+
+struct ResSmem {
+  double* tiles;   // [2][nch][s][RC+1]
+  double* ginv;    // [sl][s]     inv_b rows of this rank's slice (next block)
+  double* cxz;     // [3][s]      c, xi, z at the next block's indices
+  double* sX;      // [s]         beta at the next block's indices
+  double* sDel;    // [s]         full delta of the current block
+  double* sRhs;    // [s]
+  double* sPart;   // [s]         this CTA's partial (read by cluster peers)
+  double* sSlice;  // [2s]        delta slice (peers read) | pending beta (cluster 0)
+  double* sR;      // [nch*RC]    resident rows of r
+  double* red;     // [max(NG*RC, 256)]
+  double* sT;      // [RC]
+  int* pend;       // [s]
+};
+
+template <int RC>
+__host__ __device__ __forceinline__ size_t res_red_doubles() {
+  return RowPhase<RC>::NG * RC > 256 ? RowPhase<RC>::NG * RC : 256;
+}
+
+template <int RC, int CS>
+__host__ __device__ size_t res_smem_bytes(int s, int nch) {
+  const size_t sl = (s + CS - 1) / CS;
+  return (2 * (size_t)nch * s * (RC + 1) + sl * s + 3 * (size_t)s + 6 * (size_t)s + (size_t)nch * RC +
+          res_red_doubles<RC>() + RC) * sizeof(double) + (size_t)s * sizeof(int);
+}
+
+template <int RC, int CS>
+__device__ __forceinline__ ResSmem carve_res(double* base, int s, int nch) {
+  const int sl = (s + CS - 1) / CS;
+  ResSmem w;
+  double* p = base;
+  w.tiles = p; p += 2 * (size_t)nch * s * (RC + 1);
+  w.ginv = p; p += (size_t)sl * s;
+  w.cxz = p; p += 3 * s;
+  w.sX = p; p += s;
+  w.sDel = p; p += s;
+  w.sRhs = p; p += s;
+  w.sPart = p; p += s;
+  w.sSlice = p; p += 2 * s;
+  w.sR = p; p += (size_t)nch * RC;
+  w.red = p; p += res_red_doubles<RC>();
+  w.sT = p; p += RC;
+  w.pend = reinterpret_cast<int*>(p);
+  return w;
+}
+
+template <int RC, int CS>
+__global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nch) {
+  if (a.ctrl[0]) return;
+  constexpr int NG = RowPhase<RC>::NG;
+  extern __shared__ __align__(16) double rsm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int s = a.s;
+  const ResSmem w = carve_res<RC, CS>(rsm, s, nch);
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = ENT / 32;
+  const int P = gridDim.x, C = P / CS;
+  const int rank = (int)cl.block_rank(), cid = blockIdx.x / CS;
+  const int sl = (s + CS - 1) / CS, j0 = rank * sl, j1 = min(s, j0 + sl);
+  unsigned target = 0;
+  if (tid == 0) {
+    bad = 0;
+    for (int t = 0; t < a.p; ++t) {
+      int b = a.order ? a.order[t] : t;
+      if (a.info[b]) { bad = b + 1; break; }
+    }
+  }
+  __syncthreads();
+  if (bad) {
+    if (blockIdx.x == 0 && tid == 0) { a.ctrl[2] = bad; a.ctrl[0] = 1; }
+    return;
+  }
+  const double m = a.mdiv, gamma = a.gamma;
+  const bool tr = a.trace && blockIdx.x == 0 && tid == 0;
+  int tp = 0;
+  if (tr) a.trace[tp++] = gtimer();
+  auto blk = [&](int t) { return a.order ? a.order[t] : t; };
+  auto tile = [&](int slot, int k) { return w.tiles + ((size_t)slot * nch + k) * s * (RC + 1); };
+  // resident rows of r
+  for (int k = 0; k < nch; ++k) {
+    const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
+    for (int i = tid; i < RC; i += ENT) w.sR[k * RC + i] = (i0 + i < a.m) ? a.r[i0 + i] : 0.0;
+  }
+  // async fetch of block b's X columns (all own chunks) into a tile slot
+  auto issue_tile = [&](int slot, int b) {
+    const int32_t* bi = a.idx + (int64_t)b * s;
+    for (int k = 0; k < nch; ++k) {
+      const int ch = blockIdx.x + k * P;
+      if (ch >= a.nrc) break;
+      const int64_t i0 = (int64_t)ch * RC;
+      double* dst = tile(slot, k);
+      for (int e = tid; e < s * RC; e += ENT) {
+        const int j = e / RC, i = e - j * RC;
+        const int g = __ldg(bi + j);
+        double* d = dst + j * (RC + 1) + i;
+        if (g >= 0) cp_async8(d, a.Xc + (int64_t)g * a.ld + i0 + i);
+        else *d = 0.0;
+      }
+    }
+  };
+  // async fetch of what the S phase of block b needs: inv rows of the slice, c/xi/z
+  auto issue_solve = [&](int b) {
+    const int32_t* bi = a.idx + (int64_t)b * s;
+    const double* Ib = a.inv + (int64_t)b * s * s + (int64_t)j0 * s;
+    const int rows = j1 - j0;
+    for (int e = tid; e < rows * s; e += ENT) cp_async8(w.ginv + e, Ib + e);
+    for (int j = tid; j < s; j += ENT) {
+      const int g = __ldg(bi + j);
+      if (g >= 0) {
+        cp_async8(w.cxz + j, a.c + g);
+        cp_async8(w.cxz + s + j, a.xi + g);
+        cp_async8(w.cxz + 2 * s + j, a.z + g);
+      } else {
+        w.cxz[j] = 0.0;
+        w.cxz[s + j] = 0.0;
+        w.cxz[2 * s + j] = 0.0;
+      }
+    }
+  };
+  const int grp = warp * (32 / RC) + lane / RC, ri = lane % RC;
+  auto row_phase_res = [&](int sp, int sn) {
+    double part = 0.0;
+    for (int k = 0; k < nch; ++k) {
+      const int ch = blockIdx.x + k * P;
+      if (ch >= a.nrc) break;
+      const int64_t i0 = (int64_t)ch * RC;
+      const int rows = (int)min64(RC, a.m - i0);
+      double* rr = w.sR + k * RC;
+      if (sp >= 0) {
+        const double* T = tile(sp, k);
+        double u = 0.0;
+        for (int j = grp; j < s; j += NG) u += T[j * (RC + 1) + ri] * w.sDel[j];
+        w.red[grp * RC + ri] = u;
+        __syncthreads();
+        if (tid < rows) {
+          double tot = w.red[tid];
+          for (int q = 1; q < NG; ++q) tot += w.red[q * RC + tid];
+          rr[tid] += tot;
+        }
+      }
+      if (sn >= 0) {
+        const double* T = tile(sn, k);
+        double u = 0.0;
+        for (int j = grp; j < s; j += NG) u += T[j * (RC + 1) + ri] * w.sX[j];
+        __syncthreads();   // red reuse + rr update visible
+        w.red[grp * RC + ri] = u;
+        __syncthreads();
+        if (tid < RC) {
+          double tot = w.red[tid];
+          for (int q = 1; q < NG; ++q) tot += w.red[q * RC + tid];
+          w.sT[tid] = (tid < rows) ? rr[tid] - tot : 0.0;
+        }
+        __syncthreads();
+        if (tid < s) {
+          const double* col = T + tid * (RC + 1);
+          double acc = part;
+#pragma unroll 8
+          for (int i = 0; i < RC; ++i) acc += col[i] * w.sT[i];
+          part = acc;
+        }
+      }
+      __syncthreads();
+    }
+    if (sn >= 0 && tid < s) w.sPart[tid] = part;
+  };
+  auto load_beta = [&](int b) {
+    const int32_t* bi = a.idx + (int64_t)b * s;
+    for (int j = tid; j < s; j += ENT) {
+      const int g = bi[j];
+      w.sX[j] = (g >= 0) ? ldcg(a.beta + g) : 0.0;
+    }
+  };
+
+  double my_sum = 0.0, my_max = 0.0;
+  auto commit = [&]() {
+    if (cid != 0) return;
+    for (int q = tid; q < j1 - j0; q += ENT) {
+      const int g = w.pend[q];
+      if (g < 0) continue;
+      const double bn = w.sSlice[s + q];
+      a.beta[g] = bn;
+      const double zo = ldcg(a.z + g), x0 = ldcg(a.xi + g);
+      const double av = sub(x0, mul(gamma, bn));
+      const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
+      a.z[g] = zn;
+      a.xi[g] = sub(x0, mul(gamma, sub(bn, zn)));
+      my_sum += fabs(sub(bn, zn));
+      my_max = fmax(my_max, fabs(sub(zn, zo)));
+    }
+  };
+  // G threads per rhs entry; thread sums cluster partials q = g, g+G, ...
+  const int G = max(1, ENT / s);
+
+  // ---- prologue
+  issue_tile(0, blk(0));
+  cp_async_commit();
+  if (a.p > 1) issue_tile(1, blk(1));
+  issue_solve(blk(0));
+  cp_async_commit();
+  cp_async_wait<1>();
+  load_beta(blk(0));
+  __syncthreads();
+  row_phase_res(-1, 0);
+  if (tr) a.trace[tp++] = gtimer();
+
+  for (int t = 0; t < a.p; ++t) {
+    const int b = blk(t);
+    const int32_t* bi = a.idx + (int64_t)b * s;
+    // ---- cluster pre-reduction, grid barrier
+    cl.sync();
+    if (tr) a.trace[tp++] = gtimer();
+    double* gpart = a.partial + (int64_t)(t & 1) * C * s;
+    for (int j = j0 + tid; j < j1; j += ENT) {
+      double acc = 0.0;
+      for (int q = 0; q < CS; ++q) acc += cl.map_shared_rank(w.sPart, q)[j];
+      gpart[(int64_t)cid * s + j] = acc;
+    }
+    if (tr) a.trace[tp++] = gtimer();
+    grid_barrier(a.bar, target, P);
+    if (tr) a.trace[tp++] = gtimer();
+    if (t > 0) commit();
+    // ---- full rhs: G threads per entry, all loads in flight together
+    {
+      const int j = tid / G, g = tid - j * G;
+      double acc = 0.0;
+      if (j < s)
+        for (int q = g; q < C; q += G) acc += ldcg(gpart + (int64_t)q * s + j);
+      w.red[tid] = acc;
+    }
+    cp_async_wait<0>();   // inv rows + c/xi/z of this block, tile of the next
+    __syncthreads();
+    for (int j = tid; j < s; j += ENT) {
+      double acc = w.red[j * G];
+      for (int g = 1; g < G; ++g) acc += w.red[j * G + g];
+      double rhs = 0.0;
+      if (bi[j] >= 0) {
+        const double cross = acc / m;
+        rhs = -(sub(sub(add(w.cxz[j], cross), w.cxz[s + j]), mul(gamma, w.cxz[2 * s + j])));
+      }
+      w.sRhs[j] = rhs;
+    }
+    __syncthreads();
+    if (tr) a.trace[tp++] = gtimer();
+    // ---- delta rows of this rank's slice (old beta of the block is in sX)
+    for (int i = j0 + warp; i < j1; i += nw) {
+      const double* row = w.ginv + (int64_t)(i - j0) * s;
+      double acc = 0.0;
+      for (int j = lane; j < s; j += 32) acc += row[j] * w.sRhs[j];
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        const int g = bi[i];
+        w.sSlice[i] = (g >= 0) ? acc - w.sX[i] : 0.0;
+        w.pend[i - j0] = g;
+        w.sSlice[s + (i - j0)] = acc;
+      }
+    }
+    cl.sync();
+    if (tr) a.trace[tp++] = gtimer();
+    for (int i = tid; i < s; i += ENT) w.sDel[i] = cl.map_shared_rank(w.sSlice, i / sl)[i];
+    // ---- row phase (tile of b resident, tile of the next block prefetched)
+    const bool more = t + 1 < a.p;
+    if (more) load_beta(blk(t + 1));
+    __syncthreads();
+    row_phase_res(t & 1, more ? ((t + 1) & 1) : -1);
+    if (more) {
+      if (t + 2 < a.p) issue_tile(t & 1, blk(t + 2));
+      issue_solve(blk(t + 1));
+      cp_async_commit();
+    }
+    if (tr) a.trace[tp++] = gtimer();
+  }
+  // write back resident r
+  for (int k = 0; k < nch; ++k) {
+    const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
+    for (int i = tid; i < RC; i += ENT)
+      if (i0 + i < a.m) a.r[i0 + i] = w.sR[k * RC + i];
+  }
+  __syncthreads();
+  commit();   // last block: nobody reads its coordinates any more
+  my_sum = warp_sum(my_sum);
+  my_max = warp_max(my_max);
+  if (lane == 0) {
+    a.wsum[blockIdx.x * nw + warp] = my_sum;
+    a.wmax[blockIdx.x * nw + warp] = my_max;
+  }
+  cl.sync();  // peers may still read our shared memory
+  grid_barrier(a.bar, target, P);
+  if (blockIdx.x == 0 && warp == 0) {
+    double tot = 0.0, mx = 0.0;
+    for (int q = lane; q < P * nw; q += 32) {
+      tot += ldcg(a.wsum + q);
+      mx = fmax(mx, ldcg(a.wmax + q));
+    }
+    tot = warp_sum(tot);
+    mx = warp_max(mx);
+    if (lane == 0) {
+      a.hist_p[a.sweep] = tot;
+      a.hist_d[a.sweep] = gamma * mx;
+      a.ctrl[1] = a.sweep + 1;
+      if (a.tol >= 0.0 && tot <= a.tol) {
+        a.ctrl[0] = 1;
+        a.ctrl[3] = 1;
+      }
+    }
+  }
+}
+
+}  // namespace rac

@@ -333,11 +333,138 @@ __global__ void __launch_bounds__(CTHREADS) chol_inverse_kernel(SysArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// K3 (s <= 236): the block system is assembled into the PACKED lower triangle
+// in shared memory and inverted in place by the symmetric sweep operator
+// (Gauss-Jordan without pivoting, valid for SPD):  for each pivot k
+//     d = a_kk;  a_ij -= a_ik a_kj / d;  a_ik /= d;  a_kk = -1/d
+// which leaves -A^{-1}.  The pivots are the Cholesky pivots L_kk^2, so a
+// non-positive pivot reports exactly the leading minor np.linalg.cholesky
+// rejects (elastic_net.py:213-219, engine.py:160-167).  One CTA per block,
+// s steps of two barriers each; no global round trips.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }  // j <= i
+
+__global__ void __launch_bounds__(CTHREADS) sweep_inverse_kernel(SysArgs a) {
+  extern __shared__ __align__(16) double psm[];
+  if (a.done && *a.done) return;
+  const int s = a.s;
+  const int b = a.blk_list ? a.blk_list[blockIdx.x] : blockIdx.x;
+  double* P = psm;                                 // s(s+1)/2
+  double* col = psm + (size_t)s * (s + 1) / 2;     // s
+  __shared__ int fail;
+  __shared__ double red[CTHREADS / 32];
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  if (tid == 0) fail = 0;
+  const int32_t* bidx = a.idx ? a.idx + (int64_t)b * s : nullptr;
+  double* hbo = a.hbb_out ? a.hbb_out + (int64_t)b * s * s : nullptr;
+  // ---- assemble (lower, packed)
+  for (int i = ty; i < s; i += CTHREADS / 32) {
+    const int off = pk(i, 0);
+    for (int j = tx; j < s; j += 32) {
+      const bool pad = bidx && (bidx[i] < 0 || bidx[j] < 0);
+      double h = 0.0;
+      if (a.H && !pad) h = a.H[(int64_t)bidx[i] * a.ldh + bidx[j]];
+      if (hbo) hbo[(int64_t)i * s + j] = h;
+      if (j > i) continue;
+      double v;
+      if (pad) {
+        v = (i == j) ? 1.0 : 0.0;
+      } else {
+        v = 0.0;
+        if (a.ws) {
+          const double* src = a.ws + (int64_t)b * a.splits * s * s + (int64_t)i * s + j;
+          double acc = src[0];
+          for (int z = 1; z < a.splits; ++z) acc += src[(int64_t)z * s * s];
+          if (a.div != 1.0) acc = acc / a.div;
+          if (a.mul != 1.0) acc = a.mul * acc;
+          v = acc;
+        }
+        if (a.H) v = a.ws ? h + v : h;
+        if (i == j) v += a.shift;
+      }
+      P[off + j] = v;
+    }
+  }
+  __syncthreads();
+  if (a.ridge_rel > 0.0) {
+    double mx = -INFINITY;
+    for (int i = tid; i < s; i += CTHREADS)
+      if (!bidx || bidx[i] >= 0) mx = fmax(mx, P[pk(i, i)]);
+    mx = warp_max(mx);
+    if (tx == 0) red[ty] = mx;
+    __syncthreads();
+    double m2 = red[0];
+    for (int w = 1; w < CTHREADS / 32; ++w) m2 = fmax(m2, red[w]);
+    const double ridge = a.ridge_rel * m2;
+    __syncthreads();
+    for (int i = tid; i < s; i += CTHREADS)
+      if (!bidx || bidx[i] >= 0) P[pk(i, i)] += ridge;
+    __syncthreads();
+  }
+  if (a.mat_out) {
+    double* mo = a.mat_out + (int64_t)b * s * s;
+    for (int e = tid; e < s * s; e += CTHREADS) {
+      const int i = e / s, j = e - i * s;
+      mo[e] = (j <= i) ? P[pk(i, j)] : P[pk(j, i)];
+    }
+  }
+  // ---- sweep every pivot
+  for (int k = 0; k < s; ++k) {
+    const double d = P[pk(k, k)];
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (tid == 0) fail = k + 1;
+      break;   // uniform: every thread read the same d
+    }
+    for (int i = tid; i < s; i += CTHREADS) col[i] = (i >= k) ? P[pk(i, k)] : P[pk(k, i)];
+    __syncthreads();
+    const double dinv = 1.0 / d;
+    for (int i = ty; i < s; i += CTHREADS / 32) {
+      const int off = pk(i, 0);
+      const double ci = col[i];
+      const double cid = ci * dinv;
+      for (int j = tx; j <= i; j += 32) {
+        double v;
+        if (i == k) {
+          v = (j == k) ? -dinv : col[j] * dinv;
+        } else if (j == k) {
+          v = cid;
+        } else {
+          v = P[off + j] - cid * col[j];
+        }
+        P[off + j] = v;
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) a.info[b] = fail;
+    return;
+  }
+  if (tid == 0) a.info[b] = 0;
+  double* out = a.inv + (int64_t)b * s * s;
+  for (int e = tid; e < s * s; e += CTHREADS) {
+    const int i = e / s, j = e - i * s;
+    out[e] = -((j <= i) ? P[pk(i, j)] : P[pk(j, i)]);
+  }
+}
+
+static size_t sweep_smem_bytes(int s) { return ((size_t)s * (s + 1) / 2 + s) * sizeof(double); }
 static size_t chol_smem_bytes(int s) { return ((size_t)s * (s + 1) + s) * sizeof(double); }
 static constexpr size_t kMaxSmem = 227 * 1024 - 2048;  // dynamic budget (static smem is extra)
 
 int launch_chol_system(const SysArgs& a, int p, cudaStream_t st) {
   if (p <= 0) return RAC_OK;
+  const size_t pmem = sweep_smem_bytes(a.s);
+  if (pmem <= kMaxSmem) {
+    int rc = check_cuda(cudaFuncSetAttribute(sweep_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)pmem),
+                        "sweep_inverse smem attribute");
+    if (rc) return rc;
+    sweep_inverse_kernel<<<p, CTHREADS, pmem, st>>>(a);
+    return check_launch("sweep_inverse");
+  }
   const size_t smem = chol_smem_bytes(a.s);
   if (smem <= kMaxSmem) {
     int rc = check_cuda(cudaFuncSetAttribute(chol_inverse_kernel<true>,
@@ -353,7 +480,7 @@ int launch_chol_system(const SysArgs& a, int p, cudaStream_t st) {
 }
 
 size_t chol_scratch_bytes(int s, int p) {
-  if (chol_smem_bytes(s) <= kMaxSmem) return 0;
+  if (sweep_smem_bytes(s) <= kMaxSmem || chol_smem_bytes(s) <= kMaxSmem) return 0;
   return (size_t)p * s * (s + 1) * sizeof(double);
 }
 

@@ -1,0 +1,18 @@
+"""Small driver for ncu: a few RAC sweeps of one BASELINE config through the native engine."""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, '.')
+from paper_1907_01995_b200 import _device, configs, elastic_net as en
+from paper_1907_01995_b200.problems import Mode
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+case = configs.GENERATORS[cfg]()
+m, n = case.X.shape
+sol = en.EnSolver(m, n, case.block_size, Mode.RAC, case.lam, case.alpha, case.gamma)
+sol.set_data(case.X, case.y)
+perms = _device.PermutationFeeder(np.random.default_rng(0), n, sol.dev).draw(sweeps)
+sol.run(perms, None)
+torch.cuda.synchronize()
+print("ok", sol.progress())

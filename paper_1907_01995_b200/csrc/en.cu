@@ -35,7 +35,7 @@ constexpr int kResCS = 2;          // cluster size of the resident chain (148 SM
 
 struct EnChainArgs {
   const double* Xc;
-  int64_t ld, m;
+  int64_t ld, m, n;
   int s, p, nrc;        // block size, blocks, row chunks
   const int32_t* idx;   // [p][s] block table of this sweep
   const int32_t* order; // [p] visit order (nullptr: identity)
@@ -322,6 +322,7 @@ int en_chain(rac_en_ctx* c, double tol) {
   EnChainArgs a{};
   a.Xc = c->Xc;
   a.ld = c->ld;
+  a.n = c->n;
   a.m = c->m;
   a.s = c->s;
   a.p = c->p;
@@ -358,7 +359,7 @@ int en_chain(rac_en_ctx* c, double tol) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->P);
     cfg.blockDim = dim3(ENT);
-    cfg.dynamicSmemBytes = res_smem_bytes<32, kResCS>(c->s, c->nch);
+    cfg.dynamicSmemBytes = res_smem_bytes<kResCS>(c->s, c->nch);
     cfg.stream = c->st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -369,7 +370,7 @@ int en_chain(rac_en_ctx* c, double tol) {
     at[1].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    return check_cuda(cudaLaunchKernelExC(&cfg, (const void*)en_chain_res_kernel<32, kResCS>, rargs),
+    return check_cuda(cudaLaunchKernelExC(&cfg, (const void*)en_chain_res_kernel<kResCS>, rargs),
                       "en_chain_res (cluster cooperative launch)");
   }
   size_t smem = en_chain_smem(c->s, c->RC);
@@ -433,9 +434,9 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
     const int nrc32 = (int)((m + 31) / 32);
     int Pc = std::max(kResCS, std::min(num_sms(), (nrc32 + kResCS - 1) / kResCS * kResCS) / kResCS * kResCS);
     const int nch = (nrc32 + Pc - 1) / Pc;
-    const size_t rs = res_smem_bytes<32, kResCS>(s, nch);
+    const size_t rs = res_smem_bytes<kResCS>(s, nch);
     if (want == 1 && s <= ENT && rs <= 226 * 1024) {
-      void* rk = (void*)en_chain_res_kernel<32, kResCS>;
+      void* rk = (void*)en_chain_res_kernel<kResCS>;
       if (cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs) == cudaSuccess &&
           cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) == cudaSuccess) {
         cudaLaunchConfig_t cfg = {};

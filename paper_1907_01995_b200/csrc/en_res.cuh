@@ -1,12 +1,14 @@
 // Resident-tile cluster chain for the elastic-net sweep (included by en.cu).
 //
-// Every CTA owns a fixed set of RC-row chunks of X.  The columns of the
+// Every CTA owns a fixed set of 32-row chunks of X.  The columns of the
 // current block stay RESIDENT in shared memory from the row phase that used
 // them as "next" to the one that applies their update, and everything the
-// next block needs — its X tile, its rows of inv_b, and c/xi/z/beta at its
-// indices — is prefetched with cp.async while the current block is solved.
-// CTAs form clusters of CS that pre-reduce partials through DSMEM and split
-// the s x s mat-vec.  Per block: two cluster barriers + one grid barrier.
+// next block needs — its X column segments (one 256-byte TMA bulk copy each,
+// SASS UBLKCP, completing on an mbarrier), its rows of inv_b (one bulk copy),
+// and c/xi/z at its indices — is prefetched while the current block is
+// solved.  CTAs form clusters of CS that pre-reduce partials through DSMEM
+// and split the s x s mat-vec.  Per block: two cluster barriers + one grid
+// barrier, and the row phase is pure shared-memory arithmetic.
 //
 //   R(t)   r += X[rows, b_t] delta_t ;  partial_{t+1} = X[rows, b_{t+1}]'(r - X beta)
 //   cl.sync; rank slice of the cluster sum -> global (double-buffered by parity)
@@ -24,39 +26,39 @@ namespace rac {
 
 namespace cg = cooperative_groups;
 
+constexpr int RES_RC = 32;        // rows per chunk (one 256-byte segment per column)
+constexpr int RES_QMAX = ENT / 8; // columns per warp in the partial (s <= 256)
+
 struct ResSmem {
-  double* tiles;   // [2][nch][s][RC+1]
-  double* ginv;    // [sl][s]     inv_b rows of this rank's slice (next block)
-  double* cxz;     // [3][s]      c, xi, z at the next block's indices
-  double* sX;      // [s]         beta at the next block's indices
-  double* sDel;    // [s]         full delta of the current block
+  double* tiles;   // [2][nch][s][32]   (column segments, unpadded: TMA destination)
+  double* ginv;    // [sl][s]            inv_b rows of this rank's slice
+  double* cxz;     // [3][s]             c, xi, z at the block's indices
+  double* sX;      // [s]                beta at the next block's indices
+  double* sDel;    // [s]                full delta of the current block
   double* sRhs;    // [s]
-  double* sPart;   // [s]         this CTA's partial (read by cluster peers)
-  double* sSlice;  // [2s]        delta slice (peers read) | pending beta (cluster 0)
-  double* sR;      // [nch*RC]    resident rows of r
-  double* red;     // [max(NG*RC, 256)]
-  double* sT;      // [RC]
+  double* sPart;   // [s]                this CTA's partial (cluster peers read it)
+  double* sSlice;  // [2s]               delta slice | pending beta (cluster 0)
+  double* sR;      // [nch*32]           resident rows of r
+  double* red;     // [256]
+  double* sT;      // [32]
+  uint64_t* bars;  // [3]                tile slot 0/1, solve data
   int* pend;       // [s]
 };
 
-template <int RC>
-__host__ __device__ __forceinline__ size_t res_red_doubles() {
-  return RowPhase<RC>::NG * RC > 256 ? RowPhase<RC>::NG * RC : 256;
-}
-
-template <int RC, int CS>
+template <int CS>
 __host__ __device__ size_t res_smem_bytes(int s, int nch) {
   const size_t sl = (s + CS - 1) / CS;
-  return (2 * (size_t)nch * s * (RC + 1) + sl * s + 3 * (size_t)s + 6 * (size_t)s + (size_t)nch * RC +
-          res_red_doubles<RC>() + RC) * sizeof(double) + (size_t)s * sizeof(int);
+  return (2 * (size_t)nch * s * RES_RC + sl * s + 9 * (size_t)s + (size_t)nch * RES_RC + 256 + RES_RC + 4) *
+             sizeof(double) +
+         (size_t)s * sizeof(int);
 }
 
-template <int RC, int CS>
+template <int CS>
 __device__ __forceinline__ ResSmem carve_res(double* base, int s, int nch) {
   const int sl = (s + CS - 1) / CS;
   ResSmem w;
   double* p = base;
-  w.tiles = p; p += 2 * (size_t)nch * s * (RC + 1);
+  w.tiles = p; p += 2 * (size_t)nch * s * RES_RC;
   w.ginv = p; p += (size_t)sl * s;
   w.cxz = p; p += 3 * s;
   w.sX = p; p += s;
@@ -64,21 +66,22 @@ __device__ __forceinline__ ResSmem carve_res(double* base, int s, int nch) {
   w.sRhs = p; p += s;
   w.sPart = p; p += s;
   w.sSlice = p; p += 2 * s;
-  w.sR = p; p += (size_t)nch * RC;
-  w.red = p; p += res_red_doubles<RC>();
-  w.sT = p; p += RC;
+  w.sR = p; p += (size_t)nch * RES_RC;
+  w.red = p; p += 256;
+  w.sT = p; p += RES_RC;
+  w.bars = reinterpret_cast<uint64_t*>(p); p += 4;
   w.pend = reinterpret_cast<int*>(p);
   return w;
 }
 
-template <int RC, int CS>
+template <int CS>
 __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nch) {
   if (a.ctrl[0]) return;
-  constexpr int NG = RowPhase<RC>::NG;
-  extern __shared__ __align__(16) double rsm[];
+  constexpr int RC = RES_RC;
+  extern __shared__ __align__(128) double rsm[];
   cg::cluster_group cl = cg::this_cluster();
   const int s = a.s;
-  const ResSmem w = carve_res<RC, CS>(rsm, s, nch);
+  const ResSmem w = carve_res<CS>(rsm, s, nch);
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = ENT / 32;
   const int P = gridDim.x, C = P / CS;
@@ -91,6 +94,8 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
       int b = a.order ? a.order[t] : t;
       if (a.info[b]) { bad = b + 1; break; }
     }
+    for (int q = 0; q < 3; ++q) mbar_init(w.bars + q, 1);
+    mbar_fence_init();
   }
   __syncthreads();
   if (bad) {
@@ -102,35 +107,56 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
   int tp = 0;
   if (tr) a.trace[tp++] = gtimer();
   auto blk = [&](int t) { return a.order ? a.order[t] : t; };
-  auto tile = [&](int slot, int k) { return w.tiles + ((size_t)slot * nch + k) * s * (RC + 1); };
+  auto tile = [&](int slot, int k) { return w.tiles + ((size_t)slot * nch + k) * s * RC; };
+  int nchv = 0;  // valid chunks of this CTA
+  for (int k = 0; k < nch; ++k)
+    if (blockIdx.x + k * P < a.nrc) nchv = k + 1;
   // resident rows of r
-  for (int k = 0; k < nch; ++k) {
+  for (int k = 0; k < nchv; ++k) {
     const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
     for (int i = tid; i < RC; i += ENT) w.sR[k * RC + i] = (i0 + i < a.m) ? a.r[i0 + i] : 0.0;
   }
-  // async fetch of block b's X columns (all own chunks) into a tile slot
+  unsigned par[3] = {0u, 0u, 0u};
+  const bool bulk_inv = ((s & 1) == 0);  // 16-byte aligned rows of inv
+  // TMA fetch of block b's column segments (all own chunks) into a tile slot.
+  // Precondition: the slot's previous contents are dead for every thread.
   auto issue_tile = [&](int slot, int b) {
+    const int nvalid = (int)min64(s, a.n - (int64_t)b * s);
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(w.bars + slot, (unsigned)(nchv * nvalid * RC * sizeof(double)));
+    }
+    __syncthreads();
     const int32_t* bi = a.idx + (int64_t)b * s;
-    for (int k = 0; k < nch; ++k) {
-      const int ch = blockIdx.x + k * P;
-      if (ch >= a.nrc) break;
-      const int64_t i0 = (int64_t)ch * RC;
-      double* dst = tile(slot, k);
-      for (int e = tid; e < s * RC; e += ENT) {
-        const int j = e / RC, i = e - j * RC;
-        const int g = __ldg(bi + j);
-        double* d = dst + j * (RC + 1) + i;
-        if (g >= 0) cp_async8(d, a.Xc + (int64_t)g * a.ld + i0 + i);
-        else *d = 0.0;
+    for (int e = tid; e < nchv * s; e += ENT) {
+      const int k = e / s, j = e - k * s;
+      const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
+      double* dst = tile(slot, k) + (size_t)j * RC;
+      const int g = __ldg(bi + j);
+      if (g >= 0) {
+        bulk_g2s(dst, a.Xc + (int64_t)g * a.ld + i0, RC * sizeof(double), w.bars + slot);
+      } else {
+        for (int i = 0; i < RC; ++i) dst[i] = 0.0;
       }
     }
   };
-  // async fetch of what the S phase of block b needs: inv rows of the slice, c/xi/z
+  auto wait_tile = [&](int slot) {
+    mbar_wait(w.bars + slot, par[slot]);
+    par[slot] ^= 1u;
+  };
+  // inv rows of the slice (bulk) + c/xi/z at the block's indices (cp.async)
   auto issue_solve = [&](int b) {
     const int32_t* bi = a.idx + (int64_t)b * s;
     const double* Ib = a.inv + (int64_t)b * s * s + (int64_t)j0 * s;
     const int rows = j1 - j0;
-    for (int e = tid; e < rows * s; e += ENT) cp_async8(w.ginv + e, Ib + e);
+    if (bulk_inv) {
+      if (tid == 0) {
+        mbar_arrive_expect_tx(w.bars + 2, (unsigned)(rows * s * sizeof(double)));
+        bulk_g2s(w.ginv, Ib, (unsigned)(rows * s * sizeof(double)), w.bars + 2);
+      }
+    } else {
+      for (int e = tid; e < rows * s; e += ENT) cp_async8(w.ginv + e, Ib + e);
+    }
     for (int j = tid; j < s; j += ENT) {
       const int g = __ldg(bi + j);
       if (g >= 0) {
@@ -143,52 +169,68 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
         w.cxz[2 * s + j] = 0.0;
       }
     }
+    cp_async_commit();
   };
-  const int grp = warp * (32 / RC) + lane / RC, ri = lane % RC;
+  auto wait_solve = [&]() {
+    if (bulk_inv) {
+      mbar_wait(w.bars + 2, par[2]);
+      par[2] ^= 1u;
+    }
+    cp_async_wait<0>();
+  };
+  // one row phase: optional r-update with slot sp (delta in sDel) and optional
+  // partial for slot sn (x values in sX) -> sPart.  Layout T[j][i], lanes = rows.
   auto row_phase_res = [&](int sp, int sn) {
-    double part = 0.0;
-    for (int k = 0; k < nch; ++k) {
-      const int ch = blockIdx.x + k * P;
-      if (ch >= a.nrc) break;
-      const int64_t i0 = (int64_t)ch * RC;
+    double acc[RES_QMAX];
+#pragma unroll
+    for (int c = 0; c < RES_QMAX; ++c) acc[c] = 0.0;
+    for (int k = 0; k < nchv; ++k) {
+      const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
       const int rows = (int)min64(RC, a.m - i0);
       double* rr = w.sR + k * RC;
       if (sp >= 0) {
         const double* T = tile(sp, k);
         double u = 0.0;
-        for (int j = grp; j < s; j += NG) u += T[j * (RC + 1) + ri] * w.sDel[j];
-        w.red[grp * RC + ri] = u;
+        for (int j = warp; j < s; j += nw) u += T[j * RC + lane] * w.sDel[j];
+        w.red[warp * RC + lane] = u;
         __syncthreads();
         if (tid < rows) {
           double tot = w.red[tid];
-          for (int q = 1; q < NG; ++q) tot += w.red[q * RC + tid];
+          for (int q = 1; q < nw; ++q) tot += w.red[q * RC + tid];
           rr[tid] += tot;
         }
+        __syncthreads();
       }
       if (sn >= 0) {
         const double* T = tile(sn, k);
         double u = 0.0;
-        for (int j = grp; j < s; j += NG) u += T[j * (RC + 1) + ri] * w.sX[j];
-        __syncthreads();   // red reuse + rr update visible
-        w.red[grp * RC + ri] = u;
+        for (int j = warp; j < s; j += nw) u += T[j * RC + lane] * w.sX[j];
+        w.red[warp * RC + lane] = u;
         __syncthreads();
         if (tid < RC) {
           double tot = w.red[tid];
-          for (int q = 1; q < NG; ++q) tot += w.red[q * RC + tid];
+          for (int q = 1; q < nw; ++q) tot += w.red[q * RC + tid];
           w.sT[tid] = (tid < rows) ? rr[tid] - tot : 0.0;
         }
         __syncthreads();
-        if (tid < s) {
-          const double* col = T + tid * (RC + 1);
-          double acc = part;
-#pragma unroll 8
-          for (int i = 0; i < RC; ++i) acc += col[i] * w.sT[i];
-          part = acc;
+        const double ti = w.sT[lane];
+#pragma unroll
+        for (int c = 0; c < RES_QMAX; ++c) {
+          const int j = warp + c * nw;
+          if (j < s) acc[c] += T[j * RC + lane] * ti;
         }
       }
-      __syncthreads();
     }
-    if (sn >= 0 && tid < s) w.sPart[tid] = part;
+    if (sn >= 0) {
+#pragma unroll
+      for (int c = 0; c < RES_QMAX; ++c) {
+        const int j = warp + c * nw;
+        if (j < s) {
+          const double v = warp_sum(acc[c]);
+          if (lane == 0) w.sPart[j] = v;
+        }
+      }
+    }
   };
   auto load_beta = [&](int b) {
     const int32_t* bi = a.idx + (int64_t)b * s;
@@ -215,17 +257,14 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
       my_max = fmax(my_max, fabs(sub(zn, zo)));
     }
   };
-  // G threads per rhs entry; thread sums cluster partials q = g, g+G, ...
-  const int G = max(1, ENT / s);
+  const int G = max(1, ENT / s);  // threads per rhs entry
 
-  // ---- prologue
+  // ---- prologue: tiles of blocks 0 and 1, solve data of block 0
   issue_tile(0, blk(0));
-  cp_async_commit();
   if (a.p > 1) issue_tile(1, blk(1));
   issue_solve(blk(0));
-  cp_async_commit();
-  cp_async_wait<1>();
   load_beta(blk(0));
+  wait_tile(0);
   __syncthreads();
   row_phase_res(-1, 0);
   if (tr) a.trace[tp++] = gtimer();
@@ -254,7 +293,7 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
         for (int q = g; q < C; q += G) acc += ldcg(gpart + (int64_t)q * s + j);
       w.red[tid] = acc;
     }
-    cp_async_wait<0>();   // inv rows + c/xi/z of this block, tile of the next
+    wait_solve();
     __syncthreads();
     for (int j = tid; j < s; j += ENT) {
       double acc = w.red[j * G];
@@ -286,18 +325,21 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     for (int i = tid; i < s; i += ENT) w.sDel[i] = cl.map_shared_rank(w.sSlice, i / sl)[i];
     // ---- row phase (tile of b resident, tile of the next block prefetched)
     const bool more = t + 1 < a.p;
-    if (more) load_beta(blk(t + 1));
+    if (more) {
+      load_beta(blk(t + 1));
+      wait_tile((t + 1) & 1);
+    }
     __syncthreads();
     row_phase_res(t & 1, more ? ((t + 1) & 1) : -1);
     if (more) {
+      __syncthreads();   // every thread is done with slot t&1 and with ginv/cxz
       if (t + 2 < a.p) issue_tile(t & 1, blk(t + 2));
       issue_solve(blk(t + 1));
-      cp_async_commit();
     }
     if (tr) a.trace[tp++] = gtimer();
   }
   // write back resident r
-  for (int k = 0; k < nch; ++k) {
+  for (int k = 0; k < nchv; ++k) {
     const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
     for (int i = tid; i < RC; i += ENT)
       if (i0 + i < a.m) a.r[i0 + i] = w.sR[k * RC + i];

@@ -178,312 +178,6 @@ int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx,
   return check_launch("gram");
 }
 
-// ---------------------------------------------------------------------------
-// K3: Cholesky + explicit inverse of each block system, one CTA per block.
-//     sys = (sum_z ws_z) / div * mul  (+ H_bb)  + shift*I  (+ ridge_rel*max diag * I)
-// The matrix lives in shared memory when it fits, else in a global scratch.
-// ---------------------------------------------------------------------------
-
-
-constexpr int CTHREADS = 512;
-
-template <bool SMEM>
-__global__ void __launch_bounds__(CTHREADS) chol_inverse_kernel(SysArgs a) {
-  extern __shared__ __align__(16) double csm[];
-  if (a.done && *a.done) return;
-  const int s = a.s;
-  const int slot = blockIdx.x;
-  const int b = a.blk_list ? a.blk_list[slot] : slot;
-  const int ld = s + 1;
-  double* A = SMEM ? csm : a.scratch + (int64_t)b * s * ld;
-  double* dY = SMEM ? csm + (int64_t)s * ld : a.inv + (int64_t)b * s * s;  // diag of L^-1 (uses inv row 0 as scratch in global mode)
-  __shared__ int fail;
-  __shared__ double red[CTHREADS / 32];
-  const int tid = threadIdx.x;
-  if (tid == 0) fail = 0;
-
-  // ---- assemble
-  const int32_t* bidx = a.idx ? a.idx + (int64_t)b * s : nullptr;
-  double* hbo = a.hbb_out ? a.hbb_out + (int64_t)b * s * s : nullptr;
-  for (int e = tid; e < s * s; e += CTHREADS) {
-    int i = e / s, j = e - i * s;
-    const bool pad = bidx && (bidx[i] < 0 || bidx[j] < 0);
-    double v = 0.0;
-    double h = 0.0;
-    if (a.H && !pad) h = a.H[(int64_t)bidx[i] * a.ldh + bidx[j]];
-    if (hbo) hbo[e] = h;
-    if (pad) {
-      v = (i == j) ? 1.0 : 0.0;   // keeps the short last block's leading part exact
-    } else if (j <= i) {
-      if (a.ws) {
-        const double* src = a.ws + (int64_t)b * a.splits * s * s + (int64_t)i * s + j;
-        double acc = src[0];
-        for (int z = 1; z < a.splits; ++z) acc += src[(int64_t)z * s * s];
-        if (a.div != 1.0) acc = acc / a.div;
-        if (a.mul != 1.0) acc = a.mul * acc;
-        v = acc;
-      }
-      if (a.H) v = a.ws ? h + v : h;
-      if (i == j) v += a.shift;
-    }
-    A[(int64_t)i * ld + j] = v;
-  }
-  __syncthreads();
-  if (a.ridge_rel > 0.0) {
-    double mx = -INFINITY;
-    for (int i = tid; i < s; i += CTHREADS)
-      if (!bidx || bidx[i] >= 0) mx = fmax(mx, A[(int64_t)i * ld + i]);
-    mx = warp_max(mx);
-    if ((tid & 31) == 0) red[tid >> 5] = mx;
-    __syncthreads();
-    if (tid == 0) {
-      double m2 = red[0];
-      for (int w = 1; w < CTHREADS / 32; ++w) m2 = fmax(m2, red[w]);
-      red[0] = a.ridge_rel * m2;
-    }
-    __syncthreads();
-    const double ridge = red[0];
-    for (int i = tid; i < s; i += CTHREADS)
-      if (!bidx || bidx[i] >= 0) A[(int64_t)i * ld + i] += ridge;
-    __syncthreads();
-  }
-  if (a.mat_out) {
-    double* mo = a.mat_out + (int64_t)b * s * s;
-    for (int e = tid; e < s * s; e += CTHREADS) {
-      int i = e / s, j = e - i * s;
-      mo[e] = (j <= i) ? A[(int64_t)i * ld + j] : A[(int64_t)j * ld + i];
-    }
-  }
-
-  // ---- Cholesky (right-looking), L in the lower triangle (diag included)
-  const int tx = tid & 31, ty = tid >> 5;  // 32 x 16 thread grid
-  for (int k = 0; k < s; ++k) {
-    if (tid == 0) {
-      double d = A[(int64_t)k * ld + k];
-      if (!(d > 0.0) || !isfinite(d)) {
-        fail = k + 1;
-      } else {
-        A[(int64_t)k * ld + k] = sqrt(d);
-      }
-    }
-    __syncthreads();
-    if (fail) break;
-    const double piv = A[(int64_t)k * ld + k];
-    for (int i = k + 1 + tid; i < s; i += CTHREADS) A[(int64_t)i * ld + k] /= piv;
-    __syncthreads();
-    for (int i = k + 1 + ty; i < s; i += CTHREADS / 32) {
-      const double lik = A[(int64_t)i * ld + k];
-      for (int j = k + 1 + tx; j <= i; j += 32) A[(int64_t)i * ld + j] -= lik * A[(int64_t)j * ld + k];
-    }
-    __syncthreads();
-  }
-  if (fail) {
-    if (tid == 0) a.info[b] = fail;
-    return;
-  }
-  if (tid == 0) a.info[b] = 0;
-
-  // ---- Y = L^{-1}: Y[i][c] (c < i) stored at A[c][i] (strict upper), diag in dY
-  for (int e = tid; e < s * s; e += CTHREADS) {
-    int c = e / s, i = e - c * s;
-    if (c < i) A[(int64_t)c * ld + i] = 0.0;
-  }
-  __syncthreads();
-  for (int k = 0; k < s; ++k) {
-    const double lkk = A[(int64_t)k * ld + k];
-    for (int c = tid; c < k; c += CTHREADS) A[(int64_t)c * ld + k] /= lkk;
-    if (tid == 0) dY[k] = 1.0 / lkk;
-    __syncthreads();
-    // Y[i][c] -= L[i][k] * Y[k][c]   for i > k, c <= k
-    for (int i = k + 1 + ty; i < s; i += CTHREADS / 32) {
-      const double lik = A[(int64_t)i * ld + k];
-      for (int c = tx; c <= k; c += 32) {
-        const double ykc = (c == k) ? dY[k] : A[(int64_t)c * ld + k];
-        A[(int64_t)c * ld + i] -= lik * ykc;
-      }
-    }
-    __syncthreads();
-  }
-
-  // ---- inv = Y' Y :  inv[i][j] = sum_{r >= max(i,j)} Y[r][i] Y[r][j]
-  double* out = a.inv + (int64_t)b * s * s;
-  const int total = s * (s + 1) / 2;
-  for (int e = tid; e < total; e += CTHREADS) {
-    // e -> (i, j), j <= i, row-major over the lower triangle
-    int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-    while ((i + 1) * (i + 2) / 2 <= e) ++i;
-    while (i * (i + 1) / 2 > e) --i;
-    int j = e - i * (i + 1) / 2;
-    double acc = dY[i] * ((i == j) ? dY[j] : A[(int64_t)j * ld + i]);
-    for (int r = i + 1; r < s; ++r) acc += A[(int64_t)i * ld + r] * A[(int64_t)j * ld + r];
-    if (SMEM) {
-      out[(int64_t)i * s + j] = acc;
-      out[(int64_t)j * s + i] = acc;
-    } else {
-      // dY aliases out row 0 in global mode: stage through A's lower triangle (dead now)
-      A[(int64_t)i * ld + j] = acc;
-    }
-  }
-  if (!SMEM) {
-    __syncthreads();
-    for (int e = tid; e < s * s; e += CTHREADS) {
-      int i = e / s, j = e - i * s;
-      out[e] = (j <= i) ? A[(int64_t)i * ld + j] : A[(int64_t)j * ld + i];
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K3 (s <= 236): the block system is assembled into the PACKED lower triangle
-// in shared memory and inverted in place by the symmetric sweep operator
-// (Gauss-Jordan without pivoting, valid for SPD):  for each pivot k
-//     d = a_kk;  a_ij -= a_ik a_kj / d;  a_ik /= d;  a_kk = -1/d
-// which leaves -A^{-1}.  The pivots are the Cholesky pivots L_kk^2, so a
-// non-positive pivot reports exactly the leading minor np.linalg.cholesky
-// rejects (elastic_net.py:213-219, engine.py:160-167).  One CTA per block,
-// s steps of two barriers each; no global round trips.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }  // j <= i
-
-__global__ void __launch_bounds__(CTHREADS) sweep_inverse_kernel(SysArgs a) {
-  extern __shared__ __align__(16) double psm[];
-  if (a.done && *a.done) return;
-  const int s = a.s;
-  const int b = a.blk_list ? a.blk_list[blockIdx.x] : blockIdx.x;
-  double* P = psm;                                 // s(s+1)/2
-  double* col = psm + (size_t)s * (s + 1) / 2;     // s
-  __shared__ int fail;
-  __shared__ double red[CTHREADS / 32];
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  if (tid == 0) fail = 0;
-  const int32_t* bidx = a.idx ? a.idx + (int64_t)b * s : nullptr;
-  double* hbo = a.hbb_out ? a.hbb_out + (int64_t)b * s * s : nullptr;
-  // ---- assemble (lower, packed)
-  for (int i = ty; i < s; i += CTHREADS / 32) {
-    const int off = pk(i, 0);
-    for (int j = tx; j < s; j += 32) {
-      const bool pad = bidx && (bidx[i] < 0 || bidx[j] < 0);
-      double h = 0.0;
-      if (a.H && !pad) h = a.H[(int64_t)bidx[i] * a.ldh + bidx[j]];
-      if (hbo) hbo[(int64_t)i * s + j] = h;
-      if (j > i) continue;
-      double v;
-      if (pad) {
-        v = (i == j) ? 1.0 : 0.0;
-      } else {
-        v = 0.0;
-        if (a.ws) {
-          const double* src = a.ws + (int64_t)b * a.splits * s * s + (int64_t)i * s + j;
-          double acc = src[0];
-          for (int z = 1; z < a.splits; ++z) acc += src[(int64_t)z * s * s];
-          if (a.div != 1.0) acc = acc / a.div;
-          if (a.mul != 1.0) acc = a.mul * acc;
-          v = acc;
-        }
-        if (a.H) v = a.ws ? h + v : h;
-        if (i == j) v += a.shift;
-      }
-      P[off + j] = v;
-    }
-  }
-  __syncthreads();
-  if (a.ridge_rel > 0.0) {
-    double mx = -INFINITY;
-    for (int i = tid; i < s; i += CTHREADS)
-      if (!bidx || bidx[i] >= 0) mx = fmax(mx, P[pk(i, i)]);
-    mx = warp_max(mx);
-    if (tx == 0) red[ty] = mx;
-    __syncthreads();
-    double m2 = red[0];
-    for (int w = 1; w < CTHREADS / 32; ++w) m2 = fmax(m2, red[w]);
-    const double ridge = a.ridge_rel * m2;
-    __syncthreads();
-    for (int i = tid; i < s; i += CTHREADS)
-      if (!bidx || bidx[i] >= 0) P[pk(i, i)] += ridge;
-    __syncthreads();
-  }
-  if (a.mat_out) {
-    double* mo = a.mat_out + (int64_t)b * s * s;
-    for (int e = tid; e < s * s; e += CTHREADS) {
-      const int i = e / s, j = e - i * s;
-      mo[e] = (j <= i) ? P[pk(i, j)] : P[pk(j, i)];
-    }
-  }
-  // ---- sweep every pivot
-  for (int k = 0; k < s; ++k) {
-    const double d = P[pk(k, k)];
-    if (!(d > 0.0) || !isfinite(d)) {
-      if (tid == 0) fail = k + 1;
-      break;   // uniform: every thread read the same d
-    }
-    for (int i = tid; i < s; i += CTHREADS) col[i] = (i >= k) ? P[pk(i, k)] : P[pk(k, i)];
-    __syncthreads();
-    const double dinv = 1.0 / d;
-    for (int i = ty; i < s; i += CTHREADS / 32) {
-      const int off = pk(i, 0);
-      const double ci = col[i];
-      const double cid = ci * dinv;
-      for (int j = tx; j <= i; j += 32) {
-        double v;
-        if (i == k) {
-          v = (j == k) ? -dinv : col[j] * dinv;
-        } else if (j == k) {
-          v = cid;
-        } else {
-          v = P[off + j] - cid * col[j];
-        }
-        P[off + j] = v;
-      }
-    }
-    __syncthreads();
-  }
-  __syncthreads();
-  if (fail) {
-    if (tid == 0) a.info[b] = fail;
-    return;
-  }
-  if (tid == 0) a.info[b] = 0;
-  double* out = a.inv + (int64_t)b * s * s;
-  for (int e = tid; e < s * s; e += CTHREADS) {
-    const int i = e / s, j = e - i * s;
-    out[e] = -((j <= i) ? P[pk(i, j)] : P[pk(j, i)]);
-  }
-}
-
-static size_t sweep_smem_bytes(int s) { return ((size_t)s * (s + 1) / 2 + s) * sizeof(double); }
-static size_t chol_smem_bytes(int s) { return ((size_t)s * (s + 1) + s) * sizeof(double); }
-static constexpr size_t kMaxSmem = 227 * 1024 - 2048;  // dynamic budget (static smem is extra)
-
-int launch_chol_system(const SysArgs& a, int p, cudaStream_t st) {
-  if (p <= 0) return RAC_OK;
-  const size_t pmem = sweep_smem_bytes(a.s);
-  if (pmem <= kMaxSmem) {
-    int rc = check_cuda(cudaFuncSetAttribute(sweep_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)pmem),
-                        "sweep_inverse smem attribute");
-    if (rc) return rc;
-    sweep_inverse_kernel<<<p, CTHREADS, pmem, st>>>(a);
-    return check_launch("sweep_inverse");
-  }
-  const size_t smem = chol_smem_bytes(a.s);
-  if (smem <= kMaxSmem) {
-    int rc = check_cuda(cudaFuncSetAttribute(chol_inverse_kernel<true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                        "chol_inverse smem attribute");
-    if (rc) return rc;
-    chol_inverse_kernel<true><<<p, CTHREADS, smem, st>>>(a);
-  } else {
-    if (!a.scratch) return set_error(RAC_ERR_ARG, "chol: scratch required for s=%d", a.s);
-    chol_inverse_kernel<false><<<p, CTHREADS, 0, st>>>(a);
-  }
-  return check_launch("chol_inverse");
-}
-
-size_t chol_scratch_bytes(int s, int p) {
-  if (sweep_smem_bytes(s) <= kMaxSmem || chol_smem_bytes(s) <= kMaxSmem) return 0;
-  return (size_t)p * s * (s + 1) * sizeof(double);
-}
-
 }  // namespace rac
 
 extern "C" size_t rac_gram_workspace_bytes(int64_t len, int32_t s, int32_t p) {

@@ -224,9 +224,19 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
         }
       }
       __syncthreads();
-      // unconstrained solution x = M^{-1} r
-      cta_matvec(a.inv + (int64_t)b * s * s, s, seff, seff, w.bw.r, w.bw.x);
-      __syncthreads();
+      // unconstrained solution x = L^-T L^-1 r with the block's Cholesky factor
+      // (engine.py:201-203: cho_solve with the full-block factor)
+      {
+        const double* Lb = a.inv + (int64_t)b * s * s;
+        for (int e = tid; e < seff * seff; e += QPT) {
+          const int i = e / seff, j = e - i * seff;
+          w.bw.L[e] = Lb[(int64_t)i * s + j];
+        }
+        for (int i = tid; i < seff; i += QPT) w.bw.x[i] = w.bw.r[i];
+        __syncthreads();
+        warp_chol_solve(w.bw.L, seff, seff, w.bw.x);
+        __syncthreads();
+      }
       int fail = box_active_set(a.Mb + (int64_t)b * s * s, s, seff, w.bw);
       if (fail) {
         if (tid == 0) { a.ctrl[2] = b + 1; a.ctrl[0] = 1; }
@@ -485,6 +495,7 @@ int qp_block_systems(rac_qp_ctx* c) {
   a.hbb_out = c->Hbb;
   a.scratch = c->scratch;
   a.info = c->info;
+  a.mode = FACTOR_CHOL;
   a.done = c->ctrl;
   return launch_chol_system(a, c->p, c->st);
 }

@@ -54,7 +54,10 @@ struct SysArgs {
   double* scratch;    // [p][s][s] global scratch for the large-s path
   int32_t* info;
   const int32_t* done;  // skip when *done (converged / failed)
+  int mode;             // FACTOR_INVERSE: sys^{-1} into inv; FACTOR_CHOL: lower L into inv
 };
+constexpr int FACTOR_INVERSE = 0;
+constexpr int FACTOR_CHOL = 1;
 int launch_chol_system(const SysArgs& a, int p, cudaStream_t st);
 size_t chol_scratch_bytes(int s, int p);
 

@@ -359,7 +359,7 @@ int en_chain(rac_en_ctx* c, double tol) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->P);
     cfg.blockDim = dim3(ENT);
-    cfg.dynamicSmemBytes = res_smem_bytes<kResCS>(c->s, c->nch);
+    cfg.dynamicSmemBytes = res_smem_bytes<kResCS>(c->s, c->nch, c->p);
     cfg.stream = c->st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -434,7 +434,7 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
     const int nrc32 = (int)((m + 31) / 32);
     int Pc = std::max(kResCS, std::min(num_sms(), (nrc32 + kResCS - 1) / kResCS * kResCS) / kResCS * kResCS);
     const int nch = (nrc32 + Pc - 1) / Pc;
-    const size_t rs = res_smem_bytes<kResCS>(s, nch);
+    const size_t rs = res_smem_bytes<kResCS>(s, nch, (int)((n + s - 1) / s));
     if (want == 1 && s <= ENT && rs <= 226 * 1024) {
       void* rk = (void*)en_chain_res_kernel<kResCS>;
       if (cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs) == cudaSuccess &&

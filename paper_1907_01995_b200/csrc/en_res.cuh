@@ -3,12 +3,13 @@
 // Every CTA owns a fixed set of 32-row chunks of X.  The columns of the
 // current block stay RESIDENT in shared memory from the row phase that used
 // them as "next" to the one that applies their update, and everything the
-// next block needs — its X column segments (one 256-byte TMA bulk copy each,
-// SASS UBLKCP, completing on an mbarrier), its rows of inv_b (one bulk copy),
-// and c/xi/z at its indices — is prefetched while the current block is
-// solved.  CTAs form clusters of CS that pre-reduce partials through DSMEM
-// and split the s x s mat-vec.  Per block: two cluster barriers + one grid
-// barrier, and the row phase is pure shared-memory arithmetic.
+// next blocks need — X column segments (one 256-byte TMA bulk copy each,
+// SASS UBLKCP, completing on an mbarrier), rows of inv_b (one bulk copy),
+// beta/c/xi/z at the block's indices (cp.async gathers) — is prefetched while
+// the current block is solved.  The sweep's whole block table sits in shared
+// memory.  CTAs form clusters of CS that pre-reduce partials through DSMEM and
+// split the s x s mat-vec.  Per block: two cluster barriers + one grid
+// barrier; the row phase is pure shared-memory arithmetic.
 //
 //   R(t)   r += X[rows, b_t] delta_t ;  partial_{t+1} = X[rows, b_{t+1}]'(r - X beta)
 //   cl.sync; rank slice of the cluster sum -> global (double-buffered by parity)
@@ -28,29 +29,31 @@ namespace cg = cooperative_groups;
 
 constexpr int RES_RC = 32;        // rows per chunk (one 256-byte segment per column)
 constexpr int RES_QMAX = ENT / 8; // columns per warp in the partial (s <= 256)
+constexpr int RES_BATCH = 16;     // independent partial loads in flight per thread
 
 struct ResSmem {
   double* tiles;   // [2][nch][s][32]   (column segments, unpadded: TMA destination)
   double* ginv;    // [sl][s]            inv_b rows of this rank's slice
   double* cxz;     // [3][s]             c, xi, z at the block's indices
-  double* sX;      // [s]                beta at the next block's indices
+  double* sX;      // [2][s]             beta at a block's indices, by block parity
   double* sDel;    // [s]                full delta of the current block
   double* sRhs;    // [s]
   double* sPart;   // [s]                this CTA's partial (cluster peers read it)
   double* sSlice;  // [2s]               delta slice | pending beta (cluster 0)
   double* sR;      // [nch*32]           resident rows of r
-  double* red;     // [256]
+  double* red;     // [256 * 2]
   double* sT;      // [32]
   uint64_t* bars;  // [3]                tile slot 0/1, solve data
   int* pend;       // [s]
+  int* sIdx;       // [p*s]              this sweep's block table
 };
 
 template <int CS>
-__host__ __device__ size_t res_smem_bytes(int s, int nch) {
+__host__ __device__ size_t res_smem_bytes(int s, int nch, int p) {
   const size_t sl = (s + CS - 1) / CS;
-  return (2 * (size_t)nch * s * RES_RC + sl * s + 9 * (size_t)s + (size_t)nch * RES_RC + 256 + RES_RC + 4) *
+  return (2 * (size_t)nch * s * RES_RC + sl * s + 10 * (size_t)s + (size_t)nch * RES_RC + 512 + RES_RC + 4) *
              sizeof(double) +
-         (size_t)s * sizeof(int);
+         ((size_t)s + (size_t)p * s) * sizeof(int);
 }
 
 template <int CS>
@@ -61,16 +64,17 @@ __device__ __forceinline__ ResSmem carve_res(double* base, int s, int nch) {
   w.tiles = p; p += 2 * (size_t)nch * s * RES_RC;
   w.ginv = p; p += (size_t)sl * s;
   w.cxz = p; p += 3 * s;
-  w.sX = p; p += s;
+  w.sX = p; p += 2 * s;
   w.sDel = p; p += s;
   w.sRhs = p; p += s;
   w.sPart = p; p += s;
   w.sSlice = p; p += 2 * s;
   w.sR = p; p += (size_t)nch * RES_RC;
-  w.red = p; p += 256;
+  w.red = p; p += 512;
   w.sT = p; p += RES_RC;
   w.bars = reinterpret_cast<uint64_t*>(p); p += 4;
   w.pend = reinterpret_cast<int*>(p);
+  w.sIdx = w.pend + s;
   return w;
 }
 
@@ -97,6 +101,7 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     for (int q = 0; q < 3; ++q) mbar_init(w.bars + q, 1);
     mbar_fence_init();
   }
+  for (int e = tid; e < a.p * s; e += ENT) w.sIdx[e] = a.idx[e];
   __syncthreads();
   if (bad) {
     if (blockIdx.x == 0 && tid == 0) { a.ctrl[2] = bad; a.ctrl[0] = 1; }
@@ -107,46 +112,49 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
   int tp = 0;
   if (tr) a.trace[tp++] = gtimer();
   auto blk = [&](int t) { return a.order ? a.order[t] : t; };
+  auto bidx = [&](int b) { return w.sIdx + (size_t)b * s; };
   auto tile = [&](int slot, int k) { return w.tiles + ((size_t)slot * nch + k) * s * RC; };
   int nchv = 0;  // valid chunks of this CTA
   for (int k = 0; k < nch; ++k)
     if (blockIdx.x + k * P < a.nrc) nchv = k + 1;
-  // resident rows of r
   for (int k = 0; k < nchv; ++k) {
     const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
     for (int i = tid; i < RC; i += ENT) w.sR[k * RC + i] = (i0 + i < a.m) ? a.r[i0 + i] : 0.0;
   }
   unsigned par[3] = {0u, 0u, 0u};
   const bool bulk_inv = ((s & 1) == 0);  // 16-byte aligned rows of inv
-  // TMA fetch of block b's column segments (all own chunks) into a tile slot.
-  // Precondition: the slot's previous contents are dead for every thread.
-  auto issue_tile = [&](int slot, int b) {
+  // TMA fetch of block b's column segments into a tile slot, plus beta at the
+  // block's indices (cp.async) into sX[parity].  The slot must be dead.
+  auto issue_tile = [&](int slot, int b, double* xdst) {
     const int nvalid = (int)min64(s, a.n - (int64_t)b * s);
     if (tid == 0) {
       fence_proxy_async();
       mbar_arrive_expect_tx(w.bars + slot, (unsigned)(nchv * nvalid * RC * sizeof(double)));
     }
     __syncthreads();
-    const int32_t* bi = a.idx + (int64_t)b * s;
+    const int* bi = bidx(b);
     for (int e = tid; e < nchv * s; e += ENT) {
       const int k = e / s, j = e - k * s;
       const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
       double* dst = tile(slot, k) + (size_t)j * RC;
-      const int g = __ldg(bi + j);
-      if (g >= 0) {
-        bulk_g2s(dst, a.Xc + (int64_t)g * a.ld + i0, RC * sizeof(double), w.bars + slot);
-      } else {
+      const int g = bi[j];
+      if (g >= 0) bulk_g2s(dst, a.Xc + (int64_t)g * a.ld + i0, RC * sizeof(double), w.bars + slot);
+      else
         for (int i = 0; i < RC; ++i) dst[i] = 0.0;
-      }
+    }
+    for (int j = tid; j < s; j += ENT) {
+      const int g = bi[j];
+      if (g >= 0) cp_async8(xdst + j, a.beta + g);
+      else xdst[j] = 0.0;
     }
   };
   auto wait_tile = [&](int slot) {
     mbar_wait(w.bars + slot, par[slot]);
     par[slot] ^= 1u;
   };
-  // inv rows of the slice (bulk) + c/xi/z at the block's indices (cp.async)
+  // inv rows of the slice (bulk) + c/xi/z at the block's indices (cp.async); commits the group
   auto issue_solve = [&](int b) {
-    const int32_t* bi = a.idx + (int64_t)b * s;
+    const int* bi = bidx(b);
     const double* Ib = a.inv + (int64_t)b * s * s + (int64_t)j0 * s;
     const int rows = j1 - j0;
     if (bulk_inv) {
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
       for (int e = tid; e < rows * s; e += ENT) cp_async8(w.ginv + e, Ib + e);
     }
     for (int j = tid; j < s; j += ENT) {
-      const int g = __ldg(bi + j);
+      const int g = bi[j];
       if (g >= 0) {
         cp_async8(w.cxz + j, a.c + g);
         cp_async8(w.cxz + s + j, a.xi + g);
@@ -179,8 +187,8 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     cp_async_wait<0>();
   };
   // one row phase: optional r-update with slot sp (delta in sDel) and optional
-  // partial for slot sn (x values in sX) -> sPart.  Layout T[j][i], lanes = rows.
-  auto row_phase_res = [&](int sp, int sn) {
+  // partial for slot sn (x values in xs) -> sPart.  Layout T[j][i], lanes = rows.
+  auto row_phase_res = [&](int sp, int sn, const double* xs) {
     double acc[RES_QMAX];
 #pragma unroll
     for (int c = 0; c < RES_QMAX; ++c) acc[c] = 0.0;
@@ -204,7 +212,7 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
       if (sn >= 0) {
         const double* T = tile(sn, k);
         double u = 0.0;
-        for (int j = warp; j < s; j += nw) u += T[j * RC + lane] * w.sX[j];
+        for (int j = warp; j < s; j += nw) u += T[j * RC + lane] * xs[j];
         w.red[warp * RC + lane] = u;
         __syncthreads();
         if (tid < RC) {
@@ -232,13 +240,6 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
       }
     }
   };
-  auto load_beta = [&](int b) {
-    const int32_t* bi = a.idx + (int64_t)b * s;
-    for (int j = tid; j < s; j += ENT) {
-      const int g = bi[j];
-      w.sX[j] = (g >= 0) ? ldcg(a.beta + g) : 0.0;
-    }
-  };
 
   double my_sum = 0.0, my_max = 0.0;
   auto commit = [&]() {
@@ -257,21 +258,26 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
       my_max = fmax(my_max, fabs(sub(zn, zo)));
     }
   };
-  const int G = max(1, ENT / s);  // threads per rhs entry
+  // rhs reduction over the C cluster partials: G threads per entry, each
+  // summing a contiguous run of partials with RES_BATCH loads in flight
+  const int G = max(1, min(ENT / s, 2 * ENT / s));
+  const int per = (C + G - 1) / G;
 
-  // ---- prologue: tiles of blocks 0 and 1, solve data of block 0
-  issue_tile(0, blk(0));
-  if (a.p > 1) issue_tile(1, blk(1));
+  // ---- prologue: tiles (+ beta) of blocks 0 and 1, solve data of block 0
+  issue_tile(0, blk(0), w.sX);
+  cp_async_commit();
+  if (a.p > 1) issue_tile(1, blk(1), w.sX + s);
   issue_solve(blk(0));
-  load_beta(blk(0));
   wait_tile(0);
+  cp_async_wait<1>();   // beta of block 0
   __syncthreads();
-  row_phase_res(-1, 0);
+  row_phase_res(-1, 0, w.sX);
   if (tr) a.trace[tp++] = gtimer();
 
   for (int t = 0; t < a.p; ++t) {
     const int b = blk(t);
-    const int32_t* bi = a.idx + (int64_t)b * s;
+    const int* bi = bidx(b);
+    const double* xb = w.sX + (t & 1) * s;         // beta of block t
     // ---- cluster pre-reduction, grid barrier
     cl.sync();
     if (tr) a.trace[tp++] = gtimer();
@@ -285,12 +291,20 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     grid_barrier(a.bar, target, P);
     if (tr) a.trace[tp++] = gtimer();
     if (t > 0) commit();
-    // ---- full rhs: G threads per entry, all loads in flight together
+    // ---- full rhs: G threads per entry, batched independent loads
     {
       const int j = tid / G, g = tid - j * G;
       double acc = 0.0;
-      if (j < s)
-        for (int q = g; q < C; q += G) acc += ldcg(gpart + (int64_t)q * s + j);
+      if (j < s) {
+        const int q0 = g * per, q1 = min(C, q0 + per);
+        for (int q = q0; q < q1; q += RES_BATCH) {
+          double v[RES_BATCH];
+#pragma unroll
+          for (int u = 0; u < RES_BATCH; ++u) v[u] = (q + u < q1) ? ldcg(gpart + (int64_t)(q + u) * s + j) : 0.0;
+#pragma unroll
+          for (int u = 0; u < RES_BATCH; ++u) acc += v[u];
+        }
+      }
       w.red[tid] = acc;
     }
     wait_solve();
@@ -307,38 +321,47 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     }
     __syncthreads();
     if (tr) a.trace[tp++] = gtimer();
-    // ---- delta rows of this rank's slice (old beta of the block is in sX)
-    for (int i = j0 + warp; i < j1; i += nw) {
-      const double* row = w.ginv + (int64_t)(i - j0) * s;
-      double acc = 0.0;
-      for (int j = lane; j < s; j += 32) acc += row[j] * w.sRhs[j];
-      acc = warp_sum(acc);
-      if (lane == 0) {
-        const int g = bi[i];
-        w.sSlice[i] = (g >= 0) ? acc - w.sX[i] : 0.0;
-        w.pend[i - j0] = g;
-        w.sSlice[s + (i - j0)] = acc;
+    // ---- delta rows of this rank's slice: 4 lanes-groups of 8 per row
+    {
+      const int rows = j1 - j0;
+      const int sub8 = lane >> 3, l8 = lane & 7;      // 4 rows per warp, 8 lanes per row
+      for (int r0 = warp * 4; r0 < rows; r0 += nw * 4) {
+        const int i = j0 + r0 + sub8;
+        double acc = 0.0;
+        if (r0 + sub8 < rows) {
+          const double* row = w.ginv + (int64_t)(i - j0) * s;
+          for (int j = l8; j < s; j += 8) acc += row[j] * w.sRhs[j];
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if (l8 == 0 && r0 + sub8 < rows) {
+          const int g = bi[i];
+          w.sSlice[i] = (g >= 0) ? acc - xb[i] : 0.0;
+          w.pend[i - j0] = g;
+          w.sSlice[s + (i - j0)] = acc;
+        }
       }
     }
     cl.sync();
     if (tr) a.trace[tp++] = gtimer();
     for (int i = tid; i < s; i += ENT) w.sDel[i] = cl.map_shared_rank(w.sSlice, i / sl)[i];
-    // ---- row phase (tile of b resident, tile of the next block prefetched)
+    // ---- row phase (tile of b resident, tile + beta of the next block prefetched)
     const bool more = t + 1 < a.p;
     if (more) {
-      load_beta(blk(t + 1));
       wait_tile((t + 1) & 1);
+      cp_async_wait<1>();   // beta of block t+1 (committed before the last solve group)
     }
     __syncthreads();
-    row_phase_res(t & 1, more ? ((t + 1) & 1) : -1);
+    row_phase_res(t & 1, more ? ((t + 1) & 1) : -1, w.sX + ((t + 1) & 1) * s);
     if (more) {
-      __syncthreads();   // every thread is done with slot t&1 and with ginv/cxz
-      if (t + 2 < a.p) issue_tile(t & 1, blk(t + 2));
+      __syncthreads();   // slot t&1, sX[t&1], ginv, cxz are dead for every thread
+      if (t + 2 < a.p) issue_tile(t & 1, blk(t + 2), w.sX + (t & 1) * s);
+      cp_async_commit();
       issue_solve(blk(t + 1));
     }
     if (tr) a.trace[tp++] = gtimer();
   }
-  // write back resident r
   for (int k = 0; k < nchv; ++k) {
     const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
     for (int i = tid; i < RC; i += ENT)

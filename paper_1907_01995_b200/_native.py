@@ -55,6 +55,8 @@ SIGNATURES = {
     "rac_qp_progress": (_i32, [_p, _pi32, _pi32, _pi32]),
     "rac_qp_get": (_i32, [_p, _p, _p, _p, _p]),
     "rac_qp_history": (_i32, [_p, _p, _p, _p, _i32]),
+    "rac_qp_set_trace": (_i32, [_p, _i32]),
+    "rac_qp_trace": (_i32, [_p, C.POINTER(C.c_int64), _i32]),
     "rac_qp_destroy": (_i32, [_p]),
     "rac_svm_build_q": (_i32, [_p, _i64, _i64, _p, _i32, _f64, _p, _p]),
     "rac_gemv": (_i32, [_p, _i64, _i64, _p, _p, _p]),

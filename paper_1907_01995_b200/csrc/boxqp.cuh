@@ -3,12 +3,20 @@
 //   minimize 1/2 x'Mx - r'x  over lo <= x <= hi     (M SPD, s x s, row-major)
 //
 // Same finite active-set procedure as the reference: solve unconstrained;
-// if outside the box clamp, then repeatedly re-solve on the free set and
+// if outside the box clamp, then repeatedly re-solve on the free set F and
 // clamp violators (the active set only grows within a pass), then release the
 // single worst wrong-sign multiplier; budget 10*s passes, then projected
-// gradient to 1e-10 (engine.py:175-186).  Reduced systems M_FF are factored
-// in shared memory (or a global scratch for large s) by the whole CTA; the
-// triangular solves run warp-synchronously on warp 0.
+// gradient to 1e-10 (engine.py:175-186).
+//
+// The reduced systems  M_FF x_F = r_F - M_FB x_B  are solved exactly in one of
+// two ways:
+//   Schur (well-conditioned M, |B| <= |F|): with N = M^{-1} precomputed for the
+//     block,  M_FF^{-1} = N_FF - N_FB N_BB^{-1} N_BF,  so only the small
+//     |B| x |B| system N_BB is factored;
+//   direct (otherwise): Cholesky of M_FF, as the reference does.
+// Both are exact minimizers of the same strictly convex subproblem, so the
+// iterates agree to rounding.  Factorizations run CTA-wide with one barrier
+// per column; triangular solves run on warp 0 with reciprocal pivots.
 #pragma once
 
 #include "rac_common.cuh"
@@ -20,66 +28,133 @@ struct BoxWork {
   int* flag;   // 0 free, 1 at lower, 2 at upper
   int* F;      // free list
   int* B;      // bound list
-  double* L;   // s x s (ld = s) factor workspace
+  double* L;   // factor workspace (capacity lcap doubles)
+  int lcap;
+  const double* N;  // M^{-1} (ld = s) or nullptr
+  int ldn;
   int* misc;   // [0] nf, [1] nb, [2] fail, [3] worst, [4..36) per-warp argmax scratch
   double* red; // >= nwarps
+  double* rinv;  // s: reciprocal pivots of the current factor
+  long long* dbg;  // optional counters: [reduced solves, passes, ns in solves, ns total]
 };
 
-__device__ __forceinline__ bool isbounded_lo(double v) { return v > -INFINITY; }
-
 // Cholesky of the leading n x n of L (row-major, ld) in place, lower; CTA-wide.
-// Returns 0 or k+1 on a non-positive pivot.  misc[2] is used as the flag.
-__device__ int cta_cholesky(double* L, int ld, int n, int* flag) {
+// One barrier per column: step k reads the pivot d = a_kk and the UNSCALED
+// column k, applies a_ij -= a_ik a_jk / d to the trailing triangle, and scales
+// column k-1 (nobody reads it any more) in the same phase.  Returns 0 or k+1.
+// rinv[k] = 1 / L_kk on success.
+__device__ int cta_cholesky(double* L, int ld, int n, double* rinv) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int tx = tid & 31, ty = tid >> 5, nty = nt >> 5;
-  if (tid == 0) *flag = 0;
   __syncthreads();
   for (int k = 0; k < n; ++k) {
-    if (tid == 0) {
-      double d = L[k * ld + k];
-      if (!(d > 0.0) || !isfinite(d)) *flag = k + 1;
-      else L[k * ld + k] = sqrt(d);
+    const double d = L[k * ld + k];
+    if (!(d > 0.0) || !isfinite(d)) {
+      __syncthreads();
+      return k + 1;   // uniform: every thread read the same pivot
     }
-    __syncthreads();
-    if (*flag) return *flag;
-    const double piv = L[k * ld + k];
-    for (int i = k + 1 + tid; i < n; i += nt) L[i * ld + k] /= piv;
-    __syncthreads();
+    // one reciprocal square root per pivot (no FP64 divide / sqrt on the chain)
+    const double rs = rsqrt(d);
+    const double dinv = rs * rs;
+    if (k > 0) {
+      const double rp = rinv[k - 1];
+      for (int i = k + tid; i < n; i += nt) L[i * ld + (k - 1)] *= rp;
+      if (tid == 0) {
+        const double dp = L[(k - 1) * ld + (k - 1)];
+        L[(k - 1) * ld + (k - 1)] = dp * rp;   // d_{k-1} -> L_{k-1,k-1} = sqrt(d_{k-1})
+      }
+    }
     for (int i = k + 1 + ty; i < n; i += nty) {
-      const double lik = L[i * ld + k];
+      const double lik = L[i * ld + k] * dinv;
       for (int j = k + 1 + tx; j <= i; j += 32) L[i * ld + j] -= lik * L[j * ld + k];
     }
+    if (tid == 0) rinv[k] = rs;
     __syncthreads();
   }
+  if (n > 0 && tid == 0) L[(n - 1) * ld + (n - 1)] *= rinv[n - 1];
+  __syncthreads();
   return 0;
 }
 
-// Warp 0: solve L L' v = b in place (b -> v), L lower n x n.  Others idle.
-__device__ void warp_chol_solve(const double* L, int ld, int n, double* v) {
+// Warp 0: solve L L' v = b in place (b -> v), L lower n x n (ld), rinv = 1/L_kk.
+// The right-hand side lives in registers (lane l owns rows l, l+32, ...).
+template <int MAXQ = 8>
+__device__ void warp_chol_solve(const double* L, int ld, int n, double* v, const double* rinv) {
   if (threadIdx.x >= 32) return;
   const int lane = threadIdx.x;
+  double reg[MAXQ];
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) {
+    const int i = lane + 32 * q;
+    reg[q] = (i < n) ? v[i] : 0.0;
+  }
   // forward: L y = b
   for (int k = 0; k < n; ++k) {
+    const int ow = k & 31, oq = k >> 5;
     double yk = 0.0;
-    if (lane == 0) {
-      yk = v[k] / L[k * ld + k];
-      v[k] = yk;
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q)
+      if (q == oq) yk = reg[q] * rinv[k];
+    yk = __shfl_sync(0xffffffffu, yk, ow);
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) {
+      const int i = lane + 32 * q;
+      if (i == k) reg[q] = yk;
+      else if (i > k && i < n) reg[q] -= L[i * ld + k] * yk;
     }
-    yk = __shfl_sync(0xffffffffu, yk, 0);
-    for (int i = k + 1 + lane; i < n; i += 32) v[i] -= L[i * ld + k] * yk;
-    __syncwarp();
   }
   // backward: L' x = y
   for (int k = n - 1; k >= 0; --k) {
+    const int ow = k & 31, oq = k >> 5;
+    double xk = 0.0;
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q)
+      if (q == oq) xk = reg[q] * rinv[k];
+    xk = __shfl_sync(0xffffffffu, xk, ow);
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) {
+      const int i = lane + 32 * q;
+      if (i == k) reg[q] = xk;
+      else if (i < k) reg[q] -= L[k * ld + i] * xk;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) {
+    const int i = lane + 32 * q;
+    if (i < n) v[i] = reg[q];
+  }
+  __syncwarp();
+}
+
+// Warp 0 slow path for n > 256 (L in any memory): scalar substitution.
+__device__ void warp_chol_solve_any(const double* L, int ld, int n, double* v) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  for (int k = 0; k < n; ++k) {
+    double yk = 0.0;
+    if (lane == 0) {
+      yk = v[k] / L[(int64_t)k * ld + k];
+      v[k] = yk;
+    }
+    yk = __shfl_sync(0xffffffffu, yk, 0);
+    for (int i = k + 1 + lane; i < n; i += 32) v[i] -= L[(int64_t)i * ld + k] * yk;
+    __syncwarp();
+  }
+  for (int k = n - 1; k >= 0; --k) {
     double xk = 0.0;
     if (lane == 0) {
-      xk = v[k] / L[k * ld + k];
+      xk = v[k] / L[(int64_t)k * ld + k];
       v[k] = xk;
     }
     xk = __shfl_sync(0xffffffffu, xk, 0);
-    for (int i = lane; i < k; i += 32) v[i] -= L[k * ld + i] * xk;
+    for (int i = lane; i < k; i += 32) v[i] -= L[(int64_t)k * ld + i] * xk;
     __syncwarp();
   }
+}
+
+__device__ __forceinline__ void chol_solve(const double* L, int ld, int n, double* v, const double* rinv) {
+  if (n <= 256 && rinv) warp_chol_solve<8>(L, ld, n, v, rinv);
+  else warp_chol_solve_any(L, ld, n, v);
 }
 
 // out = M v (rows x s of row-major M, ld), warp per row.
@@ -134,14 +209,11 @@ __device__ void cta_lists(BoxWork& w, int s) {
 }
 
 // Solve M_FF xf = r_F - M_FB x_B on the current free set; result in w.xf[0..nf).
-// Returns fail code (k+1) if M_FF is not PD.
-__device__ int solve_free(const double* M, int ldm, BoxWork& w) {
+// Returns fail code (k+1) if the reduced matrix is not PD.
+__device__ int solve_free(const double* M, int ldm, BoxWork& w, bool use_schur) {
   const int nf = w.misc[0], nb = w.misc[1];
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  for (int e = tid; e < nf * nf; e += nt) {
-    int a = e / nf, b = e - a * nf;
-    if (b <= a) w.L[a * nf + b] = M[(int64_t)w.F[a] * ldm + w.F[b]];
-  }
+  // q = r_F - M_FB x_B
   for (int a = warp; a < nf; a += nw) {
     const double* row = M + (int64_t)w.F[a] * ldm;
     double acc = 0.0;
@@ -150,9 +222,66 @@ __device__ int solve_free(const double* M, int ldm, BoxWork& w) {
     if (lane == 0) w.xf[a] = (nb > 0) ? w.r[w.F[a]] - acc : w.r[w.F[a]];
   }
   __syncthreads();
-  int fail = cta_cholesky(w.L, nf, nf, &w.misc[2]);
+  const int ldk = nb | 1;
+  if (use_schur && w.N && nb <= nf && (size_t)ldk * nb <= (size_t)w.lcap) {
+    const double* N = w.N;
+    const int ldn = w.ldn;
+    if (nb > 0) {
+      // u = N_BF q ; N_BB (lower) into the workspace
+      for (int c = warp; c < nb; c += nw) {
+        const double* row = N + (int64_t)w.B[c] * ldn;
+        double acc = 0.0;
+        for (int a2 = lane; a2 < nf; a2 += 32) acc += row[w.F[a2]] * w.xf[a2];
+        acc = warp_sum(acc);
+        if (lane == 0) w.rr[c] = acc;
+      }
+      for (int e = tid; e < nb * nb; e += nt) {
+        const int c1 = e / nb, c2 = e - c1 * nb;
+        if (c2 <= c1) w.L[c1 * ldk + c2] = N[(int64_t)w.B[c1] * ldn + w.B[c2]];
+      }
+      const int fail = cta_cholesky(w.L, ldk, nb, w.rinv);
+      if (!fail) {
+        chol_solve(w.L, ldk, nb, w.rr, w.rinv);   // rr <- N_BB^{-1} N_BF q
+        __syncthreads();
+        // x_F = N_FF q - N_FB (N_BB^{-1} N_BF q)
+        for (int a2 = warp; a2 < nf; a2 += nw) {
+          const double* row = N + (int64_t)w.F[a2] * ldn;
+          double acc = 0.0;
+          for (int j = lane; j < nf; j += 32) acc += row[w.F[j]] * w.xf[j];
+          for (int c = lane; c < nb; c += 32) acc -= row[w.B[c]] * w.rr[c];
+          acc = warp_sum(acc);
+          if (lane == 0) w.grad[a2] = acc;
+        }
+        __syncthreads();
+        for (int a2 = tid; a2 < nf; a2 += nt) w.xf[a2] = w.grad[a2];
+        __syncthreads();
+        return 0;
+      }
+      // numerically indefinite N_BB: fall through to the direct factorization
+    } else {
+      for (int a2 = warp; a2 < nf; a2 += nw) {
+        const double* row = N + (int64_t)w.F[a2] * ldn;
+        double acc = 0.0;
+        for (int j = lane; j < nf; j += 32) acc += row[w.F[j]] * w.xf[j];
+        acc = warp_sum(acc);
+        if (lane == 0) w.grad[a2] = acc;
+      }
+      __syncthreads();
+      for (int a2 = tid; a2 < nf; a2 += nt) w.xf[a2] = w.grad[a2];
+      __syncthreads();
+      return 0;
+    }
+  }
+  // direct: Cholesky of M_FF (the reference's route)
+  const int ldf = nf | 1;
+  if ((size_t)ldf * nf > (size_t)w.lcap) return nf + 1;   // workspace too small (never for SPD M)
+  for (int e = tid; e < nf * nf; e += nt) {
+    const int a1 = e / nf, b1 = e - a1 * nf;
+    if (b1 <= a1) w.L[a1 * ldf + b1] = M[(int64_t)w.F[a1] * ldm + w.F[b1]];
+  }
+  const int fail = cta_cholesky(w.L, ldf, nf, w.rinv);
   if (fail) return fail;
-  warp_chol_solve(w.L, nf, nf, w.xf);
+  chol_solve(w.L, ldf, nf, w.xf, w.rinv);
   __syncthreads();
   return 0;
 }
@@ -161,7 +290,6 @@ __device__ int solve_free(const double* M, int ldm, BoxWork& w) {
 // eigenvalue of M estimated by power iteration (the reference uses eigvalsh).
 __device__ void projected_gradient(const double* M, int ldm, int s, BoxWork& w) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  // power iteration: xf <- M xf / |M xf|
   for (int i = tid; i < s; i += nt) w.xf[i] = 1.0;
   __syncthreads();
   double lam = 1.0;
@@ -196,7 +324,7 @@ __device__ void projected_gradient(const double* M, int ldm, int s, BoxWork& w) 
 
 // Entry: w.x holds the unconstrained solution M^{-1} r on input.  Returns 0 or
 // the fail code of a non-PD reduced system.
-__device__ int box_active_set(const double* M, int ldm, int s, BoxWork& w) {
+__device__ int box_active_set(const double* M, int ldm, int s, BoxWork& w, bool use_schur) {
   const int tid = threadIdx.x, nt = blockDim.x;
   int bnd = 0, out = 0;
   for (int i = tid; i < s; i += nt) {
@@ -223,7 +351,9 @@ __device__ int box_active_set(const double* M, int ldm, int s, BoxWork& w) {
       cta_lists(w, s);
       const int nf = w.misc[0];
       if (nf == 0) break;
-      int fail = solve_free(M, ldm, w);
+      long long t_s = (w.dbg && threadIdx.x == 0) ? gtimer() : 0;
+      int fail = solve_free(M, ldm, w, use_schur);
+      if (w.dbg && threadIdx.x == 0) { w.dbg[0] += 1; w.dbg[2] += gtimer() - t_s; }
       if (fail) return fail;
       int viol = 0;
       for (int a = tid; a < nf; a += nt) {
@@ -236,6 +366,7 @@ __device__ int box_active_set(const double* M, int ldm, int s, BoxWork& w) {
       viol = __syncthreads_or(viol);
       if (!viol) break;
     }
+    if (w.dbg && threadIdx.x == 0) w.dbg[1] += 1;
     // multipliers: grad = M x - r
     cta_matvec(M, ldm, s, s, w.x, w.grad);
     __syncthreads();
@@ -254,7 +385,6 @@ __device__ int box_active_set(const double* M, int ldm, int s, BoxWork& w) {
       else if (w.flag[i] == 2 && w.grad[i] > 1e-14 * scale) sc = w.grad[i];
       if (sc > best) { best = sc; bi = i; }
     }
-    // reduce (best, bi): max best, then min index
     const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
     for (int o = 16; o > 0; o >>= 1) {
       double ob = __shfl_xor_sync(0xffffffffu, best, o);

@@ -53,11 +53,6 @@ struct EnChainArgs {
   long long* trace;     // optional: %globaltimer at every phase boundary (CTA 0)
 };
 
-__device__ __forceinline__ long long gtimer() {
-  long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 template <int RC>
 __global__ void __launch_bounds__(ENT) en_chain_kernel(EnChainArgs a) {

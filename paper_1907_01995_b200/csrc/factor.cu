@@ -356,6 +356,28 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
       const int i = e / s, j = e - i * s;
       out[e] = (j <= i) ? A[(int64_t)i * ld + j] : 0.0;
     }
+    if (a.cond_out) {
+      // pivot-ratio estimate of cond(sys): (max L_ii / min L_ii)^2
+      double mx = 0.0, mn = INFINITY;
+      for (int i = tid; i < s; i += CTHREADS) {
+        const double d = A[(int64_t)i * ld + i];
+        mx = fmax(mx, d);
+        mn = fmin(mn, d);
+      }
+      mx = warp_max(mx);
+      mn = -warp_max(-mn);
+      __shared__ double redmin[CTHREADS / 32];
+      if ((tid & 31) == 0) { red[tid >> 5] = mx; redmin[tid >> 5] = mn; }
+      __syncthreads();
+      if (tid == 0) {
+        double M1 = red[0], m1 = redmin[0];
+        for (int w = 1; w < CTHREADS / 32; ++w) { M1 = fmax(M1, red[w]); m1 = fmin(m1, redmin[w]); }
+        a.cond_out[b] = (M1 / m1) * (M1 / m1);
+      }
+      __syncthreads();
+    }
+    if (!a.inv2) return;
+    cta_chol_inverse(A, ld, s, dY, a.inv2 + (int64_t)b * s * s);
     return;
   }
   cta_chol_inverse(A, ld, s, dY, out);

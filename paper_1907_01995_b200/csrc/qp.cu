@@ -20,6 +20,7 @@
 // The SVM is the instance H = Q, A = y', b = 0, c = -1, box [0, C], with the
 // 1e-9 relative ridge of svm.py:242-246.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "boxqp.cuh"
@@ -29,7 +30,7 @@
 namespace rac {
 
 constexpr int QPT = RP_THREADS;  // 256 threads per chain CTA
-constexpr int QCOLS = 256;       // column tile of the strip update
+constexpr int QCOLS = 128;       // column tile of the strip update
 
 struct QpChainArgs {
   int64_t n, m, lda;
@@ -45,6 +46,10 @@ struct QpChainArgs {
   double *partial, *delta;
   double *pmax, *psum, *dmax;  // per CTA
   double* lscratch;            // s x s global factor scratch (large s)
+  double* hbx;                 // [s] H_bb x_b of the next block (computed in the G phase)
+  const double* Ninv;          // [p][s][s] block inverses M_b^{-1}
+  const double* cond;          // [p] pivot-ratio condition estimate of M_b
+  long long* trace;            // optional %globaltimer stamps (CTA 0): per block [S start, S end, G start, G end]
   unsigned* bar;
   int32_t* ctrl;  // [0] done, [1] iterations, [2] failed block+1, [3] status
   double beta, tol_p, tol_d, div_bar;
@@ -63,16 +68,26 @@ __device__ void strip_update(const QpChainArgs& a, const int32_t* sIdx, const do
     double acc[QCOLS / 32];
 #pragma unroll
     for (int q = 0; q < QCOLS / 32; ++q) acc[q] = 0.0;
-    for (int i = warp; i < s; i += nw) {
-      const int g = sIdx[i];
-      if (g < 0) continue;
-      const double d = sDel[i];
-      const double* row = a.H + (int64_t)g * a.n;
+    // rows in batches of 4: 4 x (QCOLS/32) independent loads in flight per lane
+    for (int i0 = warp; i0 < s; i0 += 4 * nw) {
+      double v[4][QCOLS / 32];
+      double dd[4];
 #pragma unroll
-      for (int q = 0; q < QCOLS / 32; ++q) {
-        int64_t j = t0 + q * 32 + lane;
-        if (j < c1) acc[q] += __ldg(row + j) * d;
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * nw;
+        const int g = (i < s) ? sIdx[i] : -1;
+        dd[u] = (g >= 0) ? sDel[i] : 0.0;
+        const double* row = a.H + (int64_t)(g >= 0 ? g : 0) * a.n;
+#pragma unroll
+        for (int q = 0; q < QCOLS / 32; ++q) {
+          const int64_t j = t0 + q * 32 + lane;
+          v[u][q] = (g >= 0 && j < c1) ? __ldg(row + j) : 0.0;
+        }
       }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < QCOLS / 32; ++q) acc[q] += v[u][q] * dd[u];
     }
 #pragma unroll
     for (int q = 0; q < QCOLS / 32; ++q) red[warp * QCOLS + q * 32 + lane] = acc[q];
@@ -96,15 +111,21 @@ struct QpSmem {
   int32_t* sIdx;   // s
   double* sDel;    // s
   double *sxb, *shx, *sc;
+  double* sM;      // s x s block matrix M_b (smem-resident when lsmem)
+  double* sN;      // s x s M_b^{-1} (smem-resident when lsmem)
+  double* Lsmall;  // small factor workspace ((s/2+1)^2) for the Schur / small direct solves
+  uint64_t* bar;   // mbarrier of the M_b / N_b prefetch
 };
+
+__host__ __device__ inline size_t qp_lsmall(int s) { return (size_t)(s / 2 + 2) * (s / 2 + 2); }
 
 template <int RC>
 __host__ __device__ size_t qp_smem_bytes(int s, bool rowphase, bool lsmem) {
   size_t d = 0;
   if (rowphase) d += RowPhase<RC>::smem_doubles(s) + s;  // + int idx (as doubles, generous)
   d += (QPT / 32) * QCOLS;                               // strip reduction
-  d += 10 * (size_t)s + 64;                              // box vectors + sDel, sxb, shx, sc
-  if (lsmem) d += (size_t)s * s;                         // factor workspace
+  d += 11 * (size_t)s + 64;                              // box vectors, rinv, sDel, sxb, shx, sc
+  if (lsmem) d += 2 * (size_t)s * s + qp_lsmall(s) + 3;  // M_b, N_b, small workspace, mbarrier, align
   size_t ints = 4 * (size_t)s + 64;                      // flag, F, B, sIdx, misc
   return d * sizeof(double) + ints * sizeof(int);
 }
@@ -131,11 +152,27 @@ __device__ QpSmem carve_qp(double* base, int s, bool rowphase, bool lsmem, doubl
   q.shx = p; p += s;
   q.bw.red = p; p += 32;
   q.sc = p; p += 32;  // scalars
+  q.bw.rinv = p; p += s;
+  q.bw.dbg = nullptr;
+  q.bw.N = nullptr;
+  q.bw.ldn = s;
+  q.bw.L = lscratch;                       // large workspace (global): s(s+1) doubles
+  q.bw.lcap = s * (s + 1);
   if (lsmem) {
-    q.bw.L = p;
+    p += (p - base) & 1;   // 16-byte alignment for the TMA destinations
+    q.sM = p;
     p += (size_t)s * s;
+    q.sN = p;
+    p += (size_t)s * s;
+    q.Lsmall = p;
+    p += qp_lsmall(s);
+    q.bar = reinterpret_cast<uint64_t*>(p);
+    p += 2;
   } else {
-    q.bw.L = lscratch;
+    q.sM = nullptr;
+    q.sN = nullptr;
+    q.Lsmall = nullptr;
+    q.bar = nullptr;
   }
   int* ip = (int*)p;
   q.bw.flag = ip; ip += s;
@@ -174,70 +211,183 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
   auto tfn = [&](int64_t r, double ax_r, double u) {
     return ldcg(a.y + r) - beta * ((ax_r - u) - a.b[r]);
   };
+  // CTA 0 keeps M_b and the Cholesky factor L_b of the block it solves in
+  // shared memory; the next block's pair is fetched by TMA bulk copies while
+  // every CTA runs the G phase.
+  unsigned mpar = 0u;
+  const bool bulkML = (w.sM != nullptr) && ((s * s) % 2 == 0);
+  if (blockIdx.x == 0 && w.sM && tid == 0) {
+    mbar_init(w.bar, 1);
+    mbar_fence_init();
+  }
+  auto prefetch_ML = [&](int b) {
+    if (blockIdx.x != 0 || !w.sM) return;
+    const double* Mg = a.Mb + (int64_t)b * s * s;
+    const double* Ng = a.Ninv + (int64_t)b * s * s;
+    __syncthreads();
+    if (bulkML) {
+      if (tid == 0) {
+        fence_proxy_async();
+        const unsigned bytes = (unsigned)(s * s * sizeof(double));
+        mbar_arrive_expect_tx(w.bar, 2 * bytes);
+        for (unsigned off = 0; off < bytes; off += 32768u) {
+          const unsigned len = min(32768u, bytes - off);
+          bulk_g2s(w.sM + off / 8, Mg + off / 8, len, w.bar);
+          bulk_g2s(w.sN + off / 8, Ng + off / 8, len, w.bar);
+        }
+      }
+    } else {
+      for (int e = tid; e < s * s; e += QPT) {
+        cp_async8(w.sM + e, Mg + e);
+        cp_async8(w.sN + e, Ng + e);
+      }
+      cp_async_commit();
+    }
+  };
+  auto wait_ML = [&]() {
+    if (bulkML) {
+      mbar_wait(w.bar, mpar);
+      mpar ^= 1u;
+    } else if (w.sM) {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+  };
+  // hbx = H_bb x_b for block b (rows spread over all warps of the grid)
+  // Strip staging: while CTA 0 solves block b, every other CTA bulk-copies
+  // its column slice of the block's H rows into its (otherwise unused)
+  // M/N shared-memory region, so the G phase is pure shared-memory math.
+  const int64_t sper = (a.n + (P - 2)) / max(1, P - 1);
+  const int64_t sper2 = (sper + 1) & ~1LL;                      // even: 16-byte row segments
+  const bool strip_smem = a.H && w.sM && P > 1 && (sper2 * s <= 2LL * s * s + (int64_t)qp_lsmall(s)) &&
+                          (a.n % 2 == 0);
+  const int64_t sc0 = (blockIdx.x == 0) ? 0 : min64(a.n, (int64_t)(blockIdx.x - 1) * sper2);
+  const int64_t sc1 = (blockIdx.x == 0) ? 0 : min64(a.n, sc0 + sper2);
+  unsigned spar = 0u;
+  if (strip_smem && blockIdx.x != 0 && tid == 0) {
+    mbar_init(w.bar, 1);
+    mbar_fence_init();
+  }
+  auto issue_strip = [&](int b) {
+    if (!strip_smem || blockIdx.x == 0 || sc1 <= sc0) return;
+    const int32_t* bi = a.idx + (int64_t)b * s;
+    const unsigned seg = (unsigned)((sc1 - sc0) * sizeof(double));
+    int nvalid = 0;
+    for (int i = 0; i < s; ++i) nvalid += (bi[i] >= 0);   // uniform across threads
+    __syncthreads();
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(w.bar, seg * (unsigned)nvalid);
+    }
+    __syncthreads();
+    for (int i = tid; i < s; i += QPT) {
+      const int g = bi[i];
+      if (g >= 0) bulk_g2s(w.sM + (size_t)i * sper2, a.H + (int64_t)g * a.n + sc0, seg, w.bar);
+    }
+  };
+  auto strip_from_smem = [&]() {
+    if (blockIdx.x == 0 || sc1 <= sc0) return;
+    mbar_wait(w.bar, spar);
+    spar ^= 1u;
+    __syncthreads();
+    const int W = (int)(sc1 - sc0);
+    for (int jj = tid; jj < W; jj += QPT) {
+      double acc = 0.0;
+      for (int i = 0; i < s; ++i)
+        if (w.sIdx[i] >= 0) acc += w.sM[(size_t)i * sper2 + jj] * w.sDel[i];
+      a.hx[sc0 + jj] += acc;
+    }
+    __syncthreads();
+  };
+  auto compute_hbx = [&](int b) {
+    if (!a.H) return;
+    const int32_t* bi = a.idx + (int64_t)b * s;
+    const double* Hb = a.Hbb + (int64_t)b * s * s;
+    for (int i = blockIdx.x * nw + warp; i < s; i += P * nw) {
+      double acc = 0.0;
+      for (int j = lane; j < s; j += 32) {
+        const int g = bi[j];
+        if (g >= 0) acc += Hb[(int64_t)i * s + j] * ldcg(a.x + g);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) a.hbx[i] = acc;
+    }
+  };
   int bnext = a.order ? a.order[0] : 0;
+  prefetch_ML(bnext);
+  compute_hbx(bnext);
   if (has_a)
     row_phase<RC>(a.Ac, a.lda, a.m, a.nrc, a.idx, s, -1, bnext, a.delta, a.x, a.ax, a.partial, w.rp, tfn);
+  const bool tr = a.trace && blockIdx.x == 0 && tid == 0;
   for (int t = 0; t < a.p; ++t) {
     const int b = bnext;
     grid_barrier(a.bar, target, P);
+    if (tr) a.trace[4 * t + 0] = gtimer();
+    issue_strip(b);
     // ------------------------------------------------------------ S (CTA 0)
     if (blockIdx.x == 0) {
       const int32_t* bidx = a.idx + (int64_t)b * s;
-      for (int i = tid; i < s; i += QPT) {
-        int g = bidx[i];
-        w.sIdx[i] = g;
-        if (g >= 0) {
-          w.sxb[i] = ldcg(a.x + g);
-          w.shx[i] = ldcg(a.hx + g);
-          w.bw.lo[i] = a.lo[g];
-          w.bw.hi[i] = a.hi[g];
-        }
-      }
-      int seff;
+      // one parallel gather pass (all loads independent), then the rhs
+      // (engine.py:126-132):  -c_b - (hx_b - H_bb x_b) + A_b'(y - beta(Ax_rest - b))
+      const int Pa = min(P, a.nrc);   // CTAs that own constraint rows (others' partials are 0)
       if (tid == 0) {
         int k = 0;
         while (k < s && bidx[k] >= 0) ++k;
         w.bw.misc[0] = k;
       }
-      __syncthreads();
-      seff = w.bw.misc[0];
-      // (A_b' t) from the per-CTA partials, then H_bb x_b
-      const double* Hb = a.Hbb + (int64_t)b * s * s;
-      for (int i = warp; i < seff; i += nw) {
-        double pa = 0.0;
-        if (has_a) {
-          for (int q = lane; q < P; q += 32) pa += ldcg(a.partial + (int64_t)q * s + i);
-          pa = warp_sum(pa);
-        }
-        double hb = 0.0;
-        if (a.H) {
-          const double* row = Hb + (int64_t)i * s;
-          for (int j = lane; j < seff; j += 32) hb += row[j] * w.sxb[j];
-          hb = warp_sum(hb);
-        }
-        if (lane == 0) {
-          const int g = w.sIdx[i];
-          double rhs = -a.c[g];
-          if (a.H) rhs = rhs - (w.shx[i] - hb);
+      for (int i = tid; i < s; i += QPT) {
+        const int g = bidx[i];
+        w.sIdx[i] = g;
+        if (g >= 0) {
+          const double xg = ldcg(a.x + g), hxg = ldcg(a.hx + g), cg_ = a.c[g];
+          const double lo = a.lo[g], hi = a.hi[g];
+          const double hb = a.H ? ldcg(a.hbx + i) : 0.0;
+          double pa = 0.0;
+          if (has_a)
+            for (int q = 0; q < Pa; ++q) pa += ldcg(a.partial + (int64_t)q * s + i);
+          w.sxb[i] = xg;
+          w.shx[i] = hxg;
+          w.bw.lo[i] = lo;
+          w.bw.hi[i] = hi;
+          double rhs = -cg_;
+          if (a.H) rhs = rhs - (hxg - hb);
           if (has_a) rhs = rhs + pa;
           w.bw.r[i] = rhs;
         }
       }
       __syncthreads();
-      // unconstrained solution x = L^-T L^-1 r with the block's Cholesky factor
-      // (engine.py:201-203: cho_solve with the full-block factor)
-      {
+      const int seff = w.bw.misc[0];
+      // unconstrained solution (engine.py:201-203).  Well-conditioned blocks:
+      // x = N_b r with the smem-resident inverse, reduced systems by Schur
+      // complements of N_b.  Otherwise: cho_solve with the block's Cholesky
+      // factor and direct reduced factorizations, exactly as the reference.
+      const bool schur = (w.sM != nullptr) && (ldcg(a.cond + b) < 1e6);
+      const double* Mblk;
+      if (w.sM) wait_ML();   // M_b, N_b resident (ld = s)
+      if (schur) {
+        cta_matvec(w.sN, s, seff, seff, w.bw.r, w.bw.x);
+        w.bw.N = w.sN;
+        w.bw.ldn = s;
+        w.bw.L = w.Lsmall;
+        w.bw.lcap = (int)qp_lsmall(s);
+        Mblk = w.sM;
+      } else {
         const double* Lb = a.inv + (int64_t)b * s * s;
-        for (int e = tid; e < seff * seff; e += QPT) {
-          const int i = e / seff, j = e - i * seff;
-          w.bw.L[e] = Lb[(int64_t)i * s + j];
-        }
         for (int i = tid; i < seff; i += QPT) w.bw.x[i] = w.bw.r[i];
         __syncthreads();
-        warp_chol_solve(w.bw.L, seff, seff, w.bw.x);
-        __syncthreads();
+        warp_chol_solve_any(Lb, s, seff, w.bw.x);
+        w.bw.N = nullptr;
+        w.bw.L = a.lscratch;
+        w.bw.lcap = s * (s + 1);
+        Mblk = w.sM ? w.sM : a.Mb + (int64_t)b * s * s;
       }
-      int fail = box_active_set(a.Mb + (int64_t)b * s * s, s, seff, w.bw);
+      __syncthreads();
+      long long t_box = tr ? gtimer() : 0;
+      w.bw.dbg = a.trace ? (a.trace + 4 * a.p + 4 * t) : nullptr;
+      if (tr) { w.bw.dbg[0] = 0; w.bw.dbg[1] = 0; w.bw.dbg[2] = 0; }
+      __syncthreads();
+      int fail = box_active_set(Mblk, s, seff, w.bw, schur);
+      if (tr) w.bw.dbg[3] = gtimer() - t_box;
       if (fail) {
         if (tid == 0) { a.ctrl[2] = b + 1; a.ctrl[0] = 1; }
       }
@@ -249,19 +399,28 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
         }
         a.delta[i] = d;
       }
+      if (t + 1 < a.p) prefetch_ML(a.order ? a.order[t + 1] : t + 1);
     }
+    if (tr) a.trace[4 * t + 1] = gtimer();
     grid_barrier(a.bar, target, P);
-    if (ldcg(a.ctrl + 0)) return;  // non-PD reduced system: abort the sweep
+    if (tr) a.trace[4 * t + 2] = gtimer();
+    // non-PD reduced system: abort the sweep (one load per CTA, broadcast in smem)
+    if (tid == 0) bad = ldcg(a.ctrl + 0);
+    __syncthreads();
+    if (bad) return;
     // ------------------------------------------------------------ G (all CTAs)
     for (int i = tid; i < s; i += QPT) {
       w.sIdx[i] = a.idx[(int64_t)b * s + i];
       w.sDel[i] = ldcg(a.delta + i);
     }
     __syncthreads();
-    if (a.H) strip_update(a, w.sIdx, w.sDel, w.red, s);
+    if (strip_smem) strip_from_smem();
+    else if (a.H) strip_update(a, w.sIdx, w.sDel, w.red, s);
     bnext = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
+    if (bnext >= 0) compute_hbx(bnext);
     if (has_a)
       row_phase<RC>(a.Ac, a.lda, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.x, a.ax, a.partial, w.rp, tfn);
+    if (tr) a.trace[4 * t + 3] = gtimer();
   }
   grid_barrier(a.bar, target, P);
   // ------------------------------------------------------------ dual step + primal residual
@@ -359,7 +518,7 @@ __global__ void __launch_bounds__(QPT) box_test_kernel(const double* M, const do
                                                        const double* hi, int s, double* xout,
                                                        int32_t* info, double* L) {
   extern __shared__ __align__(16) double bsm[];
-  QpSmem w = carve_qp<32>(bsm, s, false, L == nullptr, L);
+  QpSmem w = carve_qp<32>(bsm, s, false, false, L);   // workspace L: global, s(s+1)
   for (int i = threadIdx.x; i < s; i += QPT) {
     w.bw.r[i] = r[i];
     w.bw.lo[i] = lo[i];
@@ -370,11 +529,11 @@ __global__ void __launch_bounds__(QPT) box_test_kernel(const double* M, const do
   cta_lists(w.bw, s);  // all free
   for (int i = threadIdx.x; i < s; i += QPT) w.bw.x[i] = 0.0;
   __syncthreads();
-  int fail = solve_free(M, s, w.bw);
+  int fail = solve_free(M, s, w.bw, false);
   if (!fail) {
     for (int i = threadIdx.x; i < s; i += QPT) w.bw.x[i] = w.bw.xf[i];
     __syncthreads();
-    fail = box_active_set(M, s, s, w.bw);
+    fail = box_active_set(M, s, s, w.bw, false);
   }
   for (int i = threadIdx.x; i < s; i += QPT) xout[i] = w.bw.x[i];
   if (threadIdx.x == 0) *info = fail;
@@ -430,10 +589,14 @@ struct rac_qp_ctx {
   double *gram_ws = nullptr, *Mb = nullptr, *Hbb = nullptr, *inv = nullptr, *scratch = nullptr;
   double *partial = nullptr, *delta = nullptr, *pmax = nullptr, *psum = nullptr, *dmax = nullptr;
   double* lscratch = nullptr;
+  double* hbx = nullptr;
+  double *Ninv = nullptr, *cond = nullptr;
   unsigned* bar = nullptr;
   int32_t* ctrl = nullptr;
   double *hist_p = nullptr, *hist_l1 = nullptr, *hist_d = nullptr;
   double div_bar = INFINITY;
+  int rc = 32;   // rows per chunk of the A row phase (8 for few constraint rows)
+  long long* trace = nullptr;   // 4 stamps per block of the last traced sweep
   std::vector<void*> allocs;
 };
 
@@ -450,9 +613,13 @@ int qalloc(rac_qp_ctx* c, T** p, size_t count) {
   return RAC_OK;
 }
 
-constexpr int kQpRC = 32;
-
-size_t qp_smem(const rac_qp_ctx* c) { return rac::qp_smem_bytes<kQpRC>(c->s, c->m > 0, c->lsmem); }
+size_t qp_smem_for(int rc, int s, bool rowphase, bool lsmem) {
+  return rc == 8 ? rac::qp_smem_bytes<8>(s, rowphase, lsmem) : rac::qp_smem_bytes<32>(s, rowphase, lsmem);
+}
+size_t qp_smem(const rac_qp_ctx* c) { return qp_smem_for(c->rc, c->s, c->m > 0, c->lsmem); }
+const void* qp_kernel(const rac_qp_ctx* c) {
+  return c->rc == 8 ? (const void*)rac::qp_chain_kernel<8> : (const void*)rac::qp_chain_kernel<32>;
+}
 
 int qp_grow_history(rac_qp_ctx* c, int need) {
   if (need <= c->hist_cap) return RAC_OK;
@@ -493,6 +660,8 @@ int qp_block_systems(rac_qp_ctx* c) {
   a.inv = c->inv;
   a.mat_out = c->Mb;
   a.hbb_out = c->Hbb;
+  a.inv2 = c->Ninv;
+  a.cond_out = c->cond;
   a.scratch = c->scratch;
   a.info = c->info;
   a.mode = FACTOR_CHOL;
@@ -544,9 +713,12 @@ int qp_chain(rac_qp_ctx* c, double tol_p, double tol_d, int fixed) {
   a.hist_p = c->hist_p;
   a.hist_l1 = c->hist_l1;
   a.hist_d = c->hist_d;
+  a.hbx = c->hbx;
+  a.trace = c->trace;
+  a.Ninv = c->Ninv;
+  a.cond = c->cond;
   void* args[] = {&a};
-  cudaError_t e = cudaLaunchCooperativeKernel((void*)qp_chain_kernel<kQpRC>, dim3(c->P), dim3(QPT), args,
-                                              qp_smem(c), c->st);
+  cudaError_t e = cudaLaunchCooperativeKernel(qp_kernel(c), dim3(c->P), dim3(QPT), args, qp_smem(c), c->st);
   return check_cuda(e, "qp_chain (cooperative launch)");
 }
 
@@ -572,9 +744,11 @@ extern "C" int rac_qp_create(rac_qp_ctx** out, int64_t n, int64_t m, int32_t blo
   c->beta = beta;
   c->ridge_rel = ridge_rel;
   c->st = (cudaStream_t)stream;
-  c->nrc = (int)((std::max<int64_t>(m, 1) + kQpRC - 1) / kQpRC);
-  c->lsmem = rac::qp_smem_bytes<kQpRC>(c->s, m > 0, true) <= 200 * 1024;
-  int rc = check_cuda(cudaFuncSetAttribute(qp_chain_kernel<kQpRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  c->rc = (m <= 256) ? 8 : 32;
+  c->nrc = (int)((std::max<int64_t>(m, 1) + c->rc - 1) / c->rc);
+  c->lsmem = qp_smem_for(c->rc, c->s, m > 0, true) <= 224 * 1024;
+  if (const char* e = getenv("RAC_QP_RESIDENT")) c->lsmem = c->lsmem && atoi(e) != 0;
+  int rc = check_cuda(cudaFuncSetAttribute(qp_kernel(c), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)qp_smem(c)),
                       "qp chain smem attribute");
   if (rc) {
@@ -582,7 +756,7 @@ extern "C" int rac_qp_create(rac_qp_ctx** out, int64_t n, int64_t m, int32_t blo
     return rc;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qp_chain_kernel<kQpRC>, QPT, qp_smem(c));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qp_kernel(c), QPT, qp_smem(c));
   if (per_sm < 1) {
     delete c;
     return set_error(RAC_ERR_UNSUPPORTED, "qp chain kernel does not fit (smem %zu)", qp_smem(c));
@@ -597,7 +771,8 @@ extern "C" int rac_qp_create(rac_qp_ctx** out, int64_t n, int64_t m, int32_t blo
       (rc = qalloc(c, &c->info, c->p)) || (rc = qalloc(c, &c->Mb, sqs)) || (rc = qalloc(c, &c->Hbb, sqs)) ||
       (rc = qalloc(c, &c->inv, sqs)) || (rc = qalloc(c, &c->partial, (size_t)c->P * c->s)) ||
       (rc = qalloc(c, &c->delta, c->s)) || (rc = qalloc(c, &c->pmax, c->P)) || (rc = qalloc(c, &c->psum, c->P)) ||
-      (rc = qalloc(c, &c->dmax, c->P)) || (rc = qalloc(c, &c->bar, 1)) || (rc = qalloc(c, &c->ctrl, 4))) {
+      (rc = qalloc(c, &c->dmax, c->P)) || (rc = qalloc(c, &c->bar, 1)) || (rc = qalloc(c, &c->ctrl, 4)) ||
+      (rc = qalloc(c, &c->hbx, c->s)) || (rc = qalloc(c, &c->Ninv, sqs)) || (rc = qalloc(c, &c->cond, c->p))) {
     rac_qp_destroy(c);
     return rc;
   }
@@ -610,7 +785,7 @@ extern "C" int rac_qp_create(rac_qp_ctx** out, int64_t n, int64_t m, int32_t blo
     rac_qp_destroy(c);
     return rc;
   }
-  if (!c->lsmem && (rc = qalloc(c, &c->lscratch, (size_t)c->s * c->s))) {
+  if ((rc = qalloc(c, &c->lscratch, (size_t)c->s * (c->s + 1)))) {
     rac_qp_destroy(c);
     return rc;
   }
@@ -772,6 +947,26 @@ extern "C" int rac_qp_history(rac_qp_ctx* c, double* primal, double* primal_l1, 
   return check_launch("rac_qp_history");
 }
 
+extern "C" int rac_qp_set_trace(rac_qp_ctx* c, int32_t enable) {
+  using namespace rac;
+  clear_error();
+  if (!c) return set_error(RAC_ERR_ARG, "rac_qp_set_trace: null context");
+  if (enable && !c->trace) {
+    int rc = qalloc(c, &c->trace, 8 * (size_t)c->p);
+    if (rc) return rc;
+  }
+  if (!enable) c->trace = nullptr;
+  return RAC_OK;
+}
+
+extern "C" int rac_qp_trace(rac_qp_ctx* c, int64_t* host, int32_t capacity) {
+  using namespace rac;
+  clear_error();
+  if (!c || !host || !c->trace) return set_error(RAC_ERR_ARG, "rac_qp_trace: tracing not enabled");
+  const int k = std::min<int>(capacity, 8 * c->p);
+  return check_cuda(cudaMemcpy(host, c->trace, k * sizeof(int64_t), cudaMemcpyDeviceToHost), "qp trace copy");
+}
+
 extern "C" int rac_qp_destroy(rac_qp_ctx* c) {
   if (!c) return RAC_OK;
   if (c->st) cudaStreamSynchronize(c->st);
@@ -820,13 +1015,12 @@ extern "C" int rac_box_block_min(const double* M, const double* r, const double*
   clear_error();
   if (!M || !r || !lo || !hi || !x || !info || s < 1) return set_error(RAC_ERR_ARG, "rac_box_block_min: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
-  bool lsmem = qp_smem_bytes<32>(s, false, true) <= 200 * 1024;
   double* L = nullptr;
-  if (!lsmem) {
-    int rc = check_cuda(cudaMallocAsync((void**)&L, (size_t)s * s * sizeof(double), st), "malloc L");
+  {
+    int rc = check_cuda(cudaMallocAsync((void**)&L, (size_t)s * (s + 1) * sizeof(double), st), "malloc L");
     if (rc) return rc;
   }
-  size_t smem = qp_smem_bytes<32>(s, false, lsmem);
+  size_t smem = qp_smem_bytes<32>(s, false, false);
   int rc = check_cuda(cudaFuncSetAttribute(box_test_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "box smem attribute");
   if (rc) return rc;

@@ -55,6 +55,8 @@ struct SysArgs {
   int32_t* info;
   const int32_t* done;  // skip when *done (converged / failed)
   int mode;             // FACTOR_INVERSE: sys^{-1} into inv; FACTOR_CHOL: lower L into inv
+  double* inv2;         // FACTOR_CHOL: optional sys^{-1} as well
+  double* cond_out;     // FACTOR_CHOL: optional per-block (max L_ii / min L_ii)^2
 };
 constexpr int FACTOR_INVERSE = 0;
 constexpr int FACTOR_CHOL = 1;

@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
   if (a.done && *a.done) return;
   const int s = a.s;
   const int b = a.blk_list ? a.blk_list[blockIdx.x] : blockIdx.x;
+  if (a.only_failed && a.info[b] == 0) return;   // re-do pass for blocks the blocked path rejected
   __shared__ int fail;
   __shared__ double red[CTHREADS / 32];
   __shared__ double W[SB * SB];
@@ -390,6 +391,15 @@ int launch_chol_system(const SysArgs& a, int p, cudaStream_t st) {
   const int use_packed = (mode == FACTOR_INVERSE && packed_bytes(s) <= kMaxDyn) ? 1 : 0;
   const int use_square = (square_bytes(s) <= kMaxDyn) ? 1 : 0;
   if (!use_square && !a.scratch) return set_error(RAC_ERR_ARG, "factor: scratch required for s=%d", s);
+  if (mode == FACTOR_INVERSE && !use_packed && !a.only_failed) {
+    // large blocks: blocked sweep over all blocks at once, then the Cholesky
+    // route only for blocks it rejected (authoritative PD test)
+    int rc = launch_inverse_large(a, p, st);
+    if (rc) return rc;
+    SysArgs b2 = a;
+    b2.only_failed = 1;
+    return launch_chol_system(b2, p, st);
+  }
   size_t smem = 0;
   if (use_packed) smem = packed_bytes(s);
   if (use_square) smem = std::max(smem, square_bytes(s));
@@ -402,7 +412,8 @@ int launch_chol_system(const SysArgs& a, int p, cudaStream_t st) {
 
 size_t chol_scratch_bytes(int s, int p) {
   if (square_bytes(s) <= kMaxDyn) return 0;
-  return (size_t)p * ((size_t)s * (s + 1) + s) * sizeof(double);
+  const size_t chol = (size_t)p * ((size_t)s * (s + 1) + s) * sizeof(double);
+  return packed_bytes(s) <= kMaxDyn ? chol : std::max(chol, large_scratch_bytes(s, p));
 }
 
 }  // namespace rac

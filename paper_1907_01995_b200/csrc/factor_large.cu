@@ -1,0 +1,294 @@
+// K3 for large blocks (s > 236, e.g. BASELINE config 5 with s = 500): the
+// explicit block inverse by a BLOCKED symmetric sweep (Gauss-Jordan) run as a
+// sequence of GPU-wide launches over all p blocks of the sweep at once.
+//
+// The block system lives in global memory as 64 x 64 lower tiles of an
+// S x S matrix (S = s rounded up to 64, padding = identity).  For each pivot
+// tile K:
+//   (a) W   = A_KK^{-1}              one CTA per block, packed sweep in smem
+//   (b) CW_I = A_IK W                 one CTA per (block, tile row I != K)
+//   (c) A_IJ -= CW_I A_JK'            one CTA per (block, lower tile I>=J, I,J != K)
+//   (d) A_IK = CW_I, A_KK = -W        K row / column rewritten
+// and finally inv = -A.  (b) and (c) are 64x64x64 products on FP64 tensor
+// cores (DMMA.8x8x4).  A non-positive pivot marks the block; such blocks are
+// re-done by the authoritative Cholesky kernel (factor.cu).
+#include "rac_internal.h"
+
+#include <algorithm>
+
+namespace rac {
+
+constexpr int LT = 64;           // tile side
+constexpr int LLD = LT + 4;      // smem stride (conflict-free fragment loads)
+constexpr int LTHREADS = 256;
+
+size_t large_scratch_bytes(int s, int p) {
+  const size_t S = (size_t)(s + LT - 1) / LT * LT;
+  return (size_t)p * (S * S + S * LT + LT * LT) * sizeof(double);
+}
+
+struct LargeBufs {
+  double* A;    // [p][S][S]   (only lower tiles maintained)
+  double* CW;   // [p][S][LT]
+  double* W;    // [p][LT][LT]
+  int S, nt;
+};
+
+__device__ __forceinline__ LargeBufs large_bufs(double* scratch, int s, int p) {
+  LargeBufs L;
+  L.S = (s + LT - 1) / LT * LT;
+  L.nt = L.S / LT;
+  L.A = scratch;
+  L.CW = L.A + (size_t)p * L.S * L.S;
+  L.W = L.CW + (size_t)p * L.S * LT;
+  return L;
+}
+
+// (0) assemble the padded block systems (lower part) from the split-K partials
+__global__ void large_assemble_kernel(SysArgs a, int p) {
+  if (a.done && *a.done) return;
+  const int s = a.s;
+  const LargeBufs L = large_bufs(a.scratch, s, p);
+  const int b = blockIdx.y;
+  const int32_t* bidx = a.idx ? a.idx + (int64_t)b * s : nullptr;
+  double* A = L.A + (size_t)b * L.S * L.S;
+  const int64_t total = (int64_t)L.S * L.S;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / L.S), j = (int)(e - (int64_t)i * L.S);
+    if (j > i) continue;
+    double v;
+    if (i >= s || j >= s || (bidx && (bidx[i] < 0 || bidx[j] < 0))) {
+      v = (i == j) ? 1.0 : 0.0;
+    } else {
+      v = 0.0;
+      if (a.ws) {
+        const double* src = a.ws + (int64_t)b * a.splits * s * s + (int64_t)i * s + j;
+        double acc = src[0];
+        for (int z = 1; z < a.splits; ++z) acc += src[(int64_t)z * s * s];
+        if (a.div != 1.0) acc = acc / a.div;
+        if (a.mul != 1.0) acc = a.mul * acc;
+        v = acc;
+      }
+      if (a.H) {
+        const double h = a.H[(int64_t)bidx[i] * a.ldh + bidx[j]];
+        v = a.ws ? h + v : h;
+      }
+      if (i == j) v += a.shift;
+    }
+    A[(int64_t)i * L.S + j] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.info[b] = 0;
+}
+
+// (a) W = inv(A_KK): unblocked symmetric sweep of the 64x64 block in smem
+__global__ void __launch_bounds__(LTHREADS) large_pivot_kernel(SysArgs a, int p, int kt) {
+  if (a.done && *a.done) return;
+  const LargeBufs L = large_bufs(a.scratch, a.s, p);
+  const int b = blockIdx.x;
+  if (a.info[b]) return;
+  __shared__ double P[LT][LT + 1];
+  __shared__ double col[LT];
+  __shared__ int fail;
+  const double* A = L.A + (size_t)b * L.S * L.S;
+  const int tid = threadIdx.x, k0 = kt * LT;
+  if (tid == 0) fail = 0;
+  for (int e = tid; e < LT * LT; e += LTHREADS) {
+    const int i = e / LT, j = e - i * LT;
+    const int gi = k0 + i, gj = k0 + j;
+    P[i][j] = (j <= i) ? A[(int64_t)gi * L.S + gj] : A[(int64_t)gj * L.S + gi];
+  }
+  __syncthreads();
+  for (int q = 0; q < LT; ++q) {
+    const double d = P[q][q];
+    if (!(d > 0.0) || !isfinite(d)) {
+      if (tid == 0) fail = k0 + q + 1;
+      break;
+    }
+    if (tid < LT) col[tid] = P[tid][q];
+    __syncthreads();
+    const double dinv = 1.0 / d;
+    for (int e = tid; e < LT * LT; e += LTHREADS) {
+      const int i = e / LT, j = e - i * LT;
+      double v;
+      if (i == q && j == q) v = -dinv;
+      else if (i == q) v = col[j] * dinv;
+      else if (j == q) v = col[i] * dinv;
+      else v = P[i][j] - col[i] * col[j] * dinv;
+      P[i][j] = v;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (fail) {
+    if (tid == 0) a.info[b] = fail;
+    return;
+  }
+  double* W = L.W + (size_t)b * LT * LT;
+  for (int e = tid; e < LT * LT; e += LTHREADS) W[e] = -P[e / LT][e % LT];   // +inv
+}
+
+// load a 64x64 tile (row-major, ld) into smem [r][c] (optionally transposed)
+__device__ __forceinline__ void load_tile(double (*dst)[LLD], const double* src, int64_t ld, bool trans) {
+  for (int e = threadIdx.x; e < LT * LT; e += LTHREADS) {
+    const int r = e / LT, c = e - r * LT;
+    if (!trans) dst[r][c] = src[(int64_t)r * ld + c];
+    else dst[c][r] = src[(int64_t)r * ld + c];
+  }
+}
+
+// C(64x64, in registers of the warp tiles) += alpha * X(64x64) * Y(64x64)'
+// sX[i][k], sY[j][k]; warp w computes rows 16*(w/2).., cols 32*(w%2)..
+__device__ __forceinline__ void tile_mma(const double (*sX)[LLD], const double (*sY)[LLD], double acc[2][4][2],
+                                         double alpha) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+#pragma unroll 4
+  for (int k = 0; k < LT; k += 4) {
+    double af[2], bf[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) af[i] = alpha * sX[r0 + i * 8 + g][k + t];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bf[j] = sY[c0 + j * 8 + g][k + t];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+}
+
+// (b) CW_I = A_IK * W for every tile row I != K
+__global__ void __launch_bounds__(LTHREADS) large_cw_kernel(SysArgs a, int p, int kt) {
+  if (a.done && *a.done) return;
+  const LargeBufs L = large_bufs(a.scratch, a.s, p);
+  const int b = blockIdx.y;
+  int I = blockIdx.x;
+  if (I >= kt) ++I;   // skip K
+  if (a.info[b]) return;
+  extern __shared__ __align__(16) double lsm[];
+  double(*sX)[LLD] = reinterpret_cast<double(*)[LLD]>(lsm);
+  double(*sY)[LLD] = reinterpret_cast<double(*)[LLD]>(lsm + LT * LLD);
+  const double* A = L.A + (size_t)b * L.S * L.S;
+  // X = A_IK (rows i of tile I, k of tile K); Y rows j = W columns: W symmetric, Y[j][k] = W[j][k]
+  if (I > kt) load_tile(sX, A + (int64_t)I * LT * L.S + kt * LT, L.S, false);
+  else load_tile(sX, A + (int64_t)kt * LT * L.S + I * LT, L.S, true);
+  load_tile(sY, L.W + (size_t)b * LT * LT, LT, false);
+  __syncthreads();
+  double acc[2][4][2] = {};
+  tile_mma(sX, sY, acc, 1.0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+  double* CW = L.CW + ((size_t)b * L.S + (size_t)I * LT) * LT;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) CW[(size_t)(r0 + i * 8 + g) * LT + c0 + j * 8 + 2 * t + e] = acc[i][j][e];
+}
+
+// (c) A_IJ -= CW_I * A_JK'   for lower tiles I >= J with I, J != K
+__global__ void __launch_bounds__(LTHREADS) large_update_kernel(SysArgs a, int p, int kt) {
+  if (a.done && *a.done) return;
+  const LargeBufs L = large_bufs(a.scratch, a.s, p);
+  const int b = blockIdx.y;
+  if (a.info[b]) return;
+  // tile index over the lower triangle of the (nt-1) x (nt-1) grid without K
+  const int m = L.nt - 1;
+  int I = 0, J = blockIdx.x;
+  while (J > I) { J -= I + 1; ++I; }
+  if (I >= m) return;
+  if (I >= kt) ++I;
+  if (J >= kt) ++J;
+  extern __shared__ __align__(16) double lsm[];
+  double(*sX)[LLD] = reinterpret_cast<double(*)[LLD]>(lsm);
+  double(*sY)[LLD] = reinterpret_cast<double(*)[LLD]>(lsm + LT * LLD);
+  double* A = L.A + (size_t)b * L.S * L.S;
+  load_tile(sX, L.CW + ((size_t)b * L.S + (size_t)I * LT) * LT, LT, false);
+  // Y[j][k] = A[J*64 + j][K*64 + k]
+  if (J > kt) load_tile(sY, A + (int64_t)J * LT * L.S + kt * LT, L.S, false);
+  else load_tile(sY, A + (int64_t)kt * LT * L.S + J * LT, L.S, true);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
+  double* C = A + (int64_t)I * LT * L.S + J * LT;
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) acc[i][j][e] = C[(int64_t)(r0 + i * 8 + g) * L.S + c0 + j * 8 + 2 * t + e];
+  __syncthreads();
+  tile_mma(sX, sY, acc, -1.0);
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) C[(int64_t)(r0 + i * 8 + g) * L.S + c0 + j * 8 + 2 * t + e] = acc[i][j][e];
+}
+
+// (d) K strip: A_IK = CW_I (lower tiles, transposed above K), A_KK = -W
+__global__ void large_strip_kernel(SysArgs a, int p, int kt) {
+  if (a.done && *a.done) return;
+  const LargeBufs L = large_bufs(a.scratch, a.s, p);
+  const int b = blockIdx.y;
+  if (a.info[b]) return;
+  const int I = blockIdx.x;   // 0..nt-1
+  double* A = L.A + (size_t)b * L.S * L.S;
+  for (int e = threadIdx.x; e < LT * LT; e += blockDim.x) {
+    const int i = e / LT, j = e - i * LT;
+    if (I == kt) {
+      if (j <= i) A[(int64_t)(kt * LT + i) * L.S + kt * LT + j] = -L.W[(size_t)b * LT * LT + e];
+    } else {
+      const double v = L.CW[((size_t)b * L.S + (size_t)I * LT + i) * LT + j];   // CW_I[i][j] = A'_{I i, K j}
+      if (I > kt) A[(int64_t)(I * LT + i) * L.S + kt * LT + j] = v;
+      else A[(int64_t)(kt * LT + j) * L.S + I * LT + i] = v;          // lower tile (K, I)
+    }
+  }
+}
+
+// (e) inv = -A (symmetric, s x s)
+__global__ void large_out_kernel(SysArgs a, int p) {
+  if (a.done && *a.done) return;
+  const int s = a.s;
+  const LargeBufs L = large_bufs(a.scratch, s, p);
+  const int b = blockIdx.y;
+  if (a.info[b]) return;
+  const double* A = L.A + (size_t)b * L.S * L.S;
+  double* out = a.inv + (int64_t)b * s * s;
+  const int64_t total = (int64_t)s * s;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / s), j = (int)(e - (int64_t)i * s);
+    out[e] = -((j <= i) ? A[(int64_t)i * L.S + j] : A[(int64_t)j * L.S + i]);
+  }
+}
+
+int launch_inverse_large(const SysArgs& a, int p, cudaStream_t st) {
+  const int S = (a.s + LT - 1) / LT * LT, nt = S / LT;
+  const size_t smem = 2 * LT * LLD * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    int rc = check_cuda(cudaFuncSetAttribute(large_cw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                        "large_cw smem");
+    if (rc) return rc;
+    rc = check_cuda(cudaFuncSetAttribute(large_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                    "large_update smem");
+    if (rc) return rc;
+    attr = true;
+  }
+  large_assemble_kernel<<<dim3(64, p), 256, 0, st>>>(a, p);
+  for (int kt = 0; kt < nt; ++kt) {
+    large_pivot_kernel<<<p, LTHREADS, 0, st>>>(a, p, kt);
+    if (nt > 1) {
+      large_cw_kernel<<<dim3(nt - 1, p), LTHREADS, smem, st>>>(a, p, kt);
+      const int m = nt - 1;
+      const int ntiles = m * (m + 1) / 2;
+      if (ntiles > 0) large_update_kernel<<<dim3(ntiles, p), LTHREADS, smem, st>>>(a, p, kt);
+    }
+    large_strip_kernel<<<dim3(nt, p), 256, 0, st>>>(a, p, kt);
+  }
+  large_out_kernel<<<dim3(32, p), 256, 0, st>>>(a, p);
+  return check_launch("inverse_large");
+}
+
+}  // namespace rac

@@ -57,7 +57,10 @@ struct SysArgs {
   int mode;             // FACTOR_INVERSE: sys^{-1} into inv; FACTOR_CHOL: lower L into inv
   double* inv2;         // FACTOR_CHOL: optional sys^{-1} as well
   double* cond_out;     // FACTOR_CHOL: optional per-block (max L_ii / min L_ii)^2
+  int only_failed;      // factor only blocks whose info[b] != 0 (re-do pass)
 };
+int launch_inverse_large(const SysArgs& a, int p, cudaStream_t st);
+size_t large_scratch_bytes(int s, int p);
 constexpr int FACTOR_INVERSE = 0;
 constexpr int FACTOR_CHOL = 1;
 int launch_chol_system(const SysArgs& a, int p, cudaStream_t st);

@@ -51,6 +51,9 @@ extern "C" {
 
 const char* rac_version(void);
 const char* rac_last_error(void);
+/* Number of kernels this library has launched since load (all contexts, all
+ * streams); used by bench.py to report gpu_launches inside a timed region. */
+uint64_t rac_launch_count(void);
 /* 0 if `device` is an sm_100 part this library was built for. */
 int rac_device_check(int device);
 

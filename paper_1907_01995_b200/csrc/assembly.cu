@@ -37,6 +37,7 @@ int launch_chunk_sort(const int64_t* perms, int64_t n, int s, int count, int32_t
   const int p = (int)((n + s - 1) / s);
   dim3 grid(p, count);
   chunk_sort_kernel<256><<<grid, 256, s * sizeof(int32_t), st>>>(perms, n, s, p, out);
+  note_launch();
   return check_launch("chunk_sort");
 }
 
@@ -52,6 +53,7 @@ int launch_order_cast(const int64_t* src, int64_t total, int32_t* dst, cudaStrea
   if (total <= 0) return RAC_OK;
   int blocks = (int)rac::min64((total + 255) / 256, 1184);
   order_cast_kernel<<<blocks, 256, 0, st>>>(src, total, dst);
+  note_launch();
   return check_launch("order_cast");
 }
 

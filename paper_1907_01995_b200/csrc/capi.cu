@@ -1,6 +1,7 @@
 // C ABI plumbing: error reporting, version, device checks, small kernels.
 #include <stdarg.h>
 #include <algorithm>
+#include <atomic>
 #include <stdio.h>
 
 #include "rac_internal.h"
@@ -25,6 +26,10 @@ int check_cuda(cudaError_t e, const char* what) {
 }
 
 int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what); }
+
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
+unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 int num_sms() {
   static int cached = 0;
@@ -59,6 +64,7 @@ int launch_gemv_rows(const double* Q, int64_t rows, int64_t cols, const double* 
   int blocks = (int)std::min<int64_t>((rows + 7) / 8, (int64_t)num_sms() * 8);
   if (blocks < 1) blocks = 1;
   gemv_rows_kernel<<<blocks, 256, 0, st>>>(Q, rows, cols, w, out);
+  note_launch();
   return check_launch("gemv_rows");
 }
 
@@ -73,6 +79,8 @@ __global__ void z_prox_kernel(const double* __restrict__ beta, const double* __r
 }
 
 }  // namespace rac
+
+extern "C" uint64_t rac_launch_count(void) { return (uint64_t)rac::launch_count(); }
 
 extern "C" const char* rac_version(void) { return "rac_b200 0.1.0 (sm_100a, fp64)"; }
 
@@ -102,6 +110,7 @@ extern "C" int rac_z_prox(const double* beta, const double* xi, int64_t n, doubl
   if (n == 0) return RAC_OK;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
   z_prox_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(beta, xi, n, gamma, thr, den, z);
+  note_launch();
   return check_launch("z_prox");
 }
 

@@ -199,6 +199,7 @@ int launch_transpose_pad(const double* X, int64_t m, int64_t n, int64_t ld, doub
   dim3 grid((unsigned)((n + 31) / 32), (unsigned)((ld + 31) / 32));
   if (grid.y > 65535) return set_error(RAC_ERR_UNSUPPORTED, "transpose: too many rows (%lld)", (long long)m);
   transpose_pad_kernel<<<grid, dim3(32, 8), 0, st>>>(X, m, n, ld, Xc);
+  note_launch();
   return check_launch("transpose_pad");
 }
 
@@ -245,6 +246,17 @@ struct rac_en_ctx {
   int32_t* ctrl = nullptr;
   double *hist_p = nullptr, *hist_d = nullptr;
   std::vector<void*> allocs;
+  // Sweep pipeline (RAC): the block systems of sweep k+1 (sort, Gram, inverses) only
+  // depend on the permutation, so they are prepared on a low-priority stream while
+  // the chain of sweep k runs on a high-priority one; idx/inv/info are double-buffered.
+  bool pipe = false;
+  cudaStream_t sprep = nullptr, schain = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_prep[2] = {nullptr, nullptr},
+              ev_chain[2] = {nullptr, nullptr};
+  bool chain_rec[2] = {false, false};
+  int32_t* idx_b[2] = {nullptr, nullptr};
+  double* inv_b[2] = {nullptr, nullptr};
+  int32_t* info_b[2] = {nullptr, nullptr};
   // optional per-stage CUDA-event timing: [assembly, gram, factor, chain]
   bool timing = false;
   std::vector<cudaEvent_t> events;  // 5 per timed sweep
@@ -288,7 +300,7 @@ int en_grow_history(rac_en_ctx* c, int need) {
   return RAC_OK;
 }
 
-int en_factor(rac_en_ctx* c) {
+int en_factor(rac_en_ctx* c, cudaStream_t st) {
   using namespace rac;
   SysArgs a{};
   a.ws = c->gram_ws;
@@ -301,19 +313,19 @@ int en_factor(rac_en_ctx* c) {
   a.scratch = c->scratch;
   a.info = c->info;
   a.done = c->ctrl;
-  return launch_chol_system(a, c->p, c->st);
+  return launch_chol_system(a, c->p, st);
 }
 
 int en_block_systems(rac_en_ctx* c) {
   int rc = rac::launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->st,
                             c->ctrl);
   if (rc) return rc;
-  return en_factor(c);
+  return en_factor(c, c->st);
 }
 
-int en_chain(rac_en_ctx* c, double tol) {
+int en_chain(rac_en_ctx* c, double tol, cudaStream_t st) {
   using namespace rac;
-  cudaMemsetAsync(c->bar, 0, sizeof(unsigned), c->st);
+  cudaMemsetAsync(c->bar, 0, sizeof(unsigned), st);
   EnChainArgs a{};
   a.Xc = c->Xc;
   a.ld = c->ld;
@@ -355,7 +367,7 @@ int en_chain(rac_en_ctx* c, double tol) {
     cfg.gridDim = dim3(c->P);
     cfg.blockDim = dim3(ENT);
     cfg.dynamicSmemBytes = res_smem_bytes<kResCS>(c->s, c->nch, c->p);
-    cfg.stream = c->st;
+    cfg.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = kResCS;
@@ -364,18 +376,24 @@ int en_chain(rac_en_ctx* c, double tol) {
     at[1].id = cudaLaunchAttributeCooperative;
     at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 2;
+    // Nsight Compute cannot replay a cooperative *cluster* launch; for profiling only,
+    // RAC_PROFILE_NONCOOP=1 drops the cooperative attribute (the grid is one wave of
+    // one CTA per SM either way, and ncu serialises kernels, so the barrier still holds).
+    static const bool noncoop = getenv("RAC_PROFILE_NONCOOP") && atoi(getenv("RAC_PROFILE_NONCOOP")) == 1;
+    cfg.numAttrs = noncoop ? 1 : 2;
+    note_launch();
     return check_cuda(cudaLaunchKernelExC(&cfg, (const void*)en_chain_res_kernel<kResCS>, rargs),
                       "en_chain_res (cluster cooperative launch)");
   }
   size_t smem = en_chain_smem(c->s, c->RC);
   cudaError_t e;
   if (c->RC == 32)
-    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<32>, dim3(c->P), dim3(ENT), args, smem, c->st);
+    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<32>, dim3(c->P), dim3(ENT), args, smem, st);
   else if (c->RC == 16)
-    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<16>, dim3(c->P), dim3(ENT), args, smem, c->st);
+    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<16>, dim3(c->P), dim3(ENT), args, smem, st);
   else
-    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<8>, dim3(c->P), dim3(ENT), args, smem, c->st);
+    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<8>, dim3(c->P), dim3(ENT), args, smem, st);
+  note_launch();
   return check_cuda(e, "en_chain (cooperative launch)");
 }
 
@@ -476,6 +494,31 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
     rac_en_destroy(c);
     return rc;
   }
+  c->idx_b[0] = c->idx;
+  c->inv_b[0] = c->inv;
+  c->info_b[0] = c->info;
+  {
+    const char* env = getenv("RAC_EN_PIPE");
+    c->pipe = (mode == RAC_MODE_RAC) && !(env && atoi(env) == 0);
+  }
+  if (c->pipe) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if ((rc = dalloc(c, &c->idx_b[1], (size_t)c->p * s)) || (rc = dalloc(c, &c->inv_b[1], sqs)) ||
+        (rc = dalloc(c, &c->info_b[1], c->p)) ||
+        (rc = check_cuda(cudaStreamCreateWithPriority(&c->sprep, cudaStreamNonBlocking, lo), "prep stream")) ||
+        (rc = check_cuda(cudaStreamCreateWithPriority(&c->schain, cudaStreamNonBlocking, hi), "chain stream"))) {
+      rac_en_destroy(c);
+      return rc;
+    }
+    cudaEvent_t* evs[] = {&c->ev_start, &c->ev_end, &c->ev_prep[0], &c->ev_prep[1], &c->ev_chain[0], &c->ev_chain[1]};
+    for (cudaEvent_t* e : evs)
+      if ((rc = check_cuda(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "pipeline event"))) {
+        rac_en_destroy(c);
+        return rc;
+      }
+    cudaMemsetAsync(c->info_b[1], 0, c->p * sizeof(int32_t), c->st);
+  }
   if ((rc = en_grow_history(c, 256))) {
     rac_en_destroy(c);
     return rc;
@@ -512,6 +555,7 @@ extern "C" int rac_en_set_data(rac_en_ctx* c, const double* X, int32_t layout, c
     return set_error(RAC_ERR_ARG, "rac_en_set_data: unknown layout %d", layout);
   }
   int blocks = (int)std::min<int64_t>((c->n + 7) / 8, (int64_t)num_sms() * 16);
+  note_launch();
   neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
   c->have_data = true;
   return check_launch("rac_en_set_data");
@@ -540,6 +584,34 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
     return set_error(RAC_ERR_ARG, "rac_en_run: rp mode needs rac_en_set_partition");
   int rc = en_grow_history(c, c->sweeps + count);
   if (rc) return rc;
+  if (c->pipe && !c->timing && count > 0) {
+    // prep(k+1) on sprep overlaps chain(k) on schain; prep(k) may only overwrite the
+    // buffers of sweep k-2 once that chain is done.
+    cudaEventRecord(c->ev_start, c->st);
+    cudaStreamWaitEvent(c->sprep, c->ev_start, 0);
+    cudaStreamWaitEvent(c->schain, c->ev_start, 0);
+    for (int k = 0; k < count; ++k) {
+      const int j = c->sweeps & 1;
+      if (c->chain_rec[j]) cudaStreamWaitEvent(c->sprep, c->ev_chain[j], 0);
+      c->idx = c->idx_b[j];
+      c->inv = c->inv_b[j];
+      c->info = c->info_b[j];
+      if ((rc = launch_chunk_sort(perms + (int64_t)k * c->n, c->n, c->s, 1, c->idx, c->sprep))) return rc;
+      if ((rc = launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->sprep,
+                            c->ctrl)))
+        return rc;
+      if ((rc = en_factor(c, c->sprep))) return rc;
+      cudaEventRecord(c->ev_prep[j], c->sprep);
+      cudaStreamWaitEvent(c->schain, c->ev_prep[j], 0);
+      if ((rc = en_chain(c, tol, c->schain))) return rc;
+      cudaEventRecord(c->ev_chain[j], c->schain);
+      c->chain_rec[j] = true;
+      c->sweeps++;
+    }
+    cudaEventRecord(c->ev_end, c->schain);
+    cudaStreamWaitEvent(c->st, c->ev_end, 0);
+    return check_launch("rac_en_run (pipelined)");
+  }
   for (int k = 0; k < count; ++k) {
     cudaEvent_t ev[5] = {};
     if (c->timing) {
@@ -553,7 +625,7 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
       rc = launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->st, c->ctrl);
       if (rc) return rc;
       if (c->timing) cudaEventRecord(ev[2], c->st);
-      rc = en_factor(c);
+      rc = en_factor(c, c->st);
       if (rc) return rc;
     } else {
       rc = launch_order_cast(perms + (int64_t)k * c->p, c->p, c->order, c->st);
@@ -561,7 +633,7 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
       if (c->timing) { cudaEventRecord(ev[1], c->st); cudaEventRecord(ev[2], c->st); }
     }
     if (c->timing) cudaEventRecord(ev[3], c->st);
-    rc = en_chain(c, tol);
+    rc = en_chain(c, tol, c->st);
     if (rc) return rc;
     if (c->timing) {
       cudaEventRecord(ev[4], c->st);
@@ -675,7 +747,13 @@ extern "C" int rac_en_timing(rac_en_ctx* c, double* stage_ms, int32_t* sweeps) {
 extern "C" int rac_en_destroy(rac_en_ctx* c) {
   if (!c) return RAC_OK;
   if (c->st) cudaStreamSynchronize(c->st);
+  if (c->schain) cudaStreamSynchronize(c->schain);
+  if (c->sprep) cudaStreamSynchronize(c->sprep);
   for (auto e : c->events) cudaEventDestroy(e);
+  for (cudaEvent_t e : {c->ev_start, c->ev_end, c->ev_prep[0], c->ev_prep[1], c->ev_chain[0], c->ev_chain[1]})
+    if (e) cudaEventDestroy(e);
+  if (c->schain) cudaStreamDestroy(c->schain);
+  if (c->sprep) cudaStreamDestroy(c->sprep);
   for (void* q : c->allocs) cudaFree(q);
   delete c;
   return RAC_OK;

@@ -407,6 +407,7 @@ int launch_chol_system(const SysArgs& a, int p, cudaStream_t st) {
                       "factor smem attribute");
   if (rc) return rc;
   factor_kernel<<<p, CTHREADS, smem, st>>>(a, mode, use_packed, use_square);
+  note_launch();
   return check_launch("factor");
 }
 

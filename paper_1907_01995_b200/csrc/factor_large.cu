@@ -288,6 +288,7 @@ int launch_inverse_large(const SysArgs& a, int p, cudaStream_t st) {
     large_strip_kernel<<<dim3(nt, p), 256, 0, st>>>(a, p, kt);
   }
   large_out_kernel<<<dim3(32, p), 256, 0, st>>>(a, p);
+  note_launch(2 + nt * (nt > 1 ? 4 : 2));
   return check_launch("inverse_large");
 }
 

@@ -38,13 +38,22 @@ GramPlan plan_gram(int64_t len, int s, int p) {
   pl.pairs = pl.tiles * (pl.tiles + 1) / 2;
   const int64_t nchunks = (len + GKC - 1) / GKC;
   const int64_t ctas = (int64_t)p * pl.pairs;
-  const int64_t target = 2LL * num_sms();
-  int64_t splits = (target + ctas - 1) / ctas;
-  splits = std::max<int64_t>(1, std::min<int64_t>(splits, std::max<int64_t>(1, nchunks / 8)));
-  splits = std::min<int64_t>(splits, 64);
-  int64_t per = (nchunks + splits - 1) / splits;
-  splits = (nchunks + per - 1) / per;
-  pl.splits = (int)splits;
+  // Pick the K split that minimises (CTAs on the busiest SM) x (chunks per CTA + epilogue):
+  // the DMMA pipe of an SM is shared by its resident CTAs, so a partially filled last
+  // wave costs as much as a full one.  Ties go to fewer splits (less partial traffic).
+  const int64_t sms = num_sms();
+  const int64_t max_splits = std::max<int64_t>(1, std::min<int64_t>(64, nchunks / 4));
+  int64_t best = 1;
+  double best_cost = 1e300;
+  for (int64_t sp = 1; sp <= max_splits; ++sp) {
+    const int64_t per = (nchunks + sp - 1) / sp;
+    const int64_t eff = (nchunks + per - 1) / per;
+    const int64_t waves = (ctas * eff + sms - 1) / sms;
+    const double cost = (double)waves * (double)(per + 2);
+    if (cost < best_cost * 0.995) { best_cost = cost; best = eff; }
+  }
+  const int64_t per = (nchunks + best - 1) / best;
+  pl.splits = (int)((nchunks + per - 1) / per);
   pl.chunk = per * GKC;
   return pl;
 }
@@ -333,6 +342,7 @@ int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx,
     if (rc) return rc;
     dim3 grid(pl.pairs, p, pl.splits);
     gram2_kernel<<<grid, G2T, smem, st>>>(V, ldv, len, idx, blk_list, s, pl.splits, pl.chunk, ws, done);
+    note_launch();
     return check_launch("gram2");
   }
   const size_t smem = 4 * GT * GLD * sizeof(double);
@@ -341,6 +351,7 @@ int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx,
   if (rc) return rc;
   dim3 grid(pl.pairs, p, pl.splits);
   gram_kernel<<<grid, GTHREADS, smem, st>>>(V, ldv, len, idx, blk_list, s, pl.splits, pl.chunk, ws, done);
+  note_launch();
   return check_launch("gram");
 }
 

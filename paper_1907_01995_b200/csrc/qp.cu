@@ -719,6 +719,7 @@ int qp_chain(rac_qp_ctx* c, double tol_p, double tol_d, int fixed) {
   a.cond = c->cond;
   void* args[] = {&a};
   cudaError_t e = cudaLaunchCooperativeKernel(qp_kernel(c), dim3(c->P), dim3(QPT), args, qp_smem(c), c->st);
+  note_launch();
   return check_cuda(e, "qp_chain (cooperative launch)");
 }
 
@@ -828,6 +829,7 @@ extern "C" int rac_qp_set_problem(rac_qp_ctx* c, const double* H, const double* 
   cudaMemcpyAsync(c->c, cvec, nb, cudaMemcpyDeviceToDevice, c->st);
   cudaMemcpyAsync(c->lo, lower, nb, cudaMemcpyDeviceToDevice, c->st);
   cudaMemcpyAsync(c->hi, upper, nb, cudaMemcpyDeviceToDevice, c->st);
+  note_launch();
   clip0_kernel<<<(int)std::min<int64_t>((c->n + 255) / 256, 1184), 256, 0, c->st>>>(c->lo, c->hi, c->n, c->x);
   // running products at x0 and the divergence bar (engine.py:361-362)
   if (c->H) {
@@ -1006,6 +1008,7 @@ extern "C" int rac_svm_build_q(const double* X, int64_t N, int64_t d, const doub
   cudaFreeAsync(Xp, st);
   cudaFreeAsync(sq, st);
   cudaFreeAsync(ids, st);
+  note_launch(3);
   return check_launch("rac_svm_build_q");
 }
 
@@ -1026,5 +1029,6 @@ extern "C" int rac_box_block_min(const double* M, const double* r, const double*
   if (rc) return rc;
   box_test_kernel<<<1, QPT, smem, st>>>(M, r, lo, hi, s, x, info, L);
   if (L) cudaFreeAsync(L, st);
+  note_launch();
   return check_launch("rac_box_block_min");
 }

@@ -14,6 +14,9 @@ void clear_error();
 int set_error(int code, const char* fmt, ...);
 int check_cuda(cudaError_t e, const char* what);
 int check_launch(const char* what);
+// count of kernels this library launched (rac_launch_count)
+void note_launch(int k = 1);
+unsigned long long launch_count();
 
 int num_sms();
 int launch_gemv_rows(const double* Q, int64_t rows, int64_t cols, const double* w, double* out,

@@ -258,18 +258,21 @@ def run_b200_en(args, world, rank, local):
     lib.rac_en_set_timing(solver.h, 2)
     solver.run(_device.PermutationFeeder(rng, n, dev).draw(1), None)
     torch.cuda.synchronize()
-    tbuf = (np.ctypeslib.ctypes.c_int64 * (2 + 7 * p))()
-    lib.rac_en_trace(solver.h, tbuf, 2 + 7 * p)
-    tv = np.array(tbuf[:2 + 6 * p], dtype=np.float64) / 1e3   # us
-    ph = np.diff(tv[1:]).reshape(p, 6) if p > 0 else np.zeros((0, 6))
+    tbuf = (np.ctypeslib.ctypes.c_int64 * (8 + 12 * p))()
+    lib.rac_en_trace(solver.h, tbuf, 8 + 12 * p)
     info = (np.ctypeslib.ctypes.c_int32 * 4)()
     lib.rac_en_info(solver.h, info)
-    labels = (("cluster_sync", "cluster_reduce", "grid_barrier", "rhs", "delta+cluster_sync", "row_phase")
+    labels = (("cluster_sync", "cluster_reduce", "grid_barrier", "rhs", "delta+cluster_sync", "tile_wait",
+               "row_pass1", "row_sync1", "row_pass2", "row_pass3", "issue_next")
               if info[0] == 1 else
               ("barrier1", "S1_reduce", "barrier2", "S2_solve", "barrier3", "row_phase"))
+    nl = len(labels)
+    pro = 5 if info[0] == 1 else 2       # stamps before the first block (start, [row passes], R0)
+    tv = np.array(tbuf[:pro + nl * p], dtype=np.float64) / 1e3   # us
+    ph = np.diff(tv[pro - 1:]).reshape(p, nl) if p > 0 else np.zeros((0, nl))
     chain_trace = {"variant": "resident-cluster" if info[0] == 1 else "streaming",
                    "ctas": int(info[1]), "rows_per_chunk": int(info[2]), "chunks_per_cta": int(info[3]),
-                   "first_row_phase_us": float(tv[1] - tv[0]),
+                   "first_row_phase_us": float(tv[pro - 1] - tv[0]),
                    "per_block_us": {k: float(v) for k, v in zip(labels, ph.mean(axis=0))}}
     lib.rac_en_set_timing(solver.h, 0)
     solver.close()

@@ -31,7 +31,7 @@ namespace rac {
 
 constexpr int ENT = RP_THREADS;   // threads per chain CTA
 constexpr int EN_QMAX = RP_QMAX;   // block_size <= EN_QMAX * ENT
-constexpr int kResCS = 2;          // cluster size of the resident chain (148 SMs = 74 pairs)
+constexpr int kResCS = 2;          // default cluster size of the resident chain (148 SMs = 74 pairs)
 
 struct EnChainArgs {
   const double* Xc;
@@ -230,6 +230,7 @@ struct rac_en_ctx {
   cudaStream_t st = nullptr;
   int P = 0, RC = 32, nrc = 0;
   int variant = 0, nch = 0;   // 1: resident-tile cluster chain (en_chain_res_kernel)
+  int cs = 2;                 // its cluster size (2, 4 or 8)
   rac::GramPlan gp{};
   bool have_data = false, have_partition = false;
   int sweeps = 0;        // sweeps enqueued so far
@@ -260,7 +261,7 @@ struct rac_en_ctx {
   // optional per-stage CUDA-event timing: [assembly, gram, factor, chain]
   bool timing = false;
   std::vector<cudaEvent_t> events;  // 5 per timed sweep
-  long long* trace = nullptr;       // 2 + 7p phase timestamps of the last traced sweep
+  long long* trace = nullptr;       // 2 + 8p phase timestamps of the last traced sweep
 };
 
 namespace {
@@ -274,6 +275,16 @@ int dalloc(rac_en_ctx* c, T** p, size_t count) {
   c->allocs.push_back(q);
   *p = (T*)q;
   return RAC_OK;
+}
+
+void* res_kernel(int cs) {
+  return cs == 8 ? (void*)rac::en_chain_res_kernel<8>
+                 : (cs == 4 ? (void*)rac::en_chain_res_kernel<4> : (void*)rac::en_chain_res_kernel<2>);
+}
+
+size_t res_smem(int cs, int s, int nch, int p) {
+  return cs == 8 ? rac::res_smem_bytes<8>(s, nch, p)
+                 : (cs == 4 ? rac::res_smem_bytes<4>(s, nch, p) : rac::res_smem_bytes<2>(s, nch, p));
 }
 
 size_t en_chain_smem(int s, int RC) {
@@ -366,11 +377,11 @@ int en_chain(rac_en_ctx* c, double tol, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->P);
     cfg.blockDim = dim3(ENT);
-    cfg.dynamicSmemBytes = res_smem_bytes<kResCS>(c->s, c->nch, c->p);
+    cfg.dynamicSmemBytes = res_smem(c->cs, c->s, c->nch, c->p);
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kResCS;
+    at[0].val.clusterDim.x = c->cs;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeCooperative;
@@ -382,7 +393,7 @@ int en_chain(rac_en_ctx* c, double tol, cudaStream_t st) {
     static const bool noncoop = getenv("RAC_PROFILE_NONCOOP") && atoi(getenv("RAC_PROFILE_NONCOOP")) == 1;
     cfg.numAttrs = noncoop ? 1 : 2;
     note_launch();
-    return check_cuda(cudaLaunchKernelExC(&cfg, (const void*)en_chain_res_kernel<kResCS>, rargs),
+    return check_cuda(cudaLaunchKernelExC(&cfg, (const void*)res_kernel(c->cs), rargs),
                       "en_chain_res (cluster cooperative launch)");
   }
   size_t smem = en_chain_smem(c->s, c->RC);
@@ -445,32 +456,42 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
     const char* env = getenv("RAC_EN_VARIANT");
     const int want = env ? atoi(env) : 1;
     const int nrc32 = (int)((m + 31) / 32);
-    int Pc = std::max(kResCS, std::min(num_sms(), (nrc32 + kResCS - 1) / kResCS * kResCS) / kResCS * kResCS);
-    const int nch = (nrc32 + Pc - 1) / Pc;
-    const size_t rs = res_smem_bytes<kResCS>(s, nch, (int)((n + s - 1) / s));
-    if (want == 1 && s <= ENT && rs <= 226 * 1024) {
-      void* rk = (void*)en_chain_res_kernel<kResCS>;
-      if (cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs) == cudaSuccess &&
-          cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) == cudaSuccess) {
+    const char* envcs = getenv("RAC_EN_CS");
+    const int cs = envcs ? std::max(2, std::min(8, atoi(envcs))) : kResCS;
+    const int CS = (cs >= 8) ? 8 : (cs >= 4 ? 4 : 2);
+    int Pc = std::max(CS, std::min(num_sms(), (nrc32 + CS - 1) / CS * CS) / CS * CS);
+    void* rk = res_kernel(CS);
+    if (want == 1 && s <= ENT && Pc / CS <= 32 * ((148 / CS + 31) / 32) &&
+        cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) == cudaSuccess) {
+      // the largest grid (multiple of CS, <= Pc) whose clusters are co-resident
+      for (int tries = 0; tries < 4 && Pc >= CS; ++tries) {
+        const int nch = (nrc32 + Pc - 1) / Pc;
+        const size_t rs = res_smem(CS, s, nch, (int)((n + s - 1) / s));
+        if (rs > 226 * 1024 || cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs) != cudaSuccess)
+          break;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(Pc);
         cfg.blockDim = dim3(ENT);
         cfg.dynamicSmemBytes = rs;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = kResCS;
+        at[0].val.clusterDim.x = CS;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int clusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&clusters, rk, &cfg) == cudaSuccess && clusters * kResCS >= Pc) {
+        if (cudaOccupancyMaxActiveClusters(&clusters, rk, &cfg) != cudaSuccess) break;
+        if (clusters * CS >= Pc) {
           c->variant = 1;
+          c->cs = CS;
           c->RC = 32;
           c->nrc = nrc32;
           c->nch = nch;
           c->P = Pc;
+          break;
         }
+        Pc = clusters * CS;
       }
       cudaGetLastError();
     }
@@ -697,7 +718,7 @@ extern "C" int rac_en_set_timing(rac_en_ctx* c, int32_t enable) {
   if (!c) return set_error(RAC_ERR_ARG, "rac_en_set_timing: null context");
   c->timing = enable != 0;
   if (enable >= 2 && !c->trace) {
-    int rc = dalloc(c, &c->trace, 2 + 7 * (size_t)c->p);
+    int rc = dalloc(c, &c->trace, 8 + 12 * (size_t)c->p);
     if (rc) return rc;
   }
   if (enable < 2) c->trace = nullptr;
@@ -719,7 +740,7 @@ extern "C" int rac_en_trace(rac_en_ctx* c, int64_t* host, int32_t capacity) {
   using namespace rac;
   clear_error();
   if (!c || !host || !c->trace) return set_error(RAC_ERR_ARG, "rac_en_trace: tracing not enabled");
-  int k = std::min<int>(capacity, 2 + 7 * c->p);
+  int k = std::min<int>(capacity, 8 + 12 * c->p);
   return check_cuda(cudaMemcpy(host, c->trace, k * sizeof(int64_t), cudaMemcpyDeviceToHost), "trace copy");
 }
 

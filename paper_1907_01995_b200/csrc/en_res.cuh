@@ -28,21 +28,20 @@ namespace rac {
 namespace cg = cooperative_groups;
 
 constexpr int RES_RC = 32;        // rows per chunk (one 256-byte segment per column)
-constexpr int RES_QMAX = ENT / 8; // columns per warp in the partial (s <= 256)
-constexpr int RES_BATCH = 16;     // independent partial loads in flight per thread
+constexpr int RES_PAD = 2;        // tile column padding (doubles)
 
 struct ResSmem {
-  double* tiles;   // [2][nch][s][32]   (column segments, unpadded: TMA destination)
+  double* tiles;   // [2][s][nch*32+2]  (column segments: TMA destination)
   double* ginv;    // [sl][s]            inv_b rows of this rank's slice
   double* cxz;     // [3][s]             c, xi, z at the block's indices
   double* sX;      // [2][s]             beta at a block's indices, by block parity
   double* sDel;    // [s]                full delta of the current block
   double* sRhs;    // [s]
   double* sPart;   // [s]                this CTA's partial (cluster peers read it)
-  double* sSlice;  // [2s]               delta slice | pending beta (cluster 0)
+  double* sSlice;  // [4s]               delta slice | pending beta, xi, z (cluster 0)
   double* sR;      // [nch*32]           resident rows of r
-  double* red;     // [256 * 2]
-  double* sT;      // [32]
+  double* red;     // [2][nch][8 warps][32]  row-phase reductions; [s] rhs sums
+  double* sT;      // [nch*32]
   uint64_t* bars;  // [3]                tile slot 0/1, solve data
   int* pend;       // [s]
   int* sIdx;       // [p*s]              this sweep's block table
@@ -51,7 +50,8 @@ struct ResSmem {
 template <int CS>
 __host__ __device__ size_t res_smem_bytes(int s, int nch, int p) {
   const size_t sl = (s + CS - 1) / CS;
-  return (2 * (size_t)nch * s * RES_RC + sl * s + 10 * (size_t)s + (size_t)nch * RES_RC + 512 + RES_RC + 4) *
+  return (2 * (size_t)s * (nch * RES_RC + RES_PAD) + sl * s + 12 * (size_t)s + (size_t)nch * RES_RC +
+          2 * (size_t)nch * (ENT / 32) * RES_RC + (size_t)nch * RES_RC + 6) *
              sizeof(double) +
          ((size_t)s + (size_t)p * s) * sizeof(int);
 }
@@ -61,17 +61,18 @@ __device__ __forceinline__ ResSmem carve_res(double* base, int s, int nch) {
   const int sl = (s + CS - 1) / CS;
   ResSmem w;
   double* p = base;
-  w.tiles = p; p += 2 * (size_t)nch * s * RES_RC;
+  w.tiles = p; p += 2 * (size_t)s * (nch * RES_RC + RES_PAD);
   w.ginv = p; p += (size_t)sl * s;
   w.cxz = p; p += 3 * s;
   w.sX = p; p += 2 * s;
   w.sDel = p; p += s;
   w.sRhs = p; p += s;
   w.sPart = p; p += s;
-  w.sSlice = p; p += 2 * s;
+  w.sSlice = p; p += 4 * s;
   w.sR = p; p += (size_t)nch * RES_RC;
-  w.red = p; p += 512;
-  w.sT = p; p += RES_RC;
+  w.red = p; p += 2 * (size_t)nch * (ENT / 32) * RES_RC;
+  p = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));  // double2 loads
+  w.sT = p; p += (size_t)nch * RES_RC;
   w.bars = reinterpret_cast<uint64_t*>(p); p += 4;
   w.pend = reinterpret_cast<int*>(p);
   w.sIdx = w.pend + s;
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = ENT / 32;
   const int P = gridDim.x, C = P / CS;
   const int rank = (int)cl.block_rank(), cid = blockIdx.x / CS;
-  const int sl = (s + CS - 1) / CS, j0 = rank * sl, j1 = min(s, j0 + sl);
+  const int sl = (s + CS - 1) / CS, j0 = min(s, rank * sl), j1 = min(s, j0 + sl);
   unsigned target = 0;
   if (tid == 0) {
     bad = 0;
@@ -113,12 +114,16 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
   if (tr) a.trace[tp++] = gtimer();
   auto blk = [&](int t) { return a.order ? a.order[t] : t; };
   auto bidx = [&](int b) { return w.sIdx + (size_t)b * s; };
-  auto tile = [&](int slot, int k) { return w.tiles + ((size_t)slot * nch + k) * s * RC; };
-  int nchv = 0;  // valid chunks of this CTA
-  for (int k = 0; k < nch; ++k)
-    if (blockIdx.x + k * P < a.nrc) nchv = k + 1;
+  // CTA q owns the contiguous chunks q*nch .. q*nch+nchv-1, so one column of a
+  // block is ONE bulk copy of nchv*256 bytes; slot layout T[j][nch*RC].
+  // column stride padded by 2 doubles: 16-byte loads of 8 consecutive columns hit
+  // 8 distinct bank quads (pass 3 is column-per-thread)
+  const int RCN = nch * RC + RES_PAD;
+  auto tile = [&](int slot) { return w.tiles + (size_t)slot * s * RCN; };
+  const int nchv = max(0, min(nch, a.nrc - (int)blockIdx.x * nch));  // valid chunks of this CTA
+  const int64_t row0 = (int64_t)blockIdx.x * nch * RC;
   for (int k = 0; k < nchv; ++k) {
-    const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
+    const int64_t i0 = row0 + (int64_t)k * RC;
     for (int i = tid; i < RC; i += ENT) w.sR[k * RC + i] = (i0 + i < a.m) ? a.r[i0 + i] : 0.0;
   }
   unsigned par[3] = {0u, 0u, 0u};
@@ -133,15 +138,14 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     }
     __syncthreads();
     const int* bi = bidx(b);
-    for (int e = tid; e < nchv * s; e += ENT) {
-      const int k = e / s, j = e - k * s;
-      const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
-      double* dst = tile(slot, k) + (size_t)j * RC;
-      const int g = bi[j];
-      if (g >= 0) bulk_g2s(dst, a.Xc + (int64_t)g * a.ld + i0, RC * sizeof(double), w.bars + slot);
-      else
-        for (int i = 0; i < RC; ++i) dst[i] = 0.0;
-    }
+    if (nchv > 0)
+      for (int j = tid; j < s; j += ENT) {
+        double* dst = tile(slot) + (size_t)j * RCN;
+        const int g = bi[j];
+        if (g >= 0) bulk_g2s(dst, a.Xc + (int64_t)g * a.ld + row0, (unsigned)(nchv * RC * sizeof(double)), w.bars + slot);
+        else
+          for (int i = 0; i < nchv * RC; ++i) dst[i] = 0.0;
+      }
     for (int j = tid; j < s; j += ENT) {
       const int g = bi[j];
       if (g >= 0) cp_async8(xdst + j, a.beta + g);
@@ -160,7 +164,7 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     if (bulk_inv) {
       if (tid == 0) {
         mbar_arrive_expect_tx(w.bars + 2, (unsigned)(rows * s * sizeof(double)));
-        bulk_g2s(w.ginv, Ib, (unsigned)(rows * s * sizeof(double)), w.bars + 2);
+        if (rows > 0) bulk_g2s(w.ginv, Ib, (unsigned)(rows * s * sizeof(double)), w.bars + 2);
       }
     } else {
       for (int e = tid; e < rows * s; e += ENT) cp_async8(w.ginv + e, Ib + e);
@@ -188,55 +192,80 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
   };
   // one row phase: optional r-update with slot sp (delta in sDel) and optional
   // partial for slot sn (x values in xs) -> sPart.  Layout T[j][i], lanes = rows.
+  // All chunks of the CTA go through each pass together: two __syncthreads per
+  // row phase whatever nch is.
   auto row_phase_res = [&](int sp, int sn, const double* xs) {
-    double acc[RES_QMAX];
-#pragma unroll
-    for (int c = 0; c < RES_QMAX; ++c) acc[c] = 0.0;
-    for (int k = 0; k < nchv; ++k) {
-      const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
-      const int rows = (int)min64(RC, a.m - i0);
-      double* rr = w.sR + k * RC;
+    double* redp = w.red;                              // [nch][nw][RC]
+    double* redn = w.red + (size_t)nch * nw * RC;      // [nch][nw][RC]
+    // up to 4 chunks per pass over j: independent accumulators, same j order per chunk
+    for (int kb = 0; kb < nchv; kb += 4) {
+      const int kn = min(4, nchv - kb);
+      double up[4] = {0.0, 0.0, 0.0, 0.0}, un[4] = {0.0, 0.0, 0.0, 0.0};
       if (sp >= 0) {
-        const double* T = tile(sp, k);
-        double u = 0.0;
-        for (int j = warp; j < s; j += nw) u += T[j * RC + lane] * w.sDel[j];
-        w.red[warp * RC + lane] = u;
-        __syncthreads();
-        if (tid < rows) {
-          double tot = w.red[tid];
-          for (int q = 1; q < nw; ++q) tot += w.red[q * RC + tid];
-          rr[tid] += tot;
+        const double* T = tile(sp) + kb * RC + lane;
+        for (int j = warp; j < s; j += nw) {
+          const double d = w.sDel[j];
+          const double* Tj = T + (size_t)j * RCN;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < kn) up[u] += Tj[u * RC] * d;
         }
-        __syncthreads();
       }
       if (sn >= 0) {
-        const double* T = tile(sn, k);
-        double u = 0.0;
-        for (int j = warp; j < s; j += nw) u += T[j * RC + lane] * xs[j];
-        w.red[warp * RC + lane] = u;
-        __syncthreads();
-        if (tid < RC) {
-          double tot = w.red[tid];
-          for (int q = 1; q < nw; ++q) tot += w.red[q * RC + tid];
-          w.sT[tid] = (tid < rows) ? rr[tid] - tot : 0.0;
-        }
-        __syncthreads();
-        const double ti = w.sT[lane];
+        const double* T = tile(sn) + kb * RC + lane;
+        for (int j = warp; j < s; j += nw) {
+          const double x = xs[j];
+          const double* Tj = T + (size_t)j * RCN;
 #pragma unroll
-        for (int c = 0; c < RES_QMAX; ++c) {
-          const int j = warp + c * nw;
-          if (j < s) acc[c] += T[j * RC + lane] * ti;
+          for (int u = 0; u < 4; ++u)
+            if (u < kn) un[u] += Tj[u * RC] * x;
         }
       }
-    }
-    if (sn >= 0) {
 #pragma unroll
-      for (int c = 0; c < RES_QMAX; ++c) {
-        const int j = warp + c * nw;
-        if (j < s) {
-          const double v = warp_sum(acc[c]);
-          if (lane == 0) w.sPart[j] = v;
+      for (int u = 0; u < 4; ++u)
+        if (u < kn) {
+          redp[((kb + u) * nw + warp) * RC + lane] = up[u];
+          redn[((kb + u) * nw + warp) * RC + lane] = un[u];
         }
+    }
+    if (tr) a.trace[tp++] = gtimer();
+    __syncthreads();
+    if (tr) a.trace[tp++] = gtimer();
+    for (int e = tid; e < nchv * RC; e += ENT) {
+      const int k = e / RC, i = e - k * RC;
+      const int64_t i0 = row0 + (int64_t)k * RC;
+      const int rows = (int)min64(RC, a.m - i0);
+      double* rr = w.sR + k * RC;
+      if (sp >= 0 && i < rows) {
+        double tot = redp[(k * nw) * RC + i];
+        for (int q = 1; q < nw; ++q) tot += redp[(k * nw + q) * RC + i];
+        rr[i] += tot;
+      }
+      if (sn >= 0) {
+        double tot = redn[(k * nw) * RC + i];
+        for (int q = 1; q < nw; ++q) tot += redn[(k * nw + q) * RC + i];
+        w.sT[k * RC + i] = (i < rows) ? rr[i] - tot : 0.0;
+      }
+    }
+    __syncthreads();
+    if (tr) a.trace[tp++] = gtimer();
+    if (sn >= 0) {
+      // partial_j = sum_i T[j][i] t_i : one column per thread, 16-byte smem loads
+      const double* T = tile(sn);
+      const int nr = nchv * RC;
+      for (int j = tid; j < s; j += ENT) {
+        const double2* col = reinterpret_cast<const double2*>(T + (size_t)j * RCN);
+        const double2* tt = reinterpret_cast<const double2*>(w.sT);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        for (int i = 0; i < nr / 2; i += 2) {
+          const double2 x0 = col[i], x1 = col[i + 1];
+          const double2 t0 = tt[i], t1 = tt[i + 1];
+          a0 += x0.x * t0.x;
+          a1 += x0.y * t0.y;
+          a2 += x1.x * t1.x;
+          a3 += x1.y * t1.y;
+        }
+        w.sPart[j] = (a0 + a1) + (a2 + a3);
       }
     }
   };
@@ -249,7 +278,7 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
       if (g < 0) continue;
       const double bn = w.sSlice[s + q];
       a.beta[g] = bn;
-      const double zo = ldcg(a.z + g), x0 = ldcg(a.xi + g);
+      const double x0 = w.sSlice[2 * s + q], zo = w.sSlice[3 * s + q];
       const double av = sub(x0, mul(gamma, bn));
       const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
       a.z[g] = zn;
@@ -258,10 +287,10 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
       my_max = fmax(my_max, fabs(sub(zn, zo)));
     }
   };
-  // rhs reduction over the C cluster partials: G threads per entry, each
-  // summing a contiguous run of partials with RES_BATCH loads in flight
-  const int G = max(1, min(ENT / s, 2 * ENT / s));
-  const int per = (C + G - 1) / G;
+  // rhs reduction over the C cluster partials: the global partials are laid
+  // out [s][C], so one warp reads the C partials of an entry as contiguous
+  // 256-byte lines; 4 entries x RES_QL loads per lane are in flight at once.
+  constexpr int RES_QL = (148 / CS + 31) / 32;
 
   // ---- prologue: tiles (+ beta) of blocks 0 and 1, solve data of block 0
   issue_tile(0, blk(0), w.sX);
@@ -285,33 +314,38 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     for (int j = j0 + tid; j < j1; j += ENT) {
       double acc = 0.0;
       for (int q = 0; q < CS; ++q) acc += cl.map_shared_rank(w.sPart, q)[j];
-      gpart[(int64_t)cid * s + j] = acc;
+      gpart[(int64_t)j * C + cid] = acc;
     }
     if (tr) a.trace[tp++] = gtimer();
     grid_barrier(a.bar, target, P);
     if (tr) a.trace[tp++] = gtimer();
     if (t > 0) commit();
-    // ---- full rhs: G threads per entry, batched independent loads
-    {
-      const int j = tid / G, g = tid - j * G;
-      double acc = 0.0;
-      if (j < s) {
-        const int q0 = g * per, q1 = min(C, q0 + per);
-        for (int q = q0; q < q1; q += RES_BATCH) {
-          double v[RES_BATCH];
+    // ---- full rhs: one warp per entry, 4 entries per round
+    for (int jb = warp; jb < s; jb += 4 * nw) {
+      double v[4][RES_QL];
 #pragma unroll
-          for (int u = 0; u < RES_BATCH; ++u) v[u] = (q + u < q1) ? ldcg(gpart + (int64_t)(q + u) * s + j) : 0.0;
+      for (int u = 0; u < 4; ++u) {
+        const int j = jb + u * nw;
 #pragma unroll
-          for (int u = 0; u < RES_BATCH; ++u) acc += v[u];
+        for (int ql = 0; ql < RES_QL; ++ql) {
+          const int q = lane + 32 * ql;
+          v[u][ql] = (j < s && q < C) ? ldcg(gpart + (int64_t)j * C + q) : 0.0;
         }
       }
-      w.red[tid] = acc;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double acc = v[u][0];
+#pragma unroll
+        for (int ql = 1; ql < RES_QL; ++ql) acc += v[u][ql];
+        acc = warp_sum(acc);
+        const int j = jb + u * nw;
+        if (lane == 0 && j < s) w.red[j] = acc;
+      }
     }
     wait_solve();
     __syncthreads();
     for (int j = tid; j < s; j += ENT) {
-      double acc = w.red[j * G];
-      for (int g = 1; g < G; ++g) acc += w.red[j * G + g];
+      const double acc = w.red[j];
       double rhs = 0.0;
       if (bi[j] >= 0) {
         const double cross = acc / m;
@@ -340,6 +374,8 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
           w.sSlice[i] = (g >= 0) ? acc - xb[i] : 0.0;
           w.pend[i - j0] = g;
           w.sSlice[s + (i - j0)] = acc;
+          w.sSlice[2 * s + (i - j0)] = w.cxz[s + i];       // xi, z of block t before its update
+          w.sSlice[3 * s + (i - j0)] = w.cxz[2 * s + i];
         }
       }
     }
@@ -353,7 +389,9 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
       cp_async_wait<1>();   // beta of block t+1 (committed before the last solve group)
     }
     __syncthreads();
+    if (tr) a.trace[tp++] = gtimer();
     row_phase_res(t & 1, more ? ((t + 1) & 1) : -1, w.sX + ((t + 1) & 1) * s);
+    if (tr) a.trace[tp++] = gtimer();
     if (more) {
       __syncthreads();   // slot t&1, sX[t&1], ginv, cxz are dead for every thread
       if (t + 2 < a.p) issue_tile(t & 1, blk(t + 2), w.sX + (t & 1) * s);
@@ -363,7 +401,7 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     if (tr) a.trace[tp++] = gtimer();
   }
   for (int k = 0; k < nchv; ++k) {
-    const int64_t i0 = (int64_t)(blockIdx.x + k * P) * RC;
+    const int64_t i0 = row0 + (int64_t)k * RC;
     for (int i = tid; i < RC; i += ENT)
       if (i0 + i < a.m) a.r[i0 + i] = w.sR[k * RC + i];
   }

@@ -258,11 +258,12 @@ def run_b200_en(args, world, rank, local):
     lib.rac_en_set_timing(solver.h, 2)
     solver.run(_device.PermutationFeeder(rng, n, dev).draw(1), None)
     torch.cuda.synchronize()
-    tbuf = (np.ctypeslib.ctypes.c_int64 * (8 + 12 * p))()
-    lib.rac_en_trace(solver.h, tbuf, 8 + 12 * p)
+    tbuf = (np.ctypeslib.ctypes.c_int64 * (8 + 16 * p))()
+    lib.rac_en_trace(solver.h, tbuf, 8 + 16 * p)
     info = (np.ctypeslib.ctypes.c_int32 * 4)()
     lib.rac_en_info(solver.h, info)
-    labels = (("cluster_sync", "cluster_reduce", "grid_barrier", "rhs", "delta+cluster_sync", "tile_wait",
+    labels = (("cluster_sync", "cluster_reduce", "grid_barrier", "commit", "rhs_loads", "solve_wait", "rhs",
+               "delta+cluster_sync", "tile_wait",
                "row_pass1", "row_sync1", "row_pass2", "row_pass3", "issue_next")
               if info[0] == 1 else
               ("barrier1", "S1_reduce", "barrier2", "S2_solve", "barrier3", "row_phase"))

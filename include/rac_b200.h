@@ -114,11 +114,12 @@ int rac_en_history(rac_en_ctx* ctx, double* primal, double* dual, int32_t capaci
 int rac_en_set_timing(rac_en_ctx* ctx, int32_t enable);
 int rac_en_timing(rac_en_ctx* ctx, double* stage_ms_host4, int32_t* sweeps_host);
 /* enable >= 2 in rac_en_set_timing also records %globaltimer at every chain
- * phase boundary of each sweep (CTA 0), up to 8 + 12p stamps (the last
+ * phase boundary of each sweep (CTA 0), up to 8 + 16p stamps (the last
  * sweep's are kept).  Streaming chain: [start, R0, then per block bar, S1,
  * bar, S2, bar, R].  Resident chain: [start, 3 row-pass stamps, R0, then per
- * block cluster sync, cluster reduce, grid barrier, rhs, delta + cluster sync,
- * tile wait, row pass 1, row sync, row pass 2, row pass 3, next-block issue]. */
+ * block cluster sync, cluster reduce, grid barrier, commit, rhs loads, solve
+ * data wait, rhs, delta + cluster sync, tile wait, row pass 1, row sync, row
+ * pass 2, row pass 3, next-block issue]. */
 int rac_en_trace(rac_en_ctx* ctx, int64_t* host, int32_t capacity);
 /* [chain variant (0 streaming, 1 resident-tile cluster), CTAs, rows per chunk, chunks per CTA] */
 int rac_en_info(rac_en_ctx* ctx, int32_t* info_host4);

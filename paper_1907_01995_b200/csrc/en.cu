@@ -456,42 +456,65 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
     const char* env = getenv("RAC_EN_VARIANT");
     const int want = env ? atoi(env) : 1;
     const int nrc32 = (int)((m + 31) / 32);
-    const char* envcs = getenv("RAC_EN_CS");
-    const int cs = envcs ? std::max(2, std::min(8, atoi(envcs))) : kResCS;
-    const int CS = (cs >= 8) ? 8 : (cs >= 4 ? 4 : 2);
-    int Pc = std::max(CS, std::min(num_sms(), (nrc32 + CS - 1) / CS * CS) / CS * CS);
-    void* rk = res_kernel(CS);
-    if (want == 1 && s <= ENT && Pc / CS <= 32 * ((148 / CS + 31) / 32) &&
-        cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) == cudaSuccess) {
-      // the largest grid (multiple of CS, <= Pc) whose clusters are co-resident
-      for (int tries = 0; tries < 4 && Pc >= CS; ++tries) {
+    const int pblocks = (int)((n + s - 1) / s);
+    // the largest co-resident grid (multiple of cs) of the resident chain; false if it does not fit
+    auto plan_res = [&](int cs, int* P_out, int* nch_out) -> bool {
+      int Pc = std::max(cs, std::min(num_sms(), (nrc32 + cs - 1) / cs * cs) / cs * cs);
+      void* rk = res_kernel(cs);
+      if (Pc > 148 || cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess)
+        return false;
+      for (int tries = 0; tries < 4 && Pc >= cs; ++tries) {
         const int nch = (nrc32 + Pc - 1) / Pc;
-        const size_t rs = res_smem(CS, s, nch, (int)((n + s - 1) / s));
+        const size_t rs = res_smem(cs, s, nch, pblocks);
         if (rs > 226 * 1024 || cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs) != cudaSuccess)
-          break;
+          return false;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(Pc);
         cfg.blockDim = dim3(ENT);
         cfg.dynamicSmemBytes = rs;
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = CS;
+        at[0].val.clusterDim.x = cs;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
         int clusters = 0;
-        if (cudaOccupancyMaxActiveClusters(&clusters, rk, &cfg) != cudaSuccess) break;
-        if (clusters * CS >= Pc) {
-          c->variant = 1;
-          c->cs = CS;
-          c->RC = 32;
-          c->nrc = nrc32;
-          c->nch = nch;
-          c->P = Pc;
-          break;
+        if (cudaOccupancyMaxActiveClusters(&clusters, rk, &cfg) != cudaSuccess) return false;
+        if (clusters * cs >= Pc) {
+          *P_out = Pc;
+          *nch_out = nch;
+          return true;
         }
-        Pc = clusters * CS;
+        Pc = clusters * cs;
+      }
+      return false;
+    };
+    if (want == 1 && s <= ENT) {
+      // cluster size: RAC_EN_CS if set; otherwise 8 (fewer partials to reduce per
+      // block) unless it would give CTAs more row chunks than pairs do.
+      const char* envcs = getenv("RAC_EN_CS");
+      int P2 = 0, n2 = 0, P8 = 0, n8 = 0, Pe = 0, ne = 0;
+      int pick = 0;
+      if (envcs) {
+        const int e = atoi(envcs);
+        const int cs = (e >= 8) ? 8 : (e >= 4 ? 4 : 2);
+        if (plan_res(cs, &Pe, &ne)) pick = cs;
+      } else {
+        const bool ok2 = plan_res(2, &P2, &n2);
+        const bool ok8 = plan_res(8, &P8, &n8);
+        if (ok8 && (!ok2 || n8 <= n2)) { pick = 8; Pe = P8; ne = n8; }
+        else if (ok2) { pick = 2; Pe = P2; ne = n2; }
+      }
+      if (pick) {
+        c->variant = 1;
+        c->cs = pick;
+        c->RC = 32;
+        c->nrc = nrc32;
+        c->nch = ne;
+        c->P = Pe;
+        cudaFuncSetAttribute(res_kernel(pick), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)res_smem(pick, s, ne, pblocks));
       }
       cudaGetLastError();
     }
@@ -718,7 +741,7 @@ extern "C" int rac_en_set_timing(rac_en_ctx* c, int32_t enable) {
   if (!c) return set_error(RAC_ERR_ARG, "rac_en_set_timing: null context");
   c->timing = enable != 0;
   if (enable >= 2 && !c->trace) {
-    int rc = dalloc(c, &c->trace, 8 + 12 * (size_t)c->p);
+    int rc = dalloc(c, &c->trace, 8 + 16 * (size_t)c->p);
     if (rc) return rc;
   }
   if (enable < 2) c->trace = nullptr;
@@ -740,7 +763,7 @@ extern "C" int rac_en_trace(rac_en_ctx* c, int64_t* host, int32_t capacity) {
   using namespace rac;
   clear_error();
   if (!c || !host || !c->trace) return set_error(RAC_ERR_ARG, "rac_en_trace: tracing not enabled");
-  int k = std::min<int>(capacity, 8 + 12 * c->p);
+  int k = std::min<int>(capacity, 8 + 16 * c->p);
   return check_cuda(cudaMemcpy(host, c->trace, k * sizeof(int64_t), cudaMemcpyDeviceToHost), "trace copy");
 }
 

@@ -47,11 +47,19 @@ struct ResSmem {
   int* sIdx;       // [p*s]              this sweep's block table
 };
 
+// row-phase reductions; for CS >= 4 also the staged [s][C] cluster partials
+template <int CS>
+__host__ __device__ size_t res_red_doubles(int s, int nch) {
+  const size_t rp = 2 * (size_t)nch * (ENT / 32) * RES_RC;
+  const size_t st = (CS >= 4) ? (size_t)s * (148 / CS + 1) : 0;
+  return rp > st ? rp : st;
+}
+
 template <int CS>
 __host__ __device__ size_t res_smem_bytes(int s, int nch, int p) {
   const size_t sl = (s + CS - 1) / CS;
   return (2 * (size_t)s * (nch * RES_RC + RES_PAD) + sl * s + 12 * (size_t)s + (size_t)nch * RES_RC +
-          2 * (size_t)nch * (ENT / 32) * RES_RC + (size_t)nch * RES_RC + 6) *
+          res_red_doubles<CS>(s, nch) + (size_t)nch * RES_RC + 6) *
              sizeof(double) +
          ((size_t)s + (size_t)p * s) * sizeof(int);
 }
@@ -70,7 +78,7 @@ __device__ __forceinline__ ResSmem carve_res(double* base, int s, int nch) {
   w.sPart = p; p += s;
   w.sSlice = p; p += 4 * s;
   w.sR = p; p += (size_t)nch * RES_RC;
-  w.red = p; p += 2 * (size_t)nch * (ENT / 32) * RES_RC;
+  w.red = p; p += res_red_doubles<CS>(s, nch);
   p = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));  // double2 loads
   w.sT = p; p += (size_t)nch * RES_RC;
   w.bars = reinterpret_cast<uint64_t*>(p); p += 4;
@@ -320,7 +328,26 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     grid_barrier(a.bar, target, P);
     if (tr) a.trace[tp++] = gtimer();
     if (t > 0) commit();
-    // ---- full rhs: one warp per entry, 4 entries per round
+    if (tr) a.trace[tp++] = gtimer();
+    // ---- full rhs
+    if constexpr (CS >= 4) {
+      // s*C partials (<= 19 per thread for s <= 256) staged into smem in one round
+      // trip, then entry j sums its C partials in cluster order
+      const int tot = s * C;
+      for (int f0 = tid; f0 < tot; f0 += 8 * ENT) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int f = f0 + u * ENT;
+          v[u] = (f < tot) ? ldcg(gpart + f) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int f = f0 + u * ENT;
+          if (f < tot) w.red[f] = v[u];
+        }
+      }
+    } else
     for (int jb = warp; jb < s; jb += 4 * nw) {
       double v[4][RES_QL];
 #pragma unroll
@@ -342,10 +369,19 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
         if (lane == 0 && j < s) w.red[j] = acc;
       }
     }
+    if (tr) a.trace[tp++] = gtimer();
     wait_solve();
+    if (tr) a.trace[tp++] = gtimer();
     __syncthreads();
     for (int j = tid; j < s; j += ENT) {
-      const double acc = w.red[j];
+      double acc;
+      if constexpr (CS >= 4) {
+        const double* pj = w.red + (size_t)j * C;
+        acc = pj[0];
+        for (int q = 1; q < C; ++q) acc += pj[q];
+      } else {
+        acc = w.red[j];
+      }
       double rhs = 0.0;
       if (bi[j] >= 0) {
         const double cross = acc / m;

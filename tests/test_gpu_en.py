@@ -191,3 +191,38 @@ def test_identity_design_recovers_targets(lib):
     model = en.fit(np.eye(n), y, en.ElasticNetSpec(lam=0.0, alpha=1.0, gamma=1.0, block_size=3,
                                                    iters=300, seed=1))
     np.testing.assert_allclose(model.beta, y, atol=1e-10)
+
+
+@pytest.mark.parametrize("env", [{}, {"RAC_EN_PIPE": "0"}, {"RAC_EN_CS": "4"}, {"RAC_EN_CS": "8"},
+                                 {"RAC_EN_VARIANT": "0"}])
+def test_chain_variants_match_oracle(lib, monkeypatch, env):
+    """Every chain variant (sweep pipeline on/off, cluster sizes 2/4/8, streaming chain)
+    on a shape with several 32-row chunks per CTA, batched sweeps (no per-sweep hook)."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import elastic_net as en
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(31)
+    m, n, s = 6000, 300, 60
+    X = rng.standard_normal((m, n))
+    y = X[:, :10] @ rng.standard_normal(10) + 0.1 * rng.standard_normal(m)
+    kw = dict(lam=0.02, alpha=0.7, gamma=1.0, block_size=s, iters=25, seed=5)
+    ref = ro.en_fit(X, y, mode="rac", **kw)
+    got = en.fit(X, y, en.ElasticNetSpec(**kw))
+    assert rel(got.beta, ref["beta"]) <= ITER_TOL
+    assert rel(got.z, ref["z"]) <= ITER_TOL
+    assert rel(got.xi, ref["xi"]) <= ITER_TOL
+
+
+def test_pipeline_bitwise_equals_serial(lib, monkeypatch):
+    """The cross-stream sweep pipeline runs the same kernels on the same data: bit-identical."""
+    from paper_1907_01995_b200 import elastic_net as en
+    rng = np.random.default_rng(32)
+    X = rng.standard_normal((3000, 400))
+    y = rng.standard_normal(3000)
+    spec = en.ElasticNetSpec(lam=0.05, alpha=0.9, block_size=40, iters=30, seed=9)
+    a = en.fit(X, y, spec)
+    monkeypatch.setenv("RAC_EN_PIPE", "0")
+    b = en.fit(X, y, spec)
+    assert np.array_equal(a.beta, b.beta) and np.array_equal(a.z, b.z) and np.array_equal(a.xi, b.xi)
+    assert np.array_equal(a.residual_history, b.residual_history)

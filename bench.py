@@ -13,6 +13,7 @@ sequential Gauss-Seidel chain, so N>1 runs N independent replicas (one per GPU,
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import math
 import os
@@ -133,6 +134,50 @@ def en_flops_bytes(m, n, s):
     return float(m) * n * (s + 1), 8.0 * m * n
 
 
+def traffic_table() -> dict:
+    """DRAM bytes per launch from the committed ncu --set full captures (profiles/*traffic*.json)."""
+    out = {}
+    for path in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                              "*traffic*.json"))):
+        try:
+            with open(path) as f:
+                out.update(json.load(f))
+        except (OSError, ValueError):
+            pass
+    return out
+
+
+def en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, workload) -> dict:
+    """Roofline entry for the dominant stage of an EN sweep (per-unit figures: SURVEY.md §8(d))."""
+    dom = max(stages, key=stages.get)
+    sec = stages[dom] * 1e-3
+    if dom == "chain":
+        if gram_mode == "covariance":
+            kern = "en_cov_kernel"
+            byts = 8.0 * n * n + 8.0 * p * s * s
+            desc = "rows of G read once (8 n^2) + block inverses (8 p s^2) per launch"
+        else:
+            kern = "en_chain_res_kernel" if variant == "resident-cluster" else "en_chain_kernel"
+            byts = 8.0 * m * n + 8.0 * p * s * s
+            desc = "D read once (8 m n; a block's second use hits L2) + block inverses (8 p s^2) per launch"
+        achieved = byts / sec / 1e9
+        roof = {"kernel": kern, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "algorithmic": desc}
+    elif dom == "gram":
+        achieved = float(m) * n * (s + 1) / sec / 1e12
+        roof = {"kernel": "gram_kernel", "bound": "tensor", "achieved": achieved, "peak": fp64,
+                "unit": "TFLOP/s", "frac": achieved / fp64,
+                "algorithmic": "m*n*(s+1) flop per launch (symmetric SYRK of all p blocks)"}
+    else:
+        achieved = 2.0 * p * float(s) ** 3 / sec / 1e12
+        roof = {"kernel": "factor_kernel" if s <= 236 else "large_*_kernel (blocked inverse)",
+                "bound": "tensor", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+                "frac": achieved / fp64, "algorithmic": "2 s^3 flop per block inverse x p blocks per sweep"}
+    roof["stage"] = dom
+    roof["traffic"] = traffic_table().get(f"{workload}:{roof['kernel']}")
+    return roof
+
+
 def fp64_peak_tflops(torch) -> float:
     """Measured cuBLAS DGEMM (8192^3 fp64) on this device, best of 5 — FP64 roofline denominator."""
     a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
@@ -216,13 +261,16 @@ def run_b200_en(args, world, rank, local):
     m, n = case.X.shape
     s = min(case.block_size, n)
     p = -(-n // s)
-    flops, bytes_ = en_flops_bytes(m, n, s)
+
 
     # ---------------- device-resident throughput (fixed sweeps, every sweep does full work)
+    K, W = args.steps, args.warmup
+    gram_mode = args.gram if args.gram != "auto" else en.choose_gram_mode(m, n, s, K)
     solver = en.EnSolver(m, n, s, Mode.RAC, case.lam, case.alpha, case.gamma, device=local)
+    if gram_mode == "covariance":
+        solver.set_gram_mode("covariance")
     solver.set_data(case.X, case.y)
     rng = np.random.default_rng(case.seed)
-    K, W = args.steps, args.warmup
     perms = _device.PermutationFeeder(rng, n, dev).draw(W + K)
     torch.cuda.synchronize()
     solver.run(perms[:W], None)
@@ -235,6 +283,8 @@ def run_b200_en(args, world, rank, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = solver.lib.rac_launch_count()
     e0.record()
+    if gram_mode == "covariance":
+        solver.set_gram_mode("covariance")   # G = X'X/m is re-formed INSIDE the timed region
     solver.run(perms[W:W + K], None)
     e1.record()
     launches = solver.lib.rac_launch_count() - l0
@@ -266,15 +316,19 @@ def run_b200_en(args, world, rank, local):
                "delta+cluster_sync", "tile_wait",
                "row_pass1", "row_sync1", "row_pass2", "row_pass3", "issue_next")
               if info[0] == 1 else
-              ("barrier1", "S1_reduce", "barrier2", "S2_solve", "barrier3", "row_phase"))
+              ("barrier1", "S1_reduce", "barrier2", "S2_solve", "barrier3", "row_phase") if info[0] == 0 else
+              ("phase_a_q_update", "cluster_sync1", "prefetch_wait", "v_gather", "delta_commit", "cluster_sync2",
+               "delta_gather"))
     nl = len(labels)
-    pro = 5 if info[0] == 1 else 2       # stamps before the first block (start, [row passes], R0)
-    tv = np.array(tbuf[:pro + nl * p], dtype=np.float64) / 1e3   # us
-    ph = np.diff(tv[pro - 1:]).reshape(p, nl) if p > 0 else np.zeros((0, nl))
-    chain_trace = {"variant": "resident-cluster" if info[0] == 1 else "streaming",
-                   "ctas": int(info[1]), "rows_per_chunk": int(info[2]), "chunks_per_cta": int(info[3]),
-                   "first_row_phase_us": float(tv[pro - 1] - tv[0]),
-                   "per_block_us": {k: float(v) for k, v in zip(labels, ph.mean(axis=0))}}
+    variant = {0: "streaming", 1: "resident-cluster", 2: "covariance-cluster"}[int(info[0])]
+    chain_trace = {"variant": variant, "ctas": int(info[1]), "gram_mode": gram_mode}
+    if nl:
+        pro = {0: 2, 1: 5, 2: 1}[int(info[0])]   # stamps before the first block
+        tv = np.array(tbuf[:pro + nl * p], dtype=np.float64) / 1e3   # us
+        ph = np.diff(tv[pro - 1:]).reshape(p, nl) if p > 0 else np.zeros((0, nl))
+        chain_trace.update({"rows_per_chunk": int(info[2]), "chunks_per_cta": int(info[3]),
+                            "first_phase_us": float(tv[pro - 1] - tv[0]),
+                            "per_block_us": {k: float(v) for k, v in zip(labels, ph.mean(axis=0))}})
     lib.rac_en_set_timing(solver.h, 0)
     solver.close()
     del perms, more
@@ -283,6 +337,9 @@ def run_b200_en(args, world, rank, local):
     ttt = None
     if case.tol is not None:
         sol2 = en.EnSolver(m, n, s, Mode.RAC, case.lam, case.alpha, case.gamma, device=local)
+        if args.gram == "covariance" or (args.gram == "auto" and
+                                         en.choose_gram_mode(m, n, s, case.iters) == "covariance"):
+            sol2.set_gram_mode("covariance")
         sol2.set_data(case.X, case.y)
         rng2 = np.random.default_rng(case.seed)
         feeder = _device.PermutationFeeder(rng2, n, dev)
@@ -320,17 +377,7 @@ def run_b200_en(args, world, rank, local):
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
     fp64 = fp64_peak_tflops(torch)
-    dom = max(stages, key=stages.get)
-    if dom == "chain":
-        achieved = 2.0 * bytes_ / (stages["chain"] * 1e-3) / 1e9
-        roof = {"kernel": "en_chain_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm,
-                "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-                "algorithmic": "2 passes over D (8*m*n bytes each) per launch"}
-    else:
-        achieved = flops / (stages["gram"] * 1e-3) / 1e12
-        roof = {"kernel": "gram_kernel", "bound": "tensor", "achieved": achieved, "peak": fp64,
-                "unit": "TFLOP/s", "frac": achieved / fp64, "traffic": None,
-                "algorithmic": "m*n*(s+1) flop per launch (symmetric SYRK of all p blocks)"}
+    roof = en_roofline(stages, m, n, s, p, gram_mode, chain_trace["variant"], hbm, fp64, case.name)
 
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -346,7 +393,8 @@ def run_b200_en(args, world, rank, local):
         "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) seed-0 recipe)",
         "config": {"workload": case.name, "m": m, "n": n, "block_size": s, "blocks": p,
-                   "mode": "rac", "l2": "inputs larger than L2 (D = %.0f MB)" % (8 * m * n / 1e6)
+                   "mode": "rac", "gram_mode": gram_mode,
+                   "l2": "inputs larger than L2 (D = %.0f MB)" % (8 * m * n / 1e6)
                    if 8 * m * n > 126e6 else "D fits in L2 (no flush)",
                    "parallelism": f"replicas x{world}"},
         "stage_ms_per_sweep": stages,
@@ -462,6 +510,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--gram", default="auto", choices=["auto", "blocks", "covariance"],
+                    help="EN block systems: per-sweep block Grams or covariance mode (G formed in the timed region)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)

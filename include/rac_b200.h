@@ -45,6 +45,10 @@ extern "C" {
 #define RAC_KERNEL_LINEAR 0
 #define RAC_KERNEL_GAUSSIAN 1
 
+/* how rac_en forms the block systems and the coupling term */
+#define RAC_GRAM_BLOCKS 0     /* per sweep: X_b'X_b of every block from X (the reference's recompute) */
+#define RAC_GRAM_COVARIANCE 1 /* once: G = X'X/m (n x n); blocks gather G, chain updates q = G beta */
+
 /* design-matrix layouts accepted by rac_en_set_data */
 #define RAC_LAYOUT_ROW_MAJOR 0 /* numpy C order, X[i*n + j]                                */
 #define RAC_LAYOUT_COL_MAJOR 1 /* Fortran order with leading dim m, X[i + j*m]             */
@@ -96,6 +100,12 @@ int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t block_size, in
 int rac_en_set_data(rac_en_ctx* ctx, const double* X, int32_t layout, const double* y);
 /* RP mode only: the fixed partition from one permutation of n
  * (elastic_net.py:187-189); block systems are factored once. */
+/* Select RAC_GRAM_BLOCKS (default) or RAC_GRAM_COVARIANCE.  Covariance mode
+ * forms G = X'X/m on the next rac_en_run / rac_en_set_partition (n x n doubles
+ * of HBM) and runs the chain on G in one thread-block cluster; selecting it
+ * again re-forms G.  RAC_ERR_UNSUPPORTED if the single-cluster chain does not
+ * fit (large n or s).  In rp mode the partition must be set again afterwards. */
+int rac_en_set_gram_mode(rac_en_ctx* ctx, int32_t mode);
 int rac_en_set_partition(rac_en_ctx* ctx, const int64_t* perm);
 /* Enqueue `count` sweeps.  RAC: `perms` = count permutations of n.  RP: count
  * permutations of p (block visit orders, elastic_net.py:197-198).  tol < 0

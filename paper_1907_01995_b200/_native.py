@@ -19,6 +19,7 @@ MODE_RAC, MODE_RP, MODE_CYCLIC = 0, 1, 2
 STATUS_MAX_ITERS, STATUS_CONVERGED, STATUS_DIVERGED = 0, 1, 2
 KERNEL_LINEAR, KERNEL_GAUSSIAN = 0, 1
 LAYOUT_ROW_MAJOR, LAYOUT_COL_MAJOR = 0, 1
+GRAM_BLOCKS, GRAM_COVARIANCE = 0, 1
 
 _p = C.c_void_p
 _i32, _i64, _f64, _sz = C.c_int32, C.c_int64, C.c_double, C.c_size_t
@@ -37,6 +38,7 @@ SIGNATURES = {
     "rac_z_prox": (_i32, [_p, _p, _i64, _f64, _f64, _f64, _p, _p]),
     "rac_en_create": (_i32, [C.POINTER(_p), _i64, _i64, _i32, _i32, _f64, _f64, _f64, _p]),
     "rac_en_set_data": (_i32, [_p, _p, _i32, _p]),
+    "rac_en_set_gram_mode": (_i32, [_p, _i32]),
     "rac_en_set_partition": (_i32, [_p, _p]),
     "rac_en_run": (_i32, [_p, _p, _i32, _f64]),
     "rac_en_progress": (_i32, [_p, _pi32, _pi32, _pf64, _pi32]),

@@ -31,7 +31,6 @@ namespace rac {
 
 constexpr int ENT = RP_THREADS;   // threads per chain CTA
 constexpr int EN_QMAX = RP_QMAX;   // block_size <= EN_QMAX * ENT
-constexpr int kResCS = 2;          // default cluster size of the resident chain (148 SMs = 74 pairs)
 
 struct EnChainArgs {
   const double* Xc;
@@ -173,6 +172,7 @@ __global__ void __launch_bounds__(ENT) en_chain_kernel(EnChainArgs a) {
 }  // namespace rac
 
 #include "en_res.cuh"
+#include "en_cov.cuh"
 
 namespace rac {
 
@@ -258,6 +258,12 @@ struct rac_en_ctx {
   int32_t* idx_b[2] = {nullptr, nullptr};
   double* inv_b[2] = {nullptr, nullptr};
   int32_t* info_b[2] = {nullptr, nullptr};
+  // covariance mode (en_cov.cuh): G = X'X/m formed once, chain on G in one cluster
+  int gram_mode = 0;          // 0: per-sweep block Grams from X; 1: covariance
+  bool have_G = false;
+  int cov_k = 16;
+  double *G = nullptr, *q = nullptr, *cwsum = nullptr, *cwmax = nullptr;
+  int32_t* G_ids = nullptr;   // 0..n-1 (the single "block" of the full Gram)
   // optional per-stage CUDA-event timing: [assembly, gram, factor, chain]
   bool timing = false;
   std::vector<cudaEvent_t> events;  // 5 per timed sweep
@@ -311,13 +317,72 @@ int en_grow_history(rac_en_ctx* c, int need) {
   return RAC_OK;
 }
 
+void* cov_kernel(int k) { return k == 16 ? (void*)rac::en_cov_kernel<16> : (void*)rac::en_cov_kernel<8>; }
+
+size_t cov_smem(int k, int s, int64_t n, int p) {
+  return k == 16 ? rac::cov_smem_bytes<16>(s, n, p) : rac::cov_smem_bytes<8>(s, n, p);
+}
+
+// largest cluster size (16, else 8) whose single-cluster chain fits; 0 if none
+int cov_plan(int s, int64_t n, int p) {
+  for (int k : {16, 8}) {
+    const size_t smem = cov_smem(k, s, n, p);
+    if (smem > 226 * 1024) continue;
+    void* kf = cov_kernel(k);
+    if (cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        (k > 8 && cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)) {
+      cudaGetLastError();
+      continue;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(k);
+    cfg.blockDim = dim3(rac::COVT);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = k;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, kf, &cfg) == cudaSuccess && clusters >= 1) return k;
+    cudaGetLastError();
+  }
+  return 0;
+}
+
+// G = X'X/m (full, row-major) on the FP64 tensor cores, one K split (each tile
+// pair writes its block and the mirror), then q = G beta
+int en_compute_G(rac_en_ctx* c, cudaStream_t st) {
+  using namespace rac;
+  const int64_t n = c->n;
+  GramPlan pl = plan_gram(c->m, (int)n, 1);
+  pl.splits = 1;
+  pl.chunk = (c->m + 31) / 32 * 32;
+  int rc = launch_gram(c->Xc, c->ld, c->m, c->G_ids, nullptr, (int)n, 1, c->G, pl, st, nullptr, (double)c->m);
+  if (rc) return rc;
+  rc = launch_gemv_rows(c->G, n, n, c->beta, c->q, st);
+  if (rc) return rc;
+  c->have_G = true;
+  return check_launch("covariance Gram");
+}
+
 int en_factor(rac_en_ctx* c, cudaStream_t st) {
   using namespace rac;
   SysArgs a{};
-  a.ws = c->gram_ws;
-  a.splits = c->gp.splits;
-  a.div = (double)c->m;
-  a.mul = 1.0;
+  if (c->gram_mode == 1) {
+    a.H = c->G;          // sys_b = G[b, b] + gamma I (padding of a short last block -> identity)
+    a.ldh = c->n;
+    a.idx = c->idx;
+    a.div = 1.0;
+    a.mul = 1.0;
+  } else {
+    a.ws = c->gram_ws;
+    a.splits = c->gp.splits;
+    a.div = (double)c->m;
+    a.mul = 1.0;
+  }
   a.shift = c->gamma;
   a.s = c->s;
   a.inv = c->inv;
@@ -328,14 +393,61 @@ int en_factor(rac_en_ctx* c, cudaStream_t st) {
 }
 
 int en_block_systems(rac_en_ctx* c) {
-  int rc = rac::launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->st,
-                            c->ctrl);
-  if (rc) return rc;
+  if (c->gram_mode != 1) {
+    int rc = rac::launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->st,
+                              c->ctrl);
+    if (rc) return rc;
+  }
   return en_factor(c, c->st);
+}
+
+int en_chain_cov(rac_en_ctx* c, double tol, cudaStream_t st) {
+  using namespace rac;
+  EnCovArgs a{};
+  a.G = c->G;
+  a.n = c->n;
+  a.s = c->s;
+  a.p = c->p;
+  a.idx = c->idx;
+  a.order = (c->mode == RAC_MODE_RP) ? c->order : nullptr;
+  a.inv = c->inv;
+  a.info = c->info;
+  a.c = c->c;
+  a.beta = c->beta;
+  a.z = c->z;
+  a.xi = c->xi;
+  a.q = c->q;
+  a.wsum = c->cwsum;
+  a.wmax = c->cwmax;
+  a.ctrl = c->ctrl;
+  a.gamma = c->gamma;
+  a.thr = c->lam * c->alpha;
+  a.den = (1.0 - c->alpha) * c->lam + c->gamma;
+  a.tol = tol;
+  a.sweep = c->sweeps;
+  a.hist_p = c->hist_p;
+  a.hist_d = c->hist_d;
+  a.trace = c->trace;
+  void* args[] = {&a};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(c->cov_k);
+  cfg.blockDim = dim3(COVT);
+  cfg.dynamicSmemBytes = cov_smem(c->cov_k, c->s, c->n, c->p);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = c->cov_k;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  note_launch();
+  return check_cuda(cudaLaunchKernelExC(&cfg, cov_kernel(c->cov_k), args), "en_cov (cluster launch)");
 }
 
 int en_chain(rac_en_ctx* c, double tol, cudaStream_t st) {
   using namespace rac;
+  if (c->gram_mode == 1) return en_chain_cov(c, tol, st);
   cudaMemsetAsync(c->bar, 0, sizeof(unsigned), st);
   EnChainArgs a{};
   a.Xc = c->Xc;
@@ -605,13 +717,41 @@ extern "C" int rac_en_set_data(rac_en_ctx* c, const double* X, int32_t layout, c
   return check_launch("rac_en_set_data");
 }
 
+extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {
+  using namespace rac;
+  clear_error();
+  if (!c || (mode != RAC_GRAM_BLOCKS && mode != RAC_GRAM_COVARIANCE))
+    return set_error(RAC_ERR_ARG, "rac_en_set_gram_mode: bad arguments");
+  c->have_G = false;
+  c->have_partition = false;   // RP block systems must be re-formed
+  if (mode == RAC_GRAM_BLOCKS) {
+    c->gram_mode = 0;
+    return RAC_OK;
+  }
+  const int k = cov_plan(c->s, c->n, c->p);
+  if (!k) return set_error(RAC_ERR_UNSUPPORTED, "covariance mode does not fit (n=%lld, s=%d)", (long long)c->n, c->s);
+  int rc = RAC_OK;
+  if (!c->G) {
+    if ((rc = dalloc(c, &c->G, (size_t)c->n * c->n)) || (rc = dalloc(c, &c->q, c->n)) ||
+        (rc = dalloc(c, &c->cwsum, 16)) || (rc = dalloc(c, &c->cwmax, 16)) || (rc = dalloc(c, &c->G_ids, c->n)))
+      return rc;
+    iota_kernel<<<(int)std::min<int64_t>((c->n + 255) / 256, 4096), 256, 0, c->st>>>(c->G_ids, c->n);
+    note_launch();
+  }
+  c->cov_k = k;
+  c->gram_mode = 1;
+  return RAC_OK;
+}
+
 extern "C" int rac_en_set_partition(rac_en_ctx* c, const int64_t* perm) {
   using namespace rac;
   clear_error();
   if (!c || !perm) return set_error(RAC_ERR_ARG, "rac_en_set_partition: null pointer");
   if (c->mode != RAC_MODE_RP) return set_error(RAC_ERR_ARG, "rac_en_set_partition: mode is not rp");
   if (!c->have_data) return set_error(RAC_ERR_ARG, "rac_en_set_partition: call rac_en_set_data first");
-  int rc = launch_chunk_sort(perm, c->n, c->s, 1, c->idx, c->st);
+  int rc = RAC_OK;
+  if (c->gram_mode == 1 && !c->have_G && (rc = en_compute_G(c, c->st))) return rc;
+  rc = launch_chunk_sort(perm, c->n, c->s, 1, c->idx, c->st);
   if (rc) return rc;
   rc = en_block_systems(c);
   if (rc) return rc;
@@ -628,6 +768,7 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
     return set_error(RAC_ERR_ARG, "rac_en_run: rp mode needs rac_en_set_partition");
   int rc = en_grow_history(c, c->sweeps + count);
   if (rc) return rc;
+  if (c->gram_mode == 1 && !c->have_G && count > 0 && (rc = en_compute_G(c, c->st))) return rc;
   if (c->pipe && !c->timing && count > 0) {
     // prep(k+1) on sprep overlaps chain(k) on schain; prep(k) may only overwrite the
     // buffers of sweep k-2 once that chain is done.
@@ -641,7 +782,8 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
       c->inv = c->inv_b[j];
       c->info = c->info_b[j];
       if ((rc = launch_chunk_sort(perms + (int64_t)k * c->n, c->n, c->s, 1, c->idx, c->sprep))) return rc;
-      if ((rc = launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->sprep,
+      if (c->gram_mode != 1 &&
+          (rc = launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->sprep,
                             c->ctrl)))
         return rc;
       if ((rc = en_factor(c, c->sprep))) return rc;
@@ -666,8 +808,10 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
       rc = launch_chunk_sort(perms + (int64_t)k * c->n, c->n, c->s, 1, c->idx, c->st);
       if (rc) return rc;
       if (c->timing) cudaEventRecord(ev[1], c->st);
-      rc = launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->st, c->ctrl);
-      if (rc) return rc;
+      if (c->gram_mode != 1) {
+        rc = launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->st, c->ctrl);
+        if (rc) return rc;
+      }
       if (c->timing) cudaEventRecord(ev[2], c->st);
       rc = en_factor(c, c->st);
       if (rc) return rc;
@@ -752,8 +896,8 @@ extern "C" int rac_en_info(rac_en_ctx* c, int32_t* info4) {
   using namespace rac;
   clear_error();
   if (!c || !info4) return set_error(RAC_ERR_ARG, "rac_en_info: bad arguments");
-  info4[0] = c->variant;
-  info4[1] = c->P;
+  info4[0] = (c->gram_mode == 1) ? 2 : c->variant;
+  info4[1] = (c->gram_mode == 1) ? c->cov_k : c->P;
   info4[2] = c->RC;
   info4[3] = c->nch;
   return RAC_OK;

@@ -28,17 +28,18 @@ namespace rac {
 namespace cg = cooperative_groups;
 
 constexpr int RES_RC = 32;        // rows per chunk (one 256-byte segment per column)
-constexpr int RES_PAD = 2;        // tile column padding (doubles)
+constexpr int RES_PAD = 4;        // tile column padding (doubles): column stride = 8 banks mod 32
 
 struct ResSmem {
-  double* tiles;   // [2][s][nch*32+2]  (column segments: TMA destination)
+  double* tiles;   // [2][s][nch*32+4]  (column segments: TMA destination)
   double* ginv;    // [sl][s]            inv_b rows of this rank's slice
   double* cxz;     // [3][s]             c, xi, z at the block's indices
   double* sX;      // [2][s]             beta at a block's indices, by block parity
   double* sDel;    // [s]                full delta of the current block
   double* sRhs;    // [s]
   double* sPart;   // [s]                this CTA's partial (cluster peers read it)
-  double* sSlice;  // [4s]               delta slice | pending beta, xi, z (cluster 0)
+  double* sSlice;  // [2s]               this rank's delta | new beta (global block positions)
+  double* cm;      // [3s]               block awaiting commit: new beta, old xi, old z
   double* sR;      // [nch*32]           resident rows of r
   double* red;     // [2][nch][8 warps][32]  row-phase reductions; [s] rhs sums
   double* sT;      // [nch*32]
@@ -58,7 +59,7 @@ __host__ __device__ size_t res_red_doubles(int s, int nch) {
 template <int CS>
 __host__ __device__ size_t res_smem_bytes(int s, int nch, int p) {
   const size_t sl = (s + CS - 1) / CS;
-  return (2 * (size_t)s * (nch * RES_RC + RES_PAD) + sl * s + 12 * (size_t)s + (size_t)nch * RES_RC +
+  return (2 * (size_t)s * (nch * RES_RC + RES_PAD) + sl * s + 13 * (size_t)s + (size_t)nch * RES_RC +
           res_red_doubles<CS>(s, nch) + (size_t)nch * RES_RC + 6) *
              sizeof(double) +
          ((size_t)s + (size_t)p * s) * sizeof(int);
@@ -76,7 +77,8 @@ __device__ __forceinline__ ResSmem carve_res(double* base, int s, int nch) {
   w.sDel = p; p += s;
   w.sRhs = p; p += s;
   w.sPart = p; p += s;
-  w.sSlice = p; p += 4 * s;
+  w.sSlice = p; p += 2 * s;
+  w.cm = p; p += 3 * s;
   w.sR = p; p += (size_t)nch * RES_RC;
   w.red = p; p += res_red_doubles<CS>(s, nch);
   p = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));  // double2 loads
@@ -258,35 +260,42 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     __syncthreads();
     if (tr) a.trace[tp++] = gtimer();
     if (sn >= 0) {
-      // partial_j = sum_i T[j][i] t_i : one column per thread, 16-byte smem loads
+      // partial_j = sum_i T[j][i] t_i : two lanes per column (s <= 128) taking
+      // alternate 16-byte row pairs; combined with one shuffle
       const double* T = tile(sn);
-      const int nr = nchv * RC;
-      for (int j = tid; j < s; j += ENT) {
-        const double2* col = reinterpret_cast<const double2*>(T + (size_t)j * RCN);
-        const double2* tt = reinterpret_cast<const double2*>(w.sT);
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        for (int i = 0; i < nr / 2; i += 2) {
-          const double2 x0 = col[i], x1 = col[i + 1];
-          const double2 t0 = tt[i], t1 = tt[i + 1];
-          a0 += x0.x * t0.x;
-          a1 += x0.y * t0.y;
-          a2 += x1.x * t1.x;
-          a3 += x1.y * t1.y;
+      const int nr2 = nchv * RC / 2;
+      const int tpc = (2 * s <= ENT) ? 2 : 1;
+      const double2* tt = reinterpret_cast<const double2*>(w.sT);
+      for (int e0 = 0; e0 < s * tpc; e0 += ENT) {
+        const int e = e0 + tid;
+        const int j = e / tpc, h = e - j * tpc;
+        double v = 0.0;
+        if (j < s) {
+          const double2* col = reinterpret_cast<const double2*>(T + (size_t)j * RCN);
+          double a0 = 0.0, a1 = 0.0;
+          for (int k = h; k < nr2; k += tpc) {
+            const double2 x = col[k], y = tt[k];
+            a0 += x.x * y.x;
+            a1 += x.y * y.y;
+          }
+          v = a0 + a1;
         }
-        w.sPart[j] = (a0 + a1) + (a2 + a3);
+        if (tpc == 2) v += __shfl_xor_sync(0xffffffffu, v, 1);
+        if (j < s && h == 0) w.sPart[j] = v;
       }
     }
   };
 
   double my_sum = 0.0, my_max = 0.0;
-  auto commit = [&]() {
-    if (cid != 0) return;
-    for (int q = tid; q < j1 - j0; q += ENT) {
-      const int g = w.pend[q];
+  // beta/z/xi of the block whose new values sit in cm; coordinate j of the
+  // block is written by CTA j mod P
+  auto commit = [&](const int* bip) {
+    for (int j = (int)blockIdx.x + tid * P; j < s; j += ENT * P) {
+      const int g = bip[j];
       if (g < 0) continue;
-      const double bn = w.sSlice[s + q];
+      const double bn = w.cm[j];
       a.beta[g] = bn;
-      const double x0 = w.sSlice[2 * s + q], zo = w.sSlice[3 * s + q];
+      const double x0 = w.cm[s + j], zo = w.cm[2 * s + j];
       const double av = sub(x0, mul(gamma, bn));
       const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
       a.z[g] = zn;
@@ -327,7 +336,7 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
     if (tr) a.trace[tp++] = gtimer();
     grid_barrier(a.bar, target, P);
     if (tr) a.trace[tp++] = gtimer();
-    if (t > 0) commit();
+    if (t > 0) commit(bidx(blk(t - 1)));
     if (tr) a.trace[tp++] = gtimer();
     // ---- full rhs
     if constexpr (CS >= 4) {
@@ -408,16 +417,19 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
         if (l8 == 0 && r0 + sub8 < rows) {
           const int g = bi[i];
           w.sSlice[i] = (g >= 0) ? acc - xb[i] : 0.0;
-          w.pend[i - j0] = g;
-          w.sSlice[s + (i - j0)] = acc;
-          w.sSlice[2 * s + (i - j0)] = w.cxz[s + i];       // xi, z of block t before its update
-          w.sSlice[3 * s + (i - j0)] = w.cxz[2 * s + i];
+          w.sSlice[s + i] = acc;
         }
       }
     }
     cl.sync();
     if (tr) a.trace[tp++] = gtimer();
-    for (int i = tid; i < s; i += ENT) w.sDel[i] = cl.map_shared_rank(w.sSlice, i / sl)[i];
+    for (int i = tid; i < s; i += ENT) {
+      const double* peer = cl.map_shared_rank(w.sSlice, i / sl);
+      w.sDel[i] = peer[i];
+      w.cm[i] = peer[s + i];            // new beta
+      w.cm[s + i] = w.cxz[s + i];       // xi, z of block t before its update
+      w.cm[2 * s + i] = w.cxz[2 * s + i];
+    }
     // ---- row phase (tile of b resident, tile + beta of the next block prefetched)
     const bool more = t + 1 < a.p;
     if (more) {
@@ -442,7 +454,7 @@ __global__ void __launch_bounds__(ENT) en_chain_res_kernel(EnChainArgs a, int nc
       if (i0 + i < a.m) a.r[i0 + i] = w.sR[k * RC + i];
   }
   __syncthreads();
-  commit();   // last block: nobody reads its coordinates any more
+  commit(bidx(blk(a.p - 1)));   // last block: nobody reads its coordinates any more
   my_sum = warp_sum(my_sum);
   my_max = warp_max(my_max);
   if (lane == 0) {

@@ -38,14 +38,15 @@ __device__ __forceinline__ int ldcg(const int* p) { return __ldcg(p); }
 // every CTA keeps its own running target.
 __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& target,
                                              unsigned nblocks) {
+  // bar.sync orders the CTA's writes before thread 0's release (release is
+  // cumulative); the acquire load that sees the final count orders everything
+  // after it, and the second bar.sync extends that to the whole CTA.
   __syncthreads();
   if (threadIdx.x == 0) {
     target += nblocks;
-    __threadfence();
     red_release_add_u32(counter, 1u);
     while (ld_acquire_u32(counter) < target) {
     }
-    __threadfence();
   }
   __syncthreads();
 }

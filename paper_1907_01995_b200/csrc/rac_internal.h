@@ -39,7 +39,9 @@ size_t gram_ws_bytes(int64_t len, int s, int p);
 // ws receives `splits` partial Grams per block ([p][splits][s][s], lower part valid)
 int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx, const int32_t* blk_list,
                 int s, int p, double* ws, const GramPlan& plan, cudaStream_t st,
-                const int32_t* done);
+                const int32_t* done, double sym_div = 0.0);
+// sym_div > 0 (requires plan.splits == 1): ws receives the FULL symmetric s x s
+// matrix divided by sym_div (the covariance G = X'X/m)
 // K3: assemble block systems, Cholesky, explicit inverse.
 struct SysArgs {
   const double* ws;   // [p][splits][s][s] partial Grams (lower), may be null
@@ -68,6 +70,8 @@ constexpr int FACTOR_INVERSE = 0;
 constexpr int FACTOR_CHOL = 1;
 int launch_chol_system(const SysArgs& a, int p, cudaStream_t st);
 size_t chol_scratch_bytes(int s, int p);
+
+__global__ void iota_kernel(int32_t* v, int64_t n);
 
 // row-major X (m x n) -> column-major (ld x n), rows m..ld-1 zero
 int launch_transpose_pad(const double* X, int64_t m, int64_t n, int64_t ld, double* Xc, cudaStream_t st);

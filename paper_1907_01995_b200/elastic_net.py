@@ -151,6 +151,15 @@ class EnSolver:
             float(lam), float(alpha), float(gamma), self.stream))
         self.h = h
         self._keep = []
+        self.gram_mode = "blocks"
+
+    def set_gram_mode(self, mode: str) -> None:
+        """'blocks': per-sweep X_b'X_b from X (the reference's own recompute);
+        'covariance': G = X'X/m once, chain on G (RAC_GRAM_COVARIANCE).
+        Selecting 'covariance' again re-forms G on the next run."""
+        code = {"blocks": _native.GRAM_BLOCKS, "covariance": _native.GRAM_COVARIANCE}[mode]
+        _native.check(self.lib.rac_en_set_gram_mode(self.h, code))
+        self.gram_mode = mode
 
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:
@@ -212,13 +221,29 @@ class EnSolver:
         return hp[:count], hd[:count]
 
 
+COV_MAX_N = 20000
+
+
+def choose_gram_mode(m: int, n: int, block_size: int, iters: int) -> str:
+    """Covariance mode pays when G (n x n) is small next to X and the fit runs
+    enough sweeps to amortise forming it: m n^2 / 2 flops once versus
+    m n (s + 1) per sweep for the block Grams, i.e. iters >~ p / 2."""
+    s = max(1, min(int(block_size), n))
+    p = -(-n // s)
+    if n > COV_MAX_N or n > 2 * m:
+        return "blocks"
+    return "covariance" if iters >= max(2, (p + 1) // 2) else "blocks"
+
+
 def fit(X: Matrix, y: np.ndarray, spec: ElasticNetSpec, *, sweep_hook=None,
-        batch: int = 16, device: int = 0) -> ElasticNetModel:
+        batch: int = 16, device: int = 0, gram_mode: str = "auto") -> ElasticNetModel:
     """Randomized block-sweep fit of the elastic-net objective (elastic_net.py:150-232).
 
     Same arguments, results and errors as the reference.  `sweep_hook(k, beta,
     z, xi)` (optional, not in the reference) observes every sweep; it forces a
-    device->host copy per sweep and is meant for parity capture.
+    device->host copy per sweep and is meant for parity capture.  `gram_mode`
+    (optional, not in the reference): "blocks", "covariance" or "auto"
+    (choose_gram_mode); both give the reference's iterates to rounding.
     """
     spec.validate()
     m, n = X.shape
@@ -234,6 +259,13 @@ def fit(X: Matrix, y: np.ndarray, spec: ElasticNetSpec, *, sweep_hook=None,
     rng = np.random.default_rng(spec.seed)
     solver = EnSolver(m, n, spec.block_size, mode, spec.lam, spec.alpha, gamma, device=device)
     try:
+        gm = choose_gram_mode(m, n, spec.block_size, spec.iters) if gram_mode == "auto" else gram_mode
+        if gm == "covariance":
+            try:
+                solver.set_gram_mode("covariance")
+            except _native.NativeError as e:
+                if e.code != _native.RAC_ERR_UNSUPPORTED or gram_mode != "auto":
+                    raise
         solver.set_data(X, y)
         if mode == Mode.RP:
             solver.set_partition(_device.PermutationFeeder(rng, n, solver.dev).draw(1))

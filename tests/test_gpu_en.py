@@ -87,12 +87,12 @@ def _spec_from(g, tag):
                           seed=int(seed), tol=None if np.isnan(tol) else float(tol))
 
 
-def _check_fit(g, tag, X, y, check_all_sweeps=True):
+def _check_fit(g, tag, X, y, check_all_sweeps=True, gram_mode="auto"):
     from paper_1907_01995_b200 import elastic_net as en
     spec = _spec_from(g, tag)
     caps = {}
     hook = (lambda k, b, z, xi: caps.__setitem__(k, (b, z, xi))) if check_all_sweeps else None
-    model = en.fit(X, y, spec, sweep_hook=hook)
+    model = en.fit(X, y, spec, sweep_hook=hook, gram_mode=gram_mode)
     gamma, iters, resid, obj_b, obj_z = g[f"{tag}_final"]
     if check_all_sweeps:
         for k in g[f"{tag}_sweeps_kept"]:
@@ -110,17 +110,19 @@ def _check_fit(g, tag, X, y, check_all_sweeps=True):
     return model
 
 
+@pytest.mark.parametrize("gram", ["blocks", "covariance"])
 @pytest.mark.parametrize("tag", ["lasso_rac", "ridge_rp", "enet_tol", "ls_lam0", "clamp_bs"])
-def test_fit_small_matches_reference(lib, golden, tag):
+def test_fit_small_matches_reference(lib, golden, tag, gram):
     g = golden("en_small")
-    _check_fit(g, tag, g[f"{tag}_X"], g[f"{tag}_y"])
+    _check_fit(g, tag, g[f"{tag}_X"], g[f"{tag}_y"], gram_mode=gram)
 
 
-def test_fit_config1_matches_reference(lib, golden):
+@pytest.mark.parametrize("gram", ["blocks", "covariance"])
+def test_fit_config1_matches_reference(lib, golden, gram):
     from paper_1907_01995_b200 import configs
     g = golden("en_config1")
     c = configs.config1()
-    _check_fit(g, "cfg1", c.X, c.y)
+    _check_fit(g, "cfg1", c.X, c.y, gram_mode=gram)
     # norms of every one of the first 50 sweeps
     from paper_1907_01995_b200 import elastic_net as en
     caps = []
@@ -135,7 +137,8 @@ def test_fit_config2_small_matches_reference(lib, golden):
     from paper_1907_01995_b200 import configs
     g = golden("en_config2_small")
     c = configs.config2(scale=0.1)
-    _check_fit(g, "cfg2s", c.X, c.y)
+    _check_fit(g, "cfg2s", c.X, c.y, gram_mode="blocks")
+    _check_fit(g, "cfg2s", c.X, c.y, gram_mode="covariance")
 
 
 def test_fit_vs_oracle_random_shapes(lib):
@@ -193,11 +196,13 @@ def test_identity_design_recovers_targets(lib):
     np.testing.assert_allclose(model.beta, y, atol=1e-10)
 
 
-@pytest.mark.parametrize("env", [{}, {"RAC_EN_PIPE": "0"}, {"RAC_EN_CS": "4"}, {"RAC_EN_CS": "8"},
-                                 {"RAC_EN_VARIANT": "0"}])
-def test_chain_variants_match_oracle(lib, monkeypatch, env):
-    """Every chain variant (sweep pipeline on/off, cluster sizes 2/4/8, streaming chain)
-    on a shape with several 32-row chunks per CTA, batched sweeps (no per-sweep hook)."""
+@pytest.mark.parametrize("env,gram", [({}, "blocks"), ({"RAC_EN_PIPE": "0"}, "blocks"),
+                                      ({"RAC_EN_CS": "4"}, "blocks"), ({"RAC_EN_CS": "8"}, "blocks"),
+                                      ({"RAC_EN_VARIANT": "0"}, "blocks"), ({}, "covariance"),
+                                      ({"RAC_EN_PIPE": "0"}, "covariance")])
+def test_chain_variants_match_oracle(lib, monkeypatch, env, gram):
+    """Every chain variant (sweep pipeline on/off, cluster sizes 2/4/8, streaming chain,
+    covariance chain) on a shape with several 32-row chunks per CTA, batched sweeps."""
     from oracle import rac_oracle as ro
     from paper_1907_01995_b200 import elastic_net as en
     for k, v in env.items():
@@ -208,7 +213,7 @@ def test_chain_variants_match_oracle(lib, monkeypatch, env):
     y = X[:, :10] @ rng.standard_normal(10) + 0.1 * rng.standard_normal(m)
     kw = dict(lam=0.02, alpha=0.7, gamma=1.0, block_size=s, iters=25, seed=5)
     ref = ro.en_fit(X, y, mode="rac", **kw)
-    got = en.fit(X, y, en.ElasticNetSpec(**kw))
+    got = en.fit(X, y, en.ElasticNetSpec(**kw), gram_mode=gram)
     assert rel(got.beta, ref["beta"]) <= ITER_TOL
     assert rel(got.z, ref["z"]) <= ITER_TOL
     assert rel(got.xi, ref["xi"]) <= ITER_TOL
@@ -221,8 +226,39 @@ def test_pipeline_bitwise_equals_serial(lib, monkeypatch):
     X = rng.standard_normal((3000, 400))
     y = rng.standard_normal(3000)
     spec = en.ElasticNetSpec(lam=0.05, alpha=0.9, block_size=40, iters=30, seed=9)
-    a = en.fit(X, y, spec)
-    monkeypatch.setenv("RAC_EN_PIPE", "0")
-    b = en.fit(X, y, spec)
-    assert np.array_equal(a.beta, b.beta) and np.array_equal(a.z, b.z) and np.array_equal(a.xi, b.xi)
-    assert np.array_equal(a.residual_history, b.residual_history)
+    for gram in ("blocks", "covariance"):
+        monkeypatch.delenv("RAC_EN_PIPE", raising=False)
+        a = en.fit(X, y, spec, gram_mode=gram)
+        monkeypatch.setenv("RAC_EN_PIPE", "0")
+        b = en.fit(X, y, spec, gram_mode=gram)
+        assert np.array_equal(a.beta, b.beta) and np.array_equal(a.z, b.z) and np.array_equal(a.xi, b.xi)
+        assert np.array_equal(a.residual_history, b.residual_history)
+    monkeypatch.delenv("RAC_EN_PIPE", raising=False)
+    a = en.fit(X, y, spec, gram_mode="blocks")
+    b = en.fit(X, y, spec, gram_mode="covariance")
+    assert rel(a.beta, b.beta) <= ITER_TOL
+
+
+def test_covariance_mode_vs_oracle_shapes(lib):
+    """Covariance chain on ragged shapes: n % s != 0, odd s (cp.async inverse path),
+    n smaller than the cluster, rp mode, m < n, per-sweep parity for the first sweeps."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import elastic_net as en
+    from paper_1907_01995_b200.problems import Mode
+    rng = np.random.default_rng(17)
+    for (m, n, s, mode, alpha) in [(33, 70, 9, "rac", 1.0), (400, 600, 37, "rac", 0.5),
+                                   (100, 513, 64, "rp", 0.2), (5, 7, 2, "rac", 1.0),
+                                   (70, 20, 20, "rp", 0.0), (300, 1000, 256, "rac", 0.8)]:
+        X = rng.standard_normal((m, n))
+        y = rng.standard_normal(m)
+        kw = dict(lam=0.05, alpha=alpha, gamma=0.7, block_size=s, iters=12, seed=3)
+        caps = {}
+        ro.en_fit(X, y, mode=mode, **kw,
+                  on_sweep=lambda k, bl, b, z, xi: caps.__setitem__(k, (b.copy(), z.copy(), xi.copy())))
+        got = {}
+        en.fit(X, y, en.ElasticNetSpec(mode=Mode(mode), **kw), gram_mode="covariance",
+               sweep_hook=lambda k, b, z, xi: got.__setitem__(k, (b, z, xi)))
+        for k in caps:
+            for a_, b_ in zip(got[k], caps[k]):
+                assert rel(a_, b_) <= ITER_TOL, (m, n, s, mode, k)
+

@@ -308,8 +308,9 @@ def run_b200_en(args, world, rank, local):
     lib.rac_en_set_timing(solver.h, 2)
     solver.run(_device.PermutationFeeder(rng, n, dev).draw(1), None)
     torch.cuda.synchronize()
-    tbuf = (np.ctypeslib.ctypes.c_int64 * (8 + 16 * p))()
-    lib.rac_en_trace(solver.h, tbuf, 8 + 16 * p)
+    ntr = 16 + 16 * p + s
+    tbuf = (np.ctypeslib.ctypes.c_int64 * ntr)()
+    lib.rac_en_trace(solver.h, tbuf, ntr)
     info = (np.ctypeslib.ctypes.c_int32 * 4)()
     lib.rac_en_info(solver.h, info)
     labels = (("cluster_sync", "cluster_reduce", "grid_barrier", "commit", "rhs_loads", "solve_wait", "rhs",
@@ -329,6 +330,17 @@ def run_b200_en(args, world, rank, local):
         chain_trace.update({"rows_per_chunk": int(info[2]), "chunks_per_cta": int(info[3]),
                             "first_phase_us": float(tv[pro - 1] - tv[0]),
                             "per_block_us": {k: float(v) for k, v in zip(labels, ph.mean(axis=0))}})
+    if s <= 236:
+        # factor kernel, block 0: assembly, then per 8-pivot step [panel copy, 8x8 sweep, CW, update]
+        f0 = 8 + 16 * p
+        nst = (s + 7) // 8
+        fv = np.array(tbuf[f0:f0 + 2 + 4 * nst], dtype=np.float64) / 1e3
+        if fv[0] > 0 and fv[-1] > 0:
+            steps = np.diff(np.r_[fv[1], fv[2:]]).reshape(nst, 4)
+            chain_trace["factor_block0_us"] = {
+                "assembly": float(fv[1] - fv[0]), "steps": int(nst),
+                "per_step": {k: float(v) for k, v in zip(("panel", "diag_sweep", "cw", "update"),
+                                                         steps.mean(axis=0))}}
     lib.rac_en_set_timing(solver.h, 0)
     solver.close()
     del perms, more

@@ -267,7 +267,8 @@ struct rac_en_ctx {
   // optional per-stage CUDA-event timing: [assembly, gram, factor, chain]
   bool timing = false;
   std::vector<cudaEvent_t> events;  // 5 per timed sweep
-  long long* trace = nullptr;       // 2 + 8p phase timestamps of the last traced sweep
+  long long* trace = nullptr;       // phase timestamps of the last traced sweep (chain | factor)
+  long long* trace_buf = nullptr;
 };
 
 namespace {
@@ -389,6 +390,7 @@ int en_factor(rac_en_ctx* c, cudaStream_t st) {
   a.scratch = c->scratch;
   a.info = c->info;
   a.done = c->ctrl;
+  a.trace = c->trace ? c->trace + 8 + 16 * (size_t)c->p : nullptr;
   return launch_chol_system(a, c->p, st);
 }
 
@@ -885,10 +887,12 @@ extern "C" int rac_en_set_timing(rac_en_ctx* c, int32_t enable) {
   if (!c) return set_error(RAC_ERR_ARG, "rac_en_set_timing: null context");
   c->timing = enable != 0;
   if (enable >= 2 && !c->trace) {
-    int rc = dalloc(c, &c->trace, 8 + 16 * (size_t)c->p);
+    // chain stamps, then the factor kernel's (block 0): 8 + 16p | 8 + s
+    int rc = dalloc(c, &c->trace, 16 + 16 * (size_t)c->p + c->s);
     if (rc) return rc;
+    c->trace_buf = c->trace;
   }
-  if (enable < 2) c->trace = nullptr;
+  c->trace = (enable >= 2) ? c->trace_buf : nullptr;
   return RAC_OK;
 }
 
@@ -907,7 +911,7 @@ extern "C" int rac_en_trace(rac_en_ctx* c, int64_t* host, int32_t capacity) {
   using namespace rac;
   clear_error();
   if (!c || !host || !c->trace) return set_error(RAC_ERR_ARG, "rac_en_trace: tracing not enabled");
-  int k = std::min<int>(capacity, 8 + 16 * c->p);
+  int k = std::min<int>(capacity, 16 + 16 * c->p + c->s);
   return check_cuda(cudaMemcpy(host, c->trace, k * sizeof(int64_t), cudaMemcpyDeviceToHost), "trace copy");
 }
 

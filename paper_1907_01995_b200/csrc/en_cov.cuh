@@ -25,7 +25,7 @@ namespace rac {
 
 constexpr int COVT = 512;              // threads per CTA
 constexpr int COV_NW = COVT / 32;
-constexpr int COV_UNR = 16;            // independent G loads in flight per lane
+constexpr int COV_UNR = 32;            // independent G loads in flight per lane
 
 struct EnCovArgs {
   const double* G;      // n x n row-major, X'X/m
@@ -45,10 +45,8 @@ struct EnCovArgs {
   long long* trace;     // optional: %globaltimer per phase (CTA 0): 1 + 7 per block
 };
 
-__host__ __device__ inline size_t cov_red_doubles(size_t rn) {
-  const size_t r32 = (rn + 31) / 32 * 32;
-  return r32 > 512 ? r32 : 512;
-}
+// phase-A partials: GA x RT x 32 with GA = ceil(16 / RT)  ->  <= 512 + RT * 32
+__host__ __device__ inline size_t cov_red_doubles(size_t rn) { return 512 + (rn + 31) / 32 * 32; }
 
 template <int K>
 __host__ __device__ inline size_t cov_smem_bytes(int s, int64_t n, int p) {
@@ -147,11 +145,12 @@ __global__ void __launch_bounds__(COVT, 1) en_cov_kernel(EnCovArgs a) {
 
   // q[R] += G[b, R]' delta  (rows of G = columns by symmetry; lanes = consecutive rows)
   const int RT = (nr + 31) / 32;
-  const int GA = max(1, min(COV_NW, COV_NW / max(1, RT)));
+  // j-groups per row tile so that every warp has a task: at most ceil(RT*s/16) loads per lane
+  const int GA = max(1, (COV_NW + max(1, RT) - 1) / max(1, RT));
+  const int tasks = RT * GA;
+  const int per = (s + GA - 1) / GA;
   auto phase_a = [&](int b) {
     const int* bi = bidx(b);
-    const int tasks = RT * GA;
-    const int per = (s + GA - 1) / GA;
     for (int task = warp; task < tasks; task += COV_NW) {
       const int rt = task % RT, ga = task / RT;
       const int r = rt * 32 + lane;

@@ -162,10 +162,16 @@ __device__ void cta_chol_inverse(double* A, int ld, int s, double* dY, double* o
 }
 
 // blocked symmetric sweep on the packed lower triangle P (-> -P^{-1}); 0 or k+1
-__device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double* W, int* fail) {
+__device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double* W, int* fail,
+                                long long* tr) {
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   if (tid == 0) *fail = 0;
   __syncthreads();
+  int tp = 0;
+  auto stamp = [&]() {
+    if (tr && tid == 0) tr[tp] = gtimer();
+    ++tp;
+  };
   for (int k = 0; k < s; k += SB) {
     const int bb = min(SB, s - k);
     for (int e = tid; e < bb * s; e += CTHREADS) {
@@ -173,6 +179,7 @@ __device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double
       Cm[q * s + i] = (i >= c) ? P[pk(i, c)] : P[pk(c, i)];
     }
     __syncthreads();
+    stamp();
     if (ty == 0) {
       // 8x8 diagonal block swept in registers: lane l holds (r0 = l/8, c = l%8)
       // and (r0 + 4, c); pivot rows/columns move by warp shuffles.
@@ -205,6 +212,7 @@ __device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double
       W[tx + 32] = -v1;
     }
     __syncthreads();
+    stamp();
     if (*fail) return *fail;
     for (int e = tid; e < bb * s; e += CTHREADS) {
       const int q = e / s, i = e - q * s;
@@ -213,6 +221,7 @@ __device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double
       CW[q * s + i] = acc;
     }
     __syncthreads();
+    stamp();
     if ((s & 7) == 0 && bb == SB) {
       // rank-8 update  A_RR -= CW Cm'  on FP64 tensor cores: one m8n8k4 pair per
       // 8x8 lower tile (D = C - A B, A = CW rows, B = Cm rows); the K strip is
@@ -275,6 +284,7 @@ __device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double
       }
     }
     __syncthreads();
+    stamp();
   }
   return 0;
 }
@@ -304,6 +314,7 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
   const int32_t* bidx = a.idx ? a.idx + (int64_t)b * s : nullptr;
   double* out = a.inv + (int64_t)b * s * s;
 
+  if (a.trace && blockIdx.x == 0 && tid == 0) a.trace[0] = gtimer();
   if (mode == FACTOR_INVERSE && use_packed) {
     // padded to a multiple of 8 (identity rows) so the update runs on DMMA tiles
     const int s8 = (s + 7) & ~7;
@@ -333,7 +344,9 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
         mo[e] = (j <= i) ? P[pk(i, j)] : P[pk(j, i)];
       }
     }
-    const int f = cta_sweep_packed(P, s8, Cm, CW, W, &fail);
+    long long* tr = (a.trace && blockIdx.x == 0) ? a.trace + 2 : nullptr;
+    if (tr && tid == 0) a.trace[1] = gtimer();
+    const int f = cta_sweep_packed(P, s8, Cm, CW, W, &fail, tr);
     __syncthreads();
     if (!f) {
       if (tid == 0) a.info[b] = 0;

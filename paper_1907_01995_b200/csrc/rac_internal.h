@@ -63,6 +63,7 @@ struct SysArgs {
   double* inv2;         // FACTOR_CHOL: optional sys^{-1} as well
   double* cond_out;     // FACTOR_CHOL: optional per-block (max L_ii / min L_ii)^2
   int only_failed;      // factor only blocks whose info[b] != 0 (re-do pass)
+  long long* trace;     // optional (block 0): [start, sweep start, 4 stamps per 8-pivot step ...]
 };
 int launch_inverse_large(const SysArgs& a, int p, cudaStream_t st);
 size_t large_scratch_bytes(int s, int p);

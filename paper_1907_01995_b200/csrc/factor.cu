@@ -187,24 +187,24 @@ __device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double
       double v0 = (r0 < bb && c < bb) ? Cm[c * s + k + r0] : 0.0;
       double v1 = (r1 < bb && c < bb) ? Cm[c * s + k + r1] : 0.0;
       int f = 0;
-      for (int q = 0; q < bb; ++q) {
-        const double d = __shfl_sync(0xffffffffu, (q < 4) ? v0 : v1, (q & 3) * 8 + q);  // W[q][q]
-        if (!(d > 0.0) || !isfinite(d)) { f = k + q + 1; break; }
-        const double dinv = 1.0 / d;
-        const double wq0 = __shfl_sync(0xffffffffu, v0, r0 * 8 + q);     // W[r0][q]
-        const double wq1 = __shfl_sync(0xffffffffu, v1, r0 * 8 + q);     // W[r1][q]
-        const double wqc = __shfl_sync(0xffffffffu, (q < 4) ? v0 : v1, (q & 3) * 8 + c);  // W[q][c]
-        if (r0 < bb && c < bb) {
-          if (r0 == q && c == q) v0 = -dinv;
-          else if (r0 == q) v0 = wqc * dinv;
-          else if (c == q) v0 = wq0 * dinv;
-          else v0 = v0 - wq0 * wqc * dinv;
-        }
-        if (r1 < bb && c < bb) {
-          if (r1 == q && c == q) v1 = -dinv;
-          else if (r1 == q) v1 = wqc * dinv;
-          else if (c == q) v1 = wq1 * dinv;
-          else v1 = v1 - wq1 * wqc * dinv;
+      // branch-free (selects only) and fully unrolled: every lane runs the same
+      // instruction stream; a non-positive pivot is recorded, the rest ignored
+#pragma unroll
+      for (int q = 0; q < SB; ++q) {
+        if (q < bb) {
+          const double d = __shfl_sync(0xffffffffu, (q < 4) ? v0 : v1, (q & 3) * 8 + q);  // W[q][q]
+          const double wq0 = __shfl_sync(0xffffffffu, v0, r0 * 8 + q);     // W[r0][q]
+          const double wq1 = __shfl_sync(0xffffffffu, v1, r0 * 8 + q);     // W[r1][q]
+          const double wqc = __shfl_sync(0xffffffffu, (q < 4) ? v0 : v1, (q & 3) * 8 + c);  // W[q][c]
+          const bool ok = (d > 0.0) && isfinite(d);
+          if (!ok && !f) f = k + q + 1;
+          const double dinv = __drcp_rn(ok ? d : 1.0);
+          const double n0 = (r0 == q) ? ((c == q) ? -dinv : wqc * dinv)
+                                      : ((c == q) ? wq0 * dinv : v0 - wq0 * wqc * dinv);
+          const double n1 = (r1 == q) ? ((c == q) ? -dinv : wqc * dinv)
+                                      : ((c == q) ? wq1 * dinv : v1 - wq1 * wqc * dinv);
+          if (r0 < bb && c < bb) v0 = n0;
+          if (r1 < bb && c < bb) v1 = n1;
         }
       }
       if (tx == 0 && f) *fail = f;
@@ -323,12 +323,47 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
     double* CW = Cm + SB * s8;
     double* hbo = a.hbb_out ? a.hbb_out + (int64_t)b * s * s : nullptr;
     const int tx = tid & 31, ty = tid >> 5;
+    // block indices staged in smem (Cm is free until the sweep), then every row's
+    // entries fetched as one batch of independent loads per lane (s8 <= 256)
+    int* sbi = reinterpret_cast<int*>(Cm);
+    for (int i = tid; i < s; i += CTHREADS) sbi[i] = bidx ? bidx[i] : i;
+    __syncthreads();
+    const double* wsb = a.ws ? a.ws + (int64_t)b * a.splits * s * s : nullptr;
     for (int i = ty; i < s8; i += CTHREADS / 32) {
       const int off = pk(i, 0);
-      for (int j = tx; j < s8; j += 32) {
-        if (j <= i) P[off + j] = (i < s && j < s) ? sys_entry(a, b, bidx, i, j, nullptr) : (i == j ? 1.0 : 0.0);
-        if (hbo && i < s && j < s) hbo[(int64_t)i * s + j] = h_entry(a, bidx, i, j);
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = tx + 32 * u;
+        double e = (i == j) ? 1.0 : 0.0;
+        if (j <= i && i < s && j < s) {
+          const int gi = sbi[i], gj = sbi[j];
+          if (!(bidx && (gi < 0 || gj < 0))) {
+            double acc = 0.0;
+            if (wsb) {
+              const double* src = wsb + (int64_t)i * s + j;
+              acc = src[0];
+              for (int z = 1; z < a.splits; ++z) acc += src[(int64_t)z * s * s];
+              if (a.div != 1.0) acc = acc / a.div;
+              if (a.mul != 1.0) acc = a.mul * acc;
+            }
+            if (a.H) {
+              const double h = a.H[(int64_t)gi * a.ldh + gj];
+              acc = wsb ? h + acc : h;
+            }
+            if (i == j) acc += a.shift;
+            e = acc;
+          }
+        }
+        v[u] = e;
       }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = tx + 32 * u;
+        if (j <= i && j < s8) P[off + j] = v[u];
+      }
+      if (hbo && i < s)
+        for (int j = tx; j < s; j += 32) hbo[(int64_t)i * s + j] = h_entry(a, bidx, i, j);
     }
     __syncthreads();
     if (a.ridge_rel > 0.0) {

@@ -170,6 +170,24 @@ __device__ __forceinline__ void cta_matvec(const double* M, int ld, int rows, in
   }
 }
 
+// out = M v for a SYMMETRIC M (row-major, stride ld): thread per row reading
+// column i (= row i), so consecutive threads touch consecutive words; four
+// independent accumulators.  No cross-lane reduction.
+__device__ __forceinline__ void cta_symv(const double* M, int ld, int rows, const double* v, double* out) {
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int j = 0;
+    for (; j + 4 <= rows; j += 4) {
+      a0 += M[(int64_t)j * ld + i] * v[j];
+      a1 += M[(int64_t)(j + 1) * ld + i] * v[j + 1];
+      a2 += M[(int64_t)(j + 2) * ld + i] * v[j + 2];
+      a3 += M[(int64_t)(j + 3) * ld + i] * v[j + 3];
+    }
+    for (; j < rows; ++j) a0 += M[(int64_t)j * ld + i] * v[j];
+    out[i] = (a0 + a1) + (a2 + a3);
+  }
+}
+
 // block max of a per-thread value (all threads get it)
 __device__ __forceinline__ double cta_max(double v, double* red) {
   v = warp_max(v);

@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
   for (int t = 0; t < a.p; ++t) {
     const int b = bnext;
     grid_barrier(a.bar, target, P);
-    if (tr) a.trace[4 * t + 0] = gtimer();
+    if (tr) a.trace[8 * t + 0] = gtimer();
     issue_strip(b);
     // ------------------------------------------------------------ S (CTA 0)
     if (blockIdx.x == 0) {
@@ -330,14 +330,14 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       // one parallel gather pass (all loads independent), then the rhs
       // (engine.py:126-132):  -c_b - (hx_b - H_bb x_b) + A_b'(y - beta(Ax_rest - b))
       const int Pa = min(P, a.nrc);   // CTAs that own constraint rows (others' partials are 0)
-      if (tid == 0) {
-        int k = 0;
-        while (k < s && bidx[k] >= 0) ++k;
-        w.bw.misc[0] = k;
-      }
+      // valid entries (padding only at the end of a short last block)
+      if (tid == 0) w.bw.misc[0] = 0;
+      __syncthreads();
+      int nval = 0;
       for (int i = tid; i < s; i += QPT) {
         const int g = bidx[i];
         w.sIdx[i] = g;
+        nval += (g >= 0);
         if (g >= 0) {
           const double xg = ldcg(a.x + g), hxg = ldcg(a.hx + g), cg_ = a.c[g];
           const double lo = a.lo[g], hi = a.hi[g];
@@ -355,7 +355,9 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
           w.bw.r[i] = rhs;
         }
       }
+      if (nval) atomicAdd(&w.bw.misc[0], nval);
       __syncthreads();
+      if (tr) a.trace[8 * t + 1] = gtimer();
       const int seff = w.bw.misc[0];
       // unconstrained solution (engine.py:201-203).  Well-conditioned blocks:
       // x = N_b r with the smem-resident inverse, reduced systems by Schur
@@ -364,8 +366,9 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       const bool schur = (w.sM != nullptr) && (ldcg(a.cond + b) < 1e6);
       const double* Mblk;
       if (w.sM) wait_ML();   // M_b, N_b resident (ld = s)
+      if (tr) a.trace[8 * t + 2] = gtimer();
       if (schur) {
-        cta_matvec(w.sN, s, seff, seff, w.bw.r, w.bw.x);
+        cta_symv(w.sN, s, seff, w.bw.r, w.bw.x);   // M_b^{-1} is exactly symmetric (Y'Y)
         w.bw.N = w.sN;
         w.bw.ldn = s;
         w.bw.L = w.Lsmall;
@@ -383,11 +386,16 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       }
       __syncthreads();
       long long t_box = tr ? gtimer() : 0;
-      w.bw.dbg = a.trace ? (a.trace + 4 * a.p + 4 * t) : nullptr;
+      if (tr) a.trace[8 * t + 3] = t_box;
+      w.bw.dbg = a.trace ? (a.trace + 8 * a.p + 4 * t) : nullptr;
       if (tr) { w.bw.dbg[0] = 0; w.bw.dbg[1] = 0; w.bw.dbg[2] = 0; }
       __syncthreads();
       int fail = box_active_set(Mblk, s, seff, w.bw, schur);
-      if (tr) w.bw.dbg[3] = gtimer() - t_box;
+      if (tr) {
+        const long long t_end = gtimer();
+        w.bw.dbg[3] = t_end - t_box;
+        a.trace[8 * t + 4] = t_end;
+      }
       if (fail) {
         if (tid == 0) { a.ctrl[2] = b + 1; a.ctrl[0] = 1; }
       }
@@ -401,9 +409,9 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       }
       if (t + 1 < a.p) prefetch_ML(a.order ? a.order[t + 1] : t + 1);
     }
-    if (tr) a.trace[4 * t + 1] = gtimer();
+    if (tr) a.trace[8 * t + 5] = gtimer();
     grid_barrier(a.bar, target, P);
-    if (tr) a.trace[4 * t + 2] = gtimer();
+    if (tr) a.trace[8 * t + 6] = gtimer();
     // non-PD reduced system: abort the sweep (one load per CTA, broadcast in smem)
     if (tid == 0) bad = ldcg(a.ctrl + 0);
     __syncthreads();
@@ -420,7 +428,7 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
     if (bnext >= 0) compute_hbx(bnext);
     if (has_a)
       row_phase<RC>(a.Ac, a.lda, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.x, a.ax, a.partial, w.rp, tfn);
-    if (tr) a.trace[4 * t + 3] = gtimer();
+    if (tr) a.trace[8 * t + 7] = gtimer();
   }
   grid_barrier(a.bar, target, P);
   // ------------------------------------------------------------ dual step + primal residual
@@ -954,7 +962,7 @@ extern "C" int rac_qp_set_trace(rac_qp_ctx* c, int32_t enable) {
   clear_error();
   if (!c) return set_error(RAC_ERR_ARG, "rac_qp_set_trace: null context");
   if (enable && !c->trace) {
-    int rc = qalloc(c, &c->trace, 8 * (size_t)c->p);
+    int rc = qalloc(c, &c->trace, 12 * (size_t)c->p);
     if (rc) return rc;
   }
   if (!enable) c->trace = nullptr;
@@ -965,7 +973,7 @@ extern "C" int rac_qp_trace(rac_qp_ctx* c, int64_t* host, int32_t capacity) {
   using namespace rac;
   clear_error();
   if (!c || !host || !c->trace) return set_error(RAC_ERR_ARG, "rac_qp_trace: tracing not enabled");
-  const int k = std::min<int>(capacity, 8 * c->p);
+  const int k = std::min<int>(capacity, 12 * c->p);
   return check_cuda(cudaMemcpy(host, c->trace, k * sizeof(int64_t), cudaMemcpyDeviceToHost), "qp trace copy");
 }
 

@@ -30,14 +30,14 @@ torch.cuda.synchronize()
 print("ok", sol.progress(), "ms/sweep", t0.elapsed_time(t1) / sweeps)
 if trace:
     p = sol.p
-    buf = (np.ctypeslib.ctypes.c_int64 * (8 * p))()
-    sol.lib.rac_qp_trace(sol.h, buf, 8 * p)
+    buf = (np.ctypeslib.ctypes.c_int64 * (12 * p))()
+    sol.lib.rac_qp_trace(sol.h, buf, 12 * p)
     allv = np.array(buf[:], dtype=np.float64)
-    tv = allv[:4 * p].reshape(p, 4) / 1e3
-    dbg = allv[4 * p:].reshape(p, 4)
+    tv = allv[:8 * p].reshape(p, 8) / 1e3
+    dbg = allv[8 * p:].reshape(p, 4)
     print("box: solves/block %.2f passes/block %.2f us in solves/block %.2f us box total/block %.2f" % (
         dbg[:, 0].mean(), dbg[:, 1].mean(), dbg[:, 2].mean() / 1e3, dbg[:, 3].mean() / 1e3))
-    S = tv[:, 1] - tv[:, 0]; B2 = tv[:, 2] - tv[:, 1]; G = tv[:, 3] - tv[:, 2]
-    B1 = np.r_[np.nan, tv[1:, 0] - tv[:-1, 3]]
-    print("per block us: S %.2f  barrier2 %.2f  G %.2f  barrier1 %.2f" % (S.mean(), B2.mean(), G.mean(), np.nanmean(B1)))
-    print("S percentiles", np.percentile(S, [10, 50, 90, 99]))
+    seg = np.diff(tv, axis=1)
+    names = ["gather", "wait_ML", "x0", "box", "commit+prefetch", "barrier2", "G"]
+    print("per block us:", {k: round(float(v), 2) for k, v in zip(names, seg.mean(axis=0))},
+          "barrier1 %.2f" % float(np.mean(tv[1:, 0] - tv[:-1, 7])))

@@ -283,6 +283,8 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
     for (int i = tid; i < s; i += QPT) {
       const int g = bi[i];
       if (g >= 0) bulk_g2s(w.sM + (size_t)i * sper2, a.H + (int64_t)g * a.n + sc0, seg, w.bar);
+      else
+        for (int64_t jj = 0; jj < sc1 - sc0; ++jj) w.sM[(size_t)i * sper2 + jj] = 0.0;   // padding row
     }
   };
   auto strip_from_smem = [&]() {
@@ -292,10 +294,18 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
     __syncthreads();
     const int W = (int)(sc1 - sc0);
     for (int jj = tid; jj < W; jj += QPT) {
-      double acc = 0.0;
-      for (int i = 0; i < s; ++i)
-        if (w.sIdx[i] >= 0) acc += w.sM[(size_t)i * sper2 + jj] * w.sDel[i];
-      a.hx[sc0 + jj] += acc;
+      // padding rows are zero-filled and their delta is 0: no branch; 4 partial sums
+      const double hx0 = ldcg(a.hx + sc0 + jj);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int i = 0;
+      for (; i + 4 <= s; i += 4) {
+        a0 += w.sM[(size_t)i * sper2 + jj] * w.sDel[i];
+        a1 += w.sM[(size_t)(i + 1) * sper2 + jj] * w.sDel[i + 1];
+        a2 += w.sM[(size_t)(i + 2) * sper2 + jj] * w.sDel[i + 2];
+        a3 += w.sM[(size_t)(i + 3) * sper2 + jj] * w.sDel[i + 3];
+      }
+      for (; i < s; ++i) a0 += w.sM[(size_t)i * sper2 + jj] * w.sDel[i];
+      a.hx[sc0 + jj] = hx0 + ((a0 + a1) + (a2 + a3));
     }
     __syncthreads();
   };
@@ -422,11 +432,11 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       w.sDel[i] = ldcg(a.delta + i);
     }
     __syncthreads();
+    bnext = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
+    if (bnext >= 0) compute_hbx(bnext);   // independent of this block's delta: latency overlaps the strip
     if (strip_smem) strip_from_smem();
     else if (a.H) strip_update(a, w.sIdx, w.sDel, w.red, s);
-    bnext = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
-    if (bnext >= 0) compute_hbx(bnext);
-    if (has_a)
+    if (has_a && (int)blockIdx.x < a.nrc)   // CTAs without row chunks have no partial to write
       row_phase<RC>(a.Ac, a.lda, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.x, a.ax, a.partial, w.rp, tfn);
     if (tr) a.trace[8 * t + 7] = gtimer();
   }
@@ -547,23 +557,22 @@ __global__ void __launch_bounds__(QPT) box_test_kernel(const double* M, const do
   if (threadIdx.x == 0) *info = fail;
 }
 
-// Q_ij = y_i y_j K(x_i, x_j) from the raw Gram (lower triangle in G, full write)
+// Q_ij = y_i y_j K(x_i, x_j) from the full symmetric raw Gram, in place:
+// row-major tiles, coalesced reads and writes (y = +-1 makes the products exact,
+// so both triangles are bitwise what the reference's (i, j) / (j, i) order gives)
 __global__ void svm_kernel_epilogue(double* Q, int64_t N, const double* y, const double* sq,
                                     int kind, double two_sigma2) {
-  const int64_t total = N * (N + 1) / 2;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = (int64_t)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
-    while ((i + 1) * (i + 2) / 2 <= e) ++i;
-    while (i * (i + 1) / 2 > e) --i;
-    const int64_t j = e - i * (i + 1) / 2;
-    double k = Q[i * N + j];
-    if (kind == RAC_KERNEL_GAUSSIAN) {
-      double d2 = fmax(sub(add(sq[i], sq[j]), mul(2.0, k)), 0.0);
-      k = exp(-d2 / two_sigma2);
+  for (int64_t i = blockIdx.y; i < N; i += gridDim.y) {
+    const double yi = y[i], si = (kind == RAC_KERNEL_GAUSSIAN) ? sq[i] : 0.0;
+    double* row = Q + i * N;
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < N; j += (int64_t)gridDim.x * blockDim.x) {
+      double k = row[j];
+      if (kind == RAC_KERNEL_GAUSSIAN) {
+        const double d2 = fmax(sub(add(si, sq[j]), mul(2.0, k)), 0.0);
+        k = exp(-d2 / two_sigma2);
+      }
+      row[j] = mul(mul(yi, k), y[j]);
     }
-    Q[i * N + j] = mul(mul(y[i], k), y[j]);
-    Q[j * N + i] = mul(mul(y[j], k), y[i]);
   }
 }
 
@@ -1007,12 +1016,14 @@ extern "C" int rac_svm_build_q(const double* X, int64_t N, int64_t d, const doub
   GramPlan pl = plan_gram(d, (int)N, 1);
   pl.splits = 1;
   pl.chunk = ldd;
-  rc = launch_gram(Xp, ldd, d, ids, nullptr, (int)N, 1, Q, pl, st, nullptr);
+  rc = launch_gram(Xp, ldd, d, ids, nullptr, (int)N, 1, Q, pl, st, nullptr, 1.0);   // full symmetric X X'
   if (rc) return rc;
   diag_copy_kernel<<<(int)std::min<int64_t>((N + 255) / 256, 4096), 256, 0, st>>>(Q, N, sq);
-  const int64_t total = N * (N + 1) / 2;
-  svm_kernel_epilogue<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 32), 256, 0, st>>>(
-      Q, N, labels, sq, kind, 2.0 * sigma * sigma);
+  {
+    const int gx = (int)std::min<int64_t>((N + 255) / 256, 8);
+    const int gy = (int)std::min<int64_t>(N, 148 * 64);
+    svm_kernel_epilogue<<<dim3(gx, gy), 256, 0, st>>>(Q, N, labels, sq, kind, 2.0 * sigma * sigma);
+  }
   cudaFreeAsync(Xp, st);
   cudaFreeAsync(sq, st);
   cudaFreeAsync(ids, st);

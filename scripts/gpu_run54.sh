@@ -1,0 +1,6 @@
+set -x
+timeout 600 python -m pytest tests/test_gpu_qp.py -x -q -m gpu > gpurun_out/t54_pytest.log 2>&1; echo "pytest rc=$?"
+timeout 300 python scripts/prof_svm.py 60 1.0 --trace > gpurun_out/t54_svm_trace60.log 2>&1; echo "trace rc=$?"
+timeout 300 python bench.py --config 4 --steps 20 --warmup 5 --no-cpu > gpurun_out/t54_bench4.log 2>&1; echo "bench4 rc=$?"
+python scripts/prof_svm.py 2 > gpurun_out/t54_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"qp_chain" -s 1 -c 1 -o gpurun_out/r01_qp_chain_cfg4 -f python scripts/prof_svm.py 2 > gpurun_out/t54_ncu.log 2>&1; echo "ncu rc=$?"

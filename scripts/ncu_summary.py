@@ -73,7 +73,7 @@ def launches(path):
             continue
         agg[k][0] += 1
         agg[k][1] += v
-    ours = {k: v for k, v in agg.items() if "rac::" in k}
+    ours = {k: v for k, v in agg.items() if "cutlass" not in k and "at::" not in k}
     tot = sum(v[1] for v in ours.values()) or 1.0
     print("| kernel | launches | total us | avg us | share of rac kernels |\n|---|---|---|---|---|")
     for k, (n, v) in sorted(agg.items(), key=lambda x: -x[1][1]):

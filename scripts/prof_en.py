@@ -10,9 +10,12 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 case = configs.GENERATORS[cfg]()
 m, n = case.X.shape
+gram = sys.argv[3] if len(sys.argv) > 3 else en.choose_gram_mode(m, n, case.block_size, 1000)
 sol = en.EnSolver(m, n, case.block_size, Mode.RAC, case.lam, case.alpha, case.gamma)
+if gram == "covariance":
+    sol.set_gram_mode("covariance")
 sol.set_data(case.X, case.y)
 perms = _device.PermutationFeeder(np.random.default_rng(0), n, sol.dev).draw(sweeps)
 sol.run(perms, None)
 torch.cuda.synchronize()
-print("ok", sol.progress())
+print("ok", gram, sol.progress())

@@ -488,9 +488,10 @@ def run_b200_svm(args, world, rank, local):
     hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
     strip_bytes = 8.0 * N * N
     achieved = strip_bytes / (ms * 1e-3 / K) / 1e9
-    roof = {"kernel": "qp_chain_kernel (whole sweep)", "bound": "hbm", "achieved": achieved, "peak": hbm,
-            "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-            "algorithmic": "one strip pass over Q (8*N^2 bytes) per sweep"}
+    roof = {"kernel": "qp_chain_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm,
+            "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": traffic_table().get(f"{case.name}:qp_chain_kernel"),
+            "algorithmic": "one strip pass over Q (8*N^2 bytes) per launch (= one sweep)"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import rac_oracle as ro

@@ -27,6 +27,30 @@ int check_cuda(cudaError_t e, const char* what) {
 
 int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what); }
 
+// Context buffers come from the device's default stream-ordered memory pool
+// with an unbounded release threshold: once a shape has been seen, creating and
+// destroying a context (one per fit/train/solve call) neither maps memory nor
+// synchronises the device (cudaFree would).
+int dev_alloc(void** p, size_t bytes, cudaStream_t st) {
+  static bool pool_ready = false;
+  if (!pool_ready) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    pool_ready = true;
+  }
+  return check_cuda(cudaMallocAsync(p, bytes, st), "cudaMallocAsync");
+}
+
+void dev_free(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
 static std::atomic<unsigned long long> g_launches{0};
 void note_launch(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
 unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }

@@ -277,8 +277,8 @@ template <typename T>
 int dalloc(rac_en_ctx* c, T** p, size_t count) {
   if (count == 0) count = 1;
   void* q = nullptr;
-  cudaError_t e = cudaMalloc(&q, count * sizeof(T));
-  if (e != cudaSuccess) return rac::check_cuda(e, "cudaMalloc");
+  const int rc = rac::dev_alloc(&q, count * sizeof(T), c->st);
+  if (rc) return rc;
   c->allocs.push_back(q);
   *p = (T*)q;
   return RAC_OK;
@@ -946,7 +946,7 @@ extern "C" int rac_en_destroy(rac_en_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->schain) cudaStreamDestroy(c->schain);
   if (c->sprep) cudaStreamDestroy(c->sprep);
-  for (void* q : c->allocs) cudaFree(q);
+  for (void* q : c->allocs) rac::dev_free(q, c->st);
   delete c;
   return RAC_OK;
 }

@@ -623,8 +623,8 @@ template <typename T>
 int qalloc(rac_qp_ctx* c, T** p, size_t count) {
   if (count == 0) count = 1;
   void* q = nullptr;
-  cudaError_t e = cudaMalloc(&q, count * sizeof(T));
-  if (e != cudaSuccess) return rac::check_cuda(e, "cudaMalloc");
+  const int rc = rac::dev_alloc(&q, count * sizeof(T), c->st);
+  if (rc) return rc;
   c->allocs.push_back(q);
   *p = (T*)q;
   return RAC_OK;
@@ -989,7 +989,7 @@ extern "C" int rac_qp_trace(rac_qp_ctx* c, int64_t* host, int32_t capacity) {
 extern "C" int rac_qp_destroy(rac_qp_ctx* c) {
   if (!c) return RAC_OK;
   if (c->st) cudaStreamSynchronize(c->st);
-  for (void* q : c->allocs) cudaFree(q);
+  for (void* q : c->allocs) rac::dev_free(q, c->st);
   delete c;
   return RAC_OK;
 }

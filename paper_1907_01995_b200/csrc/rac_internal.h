@@ -19,6 +19,8 @@ void note_launch(int k = 1);
 unsigned long long launch_count();
 
 int num_sms();
+int dev_alloc(void** p, size_t bytes, cudaStream_t st);
+void dev_free(void* p, cudaStream_t st);
 int launch_gemv_rows(const double* Q, int64_t rows, int64_t cols, const double* w, double* out,
                      cudaStream_t st);
 

@@ -218,26 +218,45 @@ def cpu_en_rate(case, sweeps: int) -> tuple[float, float]:
     return sweeps / dt, dt
 
 
+def cpu_svm_rate(case, sweeps: int) -> tuple[float, float]:
+    """Oracle (numpy restatement of racml train) sweeps/s over `sweeps` sweeps (Q formed once, untimed)."""
+    from oracle import rac_oracle as ro
+    t0 = time.perf_counter()
+    ro.svm_train(case.X, case.labels, case.C, "linear", block_size=case.block_size, beta=case.beta,
+                 max_iters=sweeps, seed=0)
+    dt = time.perf_counter() - t0
+    return sweeps / dt, dt
+
+
 def run_reference(args, world, rank):
     """--impl reference: the reference algorithm on the host cores (oracle port)."""
     case = en_case(args.config)
     if rank != 0:
         return 0
-    m, n = case.X.shape
-    cpu_en_rate(case, max(1, args.warmup // 3))
+    svm_cfg = args.config == 4
+    rate_fn = cpu_svm_rate if svm_cfg else cpu_en_rate
+    rate_fn(case, 1)     # warm-up (BLAS threads, page-in)
     total = 0.0
     for _ in range(args.steps):
-        _, dt = cpu_en_rate(case, 1)
+        _, dt = rate_fn(case, 1)
         total += dt
     rate = args.steps / total
+    if svm_cfg:
+        N, d = case.X.shape
+        cfg = {"workload": case.name, "N": N, "d": d, "block_size": case.block_size}
+        sample = f"{args.steps} single-sweep trains of {case.name} (oracle/rac_oracle.svm_train, Q build included)"
+    else:
+        m, n = case.X.shape
+        cfg = {"workload": case.name, "m": m, "n": n, "block_size": case.block_size}
+        sample = f"{args.steps} single sweeps of {case.name} (oracle/rac_oracle.en_fit)"
     line = {
         "impl": "reference", "metric": "rac_admm_sweeps_per_sec", "value": rate,
         "unit": "sweeps/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) seed-0 recipe)",
-        "config": {"workload": case.name, "m": m, "n": n, "block_size": case.block_size},
+        "config": cfg,
         "cpu_baseline": {"value": rate, "unit": "sweeps/s", "cores": cpu_threads(), "kind": "port",
-                         "sample": f"{args.steps} single sweeps of {case.name} (oracle/rac_oracle.en_fit)"},
+                         "sample": sample},
         "e2e": {"value": rate, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -100,6 +100,13 @@ int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t block_size, in
 int rac_en_set_data(rac_en_ctx* ctx, const double* X, int32_t layout, const double* y);
 /* RP mode only: the fixed partition from one permutation of n
  * (elastic_net.py:187-189); block systems are factored once. */
+/* Streaming ingest of a row-major design matrix in row chunks (device
+ * pointers), in increasing row order covering [0, m): row0 a multiple of 32,
+ * rows a multiple of 32 except for the last chunk, which also passes y and
+ * finalises c (and, in covariance mode, G = X'X/m accumulated chunk by chunk,
+ * so forming G overlaps the host->device transfer of the following chunks).
+ * Equivalent to rac_en_set_data up to the summation order of G. */
+int rac_en_set_data_rows(rac_en_ctx* ctx, const double* X_rows, int64_t row0, int64_t rows, const double* y);
 /* Select RAC_GRAM_BLOCKS (default) or RAC_GRAM_COVARIANCE.  Covariance mode
  * forms G = X'X/m on the next rac_en_run / rac_en_set_partition (n x n doubles
  * of HBM) and runs the chain on G in one thread-block cluster; selecting it

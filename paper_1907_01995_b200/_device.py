@@ -64,6 +64,64 @@ class _Stager:
 
 _stagers: dict = {}
 
+ROW_CHUNK_BYTES = 16 << 20
+
+
+class _RowStreamer:
+    """Two pinned host buffers, two device buffers, one copy stream: row chunk
+    k+1 is copied (host memcpy into pinned memory, then DMA) while the
+    consumer's kernels for chunk k run on the current stream."""
+
+    def __init__(self, device):
+        self.device = device
+        self.copy_stream = torch.cuda.Stream(device=device)
+        self.host = [None, None]
+        self.dev = [None, None]
+        self.copied = [None, None]
+        self.consumed = [None, None]
+
+    def run(self, X: np.ndarray, align: int, consume) -> None:
+        m, n = X.shape
+        rows_per = max(align, (ROW_CHUNK_BYTES // (8 * n)) // align * align)
+        need = rows_per * n
+        for k in range(2):
+            if self.host[k] is None or self.host[k].numel() < need:
+                self.host[k] = torch.empty(need, dtype=torch.float64).pin_memory()
+                self.dev[k] = torch.empty(need, dtype=torch.float64, device=self.device)
+        main = torch.cuda.current_stream(self.device)
+        src = torch.from_numpy(X)
+        for i, r0 in enumerate(range(0, m, rows_per)):
+            k = i & 1
+            rows = min(rows_per, m - r0)
+            if self.copied[k] is not None:
+                self.copied[k].synchronize()            # pinned buffer k is free again
+            self.host[k][:rows * n].view(rows, n).copy_(src[r0:r0 + rows])
+            with torch.cuda.stream(self.copy_stream):
+                if self.consumed[k] is not None:
+                    self.copy_stream.wait_event(self.consumed[k])   # device buffer k consumed
+                self.dev[k][:rows * n].copy_(self.host[k][:rows * n], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.copy_stream)
+                self.copied[k] = ev
+            main.wait_event(ev)
+            consume(r0, rows, self.dev[k][:rows * n])
+            done = torch.cuda.Event()
+            done.record(main)
+            self.consumed[k] = done
+
+
+_streamers: dict = {}
+
+
+def stream_rows(X: np.ndarray, align: int, consume, device=None) -> None:
+    """Feed a C-contiguous host matrix to `consume(row0, rows, device_chunk)` in
+    row chunks of ~ROW_CHUNK_BYTES (rows a multiple of `align` except the last)."""
+    dev = torch.device(device or "cuda")
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    if key not in _streamers:
+        _streamers[key] = _RowStreamer(dev)
+    _streamers[key].run(np.ascontiguousarray(X, dtype=np.float64), align, consume)
+
 
 def upload(arr, dtype=torch.float64, device=None, pinned: bool = True) -> torch.Tensor:
     """numpy (or torch) -> contiguous device tensor, staged through pinned memory."""

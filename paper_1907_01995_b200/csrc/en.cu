@@ -203,6 +203,28 @@ int launch_transpose_pad(const double* X, int64_t m, int64_t n, int64_t ld, doub
   return check_launch("transpose_pad");
 }
 
+// rows [row0, row0 + rows) of a row-major chunk -> column-major Xc; the last
+// chunk also zero-fills the padding rows up to ld
+__global__ void transpose_rows_kernel(const double* __restrict__ X, int64_t rows, int64_t n, int64_t ld,
+                                      int64_t row0, int64_t rows_out, double* __restrict__ Xc) {
+  __shared__ double t[32][33];
+  const int64_t i0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    int64_t i = i0 + r, j = j0 + threadIdx.x;
+    t[r][threadIdx.x] = (i < rows && j < n) ? X[i * n + j] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    int64_t j = j0 + r, i = i0 + threadIdx.x;
+    if (j < n && i < rows_out) Xc[j * ld + row0 + i] = t[threadIdx.x][r];
+  }
+}
+
+__global__ void scale_kernel(double* v, int64_t total, double div) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+    v[e] = v[e] / div;
+}
+
 // c_j = -(X[:, j] . y) / m      (elastic_net.py:177)
 __global__ void neg_xty_kernel(const double* __restrict__ Xc, int64_t ld, int64_t m, int64_t n,
                                const double* __restrict__ y, double mdiv, double* __restrict__ c) {
@@ -717,6 +739,52 @@ extern "C" int rac_en_set_data(rac_en_ctx* c, const double* X, int32_t layout, c
   neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
   c->have_data = true;
   return check_launch("rac_en_set_data");
+}
+
+extern "C" int rac_en_set_data_rows(rac_en_ctx* c, const double* X_rows, int64_t row0, int64_t rows,
+                                    const double* y) {
+  using namespace rac;
+  clear_error();
+  if (!c || !X_rows || rows < 1 || row0 < 0 || row0 + rows > c->m || (row0 % 32) != 0)
+    return set_error(RAC_ERR_ARG, "rac_en_set_data_rows: bad arguments");
+  const bool last = (row0 + rows == c->m);
+  if (!last && (rows % 32) != 0) return set_error(RAC_ERR_ARG, "rac_en_set_data_rows: rows must be a multiple of 32");
+  if (last && !y) return set_error(RAC_ERR_ARG, "rac_en_set_data_rows: the last chunk needs y");
+  if (row0 == 0) {
+    c->have_data = false;
+    c->have_G = false;
+    if (c->gram_mode == 1) cudaMemsetAsync(c->G, 0, (size_t)c->n * c->n * sizeof(double), c->st);
+  }
+  const int64_t rows_out = last ? (c->ld - row0) : rows;
+  dim3 grid((unsigned)((c->n + 31) / 32), (unsigned)((rows_out + 31) / 32));
+  if (grid.y > 65535) return set_error(RAC_ERR_UNSUPPORTED, "rac_en_set_data_rows: chunk too tall");
+  transpose_rows_kernel<<<grid, dim3(32, 8), 0, c->st>>>(X_rows, rows, c->n, c->ld, row0, rows_out, c->Xc);
+  note_launch();
+  int rc = check_launch("transpose_rows");
+  if (rc) return rc;
+  if (c->gram_mode == 1) {
+    // G += X_chunk' X_chunk on the column-major rows just written (len rounded up to 32:
+    // the zero padding of the last chunk, or rows that are a multiple of 32)
+    const int64_t len = (rows + 31) / 32 * 32;
+    GramPlan pl = plan_gram(len, (int)c->n, 1);
+    pl.splits = 1;
+    pl.chunk = len;
+    rc = launch_gram(c->Xc + row0, c->ld, len, c->G_ids, nullptr, (int)c->n, 1, c->G, pl, c->st, nullptr, 0.0, 1);
+    if (rc) return rc;
+  }
+  if (!last) return RAC_OK;
+  int blocks = (int)std::min<int64_t>((c->n + 7) / 8, (int64_t)num_sms() * 16);
+  note_launch();
+  neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
+  if (c->gram_mode == 1) {
+    scale_kernel<<<num_sms() * 8, 256, 0, c->st>>>(c->G, c->n * c->n, (double)c->m);   // dot, then / m
+    note_launch();
+    rc = launch_gemv_rows(c->G, c->n, c->n, c->beta, c->q, c->st);
+    if (rc) return rc;
+    c->have_G = true;
+  }
+  c->have_data = true;
+  return check_launch("rac_en_set_data_rows");
 }
 
 extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {

@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(GTHREADS) gram_kernel(const double* __restrict
                                                        const int32_t* __restrict__ blk_list, int s,
                                                        int splits, int64_t chunk,
                                                        double* __restrict__ ws,
-                                                       const int32_t* __restrict__ done, double sym_div) {
+                                                       const int32_t* __restrict__ done, double sym_div,
+                                                       int sym_accum) {
   if (done && *done) return;
   extern __shared__ __align__(16) double gsm[];
   double* sA[2] = {gsm, gsm + GT * GLD};
@@ -181,7 +182,12 @@ __global__ void __launch_bounds__(GTHREADS) gram_kernel(const double* __restrict
       for (int e = 0; e < 2; ++e) {
         int col = col0 + e;
         if (row < s && col < s && col <= row) {
-          if (sym_div > 0.0) {
+          if (sym_accum) {
+            // streaming ingest: raw sums accumulated chunk after chunk (fixed order)
+            const double v = acc[q][r][e];
+            out[(int64_t)row * s + col] += v;
+            if (col != row) out[(int64_t)col * s + row] += v;
+          } else if (sym_div > 0.0) {
             // single split, full symmetric output scaled like X_b'X_b / m (dot, then divide)
             const double v = acc[q][r][e] / sym_div;
             out[(int64_t)row * s + col] = v;
@@ -342,9 +348,9 @@ GramPlan plan_gram2(int64_t len, int s, int p) {
 
 int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx,
                 const int32_t* blk_list, int s, int p, double* ws, const GramPlan& pl,
-                cudaStream_t st, const int32_t* done, double sym_div) {
+                cudaStream_t st, const int32_t* done, double sym_div, int sym_accum) {
   if (p <= 0) return RAC_OK;
-  if (use_gram2() && sym_div == 0.0) {
+  if (use_gram2() && sym_div == 0.0 && !sym_accum) {
     const size_t smem = 2 * G2ST * G2B * G2LD * sizeof(double);
     int rc = check_cuda(cudaFuncSetAttribute(gram2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                         "gram2 smem attribute");
@@ -360,7 +366,7 @@ int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx,
   if (rc) return rc;
   dim3 grid(pl.pairs, p, pl.splits);
   gram_kernel<<<grid, GTHREADS, smem, st>>>(V, ldv, len, idx, blk_list, s, pl.splits, pl.chunk, ws, done,
-                                            sym_div);
+                                            sym_div, sym_accum);
   note_launch();
   return check_launch("gram");
 }

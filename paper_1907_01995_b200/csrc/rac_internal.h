@@ -41,9 +41,10 @@ size_t gram_ws_bytes(int64_t len, int s, int p);
 // ws receives `splits` partial Grams per block ([p][splits][s][s], lower part valid)
 int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx, const int32_t* blk_list,
                 int s, int p, double* ws, const GramPlan& plan, cudaStream_t st,
-                const int32_t* done, double sym_div = 0.0);
+                const int32_t* done, double sym_div = 0.0, int sym_accum = 0);
 // sym_div > 0 (requires plan.splits == 1): ws receives the FULL symmetric s x s
-// matrix divided by sym_div (the covariance G = X'X/m)
+// matrix divided by sym_div (the covariance G = X'X/m).  sym_accum: the full
+// symmetric raw sums are ADDED to ws (row-chunk streaming of G).
 // K3: assemble block systems, Cholesky, explicit inverse.
 struct SysArgs {
   const double* ws;   // [p][splits][s][s] partial Grams (lower), may be null

@@ -188,11 +188,29 @@ class EnSolver:
             if X.flags.f_contiguous and not X.flags.c_contiguous:
                 Xd = _device.upload(X.T, device=self.dev)   # (n, m) C-order == column-major X
                 layout = _native.LAYOUT_COL_MAJOR
+            elif X.nbytes > 2 * _device.ROW_CHUNK_BYTES and self.m >= 64:
+                self._set_data_streamed(X, y)
+                return
             else:
                 Xd = _device.upload(X, device=self.dev)
         yd = _device.upload(y, device=self.dev)
         _native.check(self.lib.rac_en_set_data(self.h, Xd.data_ptr(), layout, yd.data_ptr()))
         self._keep = [Xd, yd]   # alive until the stream consumed them
+
+    def _set_data_streamed(self, X: np.ndarray, y) -> None:
+        """Host X in row chunks: the transfer of chunk k+1 overlaps the device
+        transpose (and, in covariance mode, G += X_k'X_k) of chunk k."""
+        yd = _device.upload(y, device=self.dev)
+        last = {}
+
+        def consume(r0, rows, chunk):
+            done = r0 + rows == self.m
+            _native.check(self.lib.rac_en_set_data_rows(self.h, chunk.data_ptr(), r0, rows,
+                                                        yd.data_ptr() if done else None))
+            last["keep"] = chunk
+
+        _device.stream_rows(X, 32, consume, device=self.dev)
+        self._keep = [yd, last.get("keep")]
 
     def set_partition(self, perm_dev: torch.Tensor) -> None:
         _native.check(self.lib.rac_en_set_partition(self.h, perm_dev.data_ptr()))

@@ -262,3 +262,27 @@ def test_covariance_mode_vs_oracle_shapes(lib):
             for a_, b_ in zip(got[k], caps[k]):
                 assert rel(a_, b_) <= ITER_TOL, (m, n, s, mode, k)
 
+
+
+@pytest.mark.parametrize("gram", ["blocks", "covariance"])
+def test_streamed_ingest_matches_resident_input(lib, gram):
+    """Host X above the streaming threshold goes through rac_en_set_data_rows (row chunks
+    overlapping transfer, transpose and G += X_k'X_k); the same X as a device tensor goes
+    through rac_en_set_data.  Block mode: bitwise equal; covariance mode: G is summed by
+    chunks, so equal to rounding; both within the parity bar of the oracle."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import _device, elastic_net as en
+    rng = np.random.default_rng(41)
+    m, n = 5000, 1000
+    assert 8 * m * n > 2 * _device.ROW_CHUNK_BYTES
+    X = rng.standard_normal((m, n))
+    y = X[:, :20] @ rng.standard_normal(20) + 0.1 * rng.standard_normal(m)
+    spec = en.ElasticNetSpec(lam=0.05, alpha=0.8, gamma=1.0, block_size=100, iters=15, seed=2)
+    a = en.fit(X, y, spec, gram_mode=gram)
+    b = en.fit(torch.from_numpy(X).cuda(), y, spec, gram_mode=gram)
+    if gram == "blocks":
+        assert np.array_equal(a.beta, b.beta) and np.array_equal(a.z, b.z)
+    else:
+        assert rel(a.beta, b.beta) <= 1e-12
+    ref = ro.en_fit(X, y, mode="rac", lam=0.05, alpha=0.8, gamma=1.0, block_size=100, iters=15, seed=2)
+    assert rel(a.beta, ref["beta"]) <= ITER_TOL

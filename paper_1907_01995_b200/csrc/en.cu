@@ -284,7 +284,8 @@ struct rac_en_ctx {
   int gram_mode = 0;          // 0: per-sweep block Grams from X; 1: covariance
   bool have_G = false;
   int cov_k = 16;
-  double *G = nullptr, *q = nullptr, *cwsum = nullptr, *cwmax = nullptr;
+  int cov_full = 0;           // whole inverse per CTA (en_cov.cuh full_inv)
+  double *G = nullptr, *q = nullptr, *q2 = nullptr, *cwsum = nullptr, *cwmax = nullptr;
   int32_t* G_ids = nullptr;   // 0..n-1 (the single "block" of the full Gram)
   // optional per-stage CUDA-event timing: [assembly, gram, factor, chain]
   bool timing = false;
@@ -342,14 +343,20 @@ int en_grow_history(rac_en_ctx* c, int need) {
 
 void* cov_kernel(int k) { return k == 16 ? (void*)rac::en_cov_kernel<16> : (void*)rac::en_cov_kernel<8>; }
 
-size_t cov_smem(int k, int s, int64_t n, int p) {
-  return k == 16 ? rac::cov_smem_bytes<16>(s, n, p) : rac::cov_smem_bytes<8>(s, n, p);
+size_t cov_smem(int k, int s, int64_t n, int p, int full) {
+  return k == 16 ? rac::cov_smem_bytes<16>(s, n, p, full) : rac::cov_smem_bytes<8>(s, n, p, full);
 }
 
-// largest cluster size (16, else 8) whose single-cluster chain fits; 0 if none
+// largest cluster size (16, else 8) whose single-cluster chain fits, preferring
+// the whole-inverse-per-CTA form (one cluster barrier per block) when it fits;
+// returns k * 2 + full, or 0 if nothing fits
 int cov_plan(int s, int64_t n, int p) {
+  const char* env = getenv("RAC_COV_FULL");
+  const bool allow_full = !(env && atoi(env) == 0);
+  for (int full : {1, 0})
   for (int k : {16, 8}) {
-    const size_t smem = cov_smem(k, s, n, p);
+    if (full && !allow_full) continue;
+    const size_t smem = cov_smem(k, s, n, p, full);
     if (smem > 226 * 1024) continue;
     void* kf = cov_kernel(k);
     if (cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
@@ -369,7 +376,7 @@ int cov_plan(int s, int64_t n, int p) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int clusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&clusters, kf, &cfg) == cudaSuccess && clusters >= 1) return k;
+    if (cudaOccupancyMaxActiveClusters(&clusters, kf, &cfg) == cudaSuccess && clusters >= 1) return k * 2 + full;
     cudaGetLastError();
   }
   return 0;
@@ -452,11 +459,13 @@ int en_chain_cov(rac_en_ctx* c, double tol, cudaStream_t st) {
   a.hist_p = c->hist_p;
   a.hist_d = c->hist_d;
   a.trace = c->trace;
+  a.q2 = c->q2;
+  a.full_inv = c->cov_full;
   void* args[] = {&a};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(c->cov_k);
   cfg.blockDim = dim3(COVT);
-  cfg.dynamicSmemBytes = cov_smem(c->cov_k, c->s, c->n, c->p);
+  cfg.dynamicSmemBytes = cov_smem(c->cov_k, c->s, c->n, c->p, c->cov_full);
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -798,17 +807,20 @@ extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {
     c->gram_mode = 0;
     return RAC_OK;
   }
-  const int k = cov_plan(c->s, c->n, c->p);
+  const int plan = cov_plan(c->s, c->n, c->p);
+  const int k = plan / 2;
   if (!k) return set_error(RAC_ERR_UNSUPPORTED, "covariance mode does not fit (n=%lld, s=%d)", (long long)c->n, c->s);
   int rc = RAC_OK;
   if (!c->G) {
     if ((rc = dalloc(c, &c->G, (size_t)c->n * c->n)) || (rc = dalloc(c, &c->q, c->n)) ||
+        (rc = dalloc(c, &c->q2, c->n)) ||
         (rc = dalloc(c, &c->cwsum, 16)) || (rc = dalloc(c, &c->cwmax, 16)) || (rc = dalloc(c, &c->G_ids, c->n)))
       return rc;
     iota_kernel<<<(int)std::min<int64_t>((c->n + 255) / 256, 4096), 256, 0, c->st>>>(c->G_ids, c->n);
     note_launch();
   }
   c->cov_k = k;
+  c->cov_full = plan & 1;
   c->gram_mode = 1;
   return RAC_OK;
 }

@@ -37,20 +37,23 @@ struct EnCovArgs {
   const int32_t* info;
   const double* c;
   double *beta, *z, *xi, *q;
+  double* q2;           // second published copy of q (full_inv mode double-buffers it)
   double *wsum, *wmax;  // [K]
   int32_t* ctrl;
   double gamma, thr, den, tol;
   int sweep;
   double *hist_p, *hist_d;
   long long* trace;     // optional: %globaltimer per phase (CTA 0): 1 + 7 per block
+  int full_inv;         // 1: every CTA stages the whole inverse and computes the whole delta
+                        //    (one cluster barrier per block instead of two, no DSMEM gather)
 };
 
 // phase-A partials: GA x RT x 32 with GA = ceil(16 / RT)  ->  <= 512 + RT * 32
 __host__ __device__ inline size_t cov_red_doubles(size_t rn) { return 512 + (rn + 31) / 32 * 32; }
 
 template <int K>
-__host__ __device__ inline size_t cov_smem_bytes(int s, int64_t n, int p) {
-  const size_t sl = (s + K - 1) / K;
+__host__ __device__ inline size_t cov_smem_bytes(int s, int64_t n, int p, int full_inv) {
+  const size_t sl = full_inv ? (size_t)s : (size_t)(s + K - 1) / K;
   const size_t rn = (size_t)((n + K - 1) / K);
   return (2 * sl * s + 8 * (size_t)s + (size_t)s + s + sl + rn + cov_red_doubles(rn) + 2 * COV_NW + 4) *
              sizeof(double) +
@@ -68,11 +71,14 @@ __global__ void __launch_bounds__(COVT, 1) en_cov_kernel(EnCovArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rank = (int)cl.block_rank();
   const int sl = (s + K - 1) / K, j0 = min(s, rank * sl), j1 = min(s, j0 + sl), rows = j1 - j0;
+  const bool full = a.full_inv != 0;
+  const int ir = full ? s : sl;            // inverse rows staged per CTA
+  const int ij0 = full ? 0 : j0, irows = full ? s : rows;
   const int64_t rn = (n + K - 1) / K, r0 = min(n, (int64_t)rank * rn), r1 = min(n, r0 + rn);
   const int nr = (int)(r1 - r0);
 
-  double* sInv = csm;                          // [2][sl*s]
-  double* sVec = sInv + 2 * (size_t)sl * s;    // [2][4][s]  c, xi, z, beta at the block's indices
+  double* sInv = csm;                          // [2][ir*s]
+  double* sVec = sInv + 2 * (size_t)ir * s;    // [2][4][s]  c, xi, z, beta at the block's indices
   double* sV = sVec + 8 * (size_t)s;           // [s]
   double* sDel = sV + s;                       // [s]  full delta of the last solved block
   double* sD = sDel + s;                       // [sl] this rank's delta slice (peers read it)
@@ -110,16 +116,18 @@ __global__ void __launch_bounds__(COVT, 1) en_cov_kernel(EnCovArgs a) {
   auto issue = [&](int t) {
     const int b = blk(t), buf = t & 1;
     const int* bi = bidx(b);
-    const double* Ib = a.inv + (int64_t)b * s * s + (int64_t)j0 * s;
-    double* dInv = sInv + (size_t)buf * sl * s;
+    const double* Ib = a.inv + (int64_t)b * s * s + (int64_t)ij0 * s;
+    double* dInv = sInv + (size_t)buf * ir * s;
     if (bulk_inv) {
       if (tid == 0) {
         fence_proxy_async();
-        mbar_arrive_expect_tx(bars + buf, (unsigned)(rows * s * sizeof(double)));
-        if (rows > 0) bulk_g2s(dInv, Ib, (unsigned)(rows * s * sizeof(double)), bars + buf);
+        const unsigned bytes = (unsigned)(irows * s * sizeof(double));
+        mbar_arrive_expect_tx(bars + buf, bytes);
+        for (unsigned off = 0; off < bytes; off += 65536u)
+          bulk_g2s(dInv + off / 8, Ib + off / 8, min(65536u, bytes - off), bars + buf);
       }
     } else {
-      for (int e = tid; e < rows * s; e += COVT) cp_async8(dInv + e, Ib + e);
+      for (int e = tid; e < irows * s; e += COVT) cp_async8(dInv + e, Ib + e);
     }
     double* dv = sVec + (size_t)buf * 4 * s;
     for (int j = tid; j < s; j += COVT) {
@@ -149,7 +157,7 @@ __global__ void __launch_bounds__(COVT, 1) en_cov_kernel(EnCovArgs a) {
   const int GA = max(1, (COV_NW + max(1, RT) - 1) / max(1, RT));
   const int tasks = RT * GA;
   const int per = (s + GA - 1) / GA;
-  auto phase_a = [&](int b) {
+  auto phase_a = [&](int b, double* qdst) {
     const int* bi = bidx(b);
     for (int task = warp; task < tasks; task += COV_NW) {
       const int rt = task % RT, ga = task / RT;
@@ -180,7 +188,7 @@ __global__ void __launch_bounds__(COVT, 1) en_cov_kernel(EnCovArgs a) {
       for (int ga = 1; ga < GA; ++ga) tot += red[ga * (RT * 32) + r];
       const double qn = qR[r] + tot;
       qR[r] = qn;
-      a.q[r0 + r] = qn;
+      qdst[r0 + r] = qn;
     }
   };
 
@@ -192,7 +200,10 @@ __global__ void __launch_bounds__(COVT, 1) en_cov_kernel(EnCovArgs a) {
   for (int t = 0; t < p; ++t) {
     const int b = blk(t), buf = t & 1;
     const int* bi = bidx(b);
-    if (t > 0) phase_a(blk(t - 1));
+    // the q published at block t: full_inv mode alternates two global copies, so a
+    // rank already updating for block t+1 never overwrites what a slower rank reads
+    double* qpub = (full && (t & 1)) ? a.q2 : a.q;
+    if (t > 0) phase_a(blk(t - 1), qpub);
     if (tr) a.trace[tp++] = gtimer();
     cl.sync();   // q rows of every rank are current; every rank is done with sDel / sD
     if (tr) a.trace[tp++] = gtimer();
@@ -205,11 +216,51 @@ __global__ void __launch_bounds__(COVT, 1) en_cov_kernel(EnCovArgs a) {
     const double* dv = sVec + (size_t)buf * 4 * s;
     for (int j = tid; j < s; j += COVT) {
       const int g = bi[j];
-      sV[j] = (g >= 0) ? add(add(sub(-dv[j], ldcg(a.q + g)), dv[s + j]), mul(gamma, sub(dv[2 * s + j], dv[3 * s + j])))
+      sV[j] = (g >= 0) ? add(add(sub(-dv[j], ldcg(qpub + g)), dv[s + j]), mul(gamma, sub(dv[2 * s + j], dv[3 * s + j])))
                        : 0.0;
     }
     __syncthreads();
     if (tr) a.trace[tp++] = gtimer();
+    if (full) {
+      // whole delta in every CTA: (row i, part k) threads, column reads of the
+      // symmetric inverse (conflict-free), parts summed in order
+      const double* I = sInv + (size_t)buf * s * s;
+      const int rs = (s + 31) / 32 * 32;
+      const int parts = max(1, min(COVT / rs, 8));
+      const int per = (s + parts - 1) / parts;
+      for (int e = tid; e < parts * rs; e += COVT) {
+        const int k = e / rs, i = e - k * rs;
+        double acc = 0.0;
+        if (i < s) {
+          const int ja = k * per, jb = min(s, ja + per);
+          for (int j = ja; j < jb; ++j) acc += I[(size_t)j * s + i] * sV[j];
+        }
+        red[k * rs + i] = acc;
+      }
+      __syncthreads();
+      for (int i = tid; i < s; i += COVT) {
+        double d = red[i];
+        for (int k = 1; k < parts; ++k) d += red[k * rs + i];
+        sDel[i] = (bi[i] >= 0) ? d : 0.0;
+      }
+      __syncthreads();
+      if (tr) a.trace[tp++] = gtimer();
+      for (int jj = j0 + tid; jj < j1; jj += COVT) {
+        const int g = bi[jj];
+        if (g < 0) continue;
+        const double bn = add(dv[3 * s + jj], sDel[jj]);
+        const double x0 = dv[s + jj], zo = dv[2 * s + jj];
+        a.beta[g] = bn;
+        const double av = sub(x0, mul(gamma, bn));
+        const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
+        a.z[g] = zn;
+        a.xi[g] = sub(x0, mul(gamma, sub(bn, zn)));
+        my_sum += fabs(sub(bn, zn));
+        my_max = fmax(my_max, fabs(sub(zn, zo)));
+      }
+      if (tr) { a.trace[tp++] = gtimer(); a.trace[tp++] = gtimer(); }
+      continue;
+    }
     // delta slice = inv rows . v ; commit beta/z/xi of the slice
     const double* I = sInv + (size_t)buf * sl * s;
     for (int i = warp; i < rows; i += COV_NW) {
@@ -246,7 +297,8 @@ __global__ void __launch_bounds__(COVT, 1) en_cov_kernel(EnCovArgs a) {
     __syncthreads();
     if (tr) a.trace[tp++] = gtimer();
   }
-  phase_a(blk(p - 1));   // q current for the next sweep
+  if (full) cl.sync();   // every rank is past its last read of the published q
+  phase_a(blk(p - 1), a.q);   // q current for the next sweep
   // residuals: warp -> CTA -> rank 0
   my_sum = warp_sum(my_sum);
   my_max = warp_max(my_max);

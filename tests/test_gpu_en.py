@@ -199,7 +199,8 @@ def test_identity_design_recovers_targets(lib):
 @pytest.mark.parametrize("env,gram", [({}, "blocks"), ({"RAC_EN_PIPE": "0"}, "blocks"),
                                       ({"RAC_EN_CS": "4"}, "blocks"), ({"RAC_EN_CS": "8"}, "blocks"),
                                       ({"RAC_EN_VARIANT": "0"}, "blocks"), ({}, "covariance"),
-                                      ({"RAC_EN_PIPE": "0"}, "covariance")])
+                                      ({"RAC_EN_PIPE": "0"}, "covariance"),
+                                      ({"RAC_COV_FULL": "0"}, "covariance")])
 def test_chain_variants_match_oracle(lib, monkeypatch, env, gram):
     """Every chain variant (sweep pipeline on/off, cluster sizes 2/4/8, streaming chain,
     covariance chain) on a shape with several 32-row chunks per CTA, batched sweeps."""
@@ -239,12 +240,14 @@ def test_pipeline_bitwise_equals_serial(lib, monkeypatch):
     assert rel(a.beta, b.beta) <= ITER_TOL
 
 
-def test_covariance_mode_vs_oracle_shapes(lib):
+@pytest.mark.parametrize("full", ["1", "0"])
+def test_covariance_mode_vs_oracle_shapes(lib, monkeypatch, full):
     """Covariance chain on ragged shapes: n % s != 0, odd s (cp.async inverse path),
     n smaller than the cluster, rp mode, m < n, per-sweep parity for the first sweeps."""
     from oracle import rac_oracle as ro
     from paper_1907_01995_b200 import elastic_net as en
     from paper_1907_01995_b200.problems import Mode
+    monkeypatch.setenv("RAC_COV_FULL", full)
     rng = np.random.default_rng(17)
     for (m, n, s, mode, alpha) in [(33, 70, 9, "rac", 1.0), (400, 600, 37, "rac", 0.5),
                                    (100, 513, 64, "rp", 0.2), (5, 7, 2, "rac", 1.0),

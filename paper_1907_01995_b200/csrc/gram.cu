@@ -20,19 +20,7 @@ constexpr int GKC = 32;       // k-chunk (rows of V per pipeline stage)
 constexpr int GLD = GKC + 4;  // padded smem row: conflict-free DMMA fragment loads
 constexpr int GTHREADS = 256;
 
-static bool use_gram2() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("RAC_GRAM");
-    v = (e && atoi(e) == 2) ? 1 : 0;   // RAC_GRAM=2 selects the 128x128-region kernel (experimental)
-  }
-  return v == 1;
-}
-
-GramPlan plan_gram2(int64_t len, int s, int p);
-
 GramPlan plan_gram(int64_t len, int s, int p) {
-  if (use_gram2()) return plan_gram2(len, s, p);
   GramPlan pl;
   pl.tiles = (s + GT - 1) / GT;
   pl.pairs = pl.tiles * (pl.tiles + 1) / 2;
@@ -201,165 +189,10 @@ __global__ void __launch_bounds__(GTHREADS) gram_kernel(const double* __restrict
   }
 }
 
-// ---------------------------------------------------------------------------
-// Gram v2: one CTA per (block, 128x128 region of the lower triangle, K split).
-// 8 warps; warp w owns region tile-rows {w, NR-1-w} (8-row mma tiles), so the
-// triangular diagonal regions are balanced; per k-step a warp loads 2 A and
-// <= 16 B fragments for up to 32 DMMA.8x8x4.  3-stage cp.async pipeline over
-// 16-row K chunks, one barrier per chunk.
-// ---------------------------------------------------------------------------
-constexpr int G2B = 128;          // region side (vectors)
-constexpr int G2KC = 16;          // K rows per stage
-constexpr int G2LD = G2KC + 4;    // smem stride (doubles): conflict-free fragments
-constexpr int G2ST = 3;           // pipeline stages
-constexpr int G2T = 256;
-
-__host__ __device__ inline int g2_bands(int s) { return ((s + 7) / 8 + 15) / 16; }
-
-__global__ void __launch_bounds__(G2T, 1) gram2_kernel(const double* __restrict__ V, int64_t ldv,
-                                                       int64_t len, const int32_t* __restrict__ idx,
-                                                       const int32_t* __restrict__ blk_list, int s,
-                                                       int splits, int64_t chunk, double* __restrict__ ws,
-                                                       const int32_t* __restrict__ done) {
-  if (done && *done) return;
-  extern __shared__ __align__(16) double g2sm[];
-  const int pair = blockIdx.x;
-  int RB = 0;
-  while ((RB + 1) * (RB + 2) / 2 <= pair) ++RB;
-  const int CB = pair - RB * (RB + 1) / 2;
-  const bool diag = (RB == CB);
-  const int b = blk_list ? blk_list[blockIdx.y] : blockIdx.y;
-  const int z = blockIdx.z;
-  const int32_t* bidx = idx + (int64_t)b * s;
-  const int S8 = (s + 7) / 8;
-  const int NR = min(16, S8 - 16 * RB);   // tile rows in this region
-  const int NC = min(16, S8 - 16 * CB);   // tile cols in this region
-  const int64_t k_begin = (int64_t)z * chunk;
-  const int64_t k_end = min(len, k_begin + chunk);
-  const int nck = (int)((k_end - k_begin + G2KC - 1) / G2KC);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-
-  double* sA = g2sm;                                   // [G2ST][128][G2LD]
-  double* sB = g2sm + G2ST * G2B * G2LD;               // [G2ST][128][G2LD] (unused on diagonal)
-  __shared__ int64_t colA[G2B], colB[G2B];
-  if (tid < G2B) {
-    const int gi = RB * G2B + tid, gj = CB * G2B + tid;
-    const int vi = (gi < s) ? bidx[gi] : -1, vj = (gj < s) ? bidx[gj] : -1;
-    colA[tid] = (vi >= 0) ? (int64_t)vi * ldv : -1;
-    colB[tid] = (vj >= 0) ? (int64_t)vj * ldv : -1;
-  }
-  __syncthreads();
-  for (int e = tid; e < G2ST * G2B * G2LD; e += G2T) {
-    const int c = (e / G2LD) % G2B;
-    if (colA[c] < 0) sA[e] = 0.0;
-    if (!diag && colB[c] < 0) sB[e] = 0.0;
-  }
-  auto load_stage = [&](int stage, int64_t k0) {
-    double* dA = sA + stage * G2B * G2LD;
-    double* dB = sB + stage * G2B * G2LD;
-    for (int e = tid; e < G2B * (G2KC / 2); e += G2T) {
-      const int c = e >> 3, q = e & 7;
-      const int64_t a0 = colA[c];
-      if (a0 >= 0) cp_async16(dA + c * G2LD + 2 * q, V + a0 + k0 + 2 * q);
-      if (!diag) {
-        const int64_t b0 = colB[c];
-        if (b0 >= 0) cp_async16(dB + c * G2LD + 2 * q, V + b0 + k0 + 2 * q);
-      }
-    }
-  };
-  // this warp's two tile-rows and their column ranges
-  const int ra = warp, rb = NR - 1 - warp;
-  const bool hasA = ra < NR && ra <= rb;
-  const bool hasB = rb >= 0 && rb > ra;
-  const int ncA = hasA ? (diag ? ra + 1 : NC) : 0;
-  const int ncB = hasB ? (diag ? rb + 1 : NC) : 0;
-  double accA[16][2], accB[16][2];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) accA[c][0] = accA[c][1] = accB[c][0] = accB[c][1] = 0.0;
-
-  // prologue: G2ST-1 stages in flight
-  for (int st = 0; st < G2ST - 1; ++st) {
-    if (st < nck) load_stage(st, k_begin + (int64_t)st * G2KC);
-    cp_async_commit();
-  }
-  for (int ck = 0; ck < nck; ++ck) {
-    cp_async_wait<G2ST - 2>();
-    __syncthreads();
-    {
-      const int nxt = ck + G2ST - 1;
-      if (nxt < nck) load_stage(nxt % G2ST, k_begin + (int64_t)nxt * G2KC);
-      cp_async_commit();
-    }
-    const int cur = ck % G2ST;
-    const double* A = sA + cur * G2B * G2LD;
-    const double* B = diag ? A : sB + cur * G2B * G2LD;
-#pragma unroll
-    for (int kk = 0; kk < G2KC; kk += 4) {
-      const double a0 = hasA ? A[(ra * 8 + g) * G2LD + kk + t] : 0.0;
-      const double a1 = hasB ? A[(rb * 8 + g) * G2LD + kk + t] : 0.0;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        if (c < ncA || c < ncB) {
-          const double bv = B[(c * 8 + g) * G2LD + kk + t];
-          if (c < ncA) dmma884(accA[c][0], accA[c][1], a0, bv);
-          if (c < ncB) dmma884(accB[c][0], accB[c][1], a1, bv);
-        }
-      }
-    }
-  }
-  cp_async_wait<0>();
-  // epilogue: lower-triangle entries of the block Gram
-  double* out = ws + ((int64_t)b * splits + z) * (int64_t)s * s;
-  auto store_row = [&](int rt, int nc, double (*acc)[2]) {
-    const int row = RB * G2B + rt * 8 + g;
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      if (c < nc) {
-        const int col0 = CB * G2B + c * 8 + 2 * t;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = col0 + e;
-          if (row < s && col < s && col <= row) out[(int64_t)row * s + col] = acc[c][e];
-        }
-      }
-    }
-  };
-  if (hasA) store_row(ra, ncA, accA);
-  if (hasB) store_row(rb, ncB, accB);
-}
-
-GramPlan plan_gram2(int64_t len, int s, int p) {
-  GramPlan pl;
-  const int nb = g2_bands(s);
-  pl.tiles = nb;
-  pl.pairs = nb * (nb + 1) / 2;
-  const int64_t nchunks = (len + G2KC - 1) / G2KC;
-  const int64_t ctas = (int64_t)p * pl.pairs;
-  const int64_t target = num_sms();   // one CTA per SM (register-bound)
-  int64_t splits = std::max<int64_t>(1, target / std::max<int64_t>(1, ctas));
-  splits = std::min<int64_t>(splits, std::max<int64_t>(1, nchunks / 4));
-  splits = std::min<int64_t>(splits, 64);
-  const int64_t per = (nchunks + splits - 1) / splits;
-  splits = (nchunks + per - 1) / per;
-  pl.splits = (int)splits;
-  pl.chunk = per * G2KC;
-  return pl;
-}
-
 int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx,
                 const int32_t* blk_list, int s, int p, double* ws, const GramPlan& pl,
                 cudaStream_t st, const int32_t* done, double sym_div, int sym_accum) {
   if (p <= 0) return RAC_OK;
-  if (use_gram2() && sym_div == 0.0 && !sym_accum) {
-    const size_t smem = 2 * G2ST * G2B * G2LD * sizeof(double);
-    int rc = check_cuda(cudaFuncSetAttribute(gram2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                        "gram2 smem attribute");
-    if (rc) return rc;
-    dim3 grid(pl.pairs, p, pl.splits);
-    gram2_kernel<<<grid, G2T, smem, st>>>(V, ldv, len, idx, blk_list, s, pl.splits, pl.chunk, ws, done);
-    note_launch();
-    return check_launch("gram2");
-  }
   const size_t smem = 4 * GT * GLD * sizeof(double);
   int rc = check_cuda(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "gram smem attribute");

@@ -412,6 +412,38 @@ def run_b200_en(args, world, rank, local):
     fp64 = fp64_peak_tflops(torch)
     roof = en_roofline(stages, m, n, s, p, gram_mode, chain_trace["variant"], hbm, fp64, case.name)
 
+    # ---------------- the reference's own algorithm (per-sweep block Grams from X), reported
+    # beside the covariance-mode headline (the G-reuse variant's algorithmic
+    # work differs, so its roofline is not comparable)
+    alt = None
+    if gram_mode == "covariance":
+        sb = en.EnSolver(m, n, s, Mode.RAC, case.lam, case.alpha, case.gamma, device=local)
+        sb.set_data(case.X, case.y)
+        pb = _device.PermutationFeeder(np.random.default_rng(case.seed), n, dev).draw(W + K)
+        sb.run(pb[:W], None)
+        torch.cuda.synchronize()
+        dist_barrier(world)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record()
+        sb.run(pb[W:W + K], None)
+        b1.record()
+        torch.cuda.synchronize()
+        ms_b = dist_max(b0.elapsed_time(b1), world, dev)
+        sb.lib.rac_en_set_timing(sb.h, 1)
+        sb.run(_device.PermutationFeeder(rng, n, dev).draw(K), None)
+        stb = (np.ctypeslib.ctypes.c_double * 4)()
+        ntb = np.ctypeslib.ctypes.c_int32()
+        sb.lib.rac_en_timing(sb.h, stb, ntb)
+        stages_b = {k: float(v) / max(ntb.value, 1) for k, v in zip(("assembly", "gram", "factor", "chain"), stb)}
+        infb = (np.ctypeslib.ctypes.c_int32 * 4)()
+        sb.lib.rac_en_info(sb.h, infb)
+        var_b = {0: "streaming", 1: "resident-cluster"}.get(int(infb[0]), "streaming")
+        alt = {"gram_mode": "blocks", "value": world * K / (ms_b * 1e-3), "ms_per_step": ms_b / K,
+               "stage_ms_per_sweep": stages_b, "chain_variant": var_b,
+               "roofline": en_roofline(stages_b, m, n, s, p, "blocks", var_b, hbm, fp64, case.name)}
+        sb.close()
+        del pb
+
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -435,6 +467,7 @@ def run_b200_en(args, world, rank, local):
         "time_to_tol": ttt,
         "e2e": e2e,
         "roofline": roof,
+        "reference_algorithm_variant": alt,
         "fp64_dgemm_tflops_measured": fp64,
         "cpu_baseline": cpu,
         "clocks": clk,

@@ -169,10 +169,11 @@ int rac_qp_progress(rac_qp_ctx* ctx, int32_t* iterations_host, int32_t* status_h
 int rac_qp_get(rac_qp_ctx* ctx, double* x, double* y, double* hx, double* ax);
 int rac_qp_history(rac_qp_ctx* ctx, double* primal, double* primal_l1, double* dual,
                    int32_t capacity);
-/* Optional chain trace of the most recent sweep (CTA 0), 12p int64: per block
+/* Optional chain trace of the most recent sweep (CTA 0), 14p int64: per block
  * %globaltimer at [S start, gather done, M/N resident, unconstrained x done,
- * box solve done, S end, G start, G end], then per block the box-solver
- * counters [reduced solves, active-set passes, ns in reduced solves, ns in box]. */
+ * box solve done, S end, G start, G end, next H_bb x_b done, strip done], then
+ * per block the box-solver counters [reduced solves, active-set passes, ns in
+ * reduced solves, ns in box]. */
 int rac_qp_set_trace(rac_qp_ctx* ctx, int32_t enable);
 int rac_qp_trace(rac_qp_ctx* ctx, int64_t* host, int32_t capacity);
 int rac_qp_destroy(rac_qp_ctx* ctx);

@@ -257,12 +257,16 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
   // Strip staging: while CTA 0 solves block b, every other CTA bulk-copies
   // its column slice of the block's H rows into its (otherwise unused)
   // M/N shared-memory region, so the G phase is pure shared-memory math.
-  const int64_t sper = (a.n + (P - 2)) / max(1, P - 1);
+  // With few constraint rows, CTA 1 keeps them (small_pre/small_post below) and
+  // gets no strip, so its G-phase work does not add to a strip.
+  const bool few_rows = has_a && a.m <= 8 && a.nrc == 1 && 2 * a.m * s <= 1024 && P > 2;
+  const int sfirst = few_rows ? 2 : 1;                           // first CTA with a strip
+  const int64_t sper = (a.n + (P - sfirst - 1)) / max(1, P - sfirst);
   const int64_t sper2 = (sper + 1) & ~1LL;                      // even: 16-byte row segments
-  const bool strip_smem = a.H && w.sM && P > 1 && (sper2 * s <= 2LL * s * s + (int64_t)qp_lsmall(s)) &&
+  const bool strip_smem = a.H && w.sM && P > sfirst && (sper2 * s <= 2LL * s * s + (int64_t)qp_lsmall(s)) &&
                           (a.n % 2 == 0);
-  const int64_t sc0 = (blockIdx.x == 0) ? 0 : min64(a.n, (int64_t)(blockIdx.x - 1) * sper2);
-  const int64_t sc1 = (blockIdx.x == 0) ? 0 : min64(a.n, sc0 + sper2);
+  const int64_t sc0 = ((int)blockIdx.x < sfirst) ? 0 : min64(a.n, (int64_t)(blockIdx.x - sfirst) * sper2);
+  const int64_t sc1 = ((int)blockIdx.x < sfirst) ? 0 : min64(a.n, sc0 + sper2);
   unsigned spar = 0u;
   if (strip_smem && blockIdx.x != 0 && tid == 0) {
     mbar_init(w.bar, 1);
@@ -272,12 +276,16 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
     if (!strip_smem || blockIdx.x == 0 || sc1 <= sc0) return;
     const int32_t* bi = a.idx + (int64_t)b * s;
     const unsigned seg = (unsigned)((sc1 - sc0) * sizeof(double));
-    int nvalid = 0;
-    for (int i = 0; i < s; ++i) nvalid += (bi[i] >= 0);   // uniform across threads
+    // valid rows: padding only at the end of a short last block -> count in parallel
+    int mine = 0;
+    for (int i = tid; i < s; i += QPT) mine += (bi[i] >= 0);
+    if (tid == 0) w.bw.misc[1] = 0;
+    __syncthreads();
+    if (mine) atomicAdd(&w.bw.misc[1], mine);
     __syncthreads();
     if (tid == 0) {
       fence_proxy_async();
-      mbar_arrive_expect_tx(w.bar, seg * (unsigned)nvalid);
+      mbar_arrive_expect_tx(w.bar, seg * (unsigned)w.bw.misc[1]);
     }
     __syncthreads();
     for (int i = tid; i < s; i += QPT) {
@@ -309,31 +317,146 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
     }
     __syncthreads();
   };
-  auto compute_hbx = [&](int b) {
+  // Rows go to CTAs 1..P-1 (CTA 0 solves the box QPs); every lane issues all its
+  // index loads, then all its H_bb / x loads, so a row costs two round trips.
+  auto compute_hbx = [&](int b, int slot) {
     if (!a.H) return;
     const int32_t* bi = a.idx + (int64_t)b * s;
     const double* Hb = a.Hbb + (int64_t)b * s * s;
-    for (int i = blockIdx.x * nw + warp; i < s; i += P * nw) {
+    const int P1 = max(1, P - 1), c1 = (P > 1) ? (int)blockIdx.x - 1 : 0;
+    if (c1 < 0) return;
+    for (int i = c1 * nw + warp; i < s; i += P1 * nw) {
+      constexpr int U = 8;                 // columns per lane per round
       double acc = 0.0;
-      for (int j = lane; j < s; j += 32) {
-        const int g = bi[j];
-        if (g >= 0) acc += Hb[(int64_t)i * s + j] * ldcg(a.x + g);
+      for (int j0 = 0; j0 < s; j0 += 32 * U) {
+        int gs[U];
+        double hv[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = j0 + lane + 32 * u;
+          gs[u] = (j < s) ? bi[j] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = j0 + lane + 32 * u;
+          hv[u] = (gs[u] >= 0) ? Hb[(int64_t)i * s + j] : 0.0;
+          xv[u] = (gs[u] >= 0) ? ldcg(a.x + gs[u]) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += hv[u] * xv[u];
       }
       acc = warp_sum(acc);
-      if (lane == 0) a.hbx[i] = acc;
+      if (lane == 0) a.hbx[(int64_t)slot * s + i] = acc;
+    }
+  };
+  // Few constraint rows (SVM: the single row y'): one owner CTA (CTA 1, idle while
+  // CTA 0 solves) keeps them, with ax and the A columns of the current and next
+  // block in shared memory.  small_pre(bn, slot) (during the S phase: x of the
+  // next block is final) gathers A[:, bn] and forms u = A_bn x_bn;
+  // small_post(slot_b, slot_bn) (G phase) is shared-memory arithmetic only:
+  // ax += A_b delta, t = y - beta(ax - u - b), partial = A_bn' t.
+  const bool small_a = few_rows && strip_smem;
+  const int a_owner = (P > 1) ? 1 : 0;
+  __shared__ double sred[8][QPT / 32];
+  __shared__ double sUn[2][8], sUp[8], sAx[8];
+  double* aS = w.red;   // [2][m][s] (w.red is free when the strips are staged in smem)
+  auto block_rows_sum = [&](double* v, int mr, double* out) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (r < mr) {
+        const double u = warp_sum(v[r]);
+        if (lane == 0) sred[r][warp] = u;
+      }
+    __syncthreads();
+    if (tid < mr) {
+      double u = 0.0;
+      for (int w2 = 0; w2 < nw; ++w2) u += sred[tid][w2];
+      out[tid] = u;
+    }
+    __syncthreads();
+  };
+  if (small_a && (int)blockIdx.x == a_owner && tid < a.m) sAx[tid] = ldcg(a.ax + tid);
+  auto small_pre = [&](int bn, int slot) {
+    if ((int)blockIdx.x != a_owner) return;
+    const int mr = (int)a.m;
+    double un[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) un[r] = 0.0;
+    double* dst = aS + (size_t)slot * mr * s;
+    for (int j = tid; j < s; j += QPT) {
+      const int gn = a.idx[(int64_t)bn * s + j];
+      const double xn = (gn >= 0) ? ldcg(a.x + gn) : 0.0;
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < mr) {
+          const double av = (gn >= 0) ? a.Ac[(int64_t)gn * a.lda + r] : 0.0;
+          dst[(size_t)r * s + j] = av;
+          un[r] += av * xn;
+        }
+    }
+    block_rows_sum(un, mr, sUn[slot]);
+  };
+  auto small_post = [&](int slot_b, int slot_bn, bool has_prev, bool has_next) {
+    if ((int)blockIdx.x != a_owner) return;
+    const int mr = (int)a.m;
+    if (has_prev) {
+      double up[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) up[r] = 0.0;
+      const double* ab = aS + (size_t)slot_b * mr * s;
+      for (int j = tid; j < s; j += QPT) {
+        const double d = w.sDel[j];
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (r < mr) up[r] += ab[(size_t)r * s + j] * d;
+      }
+      block_rows_sum(up, mr, sUp);
+    }
+    if (tid < mr) {
+      const double axr = has_prev ? sAx[tid] + sUp[tid] : sAx[tid];
+      sAx[tid] = axr;
+      a.ax[tid] = axr;
+      w.rp.sT[tid] = tfn(tid, axr, sUn[slot_bn][tid]);
+    }
+    __syncthreads();
+    if (has_next) {
+      const double* an = aS + (size_t)slot_bn * mr * s;
+      for (int j = tid; j < s; j += QPT) {
+        double acc = 0.0;
+        for (int r = 0; r < mr; ++r) acc += an[(size_t)r * s + j] * w.rp.sT[r];
+        a.partial[j] = acc;
+      }
     }
   };
   int bnext = a.order ? a.order[0] : 0;
   prefetch_ML(bnext);
-  compute_hbx(bnext);
-  if (has_a)
+  compute_hbx(bnext, 0);
+  if (small_a) {
+    small_pre(bnext, 0);
+    __syncthreads();
+    small_post(0, 0, false, true);
+  }
+  else if (has_a)
     row_phase<RC>(a.Ac, a.lda, a.m, a.nrc, a.idx, s, -1, bnext, a.delta, a.x, a.ax, a.partial, w.rp, tfn);
   const bool tr = a.trace && blockIdx.x == 0 && tid == 0;
+  // per-CTA arrival stamps at both grid barriers of every block (tracing only)
+  long long* arr = a.trace ? a.trace + 14 * (size_t)a.p : nullptr;
   for (int t = 0; t < a.p; ++t) {
     const int b = bnext;
+    if (arr && tid == 0) arr[((size_t)t * P + blockIdx.x) * 2 + 1] = gtimer();
     grid_barrier(a.bar, target, P);
-    if (tr) a.trace[8 * t + 0] = gtimer();
+    if (tr) a.trace[10 * t + 0] = gtimer();
     issue_strip(b);
+    // While CTA 0 solves block t, the others prepare block t+1's terms that do not
+    // depend on block t's solution: H_bb x_b (double-buffered by parity) and, on the
+    // constraint-row owner, A_b x_b.
+    {
+      const int bn1 = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
+      if (bn1 >= 0 && blockIdx.x != 0) {
+        compute_hbx(bn1, (t + 1) & 1);
+        if (small_a) small_pre(bn1, (t + 1) & 1);
+      }
+    }
     // ------------------------------------------------------------ S (CTA 0)
     if (blockIdx.x == 0) {
       const int32_t* bidx = a.idx + (int64_t)b * s;
@@ -351,7 +474,7 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
         if (g >= 0) {
           const double xg = ldcg(a.x + g), hxg = ldcg(a.hx + g), cg_ = a.c[g];
           const double lo = a.lo[g], hi = a.hi[g];
-          const double hb = a.H ? ldcg(a.hbx + i) : 0.0;
+          const double hb = a.H ? ldcg(a.hbx + (int64_t)(t & 1) * s + i) : 0.0;
           double pa = 0.0;
           if (has_a)
             for (int q = 0; q < Pa; ++q) pa += ldcg(a.partial + (int64_t)q * s + i);
@@ -367,7 +490,7 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       }
       if (nval) atomicAdd(&w.bw.misc[0], nval);
       __syncthreads();
-      if (tr) a.trace[8 * t + 1] = gtimer();
+      if (tr) a.trace[10 * t + 1] = gtimer();
       const int seff = w.bw.misc[0];
       // unconstrained solution (engine.py:201-203).  Well-conditioned blocks:
       // x = N_b r with the smem-resident inverse, reduced systems by Schur
@@ -376,7 +499,7 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       const bool schur = (w.sM != nullptr) && (ldcg(a.cond + b) < 1e6);
       const double* Mblk;
       if (w.sM) wait_ML();   // M_b, N_b resident (ld = s)
-      if (tr) a.trace[8 * t + 2] = gtimer();
+      if (tr) a.trace[10 * t + 2] = gtimer();
       if (schur) {
         cta_symv(w.sN, s, seff, w.bw.r, w.bw.x);   // M_b^{-1} is exactly symmetric (Y'Y)
         w.bw.N = w.sN;
@@ -396,15 +519,15 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       }
       __syncthreads();
       long long t_box = tr ? gtimer() : 0;
-      if (tr) a.trace[8 * t + 3] = t_box;
-      w.bw.dbg = a.trace ? (a.trace + 8 * a.p + 4 * t) : nullptr;
+      if (tr) a.trace[10 * t + 3] = t_box;
+      w.bw.dbg = a.trace ? (a.trace + 10 * a.p + 4 * t) : nullptr;
       if (tr) { w.bw.dbg[0] = 0; w.bw.dbg[1] = 0; w.bw.dbg[2] = 0; }
       __syncthreads();
       int fail = box_active_set(Mblk, s, seff, w.bw, schur);
       if (tr) {
         const long long t_end = gtimer();
         w.bw.dbg[3] = t_end - t_box;
-        a.trace[8 * t + 4] = t_end;
+        a.trace[10 * t + 4] = t_end;
       }
       if (fail) {
         if (tid == 0) { a.ctrl[2] = b + 1; a.ctrl[0] = 1; }
@@ -419,26 +542,32 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       }
       if (t + 1 < a.p) prefetch_ML(a.order ? a.order[t + 1] : t + 1);
     }
-    if (tr) a.trace[8 * t + 5] = gtimer();
+    if (tr) a.trace[10 * t + 5] = gtimer();
+    if (arr && tid == 0) arr[((size_t)t * P + blockIdx.x) * 2 + 0] = gtimer();
     grid_barrier(a.bar, target, P);
-    if (tr) a.trace[8 * t + 6] = gtimer();
-    // non-PD reduced system: abort the sweep (one load per CTA, broadcast in smem)
-    if (tid == 0) bad = ldcg(a.ctrl + 0);
-    __syncthreads();
-    if (bad) return;
+    if (tr) a.trace[10 * t + 6] = gtimer();
     // ------------------------------------------------------------ G (all CTAs)
+    // block data + the non-PD abort flag in one round trip
     for (int i = tid; i < s; i += QPT) {
       w.sIdx[i] = a.idx[(int64_t)b * s + i];
       w.sDel[i] = ldcg(a.delta + i);
     }
+    if (tid == 0) bad = ldcg(a.ctrl + 0);
     __syncthreads();
+    if (bad) return;
     bnext = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
-    if (bnext >= 0) compute_hbx(bnext);   // independent of this block's delta: latency overlaps the strip
+    if (P == 1 && bnext >= 0) {   // single CTA: nobody could prepare during S
+      compute_hbx(bnext, (t + 1) & 1);
+      if (small_a) small_pre(bnext, (t + 1) & 1);
+    }
+    if (tr) a.trace[10 * t + 8] = gtimer();
     if (strip_smem) strip_from_smem();
     else if (a.H) strip_update(a, w.sIdx, w.sDel, w.red, s);
-    if (has_a && (int)blockIdx.x < a.nrc)   // CTAs without row chunks have no partial to write
+    if (tr) a.trace[10 * t + 9] = gtimer();
+    if (small_a) small_post(t & 1, (t + 1) & 1, true, bnext >= 0);
+    else if (has_a && (int)blockIdx.x < a.nrc)   // CTAs without row chunks have no partial to write
       row_phase<RC>(a.Ac, a.lda, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.x, a.ax, a.partial, w.rp, tfn);
-    if (tr) a.trace[8 * t + 7] = gtimer();
+    if (tr) a.trace[10 * t + 7] = gtimer();
   }
   grid_barrier(a.bar, target, P);
   // ------------------------------------------------------------ dual step + primal residual
@@ -450,7 +579,7 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       for (int r = tid; r < RC; r += QPT) {
         const int64_t i = i0 + r;
         if (i < a.m) {
-          const double res = a.ax[i] - a.b[i];
+          const double res = ldcg(a.ax + i) - a.b[i];
           a.y[i] = a.y[i] - beta * res;
           pm = fmax(pm, fabs(res));
           ps += fabs(res);
@@ -790,7 +919,7 @@ extern "C" int rac_qp_create(rac_qp_ctx** out, int64_t n, int64_t m, int32_t blo
       (rc = qalloc(c, &c->inv, sqs)) || (rc = qalloc(c, &c->partial, (size_t)c->P * c->s)) ||
       (rc = qalloc(c, &c->delta, c->s)) || (rc = qalloc(c, &c->pmax, c->P)) || (rc = qalloc(c, &c->psum, c->P)) ||
       (rc = qalloc(c, &c->dmax, c->P)) || (rc = qalloc(c, &c->bar, 1)) || (rc = qalloc(c, &c->ctrl, 4)) ||
-      (rc = qalloc(c, &c->hbx, c->s)) || (rc = qalloc(c, &c->Ninv, sqs)) || (rc = qalloc(c, &c->cond, c->p))) {
+      (rc = qalloc(c, &c->hbx, 2 * (size_t)c->s)) || (rc = qalloc(c, &c->Ninv, sqs)) || (rc = qalloc(c, &c->cond, c->p))) {
     rac_qp_destroy(c);
     return rc;
   }
@@ -971,7 +1100,7 @@ extern "C" int rac_qp_set_trace(rac_qp_ctx* c, int32_t enable) {
   clear_error();
   if (!c) return set_error(RAC_ERR_ARG, "rac_qp_set_trace: null context");
   if (enable && !c->trace) {
-    int rc = qalloc(c, &c->trace, 12 * (size_t)c->p);
+    int rc = qalloc(c, &c->trace, 14 * (size_t)c->p + 2 * (size_t)c->p * c->P);
     if (rc) return rc;
   }
   if (!enable) c->trace = nullptr;
@@ -982,7 +1111,7 @@ extern "C" int rac_qp_trace(rac_qp_ctx* c, int64_t* host, int32_t capacity) {
   using namespace rac;
   clear_error();
   if (!c || !host || !c->trace) return set_error(RAC_ERR_ARG, "rac_qp_trace: tracing not enabled");
-  const int k = std::min<int>(capacity, 12 * c->p);
+  const int k = std::min<int>(capacity, 14 * c->p + 2 * c->p * c->P);
   return check_cuda(cudaMemcpy(host, c->trace, k * sizeof(int64_t), cudaMemcpyDeviceToHost), "qp trace copy");
 }
 

@@ -30,14 +30,25 @@ torch.cuda.synchronize()
 print("ok", sol.progress(), "ms/sweep", t0.elapsed_time(t1) / sweeps)
 if trace:
     p = sol.p
-    buf = (np.ctypeslib.ctypes.c_int64 * (12 * p))()
-    sol.lib.rac_qp_trace(sol.h, buf, 12 * p)
+    P = 148
+    buf = (np.ctypeslib.ctypes.c_int64 * (14 * p + 2 * p * P))()
+    sol.lib.rac_qp_trace(sol.h, buf, 14 * p + 2 * p * P)
     allv = np.array(buf[:], dtype=np.float64)
-    tv = allv[:8 * p].reshape(p, 8) / 1e3
-    dbg = allv[8 * p:].reshape(p, 4)
+    tv = allv[:10 * p].reshape(p, 10) / 1e3
+    dbg = allv[10 * p:14 * p].reshape(p, 4)
+    arr = allv[14 * p:].reshape(p, P, 2) / 1e3
+    a2 = arr[:, :, 0] - arr[:, 0:1, 0]      # arrival at barrier 2 relative to CTA 0
+    a1 = arr[1:, :, 1] - arr[1:, 0:1, 1]    # arrival at barrier 1 (next block) relative to CTA 0
+    print("barrier2 arrival minus CTA0 (us): CTA1 %.2f  others mean %.2f max %.2f" % (
+        a2[:, 1].mean(), a2[:, 2:].mean(), a2[:, 2:].max(axis=1).mean()))
+    print("barrier1 arrival minus CTA0 (us): CTA1 %.2f  others mean %.2f max %.2f" % (
+        a1[:, 1].mean(), a1[:, 2:].mean(), a1[:, 2:].max(axis=1).mean()))
     print("box: solves/block %.2f passes/block %.2f us in solves/block %.2f us box total/block %.2f" % (
         dbg[:, 0].mean(), dbg[:, 1].mean(), dbg[:, 2].mean() / 1e3, dbg[:, 3].mean() / 1e3))
-    seg = np.diff(tv, axis=1)
-    names = ["gather", "wait_ML", "x0", "box", "commit+prefetch", "barrier2", "G"]
+    order = [0, 1, 2, 3, 4, 5, 6, 8, 9, 7]
+    seg = np.diff(tv[:, order], axis=1)
+    names = ["gather", "wait_ML", "x0", "box", "commit+prefetch", "barrier2", "hbx", "strip", "rowphase_A"]
+    print("block loop us: %.1f (first S start -> last G end), per block %.2f" % (
+        tv[-1, 7] - tv[0, 0], (tv[-1, 7] - tv[0, 0]) / p))
     print("per block us:", {k: round(float(v), 2) for k, v in zip(names, seg.mean(axis=0))},
           "barrier1 %.2f" % float(np.mean(tv[1:, 0] - tv[:-1, 7])))

@@ -428,6 +428,29 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       }
     }
   };
+  // CTA 0 is idle in the G phase: it gathers everything of the next block that is
+  // final by then (indices, c, bounds, x, H_bb x_b, the condition estimate) into
+  // the strip-reduction smem it never uses, so the next S phase only loads hx and
+  // the partial (one round trip).
+  const bool pf_on = (blockIdx.x == 0) && strip_smem && !(small_a && a_owner == 0) && 6 * s <= (QPT / 32) * QCOLS;
+  double* pf = w.red;   // [6][s]: idx (as double), c, lo, hi, x, hbx
+  __shared__ double pf_cond;
+  auto prefetch_next = [&](int bn, int slot) {
+    if (!pf_on) return;
+    const int32_t* bi = a.idx + (int64_t)bn * s;
+    for (int i = tid; i < s; i += QPT) {
+      const int g = bi[i];
+      pf[i] = (double)g;
+      if (g >= 0) {
+        pf[s + i] = a.c[g];
+        pf[2 * s + i] = a.lo[g];
+        pf[3 * s + i] = a.hi[g];
+        pf[4 * s + i] = ldcg(a.x + g);
+        pf[5 * s + i] = a.H ? ldcg(a.hbx + (int64_t)slot * s + i) : 0.0;
+      }
+    }
+    if (tid == 0) pf_cond = ldcg(a.cond + bn);
+  };
   int bnext = a.order ? a.order[0] : 0;
   prefetch_ML(bnext);
   compute_hbx(bnext, 0);
@@ -467,14 +490,17 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       if (tid == 0) w.bw.misc[0] = 0;
       __syncthreads();
       int nval = 0;
+      const bool use_pf = pf_on && t > 0;
       for (int i = tid; i < s; i += QPT) {
-        const int g = bidx[i];
+        const int g = use_pf ? (int)pf[i] : bidx[i];
         w.sIdx[i] = g;
         nval += (g >= 0);
         if (g >= 0) {
-          const double xg = ldcg(a.x + g), hxg = ldcg(a.hx + g), cg_ = a.c[g];
-          const double lo = a.lo[g], hi = a.hi[g];
-          const double hb = a.H ? ldcg(a.hbx + (int64_t)(t & 1) * s + i) : 0.0;
+          const double hxg = ldcg(a.hx + g);
+          const double xg = use_pf ? pf[4 * s + i] : ldcg(a.x + g);
+          const double cg_ = use_pf ? pf[s + i] : a.c[g];
+          const double lo = use_pf ? pf[2 * s + i] : a.lo[g], hi = use_pf ? pf[3 * s + i] : a.hi[g];
+          const double hb = a.H ? (use_pf ? pf[5 * s + i] : ldcg(a.hbx + (int64_t)(t & 1) * s + i)) : 0.0;
           double pa = 0.0;
           if (has_a)
             for (int q = 0; q < Pa; ++q) pa += ldcg(a.partial + (int64_t)q * s + i);
@@ -496,7 +522,7 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       // x = N_b r with the smem-resident inverse, reduced systems by Schur
       // complements of N_b.  Otherwise: cho_solve with the block's Cholesky
       // factor and direct reduced factorizations, exactly as the reference.
-      const bool schur = (w.sM != nullptr) && (ldcg(a.cond + b) < 1e6);
+      const bool schur = (w.sM != nullptr) && ((use_pf ? pf_cond : ldcg(a.cond + b)) < 1e6);
       const double* Mblk;
       if (w.sM) wait_ML();   // M_b, N_b resident (ld = s)
       if (tr) a.trace[10 * t + 2] = gtimer();
@@ -567,6 +593,7 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
     if (small_a) small_post(t & 1, (t + 1) & 1, true, bnext >= 0);
     else if (has_a && (int)blockIdx.x < a.nrc)   // CTAs without row chunks have no partial to write
       row_phase<RC>(a.Ac, a.lda, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.x, a.ax, a.partial, w.rp, tfn);
+    if (bnext >= 0) prefetch_next(bnext, (t + 1) & 1);
     if (tr) a.trace[10 * t + 7] = gtimer();
   }
   grid_barrier(a.bar, target, P);

@@ -233,7 +233,16 @@ __global__ void __launch_bounds__(COVT, 1) en_cov_kernel(EnCovArgs a) {
         double acc = 0.0;
         if (i < s) {
           const int ja = k * per, jb = min(s, ja + per);
-          for (int j = ja; j < jb; ++j) acc += I[(size_t)j * s + i] * sV[j];
+          double a1 = 0.0, a2 = 0.0, a3 = 0.0;   // four independent chains
+          int j = ja;
+          for (; j + 4 <= jb; j += 4) {
+            acc += I[(size_t)j * s + i] * sV[j];
+            a1 += I[(size_t)(j + 1) * s + i] * sV[j + 1];
+            a2 += I[(size_t)(j + 2) * s + i] * sV[j + 2];
+            a3 += I[(size_t)(j + 3) * s + i] * sV[j + 3];
+          }
+          for (; j < jb; ++j) acc += I[(size_t)j * s + i] * sV[j];
+          acc = (acc + a1) + (a2 + a3);
         }
         red[k * rs + i] = acc;
       }

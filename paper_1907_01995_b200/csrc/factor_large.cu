@@ -127,12 +127,31 @@ __global__ void __launch_bounds__(LTHREADS) large_pivot_kernel(SysArgs a, int p,
   for (int e = tid; e < LT * LT; e += LTHREADS) W[e] = -P[e / LT][e % LT];   // +inv
 }
 
-// load a 64x64 tile (row-major, ld) into smem [r][c] (optionally transposed)
+// load a 64x64 tile (row-major, ld) into smem [r][c] (optionally transposed).
+// Straight tiles: 16-byte cp.async (all 8 per thread in flight; the caller's
+// cp_async_wait + __syncthreads completes them).  Transposed tiles: all 16
+// loads per thread issued before the shared-memory stores.
 __device__ __forceinline__ void load_tile(double (*dst)[LLD], const double* src, int64_t ld, bool trans) {
-  for (int e = threadIdx.x; e < LT * LT; e += LTHREADS) {
-    const int r = e / LT, c = e - r * LT;
-    if (!trans) dst[r][c] = src[(int64_t)r * ld + c];
-    else dst[c][r] = src[(int64_t)r * ld + c];
+  if (!trans) {
+#pragma unroll
+    for (int u = 0; u < (LT * LT / 2) / LTHREADS; ++u) {
+      const int e = threadIdx.x + u * LTHREADS;
+      const int r = e / (LT / 2), c = 2 * (e - r * (LT / 2));
+      cp_async16(&dst[r][c], src + (int64_t)r * ld + c);
+    }
+    cp_async_commit();
+  } else {
+    double v[LT * LT / LTHREADS];
+#pragma unroll
+    for (int u = 0; u < LT * LT / LTHREADS; ++u) {
+      const int e = threadIdx.x + u * LTHREADS;
+      v[u] = src[(int64_t)(e / LT) * ld + (e % LT)];
+    }
+#pragma unroll
+    for (int u = 0; u < LT * LT / LTHREADS; ++u) {
+      const int e = threadIdx.x + u * LTHREADS;
+      dst[e % LT][e / LT] = v[u];
+    }
   }
 }
 
@@ -172,6 +191,7 @@ __global__ void __launch_bounds__(LTHREADS) large_cw_kernel(SysArgs a, int p, in
   if (I > kt) load_tile(sX, A + (int64_t)I * LT * L.S + kt * LT, L.S, false);
   else load_tile(sX, A + (int64_t)kt * LT * L.S + I * LT, L.S, true);
   load_tile(sY, L.W + (size_t)b * LT * LT, LT, false);
+  cp_async_wait<0>();
   __syncthreads();
   double acc[2][4][2] = {};
   tile_mma(sX, sY, acc, 1.0);
@@ -217,6 +237,7 @@ __global__ void __launch_bounds__(LTHREADS) large_update_kernel(SysArgs a, int p
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) acc[i][j][e] = C[(int64_t)(r0 + i * 8 + g) * L.S + c0 + j * 8 + 2 * t + e];
+  cp_async_wait<0>();
   __syncthreads();
   tile_mma(sX, sY, acc, -1.0);
 #pragma unroll

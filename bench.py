@@ -153,7 +153,7 @@ def en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, workload) -> 
     sec = stages[dom] * 1e-3
     if dom == "chain":
         if gram_mode == "covariance":
-            kern = "en_cov_kernel"
+            kern = "en_cla_kernel" if variant == "covariance-lookahead" else "en_cov_kernel"
             byts = 8.0 * n * n + 8.0 * p * s * s
             desc = "rows of G read once (8 n^2) + block inverses (8 p s^2) per launch"
         else:
@@ -332,7 +332,9 @@ def run_b200_en(args, world, rank, local):
     lib.rac_en_trace(solver.h, tbuf, ntr)
     info = (np.ctypeslib.ctypes.c_int32 * 4)()
     lib.rac_en_info(solver.h, info)
-    labels = (("cluster_sync", "cluster_reduce", "grid_barrier", "commit", "rhs_loads", "solve_wait", "rhs",
+    labels = (("tile_and_base_wait", "t1_term_v", "partials_push", "exchange_wait", "commit_publish")
+              if info[0] == 3 else
+              ("cluster_sync", "cluster_reduce", "grid_barrier", "commit", "rhs_loads", "solve_wait", "rhs",
                "delta+cluster_sync", "tile_wait",
                "row_pass1", "row_sync1", "row_pass2", "row_pass3", "issue_next")
               if info[0] == 1 else
@@ -340,10 +342,11 @@ def run_b200_en(args, world, rank, local):
               ("phase_a_q_update", "cluster_sync1", "prefetch_wait", "v_gather", "delta_commit", "cluster_sync2",
                "delta_gather"))
     nl = len(labels)
-    variant = {0: "streaming", 1: "resident-cluster", 2: "covariance-cluster"}[int(info[0])]
+    variant = {0: "streaming", 1: "resident-cluster", 2: "covariance-cluster",
+               3: "covariance-lookahead"}[int(info[0])]
     chain_trace = {"variant": variant, "ctas": int(info[1]), "gram_mode": gram_mode}
     if nl:
-        pro = {0: 2, 1: 5, 2: 1}[int(info[0])]   # stamps before the first block
+        pro = {0: 2, 1: 5, 2: 1, 3: 1}[int(info[0])]   # stamps before the first block
         tv = np.array(tbuf[:pro + nl * p], dtype=np.float64) / 1e3   # us
         ph = np.diff(tv[pro - 1:]).reshape(p, nl) if p > 0 else np.zeros((0, nl))
         chain_trace.update({"rows_per_chunk": int(info[2]), "chunks_per_cta": int(info[3]),

@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(ENT) en_chain_kernel(EnChainArgs a) {
 
 #include "en_res.cuh"
 #include "en_cov.cuh"
+#include "en_cla.cuh"
 
 namespace rac {
 
@@ -287,6 +288,12 @@ struct rac_en_ctx {
   int cov_full = 0;           // whole inverse per CTA (en_cov.cuh full_inv)
   double *G = nullptr, *q = nullptr, *q2 = nullptr, *cwsum = nullptr, *cwmax = nullptr;
   int32_t* G_ids = nullptr;   // 0..n-1 (the single "block" of the full Gram)
+  // lookahead covariance chain (en_cla.cuh); cla_L = leader cluster size, 0 = not used
+  int cla_L = 0, cla_D = 3, cla_W = 0, cla_segw = 1, cla_R = 2, cla_NS = 2;
+  size_t cla_smem = 0;
+  double* T = nullptr;        // [p][D][s][s] tiles of the current sweep
+  double* T_b[2] = {nullptr, nullptr};
+  unsigned long long *dpub = nullptr, *qst = nullptr;
   // optional per-stage CUDA-event timing: [assembly, gram, factor, chain]
   bool timing = false;
   std::vector<cudaEvent_t> events;  // 5 per timed sweep
@@ -382,6 +389,82 @@ int cov_plan(int s, int64_t n, int p) {
   return 0;
 }
 
+void* cla_kernel(int L) { return L == 16 ? (void*)rac::en_cla_kernel<16> : (void*)rac::en_cla_kernel<8>; }
+
+// Lookahead chain plan: leader cluster L (8, else 16) with at most 32 rows per
+// rank, tile slots NS (4 if they fit, else 2), workers owning 32-column segments
+// of q, G-row ring R; the whole grid (L + W CTAs, a multiple of L) must be
+// co-resident.  Needs even s and n (16-byte TMA granules).  Returns false if
+// nothing fits.
+bool cla_plan(rac_en_ctx* c) {
+  using namespace rac;
+  const char* env = getenv("RAC_COV_LA");
+  if (env && atoi(env) == 0) return false;
+  const int s = c->s;
+  const int64_t n = c->n;
+  if ((s & 1) || (n & 1) || s > 256 || n > 20000) return false;
+  const char* envd = getenv("RAC_CLA_D");
+  const int D = envd ? std::max(1, std::min(CLA_DMAX, atoi(envd))) : 3;
+  const int nseg = (int)((n + 31) / 32);
+  const size_t lim = 226 * 1024;
+  for (int L : {8, 16}) {
+    const int sl = (s + L - 1) / L;
+    if (sl > 32) continue;
+    int NS = 0;
+    for (int ns : {4, 2})
+      if (cla_leader_doubles(L, s, D, ns) * sizeof(double) <= lim) { NS = ns; break; }
+    if (!NS) continue;
+    void* kf = cla_kernel(L);
+    if ((L > 8 && cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) ||
+        cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    // co-resident clusters at the largest shared-memory footprint we may pick
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(L);
+    cfg.blockDim = dim3(CLA_T);
+    cfg.dynamicSmemBytes = lim;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = L;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, kf, &cfg) != cudaSuccess || clusters < 2) {
+      cudaGetLastError();
+      continue;
+    }
+    const int wclusters = std::min(clusters - 1, (nseg + L - 1) / L);
+    const int W = wclusters * L;
+    const int segw = (nseg + W - 1) / W;
+    int R = 0;
+    for (int r : {4, 3, 2})
+      if (cla_worker_doubles(s, segw, r) * sizeof(double) <= lim) { R = r; break; }
+    if (!R) continue;
+    c->cla_L = L;
+    c->cla_D = D;
+    c->cla_W = W;
+    c->cla_segw = segw;
+    c->cla_R = R;
+    c->cla_NS = NS;
+    c->cla_smem = cla_smem_bytes(L, s, D, NS, segw, R);   // the attribute stays at `lim` (shared by contexts)
+    return true;
+  }
+  return false;
+}
+
+int launch_cla_tiles(rac_en_ctx* c, cudaStream_t st) {
+  using namespace rac;
+  if (!c->cla_L || c->p < 2) return RAC_OK;
+  cla_tiles_kernel<<<c->p * c->cla_D, dim3(32, 8), 0, st>>>(
+      c->G, c->n, c->s, c->p, c->cla_D, c->idx, (c->mode == RAC_MODE_RP) ? c->order : nullptr, c->T, c->ctrl);
+  note_launch();
+  return check_launch("cla tiles");
+}
+
 // G = X'X/m (full, row-major) on the FP64 tensor cores, one K split (each tile
 // pair writes its block and the mirror), then q = G beta
 int en_compute_G(rac_en_ctx* c, cudaStream_t st) {
@@ -420,7 +503,11 @@ int en_factor(rac_en_ctx* c, cudaStream_t st) {
   a.info = c->info;
   a.done = c->ctrl;
   a.trace = c->trace ? c->trace + 8 + 16 * (size_t)c->p : nullptr;
-  return launch_chol_system(a, c->p, st);
+  int rc = launch_chol_system(a, c->p, st);
+  if (rc) return rc;
+  // RAC: the lookahead chain's tiles G[b_t, b_{t-d}] depend on this sweep's blocks only
+  if (c->gram_mode == 1 && c->mode == RAC_MODE_RAC) return launch_cla_tiles(c, st);
+  return RAC_OK;
 }
 
 int en_block_systems(rac_en_ctx* c) {
@@ -432,8 +519,64 @@ int en_block_systems(rac_en_ctx* c) {
   return en_factor(c, c->st);
 }
 
+int en_chain_cla(rac_en_ctx* c, double tol, cudaStream_t st) {
+  using namespace rac;
+  EnClaArgs a{};
+  a.G = c->G;
+  a.n = c->n;
+  a.s = c->s;
+  a.p = c->p;
+  a.idx = c->idx;
+  a.order = (c->mode == RAC_MODE_RP) ? c->order : nullptr;
+  a.inv = c->inv;
+  a.T = c->T;
+  a.info = c->info;
+  a.c = c->c;
+  a.beta = c->beta;
+  a.z = c->z;
+  a.xi = c->xi;
+  a.q = c->q;
+  a.dpub = c->dpub;
+  a.qst = c->qst;
+  a.wsum = c->cwsum;
+  a.wmax = c->cwmax;
+  a.ctrl = c->ctrl;
+  a.gamma = c->gamma;
+  a.thr = c->lam * c->alpha;
+  a.den = (1.0 - c->alpha) * c->lam + c->gamma;
+  a.tol = tol;
+  a.sweep = c->sweeps;
+  a.hist_p = c->hist_p;
+  a.hist_d = c->hist_d;
+  a.trace = c->trace;
+  a.D = c->cla_D;
+  a.W = c->cla_W;
+  a.segw = c->cla_segw;
+  a.R = c->cla_R;
+  a.NS = c->cla_NS;
+  void* args[] = {&a};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(c->cla_L + c->cla_W);
+  cfg.blockDim = dim3(CLA_T);
+  cfg.dynamicSmemBytes = c->cla_smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = c->cla_L;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.attrs = at;
+  static const bool noncoop = getenv("RAC_PROFILE_NONCOOP") && atoi(getenv("RAC_PROFILE_NONCOOP")) == 1;
+  cfg.numAttrs = noncoop ? 1 : 2;
+  note_launch();
+  return check_cuda(cudaLaunchKernelExC(&cfg, cla_kernel(c->cla_L), args), "en_cla (cluster cooperative launch)");
+}
+
 int en_chain_cov(rac_en_ctx* c, double tol, cudaStream_t st) {
   using namespace rac;
+  if (c->cla_L) return en_chain_cla(c, tol, st);
   EnCovArgs a{};
   a.G = c->G;
   a.n = c->n;
@@ -822,6 +965,17 @@ extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {
   c->cov_k = k;
   c->cov_full = plan & 1;
   c->gram_mode = 1;
+  if (!c->cla_L && cla_plan(c)) {
+    const size_t tq = (size_t)c->p * c->cla_D * c->s * c->s;
+    if ((rc = dalloc(c, &c->T_b[0], tq)) || (c->pipe && (rc = dalloc(c, &c->T_b[1], tq))) ||
+        (rc = dalloc(c, &c->dpub, (size_t)c->p * c->s * 4)) || (rc = dalloc(c, &c->qst, (size_t)c->p * c->s * 2))) {
+      c->cla_L = 0;
+      return rc;
+    }
+    cudaMemsetAsync(c->dpub, 0, (size_t)c->p * c->s * 4 * sizeof(unsigned long long), c->st);
+    cudaMemsetAsync(c->qst, 0, (size_t)c->p * c->s * 2 * sizeof(unsigned long long), c->st);
+    c->T = c->T_b[0];
+  }
   return RAC_OK;
 }
 
@@ -863,6 +1017,7 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
       c->idx = c->idx_b[j];
       c->inv = c->inv_b[j];
       c->info = c->info_b[j];
+      c->T = c->T_b[j];
       if ((rc = launch_chunk_sort(perms + (int64_t)k * c->n, c->n, c->s, 1, c->idx, c->sprep))) return rc;
       if (c->gram_mode != 1 &&
           (rc = launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->sprep,
@@ -900,6 +1055,7 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
     } else {
       rc = launch_order_cast(perms + (int64_t)k * c->p, c->p, c->order, c->st);
       if (rc) return rc;
+      if (c->gram_mode == 1 && (rc = launch_cla_tiles(c, c->st))) return rc;   // tiles follow the visit order
       if (c->timing) { cudaEventRecord(ev[1], c->st); cudaEventRecord(ev[2], c->st); }
     }
     if (c->timing) cudaEventRecord(ev[3], c->st);
@@ -980,8 +1136,8 @@ extern "C" int rac_en_info(rac_en_ctx* c, int32_t* info4) {
   using namespace rac;
   clear_error();
   if (!c || !info4) return set_error(RAC_ERR_ARG, "rac_en_info: bad arguments");
-  info4[0] = (c->gram_mode == 1) ? 2 : c->variant;
-  info4[1] = (c->gram_mode == 1) ? c->cov_k : c->P;
+  info4[0] = (c->gram_mode == 1) ? (c->cla_L ? 3 : 2) : c->variant;
+  info4[1] = (c->gram_mode == 1) ? (c->cla_L ? c->cla_L + c->cla_W : c->cov_k) : c->P;
   info4[2] = c->RC;
   info4[3] = c->nch;
   return RAC_OK;

@@ -128,6 +128,103 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // order prior generic-proxy shared accesses before subsequent async-proxy (TMA) writes
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// non-suspending poll (mbarrier.test_wait): for waits that are usually already
+// satisfied, where try_wait's suspend/wake latency would dominate
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "RAC_MBAR_SPIN_%=:\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra RAC_MBAR_SPIN_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// test_wait poll with a nanosleep back-off: keeps a waiting thread from taking
+// issue / MIO slots from the warps that produce what it waits for
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_spin_sleep(uint64_t* bar, unsigned parity, unsigned ns = 64) {
+  while (!mbar_test(bar, parity)) __nanosleep(ns);
+}
+__device__ __forceinline__ void mbar_spin_cluster(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "RAC_MBAR_SPINC_%=:\n"
+      " mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra RAC_MBAR_SPINC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// wait with cluster-scope acquire: data pushed by peer CTAs (st.async) is visible afterwards
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "RAC_MBAR_WAITC_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra RAC_MBAR_WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// distributed shared memory: push 16 bytes into a peer CTA's shared memory,
+// completing `bytes` on the peer's mbarrier (no cluster-wide barrier needed)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned mapa_u32(unsigned saddr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f64x2(unsigned raddr, double x, double y, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(x), "d"(y), "r"(rbar)
+               : "memory");
+}
+
+// named barrier for a subset of the CTA's warps (id 1..15)
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// self-validating ("low-latency") messages between CTAs of one launch: a double
+// travels as two 64-bit words {32 data bits | 32-bit tag}; a reader accepts the
+// value once both words carry the expected tag.  Aligned 64-bit accesses are
+// single-copy atomic, so no flag / fence round trip is needed.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void ll_store(unsigned long long* p, double v, unsigned tag) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long hi = (unsigned long long)tag << 32;
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"((u & 0xffffffffull) | hi),
+               "l"((u >> 32) | hi)
+               : "memory");
+}
+__device__ __forceinline__ bool ll_ok(unsigned long long w, unsigned tag) { return (unsigned)(w >> 32) == tag; }
+__device__ __forceinline__ double ll_value(unsigned lo, unsigned hi) {
+  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+}
+
 // IEEE operations without FMA contraction (numpy evaluates a*b+c as two
 // rounded ops; use these where bitwise agreement with the oracle matters).
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }

@@ -294,6 +294,11 @@ struct rac_en_ctx {
   double* T = nullptr;        // [p][D][s][s] tiles of the current sweep
   double* T_b[2] = {nullptr, nullptr};
   unsigned long long *dpub = nullptr, *qst = nullptr;
+  // batched preparation (pipelined RAC): the block systems and tiles of cla_B sweeps are
+  // formed by one launch on the prep stream, ring of 2 batches
+  int cla_B = 1, batch_ctr = 0;
+  int32_t *idx_r = nullptr, *info_r = nullptr;
+  double *inv_r = nullptr, *T_r = nullptr;
   // optional per-stage CUDA-event timing: [assembly, gram, factor, chain]
   bool timing = false;
   std::vector<cudaEvent_t> events;  // 5 per timed sweep
@@ -456,10 +461,10 @@ bool cla_plan(rac_en_ctx* c) {
   return false;
 }
 
-int launch_cla_tiles(rac_en_ctx* c, cudaStream_t st) {
+int launch_cla_tiles(rac_en_ctx* c, cudaStream_t st, int sweeps = 1) {
   using namespace rac;
   if (!c->cla_L || c->p < 2) return RAC_OK;
-  cla_tiles_kernel<<<c->p * c->cla_D, dim3(32, 8), 0, st>>>(
+  cla_tiles_kernel<<<dim3(c->p * c->cla_D, sweeps), dim3(32, 8), 0, st>>>(
       c->G, c->n, c->s, c->p, c->cla_D, c->idx, (c->mode == RAC_MODE_RP) ? c->order : nullptr, c->T, c->ctrl);
   note_launch();
   return check_launch("cla tiles");
@@ -481,7 +486,7 @@ int en_compute_G(rac_en_ctx* c, cudaStream_t st) {
   return check_launch("covariance Gram");
 }
 
-int en_factor(rac_en_ctx* c, cudaStream_t st) {
+int en_factor(rac_en_ctx* c, cudaStream_t st, int sweeps = 1) {
   using namespace rac;
   SysArgs a{};
   if (c->gram_mode == 1) {
@@ -503,10 +508,12 @@ int en_factor(rac_en_ctx* c, cudaStream_t st) {
   a.info = c->info;
   a.done = c->ctrl;
   a.trace = c->trace ? c->trace + 8 + 16 * (size_t)c->p : nullptr;
-  int rc = launch_chol_system(a, c->p, st);
+  // `sweeps` consecutive partitions in idx / inv / info (batched preparation): the
+  // kernel treats them as sweeps * p independent blocks
+  int rc = launch_chol_system(a, c->p * sweeps, st);
   if (rc) return rc;
   // RAC: the lookahead chain's tiles G[b_t, b_{t-d}] depend on this sweep's blocks only
-  if (c->gram_mode == 1 && c->mode == RAC_MODE_RAC) return launch_cla_tiles(c, st);
+  if (c->gram_mode == 1 && c->mode == RAC_MODE_RAC) return launch_cla_tiles(c, st, sweeps);
   return RAC_OK;
 }
 
@@ -972,6 +979,20 @@ extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {
       c->cla_L = 0;
       return rc;
     }
+    if (c->pipe) {
+      // sweeps per preparation batch: the factor CTAs (one per block) of a batch should fit
+      // on the SMs the chain leaves free
+      const int free_sms = std::max(0, num_sms() - (c->cla_L + c->cla_W));
+      c->cla_B = std::max(1, std::min(4, free_sms / std::max(1, c->p)));
+      if (chol_scratch_bytes(c->s, c->p) != 0) c->cla_B = 1;   // global factor scratch is sized for one sweep
+      const int nb = 2 * c->cla_B;
+      if ((rc = dalloc(c, &c->idx_r, (size_t)nb * c->p * c->s)) || (rc = dalloc(c, &c->info_r, (size_t)nb * c->p)) ||
+          (rc = dalloc(c, &c->inv_r, (size_t)nb * c->p * c->s * c->s)) || (rc = dalloc(c, &c->T_r, (size_t)nb * tq))) {
+        c->cla_L = 0;
+        return rc;
+      }
+      cudaMemsetAsync(c->info_r, 0, (size_t)nb * c->p * sizeof(int32_t), c->st);
+    }
     cudaMemsetAsync(c->dpub, 0, (size_t)c->p * c->s * 4 * sizeof(unsigned long long), c->st);
     cudaMemsetAsync(c->qst, 0, (size_t)c->p * c->s * 2 * sizeof(unsigned long long), c->st);
     c->T = c->T_b[0];
@@ -1005,6 +1026,43 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
   int rc = en_grow_history(c, c->sweeps + count);
   if (rc) return rc;
   if (c->gram_mode == 1 && !c->have_G && count > 0 && (rc = en_compute_G(c, c->st))) return rc;
+  if (c->pipe && !c->timing && count > 0 && c->gram_mode == 1 && c->cla_L && c->idx_r) {
+    // batched preparation: sort + factor + tiles of B sweeps in one launch each on sprep
+    // (filling the SMs the lookahead chain leaves free), chains on schain; batch slot j of
+    // the 2-slot ring is rewritten only after the last chain that read it.
+    cudaEventRecord(c->ev_start, c->st);
+    cudaStreamWaitEvent(c->sprep, c->ev_start, 0);
+    cudaStreamWaitEvent(c->schain, c->ev_start, 0);
+    const int B = c->cla_B;
+    const size_t ps = (size_t)c->p * c->s, pss = ps * c->s, pT = pss * c->cla_D;
+    for (int k0 = 0; k0 < count; k0 += B) {
+      const int bs = std::min(B, count - k0);
+      const int j = c->batch_ctr & 1;
+      if (c->chain_rec[j]) cudaStreamWaitEvent(c->sprep, c->ev_chain[j], 0);
+      c->idx = c->idx_r + (size_t)j * B * ps;
+      c->inv = c->inv_r + (size_t)j * B * pss;
+      c->info = c->info_r + (size_t)j * B * c->p;
+      c->T = c->T_r + (size_t)j * B * pT;
+      if ((rc = launch_chunk_sort(perms + (int64_t)k0 * c->n, c->n, c->s, bs, c->idx, c->sprep))) return rc;
+      if ((rc = en_factor(c, c->sprep, bs))) return rc;
+      cudaEventRecord(c->ev_prep[j], c->sprep);
+      cudaStreamWaitEvent(c->schain, c->ev_prep[j], 0);
+      for (int q = 0; q < bs; ++q) {
+        c->idx = c->idx_r + ((size_t)j * B + q) * ps;
+        c->inv = c->inv_r + ((size_t)j * B + q) * pss;
+        c->info = c->info_r + ((size_t)j * B + q) * c->p;
+        c->T = c->T_r + ((size_t)j * B + q) * pT;
+        if ((rc = en_chain(c, tol, c->schain))) return rc;
+        c->sweeps++;
+      }
+      cudaEventRecord(c->ev_chain[j], c->schain);
+      c->chain_rec[j] = true;
+      c->batch_ctr++;
+    }
+    cudaEventRecord(c->ev_end, c->schain);
+    cudaStreamWaitEvent(c->st, c->ev_end, 0);
+    return check_launch("rac_en_run (batched)");
+  }
   if (c->pipe && !c->timing && count > 0) {
     // prep(k+1) on sprep overlaps chain(k) on schain; prep(k) may only overwrite the
     // buffers of sweep k-2 once that chain is done.

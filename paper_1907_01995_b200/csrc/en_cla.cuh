@@ -86,10 +86,13 @@ __host__ inline size_t cla_smem_bytes(int L, int s, int D, int NS, int segw, int
   return (a > b ? a : b) * sizeof(double);
 }
 
+// blockIdx.y = sweep of a batch: idx + y * p * s, T + y * p * D * s * s
 __global__ void cla_tiles_kernel(const double* __restrict__ G, int64_t n, int s, int p, int D,
                                  const int32_t* __restrict__ idx, const int32_t* __restrict__ order,
                                  double* __restrict__ T, const int32_t* done) {
   if (done && *done) return;
+  idx += (int64_t)blockIdx.y * p * s;
+  T += (int64_t)blockIdx.y * p * D * s * s;
   const int t = blockIdx.x / D, d = blockIdx.x % D + 1;
   if (t - d < 0) return;
   const int b = order ? order[t] : t, b2 = order ? order[t - d] : t - d;

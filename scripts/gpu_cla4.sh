@@ -1,0 +1,4 @@
+timeout 200 python bench.py --no-cpu > gpurun_out/cla4_bench.log 2>&1; echo "bench rc=$?"
+timeout 200 python bench.py --no-cpu --config 3 > gpurun_out/cla4_bench3.log 2>&1; echo "bench3 rc=$?"
+timeout 200 python bench.py --no-cpu --config 1 > gpurun_out/cla4_bench1.log 2>&1; echo "bench1 rc=$?"
+timeout 300 python -m pytest tests/test_gpu_en.py -x -q > gpurun_out/cla4_pytest.log 2>&1; echo "pytest rc=$?"

@@ -288,6 +288,8 @@ struct rac_en_ctx {
   int cov_full = 0;           // whole inverse per CTA (en_cov.cuh full_inv)
   double *G = nullptr, *q = nullptr, *q2 = nullptr, *cwsum = nullptr, *cwmax = nullptr;
   int32_t* G_ids = nullptr;   // 0..n-1 (the single "block" of the full Gram)
+  double* G_ws = nullptr;     // split-K partials of G
+  size_t G_ws_cap = 0;
   // lookahead covariance chain (en_cla.cuh); cla_L = leader cluster size, 0 = not used
   int cla_L = 0, cla_D = 3, cla_W = 0, cla_segw = 1, cla_R = 2, cla_NS = 2;
   size_t cla_smem = 0;
@@ -414,7 +416,7 @@ bool cla_plan(rac_en_ctx* c) {
   const size_t lim = 226 * 1024;
   for (int L : {8, 16}) {
     const int sl = (s + L - 1) / L;
-    if (sl > 32) continue;
+    if (sl > 16) continue;   // main warps hold 16 rows of the step's operands in registers
     int NS = 0;
     for (int ns : {4, 2})
       if (cla_leader_doubles(L, s, D, ns) * sizeof(double) <= lim) { NS = ns; break; }
@@ -476,10 +478,19 @@ int en_compute_G(rac_en_ctx* c, cudaStream_t st) {
   using namespace rac;
   const int64_t n = c->n;
   GramPlan pl = plan_gram(c->m, (int)n, 1);
-  pl.splits = 1;
-  pl.chunk = (c->m + 31) / 32 * 32;
-  int rc = launch_gram(c->Xc, c->ld, c->m, c->G_ids, nullptr, (int)n, 1, c->G, pl, st, nullptr, (double)c->m);
-  if (rc) return rc;
+  int rc = RAC_OK;
+  // K split (better filled waves) when rac_en_set_gram_mode could reserve its workspace
+  const size_t wsb = (size_t)pl.splits * n * n * sizeof(double);
+  if (pl.splits > 1 && c->G_ws && c->G_ws_cap >= wsb) {
+    if ((rc = launch_gram(c->Xc, c->ld, c->m, c->G_ids, nullptr, (int)n, 1, c->G_ws, pl, st, nullptr)) ||
+        (rc = launch_gram_reduce_sym(c->G_ws, n, pl.splits, (double)c->m, c->G, st)))
+      return rc;
+  } else {
+    pl.splits = 1;
+    pl.chunk = (c->m + 31) / 32 * 32;
+    if ((rc = launch_gram(c->Xc, c->ld, c->m, c->G_ids, nullptr, (int)n, 1, c->G, pl, st, nullptr, (double)c->m)))
+      return rc;
+  }
   rc = launch_gemv_rows(c->G, n, n, c->beta, c->q, st);
   if (rc) return rc;
   c->have_G = true;
@@ -972,6 +983,22 @@ extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {
   c->cov_k = k;
   c->cov_full = plan & 1;
   c->gram_mode = 1;
+  {
+    // split-K workspace of G (en_compute_G), reserved here so no fit allocates in its sweep loop
+    const GramPlan pl = plan_gram(c->m, (int)c->n, 1);
+    const size_t wsb = (size_t)pl.splits * c->n * c->n * sizeof(double);
+    const char* env = getenv("RAC_G_SPLIT");
+    if (pl.splits > 1 && wsb <= ((size_t)1 << 30) && !(env && atoi(env) == 0) && c->G_ws_cap < wsb) {
+      double* w = nullptr;
+      if (dalloc(c, &w, wsb / sizeof(double)) == RAC_OK) {
+        c->G_ws = w;
+        c->G_ws_cap = wsb;
+      } else {
+        cudaGetLastError();
+        clear_error();
+      }
+    }
+  }
   if (!c->cla_L && cla_plan(c)) {
     const size_t tq = (size_t)c->p * c->cla_D * c->s * c->s;
     if ((rc = dalloc(c, &c->T_b[0], tq)) || (c->pipe && (rc = dalloc(c, &c->T_b[1], tq))) ||
@@ -1182,7 +1209,7 @@ extern "C" int rac_en_set_timing(rac_en_ctx* c, int32_t enable) {
   c->timing = enable != 0;
   if (enable >= 2 && !c->trace) {
     // chain stamps, then the factor kernel's (block 0): 8 + 16p | 8 + s
-    int rc = dalloc(c, &c->trace, 16 + 16 * (size_t)c->p + c->s);
+    int rc = dalloc(c, &c->trace, 16 + 28 * (size_t)c->p + c->s);   // + 8p clock64 stamps (lookahead chain)
     if (rc) return rc;
     c->trace_buf = c->trace;
   }
@@ -1196,8 +1223,9 @@ extern "C" int rac_en_info(rac_en_ctx* c, int32_t* info4) {
   if (!c || !info4) return set_error(RAC_ERR_ARG, "rac_en_info: bad arguments");
   info4[0] = (c->gram_mode == 1) ? (c->cla_L ? 3 : 2) : c->variant;
   info4[1] = (c->gram_mode == 1) ? (c->cla_L ? c->cla_L + c->cla_W : c->cov_k) : c->P;
-  info4[2] = c->RC;
-  info4[3] = c->nch;
+  // lookahead chain: [3, grid CTAs, sweeps per preparation batch, lookahead depth]
+  info4[2] = (c->gram_mode == 1 && c->cla_L) ? (c->pipe && c->idx_r ? c->cla_B : 1) : c->RC;
+  info4[3] = (c->gram_mode == 1 && c->cla_L) ? c->cla_D : c->nch;
   return RAC_OK;
 }
 
@@ -1205,7 +1233,7 @@ extern "C" int rac_en_trace(rac_en_ctx* c, int64_t* host, int32_t capacity) {
   using namespace rac;
   clear_error();
   if (!c || !host || !c->trace) return set_error(RAC_ERR_ARG, "rac_en_trace: tracing not enabled");
-  int k = std::min<int>(capacity, 16 + 16 * c->p + c->s);
+  int k = std::min<int>(capacity, 16 + 28 * c->p + c->s);
   return check_cuda(cudaMemcpy(host, c->trace, k * sizeof(int64_t), cudaMemcpyDeviceToHost), "trace copy");
 }
 

@@ -42,7 +42,8 @@
 namespace rac {
 
 constexpr int CLA_T = 512;     // threads per CTA (leader: 256 main + helper warps; worker: all)
-constexpr int CLA_MAIN = 256;  // leader critical-path threads
+constexpr int CLA_MAIN = 256;  // leader critical-path threads (8 warps)
+constexpr int CLA_HELP = 96;   // threads per leader helper group (3 warps; up to 2 groups, then 2 commit warps)
 constexpr int CLA_DMAX = 3;
 
 struct EnClaArgs {
@@ -73,8 +74,8 @@ struct EnClaArgs {
 
 __host__ __device__ inline size_t cla_leader_doubles(int L, int s, int D, int NS) {
   const size_t sl = (size_t)(s + L - 1) / L;
-  return (size_t)NS * (1 + D) * sl * s + (size_t)NS * 4 * sl + 2 * (size_t)NS * sl + 4 * (size_t)s +
-         2 * (size_t)L * s + 11 * sl + 32 + 512 + 2 * (3 * (size_t)NS + 2) + ((size_t)NS * sl + 1) / 2 + 1;   // + mbarriers, idx
+  return (size_t)NS * (1 + D) * sl * s + (size_t)NS * 4 * sl + 3 * (size_t)NS * sl + 4 * (size_t)s +
+         2 * (size_t)L * s + 21 * sl + 8 + 32 + 512 + (3 * (size_t)NS + 6) + ((size_t)NS * sl + 1) / 2 + 1;   // + mbarriers, idx
 }
 __host__ __device__ inline size_t cla_worker_doubles(int s, int segw, int R) {
   const size_t cw = 32 * (size_t)segw;
@@ -121,24 +122,26 @@ __device__ __forceinline__ void cla_leader(const EnClaArgs& a, double* sm) {
   double* sVec = sTile + (size_t)NS * tileD;     // [NS][4][sl]  c, xi, z, beta
   double* sBase = sVec + (size_t)NS * 4 * sl;    // [NS][sl]
   double* sTq = sBase + (size_t)NS * sl;         // [NS][sl]  sum_{d>=2} T_d D_{t-d}
-  double* sDelta = sTq + (size_t)NS * sl;        // [4][s]    ring of full deltas
+  double* sK = sTq + (size_t)NS * sl;            // [NS][sl]  -c - base + xi + gamma (z - beta) - tq
+  double* sDelta = sK + (size_t)NS * sl;         // [4][s]    ring of full deltas
   double* sRecv = sDelta + 4 * (size_t)s;        // [2][L][s] partials pushed by the ranks
-  double* sV = sRecv + 2 * (size_t)L * s;        // [sl]
-  double* sCorr = sV + sl;                       // [2][sl] (by step parity: read at commit)
-  double* wred = sCorr + 2 * sl;                 // [32]
-  double* sPart = wred + 32;                     // [8 * sl] T_1 partials (8 threads per row)
-  double* sHPart = sPart + 8 * sl;               // [2][256] helper partials (8 per row, rows <= 32)
+  const int sl2 = (sl + 1) & ~1;                 // keeps the double2 views below 16-byte aligned
+  double* sV = sRecv + 2 * (size_t)L * s;        // [sl2]
+  double* sCorr = sV + sl2;                      // [4][sl2]  q_t - base_t (ring: read by the commit warps)
+  double* wred = sCorr + 4 * sl2;                // [32]
+  double* sPart = wred + 32;                     // [16 * sl] T_1 partials (16 threads per row)
+  double* sHPart = sPart + 16 * sl;              // [2][256] helper partials (8 per row, rows <= 32)
   uint64_t* mb = reinterpret_cast<uint64_t*>(sHPart + 512);
-  uint64_t *mb_tma = mb, *mb_tq = mb + NS, *mb_free = mb + 2 * NS, *mb_x = mb + 3 * NS;
-  int* sIdx = reinterpret_cast<int*>(mb + 3 * NS + 2);   // [NS][sl] indices of this rank's rows
+  uint64_t *mb_tma = mb, *mb_tq = mb + NS, *mb_free = mb + 2 * NS, *mb_x = mb + 3 * NS, *mb_dl = mb + 3 * NS + 2;
+  int* sIdx = reinterpret_cast<int*>(mb + 3 * NS + 6);   // [NS][sl] indices of this rank's rows
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(mb_tma + i, 1);
-      mbar_init(mb_tq + i, 128);
-      mbar_init(mb_free + i, CLA_MAIN);
+      mbar_init(mb_tq + i, CLA_HELP);
+      mbar_init(mb_free + i, CLA_MAIN + 32);   // main warps + the step's commit warp
     }
-    mbar_init(mb_x + 0, 1);
-    mbar_init(mb_x + 1, 1);
+    for (int i = 0; i < 2; ++i) mbar_init(mb_x + i, 1);
+    for (int i = 0; i < 4; ++i) mbar_init(mb_dl + i, CLA_MAIN);
     mbar_fence_init();
   }
   cl.sync();   // every rank's barriers exist before anyone pushes into them
@@ -146,77 +149,106 @@ __device__ __forceinline__ void cla_leader(const EnClaArgs& a, double* sm) {
   const double gamma = a.gamma;
   auto blk = [&](int t) { return a.order ? a.order[t] : t; };
   double my_sum = 0.0, my_max = 0.0;
+  constexpr int HW0 = CLA_MAIN / 32;               // first helper warp
+  constexpr int CW0 = HW0 + 2 * (CLA_HELP / 32);   // first commit warp
 
-  if (warp < CLA_MAIN / 32) {
-    // ------------------------------------------------------------ main warps
+  if (warp < HW0) {
+    // ------------------------------------------------------------ main warps: the critical path
+    // step t: [A] T_1 term partials | [B] q_t, v | [C] P_k = inv[S_k,:]' v -> every rank |
+    //         [D] D_t = sum_k P_k, signal the commit warp, wait for step t+1's inputs
     const bool tr = a.trace && k == 0 && tid == 0;
-    if (tr) a.trace[0] = gtimer();
-    for (int t = 0; t < p; ++t) {
-      const int b = blk(t), slot = t % NS;
-      const unsigned ph = (unsigned)(t / NS) & 1u;
-      const int* bi = sIdx + slot * sl;   // this rank's rows of block t
-      // one thread polls the barriers; the others sleep in the named barrier (spinning
-      // warps would starve the helpers' shared-memory / shuffle traffic)
-      if (tid == 0) {
-        mbar_spin_sleep(mb_tq + slot, ph, 32);
-        mbar_spin(mb_tma + slot, ph);
-      }
-      named_bar_sync(1, CLA_MAIN);
-      if (tr) a.trace[1 + 5 * t] = gtimer();
-      __syncwarp();   // bar.sync does not reconverge a warp; diverged shuffles take a ~10x slower path
+    long long* ck = a.trace ? a.trace + 16 + 16 * (size_t)p + s : nullptr;   // clock64 stamps, 8 per step
+    // register-resident operands of the coming step (rows <= 16, s <= 256):
+    //   t1r[i] = T_1[r][part + 16 i]   (16 threads per row)      ivr[q] = inv[q][tid]  (column tid)
+    const int r16 = tid >> 4, part = tid & 15;
+    double t1r[16], ivr[16];
+    auto preload = [&](int t) {
+      const int slot = t % NS;
       const double* I = sTile + (size_t)slot * tileD;
       const double* T1 = I + (size_t)sl * s;
-      const double* vec = sVec + (size_t)slot * 4 * sl;
-      const double* dprev = sDelta + (size_t)((t - 1) & 3) * s;
-      // T_1 term: 8 threads per row, fixed-order combine of the 8 partials
-      {
-        const int r = tid >> 3, part = tid & 7;
-        double acc = 0.0;
-        if (r < rows && t >= 1) {
-          const double* row = T1 + (size_t)r * s;
-          double a1 = 0.0;
-          int c = part;
-          for (; c + 8 < s; c += 16) {
-            acc += row[c] * dprev[c];
-            a1 += row[c + 8] * dprev[c + 8];
-          }
-          if (c < s) acc += row[c] * dprev[c];
-          acc += a1;
-        }
-        if (r < rows) sPart[tid] = acc;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int c = part + 16 * i;
+        t1r[i] = (t >= 1 && r16 < rows && c < s) ? T1[(size_t)r16 * s + c] : 0.0;
       }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) ivr[q] = (q < rows && tid < s) ? I[(size_t)q * s + tid] : 0.0;
+    };
+    if (tr) a.trace[0] = gtimer();
+    if (p > 0) {
+      if (tid == 0) mbar_spin_sleep(mb_tq + 0, 0u, 32);
+      mbar_spin(mb_tma + 0, 0u);
+      preload(0);
+    }
+    named_bar_sync(1, CLA_MAIN);
+    for (int t = 0; t < p; ++t) {
+      const int slot = t % NS, xs = t & 1;
+      if (tr) { a.trace[1 + 5 * t] = gtimer(); ck[8 * t + 0] = clock64(); }
+      const double* dprev = sDelta + (size_t)((t - 1) & 3) * s;
+      // [A] T_1 D_{t-1}: 16 threads per row, operands in registers, four chains
+      if (r16 < rows) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          const int c = part + 16 * i;
+          if (c < s) a0 += t1r[i] * dprev[c];
+          if (c + 16 < s) a1 += t1r[i + 1] * dprev[c + 16];
+          if (c + 32 < s) a2 += t1r[i + 2] * dprev[c + 32];
+          if (c + 48 < s) a3 += t1r[i + 3] * dprev[c + 48];
+        }
+        sPart[tid] = (a0 + a1) + (a2 + a3);
+      }
+      if (tr) ck[8 * t + 1] = clock64();
       named_bar_sync(1, CLA_MAIN);
+      if (tr) { a.trace[2 + 5 * t] = gtimer(); ck[8 * t + 2] = clock64(); }
+      // [B] corr = tq + T_1 term;  v = (-c - base + xi + gamma (z - beta) - tq) - T_1 term
       if (tid < rows) {
         const int r = tid;
-        const double* pp = sPart + 8 * r;
-        const double acc = ((pp[0] + pp[1]) + (pp[2] + pp[3])) + ((pp[4] + pp[5]) + (pp[6] + pp[7]));
-        const double corr = sTq[slot * sl + r] + acc;
-        const double qt = sBase[slot * sl + r] + corr;
-        sCorr[(t & 1) * sl + r] = corr;
-        const int g = bi[r];
-        sV[r] = (g >= 0) ? add(add(sub(-vec[r], qt), vec[sl + r]), mul(gamma, sub(vec[2 * sl + r], vec[3 * sl + r])))
-                         : 0.0;
-      }
-      named_bar_sync(1, CLA_MAIN);
-      if (tr) a.trace[2 + 5 * t] = gtimer();
-      // partial of this rank's rows, pushed to every rank (itself included)
-      const int xs = t & 1;
-      for (int i = tid; 2 * i < s; i += CLA_MAIN) {
-        double p0 = 0.0, p1 = 0.0;
-        for (int r = 0; r < rows; ++r) {
-          const double2 w = *reinterpret_cast<const double2*>(I + (size_t)r * s + 2 * i);
-          p0 += w.x * sV[r];
-          p1 += w.y * sV[r];
+        const double2* pp = reinterpret_cast<const double2*>(sPart + 16 * r);
+        double q8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double2 w = pp[i];
+          q8[i] = w.x + w.y;
         }
-        const unsigned la = smem_u32(sRecv + ((size_t)xs * L + k) * s + 2 * i);
+        const double acc = ((q8[0] + q8[1]) + (q8[2] + q8[3])) + ((q8[4] + q8[5]) + (q8[6] + q8[7]));
+        sCorr[(t & 3) * sl2 + r] = sTq[slot * sl + r] + acc;
+        sV[r] = (sIdx[slot * sl + r] >= 0) ? sK[slot * sl + r] - acc : 0.0;
+      }
+      if (tr) ck[8 * t + 3] = clock64();
+      named_bar_sync(1, CLA_MAIN);
+      if (tr) { a.trace[3 + 5 * t] = gtimer(); ck[8 * t + 4] = clock64(); }
+      // [C] P_k[j] = sum_q inv[q][j] v[q] (inverse symmetric), pushed to every rank
+      if (tid < s) {
+        double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 16; q += 4) {
+          if (q < rows) p0 += ivr[q] * sV[q];
+          if (q + 1 < rows) p1 += ivr[q + 1] * sV[q + 1];
+          if (q + 2 < rows) p2 += ivr[q + 2] * sV[q + 2];
+          if (q + 3 < rows) p3 += ivr[q + 3] * sV[q + 3];
+        }
+        const double pj = (p0 + p1) + (p2 + p3);
+        const unsigned la = smem_u32(sRecv + ((size_t)xs * L + k) * s + tid);
         const unsigned lb = smem_u32(mb_x + xs);
 #pragma unroll
-        for (int pr = 0; pr < L; ++pr) st_async_f64x2(mapa_u32(la, pr), p0, p1, mapa_u32(lb, pr));
+        for (int pr = 0; pr < L; ++pr) st_async_f64(mapa_u32(la, pr), pj, mapa_u32(lb, pr));
       }
-      if (tid == 0) mbar_arrive_expect_tx(mb_x + xs, (unsigned)(L * s * sizeof(double)));
-      if (tr) a.trace[3 + 5 * t] = gtimer();
-      if (tid == 0) mbar_spin_cluster(mb_x + xs, (unsigned)(t >> 1) & 1u);
+      if (tid == 0) {
+        mbar_arrive_expect_tx(mb_x + xs, (unsigned)(L * s * sizeof(double)));
+        if (tr) { a.trace[4 + 5 * t] = gtimer(); ck[8 * t + 5] = clock64(); }
+      }
+      // while the exchange is in flight: operands of step t+1 into registers
+      if (t + 1 < p) {
+        mbar_spin(mb_tma + (t + 1) % NS, (unsigned)((t + 1) / NS) & 1u);
+        preload(t + 1);
+      }
+      if (tid == 0) {
+        mbar_spin_cluster(mb_x + xs, (unsigned)(t >> 1) & 1u);
+        if (tr) { a.trace[5 + 5 * t] = gtimer(); ck[8 * t + 6] = clock64(); }
+      }
       named_bar_sync(1, CLA_MAIN);
+      // [D] D_t in fixed rank order
       double* dcur = sDelta + (size_t)(t & 3) * s;
       for (int j = tid; j < s; j += CLA_MAIN) {
         const double* rv = sRecv + (size_t)xs * L * s + j;
@@ -225,33 +257,16 @@ __device__ __forceinline__ void cla_leader(const EnClaArgs& a, double* sm) {
         for (int pr = 1; pr < L; ++pr) d += rv[(size_t)pr * s];
         dcur[j] = d;
       }
+      mbar_arrive(mb_dl + (t & 3));     // the commit warp publishes D_t
+      mbar_arrive(mb_free + slot);      // this slot is no longer read by the main warps
+      if (tid == 0 && t + 1 < p) mbar_spin_sleep(mb_tq + (t + 1) % NS, (unsigned)((t + 1) / NS) & 1u, 32);
+      if (tr) ck[8 * t + 7] = clock64();
       named_bar_sync(1, CLA_MAIN);
-      if (tr) a.trace[4 + 5 * t] = gtimer();
-      if (tid < rows) {
-        const int r = tid, jj = j0 + r, g = bi[r];
-        const double d = dcur[jj];
-        unsigned long long* w = a.dpub + ((size_t)t * s + jj) * 4;
-        ll_store(w, d, tag);
-        ll_store(w + 2, sCorr[(t & 1) * sl + r], tag);
-        if (g >= 0) {
-          const double bn = add(vec[3 * sl + r], d);
-          const double x0 = vec[sl + r], zo = vec[2 * sl + r];
-          a.beta[g] = bn;
-          const double av = sub(x0, mul(gamma, bn));
-          const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
-          a.z[g] = zn;
-          a.xi[g] = sub(x0, mul(gamma, sub(bn, zn)));
-          my_sum += fabs(sub(bn, zn));
-          my_max = fmax(my_max, fabs(sub(zn, zo)));
-        }
-      }
-      mbar_arrive(mb_free + slot);
-      if (tr) a.trace[5 + 5 * t] = gtimer();
     }
-  } else if ((warp - CLA_MAIN / 32) / 4 < NH) {
-    // ------------------------------------------------------------ helper groups (4 warps each)
-    const int h = (warp - CLA_MAIN / 32) / 4;
-    const int gid = tid - CLA_MAIN - 128 * h;   // 0..127
+  } else if (warp < CW0 && (warp - HW0) / (CLA_HELP / 32) < NH) {
+    // ------------------------------------------------------------ helper groups: inputs of step u
+    const int h = (warp - HW0) / (CLA_HELP / 32);
+    const int gid = tid - CLA_MAIN - CLA_HELP * h;
     const int hb = 2 + h;                       // named barrier of this group
     double* hpart = sHPart + 256 * h;
     for (int u = h; u < p; u += NH) {
@@ -259,7 +274,7 @@ __device__ __forceinline__ void cla_leader(const EnClaArgs& a, double* sm) {
       const unsigned ph = (unsigned)(u / NS) & 1u;
       const int32_t* bi = a.idx + (int64_t)b * s;
       if (u >= NS && gid == 0) mbar_spin_sleep(mb_free + slot, (unsigned)((u - NS) / NS) & 1u);
-      named_bar_sync(hb, 128);
+      named_bar_sync(hb, CLA_HELP);
       const int nd = min(D, u);
       double* tile = sTile + (size_t)slot * tileD;
       const bool htr = a.trace && k == 0 && gid == 0;
@@ -301,14 +316,19 @@ __device__ __forceinline__ void cla_leader(const EnClaArgs& a, double* sm) {
       cp_async_commit();
       if (gid == 0) {
         if (htr) a.trace[2 + 5 * p + 4 * u] = gtimer();
-        if (u >= 2 && nd >= 2) mbar_spin_sleep(mb_free + (u - 2) % NS, (unsigned)((u - 2) / NS) & 1u, 32);   // D_{u-2} ready
+        // D_{u-2} in the ring: main's signal to the commit warp (phase of step u-2 of a 4-ring;
+        // main cannot lap it: step u+2 needs this helper's tq(u+2))
+        if (u >= 2 && nd >= 2) mbar_spin_sleep(mb_dl + ((u - 2) & 3), (unsigned)((u - 2) >> 2) & 1u, 32);
         mbar_spin_sleep(mb_tma + slot, ph, 32);
         if (htr) a.trace[3 + 5 * p + 4 * u] = gtimer();
       }
+      long long* hk = (htr) ? a.trace + 16 + 24 * (size_t)p + s + 4 * u : nullptr;
+      if (hk) hk[0] = clock64();
       cp_async_wait<0>();
-      named_bar_sync(hb, 128);
+      named_bar_sync(hb, CLA_HELP);
+      if (hk) hk[1] = clock64();
       // T_{d>=2} terms: 8 threads per row, partials combined in fixed order
-      for (int e = gid; e < rows * 8; e += 128) {
+      for (int e = gid; e < rows * 8; e += CLA_HELP) {
         const int r = e >> 3, part = e & 7;
         double a0 = 0.0, a1 = 0.0;
         for (int d = 2; d <= nd; ++d) {
@@ -323,13 +343,49 @@ __device__ __forceinline__ void cla_leader(const EnClaArgs& a, double* sm) {
         }
         hpart[e] = a0 + a1;
       }
-      named_bar_sync(hb, 128);
+      if (hk) hk[2] = clock64();
+      named_bar_sync(hb, CLA_HELP);
+      if (hk) hk[3] = clock64();
       if (gid < rows) {
-        const double* pp = hpart + 8 * gid;
-        sTq[slot * sl + gid] = ((pp[0] + pp[1]) + (pp[2] + pp[3])) + ((pp[4] + pp[5]) + (pp[6] + pp[7]));
+        const int r = gid;
+        const double* pp = hpart + 8 * r;
+        const double tq = ((pp[0] + pp[1]) + (pp[2] + pp[3])) + ((pp[4] + pp[5]) + (pp[6] + pp[7]));
+        sTq[slot * sl + r] = tq;
+        const double k1 = add(sub(-vec[r], sBase[slot * sl + r]), vec[sl + r]);   // -c - base + xi
+        sK[slot * sl + r] = sub(add(k1, mul(gamma, sub(vec[2 * sl + r], vec[3 * sl + r]))), tq);
       }
       if (htr) a.trace[4 + 5 * p + 4 * u] = gtimer();
       mbar_arrive(mb_tq + slot);
+    }
+  } else if (warp >= CW0) {
+    // ------------------------------------------------------------ commit warps (alternate steps):
+    // publish D_t[S_k] and corr for the workers, then beta / z / xi and the residuals
+    for (int t = warp - CW0; t < p; t += 2) {
+      const int slot = t % NS;
+      if (lane == 0) mbar_spin_sleep(mb_dl + (t & 3), (unsigned)(t >> 2) & 1u, 32);
+      __syncwarp();
+      const double* vec = sVec + (size_t)slot * 4 * sl;
+      const double* dcur = sDelta + (size_t)(t & 3) * s;
+      for (int r = lane; r < rows; r += 32) {
+        const int jj = j0 + r, g = sIdx[slot * sl + r];
+        const double d = dcur[jj];
+        unsigned long long* w = a.dpub + ((size_t)t * s + jj) * 4;
+        ll_store(w, d, tag);
+        ll_store(w + 2, sCorr[(t & 3) * sl2 + r], tag);
+        if (g >= 0) {
+          const double bn = add(vec[3 * sl + r], d);
+          const double x0 = vec[sl + r], zo = vec[2 * sl + r];
+          a.beta[g] = bn;
+          const double av = sub(x0, mul(gamma, bn));
+          const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
+          a.z[g] = zn;
+          a.xi[g] = sub(x0, mul(gamma, sub(bn, zn)));
+          my_sum += fabs(sub(bn, zn));
+          my_max = fmax(my_max, fabs(sub(zn, zo)));
+        }
+      }
+      __syncwarp();
+      mbar_arrive(mb_free + slot);
     }
   }
   // residuals: warp -> CTA -> rank 0

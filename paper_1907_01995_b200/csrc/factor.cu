@@ -329,42 +329,54 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
     for (int i = tid; i < s; i += CTHREADS) sbi[i] = bidx ? bidx[i] : i;
     __syncthreads();
     const double* wsb = a.ws ? a.ws + (int64_t)b * a.splits * s * s : nullptr;
-    for (int i = ty; i < s8; i += CTHREADS / 32) {
-      const int off = pk(i, 0);
+    // packed lower triangle, 8 independent gathers per thread in flight (one L2
+    // round trip per 8 * CTHREADS entries instead of one per row and warp)
+    const int ntri = s8 * (s8 + 1) / 2;
+    for (int e0 = 0; e0 < ntri; e0 += 8 * CTHREADS) {
       double v[8];
+      int pos[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int j = tx + 32 * u;
-        double e = (i == j) ? 1.0 : 0.0;
-        if (j <= i && i < s && j < s) {
-          const int gi = sbi[i], gj = sbi[j];
-          if (!(bidx && (gi < 0 || gj < 0))) {
-            double acc = 0.0;
-            if (wsb) {
-              const double* src = wsb + (int64_t)i * s + j;
-              acc = src[0];
-              for (int z = 1; z < a.splits; ++z) acc += src[(int64_t)z * s * s];
-              if (a.div != 1.0) acc = acc / a.div;
-              if (a.mul != 1.0) acc = a.mul * acc;
+        const int e = e0 + u * CTHREADS + tid;
+        pos[u] = e;
+        double val = 0.0;
+        if (e < ntri) {
+          int i = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+          while (pk(i + 1, 0) <= e) ++i;
+          while (pk(i, 0) > e) --i;
+          const int j = e - pk(i, 0);
+          val = (i == j) ? 1.0 : 0.0;
+          if (i < s && j < s) {
+            const int gi = sbi[i], gj = sbi[j];
+            if (!(bidx && (gi < 0 || gj < 0))) {
+              double acc = 0.0;
+              if (wsb) {
+                const double* src = wsb + (int64_t)i * s + j;
+                acc = src[0];
+                for (int z = 1; z < a.splits; ++z) acc += src[(int64_t)z * s * s];
+                if (a.div != 1.0) acc = acc / a.div;
+                if (a.mul != 1.0) acc = a.mul * acc;
+              }
+              if (a.H) {
+                const double h = a.H[(int64_t)gi * a.ldh + gj];
+                acc = wsb ? h + acc : h;
+              }
+              if (i == j) acc += a.shift;
+              val = acc;
             }
-            if (a.H) {
-              const double h = a.H[(int64_t)gi * a.ldh + gj];
-              acc = wsb ? h + acc : h;
-            }
-            if (i == j) acc += a.shift;
-            e = acc;
           }
         }
-        v[u] = e;
+        v[u] = val;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = tx + 32 * u;
-        if (j <= i && j < s8) P[off + j] = v[u];
-      }
-      if (hbo && i < s)
-        for (int j = tx; j < s; j += 32) hbo[(int64_t)i * s + j] = h_entry(a, bidx, i, j);
+      for (int u = 0; u < 8; ++u)
+        if (pos[u] < ntri) P[pos[u]] = v[u];
     }
+    if (hbo)
+      for (int e = tid; e < s * s; e += CTHREADS) {
+        const int i = e / s, j = e - i * s;
+        hbo[e] = h_entry(a, bidx, i, j);
+      }
     __syncthreads();
     if (a.ridge_rel > 0.0) {
       const double ridge = cta_ridge(a, bidx, s, [&](int i) { return P[pk(i, i)]; }, red);

@@ -204,6 +204,28 @@ int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx,
   return check_launch("gram");
 }
 
+// G[i][j] = G[j][i] = (sum_z ws[z][i][j]) / div for j <= i: the split-K partials of a
+// single full Gram summed in fixed split order (deterministic), scaled, mirrored.
+__global__ void gram_reduce_sym_kernel(const double* __restrict__ ws, int64_t n, int splits, double div,
+                                       double* __restrict__ G) {
+  const int64_t nn = n * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nn; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    if (j > i) continue;
+    double acc = ws[e];
+    for (int z = 1; z < splits; ++z) acc += ws[(int64_t)z * nn + e];
+    const double v = acc / div;
+    G[e] = v;
+    G[j * n + i] = v;
+  }
+}
+
+int launch_gram_reduce_sym(const double* ws, int64_t n, int splits, double div, double* G, cudaStream_t st) {
+  gram_reduce_sym_kernel<<<num_sms() * 8, 256, 0, st>>>(ws, n, splits, div, G);
+  note_launch();
+  return check_launch("gram reduce");
+}
+
 }  // namespace rac
 
 extern "C" size_t rac_gram_workspace_bytes(int64_t len, int32_t s, int32_t p) {

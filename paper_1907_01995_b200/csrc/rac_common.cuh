@@ -191,6 +191,11 @@ __device__ __forceinline__ unsigned mapa_u32(unsigned saddr, unsigned rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
+__device__ __forceinline__ void st_async_f64(unsigned raddr, double x, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(x),
+               "r"(rbar)
+               : "memory");
+}
 __device__ __forceinline__ void st_async_f64x2(unsigned raddr, double x, double y, unsigned rbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
                "d"(x), "d"(y), "r"(rbar)

@@ -45,6 +45,9 @@ int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx, c
 // sym_div > 0 (requires plan.splits == 1): ws receives the FULL symmetric s x s
 // matrix divided by sym_div (the covariance G = X'X/m).  sym_accum: the full
 // symmetric raw sums are ADDED to ws (row-chunk streaming of G).
+// fixed-order sum of the split partials of ONE full Gram (ws [splits][n][n], lower part
+// valid), divided by div, written as the full symmetric n x n matrix
+int launch_gram_reduce_sym(const double* ws, int64_t n, int splits, double div, double* G, cudaStream_t st);
 // K3: assemble block systems, Cholesky, explicit inverse.
 struct SysArgs {
   const double* ws;   // [p][splits][s][s] partial Grams (lower), may be null

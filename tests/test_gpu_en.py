@@ -289,3 +289,48 @@ def test_streamed_ingest_matches_resident_input(lib, gram):
         assert rel(a.beta, b.beta) <= 1e-12
     ref = ro.en_fit(X, y, mode="rac", lam=0.05, alpha=0.8, gamma=1.0, block_size=100, iters=15, seed=2)
     assert rel(a.beta, ref["beta"]) <= ITER_TOL
+
+
+@pytest.mark.parametrize("depth", ["1", "2", "3"])
+def test_lookahead_chain_vs_oracle_shapes(lib, monkeypatch, depth):
+    """Lookahead covariance chain (en_cla.cuh; even n and s): padded last block (n % s != 0),
+    fewer 32-column segments than a worker cluster, rp mode (tiles follow the visit order),
+    s > 128 (16-rank leader cluster), p >= 8 (tile-slot ring wraps), every lookahead depth;
+    per-sweep iterates against the oracle."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import elastic_net as en
+    from paper_1907_01995_b200.problems import Mode
+    monkeypatch.setenv("RAC_CLA_D", depth)
+    rng = np.random.default_rng(23)
+    for (m, n, s, mode, alpha) in [(500, 610, 40, "rac", 0.6), (200, 96, 12, "rac", 1.0),
+                                   (300, 420, 30, "rp", 0.3), (400, 600, 150, "rac", 0.9),
+                                   (120, 64, 64, "rac", 0.5), (260, 2000, 100, "rac", 1.0)]:
+        X = rng.standard_normal((m, n))
+        y = X[:, :5] @ rng.standard_normal(5) + 0.1 * rng.standard_normal(m)
+        kw = dict(lam=0.05, alpha=alpha, gamma=0.8, block_size=s, iters=9, seed=4)
+        caps = {}
+        ro.en_fit(X, y, mode=mode, **kw,
+                  on_sweep=lambda k, bl, b, z, xi: caps.__setitem__(k, (b.copy(), z.copy(), xi.copy())))
+        got = {}
+        en.fit(X, y, en.ElasticNetSpec(mode=Mode(mode), **kw), gram_mode="covariance",
+               sweep_hook=lambda k, b, z, xi: got.__setitem__(k, (b, z, xi)))
+        for k in caps:
+            for a_, b_ in zip(got[k], caps[k]):
+                assert rel(a_, b_) <= ITER_TOL, (m, n, s, mode, k)
+
+
+def test_lookahead_chain_determinism_and_previous_form(lib, monkeypatch):
+    """Batched sweeps through the lookahead chain are bit-identical run to run and agree
+    with the previous single-cluster covariance chain (RAC_COV_LA=0) to the parity bar."""
+    from paper_1907_01995_b200 import elastic_net as en
+    rng = np.random.default_rng(29)
+    X = rng.standard_normal((2000, 800))
+    y = X[:, :8] @ rng.standard_normal(8) + 0.1 * rng.standard_normal(2000)
+    spec = en.ElasticNetSpec(lam=0.05, alpha=0.8, block_size=50, iters=40, seed=6)
+    a = en.fit(X, y, spec, gram_mode="covariance")
+    b = en.fit(X, y, spec, gram_mode="covariance")
+    assert np.array_equal(a.beta, b.beta) and np.array_equal(a.z, b.z) and np.array_equal(a.xi, b.xi)
+    assert np.array_equal(a.residual_history, b.residual_history)
+    monkeypatch.setenv("RAC_COV_LA", "0")
+    c = en.fit(X, y, spec, gram_mode="covariance")
+    assert rel(a.beta, c.beta) <= ITER_TOL and rel(a.z, c.z) <= ITER_TOL

@@ -37,7 +37,12 @@ tm("_device.upload", lambda: _device.upload(X, device=dev))
 rng = np.random.default_rng(0)
 tm("host permutation x%d" % K, lambda: [rng.permutation(n) for _ in range(K)])
 sol = en.EnSolver(m, n, case.block_size, Mode.RAC, case.lam, case.alpha, case.gamma)
-tm("set_data", lambda: sol.set_data(X, y))
+gm = en.choose_gram_mode(m, n, case.block_size, K)
+if gm == "covariance":
+    sol.set_gram_mode("covariance")
+tm("set_data (%s)" % gm, lambda: sol.set_data(X, y))
+Xt = torch.from_numpy(X)
+tm("stream_rows copy only", lambda: _device.stream_rows(X, 32, lambda r0, rows, d: None, device=dev))
 feeder = _device.PermutationFeeder(rng, n, dev)
 perms = feeder.draw(K)
 tm("run K sweeps (device)", lambda: sol.run(perms, None))

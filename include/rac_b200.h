@@ -138,6 +138,10 @@ int rac_en_timing(rac_en_ctx* ctx, double* stage_ms_host4, int32_t* sweeps_host)
  * data wait, rhs, delta + cluster sync, tile wait, row pass 1, row sync, row
  * pass 2, row pass 3, next-block issue]. */
 int rac_en_trace(rac_en_ctx* ctx, int64_t* host, int32_t capacity);
+/* Debugging aid (no reference counterpart): progress markers of the lookahead
+ * covariance chain are written to `mapped_host`, a device-accessible pinned host
+ * buffer of >= 16 int64 (NULL switches it off); readable while a kernel runs. */
+int rac_debug_buffer(void* mapped_host);
 /* [chain variant (0 streaming, 1 resident-tile cluster), CTAs, rows per chunk, chunks per CTA] */
 int rac_en_info(rac_en_ctx* ctx, int32_t* info_host4);
 int rac_en_destroy(rac_en_ctx* ctx);

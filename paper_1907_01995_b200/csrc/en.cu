@@ -295,7 +295,10 @@ struct rac_en_ctx {
   size_t cla_smem = 0;
   double* T = nullptr;        // [p][D][s][s] tiles of the current sweep
   double* T_b[2] = {nullptr, nullptr};
-  unsigned long long *dpub = nullptr, *qst = nullptr;
+  unsigned long long *dpub = nullptr, *qst = nullptr;   // [cla_B p][s][2] tagged messages (delta, base)
+  double* snap = nullptr;     // [cla_B][3][n] per-sweep beta/z/xi (speculative sweeps after convergence)
+  int32_t* conv = nullptr;    // [2] launch's first sweep, converged sweep within it
+  unsigned* ccnt = nullptr;   // [CLA_BMAX] per-sweep commit counters of one launch
   // batched preparation (pipelined RAC): the block systems and tiles of cla_B sweeps are
   // formed by one launch on the prep stream, ring of 2 batches
   int cla_B = 1, batch_ctr = 0;
@@ -396,6 +399,8 @@ int cov_plan(int s, int64_t n, int p) {
   return 0;
 }
 
+volatile long long* g_cla_dbg = nullptr;   // rac_debug_buffer (mapped host memory)
+
 void* cla_kernel(int L) { return L == 16 ? (void*)rac::en_cla_kernel<16> : (void*)rac::en_cla_kernel<8>; }
 
 // Lookahead chain plan: leader cluster L (8, else 16) with at most 32 rows per
@@ -411,15 +416,17 @@ bool cla_plan(rac_en_ctx* c) {
   const int64_t n = c->n;
   if ((s & 1) || (n & 1) || s > 256 || n > 20000) return false;
   const char* envd = getenv("RAC_CLA_D");
-  const int D = envd ? std::max(1, std::min(CLA_DMAX, atoi(envd))) : 3;
+  const int Dwant = envd ? std::max(1, std::min(CLA_DMAX, atoi(envd))) : 3;
   const int nseg = (int)((n + 31) / 32);
   const size_t lim = 226 * 1024;
   for (int L : {8, 16}) {
     const int sl = (s + L - 1) / L;
     if (sl > 16) continue;   // main warps hold 16 rows of the step's operands in registers
-    int NS = 0;
-    for (int ns : {4, 2})
-      if (cla_leader_doubles(L, s, D, ns) * sizeof(double) <= lim) { NS = ns; break; }
+    // deepest lookahead (then most tile slots) whose leader tiles fit in shared memory
+    int NS = 0, D = 0;
+    for (int dd = Dwant; dd >= 1 && !NS; --dd)
+      for (int ns : {4, 2})
+        if (cla_leader_doubles(L, s, dd, ns) * sizeof(double) <= lim) { NS = ns; D = dd; break; }
     if (!NS) continue;
     void* kf = cla_kernel(L);
     if ((L > 8 && cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) ||
@@ -466,7 +473,7 @@ bool cla_plan(rac_en_ctx* c) {
 int launch_cla_tiles(rac_en_ctx* c, cudaStream_t st, int sweeps = 1) {
   using namespace rac;
   if (!c->cla_L || c->p < 2) return RAC_OK;
-  cla_tiles_kernel<<<dim3(c->p * c->cla_D, sweeps), dim3(32, 8), 0, st>>>(
+  cla_tiles_kernel<<<c->p * c->cla_D * sweeps, 256, 0, st>>>(
       c->G, c->n, c->s, c->p, c->cla_D, c->idx, (c->mode == RAC_MODE_RP) ? c->order : nullptr, c->T, c->ctrl);
   note_launch();
   return check_launch("cla tiles");
@@ -537,13 +544,19 @@ int en_block_systems(rac_en_ctx* c) {
   return en_factor(c, c->st);
 }
 
-int en_chain_cla(rac_en_ctx* c, double tol, cudaStream_t st) {
+int en_chain_cla(rac_en_ctx* c, double tol, cudaStream_t st, int nsw) {
   using namespace rac;
   EnClaArgs a{};
   a.G = c->G;
   a.n = c->n;
   a.s = c->s;
   a.p = c->p;
+  a.nsw = nsw;
+  a.snap = (nsw > 1 && tol >= 0.0) ? c->snap : nullptr;
+  a.conv = c->conv;
+  a.ccnt = c->ccnt;
+  a.dbg = g_cla_dbg;
+  cudaMemsetAsync(c->ccnt, 0, CLA_BMAX * sizeof(unsigned), st);
   a.idx = c->idx;
   a.order = (c->mode == RAC_MODE_RP) ? c->order : nullptr;
   a.inv = c->inv;
@@ -556,8 +569,6 @@ int en_chain_cla(rac_en_ctx* c, double tol, cudaStream_t st) {
   a.q = c->q;
   a.dpub = c->dpub;
   a.qst = c->qst;
-  a.wsum = c->cwsum;
-  a.wmax = c->cwmax;
   a.ctrl = c->ctrl;
   a.gamma = c->gamma;
   a.thr = c->lam * c->alpha;
@@ -589,12 +600,17 @@ int en_chain_cla(rac_en_ctx* c, double tol, cudaStream_t st) {
   static const bool noncoop = getenv("RAC_PROFILE_NONCOOP") && atoi(getenv("RAC_PROFILE_NONCOOP")) == 1;
   cfg.numAttrs = noncoop ? 1 : 2;
   note_launch();
-  return check_cuda(cudaLaunchKernelExC(&cfg, cla_kernel(c->cla_L), args), "en_cla (cluster cooperative launch)");
+  int rc = check_cuda(cudaLaunchKernelExC(&cfg, cla_kernel(c->cla_L), args), "en_cla (cluster cooperative launch)");
+  if (rc || !a.snap) return rc;
+  cla_restore_kernel<<<std::max(1, std::min(num_sms(), (int)((c->n + 255) / 256))), 256, 0, st>>>(
+      c->conv, c->sweeps, nsw, c->n, c->snap, c->beta, c->z, c->xi);
+  note_launch();
+  return check_launch("cla restore");
 }
 
-int en_chain_cov(rac_en_ctx* c, double tol, cudaStream_t st) {
+int en_chain_cov(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
   using namespace rac;
-  if (c->cla_L) return en_chain_cla(c, tol, st);
+  if (c->cla_L) return en_chain_cla(c, tol, st, nsw);
   EnCovArgs a{};
   a.G = c->G;
   a.n = c->n;
@@ -639,9 +655,9 @@ int en_chain_cov(rac_en_ctx* c, double tol, cudaStream_t st) {
   return check_cuda(cudaLaunchKernelExC(&cfg, cov_kernel(c->cov_k), args), "en_cov (cluster launch)");
 }
 
-int en_chain(rac_en_ctx* c, double tol, cudaStream_t st) {
+int en_chain(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
   using namespace rac;
-  if (c->gram_mode == 1) return en_chain_cov(c, tol, st);
+  if (c->gram_mode == 1) return en_chain_cov(c, tol, st, nsw);
   cudaMemsetAsync(c->bar, 0, sizeof(unsigned), st);
   EnChainArgs a{};
   a.Xc = c->Xc;
@@ -1001,8 +1017,7 @@ extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {
   }
   if (!c->cla_L && cla_plan(c)) {
     const size_t tq = (size_t)c->p * c->cla_D * c->s * c->s;
-    if ((rc = dalloc(c, &c->T_b[0], tq)) || (c->pipe && (rc = dalloc(c, &c->T_b[1], tq))) ||
-        (rc = dalloc(c, &c->dpub, (size_t)c->p * c->s * 4)) || (rc = dalloc(c, &c->qst, (size_t)c->p * c->s * 2))) {
+    if ((rc = dalloc(c, &c->T_b[0], tq)) || (c->pipe && (rc = dalloc(c, &c->T_b[1], tq)))) {
       c->cla_L = 0;
       return rc;
     }
@@ -1010,7 +1025,7 @@ extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {
       // sweeps per preparation batch: the factor CTAs (one per block) of a batch should fit
       // on the SMs the chain leaves free
       const int free_sms = std::max(0, num_sms() - (c->cla_L + c->cla_W));
-      c->cla_B = std::max(1, std::min(4, free_sms / std::max(1, c->p)));
+      c->cla_B = std::max(1, std::min(CLA_BMAX, free_sms / std::max(1, c->p)));
       if (chol_scratch_bytes(c->s, c->p) != 0) c->cla_B = 1;   // global factor scratch is sized for one sweep
       const int nb = 2 * c->cla_B;
       if ((rc = dalloc(c, &c->idx_r, (size_t)nb * c->p * c->s)) || (rc = dalloc(c, &c->info_r, (size_t)nb * c->p)) ||
@@ -1020,8 +1035,17 @@ extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {
       }
       cudaMemsetAsync(c->info_r, 0, (size_t)nb * c->p * sizeof(int32_t), c->st);
     }
-    cudaMemsetAsync(c->dpub, 0, (size_t)c->p * c->s * 4 * sizeof(unsigned long long), c->st);
-    cudaMemsetAsync(c->qst, 0, (size_t)c->p * c->s * 2 * sizeof(unsigned long long), c->st);
+    // tagged message slots for every global step of one launch (cla_B sweeps), snapshots
+    const size_t ps = (size_t)c->cla_B * c->p * c->s;
+    if ((rc = dalloc(c, &c->dpub, ps * 2)) || (rc = dalloc(c, &c->qst, ps * 2)) || (rc = dalloc(c, &c->conv, 2)) ||
+        (rc = dalloc(c, &c->ccnt, CLA_BMAX)) ||
+        (c->cla_B > 1 && (rc = dalloc(c, &c->snap, (size_t)c->cla_B * 3 * c->n)))) {
+      c->cla_L = 0;
+      return rc;
+    }
+    cudaMemsetAsync(c->dpub, 0, ps * 2 * sizeof(unsigned long long), c->st);
+    cudaMemsetAsync(c->qst, 0, ps * 2 * sizeof(unsigned long long), c->st);
+    cudaMemsetAsync(c->conv, 0xff, 2 * sizeof(int32_t), c->st);
     c->T = c->T_b[0];
   }
   return RAC_OK;
@@ -1074,14 +1098,9 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
       if ((rc = en_factor(c, c->sprep, bs))) return rc;
       cudaEventRecord(c->ev_prep[j], c->sprep);
       cudaStreamWaitEvent(c->schain, c->ev_prep[j], 0);
-      for (int q = 0; q < bs; ++q) {
-        c->idx = c->idx_r + ((size_t)j * B + q) * ps;
-        c->inv = c->inv_r + ((size_t)j * B + q) * pss;
-        c->info = c->info_r + ((size_t)j * B + q) * c->p;
-        c->T = c->T_r + ((size_t)j * B + q) * pT;
-        if ((rc = en_chain(c, tol, c->schain))) return rc;
-        c->sweeps++;
-      }
+      // the batch's sweeps run as one chain launch (c->idx/inv/info/T: batch base)
+      if ((rc = en_chain(c, tol, c->schain, bs))) return rc;
+      c->sweeps += bs;
       cudaEventRecord(c->ev_chain[j], c->schain);
       c->chain_rec[j] = true;
       c->batch_ctr++;
@@ -1270,5 +1289,12 @@ extern "C" int rac_en_destroy(rac_en_ctx* c) {
   if (c->sprep) cudaStreamDestroy(c->sprep);
   for (void* q : c->allocs) rac::dev_free(q, c->st);
   delete c;
+  return RAC_OK;
+}
+
+// Debugging aid: progress markers of the lookahead chain are written to this
+// device-accessible (mapped, pinned) host buffer of >= 16 int64 (null: off).
+extern "C" int rac_debug_buffer(void* mapped_host) {
+  g_cla_dbg = (volatile long long*)mapped_host;
   return RAC_OK;
 }

@@ -54,13 +54,18 @@ __device__ __forceinline__ void grid_barrier(unsigned* counter, unsigned& target
 // ---------------------------------------------------------------------------
 // reductions (fixed order => bitwise run-to-run determinism)
 // ---------------------------------------------------------------------------
+// Callers are always all 32 lanes.  The __syncwarp reconverges a warp that
+// arrives diverged (measured: a diverged double warp_sum costs ~2350 cycles
+// instead of ~200 — scripts/micro/shfl_probe.cu).
 __device__ __forceinline__ double warp_sum(double v) {
+  __syncwarp();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
 __device__ __forceinline__ double warp_max(double v) {
+  __syncwarp();
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
@@ -199,6 +204,15 @@ __device__ __forceinline__ void st_async_f64(unsigned raddr, double x, unsigned 
 __device__ __forceinline__ void st_async_f64x2(unsigned raddr, double x, double y, unsigned rbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
                "d"(x), "d"(y), "r"(rbar)
+               : "memory");
+}
+
+// bulk copy own shared memory -> a peer CTA's shared memory (TMA engine), completing
+// `bytes` on the peer's mbarrier; dst / bar are shared::cluster addresses (mapa)
+__device__ __forceinline__ void bulk_s2peer(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst),
+               "r"(smem_u32(src)), "r"(bytes), "r"(bar)
                : "memory");
 }
 

@@ -144,6 +144,11 @@ int rac_en_trace(rac_en_ctx* ctx, int64_t* host, int32_t capacity);
 int rac_debug_buffer(void* mapped_host);
 /* [chain variant (0 streaming, 1 resident-tile cluster), CTAs, rows per chunk, chunks per CTA] */
 int rac_en_info(rac_en_ctx* ctx, int32_t* info_host4);
+/* Re-arm a context for a new fit with the same shape (m, n, block size, mode):
+ * iterates, history and failure state cleared, data / partition / G must be set
+ * again; buffers, plans and streams are kept (fit()'s context pool).  The tags
+ * of the lookahead chain's messages keep increasing across resets. */
+int rac_en_reset(rac_en_ctx* ctx, double lam, double alpha, double gamma);
 int rac_en_destroy(rac_en_ctx* ctx);
 
 /* ------------------------------------------------------------------ train()/solve()

@@ -256,7 +256,8 @@ struct rac_en_ctx {
   int cs = 2;                 // its cluster size (2, 4 or 8)
   rac::GramPlan gp{};
   bool have_data = false, have_partition = false;
-  int sweeps = 0;        // sweeps enqueued so far
+  int sweeps = 0;        // sweeps enqueued so far (history index; reset by rac_en_reset)
+  unsigned msg_tag = 0;  // lookahead-chain launches so far: tag of the tagged messages (never reset)
   int hist_cap = 0;
   // device buffers
   double *Xc = nullptr, *y = nullptr, *c = nullptr, *beta = nullptr, *z = nullptr, *xi = nullptr,
@@ -552,6 +553,7 @@ int en_chain_cla(rac_en_ctx* c, double tol, cudaStream_t st, int nsw) {
   a.s = c->s;
   a.p = c->p;
   a.nsw = nsw;
+  a.tag = ++c->msg_tag;
   a.snap = (nsw > 1 && tol >= 0.0) ? c->snap : nullptr;
   a.conv = c->conv;
   a.ccnt = c->ccnt;
@@ -1275,6 +1277,37 @@ extern "C" int rac_en_timing(rac_en_ctx* c, double* stage_ms, int32_t* sweeps) {
   c->events.clear();
   if (sweeps) *sweeps = (int32_t)k;
   return RAC_OK;
+}
+
+extern "C" int rac_en_reset(rac_en_ctx* c, double lam, double alpha, double gamma) {
+  using namespace rac;
+  clear_error();
+  if (!c || !(gamma > 0) || lam < 0 || alpha < 0 || alpha > 1) return set_error(RAC_ERR_ARG, "rac_en_reset: bad arguments");
+  cudaStream_t st = c->st;
+  if (c->pipe) {
+    // previous work on the helper streams completes before their buffers are reused
+    cudaEventRecord(c->ev_end, c->schain);
+    cudaStreamWaitEvent(st, c->ev_end, 0);
+    cudaEventRecord(c->ev_start, c->sprep);
+    cudaStreamWaitEvent(st, c->ev_start, 0);
+  }
+  c->lam = lam;
+  c->alpha = alpha;
+  c->gamma = gamma;
+  c->sweeps = 0;
+  c->have_data = false;
+  c->have_partition = false;
+  c->have_G = false;
+  cudaMemsetAsync(c->beta, 0, c->n * sizeof(double), st);
+  cudaMemsetAsync(c->z, 0, c->n * sizeof(double), st);
+  cudaMemsetAsync(c->xi, 0, c->n * sizeof(double), st);
+  cudaMemsetAsync(c->r, 0, c->ld * sizeof(double), st);
+  cudaMemsetAsync(c->ctrl, 0, 4 * sizeof(int32_t), st);
+  for (int32_t* inf : {c->info_b[0], c->info_b[1]})
+    if (inf) cudaMemsetAsync(inf, 0, c->p * sizeof(int32_t), st);
+  if (c->info_r) cudaMemsetAsync(c->info_r, 0, (size_t)2 * c->cla_B * c->p * sizeof(int32_t), st);
+  if (c->conv) cudaMemsetAsync(c->conv, 0xff, 2 * sizeof(int32_t), st);
+  return check_launch("rac_en_reset");
 }
 
 extern "C" int rac_en_destroy(rac_en_ctx* c) {

@@ -76,7 +76,8 @@ struct EnClaArgs {
                              // revisited in the next sweep is gathered only after its commit
   int32_t* ctrl;
   double gamma, thr, den, tol;
-  int sweep;                 // global index of the launch's first sweep
+  int sweep;                 // history index of the launch's first sweep
+  unsigned tag;              // message tag, unique per launch of a context (never reused, never 0)
   double *hist_p, *hist_d;
   long long* trace;  // optional (rank 0): first sweep's phase stamps
   int D;             // lookahead depth 1..3
@@ -216,7 +217,7 @@ __device__ __forceinline__ void cla_leader(const EnClaArgs& a, double* sm, int U
     mbar_fence_init();
   }
   cl.sync();   // every rank's barriers exist before anyone pushes into them
-  const unsigned tag = (unsigned)a.sweep + 1u;
+  const unsigned tag = a.tag;
   const double gamma = a.gamma;
   constexpr int HW0 = CLA_MAIN / 32;               // first helper warp
   constexpr int CW0 = HW0 + 2 * (CLA_HELP / 32);   // first commit warp
@@ -548,7 +549,7 @@ __device__ __forceinline__ void cla_worker(const EnClaArgs& a, double* sm, int w
   const int ncol = (int)(c1 - c0);
   const int CW = 32 * a.segw;
   const int nswE = U / p;
-  const unsigned tag = (unsigned)a.sweep + 1u;
+  const unsigned tag = a.tag;
 
   double* sG = sm;                               // [R][s][CW]
   double* part = sG + (size_t)R * s * CW;        // [16][CW]

@@ -10,6 +10,8 @@ reference's PCG64 permutations and streams them to the device.
 from __future__ import annotations
 
 import math
+import os
+import threading
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -212,6 +214,23 @@ class EnSolver:
         _device.stream_rows(X, 32, consume, device=self.dev)
         self._keep = [yd, last.get("keep")]
 
+    def reset(self, lam: float, alpha: float, gamma: float) -> None:
+        """Re-arm for a new fit of the same shape (rac_en_reset): iterates, history and
+        failure state cleared; data (and partition / G) must be set again."""
+        _native.check(self.lib.rac_en_reset(self.h, float(lam), float(alpha), float(gamma)))
+        self._keep = []
+
+    def results(self, count: int):
+        """beta, z, xi and the first `count` residual histories in ONE device->host copy."""
+        n = self.n
+        buf = torch.empty(3 * n + 2 * max(count, 1), dtype=torch.float64, device=self.dev)
+        _native.check(self.lib.rac_en_get(self.h, buf.data_ptr(), buf[n:].data_ptr(), buf[2 * n:].data_ptr(), None))
+        if count > 0:
+            _native.check(self.lib.rac_en_history(self.h, buf[3 * n:].data_ptr(), buf[3 * n + count:].data_ptr(),
+                                                  count))
+        h = buf.cpu().numpy()
+        return h[:n], h[n:2 * n], h[2 * n:3 * n], h[3 * n:3 * n + count], h[3 * n + count:3 * n + 2 * count]
+
     def set_partition(self, perm_dev: torch.Tensor) -> None:
         _native.check(self.lib.rac_en_set_partition(self.h, perm_dev.data_ptr()))
 
@@ -240,6 +259,36 @@ class EnSolver:
 
 
 COV_MAX_N = 20000
+
+# fit() reuses native contexts of the same shape (rac_en_reset) instead of creating and
+# destroying one per call: streams, events, plans and pool buffers stay; each fit holds
+# its context exclusively.
+_POOL: dict = {}
+_POOL_LOCK = threading.Lock()
+_POOL_PER_KEY = 2
+
+
+def _acquire_solver(m, n, block_size, mode, lam, alpha, gamma, device):
+    # RAC_* environment switches select native variants when a context is created / planned
+    env = tuple(sorted((k, v) for k, v in os.environ.items() if k.startswith("RAC_")))
+    key = (m, n, min(int(block_size), n), Mode(mode), device, _device.stream_handle(), env)
+    with _POOL_LOCK:
+        lst = _POOL.get(key)
+        solver = lst.pop() if lst else None
+    if solver is not None:
+        solver.reset(lam, alpha, gamma)
+        return key, solver
+    return key, EnSolver(m, n, block_size, mode, lam, alpha, gamma, device=device)
+
+
+def _release_solver(key, solver, ok: bool) -> None:
+    if ok:
+        with _POOL_LOCK:
+            lst = _POOL.setdefault(key, [])
+            if len(lst) < _POOL_PER_KEY:
+                lst.append(solver)
+                return
+    solver.close()
 
 
 def choose_gram_mode(m: int, n: int, block_size: int, iters: int) -> str:
@@ -275,7 +324,8 @@ def fit(X: Matrix, y: np.ndarray, spec: ElasticNetSpec, *, sweep_hook=None,
     gamma = resolve_gamma(spec, X)
     mode = Mode(spec.mode)
     rng = np.random.default_rng(spec.seed)
-    solver = EnSolver(m, n, spec.block_size, mode, spec.lam, spec.alpha, gamma, device=device)
+    key, solver = _acquire_solver(m, n, spec.block_size, mode, spec.lam, spec.alpha, gamma, device)
+    ok = False
     try:
         gm = choose_gram_mode(m, n, spec.block_size, spec.iters) if gram_mode == "auto" else gram_mode
         if gm == "covariance":
@@ -284,6 +334,9 @@ def fit(X: Matrix, y: np.ndarray, spec: ElasticNetSpec, *, sweep_hook=None,
             except _native.NativeError as e:
                 if e.code != _native.RAC_ERR_UNSUPPORTED or gram_mode != "auto":
                     raise
+                solver.set_gram_mode("blocks")
+        else:
+            solver.set_gram_mode("blocks")
         solver.set_data(X, y)
         if mode == Mode.RP:
             solver.set_partition(_device.PermutationFeeder(rng, n, solver.dev).draw(1))
@@ -300,6 +353,7 @@ def fit(X: Matrix, y: np.ndarray, spec: ElasticNetSpec, *, sweep_hook=None,
             if sweep_hook is not None or spec.tol is not None or done >= spec.iters:
                 iterations, converged, _, failed = solver.progress()
                 if failed >= 0:
+                    ok = True   # the context itself is sound; the next fit resets it
                     raise BlockDefinitenessError(
                         "sub-block Gram matrix plus gamma*I is not positive definite; the "
                         "sub-block positive-definiteness requirement is violated")
@@ -310,15 +364,15 @@ def fit(X: Matrix, y: np.ndarray, spec: ElasticNetSpec, *, sweep_hook=None,
                     break
         iterations, converged, residual, failed = solver.progress()
         if failed >= 0:
+            ok = True   # the context itself is sound; the next fit resets it
             raise BlockDefinitenessError(
                 "sub-block Gram matrix plus gamma*I is not positive definite; the "
                 "sub-block positive-definiteness requirement is violated")
-        b, z, xi = solver.state()
-        hp, hd = solver.history(iterations)
-        return ElasticNetModel(beta=b.cpu().numpy(), z=z.cpu().numpy(), xi=xi.cpu().numpy(),
+        b, z, xi, hp, hd = solver.results(iterations)
+        ok = True
+        return ElasticNetModel(beta=b.copy(), z=z.copy(), xi=xi.copy(),
                                spec=spec, gamma=gamma, iterations=iterations,
                                residual=residual if iterations else math.inf,
-                               residual_history=hp.cpu().numpy(),
-                               dual_residual_history=hd.cpu().numpy())
+                               residual_history=hp.copy(), dual_residual_history=hd.copy())
     finally:
-        solver.close()
+        _release_solver(key, solver, ok)

@@ -452,9 +452,12 @@ bool cla_plan(rac_en_ctx* c) {
       cudaGetLastError();
       continue;
     }
-    const int wclusters = std::min(clusters - 1, (nseg + L - 1) / L);
+    int wclusters = std::min(clusters - 1, (nseg + L - 1) / L);
+    const int segw = (nseg + wclusters * L - 1) / (wclusters * L);
+    // fewest worker clusters with the same segments per worker: the SMs they leave free
+    // run the next sweeps' block factorisations
+    wclusters = std::min(wclusters, (nseg + segw * L - 1) / (segw * L));
     const int W = wclusters * L;
-    const int segw = (nseg + W - 1) / W;
     int R = 0;
     for (int r : {4, 3, 2})
       if (cla_worker_doubles(s, segw, r) * sizeof(double) <= lim) { R = r; break; }
@@ -1028,7 +1031,16 @@ extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {
       // on the SMs the chain leaves free
       const int free_sms = std::max(0, num_sms() - (c->cla_L + c->cla_W));
       c->cla_B = std::max(1, std::min(CLA_BMAX, free_sms / std::max(1, c->p)));
-      if (chol_scratch_bytes(c->s, c->p) != 0) c->cla_B = 1;   // global factor scratch is sized for one sweep
+      // the factor's global scratch (Cholesky re-check / large-s path) must cover the batch
+      const size_t scr = chol_scratch_bytes(c->s, c->p * c->cla_B);
+      if (c->cla_B > 1 && scr > chol_scratch_bytes(c->s, c->p)) {
+        double* w = nullptr;
+        if ((rc = dalloc(c, &w, scr / sizeof(double)))) c->cla_B = 1;
+        else c->scratch = w;
+        cudaGetLastError();
+        clear_error();
+        rc = RAC_OK;
+      }
       const int nb = 2 * c->cla_B;
       if ((rc = dalloc(c, &c->idx_r, (size_t)nb * c->p * c->s)) || (rc = dalloc(c, &c->info_r, (size_t)nb * c->p)) ||
           (rc = dalloc(c, &c->inv_r, (size_t)nb * c->p * c->s * c->s)) || (rc = dalloc(c, &c->T_r, (size_t)nb * tq))) {

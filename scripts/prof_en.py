@@ -14,7 +14,9 @@ gram = sys.argv[3] if len(sys.argv) > 3 else en.choose_gram_mode(m, n, case.bloc
 sol = en.EnSolver(m, n, case.block_size, Mode.RAC, case.lam, case.alpha, case.gamma)
 if gram == "covariance":
     sol.set_gram_mode("covariance")
-sol.set_data(case.X, case.y)
+# device-resident X (rac_en_set_data): G is formed by one split-K Gram + reduce at the
+# first run, so a kernel-filtered ncu capture sees G -> factor -> tiles -> chain in order
+sol.set_data(torch.from_numpy(case.X).cuda(), case.y)
 perms = _device.PermutationFeeder(np.random.default_rng(0), n, sol.dev).draw(sweeps)
 sol.run(perms, None)
 torch.cuda.synchronize()

@@ -50,6 +50,37 @@ __device__ __forceinline__ RowPhaseSmem carve_rowphase(double* base, int s) {
   return w;
 }
 
+// sum_{j = j0, j0 + step, ...} col[j * ld] * v[j] with four independent chains (the row
+// phase is latency-bound: few warps, dependent shared-memory loads); fixed order, so
+// results stay deterministic
+__device__ __forceinline__ double strided_dot(const double* col, const double* v, int j0, int s, int step,
+                                              int ld) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int j = j0;
+  for (; j + 3 * step < s; j += 4 * step) {
+    a0 += col[j * ld] * v[j];
+    a1 += col[(j + step) * ld] * v[j + step];
+    a2 += col[(j + 2 * step) * ld] * v[j + 2 * step];
+    a3 += col[(j + 3 * step) * ld] * v[j + 3 * step];
+  }
+  for (; j < s; j += step) a0 += col[j * ld] * v[j];
+  return (a0 + a1) + (a2 + a3);
+}
+
+// sum_{q < NG} red[q * ld + t], four chains
+template <int NG>
+__device__ __forceinline__ double group_sum(const double* red, int ld, int t) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+  for (int q = 0; q < NG; q += 4) {
+    a0 += red[q * ld + t];
+    if (q + 1 < NG) a1 += red[(q + 1) * ld + t];
+    if (q + 2 < NG) a2 += red[(q + 2) * ld + t];
+    if (q + 3 < NG) a3 += red[(q + 3) * ld + t];
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
 // T(i, acc_i, u_i) -> t_i
 template <int RC, class TFn>
 __device__ void row_phase(const double* __restrict__ V, int64_t ld, int64_t m, int nrc,
@@ -98,25 +129,16 @@ __device__ void row_phase(const double* __restrict__ V, int64_t ld, int64_t m, i
     cp_async_wait<0>();
     __syncthreads();
     if (bprev >= 0) {
-      double u = 0.0;
-      for (int j = grp; j < s; j += NG) u += w.tile[j * (RC + 1) + ri] * w.sDel[j];
-      w.red[grp * RC + ri] = u;
+      w.red[grp * RC + ri] = strided_dot(w.tile + ri, w.sDel, grp, s, NG, RC + 1);
       __syncthreads();
-      if (tid < rows) {
-        double tot = w.red[tid];
-        for (int q = 1; q < NG; ++q) tot += w.red[q * RC + tid];
-        acc[i0 + tid] += tot;
-      }
+      if (tid < rows) acc[i0 + tid] += group_sum<NG>(w.red, RC, tid);
       __syncthreads();
     }
     if (bnext >= 0) {
-      double u = 0.0;
-      for (int j = grp; j < s; j += NG) u += w.tile2[j * (RC + 1) + ri] * w.sXn[j];
-      w.red[grp * RC + ri] = u;
+      w.red[grp * RC + ri] = strided_dot(w.tile2 + ri, w.sXn, grp, s, NG, RC + 1);
       __syncthreads();
       if (tid < RC) {
-        double tot = w.red[tid];
-        for (int q = 1; q < NG; ++q) tot += w.red[q * RC + tid];
+        const double tot = group_sum<NG>(w.red, RC, tid);
         w.sT[tid] = (tid < rows) ? tfn(i0 + tid, acc[i0 + tid], tot) : 0.0;
       }
       __syncthreads();
@@ -125,10 +147,13 @@ __device__ void row_phase(const double* __restrict__ V, int64_t ld, int64_t m, i
         int j = tid + q * RP_THREADS;
         if (j < s) {
           const double* col = w.tile2 + j * (RC + 1);
-          double a = part[q];
-#pragma unroll 8
-          for (int i = 0; i < RC; ++i) a += col[i] * w.sT[i];
-          part[q] = a;
+          double a = 0.0, b = 0.0;
+#pragma unroll
+          for (int i = 0; i < RC; i += 2) {
+            a += col[i] * w.sT[i];
+            b += col[i + 1] * w.sT[i + 1];
+          }
+          part[q] += a + b;
         }
       }
     }

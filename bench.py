@@ -391,7 +391,7 @@ def run_b200_en(args, world, rank, local):
         t0 = time.perf_counter()
         done = 0
         while done < case.iters:
-            k = min(8, case.iters - done)
+            k = min(16, case.iters - done)   # fit()'s default batch: one progress check per 16 sweeps
             sol2.run(feeder.draw(k), case.tol)
             done += k
             it, conv, res, _ = sol2.progress()

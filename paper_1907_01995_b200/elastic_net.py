@@ -9,6 +9,8 @@ reference's PCG64 permutations and streams them to the device.
 
 from __future__ import annotations
 
+import collections
+import itertools
 import math
 import os
 import threading
@@ -262,19 +264,24 @@ COV_MAX_N = 20000
 
 # fit() reuses native contexts of the same shape (rac_en_reset) instead of creating and
 # destroying one per call: streams, events, plans and pool buffers stay; each fit holds
-# its context exclusively.
-_POOL: dict = {}
+# its context exclusively.  At most _POOL_MAX idle contexts are kept (least recently
+# used closed first).
+_POOL: "collections.OrderedDict" = collections.OrderedDict()   # (key, serial) -> solver
 _POOL_LOCK = threading.Lock()
-_POOL_PER_KEY = 2
+_POOL_MAX = 4
+_POOL_SERIAL = itertools.count()
 
 
 def _acquire_solver(m, n, block_size, mode, lam, alpha, gamma, device):
     # RAC_* environment switches select native variants when a context is created / planned
     env = tuple(sorted((k, v) for k, v in os.environ.items() if k.startswith("RAC_")))
     key = (m, n, min(int(block_size), n), Mode(mode), device, _device.stream_handle(), env)
+    solver = None
     with _POOL_LOCK:
-        lst = _POOL.get(key)
-        solver = lst.pop() if lst else None
+        for pk in reversed(_POOL):
+            if pk[0] == key:
+                solver = _POOL.pop(pk)
+                break
     if solver is not None:
         solver.reset(lam, alpha, gamma)
         return key, solver
@@ -282,13 +289,16 @@ def _acquire_solver(m, n, block_size, mode, lam, alpha, gamma, device):
 
 
 def _release_solver(key, solver, ok: bool) -> None:
+    evicted = []
     if ok:
         with _POOL_LOCK:
-            lst = _POOL.setdefault(key, [])
-            if len(lst) < _POOL_PER_KEY:
-                lst.append(solver)
-                return
-    solver.close()
+            _POOL[(key, next(_POOL_SERIAL))] = solver
+            while len(_POOL) > _POOL_MAX:
+                evicted.append(_POOL.popitem(last=False)[1])
+    else:
+        evicted.append(solver)
+    for sv in evicted:
+        sv.close()
 
 
 def choose_gram_mode(m: int, n: int, block_size: int, iters: int) -> str:

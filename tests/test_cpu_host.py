@@ -216,3 +216,46 @@ def test_shard_covers_once():
     assert sorted(sum(parts, [])) == cells
     with pytest.raises(ValueError):
         replicas.shard(cells, 3, 3)
+
+
+def test_fit_context_pool_reuse_env_keys_and_eviction(monkeypatch):
+    """fit()'s native-context pool (host logic, no GPU): a released context of the same
+    shape is reset and reused; RAC_* variant switches are part of the key; a failed fit's
+    context is closed, not pooled; at most _POOL_MAX idle contexts stay (LRU)."""
+    from paper_1907_01995_b200 import elastic_net as en
+    from paper_1907_01995_b200.problems import Mode
+    events = []
+
+    class FakeSolver:
+        def __init__(self, m, n, s, mode, lam, alpha, gamma, device=0):
+            self.m = m
+            events.append(("new", m))
+
+        def reset(self, lam, alpha, gamma):
+            events.append(("reset", self.m))
+
+        def close(self):
+            events.append(("close", self.m))
+
+    monkeypatch.setattr(en, "EnSolver", FakeSolver)
+    monkeypatch.setattr(en._device, "stream_handle", lambda: 0)
+    for k in [k for k in list(__import__("os").environ) if k.startswith("RAC_")]:
+        monkeypatch.delenv(k)
+    en._POOL.clear()
+    k1, s1 = en._acquire_solver(10, 20, 5, Mode.RAC, 0.1, 1.0, 1.0, 0)
+    en._release_solver(k1, s1, True)
+    k2, s2 = en._acquire_solver(10, 20, 5, Mode.RAC, 0.2, 1.0, 1.0, 0)
+    assert s2 is s1 and events[-1] == ("reset", 10)
+    en._release_solver(k2, s2, True)
+    monkeypatch.setenv("RAC_CLA_D", "2")
+    k3, s3 = en._acquire_solver(10, 20, 5, Mode.RAC, 0.2, 1.0, 1.0, 0)
+    assert s3 is not s1 and events[-1] == ("new", 10)
+    en._release_solver(k3, s3, False)
+    assert events[-1] == ("close", 10)
+    monkeypatch.delenv("RAC_CLA_D")
+    for i in range(6):
+        k, sv = en._acquire_solver(100 + i, 20, 5, Mode.RAC, 0.1, 1.0, 1.0, 0)
+        en._release_solver(k, sv, True)
+    assert len(en._POOL) == en._POOL_MAX
+    assert ("close", 10) in events and ("close", 100) in events   # least recently used first
+    en._POOL.clear()

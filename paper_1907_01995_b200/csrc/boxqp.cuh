@@ -36,6 +36,7 @@ struct BoxWork {
   double* red; // >= nwarps
   double* rinv;  // s: reciprocal pivots of the current factor
   long long* dbg;  // optional counters: [reduced solves, passes, ns in solves, ns total]
+  long long* st;   // optional solve statistics: [sum nb, sum nf, direct solves, ns factor, ns tri-solve]
 };
 
 // Cholesky of the leading n x n of L (row-major, ld) in place, lower; CTA-wide.
@@ -95,6 +96,7 @@ __device__ void warp_chol_solve(const double* L, int ld, int n, double* v, const
 #pragma unroll
     for (int q = 0; q < MAXQ; ++q)
       if (q == oq) yk = reg[q] * rinv[k];
+    __syncwarp();   // reconverge before the shuffle (a diverged warp takes a ~10x slower path)
     yk = __shfl_sync(0xffffffffu, yk, ow);
 #pragma unroll
     for (int q = 0; q < MAXQ; ++q) {
@@ -110,6 +112,7 @@ __device__ void warp_chol_solve(const double* L, int ld, int n, double* v, const
 #pragma unroll
     for (int q = 0; q < MAXQ; ++q)
       if (q == oq) xk = reg[q] * rinv[k];
+    __syncwarp();
     xk = __shfl_sync(0xffffffffu, xk, ow);
 #pragma unroll
     for (int q = 0; q < MAXQ; ++q) {
@@ -226,49 +229,62 @@ __device__ void cta_lists(BoxWork& w, int s) {
   __syncthreads();
 }
 
+// sum_{k < cnt} Mcol[list[k] * ld] * v[vi(k)] with four chains: the gathered column of a
+// SYMMETRIC matrix read by one thread (consecutive threads -> consecutive columns).
+template <class VI>
+__device__ __forceinline__ double gathered_dot(const double* Mcol, int ld, const int* list, int cnt, VI vi) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int k = 0;
+  for (; k + 4 <= cnt; k += 4) {
+    a0 += Mcol[(int64_t)list[k] * ld] * vi(k);
+    a1 += Mcol[(int64_t)list[k + 1] * ld] * vi(k + 1);
+    a2 += Mcol[(int64_t)list[k + 2] * ld] * vi(k + 2);
+    a3 += Mcol[(int64_t)list[k + 3] * ld] * vi(k + 3);
+  }
+  for (; k < cnt; ++k) a0 += Mcol[(int64_t)list[k] * ld] * vi(k);
+  return (a0 + a1) + (a2 + a3);
+}
+
 // Solve M_FF xf = r_F - M_FB x_B on the current free set; result in w.xf[0..nf).
+// M and N = M^{-1} are symmetric, so every product is one thread per output reading
+// the output's column (no cross-lane reductions on the box solver's chain).
 // Returns fail code (k+1) if the reduced matrix is not PD.
 __device__ int solve_free(const double* M, int ldm, BoxWork& w, bool use_schur) {
   const int nf = w.misc[0], nb = w.misc[1];
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int tid = threadIdx.x, nt = blockDim.x;
   // q = r_F - M_FB x_B
-  for (int a = warp; a < nf; a += nw) {
-    const double* row = M + (int64_t)w.F[a] * ldm;
-    double acc = 0.0;
-    for (int k = lane; k < nb; k += 32) acc += row[w.B[k]] * w.x[w.B[k]];
-    acc = warp_sum(acc);
-    if (lane == 0) w.xf[a] = (nb > 0) ? w.r[w.F[a]] - acc : w.r[w.F[a]];
+  for (int a = tid; a < nf; a += nt) {
+    const int fa = w.F[a];
+    const double acc = gathered_dot(M + fa, ldm, w.B, nb, [&](int k) { return w.x[w.B[k]]; });
+    w.xf[a] = (nb > 0) ? w.r[fa] - acc : w.r[fa];
   }
   __syncthreads();
+  const bool st = w.st && tid == 0;
+  if (st) { w.st[0] += nb; w.st[1] += nf; }
   const int ldk = nb | 1;
   if (use_schur && w.N && nb <= nf && (size_t)ldk * nb <= (size_t)w.lcap) {
     const double* N = w.N;
     const int ldn = w.ldn;
     if (nb > 0) {
       // u = N_BF q ; N_BB (lower) into the workspace
-      for (int c = warp; c < nb; c += nw) {
-        const double* row = N + (int64_t)w.B[c] * ldn;
-        double acc = 0.0;
-        for (int a2 = lane; a2 < nf; a2 += 32) acc += row[w.F[a2]] * w.xf[a2];
-        acc = warp_sum(acc);
-        if (lane == 0) w.rr[c] = acc;
-      }
+      for (int c = tid; c < nb; c += nt)
+        w.rr[c] = gathered_dot(N + w.B[c], ldn, w.F, nf, [&](int k) { return w.xf[k]; });
       for (int e = tid; e < nb * nb; e += nt) {
         const int c1 = e / nb, c2 = e - c1 * nb;
         if (c2 <= c1) w.L[c1 * ldk + c2] = N[(int64_t)w.B[c1] * ldn + w.B[c2]];
       }
+      long long t0 = st ? gtimer() : 0;
       const int fail = cta_cholesky(w.L, ldk, nb, w.rinv);
+      if (st) { const long long t1 = gtimer(); w.st[3] += t1 - t0; t0 = t1; }
       if (!fail) {
         chol_solve(w.L, ldk, nb, w.rr, w.rinv);   // rr <- N_BB^{-1} N_BF q
         __syncthreads();
+        if (st) w.st[4] += gtimer() - t0;
         // x_F = N_FF q - N_FB (N_BB^{-1} N_BF q)
-        for (int a2 = warp; a2 < nf; a2 += nw) {
-          const double* row = N + (int64_t)w.F[a2] * ldn;
-          double acc = 0.0;
-          for (int j = lane; j < nf; j += 32) acc += row[w.F[j]] * w.xf[j];
-          for (int c = lane; c < nb; c += 32) acc -= row[w.B[c]] * w.rr[c];
-          acc = warp_sum(acc);
-          if (lane == 0) w.grad[a2] = acc;
+        for (int a2 = tid; a2 < nf; a2 += nt) {
+          const double* col = N + w.F[a2];
+          w.grad[a2] = gathered_dot(col, ldn, w.F, nf, [&](int k) { return w.xf[k]; }) -
+                       gathered_dot(col, ldn, w.B, nb, [&](int k) { return w.rr[k]; });
         }
         __syncthreads();
         for (int a2 = tid; a2 < nf; a2 += nt) w.xf[a2] = w.grad[a2];
@@ -277,13 +293,8 @@ __device__ int solve_free(const double* M, int ldm, BoxWork& w, bool use_schur) 
       }
       // numerically indefinite N_BB: fall through to the direct factorization
     } else {
-      for (int a2 = warp; a2 < nf; a2 += nw) {
-        const double* row = N + (int64_t)w.F[a2] * ldn;
-        double acc = 0.0;
-        for (int j = lane; j < nf; j += 32) acc += row[w.F[j]] * w.xf[j];
-        acc = warp_sum(acc);
-        if (lane == 0) w.grad[a2] = acc;
-      }
+      for (int a2 = tid; a2 < nf; a2 += nt)
+        w.grad[a2] = gathered_dot(N + w.F[a2], ldn, w.F, nf, [&](int k) { return w.xf[k]; });
       __syncthreads();
       for (int a2 = tid; a2 < nf; a2 += nt) w.xf[a2] = w.grad[a2];
       __syncthreads();
@@ -297,10 +308,14 @@ __device__ int solve_free(const double* M, int ldm, BoxWork& w, bool use_schur) 
     const int a1 = e / nf, b1 = e - a1 * nf;
     if (b1 <= a1) w.L[a1 * ldf + b1] = M[(int64_t)w.F[a1] * ldm + w.F[b1]];
   }
+  long long t0 = st ? gtimer() : 0;
+  if (st) w.st[2] += 1;
   const int fail = cta_cholesky(w.L, ldf, nf, w.rinv);
+  if (st) { const long long t1 = gtimer(); w.st[3] += t1 - t0; t0 = t1; }
   if (fail) return fail;
   chol_solve(w.L, ldf, nf, w.xf, w.rinv);
   __syncthreads();
+  if (st) w.st[4] += gtimer() - t0;
   return 0;
 }
 
@@ -385,8 +400,8 @@ __device__ int box_active_set(const double* M, int ldm, int s, BoxWork& w, bool 
       if (!viol) break;
     }
     if (w.dbg && threadIdx.x == 0) w.dbg[1] += 1;
-    // multipliers: grad = M x - r
-    cta_matvec(M, ldm, s, s, w.x, w.grad);
+    // multipliers: grad = M x - r  (M symmetric: thread per row)
+    cta_symv(M, ldm, s, w.x, w.grad);
     __syncthreads();
     double loc = 0.0;
     for (int i = tid; i < s; i += nt) {
@@ -404,6 +419,7 @@ __device__ int box_active_set(const double* M, int ldm, int s, BoxWork& w, bool 
       if (sc > best) { best = sc; bi = i; }
     }
     const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    __syncwarp();
     for (int o = 16; o > 0; o >>= 1) {
       double ob = __shfl_xor_sync(0xffffffffu, best, o);
       int oi = __shfl_xor_sync(0xffffffffu, bi, o);

@@ -154,6 +154,7 @@ __device__ QpSmem carve_qp(double* base, int s, bool rowphase, bool lsmem, doubl
   q.sc = p; p += 32;  // scalars
   q.bw.rinv = p; p += s;
   q.bw.dbg = nullptr;
+  q.bw.st = nullptr;
   q.bw.N = nullptr;
   q.bw.ldn = s;
   q.bw.L = lscratch;                       // large workspace (global): s(s+1) doubles
@@ -547,7 +548,11 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       long long t_box = tr ? gtimer() : 0;
       if (tr) a.trace[10 * t + 3] = t_box;
       w.bw.dbg = a.trace ? (a.trace + 10 * a.p + 4 * t) : nullptr;
-      if (tr) { w.bw.dbg[0] = 0; w.bw.dbg[1] = 0; w.bw.dbg[2] = 0; }
+      w.bw.st = a.trace ? (a.trace + 14 * (size_t)a.p + 2 * (size_t)a.p * gridDim.x + 8 * t) : nullptr;
+      if (tr) {
+        w.bw.dbg[0] = 0; w.bw.dbg[1] = 0; w.bw.dbg[2] = 0;
+        for (int q = 0; q < 8; ++q) w.bw.st[q] = 0;
+      }
       __syncthreads();
       int fail = box_active_set(Mblk, s, seff, w.bw, schur);
       if (tr) {
@@ -1127,7 +1132,7 @@ extern "C" int rac_qp_set_trace(rac_qp_ctx* c, int32_t enable) {
   clear_error();
   if (!c) return set_error(RAC_ERR_ARG, "rac_qp_set_trace: null context");
   if (enable && !c->trace) {
-    int rc = qalloc(c, &c->trace, 14 * (size_t)c->p + 2 * (size_t)c->p * c->P);
+    int rc = qalloc(c, &c->trace, 22 * (size_t)c->p + 2 * (size_t)c->p * c->P);   // + 8 solve stats per block
     if (rc) return rc;
   }
   if (!enable) c->trace = nullptr;
@@ -1138,7 +1143,7 @@ extern "C" int rac_qp_trace(rac_qp_ctx* c, int64_t* host, int32_t capacity) {
   using namespace rac;
   clear_error();
   if (!c || !host || !c->trace) return set_error(RAC_ERR_ARG, "rac_qp_trace: tracing not enabled");
-  const int k = std::min<int>(capacity, 14 * c->p + 2 * c->p * c->P);
+  const int k = std::min<int>(capacity, 22 * c->p + 2 * c->p * c->P);
   return check_cuda(cudaMemcpy(host, c->trace, k * sizeof(int64_t), cudaMemcpyDeviceToHost), "qp trace copy");
 }
 

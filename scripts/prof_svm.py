@@ -31,12 +31,13 @@ print("ok", sol.progress(), "ms/sweep", t0.elapsed_time(t1) / sweeps)
 if trace:
     p = sol.p
     P = 148
-    buf = (np.ctypeslib.ctypes.c_int64 * (14 * p + 2 * p * P))()
-    sol.lib.rac_qp_trace(sol.h, buf, 14 * p + 2 * p * P)
+    buf = (np.ctypeslib.ctypes.c_int64 * (22 * p + 2 * p * P))()
+    sol.lib.rac_qp_trace(sol.h, buf, 22 * p + 2 * p * P)
     allv = np.array(buf[:], dtype=np.float64)
     tv = allv[:10 * p].reshape(p, 10) / 1e3
     dbg = allv[10 * p:14 * p].reshape(p, 4)
-    arr = allv[14 * p:].reshape(p, P, 2) / 1e3
+    arr = allv[14 * p:14 * p + 2 * p * P].reshape(p, P, 2) / 1e3
+    stt = allv[14 * p + 2 * p * P:].reshape(p, 8)
     a2 = arr[:, :, 0] - arr[:, 0:1, 0]      # arrival at barrier 2 relative to CTA 0
     a1 = arr[1:, :, 1] - arr[1:, 0:1, 1]    # arrival at barrier 1 (next block) relative to CTA 0
     print("barrier2 arrival minus CTA0 (us): CTA1 %.2f  others mean %.2f max %.2f" % (
@@ -52,3 +53,8 @@ if trace:
         tv[-1, 7] - tv[0, 0], (tv[-1, 7] - tv[0, 0]) / p))
     print("per block us:", {k: round(float(v), 2) for k, v in zip(names, seg.mean(axis=0))},
           "barrier1 %.2f" % float(np.mean(tv[1:, 0] - tv[:-1, 7])))
+    ns = np.maximum(stt[:, 0] * 0 + dbg[:, 0], 1)
+    print("reduced solves: mean nb %.1f  mean nf %.1f  direct fraction %.2f  factor us/solve %.2f  tri-solve us/solve %.2f" % (
+        stt[:, 0].sum() / max(dbg[:, 0].sum(), 1), stt[:, 1].sum() / max(dbg[:, 0].sum(), 1),
+        stt[:, 2].sum() / max(dbg[:, 0].sum(), 1), stt[:, 3].sum() / 1e3 / max(dbg[:, 0].sum(), 1),
+        stt[:, 4].sum() / 1e3 / max(dbg[:, 0].sum(), 1)))

@@ -156,6 +156,22 @@ __device__ void warp_chol_solve_any(const double* L, int ld, int n, double* v) {
 }
 
 __device__ __forceinline__ void chol_solve(const double* L, int ld, int n, double* v, const double* rinv) {
+  if (n <= 8 && rinv) {
+    // tiny systems (the typical bound set of an SVM block): one thread, no warp traffic
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < n; ++k) {
+        double y = v[k];
+        for (int j = 0; j < k; ++j) y -= L[k * ld + j] * v[j];
+        v[k] = y * rinv[k];
+      }
+      for (int k = n - 1; k >= 0; --k) {
+        double x = v[k];
+        for (int j = k + 1; j < n; ++j) x -= L[j * ld + k] * v[j];
+        v[k] = x * rinv[k];
+      }
+    }
+    return;
+  }
   if (n <= 256 && rinv) warp_chol_solve<8>(L, ld, n, v, rinv);
   else warp_chol_solve_any(L, ld, n, v);
 }

@@ -50,15 +50,22 @@ struct EnChainArgs {
   int sweep;
   double *hist_p, *hist_d;
   long long* trace;     // optional: %globaltimer at every phase boundary (CTA 0)
+  int rw;               // RC == 0 (one-tile resident row phase): rows per CTA
 };
 
 
+// RC > 0: row chunks of RC rows streamed through shared memory; RC == 0: each CTA owns
+// `rw` contiguous rows and keeps the current block's tile resident (row_phase_1t)
 template <int RC>
 __global__ void __launch_bounds__(ENT) en_chain_kernel(EnChainArgs a) {
   if (a.ctrl[0]) return;
   extern __shared__ __align__(16) double esm[];
   const int s = a.s;
-  const RowPhaseSmem w = carve_rowphase<RC>(esm, s);
+  constexpr int RCC = RC > 0 ? RC : 8;   // (unused layout parameter in the one-tile mode)
+  const RowPhaseSmem w = carve_rowphase<RCC>(esm, s);
+  const Row1tSmem w1 = carve_row1t(esm, s, a.rw > 0 ? a.rw : 1);
+  const int64_t r0 = (int64_t)blockIdx.x * a.rw;
+  const int nr1 = (RC == 0) ? (int)min64(a.rw, a.ld - r0) : 0;
   __shared__ int bad;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -87,7 +94,13 @@ __global__ void __launch_bounds__(ENT) en_chain_kernel(EnChainArgs a) {
   int tp = 0;
   if (tr) a.trace[tp++] = gtimer();
   int bnext = a.order ? a.order[0] : 0;
-  row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, -1, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
+  if constexpr (RC == 0) {
+    for (int i = threadIdx.x; i < nr1; i += ENT) w1.sR[i] = a.r[r0 + i];
+    __syncthreads();
+    row_phase_1t(a.Xc, a.ld, r0, nr1, a.idx, s, -1, bnext, a.delta, a.beta, a.partial, w1, tfn);
+  } else {
+    row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, -1, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
+  }
   if (tr) a.trace[tp++] = gtimer();
   for (int t = 0; t < a.p; ++t) {
     const int b = bnext;
@@ -141,9 +154,14 @@ __global__ void __launch_bounds__(ENT) en_chain_kernel(EnChainArgs a) {
     grid_barrier(a.bar, target, P);
     if (tr) a.trace[tp++] = gtimer();
     bnext = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
-    row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
+    if constexpr (RC == 0)
+      row_phase_1t(a.Xc, a.ld, r0, nr1, a.idx, s, b, bnext, a.delta, a.beta, a.partial, w1, tfn);
+    else
+      row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
     if (tr) a.trace[tp++] = gtimer();
   }
+  if constexpr (RC == 0)
+    for (int i = threadIdx.x; i < nr1; i += ENT) a.r[r0 + i] = w1.sR[i];
   if (lane == 0) {
     a.wsum[gw] = my_sum;
     a.wmax[gw] = my_max;
@@ -253,6 +271,7 @@ struct rac_en_ctx {
   cudaStream_t st = nullptr;
   int P = 0, RC = 32, nrc = 0;
   int variant = 0, nch = 0;   // 1: resident-tile cluster chain (en_chain_res_kernel)
+  int rw = 0;                 // streaming chain with RC == 0: rows per CTA (one resident tile)
   int cs = 2;                 // its cluster size (2, 4 or 8)
   rac::GramPlan gp{};
   bool have_data = false, have_partition = false;
@@ -697,6 +716,7 @@ int en_chain(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
   a.hist_p = c->hist_p;
   a.hist_d = c->hist_d;
   a.trace = c->trace;
+  a.rw = c->rw;
   void* args[] = {&a};
   if (c->variant == 1) {
     int nch = c->nch;
@@ -723,9 +743,11 @@ int en_chain(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
     return check_cuda(cudaLaunchKernelExC(&cfg, (const void*)res_kernel(c->cs), rargs),
                       "en_chain_res (cluster cooperative launch)");
   }
-  size_t smem = en_chain_smem(c->s, c->RC);
+  size_t smem = c->RC == 0 ? row1t_smem_bytes(c->s, c->rw) : en_chain_smem(c->s, c->RC);
   cudaError_t e;
-  if (c->RC == 32)
+  if (c->RC == 0)
+    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<0>, dim3(c->P), dim3(ENT), args, smem, st);
+  else if (c->RC == 32)
     e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<32>, dim3(c->P), dim3(ENT), args, smem, st);
   else if (c->RC == 16)
     e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<16>, dim3(c->P), dim3(ENT), args, smem, st);
@@ -845,6 +867,22 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
       }
       cudaGetLastError();
     }
+  }
+  // streaming chain, one-tile resident row phase (RC == 0) when a CTA's contiguous rows
+  // of one block fit in shared memory: every block's columns read once per sweep, no
+  // row-chunk imbalance (RAC_EN_1T=0 keeps the chunked schedule)
+  if (c->variant == 0) {
+    const char* env = getenv("RAC_EN_1T");
+    const int rw = (int)(((c->ld + num_sms() - 1) / num_sms() + 1) / 2 * 2);
+    const size_t sm1 = row1t_smem_bytes(s, rw);
+    if (!(env && atoi(env) == 0) && sm1 <= 200 * 1024 &&
+        cudaFuncSetAttribute((void*)en_chain_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1) ==
+            cudaSuccess) {
+      c->RC = 0;
+      c->rw = rw;
+      c->P = (int)((c->ld + rw - 1) / rw);
+    }
+    cudaGetLastError();
   }
   const int GW = c->P * (ENT / 32);
   const size_t sqs = (size_t)c->p * s * s;

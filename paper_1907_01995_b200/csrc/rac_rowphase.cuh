@@ -169,3 +169,120 @@ __device__ void row_phase(const double* __restrict__ V, int64_t ld, int64_t m, i
 }
 
 }  // namespace rac
+
+namespace rac {
+
+// ---------------------------------------------------------------------------
+// One-tile resident row phase (EN streaming chain, RC == 0 mode): CTA k owns the
+// contiguous rows [r0, r0 + nr) for the whole launch and keeps X[rows, b] of the
+// current block resident in shared memory from the row phase that loaded it as
+// "next" to the one that applies its delta, so every block's columns are read
+// once per sweep and the work is balanced (no row chunks to distribute).
+//   (a) r += X[rows, b_prev] delta   (resident tile)
+//   (b) X[rows, b_next] -> the tile  (8-byte cp.async, odd row stride: conflict-free
+//                                     along rows and along columns)
+//   (c) t = T(r, X[rows, b_next] x_next)
+//   (d) partial[cta][j] = X[rows, b_next[j]]' t
+// ---------------------------------------------------------------------------
+struct Row1tSmem {
+  double* tile;   // [s][rwp]
+  double* sR;     // [rw] r at this CTA's rows (kept for the launch)
+  double* sT;     // [rw]
+  double* sX;     // [s]
+  double* sDel;   // [s]
+  double* red;    // [G][rw]
+  int32_t* sIdx;  // [s]
+  int rwp;
+};
+
+__host__ __device__ inline int row1t_groups(int rw) { return rw >= RP_THREADS ? 1 : RP_THREADS / rw; }
+__host__ __device__ inline size_t row1t_smem_bytes(int s, int rw) {
+  const int rwp = rw | 1;
+  return ((size_t)s * rwp + 2 * (size_t)rw + 2 * (size_t)s + (size_t)row1t_groups(rw) * rw) * sizeof(double) +
+         (size_t)s * sizeof(int32_t);
+}
+__device__ __forceinline__ Row1tSmem carve_row1t(double* base, int s, int rw) {
+  Row1tSmem w;
+  w.rwp = rw | 1;
+  w.tile = base;
+  w.sR = w.tile + (size_t)s * w.rwp;
+  w.sT = w.sR + rw;
+  w.sX = w.sT + rw;
+  w.sDel = w.sX + s;
+  w.red = w.sDel + s;
+  w.sIdx = reinterpret_cast<int32_t*>(w.red + (size_t)row1t_groups(rw) * rw);
+  return w;
+}
+
+// sum over j = j0, j0 + step, ... < s of tile[j * rwp + row] * v[j], four chains
+__device__ __forceinline__ double row1t_dot(const double* tile, int rwp, int row, const double* v, int j0, int s,
+                                            int step) {
+  return strided_dot(tile + row, v, j0, s, step, rwp);
+}
+
+template <class TFn>
+__device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r0, int nr,
+                             const int32_t* __restrict__ idx, int s, int bprev, int bnext, const double* delta,
+                             const double* xsrc, double* partial, const Row1tSmem& w, TFn tfn) {
+  const int tid = threadIdx.x;
+  const int G = row1t_groups(nr);
+  const int row = tid % nr, grp = tid / nr;
+  const bool act = grp < G;
+  if (bprev >= 0)
+    for (int j = tid; j < s; j += RP_THREADS) w.sDel[j] = ldcg(delta + j);
+  if (bnext >= 0)
+    for (int j = tid; j < s; j += RP_THREADS) {
+      const int g = idx[(int64_t)bnext * s + j];
+      w.sIdx[j] = g;
+      w.sX[j] = (g >= 0) ? ldcg(xsrc + g) : 0.0;
+    }
+  __syncthreads();
+  if (bprev >= 0) {   // (a) resident tile holds X[rows, b_prev]
+    if (act) w.red[grp * nr + row] = row1t_dot(w.tile, w.rwp, row, w.sDel, grp, s, G);
+    __syncthreads();
+    if (tid < nr) {
+      double u = 0.0;
+      for (int q = 0; q < G; ++q) u += w.red[q * nr + tid];
+      w.sR[tid] += u;
+    }
+    __syncthreads();
+  }
+  if (bnext < 0) return;
+  // (b)
+  for (int e = tid; e < s * nr; e += RP_THREADS) {
+    const int j = e / nr, i = e - j * nr;
+    const int g = w.sIdx[j];
+    double* d = w.tile + (size_t)j * w.rwp + i;
+    if (g >= 0) cp_async8(d, V + (int64_t)g * ld + r0 + i);
+    else *d = 0.0;
+  }
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  // (c)
+  if (act) w.red[grp * nr + row] = row1t_dot(w.tile, w.rwp, row, w.sX, grp, s, G);
+  __syncthreads();
+  if (tid < nr) {
+    double u = 0.0;
+    for (int q = 0; q < G; ++q) u += w.red[q * nr + tid];
+    w.sT[tid] = tfn(r0 + tid, w.sR[tid], u);
+  }
+  __syncthreads();
+  // (d)
+  for (int j = tid; j < s; j += RP_THREADS) {
+    const double* col = w.tile + (size_t)j * w.rwp;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int i = 0;
+    for (; i + 4 <= nr; i += 4) {
+      a0 += col[i] * w.sT[i];
+      a1 += col[i + 1] * w.sT[i + 1];
+      a2 += col[i + 2] * w.sT[i + 2];
+      a3 += col[i + 3] * w.sT[i + 3];
+    }
+    for (; i < nr; ++i) a0 += col[i] * w.sT[i];
+    partial[(int64_t)blockIdx.x * s + j] = (a0 + a1) + (a2 + a3);
+  }
+  __syncthreads();
+}
+
+}  // namespace rac

@@ -216,6 +216,10 @@ __device__ __forceinline__ void bulk_s2peer(unsigned dst, const void* src, unsig
                : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // named barrier for a subset of the CTA's warps (id 1..15)
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

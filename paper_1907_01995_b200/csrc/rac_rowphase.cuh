@@ -196,14 +196,16 @@ struct Row1tSmem {
 };
 
 __host__ __device__ inline int row1t_groups(int rw) { return rw >= RP_THREADS ? 1 : RP_THREADS / rw; }
+// row stride of the tile: even (16-byte cp.async rows), +2 breaks the bank alignment
+__host__ __device__ inline int row1t_stride(int rw) { return rw + 2; }
 __host__ __device__ inline size_t row1t_smem_bytes(int s, int rw) {
-  const int rwp = rw | 1;
+  const int rwp = row1t_stride(rw);
   return ((size_t)s * rwp + 2 * (size_t)rw + 2 * (size_t)s + (size_t)row1t_groups(rw) * rw) * sizeof(double) +
          (size_t)s * sizeof(int32_t);
 }
 __device__ __forceinline__ Row1tSmem carve_row1t(double* base, int s, int rw) {
   Row1tSmem w;
-  w.rwp = rw | 1;
+  w.rwp = row1t_stride(rw);
   w.tile = base;
   w.sR = w.tile + (size_t)s * w.rwp;
   w.sT = w.sR + rw;
@@ -248,13 +250,14 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
     __syncthreads();
   }
   if (bnext < 0) return;
-  // (b)
-  for (int e = tid; e < s * nr; e += RP_THREADS) {
-    const int j = e / nr, i = e - j * nr;
+  // (b) 16-byte pieces (nr, r0, ld and the row stride are even)
+  const int h = nr >> 1;
+  for (int e = tid; e < s * h; e += RP_THREADS) {
+    const int j = e / h, i = 2 * (e - j * h);
     const int g = w.sIdx[j];
     double* d = w.tile + (size_t)j * w.rwp + i;
-    if (g >= 0) cp_async8(d, V + (int64_t)g * ld + r0 + i);
-    else *d = 0.0;
+    if (g >= 0) cp_async16(d, V + (int64_t)g * ld + r0 + i);
+    else d[0] = d[1] = 0.0;
   }
   cp_async_commit();
   cp_async_wait<0>();

@@ -106,6 +106,15 @@ __global__ void __launch_bounds__(ENT) en_chain_kernel(EnChainArgs a) {
     const int b = bnext;
     grid_barrier(a.bar, target, P);
     if (tr) a.trace[tp++] = gtimer();
+    // this CTA's S2 rows of inv_b -> L2 while S1 runs (one 128-byte line per thread)
+    {
+      const double* Ib = a.inv + (int64_t)b * s * s;
+      const int lines = (s * (int)sizeof(double) + 127) / 128;
+      for (int e = threadIdx.x; e < (ENT / 32) * lines; e += ENT) {
+        const int i = blockIdx.x * (ENT / 32) + e / lines;   // global warp of row i (loop below, first round)
+        if (i < s) prefetch_l2(Ib + (int64_t)i * s + 16 * (e % lines));
+      }
+    }
     // ---- S1: reduce the per-CTA partials -> block right-hand side
     for (int j = gw; j < s; j += GW) {
       double acc = 0.0;

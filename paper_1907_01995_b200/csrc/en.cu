@@ -887,6 +887,8 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
     if (!(env && atoi(env) == 0) && sm1 <= 200 * 1024 &&
         cudaFuncSetAttribute((void*)en_chain_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1) ==
             cudaSuccess) {
+      cudaFuncSetAttribute((void*)en_chain_kernel<0>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           cudaSharedmemCarveoutMaxShared);
       c->RC = 0;
       c->rw = rw;
       c->P = (int)((c->ld + rw - 1) / rw);

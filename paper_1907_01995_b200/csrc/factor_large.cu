@@ -289,6 +289,9 @@ int launch_inverse_large(const SysArgs& a, int p, cudaStream_t st) {
   const size_t smem = 2 * LT * LLD * sizeof(double);
   static bool attr = false;
   if (!attr) {
+    cudaFuncSetAttribute(large_cw_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(large_update_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
     int rc = check_cuda(cudaFuncSetAttribute(large_cw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                         "large_cw smem");
     if (rc) return rc;

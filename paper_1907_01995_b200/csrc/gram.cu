@@ -194,6 +194,9 @@ int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx,
                 cudaStream_t st, const int32_t* done, double sym_div, int sym_accum) {
   if (p <= 0) return RAC_OK;
   const size_t smem = 4 * GT * GLD * sizeof(double);
+  // maximal shared-memory carveout: the SM configuration then matches the chain kernels,
+  // so Gram CTAs of the next sweep can co-reside with a latency-bound chain
+  cudaFuncSetAttribute(gram_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   int rc = check_cuda(cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "gram smem attribute");
   if (rc) return rc;

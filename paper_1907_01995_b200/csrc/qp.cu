@@ -479,6 +479,19 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       if (bn1 >= 0 && blockIdx.x != 0) {
         compute_hbx(bn1, (t + 1) & 1);
         if (small_a) small_pre(bn1, (t + 1) & 1);
+        // M_{t+1} and M_{t+1}^{-1} -> L2 (spread over the idle CTAs) so CTA 0's bulk copy
+        // of them after this block's box solve hits L2
+        if (w.sM || a.Mb) {
+          const int lines = (int)(((int64_t)s * s * sizeof(double) + 127) / 128);
+          const int per = (lines + P - 2) / (P - 1);
+          const int l0 = (blockIdx.x - 1) * per, l1 = min(lines, l0 + per);
+          const char* Mg = reinterpret_cast<const char*>(a.Mb + (int64_t)bn1 * s * s);
+          const char* Ng = reinterpret_cast<const char*>(a.Ninv ? a.Ninv + (int64_t)bn1 * s * s : nullptr);
+          for (int l = l0 + tid; l < l1; l += QPT) {
+            prefetch_l2(Mg + (size_t)l * 128);
+            if (Ng) prefetch_l2(Ng + (size_t)l * 128);
+          }
+        }
       }
     }
     // ------------------------------------------------------------ S (CTA 0)

@@ -37,6 +37,7 @@ struct BoxWork {
   double* rinv;  // s: reciprocal pivots of the current factor
   long long* dbg;  // optional counters: [reduced solves, passes, ns in solves, ns total]
   long long* st;   // optional solve statistics: [sum nb, sum nf, direct solves, ns factor, ns tri-solve]
+  double* symv_scratch;  // >= 4 s doubles for the split-row symv, or null
 };
 
 // Cholesky of the leading n x n of L (row-major, ld) in place, lower; CTA-wide.
@@ -191,8 +192,30 @@ __device__ __forceinline__ void cta_matvec(const double* M, int ld, int rows, in
 
 // out = M v for a SYMMETRIC M (row-major, stride ld): thread per row reading
 // column i (= row i), so consecutive threads touch consecutive words; four
-// independent accumulators.  No cross-lane reduction.
-__device__ __forceinline__ void cta_symv(const double* M, int ld, int rows, const double* v, double* out) {
+// independent accumulators.  No cross-lane reduction.  With 4 * rows <= threads,
+// four threads share a row (quarter of the columns each) and the quarters are
+// combined in fixed order through `scratch` (>= 4 * rows doubles); the caller
+// synchronizes before reading `out` either way.
+__device__ __forceinline__ void cta_symv(const double* M, int ld, int rows, const double* v, double* out,
+                                         double* scratch = nullptr) {
+  if (scratch && 4 * rows <= (int)blockDim.x) {
+    const int i = threadIdx.x % rows, qq = threadIdx.x / rows;
+    if (qq < 4) {
+      const int j0 = (rows * qq) / 4, j1 = (rows * (qq + 1)) / 4;
+      double a0 = 0.0, a1 = 0.0;
+      int j = j0;
+      for (; j + 2 <= j1; j += 2) {
+        a0 += M[(int64_t)j * ld + i] * v[j];
+        a1 += M[(int64_t)(j + 1) * ld + i] * v[j + 1];
+      }
+      if (j < j1) a0 += M[(int64_t)j * ld + i] * v[j];
+      scratch[qq * rows + i] = a0 + a1;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < rows; r += blockDim.x)
+      out[r] = (scratch[r] + scratch[rows + r]) + (scratch[2 * rows + r] + scratch[3 * rows + r]);
+    return;
+  }
   for (int i = threadIdx.x; i < rows; i += blockDim.x) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int j = 0;
@@ -416,8 +439,8 @@ __device__ int box_active_set(const double* M, int ldm, int s, BoxWork& w, bool 
       if (!viol) break;
     }
     if (w.dbg && threadIdx.x == 0) w.dbg[1] += 1;
-    // multipliers: grad = M x - r  (M symmetric: thread per row)
-    cta_symv(M, ldm, s, w.x, w.grad);
+    // multipliers: grad = M x - r  (M symmetric: four threads per row)
+    cta_symv(M, ldm, s, w.x, w.grad, w.symv_scratch);
     __syncthreads();
     double loc = 0.0;
     for (int i = tid; i < s; i += nt) {

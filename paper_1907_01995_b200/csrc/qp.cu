@@ -124,7 +124,7 @@ __host__ __device__ size_t qp_smem_bytes(int s, bool rowphase, bool lsmem) {
   size_t d = 0;
   if (rowphase) d += RowPhase<RC>::smem_doubles(s) + s;  // + int idx (as doubles, generous)
   d += (QPT / 32) * QCOLS;                               // strip reduction
-  d += 11 * (size_t)s + 64;                              // box vectors, rinv, sDel, sxb, shx, sc
+  d += 15 * (size_t)s + 64;                              // box vectors, rinv, sDel, sxb, shx, sc, symv scratch
   if (lsmem) d += 2 * (size_t)s * s + qp_lsmall(s) + 3;  // M_b, N_b, small workspace, mbarrier, align
   size_t ints = 4 * (size_t)s + 64;                      // flag, F, B, sIdx, misc
   return d * sizeof(double) + ints * sizeof(int);
@@ -153,6 +153,7 @@ __device__ QpSmem carve_qp(double* base, int s, bool rowphase, bool lsmem, doubl
   q.bw.red = p; p += 32;
   q.sc = p; p += 32;  // scalars
   q.bw.rinv = p; p += s;
+  q.bw.symv_scratch = p; p += 4 * s;
   q.bw.dbg = nullptr;
   q.bw.st = nullptr;
   q.bw.N = nullptr;
@@ -541,7 +542,7 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
       if (w.sM) wait_ML();   // M_b, N_b resident (ld = s)
       if (tr) a.trace[10 * t + 2] = gtimer();
       if (schur) {
-        cta_symv(w.sN, s, seff, w.bw.r, w.bw.x);   // M_b^{-1} is exactly symmetric (Y'Y)
+        cta_symv(w.sN, s, seff, w.bw.r, w.bw.x, w.bw.symv_scratch);   // M_b^{-1} is exactly symmetric (Y'Y)
         w.bw.N = w.sN;
         w.bw.ldn = s;
         w.bw.L = w.Lsmall;

@@ -187,12 +187,20 @@ def train(X: Matrix, labels: np.ndarray, C: float, kernel: KernelSpec,
     bias = _bias_from_q(Q, z, y, C)
     del Q
     support = z > SUPPORT_THRESHOLD
-    model = SvmModel(support_points=Xd[support].copy(), support_duals=z[support].copy(),
+    model = SvmModel(support_points=_gather_rows(Xd, support), support_duals=z[support].copy(),
                      support_labels=y[support].copy(), bias=bias, kernel=kernel, C=C)
     if return_diagnostics:
         return model, TrainDiagnostics(iterations=it, status=status, primal_residual_history=hp,
                                        dual_residual_history=hd, duals=z, eq_dual=nu)
     return model
+
+
+def _gather_rows(X: np.ndarray, mask: np.ndarray) -> np.ndarray:
+    """X[mask] as a fresh array; multi-threaded index_select (the boolean-mask copy of the
+    support vectors is single-threaded numpy: ~4x slower for config 4's 80 MB)."""
+    rows = np.flatnonzero(mask)
+    Xc = np.ascontiguousarray(X)
+    return torch.from_numpy(Xc).index_select(0, torch.from_numpy(rows)).numpy()
 
 
 # ---------------------------------------------------------------- host post-processing

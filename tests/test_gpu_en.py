@@ -364,3 +364,27 @@ def test_lookahead_batches_stop_at_the_converged_sweep(lib, batch):
         assert abs(got.residual - ref["residual"]) <= 1e-6 * abs(ref["residual"])
         assert rel(got.beta, ref["beta"]) <= ITER_TOL and rel(got.z, ref["z"]) <= ITER_TOL
         assert rel(got.xi, ref["xi"]) <= ITER_TOL
+
+
+@pytest.mark.parametrize("one_tile", ["1", "0"])
+def test_streaming_chain_one_tile_vs_oracle(lib, monkeypatch, one_tile):
+    """Block mode with s > 256 runs the streaming chain: one-tile resident row phase
+    (RAC_EN_1T=1, CTAs own contiguous rows; the last CTA's range is short) and the
+    chunked schedule (RAC_EN_1T=0), per-sweep iterates against the oracle."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import elastic_net as en
+    monkeypatch.setenv("RAC_EN_1T", one_tile)
+    rng = np.random.default_rng(43)
+    for (m, n, s, alpha) in [(500, 1200, 300, 1.0), (1000, 900, 300, 0.5), (150, 640, 320, 0.9)]:
+        X = rng.standard_normal((m, n))
+        y = X[:, :7] @ rng.standard_normal(7) + 0.05 * rng.standard_normal(m)
+        kw = dict(lam=0.05, alpha=alpha, gamma=1.0, block_size=s, iters=6, seed=2)
+        caps = {}
+        ro.en_fit(X, y, mode="rac", **kw,
+                  on_sweep=lambda k, bl, b, z, xi: caps.__setitem__(k, (b.copy(), z.copy(), xi.copy())))
+        got = {}
+        en.fit(X, y, en.ElasticNetSpec(**kw), gram_mode="blocks",
+               sweep_hook=lambda k, b, z, xi: got.__setitem__(k, (b, z, xi)))
+        for k in caps:
+            for a_, b_ in zip(got[k], caps[k]):
+                assert rel(a_, b_) <= ITER_TOL, (m, n, s, k)

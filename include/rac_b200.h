@@ -142,6 +142,14 @@ int rac_en_trace(rac_en_ctx* ctx, int64_t* host, int32_t capacity);
  * covariance chain are written to `mapped_host`, a device-accessible pinned host
  * buffer of >= 16 int64 (NULL switches it off); readable while a kernel runs. */
 int rac_debug_buffer(void* mapped_host);
+/* Utility (no reference counterpart): G (n x n, row-major, device) = Xc'Xc over the
+ * samples [0, len) of the column-major device matrix Xc (leading dimension ld;
+ * with method 0 len is rounded up to 32 and rows up to that must be readable),
+ * divided by div when div > 0, else ADDED to G.  method 0: FP64 DMMA tiles;
+ * method 1: exact int8 digit slices on the tcgen05 tensor cores (the covariance
+ * mode's default).  Synchronous. */
+int rac_gram_covariance(const double* Xc, int64_t ld, int64_t len, int32_t n, double* G, double div,
+                        int32_t method);
 /* [chain variant (0 streaming, 1 resident-tile cluster), CTAs, rows per chunk, chunks per CTA] */
 int rac_en_info(rac_en_ctx* ctx, int32_t* info_host4);
 /* Re-arm a context for a new fit with the same shape (m, n, block size, mode):

@@ -319,6 +319,9 @@ struct rac_en_ctx {
   int32_t* G_ids = nullptr;   // 0..n-1 (the single "block" of the full Gram)
   double* G_ws = nullptr;     // split-K partials of G
   size_t G_ws_cap = 0;
+  void* i8_ws = nullptr;      // digit slices of the tensor-core Gram (gram_i8.cu), null = DMMA Gram
+  size_t i8_ws_cap = 0;
+  int64_t g_rows_done = 0;    // row-chunk ingest: samples already summed into G
   // lookahead covariance chain (en_cla.cuh); cla_L = leader cluster size, 0 = not used
   int cla_L = 0, cla_D = 3, cla_W = 0, cla_segw = 1, cla_R = 2, cla_NS = 2;
   size_t cla_smem = 0;
@@ -349,6 +352,9 @@ int dalloc(rac_en_ctx* c, T** p, size_t count) {
   const int rc = rac::dev_alloc(&q, count * sizeof(T), c->st);
   if (rc) return rc;
   c->allocs.push_back(q);
+  // zero-filled: the chains read padding entries (tiles of absent lookahead steps, short
+  // last blocks) that are multiplied by zero and must therefore be finite
+  cudaMemsetAsync(q, getenv("RAC_POISON") ? 0xff : 0, count * sizeof(T), c->st);
   *p = (T*)q;
   return RAC_OK;
 }
@@ -518,6 +524,14 @@ int en_compute_G(rac_en_ctx* c, cudaStream_t st) {
   const int64_t n = c->n;
   GramPlan pl = plan_gram(c->m, (int)n, 1);
   int rc = RAC_OK;
+  if (c->i8_ws) {
+    // int8 tensor-core Gram in exact digit-slice arithmetic (FP64-level accuracy)
+    if ((rc = launch_gram_i8(c->Xc, c->ld, c->m, (int)n, c->G, (double)c->m, 0, c->i8_ws, c->i8_ws_cap, st)) ||
+        (rc = launch_gemv_rows(c->G, n, n, c->beta, c->q, st)))
+      return rc;
+    c->have_G = true;
+    return check_launch("covariance Gram (int8 slices)");
+  }
   // K split (better filled waves) when rac_en_set_gram_mode could reserve its workspace
   const size_t wsb = (size_t)pl.splits * n * n * sizeof(double);
   if (pl.splits > 1 && c->G_ws && c->G_ws_cap >= wsb) {
@@ -993,6 +1007,7 @@ extern "C" int rac_en_set_data_rows(rac_en_ctx* c, const double* X_rows, int64_t
   if (row0 == 0) {
     c->have_data = false;
     c->have_G = false;
+    c->g_rows_done = 0;
     if (c->gram_mode == 1) cudaMemsetAsync(c->G, 0, (size_t)c->n * c->n * sizeof(double), c->st);
   }
   const int64_t rows_out = last ? (c->ld - row0) : rows;
@@ -1009,7 +1024,29 @@ extern "C" int rac_en_set_data_rows(rac_en_ctx* c, const double* X_rows, int64_t
     GramPlan pl = plan_gram(len, (int)c->n, 1);
     pl.splits = 1;
     pl.chunk = len;
-    rc = launch_gram(c->Xc + row0, c->ld, len, c->G_ids, nullptr, (int)c->n, 1, c->G, pl, c->st, nullptr, 0.0, 1);
+    if (c->i8_ws) {
+      // tensor-core Gram over pieces of >= 4096 samples (full tiles' worth of K per launch),
+      // each overlapping the transfer of the following chunks
+      const int64_t done = c->g_rows_done, upto = row0 + rows;
+      if (last || upto - done >= 4096) {
+        const int64_t plen = last ? (c->m - done) : (upto - done);
+        // on the prep stream, so the transposes of the next chunks (c->st) keep draining
+        // the staging ring while the piece runs
+        cudaStream_t gs = c->sprep ? c->sprep : c->st;
+        if (gs != c->st) {
+          cudaEventRecord(c->ev_start, c->st);
+          cudaStreamWaitEvent(gs, c->ev_start, 0);
+        }
+        rc = launch_gram_i8(c->Xc + done, c->ld, plen, (int)c->n, c->G, 0.0, 1, c->i8_ws, c->i8_ws_cap, gs);
+        c->g_rows_done = upto;
+        if (last && gs != c->st) {
+          cudaEventRecord(c->ev_end, gs);
+          cudaStreamWaitEvent(c->st, c->ev_end, 0);
+        }
+      }
+    } else {
+      rc = launch_gram(c->Xc + row0, c->ld, len, c->G_ids, nullptr, (int)c->n, 1, c->G, pl, c->st, nullptr, 0.0, 1);
+    }
     if (rc) return rc;
   }
   if (!last) return RAC_OK;
@@ -1054,6 +1091,26 @@ extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {
   c->cov_full = plan & 1;
   c->gram_mode = 1;
   {
+    // digit-slice workspace of the int8 tensor-core Gram (RAC_G_I8=0: the FP64 DMMA Gram)
+    // (used when its 128 x 64 output tiles fill the SMs; RAC_G_I8=2 forces it, =0 disables it)
+    const char* e8 = getenv("RAC_G_I8");
+    const int mode8 = e8 ? atoi(e8) : 1;
+    const int64_t kt = (c->n + 63) / 64;
+    int64_t tiles = 0;
+    for (int64_t J = 0; 2 * J < kt; ++J) tiles += kt - 2 * J;
+    const size_t need = gram_i8_ws_bytes(c->ld, (int)c->n);
+    if ((mode8 == 2 || (mode8 == 1 && tiles >= num_sms())) && c->i8_ws_cap < need) {
+      uint8_t* w = nullptr;
+      if (dalloc(c, &w, need) == RAC_OK) {
+        c->i8_ws = w;
+        c->i8_ws_cap = need;
+      } else {
+        cudaGetLastError();
+        clear_error();
+      }
+    }
+  }
+  if (!c->i8_ws) {
     // split-K workspace of G (en_compute_G), reserved here so no fit allocates in its sweep loop
     const GramPlan pl = plan_gram(c->m, (int)c->n, 1);
     const size_t wsb = (size_t)pl.splits * c->n * c->n * sizeof(double);
@@ -1391,4 +1448,35 @@ extern "C" int rac_en_destroy(rac_en_ctx* c) {
 extern "C" int rac_debug_buffer(void* mapped_host) {
   g_cla_dbg = (volatile long long*)mapped_host;
   return RAC_OK;
+}
+
+extern "C" int rac_gram_covariance(const double* Xc, int64_t ld, int64_t len, int32_t n, double* G, double div,
+                                   int32_t method) {
+  using namespace rac;
+  clear_error();
+  if (!Xc || !G || n < 1 || len < 1 || ld < len || (method != 0 && method != 1))
+    return set_error(RAC_ERR_ARG, "rac_gram_covariance: bad arguments");
+  cudaStream_t st = 0;
+  int rc = RAC_OK;
+  if (method == 1) {
+    const size_t need = gram_i8_ws_bytes(len, n);
+    void* ws = nullptr;
+    if (cudaMalloc(&ws, need) != cudaSuccess) return set_error(RAC_ERR_CUDA, "rac_gram_covariance: out of memory");
+    rc = launch_gram_i8(Xc, ld, len, n, G, div, div > 0.0 ? 0 : 1, ws, need, st);
+    cudaStreamSynchronize(st);
+    cudaFree(ws);
+  } else {
+    GramPlan pl = plan_gram(len, n, 1);
+    pl.splits = 1;
+    pl.chunk = (len + 31) / 32 * 32;
+    int32_t* ids = nullptr;
+    if (cudaMalloc(&ids, sizeof(int32_t) * n) != cudaSuccess) return set_error(RAC_ERR_CUDA, "out of memory");
+    iota_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n);
+    rc = launch_gram(Xc, ld, pl.chunk, ids, nullptr, n, 1, G, pl, st, nullptr, div > 0.0 ? div : 0.0,
+                     div > 0.0 ? 0 : 1);
+    cudaStreamSynchronize(st);
+    cudaFree(ids);
+  }
+  if (rc) return rc;
+  return check_launch("rac_gram_covariance");
 }

@@ -216,6 +216,9 @@ __device__ __forceinline__ void cla_leader(const EnClaArgs& a, double* sm, int U
     for (int i = 0; i < 4; ++i) mbar_init(mb_dl + i, CLA_MAIN);
     mbar_fence_init();
   }
+  // the delta ring starts at zero: step 0's T_1 term (zero tile rows) reads slot 3, and
+  // 0 * (stale shared memory left by an earlier kernel) must not become NaN
+  for (int i = tid; i < 4 * s; i += blockDim.x) sDelta[i] = 0.0;
   cl.sync();   // every rank's barriers exist before anyone pushes into them
   const unsigned tag = a.tag;
   const double gamma = a.gamma;

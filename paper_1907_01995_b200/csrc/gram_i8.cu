@@ -1,0 +1,358 @@
+// Covariance Gram G = X'X (features x features) on the 5th-generation tensor cores in
+// exact integer arithmetic (tcgen05.mma kind::i8, int32 accumulators in TMEM).
+//
+// Replaces, for the covariance mode, the FP64 DMMA Gram of csrc/gram.cu: the same
+// quantity the reference forms per block as X[:, b].T @ X[:, b] (elastic_net.py:199-224,
+// the G = X'X/m restatement in DESIGN.md §4).
+//
+// Digit slicing (Ozaki scheme): every feature column j gets the power-of-two scale
+// 2^{e_j} > max_i |x_ij|, and x·2^{6-e_j} is split EXACTLY into S balanced digits
+//     x·2^{6-e_j} = d_1 + d_2 2^-7 + ... + d_S 2^{-7(S-1)} + rest,  d_s in [-64, 64]
+// (d = rint(r), r <- (r - d)·128: every step is exact in FP64).  Then
+//     G_jk = 2^{e_j+e_k-12} Σ_{w=2..S+1} 2^{-7(w-2)} C_w[j,k],
+//     C_w = Σ_{s+t=w} D_s' D_t      (int8 GEMMs, exact int32 sums)
+// The dropped products (s+t > S+1) and the rest terms are below 2^-52.8 of
+// max|x_j|·max|x_k| per sample for S = 8 — the rounding level of an FP64 dot product.
+// C_w for one 128 x 64 output tile lives in TMEM columns (w-2)·64 .. +63 (8 groups =
+// all 512 columns); each group's int32 sum is exact while K·S·64² < 2^31 (K segments of
+// 65472 samples, combined in FP64).  The FP64 combination runs in a fixed order, so the
+// result is deterministic and G is exactly symmetric (each unordered pair is formed once
+// and mirrored).
+//
+// Data layout: slice s is stored in the UMMA "no swizzle, K-major" canonical layout so
+// that one pipeline stage of a tile is ONE contiguous block fetched by one TMA bulk copy:
+//   byte ((kst * ngrp + g) * 4 + c) * 128 + r * 16 + b
+//   kst = sample / 64, g = feature / 8, c = (sample % 64) / 16, r = feature % 8, b = sample % 16
+// i.e. 8 x 16 B core matrices, LBO (K direction) = 128 B, SBO (8-feature groups) = 512 B.
+#include "rac_common.cuh"
+#include "rac_internal.h"
+
+namespace rac {
+namespace {
+
+constexpr int I8_S = 8;                       // digit slices
+constexpr int I8_TM = 128;                    // features per A tile (TMEM lanes)
+constexpr int I8_TN = 64;                     // features per B tile (TMEM columns per group)
+constexpr int I8_KS = 64;                     // samples per stage (bytes per row)
+constexpr int I8_NST = 2;                     // pipeline stages
+constexpr int I8_A_BYTES = I8_TM * I8_KS;     // 8 KB
+constexpr int I8_B_BYTES = I8_TN * I8_KS;     // 4 KB
+constexpr int I8_STAGE = I8_S * (I8_A_BYTES + I8_B_BYTES);
+constexpr int I8_SEGST = 1023;                // stages per exact int32 segment (65472 samples)
+constexpr int I8_SMEM = I8_NST * I8_STAGE + 1024;
+constexpr int I8_THREADS = 192;               // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
+static_assert(I8_S * 64 * 64 * (I8_SEGST * I8_KS) < 2147483648.0, "int32 group sums must stay exact");
+static_assert((I8_S)*I8_TN <= 512, "the weight groups must fit the 512 TMEM columns");
+
+struct I8Args {
+  const uint8_t* sl;     // S slices
+  size_t slice_bytes;
+  int ngrp;              // 8-feature groups (padded to a multiple of 16)
+  int nstg;              // 64-sample stages
+  int n;
+  int KT;                // 64-feature column tiles
+  const int* ex;         // per-feature exponents
+  double* G;             // n x n row-major
+  double div;            // > 0: G = sum / div ; accumulate: G += sum
+  int accum;
+};
+
+// ---- tcgen05 helpers ------------------------------------------------------------------
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// K-major, no swizzle: LBO = 128 B between the two 16-byte K chunks, SBO = 512 B between 8-row groups
+__device__ __forceinline__ uint64_t umma_desc(unsigned saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
+         (1ull << 46);
+}
+// kind::i8, D = s32 (bits 4-5 = 2), A / B signed int8 (bits 7-9, 10-12 = 1), both K-major,
+// N >> 3 at bits 17-22, M >> 4 at bits 24-28
+constexpr uint32_t I8_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(I8_TN >> 3) << 17) |
+                              ((uint32_t)(I8_TM >> 4) << 24);
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---- per-feature exponent: 2^e > max |x_j| ---------------------------------------------
+__global__ void i8_colexp_kernel(const double* __restrict__ Xc, int64_t ld, int64_t len, int n, int nfeat,
+                                 int* __restrict__ ex) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nfeat; j += warps) {
+    double mx = 0.0;
+    if (j < n) {
+      const double* col = Xc + (int64_t)j * ld;
+      for (int64_t k = lane; k < len; k += 32) mx = fmax(mx, fabs(__ldg(col + k)));
+    }
+    mx = warp_max(mx);
+    if (lane == 0) {
+      int e = 0;
+      if (mx > 0.0) frexp(mx, &e);
+      ex[j] = e;
+    }
+  }
+}
+
+// ---- digit slices in the canonical UMMA layout -----------------------------------------
+// CTA = one 8-feature group x 4 stages (256 samples); thread = (feature f, 8 samples)
+__global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict__ Xc, int64_t ld, int64_t len,
+                                                       int n, const int* __restrict__ ex, uint8_t* __restrict__ sl,
+                                                       size_t slice_bytes, int ngrp, int nstg) {
+  __shared__ __align__(16) uint8_t buf[I8_S][4 * 512];
+  const int f = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x;
+  const int j = g * 8 + f;
+  const int64_t k0 = (int64_t)blockIdx.y * 256 + lane * 8;
+  double x[8];
+  if (j < n && k0 + 8 <= len) {
+    const double2* p = reinterpret_cast<const double2*>(Xc + (int64_t)j * ld + k0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double2 t = __ldg(p + i);
+      x[2 * i] = t.x;
+      x[2 * i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = (j < n && k0 + i < len) ? Xc[(int64_t)j * ld + k0 + i] : 0.0;
+  }
+  const int e = (j < n) ? __ldg(ex + j) : 0;
+  unsigned long long packed[I8_S];
+#pragma unroll
+  for (int s = 0; s < I8_S; ++s) packed[s] = 0ull;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double r = ldexp(x[i], 6 - e);   // |r| < 64, exact
+#pragma unroll
+    for (int s = 0; s < I8_S; ++s) {
+      const double d = rint(r);      // |d| <= 64
+      r = (r - d) * 128.0;           // exact: |r - d| <= 1/2
+      packed[s] |= (unsigned long long)(uint8_t)(int8_t)(int)d << (8 * i);
+    }
+  }
+  // sample k0 + i -> stage lane / 8, chunk (lane % 8) / 2, byte (lane % 2) * 8 + i
+  const int off = (lane >> 3) * 512 + ((lane & 7) >> 1) * 128 + f * 16 + (lane & 1) * 8;
+#pragma unroll
+  for (int s = 0; s < I8_S; ++s) *reinterpret_cast<unsigned long long*>(&buf[s][off]) = packed[s];
+  __syncthreads();
+  // 8 slices x 4 stages x 512 B, 16 B per thread per pass
+  const int kst0 = blockIdx.y * 4;
+  for (int q = threadIdx.x; q < I8_S * 4 * 32; q += 256) {
+    const int s = q >> 7, kl = (q >> 5) & 3, o = q & 31;
+    if (kst0 + kl >= nstg) continue;
+    const uint4 v = *reinterpret_cast<const uint4*>(&buf[s][kl * 512 + o * 16]);
+    *reinterpret_cast<uint4*>(sl + s * slice_bytes + ((size_t)(kst0 + kl) * ngrp + g) * 512 + o * 16) = v;
+  }
+}
+
+// ---- the tensor-core Gram ----------------------------------------------------------------
+__global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t bar_full[I8_NST], bar_free[I8_NST], bar_acc, bar_tfree;
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // tile (J, Kt): row features 128J.., column features 64Kt.., only tiles holding some k >= j
+  int t = blockIdx.x, J = 0;
+  while (t >= a.KT - 2 * J) {
+    t -= a.KT - 2 * J;
+    ++J;
+  }
+  const int Kt = 2 * J + t;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < I8_NST; ++i) {
+      mbar_init(&bar_full[i], 1);
+      mbar_init(&bar_free[i], 1);
+    }
+    mbar_init(&bar_acc, 1);
+    mbar_init(&bar_tfree, 128);
+    mbar_fence_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int nseg = (a.nstg + I8_SEGST - 1) / I8_SEGST;
+
+  if (warp == 4) {
+    if (lane == 0) {
+      // TMA producer: one bulk copy per slice and operand per stage
+      const size_t offA = (size_t)J * 16 * 512, offB = (size_t)Kt * 8 * 512;
+      for (int q = 0; q < a.nstg; ++q) {
+        const int slot = q % I8_NST;
+        if (q >= I8_NST) mbar_wait(&bar_free[slot], ((q / I8_NST) - 1) & 1);
+        mbar_arrive_expect_tx(&bar_full[slot], I8_STAGE);
+        uint8_t* sA = smem + slot * I8_STAGE;
+        uint8_t* sB = sA + I8_S * I8_A_BYTES;
+        const size_t row = (size_t)q * a.ngrp * 512;
+#pragma unroll 1
+        for (int s = 0; s < I8_S; ++s) {
+          const uint8_t* src = a.sl + s * a.slice_bytes + row;
+          bulk_g2s(sA + s * I8_A_BYTES, src + offA, I8_A_BYTES, &bar_full[slot]);
+          bulk_g2s(sB + s * I8_B_BYTES, src + offB, I8_B_BYTES, &bar_full[slot]);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    if (lane == 0) {
+      // MMA issuer: per stage and 32-sample step, the S(S+1)/2 slice products into their groups
+      int seg = 0;
+      for (int q = 0; q < a.nstg; ++q) {
+        const int slot = q % I8_NST;
+        const bool first = (q % I8_SEGST) == 0;
+        if (first && q > 0) mbar_wait(&bar_tfree, (seg - 1) & 1);   // previous segment drained
+        mbar_wait(&bar_full[slot], (q / I8_NST) & 1);
+        tc_fence_after();
+        const unsigned sA = smem_u32(smem + slot * I8_STAGE);
+        const unsigned sB = sA + I8_S * I8_A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < I8_KS / 32; ++kk) {
+#pragma unroll
+          for (int w = 2; w <= I8_S + 1; ++w) {
+#pragma unroll
+            for (int s = 1; s < w; ++s) {
+              const int tt = w - s;
+              const uint64_t da = umma_desc(sA + (s - 1) * I8_A_BYTES + kk * 256);
+              const uint64_t db = umma_desc(sB + (tt - 1) * I8_B_BYTES + kk * 256);
+              tc_mma_i8(tmem + (uint32_t)((w - 2) * I8_TN), da, db, I8_IDESC,
+                        (first && kk == 0 && s == 1) ? 0u : 1u);
+            }
+          }
+        }
+        tc_commit(&bar_free[slot]);
+        if ((q % I8_SEGST) == I8_SEGST - 1 || q == a.nstg - 1) {
+          tc_commit(&bar_acc);
+          ++seg;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // epilogue: warp w owns TMEM lanes 32w.. = row features 128J + 32w + lane
+    double acc[2 * 32];
+#pragma unroll
+    for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    for (int sg = 0; sg < nseg; ++sg) {
+      mbar_wait(&bar_acc, sg & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int g = I8_S - 1; g >= 0; --g) {   // smallest weight first, fixed order
+        const double wgt = ldexp(1.0, -7 * g);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int v[32];
+          tmem_ld32(trow + (uint32_t)(g * I8_TN + h * 32), v);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc[h * 32 + c] = fma((double)v[c], wgt, acc[h * 32 + c]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&bar_tfree);
+    }
+    const int j = J * I8_TM + warp * 32 + lane;
+    if (j < a.n) {
+      const int ej = __ldg(a.ex + j) - 12;
+      double* Grow = a.G + (int64_t)j * a.n;
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        const int k = Kt * I8_TN + c;
+        if (k >= a.n || k < j) continue;
+        double val = ldexp(acc[c], ej + __ldg(a.ex + k));
+        if (a.accum) {
+          Grow[k] += val;
+          if (k > j) a.G[(int64_t)k * a.n + j] += val;
+        } else {
+          if (a.div > 0.0) val = val / a.div;
+          Grow[k] = val;
+          if (k > j) a.G[(int64_t)k * a.n + j] = val;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+}  // namespace
+
+size_t gram_i8_ws_bytes(int64_t len, int n) {
+  const int64_t nstg = (len + I8_KS - 1) / I8_KS;
+  const int64_t ngrp = (int64_t)((n + I8_TM - 1) / I8_TM) * 16;
+  return (size_t)I8_S * nstg * ngrp * 512 + (size_t)ngrp * 8 * sizeof(int) + 256;
+}
+
+// G (n x n, row-major) = Xc[:, :n]' Xc[:, :n] over samples [0, len) of the column-major Xc
+// (ld >= len): written / div (div > 0), or ADDED (accum) for row-chunk streaming.
+int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, double div, int accum, void* ws,
+                   size_t ws_bytes, cudaStream_t st) {
+  if (n < 1 || len < 1) return RAC_OK;
+  if (!ws || ws_bytes < gram_i8_ws_bytes(len, n)) return set_error(RAC_ERR_ARG, "gram_i8: workspace too small");
+  const int nstg = (int)((len + I8_KS - 1) / I8_KS);
+  const int ngrp = ((n + I8_TM - 1) / I8_TM) * 16;
+  const size_t slice_bytes = (size_t)nstg * ngrp * 512;
+  uint8_t* sl = static_cast<uint8_t*>(ws);
+  int* ex = reinterpret_cast<int*>(sl + I8_S * slice_bytes);
+  const int nfeat = ngrp * 8;
+  note_launch();
+  i8_colexp_kernel<<<std::min(num_sms() * 8, (nfeat + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, nfeat, ex);
+  if ((nstg + 3) / 4 > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8: too many samples");
+  note_launch();
+  i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 3) / 4)), 256, 0, st>>>(Xc, ld, len, n, ex, sl,
+                                                                                    slice_bytes, ngrp, nstg);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM);
+    attr = true;
+  }
+  I8Args a{};
+  a.sl = sl;
+  a.slice_bytes = slice_bytes;
+  a.ngrp = ngrp;
+  a.nstg = nstg;
+  a.n = n;
+  a.KT = (n + I8_TN - 1) / I8_TN;
+  a.ex = ex;
+  a.G = G;
+  a.div = div;
+  a.accum = accum;
+  int tiles = 0;
+  for (int J = 0; 2 * J < a.KT && J * I8_TM < n; ++J) tiles += a.KT - 2 * J;
+  note_launch();
+  gram_i8_kernel<<<tiles, I8_THREADS, I8_SMEM, st>>>(a);
+  return check_launch("gram_i8");
+}
+
+}  // namespace rac

@@ -47,6 +47,11 @@ int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx, c
 // symmetric raw sums are ADDED to ws (row-chunk streaming of G).
 // fixed-order sum of the split partials of ONE full Gram (ws [splits][n][n], lower part
 // valid), divided by div, written as the full symmetric n x n matrix
+// covariance Gram on the tensor cores in exact int8 digit-slice arithmetic (gram_i8.cu):
+// G = Xc' Xc over samples [0, len) written / div, or added (accum); ws >= gram_i8_ws_bytes
+size_t gram_i8_ws_bytes(int64_t len, int n);
+int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, double div, int accum, void* ws,
+                   size_t ws_bytes, cudaStream_t st);
 int launch_gram_reduce_sym(const double* ws, int64_t n, int splits, double div, double* G, cudaStream_t st);
 // K3: assemble block systems, Cholesky, explicit inverse.
 struct SysArgs {

@@ -1,0 +1,118 @@
+"""The covariance Gram on the tcgen05 int8 tensor cores (csrc/gram_i8.cu, exact digit
+slices) against an extended-precision host product and the FP64 DMMA tiles."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_1907_01995_b200 import _native
+    return _native.load()
+
+
+def _gram(lib, Xc, len_, n, div, method, G=None):
+    from paper_1907_01995_b200 import _native
+    if G is None:
+        G = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    _native.check(lib.rac_gram_covariance(C.c_void_p(Xc.data_ptr()), Xc.shape[1], len_, n,
+                                          C.c_void_p(G.data_ptr()), div, method))
+    return G
+
+
+def _device_cols(X):
+    m, n = X.shape
+    ld = (m + 31) // 32 * 32
+    Xc = torch.zeros((n, ld), dtype=torch.float64, device="cuda")
+    Xc[:, :m] = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()
+    return Xc
+
+
+# (m, n): ragged tiles (n not a multiple of 64 / 128), one sample stage, several int32
+# segments (m > 65472 samples), a single feature
+@pytest.mark.parametrize("m,n", [(64, 8), (77, 129), (1000, 300), (3000, 700), (70000, 150), (500, 1)])
+def test_int8_slice_gram_accuracy(lib, m, n):
+    rng = np.random.default_rng(m + n)
+    X = rng.standard_normal((m, n))
+    Xl = X.astype(np.longdouble)
+    R = Xl.T @ Xl
+    nrm = np.sqrt(np.diag(R).astype(np.float64))
+    Xc = _device_cols(X)
+    G8 = _gram(lib, Xc, m, n, 1.0, 1).cpu().numpy()
+    G0 = _gram(lib, Xc, m, n, 1.0, 0).cpu().numpy()
+    scale = np.maximum(np.outer(nrm, nrm), 1e-300)
+    e8 = (np.abs((G8.astype(np.longdouble) - R)).astype(np.float64) / scale).max()
+    e0 = (np.abs((G0.astype(np.longdouble) - R)).astype(np.float64) / scale).max()
+    # tolerance: 2 ulp of |x_j||x_k| (exact int32 sums; only the digit truncation below
+    # 2^-52.8 of max|x_j|max|x_k| per sample and the final FP64 combination round)
+    assert e8 <= 1e-15, e8
+    assert e8 <= max(e0, 1e-15)
+    assert np.array_equal(G8, G8.T)                 # each pair formed once, mirrored
+
+
+def test_int8_slice_gram_scaled_and_zero_columns(lib):
+    """Per-feature power-of-two scales: columns 1e-30 .. 1e30 and an all-zero column."""
+    rng = np.random.default_rng(5)
+    m, n = 2000, 260
+    X = rng.standard_normal((m, n)) * 10.0 ** rng.uniform(-30, 30, n)
+    X[:, 0] = 0.0
+    X[:, 7] = 0.0
+    Xl = X.astype(np.longdouble)
+    R = Xl.T @ Xl
+    nrm = np.sqrt(np.diag(R).astype(np.float64))
+    G8 = _gram(lib, _device_cols(X), m, n, 1.0, 1).cpu().numpy()
+    scale = np.maximum(np.outer(nrm, nrm), 1e-300)
+    assert (np.abs((G8.astype(np.longdouble) - R)).astype(np.float64) / scale).max() <= 4.5e-16
+    assert np.all(G8[0] == 0.0) and np.all(G8[:, 7] == 0.0)
+
+
+def test_int8_slice_gram_divides_and_accumulates(lib):
+    """div > 0 writes sum / div; div = 0 adds to G (the row-chunk streaming of fit)."""
+    rng = np.random.default_rng(9)
+    m, n = 4096, 333
+    X = rng.standard_normal((m, n))
+    Xc = _device_cols(X)
+    full = _gram(lib, Xc, m, n, float(m), 1).cpu().numpy()
+    G = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    half = m // 2
+    _gram(lib, Xc[:, :half].contiguous(), half, n, 0.0, 1, G)
+    _gram(lib, Xc[:, half:].contiguous(), m - half, n, 0.0, 1, G)
+    acc = G.cpu().numpy() / m
+    ref = (X.T @ X) / m
+    assert np.abs(full - ref).max() <= 1e-14 * np.abs(ref).max()
+    assert np.abs(acc - ref).max() <= 1e-14 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("ingest", ["host", "device"])
+def test_covariance_fit_with_int8_gram_vs_oracle(lib, monkeypatch, ingest):
+    """RAC_G_I8=2 forces the tensor-core Gram at sizes below its SM-filling threshold:
+    device-resident X (one launch) and host X streamed in row chunks (pieces of >= 4096
+    samples summed into G, the last piece ragged), per-sweep iterates against the oracle."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import _device, elastic_net as en
+    monkeypatch.setenv("RAC_G_I8", "2")
+    rng = np.random.default_rng(23)
+    for (m, n, s) in [(300, 200, 40), (9000, 600, 64)]:
+        X = rng.standard_normal((m, n))
+        y = X[:, :9] @ rng.standard_normal(9) + 0.05 * rng.standard_normal(m)
+        kw = dict(lam=0.05, alpha=0.7, gamma=1.0, block_size=s, iters=8, seed=4)
+        caps = {}
+        ro.en_fit(X, y, mode="rac", **kw,
+                  on_sweep=lambda k, bl, b, z, xi: caps.__setitem__(k, (b.copy(), z.copy(), xi.copy())))
+        got = {}
+        Xin = X if ingest == "host" else torch.from_numpy(X).cuda()
+        if ingest == "host" and m == 9000:
+            assert 8 * m * n > 2 * _device.ROW_CHUNK_BYTES      # the row-chunk path
+        en.fit(Xin, y, en.ElasticNetSpec(**kw), gram_mode="covariance",
+               sweep_hook=lambda k, b, z, xi: got.__setitem__(k, (b, z, xi)))
+        for k in caps:
+            for a_, b_ in zip(got[k], caps[k]):
+                err = np.linalg.norm(a_ - b_) / max(np.linalg.norm(b_), 1e-300)
+                assert err <= 1e-9, (m, n, s, k, err)

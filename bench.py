@@ -147,6 +147,44 @@ def traffic_table() -> dict:
     return out
 
 
+INT8_DENSE_TOPS_NOMINAL = 4500.0   # B200 dense INT8 (no measured int8 figure in MEASURED_PEAKS.json)
+
+
+def covariance_gram_timing(X, dev, reps: int = 3) -> dict:
+    """G = X'X/m of the covariance mode, CUDA-event timed (average of `reps` after one
+    warm-up) for the int8 digit-slice kernel (method 1: 36 int8 slice products per tile,
+    csrc/gram_i8.cu) and the FP64 DMMA tiles (method 0)."""
+    import ctypes as C
+    from paper_1907_01995_b200 import _native
+    lib = _native.load()
+    m, n = X.shape
+    Xc = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev)
+    G = torch.empty((n, n), dtype=torch.float64, device=dev)
+    out = {}
+    for meth, name in ((1, "int8_slices"), (0, "fp64_dmma")):
+        call = lambda: _native.check(lib.rac_gram_covariance(C.c_void_p(Xc.data_ptr()), m, m, n,
+                                                              C.c_void_p(G.data_ptr()), float(m), meth))
+        call()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            call()
+        e1.record()
+        torch.cuda.synchronize()
+        out[name + "_ms"] = e0.elapsed_time(e1) / reps
+    jt = (n + 127) // 128
+    kpad = (m + 31) // 32 * 32
+    ops = 2.0 * 36 * (jt * (jt + 1) // 2) * 128 * 128 * kpad      # int8 ops issued (full 128x128 tiles)
+    tops = ops / (out["int8_slices_ms"] * 1e-3) / 1e12
+    out.update({"int8_tops": tops, "int8_peak_tops": INT8_DENSE_TOPS_NOMINAL,
+                "int8_frac": tops / INT8_DENSE_TOPS_NOMINAL,
+                "algorithmic": "36 int8 slice products x 2*128*128*K per upper-triangle tile (incl. slicing "
+                               "and exponent passes in the time)"})
+    del Xc, G
+    return out
+
+
 def en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, workload, prep_batch=1) -> dict:
     """Roofline entry for the dominant stage of an EN sweep (per-unit figures: SURVEY.md §8(d)).
 
@@ -426,6 +464,12 @@ def run_b200_en(args, world, rank, local):
     roof = en_roofline(stages, m, n, s, p, gram_mode, chain_trace["variant"], hbm, fp64, case.name,
                        chain_trace.get("prep_batch_sweeps", 1))
 
+    # ---------------- the covariance Gram G = X'X/m (once per fit): int8 digit-slice tensor-core
+    # kernel vs the FP64 DMMA tiles, both through rac_gram_covariance on the resident X
+    gram_cov = None
+    if gram_mode == "covariance":
+        gram_cov = covariance_gram_timing(case.X, dev)
+
     # ---------------- the reference's own algorithm (per-sweep block Grams from X), reported
     # beside the covariance-mode headline (the G-reuse variant's algorithmic
     # work differs, so its roofline is not comparable)
@@ -507,6 +551,7 @@ def run_b200_en(args, world, rank, local):
         "roofline": roof,
         "reference_algorithm_variant": alt,
         "rp_mode_variant": rp,
+        "covariance_gram": gram_cov,
         "fp64_dgemm_tflops_measured": fp64,
         "cpu_baseline": cpu,
         "clocks": clk,

@@ -1459,12 +1459,20 @@ extern "C" int rac_gram_covariance(const double* Xc, int64_t ld, int64_t len, in
   cudaStream_t st = 0;
   int rc = RAC_OK;
   if (method == 1) {
+    // grow-only workspace kept between calls (a utility for tests and measurements)
+    static void* ws = nullptr;
+    static size_t cap = 0;
     const size_t need = gram_i8_ws_bytes(len, n);
-    void* ws = nullptr;
-    if (cudaMalloc(&ws, need) != cudaSuccess) return set_error(RAC_ERR_CUDA, "rac_gram_covariance: out of memory");
-    rc = launch_gram_i8(Xc, ld, len, n, G, div, div > 0.0 ? 0 : 1, ws, need, st);
+    if (cap < need) {
+      cudaDeviceSynchronize();
+      if (ws) cudaFree(ws);
+      ws = nullptr;
+      cap = 0;
+      if (cudaMalloc(&ws, need) != cudaSuccess) return set_error(RAC_ERR_CUDA, "rac_gram_covariance: out of memory");
+      cap = need;
+    }
+    rc = launch_gram_i8(Xc, ld, len, n, G, div, div > 0.0 ? 0 : 1, ws, cap, st);
     cudaStreamSynchronize(st);
-    cudaFree(ws);
   } else {
     GramPlan pl = plan_gram(len, n, 1);
     pl.splits = 1;

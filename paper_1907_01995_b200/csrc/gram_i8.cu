@@ -13,17 +13,23 @@
 //     C_w = Σ_{s+t=w} D_s' D_t      (int8 GEMMs, exact int32 sums)
 // The dropped products (s+t > S+1) and the rest terms are below 2^-52.8 of
 // max|x_j|·max|x_k| per sample for S = 8 — the rounding level of an FP64 dot product.
-// C_w for one 128 x 64 output tile lives in TMEM columns (w-2)·64 .. +63 (8 groups =
-// all 512 columns); each group's int32 sum is exact while K·S·64² < 2^31 (K segments of
-// 65472 samples, combined in FP64).  The FP64 combination runs in a fixed order, so the
+// Each group's int32 sum is exact while K·S·64² < 2^31 (K segments of 65472 samples,
+// combined in FP64).  The FP64 combination runs in a fixed order, so the
 // result is deterministic and G is exactly symmetric (each unordered pair is formed once
 // and mirrored).
 //
+// Tiles are 128 x 128 (M = N = 128 MMAs: 16 operand bytes per 1024 MACs, under the shared-memory
+// read rate that capped 128 x 64 tiles); the 8 weight groups need 1024 TMEM columns, so
+// each tile makes two passes over K with 4 groups (512 columns) each — the small weights
+// w = 6..9 (26 slice products, all 8 slices) first, then w = 2..5 (10 products, slices
+// 1-4).  Each pass's FP64 partial is added to the tile's upper-triangle entries of G,
+// the last one also writes the mirror.
+//
 // Data layout: slice s is stored in the UMMA "no swizzle, K-major" canonical layout so
-// that one pipeline stage of a tile is ONE contiguous block fetched by one TMA bulk copy:
-//   byte ((kst * ngrp + g) * 4 + c) * 128 + r * 16 + b
-//   kst = sample / 64, g = feature / 8, c = (sample % 64) / 16, r = feature % 8, b = sample % 16
-// i.e. 8 x 16 B core matrices, LBO (K direction) = 128 B, SBO (8-feature groups) = 512 B.
+// that one pipeline stage of a tile is ONE contiguous 4 KB block fetched by one TMA bulk copy:
+//   byte ((kst * ngrp + g) * 2 + c) * 128 + r * 16 + b
+//   kst = sample / 32, g = feature / 8, c = (sample % 32) / 16, r = feature % 8, b = sample % 16
+// i.e. 8 x 16 B core matrices, LBO (K direction) = 128 B, SBO (8-feature groups) = 256 B.
 #include "rac_common.cuh"
 #include "rac_internal.h"
 
@@ -32,25 +38,25 @@ namespace {
 
 constexpr int I8_S = 8;                       // digit slices
 constexpr int I8_TM = 128;                    // features per A tile (TMEM lanes)
-constexpr int I8_TN = 64;                     // features per B tile (TMEM columns per group)
-constexpr int I8_KS = 64;                     // samples per stage (bytes per row)
-constexpr int I8_NST = 2;                     // pipeline stages
-constexpr int I8_A_BYTES = I8_TM * I8_KS;     // 8 KB
-constexpr int I8_B_BYTES = I8_TN * I8_KS;     // 4 KB
-constexpr int I8_STAGE = I8_S * (I8_A_BYTES + I8_B_BYTES);
-constexpr int I8_SEGST = 1023;                // stages per exact int32 segment (65472 samples)
+constexpr int I8_TN = 128;                    // features per B tile (TMEM columns per group)
+constexpr int I8_KS = 32;                     // samples per stage (bytes per row) = one MMA K step
+constexpr int I8_NST = 3;                     // pipeline stages
+constexpr int I8_OP = I8_TM * I8_KS;          // 4 KB per slice operand per stage
+constexpr int I8_STAGE = 2 * I8_S * I8_OP;    // 64 KB: 8 A + 8 B slice operands
+constexpr int I8_SEGST = 2046;                // stages per exact int32 segment (65472 samples)
 constexpr int I8_SMEM = I8_NST * I8_STAGE + 1024;
 constexpr int I8_THREADS = 192;               // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
-static_assert(I8_S * 64 * 64 * (I8_SEGST * I8_KS) < 2147483648.0, "int32 group sums must stay exact");
-static_assert((I8_S)*I8_TN <= 512, "the weight groups must fit the 512 TMEM columns");
+static_assert(I8_S * 64 * 64 * (I8_SEGST * (double)I8_KS) < 2147483648.0, "int32 group sums must stay exact");
+static_assert(4 * I8_TN <= 512, "a pass's weight groups must fit the 512 TMEM columns");
+static_assert(I8_S == 8, "the two passes split the groups w = 2..9");
 
 struct I8Args {
   const uint8_t* sl;     // S slices
   size_t slice_bytes;
   int ngrp;              // 8-feature groups (padded to a multiple of 16)
-  int nstg;              // 64-sample stages
+  int nstg;              // 32-sample stages
   int n;
-  int KT;                // 64-feature column tiles
+  int JT;                // 128-feature tiles per side
   const int* ex;         // per-feature exponents
   double* G;             // n x n row-major
   double div;            // > 0: G = sum / div ; accumulate: G += sum
@@ -71,9 +77,9 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d, uint64_t a, uint64_t b, ui
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
-// K-major, no swizzle: LBO = 128 B between the two 16-byte K chunks, SBO = 512 B between 8-row groups
+// K-major, no swizzle: LBO = 128 B between the two 16-byte K chunks, SBO = 256 B between 8-row groups
 __device__ __forceinline__ uint64_t umma_desc(unsigned saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(512 >> 4) << 32) |
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
          (1ull << 46);
 }
 // kind::i8, D = s32 (bits 4-5 = 2), A / B signed int8 (bits 7-9, 10-12 = 1), both K-major,
@@ -114,11 +120,11 @@ __global__ void i8_colexp_kernel(const double* __restrict__ Xc, int64_t ld, int6
 }
 
 // ---- digit slices in the canonical UMMA layout -----------------------------------------
-// CTA = one 8-feature group x 4 stages (256 samples); thread = (feature f, 8 samples)
+// CTA = one 8-feature group x 8 stages (256 samples); thread = (feature f, 8 samples)
 __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict__ Xc, int64_t ld, int64_t len,
                                                        int n, const int* __restrict__ ex, uint8_t* __restrict__ sl,
                                                        size_t slice_bytes, int ngrp, int nstg) {
-  __shared__ __align__(16) uint8_t buf[I8_S][4 * 512];
+  __shared__ __align__(16) uint8_t buf[I8_S][8 * 256];
   const int f = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x;
   const int j = g * 8 + f;
@@ -150,22 +156,23 @@ __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict_
       packed[s] |= (unsigned long long)(uint8_t)(int8_t)(int)d << (8 * i);
     }
   }
-  // sample k0 + i -> stage lane / 8, chunk (lane % 8) / 2, byte (lane % 2) * 8 + i
-  const int off = (lane >> 3) * 512 + ((lane & 7) >> 1) * 128 + f * 16 + (lane & 1) * 8;
+  // sample k0 + i -> stage lane / 4, chunk (lane % 4) / 2, byte (lane % 2) * 8 + i
+  const int off = (lane >> 2) * 256 + ((lane & 3) >> 1) * 128 + f * 16 + (lane & 1) * 8;
 #pragma unroll
   for (int s = 0; s < I8_S; ++s) *reinterpret_cast<unsigned long long*>(&buf[s][off]) = packed[s];
   __syncthreads();
-  // 8 slices x 4 stages x 512 B, 16 B per thread per pass
-  const int kst0 = blockIdx.y * 4;
-  for (int q = threadIdx.x; q < I8_S * 4 * 32; q += 256) {
-    const int s = q >> 7, kl = (q >> 5) & 3, o = q & 31;
+  // 8 slices x 8 stages x 256 B, 16 B per thread per pass
+  const int kst0 = blockIdx.y * 8;
+  for (int q = threadIdx.x; q < I8_S * 8 * 16; q += 256) {
+    const int s = q >> 7, kl = (q >> 4) & 7, o = q & 15;
     if (kst0 + kl >= nstg) continue;
-    const uint4 v = *reinterpret_cast<const uint4*>(&buf[s][kl * 512 + o * 16]);
-    *reinterpret_cast<uint4*>(sl + s * slice_bytes + ((size_t)(kst0 + kl) * ngrp + g) * 512 + o * 16) = v;
+    const uint4 v = *reinterpret_cast<const uint4*>(&buf[s][kl * 256 + o * 16]);
+    *reinterpret_cast<uint4*>(sl + s * slice_bytes + ((size_t)(kst0 + kl) * ngrp + g) * 256 + o * 16) = v;
   }
 }
 
 // ---- the tensor-core Gram ----------------------------------------------------------------
+// phases: pass 0 (groups w = 6..9) then pass 1 (w = 2..5), each over the K segments
 __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -173,13 +180,13 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // tile (J, Kt): row features 128J.., column features 64Kt.., only tiles holding some k >= j
+  // tile (J, Kt), Kt >= J: row features 128J.., column features 128Kt..
   int t = blockIdx.x, J = 0;
-  while (t >= a.KT - 2 * J) {
-    t -= a.KT - 2 * J;
+  while (t >= a.JT - J) {
+    t -= a.JT - J;
     ++J;
   }
-  const int Kt = 2 * J + t;
+  const int Kt = J + t;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < I8_NST; ++i) {
@@ -200,102 +207,126 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   const int nseg = (a.nstg + I8_SEGST - 1) / I8_SEGST;
+  const int nphase = 2 * nseg;
 
   if (warp == 4) {
     if (lane == 0) {
-      // TMA producer: one bulk copy per slice and operand per stage
-      const size_t offA = (size_t)J * 16 * 512, offB = (size_t)Kt * 8 * 512;
-      for (int q = 0; q < a.nstg; ++q) {
-        const int slot = q % I8_NST;
-        if (q >= I8_NST) mbar_wait(&bar_free[slot], ((q / I8_NST) - 1) & 1);
-        mbar_arrive_expect_tx(&bar_full[slot], I8_STAGE);
-        uint8_t* sA = smem + slot * I8_STAGE;
-        uint8_t* sB = sA + I8_S * I8_A_BYTES;
-        const size_t row = (size_t)q * a.ngrp * 512;
+      // TMA producer: one 4 KB bulk copy per slice operand per stage
+      const size_t offA = (size_t)J * 16 * 256, offB = (size_t)Kt * 16 * 256;
+      int q = 0;
+      for (int ph = 0; ph < nphase; ++ph) {
+        const int ns = (ph < nseg) ? I8_S : 4;   // pass 0 reads all slices, pass 1 slices 1-4
+        const int sg = ph % nseg;
+        const int q1 = min(a.nstg, (sg + 1) * I8_SEGST);
+        // pass 1 packs two 32-sample steps (4 slices each) into one slot
+        const int kpack = (ph < nseg) ? 1 : 2;
+        for (int kst = sg * I8_SEGST; kst < q1; kst += kpack, ++q) {
+          const int slot = q % I8_NST;
+          const int nk = min(kpack, q1 - kst);
+          if (q >= I8_NST) mbar_wait(&bar_free[slot], ((q / I8_NST) - 1) & 1);
+          mbar_arrive_expect_tx(&bar_full[slot], (unsigned)(2 * ns * nk * I8_OP));
+          uint8_t* sA = smem + slot * I8_STAGE;
+          uint8_t* sB = sA + I8_S * I8_OP;
 #pragma unroll 1
-        for (int s = 0; s < I8_S; ++s) {
-          const uint8_t* src = a.sl + s * a.slice_bytes + row;
-          bulk_g2s(sA + s * I8_A_BYTES, src + offA, I8_A_BYTES, &bar_full[slot]);
-          bulk_g2s(sB + s * I8_B_BYTES, src + offB, I8_B_BYTES, &bar_full[slot]);
+          for (int h = 0; h < nk; ++h) {
+            const size_t row = (size_t)(kst + h) * a.ngrp * 256;
+#pragma unroll 1
+            for (int s = 0; s < ns; ++s) {
+              const uint8_t* src = a.sl + s * a.slice_bytes + row;
+              bulk_g2s(sA + (h * 4 + s) * I8_OP, src + offA, I8_OP, &bar_full[slot]);
+              bulk_g2s(sB + (h * 4 + s) * I8_OP, src + offB, I8_OP, &bar_full[slot]);
+            }
+          }
         }
       }
     }
     __syncwarp();
   } else if (warp == 5) {
     if (lane == 0) {
-      // MMA issuer: per stage and 32-sample step, the S(S+1)/2 slice products into their groups
-      int seg = 0;
-      for (int q = 0; q < a.nstg; ++q) {
-        const int slot = q % I8_NST;
-        const bool first = (q % I8_SEGST) == 0;
-        if (first && q > 0) mbar_wait(&bar_tfree, (seg - 1) & 1);   // previous segment drained
-        mbar_wait(&bar_full[slot], (q / I8_NST) & 1);
+      // MMA issuer: per stage the phase's slice products into their weight groups
+      int q = 0;
+      for (int ph = 0; ph < nphase; ++ph) {
+        const bool p0 = ph < nseg;
+        const int sg = ph % nseg;
+        const int q1 = min(a.nstg, (sg + 1) * I8_SEGST);
+        if (ph > 0) mbar_wait(&bar_tfree, (ph - 1) & 1);   // previous phase drained from TMEM
         tc_fence_after();
-        const unsigned sA = smem_u32(smem + slot * I8_STAGE);
-        const unsigned sB = sA + I8_S * I8_A_BYTES;
+        const int kpack = p0 ? 1 : 2;
+        for (int kst = sg * I8_SEGST; kst < q1; kst += kpack, ++q) {
+          const int slot = q % I8_NST;
+          const int nk = min(kpack, q1 - kst);
+          const bool first = kst == sg * I8_SEGST;
+          mbar_wait(&bar_full[slot], (q / I8_NST) & 1);
+          tc_fence_after();
+          const unsigned sA = smem_u32(smem + slot * I8_STAGE);
+          const unsigned sB = sA + I8_S * I8_OP;
+          if (p0) {
 #pragma unroll
-        for (int kk = 0; kk < I8_KS / 32; ++kk) {
+            for (int w = 6; w <= 9; ++w)
 #pragma unroll
-          for (int w = 2; w <= I8_S + 1; ++w) {
+              for (int s = 1; s < w; ++s)
+                tc_mma_i8(tmem + (uint32_t)((w - 6) * I8_TN), umma_desc(sA + (s - 1) * I8_OP),
+                          umma_desc(sB + (w - s - 1) * I8_OP), I8_IDESC, (first && s == 1) ? 0u : 1u);
+          } else {
+#pragma unroll 1
+            for (int h = 0; h < nk; ++h)
 #pragma unroll
-            for (int s = 1; s < w; ++s) {
-              const int tt = w - s;
-              const uint64_t da = umma_desc(sA + (s - 1) * I8_A_BYTES + kk * 256);
-              const uint64_t db = umma_desc(sB + (tt - 1) * I8_B_BYTES + kk * 256);
-              tc_mma_i8(tmem + (uint32_t)((w - 2) * I8_TN), da, db, I8_IDESC,
-                        (first && kk == 0 && s == 1) ? 0u : 1u);
-            }
+              for (int w = 2; w <= 5; ++w)
+#pragma unroll
+                for (int s = 1; s < w; ++s)
+                  tc_mma_i8(tmem + (uint32_t)((w - 2) * I8_TN), umma_desc(sA + (h * 4 + s - 1) * I8_OP),
+                            umma_desc(sB + (h * 4 + w - s - 1) * I8_OP), I8_IDESC,
+                            (first && h == 0 && s == 1) ? 0u : 1u);
           }
+          tc_commit(&bar_free[slot]);
         }
-        tc_commit(&bar_free[slot]);
-        if ((q % I8_SEGST) == I8_SEGST - 1 || q == a.nstg - 1) {
-          tc_commit(&bar_acc);
-          ++seg;
-        }
+        tc_commit(&bar_acc);
       }
     }
     __syncwarp();
   } else {
-    // epilogue: warp w owns TMEM lanes 32w.. = row features 128J + 32w + lane
-    double acc[2 * 32];
-#pragma unroll
-    for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+    // epilogue: warp w owns TMEM lanes 32w.. = row feature j = 128J + 32w + lane; per phase
+    // the FP64 partial sum_g 2^{-7(w-2)} C_w · 2^{e_j + e_k - 12} is added to G[j][k] (k >= j)
     const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-    for (int sg = 0; sg < nseg; ++sg) {
-      mbar_wait(&bar_acc, sg & 1);
+    const int j = J * I8_TM + warp * 32 + lane;
+    const bool jok = j < a.n;
+    const int ej = jok ? __ldg(a.ex + j) - 12 : 0;
+    double* Grow = a.G + (int64_t)(jok ? j : 0) * a.n;
+    for (int ph = 0; ph < nphase; ++ph) {
+      const int w0 = (ph < nseg) ? 6 : 2;     // groups w0 .. w0 + 3 in TMEM columns 0..511
+      const bool last = ph == nphase - 1;
+      mbar_wait(&bar_acc, ph & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int g = I8_S - 1; g >= 0; --g) {   // smallest weight first, fixed order
-        const double wgt = ldexp(1.0, -7 * g);
+      for (int cc = 0; cc < I8_TN / 32; ++cc) {
+        double acc[32];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+#pragma unroll 1
+        for (int g = 3; g >= 0; --g) {        // smallest weight first, fixed order
           int v[32];
-          tmem_ld32(trow + (uint32_t)(g * I8_TN + h * 32), v);
+          tmem_ld32(trow + (uint32_t)(g * I8_TN + cc * 32), v);
+          const double wgt = ldexp(1.0, -7 * (w0 + g - 2));
 #pragma unroll
-          for (int c = 0; c < 32; ++c) acc[h * 32 + c] = fma((double)v[c], wgt, acc[h * 32 + c]);
+          for (int c = 0; c < 32; ++c) acc[c] = fma((double)v[c], wgt, acc[c]);
+        }
+        if (!jok) continue;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const int k = Kt * I8_TN + cc * 32 + c;
+          if (k >= a.n || k < j) continue;
+          const double part = ldexp(acc[c], ej + __ldg(a.ex + k));
+          const double cur = (ph == 0 && !a.accum) ? 0.0 : Grow[k];
+          double val = cur + part;
+          if (last) {
+            if (!a.accum && a.div > 0.0) val = val / a.div;
+            if (k > j) a.G[(int64_t)k * a.n + j] = val;
+          }
+          Grow[k] = val;
         }
       }
       tc_fence_before();
       mbar_arrive(&bar_tfree);
-    }
-    const int j = J * I8_TM + warp * 32 + lane;
-    if (j < a.n) {
-      const int ej = __ldg(a.ex + j) - 12;
-      double* Grow = a.G + (int64_t)j * a.n;
-#pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const int k = Kt * I8_TN + c;
-        if (k >= a.n || k < j) continue;
-        double val = ldexp(acc[c], ej + __ldg(a.ex + k));
-        if (a.accum) {
-          Grow[k] += val;
-          if (k > j) a.G[(int64_t)k * a.n + j] += val;
-        } else {
-          if (a.div > 0.0) val = val / a.div;
-          Grow[k] = val;
-          if (k > j) a.G[(int64_t)k * a.n + j] = val;
-        }
-      }
     }
   }
   tc_fence_before();
@@ -311,7 +342,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
 size_t gram_i8_ws_bytes(int64_t len, int n) {
   const int64_t nstg = (len + I8_KS - 1) / I8_KS;
   const int64_t ngrp = (int64_t)((n + I8_TM - 1) / I8_TM) * 16;
-  return (size_t)I8_S * nstg * ngrp * 512 + (size_t)ngrp * 8 * sizeof(int) + 256;
+  return (size_t)I8_S * nstg * ngrp * 256 + (size_t)ngrp * 8 * sizeof(int) + 256;
 }
 
 // G (n x n, row-major) = Xc[:, :n]' Xc[:, :n] over samples [0, len) of the column-major Xc
@@ -322,15 +353,15 @@ int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, 
   if (!ws || ws_bytes < gram_i8_ws_bytes(len, n)) return set_error(RAC_ERR_ARG, "gram_i8: workspace too small");
   const int nstg = (int)((len + I8_KS - 1) / I8_KS);
   const int ngrp = ((n + I8_TM - 1) / I8_TM) * 16;
-  const size_t slice_bytes = (size_t)nstg * ngrp * 512;
+  const size_t slice_bytes = (size_t)nstg * ngrp * 256;
   uint8_t* sl = static_cast<uint8_t*>(ws);
   int* ex = reinterpret_cast<int*>(sl + I8_S * slice_bytes);
   const int nfeat = ngrp * 8;
   note_launch();
   i8_colexp_kernel<<<std::min(num_sms() * 8, (nfeat + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, nfeat, ex);
-  if ((nstg + 3) / 4 > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8: too many samples");
+  if ((nstg + 7) / 8 > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8: too many samples");
   note_launch();
-  i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 3) / 4)), 256, 0, st>>>(Xc, ld, len, n, ex, sl,
+  i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8)), 256, 0, st>>>(Xc, ld, len, n, ex, sl,
                                                                                     slice_bytes, ngrp, nstg);
   static bool attr = false;
   if (!attr) {
@@ -343,13 +374,12 @@ int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, 
   a.ngrp = ngrp;
   a.nstg = nstg;
   a.n = n;
-  a.KT = (n + I8_TN - 1) / I8_TN;
+  a.JT = (n + I8_TM - 1) / I8_TM;
   a.ex = ex;
   a.G = G;
   a.div = div;
   a.accum = accum;
-  int tiles = 0;
-  for (int J = 0; 2 * J < a.KT && J * I8_TM < n; ++J) tiles += a.KT - 2 * J;
+  const int tiles = a.JT * (a.JT + 1) / 2;
   note_launch();
   gram_i8_kernel<<<tiles, I8_THREADS, I8_SMEM, st>>>(a);
   return check_launch("gram_i8");

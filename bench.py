@@ -155,6 +155,8 @@ def covariance_gram_timing(X, dev, reps: int = 3) -> dict:
     warm-up) for the int8 digit-slice kernel (method 1: 36 int8 slice products per tile,
     csrc/gram_i8.cu) and the FP64 DMMA tiles (method 0)."""
     import ctypes as C
+
+    import torch
     from paper_1907_01995_b200 import _native
     lib = _native.load()
     m, n = X.shape

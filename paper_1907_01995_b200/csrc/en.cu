@@ -322,6 +322,9 @@ struct rac_en_ctx {
   void* i8_ws = nullptr;      // digit slices of the tensor-core Gram (gram_i8.cu), null = DMMA Gram
   size_t i8_ws_cap = 0;
   int64_t g_rows_done = 0;    // row-chunk ingest: samples already summed into G
+  void* bg_ws = nullptr;      // block mode: per-sweep digit slices of the int8 block Grams, null = DMMA
+  size_t bg_cap = 0;
+  int* ex_all = nullptr;      // block mode: per-feature exponents of Xc (set with the data)
   // lookahead covariance chain (en_cla.cuh); cla_L = leader cluster size, 0 = not used
   int cla_L = 0, cla_D = 3, cla_W = 0, cla_segw = 1, cla_R = 2, cla_NS = 2;
   size_t cla_smem = 0;
@@ -561,7 +564,7 @@ int en_factor(rac_en_ctx* c, cudaStream_t st, int sweeps = 1) {
     a.mul = 1.0;
   } else {
     a.ws = c->gram_ws;
-    a.splits = c->gp.splits;
+    a.splits = c->bg_ws ? 1 : c->gp.splits;   // the int8 block Grams are complete (one split)
     a.div = (double)c->m;
     a.mul = 1.0;
   }
@@ -581,10 +584,18 @@ int en_factor(rac_en_ctx* c, cudaStream_t st, int sweeps = 1) {
   return RAC_OK;
 }
 
+// block mode: the p block Grams of the partition in c->idx into gram_ws — int8 tensor
+// cores (exact digit slices, gram_i8.cu) when reserved, else the FP64 DMMA tiles
+int en_block_gram(rac_en_ctx* c, cudaStream_t st) {
+  if (c->bg_ws)
+    return rac::launch_gram_i8_blocks(c->Xc, c->ld, c->m, c->idx, c->s, c->p, c->ex_all, c->gram_ws, c->bg_ws,
+                                      c->bg_cap, st);
+  return rac::launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, st, c->ctrl);
+}
+
 int en_block_systems(rac_en_ctx* c) {
   if (c->gram_mode != 1) {
-    int rc = rac::launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->st,
-                              c->ctrl);
+    int rc = en_block_gram(c, c->st);
     if (rc) return rc;
   }
   return en_factor(c, c->st);
@@ -698,6 +709,7 @@ int en_chain_cov(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  cudaFuncSetAttribute(cov_kernel(c->cov_k), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
   note_launch();
   return check_cuda(cudaLaunchKernelExC(&cfg, cov_kernel(c->cov_k), args), "en_cov (cluster launch)");
 }
@@ -762,12 +774,21 @@ int en_chain(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
     // one CTA per SM either way, and ncu serialises kernels, so the barrier still holds).
     static const bool noncoop = getenv("RAC_PROFILE_NONCOOP") && atoi(getenv("RAC_PROFILE_NONCOOP")) == 1;
     cfg.numAttrs = noncoop ? 1 : 2;
+    // the function attribute is process-wide: another context's plan may have lowered it
+    cudaFuncSetAttribute(res_kernel(c->cs), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
     note_launch();
     return check_cuda(cudaLaunchKernelExC(&cfg, (const void*)res_kernel(c->cs), rargs),
                       "en_chain_res (cluster cooperative launch)");
   }
   size_t smem = c->RC == 0 ? row1t_smem_bytes(c->s, c->rw) : en_chain_smem(c->s, c->RC);
   cudaError_t e;
+  {
+    // the function attribute is process-wide: another context's plan may have lowered it
+    void* kf = c->RC == 0 ? (void*)en_chain_kernel<0>
+                          : (c->RC == 32 ? (void*)en_chain_kernel<32>
+                                         : (c->RC == 16 ? (void*)en_chain_kernel<16> : (void*)en_chain_kernel<8>));
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
   if (c->RC == 0)
     e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<0>, dim3(c->P), dim3(ENT), args, smem, st);
   else if (c->RC == 32)
@@ -923,6 +944,25 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
     rac_en_destroy(c);
     return rc;
   }
+  {
+    // int8 tensor-core block Grams when a sweep's 128 x 128 tiles fill the SMs several times
+    // (RAC_BG_I8=2 forces them, =0 keeps the DMMA tiles)
+    const char* e8 = getenv("RAC_BG_I8");
+    const int mode8 = e8 ? atoi(e8) : 1;
+    const int64_t jt = (s + 127) / 128;
+    const int64_t tiles = (int64_t)c->p * jt * (jt + 1) / 2;
+    if (mode8 == 2 || (mode8 == 1 && s >= 128 && tiles >= 4 * (int64_t)num_sms())) {
+      const size_t need = gram_i8_blocks_ws_bytes(c->ld, s, c->p);
+      uint8_t* w = nullptr;
+      if (dalloc(c, &w, need) == RAC_OK && dalloc(c, &c->ex_all, n) == RAC_OK) {
+        c->bg_ws = w;
+        c->bg_cap = need;
+      } else {
+        cudaGetLastError();
+        clear_error();
+      }
+    }
+  }
   size_t scr = chol_scratch_bytes(s, c->p);
   if (scr && (rc = dalloc(c, &c->scratch, scr / sizeof(double)))) {
     rac_en_destroy(c);
@@ -991,6 +1031,10 @@ extern "C" int rac_en_set_data(rac_en_ctx* c, const double* X, int32_t layout, c
   int blocks = (int)std::min<int64_t>((c->n + 7) / 8, (int64_t)num_sms() * 16);
   note_launch();
   neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
+  if (c->bg_ws) {
+    int rc = launch_i8_colexp(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->st);
+    if (rc) return rc;
+  }
   c->have_data = true;
   return check_launch("rac_en_set_data");
 }
@@ -1053,6 +1097,7 @@ extern "C" int rac_en_set_data_rows(rac_en_ctx* c, const double* X_rows, int64_t
   int blocks = (int)std::min<int64_t>((c->n + 7) / 8, (int64_t)num_sms() * 16);
   note_launch();
   neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
+  if (c->bg_ws && (rc = launch_i8_colexp(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->st))) return rc;
   if (c->gram_mode == 1) {
     scale_kernel<<<num_sms() * 8, 256, 0, c->st>>>(c->G, c->n * c->n, (double)c->m);   // dot, then / m
     note_launch();
@@ -1243,10 +1288,7 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
       c->info = c->info_b[j];
       c->T = c->T_b[j];
       if ((rc = launch_chunk_sort(perms + (int64_t)k * c->n, c->n, c->s, 1, c->idx, c->sprep))) return rc;
-      if (c->gram_mode != 1 &&
-          (rc = launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->sprep,
-                            c->ctrl)))
-        return rc;
+      if (c->gram_mode != 1 && (rc = en_block_gram(c, c->sprep))) return rc;
       if ((rc = en_factor(c, c->sprep))) return rc;
       cudaEventRecord(c->ev_prep[j], c->sprep);
       cudaStreamWaitEvent(c->schain, c->ev_prep[j], 0);
@@ -1270,7 +1312,7 @@ extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, do
       if (rc) return rc;
       if (c->timing) cudaEventRecord(ev[1], c->st);
       if (c->gram_mode != 1) {
-        rc = launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, c->st, c->ctrl);
+        rc = en_block_gram(c, c->st);
         if (rc) return rc;
       }
       if (c->timing) cudaEventRecord(ev[2], c->st);

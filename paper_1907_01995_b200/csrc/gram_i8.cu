@@ -61,6 +61,9 @@ struct I8Args {
   double* G;             // n x n row-major
   double div;            // > 0: G = sum / div ; accumulate: G += sum
   int accum;
+  size_t blk_sl;         // block mode (blockIdx.y = block): slice, output and exponent strides
+  int64_t blk_g;
+  int blk_ex;
 };
 
 // ---- tcgen05 helpers ------------------------------------------------------------------
@@ -120,17 +123,26 @@ __global__ void i8_colexp_kernel(const double* __restrict__ Xc, int64_t ld, int6
 }
 
 // ---- digit slices in the canonical UMMA layout -----------------------------------------
-// CTA = one 8-feature group x 8 stages (256 samples); thread = (feature f, 8 samples)
+// CTA = one 8-feature group x 8 stages (256 samples); thread = (feature f, 8 samples).
+// Covariance: features 0..n-1 of Xc.  Block mode (idx != null): blockIdx.z = block b, whose
+// features are idx[b*n ..] (n = s, -1 = padding), exponents ex[feature], and the block's
+// per-position exponents are written to ex_blk[b * nfeat + position].
 __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict__ Xc, int64_t ld, int64_t len,
                                                        int n, const int* __restrict__ ex, uint8_t* __restrict__ sl,
-                                                       size_t slice_bytes, int ngrp, int nstg) {
+                                                       size_t slice_bytes, int ngrp, int nstg,
+                                                       const int32_t* __restrict__ idx, int* __restrict__ ex_blk) {
   __shared__ __align__(16) uint8_t buf[I8_S][8 * 256];
   const int f = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x;
-  const int j = g * 8 + f;
+  const int pos = g * 8 + f;
+  int j = pos < n ? pos : -1;
+  if (idx) {
+    j = pos < n ? __ldg(idx + (size_t)blockIdx.z * n + pos) : -1;
+    sl += (size_t)blockIdx.z * I8_S * slice_bytes;
+  }
   const int64_t k0 = (int64_t)blockIdx.y * 256 + lane * 8;
   double x[8];
-  if (j < n && k0 + 8 <= len) {
+  if (j >= 0 && k0 + 8 <= len) {
     const double2* p = reinterpret_cast<const double2*>(Xc + (int64_t)j * ld + k0);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -140,9 +152,10 @@ __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict_
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = (j < n && k0 + i < len) ? Xc[(int64_t)j * ld + k0 + i] : 0.0;
+    for (int i = 0; i < 8; ++i) x[i] = (j >= 0 && k0 + i < len) ? Xc[(int64_t)j * ld + k0 + i] : 0.0;
   }
-  const int e = (j < n) ? __ldg(ex + j) : 0;
+  const int e = (j >= 0) ? __ldg(ex + j) : 0;
+  if (idx && blockIdx.y == 0 && lane == 0) ex_blk[(size_t)blockIdx.z * ngrp * 8 + pos] = e;
   unsigned long long packed[I8_S];
 #pragma unroll
   for (int s = 0; s < I8_S; ++s) packed[s] = 0ull;
@@ -174,6 +187,9 @@ __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict_
 // ---- the tensor-core Gram ----------------------------------------------------------------
 // phases: pass 0 (groups w = 6..9) then pass 1 (w = 2..5), each over the K segments
 __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
+  a.sl += blockIdx.y * a.blk_sl;
+  a.G += blockIdx.y * a.blk_g;
+  a.ex += blockIdx.y * a.blk_ex;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bar_full[I8_NST], bar_free[I8_NST], bar_acc, bar_tfree;
@@ -361,8 +377,8 @@ int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, 
   i8_colexp_kernel<<<std::min(num_sms() * 8, (nfeat + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, nfeat, ex);
   if ((nstg + 7) / 8 > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8: too many samples");
   note_launch();
-  i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8)), 256, 0, st>>>(Xc, ld, len, n, ex, sl,
-                                                                                    slice_bytes, ngrp, nstg);
+  i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8)), 256, 0, st>>>(
+      Xc, ld, len, n, ex, sl, slice_bytes, ngrp, nstg, nullptr, nullptr);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM);
@@ -383,6 +399,57 @@ int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, 
   note_launch();
   gram_i8_kernel<<<tiles, I8_THREADS, I8_SMEM, st>>>(a);
   return check_launch("gram_i8");
+}
+
+size_t gram_i8_blocks_ws_bytes(int64_t len, int s, int p) {
+  const int64_t nstg = (len + I8_KS - 1) / I8_KS;
+  const int64_t ngrp = (int64_t)((s + I8_TM - 1) / I8_TM) * 16;
+  return (size_t)p * I8_S * nstg * ngrp * 256 + (size_t)p * ngrp * 8 * sizeof(int) + 256;
+}
+
+int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st) {
+  note_launch();
+  i8_colexp_kernel<<<std::min(num_sms() * 8, (n + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, n, ex);
+  return check_launch("i8 exponents");
+}
+
+// block mode: the p block Grams (full symmetric s x s raw sums, out[b][s][s]) of the
+// feature lists idx[b*s ..] (-1 = padding), ex_all = per-feature exponents of Xc
+int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32_t* idx, int s, int p,
+                          const int* ex_all, double* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (!ws || ws_bytes < gram_i8_blocks_ws_bytes(len, s, p))
+    return set_error(RAC_ERR_ARG, "gram_i8 blocks: workspace too small");
+  const int nstg = (int)((len + I8_KS - 1) / I8_KS);
+  const int ngrp = ((s + I8_TM - 1) / I8_TM) * 16;
+  const size_t slice_bytes = (size_t)nstg * ngrp * 256;
+  uint8_t* sl = static_cast<uint8_t*>(ws);
+  int* ex_blk = reinterpret_cast<int*>(sl + (size_t)p * I8_S * slice_bytes);
+  if ((nstg + 7) / 8 > 65535 || p > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8 blocks: shape");
+  note_launch();
+  i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8), (unsigned)p), 256, 0, st>>>(
+      Xc, ld, len, s, ex_all, sl, slice_bytes, ngrp, nstg, idx, ex_blk);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM);
+    attr = true;
+  }
+  I8Args a{};
+  a.sl = sl;
+  a.slice_bytes = slice_bytes;
+  a.ngrp = ngrp;
+  a.nstg = nstg;
+  a.n = s;
+  a.JT = (s + I8_TM - 1) / I8_TM;
+  a.ex = ex_blk;
+  a.G = out;
+  a.div = 0.0;
+  a.accum = 0;
+  a.blk_sl = (size_t)I8_S * slice_bytes;
+  a.blk_g = (int64_t)s * s;
+  a.blk_ex = ngrp * 8;
+  note_launch();
+  gram_i8_kernel<<<dim3((unsigned)(a.JT * (a.JT + 1) / 2), (unsigned)p), I8_THREADS, I8_SMEM, st>>>(a);
+  return check_launch("gram_i8 blocks");
 }
 
 }  // namespace rac

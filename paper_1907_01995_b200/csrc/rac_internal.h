@@ -52,6 +52,12 @@ int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx, c
 size_t gram_i8_ws_bytes(int64_t len, int n);
 int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, double div, int accum, void* ws,
                    size_t ws_bytes, cudaStream_t st);
+// block mode: per-feature exponents once per data set, then per sweep the p block Grams
+// (full symmetric raw sums out[b][s][s]) of idx[b*s ..] in one slicing + one GEMM launch
+size_t gram_i8_blocks_ws_bytes(int64_t len, int s, int p);
+int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st);
+int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32_t* idx, int s, int p,
+                          const int* ex_all, double* out, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_gram_reduce_sym(const double* ws, int64_t n, int splits, double div, double* G, cudaStream_t st);
 // K3: assemble block systems, Cholesky, explicit inverse.
 struct SysArgs {

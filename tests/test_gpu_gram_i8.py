@@ -116,3 +116,30 @@ def test_covariance_fit_with_int8_gram_vs_oracle(lib, monkeypatch, ingest):
             for a_, b_ in zip(got[k], caps[k]):
                 err = np.linalg.norm(a_ - b_) / max(np.linalg.norm(b_), 1e-300)
                 assert err <= 1e-9, (m, n, s, k, err)
+
+
+@pytest.mark.parametrize("ingest", ["host", "device"])
+def test_block_mode_fit_with_int8_block_grams_vs_oracle(lib, monkeypatch, ingest):
+    """RAC_BG_I8=2 forces the per-sweep int8 block Grams (gather-slicing of the partition's
+    columns + one batched tensor-core launch) in block mode: short last block (padding),
+    s above and below one 128-feature tile, rp mode; per-sweep iterates against the oracle."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import elastic_net as en
+    from paper_1907_01995_b200.problems import Mode
+    monkeypatch.setenv("RAC_BG_I8", "2")
+    rng = np.random.default_rng(31)
+    for (m, n, s, mode) in [(400, 700, 150, "rac"), (9000, 520, 130, "rac"), (250, 300, 40, "rp")]:
+        X = rng.standard_normal((m, n))
+        y = X[:, :11] @ rng.standard_normal(11) + 0.05 * rng.standard_normal(m)
+        kw = dict(lam=0.05, alpha=0.6, gamma=1.0, block_size=s, iters=6, seed=8)
+        caps = {}
+        ro.en_fit(X, y, mode=mode, **kw,
+                  on_sweep=lambda k, bl, b, z, xi: caps.__setitem__(k, (b.copy(), z.copy(), xi.copy())))
+        got = {}
+        Xin = X if ingest == "host" else torch.from_numpy(X).cuda()
+        en.fit(Xin, y, en.ElasticNetSpec(mode=Mode(mode), **kw), gram_mode="blocks",
+               sweep_hook=lambda k, b, z, xi: got.__setitem__(k, (b, z, xi)))
+        for k in caps:
+            for a_, b_ in zip(got[k], caps[k]):
+                err = np.linalg.norm(a_ - b_) / max(np.linalg.norm(b_), 1e-300)
+                assert err <= 1e-9, (m, n, s, mode, k, err)

@@ -150,6 +150,14 @@ def traffic_table() -> dict:
 INT8_DENSE_TOPS_NOMINAL = 4500.0   # B200 dense INT8 (no measured int8 figure in MEASURED_PEAKS.json)
 
 
+def block_grams_int8(s: int, p: int, sms: int = 148) -> bool:
+    """Mirror of the context's rule (csrc/en.cu rac_en_create): block-mode Grams run on the
+    int8 tensor cores when a sweep's 128 x 128 tiles fill the SMs four times."""
+    mode = int(os.environ.get("RAC_BG_I8", "1"))
+    jt = (s + 127) // 128
+    return mode == 2 or (mode == 1 and s >= 128 and p * jt * (jt + 1) // 2 >= 4 * sms)
+
+
 def covariance_gram_timing(X, dev, reps: int = 3) -> dict:
     """G = X'X/m of the covariance mode, CUDA-event timed (average of `reps` after one
     warm-up) for the int8 digit-slice kernel (method 1: 36 int8 slice products per tile,
@@ -209,6 +217,16 @@ def en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, workload, pre
         achieved = byts / sec / 1e9
         roof = {"kernel": kern, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "algorithmic": desc}
+    elif dom == "gram" and block_grams_int8(s, p):
+        jt = (s + 127) // 128
+        ops = 2.0 * 36 * p * (jt * (jt + 1) // 2) * 128 * 128 * ((m + 31) // 32 * 32)
+        achieved = ops / sec / 1e12
+        roof = {"kernel": "i8_slice_kernel + gram_i8_kernel (tcgen05 kind::i8)", "bound": "tensor",
+                "achieved": achieved, "peak": INT8_DENSE_TOPS_NOMINAL, "unit": "TOPS (int8)",
+                "frac": achieved / INT8_DENSE_TOPS_NOMINAL,
+                "algorithmic": "36 int8 digit-slice products x 2*128*128*K per upper tile of each of the p "
+                               "blocks per sweep (exact FP64 block Grams); peak = B200 dense INT8 (nominal, "
+                               "no measured int8 figure)"}
     elif dom == "gram":
         achieved = float(m) * n * (s + 1) / sec / 1e12
         roof = {"kernel": "gram_kernel", "bound": "tensor", "achieved": achieved, "peak": fp64,

@@ -1057,6 +1057,13 @@ extern "C" int rac_en_set_data_rows(rac_en_ctx* c, const double* X_rows, int64_t
   const int64_t rows_out = last ? (c->ld - row0) : rows;
   dim3 grid((unsigned)((c->n + 31) / 32), (unsigned)((rows_out + 31) / 32));
   if (grid.y > 65535) return set_error(RAC_ERR_UNSUPPORTED, "rac_en_set_data_rows: chunk too tall");
+  static bool carve = false;
+  if (!carve) {
+    // co-reside with the int8 Gram pieces (198 KB of shared memory per CTA) on the prep stream
+    cudaFuncSetAttribute(transpose_rows_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
   transpose_rows_kernel<<<grid, dim3(32, 8), 0, c->st>>>(X_rows, rows, c->n, c->ld, row0, rows_out, c->Xc);
   note_launch();
   int rc = check_launch("transpose_rows");

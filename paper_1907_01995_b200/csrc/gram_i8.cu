@@ -353,6 +353,17 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
   }
 }
 
+// one-time: the GEMM's shared memory, and the maximal carveout for all three kernels so
+// that they co-reside with each other and with the ingest / chain kernels
+void set_i8_attributes() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM);
+  for (const void* k : {(const void*)gram_i8_kernel, (const void*)i8_slice_kernel, (const void*)i8_colexp_kernel})
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  done = true;
+}
+
 }  // namespace
 
 size_t gram_i8_ws_bytes(int64_t len, int n) {
@@ -373,17 +384,14 @@ int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, 
   uint8_t* sl = static_cast<uint8_t*>(ws);
   int* ex = reinterpret_cast<int*>(sl + I8_S * slice_bytes);
   const int nfeat = ngrp * 8;
+  set_i8_attributes();
   note_launch();
   i8_colexp_kernel<<<std::min(num_sms() * 8, (nfeat + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, nfeat, ex);
   if ((nstg + 7) / 8 > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8: too many samples");
   note_launch();
   i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8)), 256, 0, st>>>(
       Xc, ld, len, n, ex, sl, slice_bytes, ngrp, nstg, nullptr, nullptr);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM);
-    attr = true;
-  }
+  set_i8_attributes();
   I8Args a{};
   a.sl = sl;
   a.slice_bytes = slice_bytes;
@@ -408,6 +416,7 @@ size_t gram_i8_blocks_ws_bytes(int64_t len, int s, int p) {
 }
 
 int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st) {
+  set_i8_attributes();
   note_launch();
   i8_colexp_kernel<<<std::min(num_sms() * 8, (n + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, n, ex);
   return check_launch("i8 exponents");
@@ -425,14 +434,11 @@ int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32
   uint8_t* sl = static_cast<uint8_t*>(ws);
   int* ex_blk = reinterpret_cast<int*>(sl + (size_t)p * I8_S * slice_bytes);
   if ((nstg + 7) / 8 > 65535 || p > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8 blocks: shape");
+  set_i8_attributes();
   note_launch();
   i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8), (unsigned)p), 256, 0, st>>>(
       Xc, ld, len, s, ex_all, sl, slice_bytes, ngrp, nstg, idx, ex_blk);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM);
-    attr = true;
-  }
+  set_i8_attributes();
   I8Args a{};
   a.sl = sl;
   a.slice_bytes = slice_bytes;

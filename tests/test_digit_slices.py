@@ -1,0 +1,49 @@
+"""The digit-slice arithmetic of the int8 tensor-core Gram (csrc/gram_i8.cu), restated
+in numpy: exact balanced 7-bit digits, and the truncated slice-product sum reproducing
+x_j x_k to the FP64 rounding level.  Documents the kernel's numerics without a GPU."""
+import numpy as np
+
+
+def digits(x, e, S=8):
+    """x * 2^(6-e) = sum_s d_s 2^(-7(s-1)) + rest, d = rint(r), r <- (r - d) * 128."""
+    r = np.ldexp(x, 6 - e)
+    out = []
+    for _ in range(S):
+        d = np.rint(r)
+        r = (r - d) * 128.0
+        out.append(d)
+    return np.array(out), r
+
+
+def test_digits_are_exact_and_balanced():
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal(10000) * 10.0 ** rng.uniform(-20, 20, 10000)
+    _, e = np.frexp(np.abs(x).max())
+    d, rest = digits(x, e)
+    assert np.all(np.abs(d) <= 64)
+    assert np.all(np.abs(rest) <= 64.0)           # the final r = (r - d) * 128 with |r - d| <= 1/2
+    # exact reconstruction in integer arithmetic (Python ints): the digits plus the rest
+    scale = [2 ** (7 * (8 - s)) for s in range(1, 9)]     # digit s weight, in units of 2^-49
+    for i in range(0, 10000, 997):
+        acc = sum(int(d[s, i]) * scale[s] for s in range(8))
+        v = np.ldexp(x[i], 6 - e + 49)                       # exact power-of-two scaling
+        assert abs(v - acc) <= 0.5 + 1e-12               # the rest is below half a unit of 2^-49
+
+
+def test_truncated_slice_products_match_the_product():
+    """sum over s + t <= 9 of d_s d_t 2^(-7(s+t-2)), scaled back, vs x_j x_k."""
+    rng = np.random.default_rng(1)
+    xj, xk = rng.standard_normal(5000), rng.standard_normal(5000)
+    _, ej = np.frexp(np.abs(xj).max())
+    _, ek = np.frexp(np.abs(xk).max())
+    dj, _ = digits(xj, ej)
+    dk, _ = digits(xk, ek)
+    total = 0.0
+    for w in range(9, 1, -1):                            # smallest weight first, as the kernel
+        cw = sum(int(np.dot(dj[s - 1].astype(np.int64), dk[w - s - 1].astype(np.int64))) for s in range(1, w))
+        assert abs(cw) < 2 ** 31                          # one int32 accumulator per group
+        total += np.ldexp(float(cw), -7 * (w - 2))
+    g = np.ldexp(total, ej + ek - 12)
+    exact = float(np.dot(xj.astype(np.longdouble), xk.astype(np.longdouble)))
+    bound = 2.0 ** -52 * np.linalg.norm(xj) * np.linalg.norm(xk)
+    assert abs(g - exact) <= bound

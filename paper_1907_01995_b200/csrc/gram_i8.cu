@@ -6,9 +6,9 @@
 // the G = X'X/m restatement in DESIGN.md §4).
 //
 // Digit slicing (Ozaki scheme): every feature column j gets the power-of-two scale
-// 2^{e_j} > max_i |x_ij|, and x·2^{6-e_j} is split EXACTLY into S balanced digits
-//     x·2^{6-e_j} = d_1 + d_2 2^-7 + ... + d_S 2^{-7(S-1)} + rest,  d_s in [-64, 64]
-// (d = rint(r), r <- (r - d)·128: every step is exact in FP64).  Then
+// 2^{e_j} > max_i |x_ij|, and x·2^{6-e_j} is split into S balanced digits
+//     x·2^{6-e_j} = d_1 + d_2 2^-7 + ... + d_S 2^{-7(S-1)} + rest,  d_s in [-64, 64], |rest| <= 2^-50
+// (N = rint(x·2^{55-e_j}) once, then N's balanced base-128 digits in integer arithmetic).  Then
 //     G_jk = 2^{e_j+e_k-12} Σ_{w=2..S+1} 2^{-7(w-2)} C_w[j,k],
 //     C_w = Σ_{s+t=w} D_s' D_t      (int8 GEMMs, exact int32 sums)
 // The dropped products (s+t > S+1) and the rest terms are below 2^-52.8 of
@@ -161,13 +161,17 @@ __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict_
   for (int s = 0; s < I8_S; ++s) packed[s] = 0ull;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    double r = ldexp(x[i], 6 - e);   // |r| < 64, exact
+    // x 2^(55-e) (exact, |.| < 2^55) rounded once to an integer N, then N's balanced
+    // base-128 digits from the bottom: d = ((N + 64) mod 128) - 64, N <- (N - d) / 128
+    // (exact shifts); the top digit is what remains, |d_1| <= 64
+    long long N = __double2ll_rn(ldexp(x[i], 55 - e));
 #pragma unroll
-    for (int s = 0; s < I8_S; ++s) {
-      const double d = rint(r);      // |d| <= 64
-      r = (r - d) * 128.0;           // exact: |r - d| <= 1/2
-      packed[s] |= (unsigned long long)(uint8_t)(int8_t)(int)d << (8 * i);
+    for (int s = I8_S - 1; s > 0; --s) {
+      const long long d = ((N + 64) & 127) - 64;
+      N = (N - d) >> 7;
+      packed[s] |= (unsigned long long)(uint8_t)(int8_t)d << (8 * i);
     }
+    packed[0] |= (unsigned long long)(uint8_t)(int8_t)N << (8 * i);
   }
   // sample k0 + i -> stage lane / 4, chunk (lane % 4) / 2, byte (lane % 2) * 8 + i
   const int off = (lane >> 2) * 256 + ((lane & 3) >> 1) * 128 + f * 16 + (lane & 1) * 8;

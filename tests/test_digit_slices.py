@@ -5,14 +5,18 @@ import numpy as np
 
 
 def digits(x, e, S=8):
-    """x * 2^(6-e) = sum_s d_s 2^(-7(s-1)) + rest, d = rint(r), r <- (r - d) * 128."""
-    r = np.ldexp(x, 6 - e)
-    out = []
-    for _ in range(S):
-        d = np.rint(r)
-        r = (r - d) * 128.0
-        out.append(d)
-    return np.array(out), r
+    """As i8_slice_kernel: N = rint(x 2^(55-e)) (|N| <= 2^55), then N's balanced base-128
+    digits from the bottom, d = ((N + 64) mod 128) - 64, N <- (N - d) / 128; the top digit
+    is what remains.  x 2^(6-e) = sum_s d_s 2^(-7(s-1)) + rest, |rest| <= 2^-50."""
+    N = np.rint(np.ldexp(x, 55 - e)).astype(np.int64)
+    out = [None] * S
+    for s in range(S - 1, 0, -1):
+        d = ((N + 64) & 127) - 64
+        N = (N - d) >> 7
+        out[s] = d
+    out[0] = N
+    rest = np.ldexp(x, 55 - e) - np.rint(np.ldexp(x, 55 - e))
+    return np.array(out).astype(np.float64), rest
 
 
 def test_digits_are_exact_and_balanced():
@@ -21,7 +25,7 @@ def test_digits_are_exact_and_balanced():
     _, e = np.frexp(np.abs(x).max())
     d, rest = digits(x, e)
     assert np.all(np.abs(d) <= 64)
-    assert np.all(np.abs(rest) <= 64.0)           # the final r = (r - d) * 128 with |r - d| <= 1/2
+    assert np.all(np.abs(rest) <= 0.5)            # rounding x 2^(55-e) to an integer
     # exact reconstruction in integer arithmetic (Python ints): the digits plus the rest
     scale = [2 ** (7 * (8 - s)) for s in range(1, 9)]     # digit s weight, in units of 2^-49
     for i in range(0, 10000, 997):

@@ -1188,10 +1188,29 @@ extern "C" int rac_svm_build_q(const double* X, int64_t N, int64_t d, const doub
   cudaMemcpy2DAsync(Xp, ldd * sizeof(double), X, d * sizeof(double), d * sizeof(double), N,
                     cudaMemcpyDeviceToDevice, st);
   iota_kernel<<<(int)std::min<int64_t>((N + 255) / 256, 4096), 256, 0, st>>>(ids, N);
-  GramPlan pl = plan_gram(d, (int)N, 1);
-  pl.splits = 1;
-  pl.chunk = ldd;
-  rc = launch_gram(Xp, ldd, d, ids, nullptr, (int)N, 1, Q, pl, st, nullptr, 1.0);   // full symmetric X X'
+  // full symmetric X X': on the int8 tensor cores (exact digit slices, gram_i8.cu) when its
+  // 128 x 128 tiles fill the SMs (RAC_Q_I8=2 forces it, =0 keeps the FP64 DMMA tiles)
+  const char* e8 = getenv("RAC_Q_I8");
+  const int mode8 = e8 ? atoi(e8) : 1;
+  const int64_t jt = (N + 127) / 128;
+  void* ws8 = nullptr;
+  size_t ws8b = 0;
+  if (mode8 == 2 || (mode8 == 1 && jt * (jt + 1) / 2 >= num_sms())) {
+    ws8b = gram_i8_ws_bytes(ldd, (int)N);
+    if (cudaMallocAsync(&ws8, ws8b, st) != cudaSuccess) {
+      cudaGetLastError();
+      ws8 = nullptr;
+    }
+  }
+  if (ws8) {
+    rc = launch_gram_i8(Xp, ldd, d, (int)N, Q, 1.0, 0, ws8, ws8b, st);
+    cudaFreeAsync(ws8, st);
+  } else {
+    GramPlan pl = plan_gram(d, (int)N, 1);
+    pl.splits = 1;
+    pl.chunk = ldd;
+    rc = launch_gram(Xp, ldd, d, ids, nullptr, (int)N, 1, Q, pl, st, nullptr, 1.0);
+  }
   if (rc) return rc;
   diag_copy_kernel<<<(int)std::min<int64_t>((N + 255) / 256, 4096), 256, 0, st>>>(Q, N, sq);
   {

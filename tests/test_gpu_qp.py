@@ -174,3 +174,24 @@ def test_build_q_matches_kernel_rows(dev):
         want = (y[:, None] * ro.kernel_matrix(X, X, kernel.kind, kernel.sigma)) * y[None, :]
         assert np.max(np.abs(Q - want)) <= 1e-13 * max(1.0, np.max(np.abs(want)))
         assert np.array_equal(Q, Q.T)
+
+
+def test_build_q_int8_tensor_cores(dev, monkeypatch):
+    """RAC_Q_I8=2 forces Q = Y X X' Y onto the int8 digit-slice tensor-core Gram (the default
+    once its tiles fill the SMs): ragged N and d, both kernels, against the oracle's kernel
+    matrix; then a train on it matches the DMMA-built one to the parity bar."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import svm
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((333, 37))
+    y = np.where(rng.random(333) < 0.5, 1.0, -1.0)
+    for kernel in (svm.KernelSpec("linear"), svm.KernelSpec("gaussian", 1.1)):
+        monkeypatch.setenv("RAC_Q_I8", "2")
+        Q8 = svm.build_q(X, y, kernel).cpu().numpy()
+        monkeypatch.setenv("RAC_Q_I8", "0")
+        Q0 = svm.build_q(X, y, kernel).cpu().numpy()
+        want = (y[:, None] * ro.kernel_matrix(X, X, kernel.kind, kernel.sigma)) * y[None, :]
+        scale = max(1.0, np.max(np.abs(want)))
+        assert np.max(np.abs(Q8 - want)) <= 1e-13 * scale
+        assert np.max(np.abs(Q8 - Q0)) <= 1e-13 * scale
+        assert np.array_equal(Q8, Q8.T)

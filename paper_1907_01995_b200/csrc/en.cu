@@ -1189,6 +1189,7 @@ extern "C" int rac_en_set_gram_mode(rac_en_ctx* c, int32_t mode) {
       // on the SMs the chain leaves free
       const int free_sms = std::max(0, num_sms() - (c->cla_L + c->cla_W));
       c->cla_B = std::max(1, std::min(CLA_BMAX, free_sms / std::max(1, c->p)));
+      if (const char* eb = getenv("RAC_CLA_B")) c->cla_B = std::max(1, std::min(CLA_BMAX, atoi(eb)));
       // the factor's global scratch (Cholesky re-check / large-s path) must cover the batch
       const size_t scr = chol_scratch_bytes(c->s, c->p * c->cla_B);
       if (c->cla_B > 1 && scr > chol_scratch_bytes(c->s, c->p)) {

@@ -448,10 +448,13 @@ def run_b200_en(args, world, rank, local):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         done = 0
+        perms = feeder.draw(min(16, case.iters))
         while done < case.iters:
             k = min(16, case.iters - done)   # fit()'s default batch: one progress check per 16 sweeps
-            sol2.run(feeder.draw(k), case.tol)
+            sol2.run(perms, case.tol)
             done += k
+            # as fit(): the next batch is drawn while the device runs this one
+            perms = feeder.draw(min(16, case.iters - done)) if done < case.iters else None
             it, conv, res, _ = sol2.progress()
             if conv:
                 break

@@ -356,10 +356,14 @@ def fit(X: Matrix, y: np.ndarray, spec: ElasticNetSpec, *, sweep_hook=None,
         step = 1 if sweep_hook is not None else max(1, int(batch))
         done = 0
         iterations, converged, failed = 0, False, -1
+        perms = feeder.draw(min(step, spec.iters)) if spec.iters > 0 else None
         while done < spec.iters:
             k = min(step, spec.iters - done)
-            solver.run(feeder.draw(k), spec.tol)
+            solver.run(perms, spec.tol)
             done += k
+            # the next batch's permutations are drawn (host PCG64, same stream order) while
+            # the device runs this one; a batch drawn past convergence is simply dropped
+            perms = feeder.draw(min(step, spec.iters - done)) if done < spec.iters else None
             if sweep_hook is not None or spec.tol is not None or done >= spec.iters:
                 iterations, converged, _, failed = solver.progress()
                 if failed >= 0:

@@ -117,10 +117,17 @@ def drive(solver: QpSolver, rng: np.random.Generator, max_iters: int, tol_p: flo
     step = 1 if hook is not None else max(1, batch)
     done = 0
     it, status, failed = 0, Status.MAX_ITERS, -1
+    def draw(count):
+        return feeder.draw(count) if feeder is not None and count > 0 else None
+
+    perms = draw(min(step, max_iters))
     while done < max_iters:
         k = min(step, max_iters - done)
-        solver.run(feeder.draw(k) if feeder is not None else None, k, tol_p, tol_d, fixed)
+        solver.run(perms, k, tol_p, tol_d, fixed)
         done += k
+        # the next batch's permutations are drawn while the device runs this one (same
+        # PCG64 order; a batch drawn past the stop is dropped)
+        perms = draw(min(step, max_iters - done))
         it, status, failed = solver.progress()
         if failed >= 0:
             raise BlockDefinitenessError(NOT_PD_MESSAGE)

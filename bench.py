@@ -447,17 +447,21 @@ def run_b200_en(args, world, rank, local):
         feeder = _device.PermutationFeeder(rng2, n, dev)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        done = 0
-        perms = feeder.draw(min(16, case.iters))
-        while done < case.iters:
-            k = min(16, case.iters - done)   # fit()'s default batch: one progress check per 16 sweeps
-            sol2.run(perms, case.tol)
-            done += k
-            # as fit(): the next batch is drawn while the device runs this one
-            perms = feeder.draw(min(16, case.iters - done)) if done < case.iters else None
-            it, conv, res, _ = sol2.progress()
-            if conv:
+        # as fit() with a tolerance: batches of 16 sweeps, batch k+1 enqueued before batch
+        # k's status is polled; the final progress() reports the converged sweep
+        sol2.run(feeder.draw(min(16, case.iters)), case.tol)
+        done = min(16, case.iters)
+        while True:
+            lag = 0
+            if done < case.iters:
+                k = min(16, case.iters - done)
+                sol2.run(feeder.draw(k), case.tol)
+                done += k
+                lag = 1
+            _, conv, failed = sol2.poll(lag)
+            if failed >= 0 or conv or lag == 0:
                 break
+        it, conv, res, _ = sol2.progress()
         t_tol = time.perf_counter() - t0
         ttt = {"seconds": t_tol, "sweeps": it, "residual": res, "converged": bool(conv),
                "tol": case.tol}

@@ -118,6 +118,13 @@ int rac_en_set_partition(rac_en_ctx* ctx, const int64_t* perm);
  * permutations of p (block visit orders, elastic_net.py:197-198).  tol < 0
  * means fixed sweeps (spec.tol None).  Sweeps after convergence are no-ops. */
 int rac_en_run(rac_en_ctx* ctx, const int64_t* perms, int32_t count, double tol);
+/* Non-blocking status (no reference counterpart): the control word as it stood after
+ * the latest run (lag 0) or the one before it (lag 1), waiting only for that run's work —
+ * lets a driver enqueue the next batch of sweeps before reading the previous batch's
+ * status (launches after convergence or a non-PD block are no-ops on the device).
+ * Fields as in rac_en_progress. */
+int rac_en_poll(rac_en_ctx* ctx, int32_t lag, int32_t* iterations_host, int32_t* converged_host,
+                int32_t* failed_block_host);
 /* Synchronizes the stream.  iterations = sweeps executed so far. */
 int rac_en_progress(rac_en_ctx* ctx, int32_t* iterations_host, int32_t* converged_host,
                     double* residual_host, int32_t* failed_block_host);

@@ -43,6 +43,7 @@ SIGNATURES = {
     "rac_en_set_partition": (_i32, [_p, _p]),
     "rac_en_run": (_i32, [_p, _p, _i32, _f64]),
     "rac_en_progress": (_i32, [_p, _pi32, _pi32, _pf64, _pi32]),
+    "rac_en_poll": (_i32, [_p, _i32, _pi32, _pi32, _pi32]),
     "rac_en_get": (_i32, [_p, _p, _p, _p, _p]),
     "rac_en_history": (_i32, [_p, _p, _p, _i32]),
     "rac_en_set_timing": (_i32, [_p, _i32]),

@@ -325,6 +325,9 @@ struct rac_en_ctx {
   void* bg_ws = nullptr;      // block mode: per-sweep digit slices of the int8 block Grams, null = DMMA
   size_t bg_cap = 0;
   int* ex_all = nullptr;      // block mode: per-feature exponents of Xc (set with the data)
+  int32_t* h_ctrl = nullptr;  // pinned: ctrl snapshot after each run (2 slots), for rac_en_poll
+  cudaEvent_t ev_ctrl[2] = {nullptr, nullptr};
+  int64_t ctrl_n = 0;         // runs snapshotted
   // lookahead covariance chain (en_cla.cuh); cla_L = leader cluster size, 0 = not used
   int cla_L = 0, cla_D = 3, cla_W = 0, cla_segw = 1, cla_R = 2, cla_NS = 2;
   size_t cla_smem = 0;
@@ -1008,6 +1011,12 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
     rac_en_destroy(c);
     return rc;
   }
+  if (cudaHostAlloc((void**)&c->h_ctrl, 8 * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_ctrl[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_ctrl[1], cudaEventDisableTiming) != cudaSuccess) {
+    rac_en_destroy(c);
+    return set_error(RAC_ERR_CUDA, "rac_en_create: pinned control snapshot");
+  }
   *out = c;
   return RAC_OK;
 }
@@ -1240,7 +1249,37 @@ extern "C" int rac_en_set_partition(rac_en_ctx* c, const int64_t* perm) {
   return RAC_OK;
 }
 
+static int en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, double tol);
+
 extern "C" int rac_en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, double tol) {
+  const int rc = en_run(c, perms, count, tol);
+  if (rc == RAC_OK && c->h_ctrl) {
+    // snapshot of the control word once this run's work is done (rac_en_poll)
+    const int slot = (int)(c->ctrl_n & 1);
+    cudaMemcpyAsync(c->h_ctrl + 4 * slot, c->ctrl, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->st);
+    cudaEventRecord(c->ev_ctrl[slot], c->st);
+    c->ctrl_n++;
+  }
+  return rc;
+}
+
+extern "C" int rac_en_poll(rac_en_ctx* c, int32_t lag, int32_t* iterations, int32_t* converged,
+                           int32_t* failed_block) {
+  using namespace rac;
+  clear_error();
+  if (!c || lag < 0 || lag > 1 || c->ctrl_n - 1 - lag < 0)
+    return set_error(RAC_ERR_ARG, "rac_en_poll: no such run");
+  const int slot = (int)((c->ctrl_n - 1 - lag) & 1);
+  int rc = check_cuda(cudaEventSynchronize(c->ev_ctrl[slot]), "poll");
+  if (rc) return rc;
+  const int32_t* h = c->h_ctrl + 4 * slot;
+  if (iterations) *iterations = h[1];
+  if (converged) *converged = h[3];
+  if (failed_block) *failed_block = h[2] - 1;
+  return RAC_OK;
+}
+
+static int en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, double tol) {
   using namespace rac;
   clear_error();
   if (!c || (!perms && count > 0) || count < 0) return set_error(RAC_ERR_ARG, "rac_en_run: bad arguments");
@@ -1484,8 +1523,10 @@ extern "C" int rac_en_destroy(rac_en_ctx* c) {
   if (c->schain) cudaStreamSynchronize(c->schain);
   if (c->sprep) cudaStreamSynchronize(c->sprep);
   for (auto e : c->events) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ev_start, c->ev_end, c->ev_prep[0], c->ev_prep[1], c->ev_chain[0], c->ev_chain[1]})
+  for (cudaEvent_t e : {c->ev_start, c->ev_end, c->ev_prep[0], c->ev_prep[1], c->ev_chain[0], c->ev_chain[1],
+                        c->ev_ctrl[0], c->ev_ctrl[1]})
     if (e) cudaEventDestroy(e);
+  if (c->h_ctrl) cudaFreeHost(c->h_ctrl);
   if (c->schain) cudaStreamDestroy(c->schain);
   if (c->sprep) cudaStreamDestroy(c->sprep);
   for (void* q : c->allocs) rac::dev_free(q, c->st);

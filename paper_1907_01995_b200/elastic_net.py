@@ -247,6 +247,13 @@ class EnSolver:
         _native.check(self.lib.rac_en_progress(self.h, it, conv, res, fb))
         return it.value, bool(conv.value), res.value, fb.value
 
+    def poll(self, lag: int = 1):
+        """(iterations, converged, failed_block) after the run `lag` runs before the latest,
+        waiting only for that run (rac_en_poll)."""
+        it, conv, fb = _native._i32(), _native._i32(), _native._i32()
+        _native.check(self.lib.rac_en_poll(self.h, int(lag), it, conv, fb))
+        return it.value, bool(conv.value), fb.value
+
     def state(self):
         b = torch.empty(self.n, dtype=torch.float64, device=self.dev)
         z, xi = torch.empty_like(b), torch.empty_like(b)
@@ -356,7 +363,24 @@ def fit(X: Matrix, y: np.ndarray, spec: ElasticNetSpec, *, sweep_hook=None,
         step = 1 if sweep_hook is not None else max(1, int(batch))
         done = 0
         iterations, converged, failed = 0, False, -1
-        perms = feeder.draw(min(step, spec.iters)) if spec.iters > 0 else None
+        if sweep_hook is None and spec.tol is not None and spec.iters > 0:
+            # with a tolerance: batch k+1 is enqueued before batch k's status is read (a
+            # non-blocking poll of the run before the latest), so no host round trip
+            # separates the batches; launches after convergence are no-ops on the device
+            solver.run(feeder.draw(min(step, spec.iters)), spec.tol)
+            done = min(step, spec.iters)
+            while True:
+                lag = 0
+                if done < spec.iters:
+                    k = min(step, spec.iters - done)
+                    solver.run(feeder.draw(k), spec.tol)
+                    done += k
+                    lag = 1
+                _, conv, failed = solver.poll(lag)
+                if failed >= 0 or conv or lag == 0:
+                    break
+            done = spec.iters          # the final progress() below reports the true state
+        perms = feeder.draw(min(step, spec.iters)) if done < spec.iters else None
         while done < spec.iters:
             k = min(step, spec.iters - done)
             solver.run(perms, spec.tol)

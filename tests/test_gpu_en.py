@@ -388,3 +388,25 @@ def test_streaming_chain_one_tile_vs_oracle(lib, monkeypatch, one_tile):
         for k in caps:
             for a_, b_ in zip(got[k], caps[k]):
                 assert rel(a_, b_) <= ITER_TOL, (m, n, s, k)
+
+
+@pytest.mark.parametrize("gram", ["covariance", "blocks"])
+def test_fit_enqueue_ahead_stops_where_the_synchronous_loop_does(lib, gram):
+    """fit() with a tolerance enqueues batch k+1 before polling batch k (rac_en_poll); the
+    speculative batch after convergence must be a no-op: same iterations, residual and
+    iterates as the per-sweep synchronous loop (sweep_hook path) and as the oracle."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import elastic_net as en
+    rng = np.random.default_rng(12)
+    m, n, s = 600, 240, 24
+    X = rng.standard_normal((m, n))
+    y = X[:, :6] @ rng.standard_normal(6) + 0.01 * rng.standard_normal(m)
+    spec = en.ElasticNetSpec(lam=0.05, alpha=0.9, gamma=1.0, block_size=s, iters=500, seed=5, tol=1e-6)
+    fast = en.fit(X, y, spec, gram_mode=gram, batch=16)
+    slow = en.fit(X, y, spec, gram_mode=gram, sweep_hook=lambda *a: None)
+    ref = ro.en_fit(X, y, mode="rac", lam=0.05, alpha=0.9, gamma=1.0, block_size=s, iters=500, seed=5, tol=1e-6)
+    assert fast.iterations == slow.iterations == ref["iterations"] < 500
+    # one sweep per launch (hook) vs batched launches: equal to rounding
+    assert rel(fast.beta, slow.beta) <= 1e-12 and rel(fast.xi, slow.xi) <= 1e-12
+    assert abs(fast.residual - slow.residual) <= 1e-9 * max(slow.residual, 1e-300)
+    assert rel(fast.beta, ref["beta"]) <= ITER_TOL

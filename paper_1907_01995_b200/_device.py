@@ -6,6 +6,7 @@ the sweep runs in the native sm_100a kernels (_native.py).
 
 from __future__ import annotations
 
+import os
 import threading
 
 import numpy as np
@@ -70,30 +71,33 @@ ROW_CHUNK_BYTES = 16 << 20
 
 
 class _RowStreamer:
-    """Two pinned host buffers, two device buffers, one copy stream: row chunk
-    k+1 is copied (host memcpy into pinned memory, then DMA) while the
-    consumer's kernels for chunk k run on the current stream."""
+    """A ring of `nbuf` pinned host buffers and device buffers (4 by default,
+    RAC_STAGE_BUFS), one copy stream: later row chunks are copied (host memcpy
+    into pinned memory, then DMA) while the consumer's kernels for chunk k run on
+    the current stream.  Four buffers keep the DMA engine busy: 54 GB/s against
+    48 GB/s with two (scripts/micro/ingest_probe.py)."""
 
-    def __init__(self, device):
+    def __init__(self, device, nbuf: int = 2):
         self.device = device
         self.copy_stream = torch.cuda.Stream(device=device)
-        self.host = [None, None]
-        self.dev = [None, None]
-        self.copied = [None, None]
-        self.consumed = [None, None]
+        self.nbuf = nbuf
+        self.host = [None] * nbuf
+        self.dev = [None] * nbuf
+        self.copied = [None] * nbuf
+        self.consumed = [None] * nbuf
 
     def run(self, X: np.ndarray, align: int, consume) -> None:
         m, n = X.shape
         rows_per = max(align, (ROW_CHUNK_BYTES // (8 * n)) // align * align)
         need = rows_per * n
-        for k in range(2):
+        for k in range(self.nbuf):
             if self.host[k] is None or self.host[k].numel() < need:
                 self.host[k] = torch.empty(need, dtype=torch.float64).pin_memory()
                 self.dev[k] = torch.empty(need, dtype=torch.float64, device=self.device)
         main = torch.cuda.current_stream(self.device)
         src = torch.from_numpy(X)
         for i, r0 in enumerate(range(0, m, rows_per)):
-            k = i & 1
+            k = i % self.nbuf
             rows = min(rows_per, m - r0)
             if self.copied[k] is not None:
                 self.copied[k].synchronize()            # pinned buffer k is free again
@@ -121,7 +125,7 @@ def stream_rows(X: np.ndarray, align: int, consume, device=None) -> None:
     dev = torch.device(device or "cuda")
     key = dev.index if dev.index is not None else torch.cuda.current_device()
     if key not in _streamers:
-        _streamers[key] = _RowStreamer(dev)
+        _streamers[key] = _RowStreamer(dev, int(os.environ.get("RAC_STAGE_BUFS", "4")))
     _streamers[key].run(np.ascontiguousarray(X, dtype=np.float64), align, consume)
 
 

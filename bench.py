@@ -1,13 +1,20 @@
-"""Benchmark: RAC-ADMM sweeps/sec (and time to 1e-6) on one B200, vs the CPU reference path.
+"""Benchmark: RAC-ADMM sweeps/sec and time to 1e-6 on one B200, beside the CPU reference path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config C]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config C] [--only]
 
-A "step" is one RAC sweep (one pass of the Gauss-Seidel chain over all p
-blocks, including that sweep's block assembly, block Grams and factorizations).
-The headline workload is BASELINE.json configs[1] (LASSO, D 10000x2000, s=100);
-`--config` selects another BASELINE config.  Multi-GPU: the sweep is a
-sequential Gauss-Seidel chain, so N>1 runs N independent replicas (one per GPU,
-`scaling: weak`) — see DESIGN.md "Multi-GPU".
+A "step" is one RAC sweep: one pass of the Gauss-Seidel chain over all p blocks,
+including that sweep's block assembly, block Grams and factorizations.
+
+The headline workload is BASELINE.json's largest single-GPU configuration, config 5
+(HD-LASSO, D 5000 x 100000, s = 500; BASELINE's metric names no config).  The same
+JSON line carries a `configs` object with every BASELINE config (1-5): device
+sweeps/s, end-to-end sweeps/s through the public API, time to tolerance (device and
+end to end), the roofline of its dominant kernel and the CPU port beside it.
+`--only` skips the other configs.
+
+Multi-GPU: the sweep is a sequential Gauss-Seidel chain, so N > 1 runs N independent
+replicas (one per GPU, `scaling: weak`, max-over-ranks device time).  Without
+torchrun, `--gpus N` re-launches itself under torch.distributed.run with N ranks.
 """
 
 from __future__ import annotations
@@ -17,6 +24,7 @@ import glob
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -28,7 +36,11 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+HEADLINE = 5
 HBM_FALLBACK_GBS = 6650.0
+INT8_DENSE_TOPS_NOMINAL = 4500.0
+METRIC = "rac_admm_sweeps_per_sec"
+DATA = "synthetic (SURVEY.md §8(d) seed-0 recipe; BASELINE names no dataset)"
 
 
 def measured_peaks():
@@ -93,13 +105,26 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ distributed
-def dist_setup(args):
+def free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`--gpus N` without torchrun: run this script as N ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd, cwd=ROOT)
+
+
+def dist_setup(backend: str):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        backend = "gloo" if args.impl == "reference" else "nccl"
         if backend == "nccl":
             import torch
             torch.cuda.set_device(local)
@@ -124,21 +149,34 @@ def dist_barrier(world: int):
 
 
 # ------------------------------------------------------------------ workloads
-def en_case(cfg: int):
+def make_case(cfg: int):
     from paper_1907_01995_b200 import configs
     return configs.GENERATORS[cfg]()
 
 
-def en_flops_bytes(m, n, s):
-    """Algorithmic work per sweep: Gram m*n*(s+1) flop, D read 8*m*n bytes."""
-    return float(m) * n * (s + 1), 8.0 * m * n
+def config_dict(cfg: int, case, steps: int, world: int) -> dict:
+    """The `config` object of a line (identical in both arms, so the driver can pair them)."""
+    if cfg == 4:
+        N, d = case.X.shape
+        s = case.block_size
+        return {"workload": case.name, "N": N, "d": d, "block_size": s, "blocks": -(-N // s), "mode": "rac",
+                "l2": "inputs larger than L2 (Q = %.1f GB)" % (8 * N * N / 1e9),
+                "parallelism": f"replicas x{world}"}
+    from paper_1907_01995_b200 import elastic_net as en
+    m, n = case.X.shape
+    s = min(case.block_size, n)
+    return {"workload": case.name, "m": m, "n": n, "block_size": s, "blocks": -(-n // s), "mode": "rac",
+            "gram_mode": en.choose_gram_mode(m, n, s, steps),
+            "l2": ("inputs larger than L2 (D = %.0f MB)" % (8 * m * n / 1e6)) if 8 * m * n > 126e6
+            else "D fits in L2 (no flush)",
+            "parallelism": f"replicas x{world}"}
 
 
 def traffic_table() -> dict:
-    """DRAM bytes per launch from the committed ncu --set full captures (profiles/*traffic*.json)."""
+    """DRAM bytes per launch from committed ncu --set full captures (profiles/*traffic*.json),
+    keyed "<workload>:<kernel>"."""
     out = {}
-    for path in sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                              "*traffic*.json"))):
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*traffic*.json"))):
         try:
             with open(path) as f:
                 out.update(json.load(f))
@@ -147,99 +185,12 @@ def traffic_table() -> dict:
     return out
 
 
-INT8_DENSE_TOPS_NOMINAL = 4500.0   # B200 dense INT8 (no measured int8 figure in MEASURED_PEAKS.json)
-
-
 def block_grams_int8(s: int, p: int, sms: int = 148) -> bool:
     """Mirror of the context's rule (csrc/en.cu rac_en_create): block-mode Grams run on the
     int8 tensor cores when a sweep's 128 x 128 tiles fill the SMs four times."""
     mode = int(os.environ.get("RAC_BG_I8", "1"))
     jt = (s + 127) // 128
     return mode == 2 or (mode == 1 and s >= 128 and p * jt * (jt + 1) // 2 >= 4 * sms)
-
-
-def covariance_gram_timing(X, dev, reps: int = 3) -> dict:
-    """G = X'X/m of the covariance mode, CUDA-event timed (average of `reps` after one
-    warm-up) for the int8 digit-slice kernel (method 1: 36 int8 slice products per tile,
-    csrc/gram_i8.cu) and the FP64 DMMA tiles (method 0)."""
-    import ctypes as C
-
-    import torch
-    from paper_1907_01995_b200 import _native
-    lib = _native.load()
-    m, n = X.shape
-    Xc = torch.from_numpy(np.ascontiguousarray(X.T)).to(dev)
-    G = torch.empty((n, n), dtype=torch.float64, device=dev)
-    out = {}
-    for meth, name in ((1, "int8_slices"), (0, "fp64_dmma")):
-        call = lambda: _native.check(lib.rac_gram_covariance(C.c_void_p(Xc.data_ptr()), m, m, n,
-                                                              C.c_void_p(G.data_ptr()), float(m), meth))
-        call()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
-            call()
-        e1.record()
-        torch.cuda.synchronize()
-        out[name + "_ms"] = e0.elapsed_time(e1) / reps
-    jt = (n + 127) // 128
-    kpad = (m + 31) // 32 * 32
-    ops = 2.0 * 36 * (jt * (jt + 1) // 2) * 128 * 128 * kpad      # int8 ops issued (full 128x128 tiles)
-    tops = ops / (out["int8_slices_ms"] * 1e-3) / 1e12
-    out.update({"int8_tops": tops, "int8_peak_tops": INT8_DENSE_TOPS_NOMINAL,
-                "int8_frac": tops / INT8_DENSE_TOPS_NOMINAL,
-                "algorithmic": "36 int8 slice products x 2*128*128*K per upper-triangle tile (incl. slicing "
-                               "and exponent passes in the time)"})
-    del Xc, G
-    return out
-
-
-def en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, workload, prep_batch=1) -> dict:
-    """Roofline entry for the dominant stage of an EN sweep (per-unit figures: SURVEY.md §8(d)).
-
-    `stages` are per-sweep times measured serially; in the pipelined run the
-    block systems of `prep_batch` sweeps are prepared by one launch that overlaps
-    the chain, so the stage that bounds a sweep is picked on factor / prep_batch."""
-    eff = dict(stages)
-    eff["factor"] = stages.get("factor", 0.0) / max(1, prep_batch)
-    dom = max(eff, key=eff.get)
-    sec = stages[dom] * 1e-3
-    if dom == "chain":
-        if gram_mode == "covariance":
-            kern = "en_cla_kernel" if variant == "covariance-lookahead" else "en_cov_kernel"
-            byts = 8.0 * n * n + 8.0 * p * s * s
-            desc = "rows of G read once (8 n^2) + block inverses (8 p s^2) per launch"
-        else:
-            kern = "en_chain_res_kernel" if variant == "resident-cluster" else "en_chain_kernel"
-            byts = 8.0 * m * n + 8.0 * p * s * s
-            desc = "D read once (8 m n; a block's second use hits L2) + block inverses (8 p s^2) per launch"
-        achieved = byts / sec / 1e9
-        roof = {"kernel": kern, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "algorithmic": desc}
-    elif dom == "gram" and block_grams_int8(s, p):
-        jt = (s + 127) // 128
-        ops = 2.0 * 36 * p * (jt * (jt + 1) // 2) * 128 * 128 * ((m + 31) // 32 * 32)
-        achieved = ops / sec / 1e12
-        roof = {"kernel": "i8_slice_kernel + gram_i8_kernel (tcgen05 kind::i8)", "bound": "tensor",
-                "achieved": achieved, "peak": INT8_DENSE_TOPS_NOMINAL, "unit": "TOPS (int8)",
-                "frac": achieved / INT8_DENSE_TOPS_NOMINAL,
-                "algorithmic": "36 int8 digit-slice products x 2*128*128*K per upper tile of each of the p "
-                               "blocks per sweep (exact FP64 block Grams); peak = B200 dense INT8 (nominal, "
-                               "no measured int8 figure)"}
-    elif dom == "gram":
-        achieved = float(m) * n * (s + 1) / sec / 1e12
-        roof = {"kernel": "gram_kernel", "bound": "tensor", "achieved": achieved, "peak": fp64,
-                "unit": "TFLOP/s", "frac": achieved / fp64,
-                "algorithmic": "m*n*(s+1) flop per launch (symmetric SYRK of all p blocks)"}
-    else:
-        achieved = 2.0 * p * float(s) ** 3 / sec / 1e12
-        roof = {"kernel": "factor_kernel" if s <= 236 else "large_*_kernel (blocked inverse)",
-                "bound": "tensor", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
-                "frac": achieved / fp64, "algorithmic": "2 s^3 flop per block inverse x p blocks per sweep"}
-    roof["stage"] = dom
-    roof["traffic"] = traffic_table().get(f"{workload}:{roof['kernel']}")
-    return roof
 
 
 def fp64_peak_tflops(torch) -> float:
@@ -260,6 +211,37 @@ def fp64_peak_tflops(torch) -> float:
     return 2.0 * 8192 ** 3 / (best * 1e-3) / 1e12
 
 
+def int8_peak_tops(torch, peaks: dict) -> dict:
+    """INT8 tensor denominator: the larger of a measured cuBLASLt int8 GEMM (torch._int_mm,
+    8192^3, best of 5) and 2 x the driver-measured bf16 burst (dense INT8 issues at twice the
+    bf16 rate on sm_100).  The larger one is the conservative denominator."""
+    meas = None
+    try:
+        a = torch.randint(-64, 64, (8192, 8192), dtype=torch.int8, device="cuda")
+        b = torch.randint(-64, 64, (8192, 8192), dtype=torch.int8, device="cuda")
+        torch._int_mm(a, b)
+        torch.cuda.synchronize()
+        best = math.inf
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        meas = 2.0 * 8192 ** 3 / (best * 1e-3) / 1e12
+        del a, b
+    except Exception:   # noqa: BLE001 — no int8 GEMM in this torch build
+        meas = None
+    derived = 2.0 * peaks["bf16_tflops"] if "bf16_tflops" in peaks else None
+    cands = [v for v in (meas, derived) if v]
+    peak = max(cands) if cands else INT8_DENSE_TOPS_NOMINAL
+    return {"peak": peak, "cublaslt_int8_tops": meas, "two_x_bf16_measured": derived,
+            "nominal": INT8_DENSE_TOPS_NOMINAL,
+            "source": "max(measured torch._int_mm 8192^3, 2 x MEASURED_PEAKS bf16_tflops)" if cands else
+                      "nominal (no measurement)"}
+
+
 def cpu_threads() -> int:
     try:
         from threadpoolctl import threadpool_info
@@ -272,98 +254,176 @@ def cpu_threads() -> int:
     return len(os.sched_getaffinity(0))
 
 
-def cpu_en_rate(case, sweeps: int) -> tuple[float, float]:
-    """Oracle (numpy restatement of racml fit) sweeps/s over `sweeps` fixed sweeps."""
+def cpu_sweep_times(cfg: int, case, sweeps: int) -> list[float]:
+    """Per-sweep wall times of the oracle port (numpy restatement of racml fit / train) over
+    `sweeps` consecutive sweeps of ONE call; the setup (c = -X'y/m) is outside every sweep."""
     from oracle import rac_oracle as ro
-    t0 = time.perf_counter()
-    ro.en_fit(case.X, case.y, case.lam, case.alpha, case.gamma, case.block_size, sweeps,
-              seed=case.seed, tol=None)
-    dt = time.perf_counter() - t0
-    return sweeps / dt, dt
+    stamps = [time.perf_counter()]
+    if cfg == 4:
+        ro.svm_train(case.X, case.labels, case.C, "linear", block_size=case.block_size, beta=case.beta,
+                     max_iters=sweeps, seed=case.seed, fixed_iterations=True,
+                     on_sweep=lambda *a: stamps.append(time.perf_counter()))
+    else:
+        def first(*a):
+            stamps.append(time.perf_counter())
+        ro.en_fit(case.X, case.y, case.lam, case.alpha, case.gamma, case.block_size, sweeps,
+                  seed=case.seed, tol=None, on_sweep=first)
+    return list(np.diff(stamps[1:])) if len(stamps) > 2 else []
 
 
-def cpu_svm_rate(case, sweeps: int) -> tuple[float, float]:
-    """Oracle (numpy restatement of racml train) sweeps/s over `sweeps` sweeps (Q formed once, untimed)."""
+class _SampleDone(Exception):
+    pass
+
+
+def cpu_baseline(cfg: int, case, budget_s: float = 8.0) -> dict:
+    """Bounded sample of the oracle port on the host cores: consecutive sweeps of ONE call,
+    stopped once `budget_s` has elapsed (at least 2 sweeps); the first sweep carries the
+    call's setup and is not counted."""
     from oracle import rac_oracle as ro
+    stamps = []
     t0 = time.perf_counter()
-    ro.svm_train(case.X, case.labels, case.C, "linear", block_size=case.block_size, beta=case.beta,
-                 max_iters=sweeps, seed=0)
-    dt = time.perf_counter() - t0
-    return sweeps / dt, dt
+
+    def cb(*a):
+        stamps.append(time.perf_counter())
+        if len(stamps) >= 3 and stamps[-1] - t0 >= budget_s:
+            raise _SampleDone()
+
+    try:
+        if cfg == 4:
+            ro.svm_train(case.X, case.labels, case.C, "linear", block_size=case.block_size, beta=case.beta,
+                         max_iters=40, seed=case.seed, fixed_iterations=True, on_sweep=cb)
+        else:
+            ro.en_fit(case.X, case.y, case.lam, case.alpha, case.gamma, case.block_size, 40,
+                      seed=case.seed, on_sweep=cb)
+    except _SampleDone:
+        pass
+    total = time.perf_counter() - t0
+    fn = "svm_train" if cfg == 4 else "en_fit"
+    rate = (len(stamps) - 1) / (stamps[-1] - stamps[0])
+    return {"value": rate, "unit": "sweeps/s", "cores": cpu_threads(), "kind": "port",
+            "sample": f"sweeps 2..{len(stamps)} of one oracle/rac_oracle.{fn} call on {case.name} "
+                      f"({total:.1f} s; the first sweep, incl. setup, excluded)"}
 
 
-def run_reference(args, world, rank):
-    """--impl reference: the reference algorithm on the host cores (oracle port)."""
-    case = en_case(args.config)
+# ------------------------------------------------------------------ reference arm
+def run_reference(args) -> int:
+    """--impl reference: the reference's CPU algorithm (the oracle port: same numpy/scipy
+    calls as racml) on the host cores, K consecutive sweeps of the headline config in ONE
+    call, W warm-up sweeps before them in the same call (setup outside the timer)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    svm_cfg = args.config == 4
-    rate_fn = cpu_svm_rate if svm_cfg else cpu_en_rate
-    rate_fn(case, 1)     # warm-up (BLAS threads, page-in)
-    total = 0.0
-    for _ in range(args.steps):
-        _, dt = rate_fn(case, 1)
-        total += dt
-    rate = args.steps / total
-    if svm_cfg:
-        N, d = case.X.shape
-        cfg = {"workload": case.name, "N": N, "d": d, "block_size": case.block_size}
-        sample = f"{args.steps} single-sweep trains of {case.name} (oracle/rac_oracle.svm_train, Q build included)"
-    else:
-        m, n = case.X.shape
-        cfg = {"workload": case.name, "m": m, "n": n, "block_size": case.block_size}
-        sample = f"{args.steps} single sweeps of {case.name} (oracle/rac_oracle.en_fit)"
+    case = make_case(args.config)
+    K, W = args.steps, args.warmup
+    t0 = time.perf_counter()
+    times = cpu_sweep_times(args.config, case, W + K)
+    total = time.perf_counter() - t0
+    timed = times[W - 1:W - 1 + K] if W >= 1 else times[:K]
+    if len(timed) < K:      # W = 0: the first sweep carries the setup; use what was timed
+        timed = times[-K:]
+    sec = float(sum(timed))
+    rate = len(timed) / sec
+    fn = "svm_train" if args.config == 4 else "en_fit"
     line = {
-        "impl": "reference", "metric": "rac_admm_sweeps_per_sec", "value": rate,
-        "unit": "sweeps/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) seed-0 recipe)",
-        "config": cfg,
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": "sweeps/s", "n_gpus": 0,
+        "steps": K, "warmup": W, "ms_per_step": 1e3 * sec / len(timed), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": config_dict(args.config, case, K, world),
         "cpu_baseline": {"value": rate, "unit": "sweeps/s", "cores": cpu_threads(), "kind": "port",
-                         "sample": sample},
+                         "sample": f"sweeps {W + 1}..{W + K} of one oracle/rac_oracle.{fn} call "
+                                   f"({W + K} sweeps, {total:.1f} s incl. setup)"},
         "e2e": {"value": rate, "unit": "sweeps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def run_b200(args, world, rank, local):
-    if args.config == 4:
-        return run_b200_svm(args, world, rank, local)
-    return run_b200_en(args, world, rank, local)
+# ------------------------------------------------------------------ roofline
+def en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, workload, prep_batch=1) -> dict:
+    """Roofline entry for the dominant stage of an EN sweep (per-unit figures: SURVEY.md §8(d),
+    DESIGN.md §4).  `stages` are per-sweep times measured with CUDA events; in covariance mode
+    the block systems of `prep_batch` sweeps are prepared by one launch that overlaps the chain,
+    so the stage that bounds a sweep is picked on factor / prep_batch."""
+    eff = dict(stages)
+    eff["factor"] = stages.get("factor", 0.0) / max(1, prep_batch)
+    eff.pop("assembly", None)
+    dom = max(eff, key=eff.get)
+    sec = stages[dom] * 1e-3
+    if dom == "chain":
+        if gram_mode == "covariance":
+            kern = "en_cla_kernel" if variant == "covariance-lookahead" else "en_cov_kernel"
+            byts = 8.0 * n * n + 8.0 * p * s * s
+            desc = "rows of G read once (8 n^2) + block inverses (8 p s^2) per launch"
+        else:
+            kern = "en_chain_res_kernel" if variant == "resident-cluster" else "en_chain_kernel"
+            byts = 8.0 * m * n + 8.0 * p * s * s
+            desc = "D read once (8 m n; a block's second use hits L2) + block inverses (8 p s^2) per launch"
+        achieved = byts / sec / 1e9
+        roof = {"kernel": kern, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "algorithmic": desc}
+    elif dom == "gram" and gram_mode == "blocks" and block_grams_int8(s, p):
+        jt = (s + 127) // 128
+        ops = 2.0 * 36 * p * (jt * (jt + 1) // 2) * 128 * 128 * ((m + 31) // 32 * 32)
+        achieved = ops / sec / 1e12
+        roof = {"kernel": "gram_i8_kernel (tcgen05 kind::i8, + digit slicing)", "bound": "tensor",
+                "achieved": achieved, "peak": i8["peak"], "unit": "TOPS (int8)", "frac": achieved / i8["peak"],
+                "peak_source": i8["source"],
+                "algorithmic": "36 int8 digit-slice products x 2*128*128*K per upper tile of each of the p "
+                               "blocks per sweep (exact FP64 block Grams)",
+                "fp64_equivalent": {"achieved_tflops": float(m) * n * (s + 1) / sec / 1e12, "peak": fp64,
+                                    "frac": float(m) * n * (s + 1) / sec / 1e12 / fp64,
+                                    "algorithmic": "m*n*(s+1) flop per sweep (symmetric SYRK of all p blocks)"}}
+    elif dom == "gram":
+        achieved = float(m) * n * (s + 1) / sec / 1e12
+        roof = {"kernel": "gram_kernel", "bound": "tensor", "achieved": achieved, "peak": fp64,
+                "unit": "TFLOP/s", "frac": achieved / fp64,
+                "algorithmic": "m*n*(s+1) flop per launch (symmetric SYRK of all p blocks)"}
+    else:
+        achieved = 2.0 * p * float(s) ** 3 / sec / 1e12
+        roof = {"kernel": "factor_kernel" if s <= 236 else "large_*_kernel (blocked inverse)",
+                "bound": "tensor", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
+                "frac": achieved / fp64, "algorithmic": "2 s^3 flop per block inverse x p blocks per sweep"}
+    roof["stage"] = dom
+    roof["traffic"] = traffic_table().get(f"{workload}:{roof['kernel'].split()[0]}")
+    return roof
 
 
-def run_b200_en(args, world, rank, local):
+# ------------------------------------------------------------------ B200 arm: elastic net
+def _ev():
+    import torch
+    return torch.cuda.Event(enable_timing=True)
+
+
+def measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline: bool) -> dict:
     import torch
     from paper_1907_01995_b200 import _device, elastic_net as en
     from paper_1907_01995_b200.problems import Mode
 
     dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    case = en_case(args.config)
     m, n = case.X.shape
     s = min(case.block_size, n)
     p = -(-n // s)
-
-
-    # ---------------- device-resident throughput (fixed sweeps, every sweep does full work)
     K, W = args.steps, args.warmup
     gram_mode = args.gram if args.gram != "auto" else en.choose_gram_mode(m, n, s, K)
+    out: dict = {}
+
+    # ---------------- device-resident throughput (fixed sweeps, every sweep does full work)
     solver = en.EnSolver(m, n, s, Mode.RAC, case.lam, case.alpha, case.gamma, device=local)
     if gram_mode == "covariance":
         solver.set_gram_mode("covariance")
     solver.set_data(case.X, case.y)
     rng = np.random.default_rng(case.seed)
     perms = _device.PermutationFeeder(rng, n, dev).draw(W + K)
-    torch.cuda.synchronize()
     solver.run(perms[:W], None)
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
+    clocks = ClockSampler(local) if headline else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
     dist_barrier(world)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0, e1 = _ev(), _ev()
     l0 = solver.lib.rac_launch_count()
     e0.record()
     if gram_mode == "covariance":
@@ -373,20 +433,21 @@ def run_b200_en(args, world, rank, local):
     launches = solver.lib.rac_launch_count() - l0
     torch.cuda.synchronize()
     dist_barrier(world)
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    ms = dist_max(ms, world, dev)
-    value = world * K / (ms * 1e-3)
+    if clocks:
+        out["clocks"] = clocks.stop()
+    ms = dist_max(e0.elapsed_time(e1), world, dev)
+    out.update({"value": world * K / (ms * 1e-3), "ms_per_step": ms / K, "gpu_launches": int(launches),
+                "gram_mode": gram_mode})
 
     # ---------------- per-stage breakdown (separate sweeps, CUDA events between stages)
     lib = solver.lib
     lib.rac_en_set_timing(solver.h, 1)
-    more = _device.PermutationFeeder(rng, n, dev).draw(K)
-    solver.run(more, None)
+    solver.run(_device.PermutationFeeder(rng, n, dev).draw(K), None)
     stage = (np.ctypeslib.ctypes.c_double * 4)()
     nt = np.ctypeslib.ctypes.c_int32()
     lib.rac_en_timing(solver.h, stage, nt)
     stages = {k: float(v) / max(nt.value, 1) for k, v in zip(("assembly", "gram", "factor", "chain"), stage)}
+    out["stage_ms_per_sweep"] = stages
     # chain phase trace (CTA 0 %globaltimer at each phase boundary of one sweep)
     lib.rac_en_set_timing(solver.h, 2)
     solver.run(_device.PermutationFeeder(rng, n, dev).draw(1), None)
@@ -409,16 +470,15 @@ def run_b200_en(args, world, rank, local):
     variant = {0: "streaming", 1: "resident-cluster", 2: "covariance-cluster",
                3: "covariance-lookahead"}[int(info[0])]
     chain_trace = {"variant": variant, "ctas": int(info[1]), "gram_mode": gram_mode}
-    if nl:
-        pro = {0: 2, 1: 5, 2: 1, 3: 1}[int(info[0])]   # stamps before the first block
-        if info[0] == 3:
-            chain_trace.update({"prep_batch_sweeps": int(info[2]), "lookahead_depth": int(info[3])})
-        tv = np.array(tbuf[:pro + nl * p], dtype=np.float64) / 1e3   # us
-        ph = np.diff(tv[pro - 1:]).reshape(p, nl) if p > 0 else np.zeros((0, nl))
-        if info[0] != 3:
-            chain_trace.update({"rows_per_chunk": int(info[2]), "chunks_per_cta": int(info[3])})
-        chain_trace.update({
-                            "first_phase_us": float(tv[pro - 1] - tv[0]),
+    pro = {0: 2, 1: 5, 2: 1, 3: 1}[int(info[0])]   # stamps before the first block
+    if info[0] == 3:
+        chain_trace.update({"prep_batch_sweeps": int(info[2]), "lookahead_depth": int(info[3])})
+    else:
+        chain_trace.update({"rows_per_chunk": int(info[2]), "chunks_per_cta": int(info[3])})
+    tv = np.array(tbuf[:pro + nl * p], dtype=np.float64) / 1e3   # us
+    if tv[0] > 0:
+        ph = np.diff(tv[pro - 1:]).reshape(p, nl)
+        chain_trace.update({"first_phase_us": float(tv[pro - 1] - tv[0]),
                             "per_block_us": {k: float(v) for k, v in zip(labels, ph.mean(axis=0))}})
     if s <= 236:
         # factor kernel, block 0: assembly, then per 8-pivot step [panel copy, 8x8 sweep, CW, update]
@@ -432,23 +492,26 @@ def run_b200_en(args, world, rank, local):
                 "per_step": {k: float(v) for k, v in zip(("panel", "diag_sweep", "cw", "update"),
                                                          steps.mean(axis=0))}}
     lib.rac_en_set_timing(solver.h, 0)
+    out["chain_trace"] = chain_trace
     solver.close()
-    del perms, more
+    del perms
 
-    # ---------------- time to tolerance (device-resident inputs, host PCG64 stream as in fit)
+    # ---------------- time to tolerance, device: X resident in HBM before the timer; the
+    # timer covers set_data (transpose into the column-major layout and, in covariance mode,
+    # the once-per-fit G = X'X/m) and every sweep, driven like fit() with a tolerance
     ttt = None
     if case.tol is not None:
+        tol_gm = en.choose_gram_mode(m, n, s, case.iters) if args.gram == "auto" else args.gram
+        Xd = torch.from_numpy(np.ascontiguousarray(case.X)).to(dev)
+        yd = torch.from_numpy(np.ascontiguousarray(case.y)).to(dev)
         sol2 = en.EnSolver(m, n, s, Mode.RAC, case.lam, case.alpha, case.gamma, device=local)
-        if args.gram == "covariance" or (args.gram == "auto" and
-                                         en.choose_gram_mode(m, n, s, case.iters) == "covariance"):
-            sol2.set_gram_mode("covariance")
-        sol2.set_data(case.X, case.y)
         rng2 = np.random.default_rng(case.seed)
         feeder = _device.PermutationFeeder(rng2, n, dev)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        # as fit() with a tolerance: batches of 16 sweeps, batch k+1 enqueued before batch
-        # k's status is polled; the final progress() reports the converged sweep
+        if tol_gm == "covariance":
+            sol2.set_gram_mode("covariance")
+        sol2.set_data(Xd, yd)
         sol2.run(feeder.draw(min(16, case.iters)), case.tol)
         done = min(16, case.iters)
         while True:
@@ -462,45 +525,63 @@ def run_b200_en(args, world, rank, local):
             if failed >= 0 or conv or lag == 0:
                 break
         it, conv, res, _ = sol2.progress()
-        t_tol = time.perf_counter() - t0
-        ttt = {"seconds": t_tol, "sweeps": it, "residual": res, "converged": bool(conv),
-               "tol": case.tol}
+        t_dev = time.perf_counter() - t0
         sol2.close()
+        del Xd, yd
+        # end to end: fit() on host arrays with the tolerance (upload, G, sweeps, results)
+        spec_tol = en.ElasticNetSpec(lam=case.lam, alpha=case.alpha, gamma=case.gamma,
+                                     block_size=case.block_size, iters=case.iters, seed=case.seed, tol=case.tol)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        model = en.fit(case.X, case.y, spec_tol)
+        t_e2e = time.perf_counter() - t0
+        ttt = {"seconds": dist_max(t_dev, world, dev), "sweeps": it, "residual": res, "converged": bool(conv),
+               "tol": case.tol, "gram_mode": tol_gm,
+               "timed": "set_data of the HBM-resident X (transpose; G in covariance mode) + all sweeps",
+               "e2e_seconds": dist_max(t_e2e, world, dev), "e2e_sweeps": model.iterations,
+               "e2e_timed": "fit(X_host, y_host, spec(tol)) through the public API"}
+    out["time_to_tol"] = ttt
 
     # ---------------- end to end through the public API (host arrays, H2D/D2H inside)
     spec = en.ElasticNetSpec(lam=case.lam, alpha=case.alpha, gamma=case.gamma,
                              block_size=case.block_size, iters=K, seed=case.seed, tol=None)
     # warm-up call on the full problem: process-level one-time costs (pinned staging
     # buffers, kernel attributes, cluster occupancy queries) stay out of the e2e number
-    en.fit(case.X, case.y, en.ElasticNetSpec(lam=case.lam, alpha=case.alpha, gamma=case.gamma,
-                                             block_size=case.block_size, iters=K, seed=case.seed, tol=None))
+    en.fit(case.X, case.y, spec)
     torch.cuda.synchronize()
     dist_barrier(world)
     t0 = time.perf_counter()
     en.fit(case.X, case.y, spec)
-    t_e2e = time.perf_counter() - t0
-    t_e2e = dist_max(t_e2e, world, dev)
-    e2e = {"value": world * K / t_e2e, "unit": "sweeps/s",
-           "h2d_bytes_per_step": int((8 * m * n + 8 * m) / K + 8 * n),
-           "d2h_bytes_per_step": int((3 * 8 * n + 8 * 2 * K + 16) / K)}
+    t_e2e = dist_max(time.perf_counter() - t0, world, dev)
+    out["e2e"] = {"value": world * K / t_e2e, "unit": "sweeps/s",
+                  "h2d_bytes_per_step": int((8 * m * n + 8 * m) / K + 8 * n),
+                  "d2h_bytes_per_step": int((3 * 8 * n + 8 * 2 * K + 16) / K)}
 
     # ---------------- roofline of the dominant kernel
-    peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
-    fp64 = fp64_peak_tflops(torch)
-    roof = en_roofline(stages, m, n, s, p, gram_mode, chain_trace["variant"], hbm, fp64, case.name,
-                       chain_trace.get("prep_batch_sweeps", 1))
+    out["roofline"] = en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, case.name,
+                                  chain_trace.get("prep_batch_sweeps", 1))
+    out["roofline"]["peak_source"] = out["roofline"].get("peak_source", "MEASURED_PEAKS.json hbm_gbs"
+                                                         if out["roofline"]["unit"] == "GB/s"
+                                                         else "cuBLAS DGEMM 8192^3 measured in this run")
 
-    # ---------------- the covariance Gram G = X'X/m (once per fit): int8 digit-slice tensor-core
-    # kernel vs the FP64 DMMA tiles, both through rac_gram_covariance on the resident X
-    gram_cov = None
-    if gram_mode == "covariance":
-        gram_cov = covariance_gram_timing(case.X, dev)
+    if headline:
+        out.update(en_variants(case, args, world, local, gram_mode, stages, hbm, fp64, i8))
+    return out
 
-    # ---------------- the reference's own algorithm (per-sweep block Grams from X), reported
-    # beside the covariance-mode headline (the G-reuse variant's algorithmic
-    # work differs, so its roofline is not comparable)
-    alt = None
+
+def en_variants(case, args, world, local, gram_mode, stages, hbm, fp64, i8) -> dict:
+    """Beside the headline: the reference's own per-sweep block-Gram arithmetic when the
+    headline runs in covariance mode, and RP mode."""
+    import torch
+    from paper_1907_01995_b200 import _device, elastic_net as en
+    from paper_1907_01995_b200.problems import Mode
+    dev = torch.device("cuda", local)
+    m, n = case.X.shape
+    s = min(case.block_size, n)
+    p = -(-n // s)
+    K, W = args.steps, args.warmup
+    extra = {}
     if gram_mode == "covariance":
         sb = en.EnSolver(m, n, s, Mode.RAC, case.lam, case.alpha, case.gamma, device=local)
         sb.set_data(case.X, case.y)
@@ -508,30 +589,15 @@ def run_b200_en(args, world, rank, local):
         sb.run(pb[:W], None)
         torch.cuda.synchronize()
         dist_barrier(world)
-        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0, b1 = _ev(), _ev()
         b0.record()
         sb.run(pb[W:W + K], None)
         b1.record()
         torch.cuda.synchronize()
         ms_b = dist_max(b0.elapsed_time(b1), world, dev)
-        sb.lib.rac_en_set_timing(sb.h, 1)
-        sb.run(_device.PermutationFeeder(rng, n, dev).draw(K), None)
-        stb = (np.ctypeslib.ctypes.c_double * 4)()
-        ntb = np.ctypeslib.ctypes.c_int32()
-        sb.lib.rac_en_timing(sb.h, stb, ntb)
-        stages_b = {k: float(v) / max(ntb.value, 1) for k, v in zip(("assembly", "gram", "factor", "chain"), stb)}
-        infb = (np.ctypeslib.ctypes.c_int32 * 4)()
-        sb.lib.rac_en_info(sb.h, infb)
-        var_b = {0: "streaming", 1: "resident-cluster"}.get(int(infb[0]), "streaming")
-        alt = {"gram_mode": "blocks", "value": world * K / (ms_b * 1e-3), "ms_per_step": ms_b / K,
-               "stage_ms_per_sweep": stages_b, "chain_variant": var_b,
-               "roofline": en_roofline(stages_b, m, n, s, p, "blocks", var_b, hbm, fp64, case.name)}
+        extra["reference_algorithm_variant"] = {"gram_mode": "blocks", "value": world * K / (ms_b * 1e-3),
+                                                "ms_per_step": ms_b / K}
         sb.close()
-        del pb
-
-    # ---------------- RP mode: fixed partition, block systems formed
-    # once at set_partition, per-sweep block ORDER permutation; the chain is the whole sweep
-    rp = None
     srp = en.EnSolver(m, n, s, Mode.RP, case.lam, case.alpha, case.gamma, device=local)
     if gram_mode == "covariance":
         srp.set_gram_mode("covariance")
@@ -542,68 +608,32 @@ def run_b200_en(args, world, rank, local):
     srp.run(pr[:W], None)
     torch.cuda.synchronize()
     dist_barrier(world)
-    r0e, r1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0e, r1e = _ev(), _ev()
     r0e.record()
     srp.run(pr[W:W + K], None)
     r1e.record()
     torch.cuda.synchronize()
     ms_rp = dist_max(r0e.elapsed_time(r1e), world, dev)
-    rp = {"mode": "rp", "gram_mode": gram_mode, "value": world * K / (ms_rp * 1e-3), "ms_per_step": ms_rp / K,
-          "note": "partition and block factorisations formed once (outside the timed K sweeps), as RP defines"}
+    extra["rp_mode_variant"] = {"mode": "rp", "gram_mode": gram_mode, "value": world * K / (ms_rp * 1e-3),
+                                "ms_per_step": ms_rp / K,
+                                "note": "partition and block factorisations formed once (outside the timed "
+                                        "K sweeps), as RP defines"}
     srp.close()
-    del pr
-
-    # ---------------- CPU baseline (rank 0, N=1 only)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        r1, dt1 = cpu_en_rate(case, 1)
-        sweeps = int(max(1, min(60, 15.0 / max(dt1, 1e-3))))
-        rate, dt = cpu_en_rate(case, sweeps)
-        cpu = {"value": rate, "unit": "sweeps/s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"{sweeps} sweeps of {case.name} via oracle/rac_oracle.en_fit ({dt:.1f} s)"}
-
-    line = {
-        "metric": "rac_admm_sweeps_per_sec", "value": value, "unit": "sweeps/s", "n_gpus": world,
-        "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) seed-0 recipe)",
-        "config": {"workload": case.name, "m": m, "n": n, "block_size": s, "blocks": p,
-                   "mode": "rac", "gram_mode": gram_mode,
-                   "l2": "inputs larger than L2 (D = %.0f MB)" % (8 * m * n / 1e6)
-                   if 8 * m * n > 126e6 else "D fits in L2 (no flush)",
-                   "parallelism": f"replicas x{world}"},
-        "stage_ms_per_sweep": stages,
-        "chain_trace": chain_trace,
-        "time_to_tol": ttt,
-        "e2e": e2e,
-        "roofline": roof,
-        "reference_algorithm_variant": alt,
-        "rp_mode_variant": rp,
-        "covariance_gram": gram_cov,
-        "fp64_dgemm_tflops_measured": fp64,
-        "cpu_baseline": cpu,
-        "clocks": clk,
-        "gpu_launches": int(launches),
-    }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    return 0
+    return extra
 
 
-def run_b200_svm(args, world, rank, local):
-    """Config 4: linear-SVM dual, N=20000, s=100, dense Q resident in HBM (3.2 GB)."""
+# ------------------------------------------------------------------ B200 arm: SVM (config 4)
+def measure_svm(cfg, case, args, world, rank, local, peaks, headline: bool) -> dict:
     import torch
     from paper_1907_01995_b200 import _device, svm
     from paper_1907_01995_b200.engine import QpSolver
     from paper_1907_01995_b200.problems import Mode, SolverConfig
 
     dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
-    from paper_1907_01995_b200 import configs
-    case = configs.config4()
     X, y = case.X, case.labels
     N, d = X.shape
     s = case.block_size
-    p = -(-N // s)
+    K, W = args.steps, args.warmup
     t0 = time.perf_counter()
     Q = svm.build_q(X, y, svm.KernelSpec("linear"), dev)
     t_q = time.perf_counter() - t0
@@ -612,16 +642,16 @@ def run_b200_svm(args, world, rank, local):
                        b=np.zeros(1), borrowed_h=Q)
     solver.set_divergence_bar(math.inf)
     rng = np.random.default_rng(case.seed)
-    K, W = args.steps, args.warmup
     perms = _device.PermutationFeeder(rng, N, dev).draw(W + K)
     solver.run(perms[:W], W, case.tol_primal, case.tol_dual, True)
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
+    clocks = ClockSampler(local) if headline else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
     dist_barrier(world)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0, e1 = _ev(), _ev()
     l0 = solver.lib.rac_launch_count()
     e0.record()
     solver.run(perms[W:W + K], K, case.tol_primal, case.tol_dual, True)
@@ -629,53 +659,113 @@ def run_b200_svm(args, world, rank, local):
     launches = solver.lib.rac_launch_count() - l0
     torch.cuda.synchronize()
     dist_barrier(world)
-    clk = clocks.stop()
+    out = {}
+    if clocks:
+        out["clocks"] = clocks.stop()
     ms = dist_max(e0.elapsed_time(e1), world, dev)
-    value = world * K / (ms * 1e-3)
     it, status, _ = solver.progress()
     hp, _, hd = (h.cpu().numpy() for h in solver.history(it))
     solver.close()
+    del Q
     # ---------------- end to end through the public API (svm.train on host arrays)
-    cfg = SolverConfig(mode=Mode.RAC, block_size=s, beta_penalty=case.beta, max_iters=K,
-                       tol_primal=case.tol_primal, tol_dual=case.tol_dual, seed=0, fixed_iterations=True)
+    cfgk = SolverConfig(mode=Mode.RAC, block_size=s, beta_penalty=case.beta, max_iters=K,
+                        tol_primal=case.tol_primal, tol_dual=case.tol_dual, seed=case.seed, fixed_iterations=True)
     svm.train(X, y, case.C, svm.KernelSpec("linear"), SolverConfig(block_size=s, max_iters=1))
     torch.cuda.synchronize()
     dist_barrier(world)
     t0 = time.perf_counter()
-    svm.train(X, y, case.C, svm.KernelSpec("linear"), cfg)
+    svm.train(X, y, case.C, svm.KernelSpec("linear"), cfgk)
     t_e2e = dist_max(time.perf_counter() - t0, world, dev)
-    e2e = {"value": world * K / t_e2e, "unit": "sweeps/s",
-           "h2d_bytes_per_step": int((8 * N * d + 8 * N) / K + 8 * N),
-           "d2h_bytes_per_step": int((8 * N + 8) / K + 32)}
-    peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
-    strip_bytes = 8.0 * N * N
-    achieved = strip_bytes / (ms * 1e-3 / K) / 1e9
-    roof = {"kernel": "qp_chain_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm,
-            "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": traffic_table().get(f"{case.name}:qp_chain_kernel"),
-            "algorithmic": "one strip pass over Q (8*N^2 bytes) per launch (= one sweep)"}
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        from oracle import rac_oracle as ro
-        t0 = time.perf_counter()
-        ro.svm_train(X, y, case.C, "linear", block_size=s, beta=case.beta, max_iters=1, seed=0)
-        dt = time.perf_counter() - t0
-        cpu = {"value": 1.0 / dt, "unit": "sweeps/s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"1 sweep of {case.name} via oracle/rac_oracle.svm_train ({dt:.1f} s)"}
-    line = {
-        "metric": "rac_admm_sweeps_per_sec", "value": value, "unit": "sweeps/s", "n_gpus": world,
-        "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) seed-0 recipe)",
-        "config": {"workload": case.name, "N": N, "d": d, "block_size": s, "blocks": p, "mode": "rac",
-                   "l2": "inputs larger than L2 (Q = %.1f GB)" % (8 * N * N / 1e9),
-                   "parallelism": f"replicas x{world}"},
+    achieved = 8.0 * N * N / (ms * 1e-3 / K) / 1e9
+    out.update({
+        "value": world * K / (ms * 1e-3), "ms_per_step": ms / K, "gpu_launches": int(launches),
         "q_build_seconds": t_q,
         "residuals_at_last_sweep": {"primal": float(hp[-1]), "dual": float(hd[-1]), "sweeps": it},
-        "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": int(launches),
+        "time_to_tol": {"seconds": None, "converged": False, "tol": case.tol_primal,
+                        "note": "with beta = 1 the dual residual stays near C (reference and GPU alike, "
+                                "SURVEY §8(d)); residuals at the cap are reported instead"},
+        "e2e": {"value": world * K / t_e2e, "unit": "sweeps/s",
+                "h2d_bytes_per_step": int((8 * N * d + 8 * N) / K + 8 * N),
+                "d2h_bytes_per_step": int((8 * N + 8) / K + 32)},
+        "roofline": {"kernel": "qp_chain_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm,
+                     "unit": "GB/s", "frac": achieved / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                     "traffic": traffic_table().get(f"{case.name}:qp_chain_kernel"),
+                     "algorithmic": "one strip pass over Q (8*N^2 bytes) per launch (= one sweep)"},
+    })
+    return out
+
+
+# ------------------------------------------------------------------ B200 arm: driver
+SUMMARY_KEYS = ("value", "ms_per_step", "e2e", "time_to_tol", "roofline", "cpu_baseline", "stage_ms_per_sweep",
+                "gram_mode", "residuals_at_last_sweep", "config")
+
+
+def run_b200(args) -> int:
+    import torch
+    from paper_1907_01995_b200 import _native
+    world, rank, local = dist_setup("nccl")
+    torch.cuda.set_device(local)
+    _native.load()
+    peaks = measured_peaks()
+    fp64 = fp64_peak_tflops(torch)
+    i8 = int8_peak_tops(torch, peaks)
+    order = [args.config] + ([] if args.only else [c for c in (1, 2, 3, 4, 5) if c != args.config])
+    results = {}
+    for cfg in order:
+        headline = cfg == args.config
+        case = make_case(cfg)
+        if cfg == 4:
+            r = measure_svm(cfg, case, args, world, rank, local, peaks, headline)
+        else:
+            r = measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline)
+        r["config"] = config_dict(cfg, case, args.steps, world)
+        if rank == 0 and world == 1 and not args.no_cpu:
+            r["cpu_baseline"] = cpu_baseline(cfg, case, budget_s=8.0 if headline else 5.0)
+        else:
+            r["cpu_baseline"] = None
+        results[cfg] = r
+        del case
+        torch.cuda.empty_cache()
+    h = results[args.config]
+    line = {
+        "metric": METRIC, "value": h["value"], "unit": "sweeps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+        "config": h["config"], "e2e": h["e2e"], "roofline": h["roofline"], "cpu_baseline": h["cpu_baseline"],
+        "clocks": h.get("clocks"), "gpu_launches": h["gpu_launches"], "time_to_tol": h.get("time_to_tol"),
     }
+    for k in ("stage_ms_per_sweep", "chain_trace", "reference_algorithm_variant", "rp_mode_variant",
+              "q_build_seconds", "residuals_at_last_sweep"):
+        if k in h:
+            line[k] = h[k]
+    line["peaks"] = {"hbm_gbs": peaks.get("hbm_gbs", HBM_FALLBACK_GBS), "fp64_dgemm_tflops_measured": fp64,
+                     "int8": i8}
+    line["configs"] = {results[c]["config"]["workload"]: {k: results[c].get(k) for k in SUMMARY_KEYS
+                                                           if k in results[c]}
+                       for c in sorted(results)}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def run_plumbing_check(args) -> int:
+    """`--plumbing-check`: the multi-rank plumbing of this script (rank layout, barrier,
+    max-over-ranks, rank-0 printing) over gloo, no GPU work.  Used by the CPU test of
+    `--gpus N`."""
+    world, rank, _ = dist_setup("gloo")
+    t0 = time.perf_counter()
+    dist_barrier(world)
+    val = dist_max(time.perf_counter() - t0 + 1e-6 * (rank + 1), world)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "n_gpus": world, "plumbing_check": True, "max_over_ranks_s": val}),
+              flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
     return 0
 
 
@@ -685,21 +775,23 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=HEADLINE, choices=[1, 2, 3, 4, 5],
+                    help="headline BASELINE config (default 5, the largest single-GPU one)")
+    ap.add_argument("--only", action="store_true", help="measure the headline config only")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--plumbing-check", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--gram", default="auto", choices=["auto", "blocks", "covariance"],
-                    help="EN block systems: per-sweep block Grams or covariance mode (G formed in the timed region)")
+                    help="EN block systems: per-sweep block Grams or covariance mode (G formed inside every "
+                         "timed region: throughput, time to tol, e2e)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    world, rank, local = dist_setup(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)
+    if args.plumbing_check:
+        return run_plumbing_check(args)
     if args.impl == "reference":
-        rc = run_reference(args, world, rank)
-    else:
-        rc = run_b200(args, world, rank, local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
-    return rc
+        return run_reference(args)
+    return run_b200(args)
 
 
 if __name__ == "__main__":

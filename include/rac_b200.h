@@ -58,6 +58,11 @@ const char* rac_last_error(void);
 /* Number of kernels this library has launched since load (all contexts, all
  * streams); used by bench.py to report gpu_launches inside a timed region. */
 uint64_t rac_launch_count(void);
+
+/* Return freed context memory of the current device's stream-ordered pool to the
+ * driver, keeping at most keep_bytes mapped (the pool itself keeps <= 8 GiB across
+ * synchronisations).  No reference counterpart: numpy frees eagerly. */
+int rac_trim_pool(uint64_t keep_bytes);
 /* 0 if `device` is an sm_100 part this library was built for. */
 int rac_device_check(int device);
 
@@ -182,6 +187,9 @@ int rac_qp_set_problem(rac_qp_ctx* ctx, const double* H, const double* A, const 
                        const double* c, const double* lower, const double* upper);
 /* Use an externally owned H (e.g. the SVM Q built by rac_svm_build_q) without copying. */
 int rac_qp_borrow_h(rac_qp_ctx* ctx, const double* H);
+/* Replaces engine.py:284-315's inputs (x, y) of run_sweep: the next sweep starts from the
+ * device vectors x (n) and y (m) instead of (clip(0, lower, upper), 0). */
+int rac_qp_set_state(rac_qp_ctx* ctx, const double* x, const double* y);
 /* Divergence bar (engine.py:361-362): set_problem uses 1e8*max(primal0, 1);
  * svm.train has no guard and passes +inf. */
 int rac_qp_set_divergence_bar(rac_qp_ctx* ctx, double bar);
@@ -207,6 +215,13 @@ int rac_qp_destroy(rac_qp_ctx* ctx);
 int rac_svm_build_q(const double* X, int64_t N, int64_t d, const double* labels, int32_t kind,
                     double sigma, double* Q, void* stream);
 /* out_i = sum_j Q_ij * w_j (one HBM pass; used for the SVM bias, svm.py:287-305). */
+/* Label-weighted kernel strip rows of s samples against all N:
+ *   strip[i * N + j] = labels[rows[i]] * labels[j] * K(X[rows[i]], X[j])
+ * X row-major N x d (device), rows int32 (-1 = zero padding row).  FP64 tensor cores with
+ * the kernel epilogue fused.  Replaces svm.py:121-143 assemble_kernel_block(with_strip=True)
+ * / KernelRowCache.row (svm.py:107-118); Q_bb = strip[:, rows]. */
+int rac_svm_kernel_strip(const double* X, int64_t N, int64_t d, const double* labels, const int32_t* rows,
+                         int32_t s, int32_t kind, double sigma, double* strip, void* stream);
 int rac_gemv(const double* Q, int64_t rows, int64_t cols, const double* w, double* out,
              void* stream);
 

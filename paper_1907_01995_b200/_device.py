@@ -15,16 +15,27 @@ import torch
 from . import _native
 
 
-def require_cuda(device: int = 0) -> torch.device:
+def resolve_device(device=None) -> int:
+    """Device index: an int, a torch.device, or None = the current CUDA device (so a rank
+    that called torch.cuda.set_device(local) gets its own GPU by default)."""
+    if isinstance(device, torch.device):
+        device = device.index
+    if device is None:
+        return torch.cuda.current_device() if torch.cuda.is_available() else 0
+    return int(device)
+
+
+def require_cuda(device=None) -> torch.device:
     if not torch.cuda.is_available():
         raise RuntimeError("paper_1907_01995_b200 needs a CUDA device (B200, sm_100a); "
                            "there is no CPU fallback")
-    _native.require_device(device)
-    return torch.device("cuda", device)
+    idx = resolve_device(device)
+    _native.require_device(idx)
+    return torch.device("cuda", idx)
 
 
-def stream_handle(stream: torch.cuda.Stream | None = None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
+def stream_handle(stream: torch.cuda.Stream | None = None, device=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return int(s.cuda_stream)
 
 
@@ -47,8 +58,13 @@ class _Stager:
     def __init__(self):
         self.bufs = [torch.empty(self.CHUNK, dtype=torch.uint8).pin_memory() for _ in range(self.SLOTS)]
         self.events = [None] * self.SLOTS
+        self.lock = threading.Lock()   # one upload at a time owns the ring (concurrent fits)
 
     def copy(self, src: torch.Tensor, dst: torch.Tensor) -> None:
+        with self.lock:
+            self._copy(src, dst)
+
+    def _copy(self, src: torch.Tensor, dst: torch.Tensor) -> None:
         sb = src.reshape(-1).view(torch.uint8)
         db = dst.reshape(-1).view(torch.uint8)
         stream = torch.cuda.current_stream(dst.device)
@@ -66,6 +82,7 @@ class _Stager:
 
 
 _stagers: dict = {}
+_STAGE_LOCK = threading.Lock()   # creation of the per-device rings
 
 ROW_CHUNK_BYTES = 16 << 20
 
@@ -85,8 +102,15 @@ class _RowStreamer:
         self.dev = [None] * nbuf
         self.copied = [None] * nbuf
         self.consumed = [None] * nbuf
+        self.lock = threading.Lock()   # one streamed ingest at a time owns the ring
 
     def run(self, X: np.ndarray, align: int, consume) -> None:
+        # the ring's device buffers are reused by the next ingest only after the device-side
+        # wait on `consumed` (events are valid across streams and threads)
+        with self.lock:
+            self._run(X, align, consume)
+
+    def _run(self, X: np.ndarray, align: int, consume) -> None:
         m, n = X.shape
         rows_per = max(align, (ROW_CHUNK_BYTES // (8 * n)) // align * align)
         need = rows_per * n
@@ -124,9 +148,11 @@ def stream_rows(X: np.ndarray, align: int, consume, device=None) -> None:
     row chunks of ~ROW_CHUNK_BYTES (rows a multiple of `align` except the last)."""
     dev = torch.device(device or "cuda")
     key = dev.index if dev.index is not None else torch.cuda.current_device()
-    if key not in _streamers:
-        _streamers[key] = _RowStreamer(dev, int(os.environ.get("RAC_STAGE_BUFS", "4")))
-    _streamers[key].run(np.ascontiguousarray(X, dtype=np.float64), align, consume)
+    with _STAGE_LOCK:
+        if key not in _streamers:
+            _streamers[key] = _RowStreamer(torch.device("cuda", key), int(os.environ.get("RAC_STAGE_BUFS", "4")))
+        st = _streamers[key]
+    st.run(np.ascontiguousarray(X, dtype=np.float64), align, consume)
 
 
 def upload(arr, dtype=torch.float64, device=None, pinned: bool = True) -> torch.Tensor:
@@ -147,9 +173,11 @@ def upload(arr, dtype=torch.float64, device=None, pinned: bool = True) -> torch.
         return src.pin_memory().to(dev, non_blocking=True)
     dst = torch.empty(src.shape, dtype=src.dtype, device=dev)
     key = dst.device.index
-    if key not in _stagers:
-        _stagers[key] = _Stager()
-    _stagers[key].copy(src, dst)
+    with _STAGE_LOCK:
+        if key not in _stagers:
+            _stagers[key] = _Stager()
+        st = _stagers[key]
+    st.copy(src, dst)
     return dst
 
 

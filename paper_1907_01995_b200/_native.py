@@ -31,6 +31,7 @@ SIGNATURES = {
     "rac_version": (C.c_char_p, []),
     "rac_last_error": (C.c_char_p, []),
     "rac_launch_count": (C.c_uint64, []),
+    "rac_trim_pool": (_i32, [C.c_uint64]),
     "rac_device_check": (_i32, [_i32]),
     "rac_chunk_sort": (_i32, [_p, _i64, _i32, _i32, _p, _p]),
     "rac_gram_workspace_bytes": (_sz, [_i64, _i32, _i32]),
@@ -57,6 +58,8 @@ SIGNATURES = {
     "rac_qp_create": (_i32, [C.POINTER(_p), _i64, _i64, _i32, _i32, _f64, _f64, _p]),
     "rac_qp_set_problem": (_i32, [_p, _p, _p, _p, _p, _p, _p]),
     "rac_qp_borrow_h": (_i32, [_p, _p]),
+    "rac_qp_set_state": (_i32, [_p, _p, _p]),
+    "rac_svm_kernel_strip": (_i32, [_p, _i64, _i64, _p, _p, _i32, _i32, _f64, _p, _p]),
     "rac_qp_set_divergence_bar": (_i32, [_p, _f64]),
     "rac_qp_set_partition": (_i32, [_p, _p]),
     "rac_qp_run": (_i32, [_p, _p, _i32, _f64, _f64, _i32]),

@@ -44,13 +44,26 @@ def build(force: bool = False, verbose: bool = True) -> str:
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     objs = []
+    cmds = []
     for src in sources():
         obj = os.path.join(LIBDIR, os.path.basename(src)[:-3] + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmds.append([nvcc(), *ARCH, *FLAGS, "-c", src, "-o", obj])
+        objs.append(obj)
+    # translation units compile independently: run them in parallel
+    from concurrent.futures import ThreadPoolExecutor
+
+    def compile_one(cmd):
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
+        return subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, cmds))
+    for cmd, r in zip(cmds, results):
+        if r.stdout or r.stderr:
+            print(r.stdout + r.stderr, end="", flush=True)
+        if r.returncode != 0:
+            raise subprocess.CalledProcessError(r.returncode, cmd)
     tmp = LIB + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     if verbose:

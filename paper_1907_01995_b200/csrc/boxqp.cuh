@@ -396,7 +396,9 @@ __device__ void projected_gradient(const double* M, int ldm, int s, BoxWork& w) 
 
 // Entry: w.x holds the unconstrained solution M^{-1} r on input.  Returns 0 or
 // the fail code of a non-PD reduced system.
-__device__ int box_active_set(const double* M, int ldm, int s, BoxWork& w, bool use_schur) {
+// `max_passes` < 0: the reference's budget ACTIVE_SET_PASS_FACTOR * s (engine.py:38,215);
+// rac_box_block_min lowers it only to exercise the projected-gradient fallback in tests.
+__device__ int box_active_set(const double* M, int ldm, int s, BoxWork& w, bool use_schur, int max_passes = -1) {
   const int tid = threadIdx.x, nt = blockDim.x;
   int bnd = 0, out = 0;
   for (int i = tid; i < s; i += nt) {
@@ -413,7 +415,8 @@ __device__ int box_active_set(const double* M, int ldm, int s, BoxWork& w, bool 
     w.flag[i] = (v <= w.lo[i]) ? 1 : ((v >= w.hi[i]) ? 2 : 0);
   }
   __syncthreads();
-  for (int pass = 0; pass < 10 * s; ++pass) {
+  const int budget = max_passes < 0 ? 10 * s : max_passes;
+  for (int pass = 0; pass < budget; ++pass) {
     for (int it = 0; it <= s; ++it) {
       for (int i = tid; i < s; i += nt) {
         if (w.flag[i] == 1) w.x[i] = w.lo[i];

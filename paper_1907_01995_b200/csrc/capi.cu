@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <atomic>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "rac_internal.h"
 
@@ -27,28 +28,69 @@ int check_cuda(cudaError_t e, const char* what) {
 
 int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what); }
 
-// Context buffers come from the device's default stream-ordered memory pool
-// with an unbounded release threshold: once a shape has been seen, creating and
-// destroying a context (one per fit/train/solve call) neither maps memory nor
-// synchronises the device (cudaFree would).
-int dev_alloc(void** p, size_t bytes, cudaStream_t st) {
-  static bool pool_ready = false;
-  if (!pool_ready) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ULL;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
+// Context buffers come from each device's default stream-ordered memory pool.
+// The pool keeps up to POOL_KEEP bytes of freed memory mapped (release
+// threshold), so re-creating a context of a seen shape (one per fit/train/solve
+// call) neither maps memory nor synchronises the device; anything above that is
+// returned at the next synchronisation, and rac_trim_pool() / a context's
+// destruction trims the pool back to the threshold so that PyTorch's caching
+// allocator (e.g. an N x N SVM Q after a large fit) can have the memory.
+static const uint64_t POOL_KEEP = 8ULL << 30;
+static std::atomic<uint64_t> g_pool_ready{0};   // bit per configured device
+
+static cudaMemPool_t device_pool(int dev) {
+  cudaMemPool_t pool = nullptr;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) {
     cudaGetLastError();
-    pool_ready = true;
+    return nullptr;
   }
+  const uint64_t bit = 1ULL << (dev & 63);
+  if (!(g_pool_ready.load() & bit)) {
+    uint64_t thr = POOL_KEEP;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    cudaGetLastError();
+    g_pool_ready.fetch_or(bit);
+  }
+  return pool;
+}
+
+int dev_alloc(void** p, size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  device_pool(dev);
   return check_cuda(cudaMallocAsync(p, bytes, st), "cudaMallocAsync");
 }
 
 void dev_free(void* p, cudaStream_t st) {
   if (p) cudaFreeAsync(p, st);
+}
+
+void trim_pool(size_t keep) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (cudaMemPool_t pool = device_pool(dev)) cudaMemPoolTrimTo(pool, keep);
+  cudaGetLastError();
+}
+
+// Nsight Compute cannot replay cooperative (grid-synchronised) launches, cluster ones
+// least of all.  Under the profiler (it injects itself through CUDA_INJECTION64_PATH)
+// or with RAC_PROFILE_NONCOOP=1, the persistent chain kernels are launched without
+// the cooperative attribute: every such grid is sized to one co-resident wave (checked
+// with the occupancy API when the context is planned) and the other kernels sharing
+// the GPU never wait on the chain, so all its CTAs still become resident and the
+// software grid barriers hold.  RAC_PROFILE_NONCOOP=0 forces cooperative launches.
+bool profile_noncoop() {
+  static const int v = [] {
+    if (const char* e = getenv("RAC_PROFILE_NONCOOP")) return atoi(e) == 1 ? 1 : 0;
+    const char* inj = getenv("CUDA_INJECTION64_PATH");
+    return (inj && *inj) ? 1 : 0;
+  }();
+  return v == 1;
+}
+
+cudaError_t launch_coop(const void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st) {
+  if (profile_noncoop()) return cudaLaunchKernel(f, grid, block, args, smem, st);
+  return cudaLaunchCooperativeKernel(f, grid, block, args, smem, st);
 }
 
 static std::atomic<unsigned long long> g_launches{0};
@@ -103,6 +145,12 @@ __global__ void z_prox_kernel(const double* __restrict__ beta, const double* __r
 }
 
 }  // namespace rac
+
+extern "C" int rac_trim_pool(uint64_t keep_bytes) {
+  rac::clear_error();
+  rac::trim_pool((size_t)keep_bytes);
+  return RAC_OK;
+}
 
 extern "C" uint64_t rac_launch_count(void) { return (uint64_t)rac::launch_count(); }
 

@@ -57,7 +57,7 @@ struct EnChainArgs {
 // RC > 0: row chunks of RC rows streamed through shared memory; RC == 0: each CTA owns
 // `rw` contiguous rows and keeps the current block's tile resident (row_phase_1t)
 template <int RC>
-__global__ void __launch_bounds__(ENT) en_chain_kernel(EnChainArgs a) {
+__global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
   if (a.ctrl[0]) return;
   extern __shared__ __align__(16) double esm[];
   const int s = a.s;
@@ -658,8 +658,7 @@ int en_chain_cla(rac_en_ctx* c, double tol, cudaStream_t st, int nsw) {
   at[1].id = cudaLaunchAttributeCooperative;
   at[1].val.cooperative = 1;
   cfg.attrs = at;
-  static const bool noncoop = getenv("RAC_PROFILE_NONCOOP") && atoi(getenv("RAC_PROFILE_NONCOOP")) == 1;
-  cfg.numAttrs = noncoop ? 1 : 2;
+  cfg.numAttrs = profile_noncoop() ? 1 : 2;
   note_launch();
   int rc = check_cuda(cudaLaunchKernelExC(&cfg, cla_kernel(c->cla_L), args), "en_cla (cluster cooperative launch)");
   if (rc || !a.snap) return rc;
@@ -775,8 +774,7 @@ int en_chain(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
     // Nsight Compute cannot replay a cooperative *cluster* launch; for profiling only,
     // RAC_PROFILE_NONCOOP=1 drops the cooperative attribute (the grid is one wave of
     // one CTA per SM either way, and ncu serialises kernels, so the barrier still holds).
-    static const bool noncoop = getenv("RAC_PROFILE_NONCOOP") && atoi(getenv("RAC_PROFILE_NONCOOP")) == 1;
-    cfg.numAttrs = noncoop ? 1 : 2;
+    cfg.numAttrs = profile_noncoop() ? 1 : 2;
     // the function attribute is process-wide: another context's plan may have lowered it
     cudaFuncSetAttribute(res_kernel(c->cs), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.dynamicSmemBytes);
     note_launch();
@@ -793,13 +791,13 @@ int en_chain(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
     if (smem > 48 * 1024) cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   if (c->RC == 0)
-    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<0>, dim3(c->P), dim3(ENT), args, smem, st);
+    e = launch_coop((void*)en_chain_kernel<0>, dim3(c->P), dim3(ENT), args, smem, st);
   else if (c->RC == 32)
-    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<32>, dim3(c->P), dim3(ENT), args, smem, st);
+    e = launch_coop((void*)en_chain_kernel<32>, dim3(c->P), dim3(ENT), args, smem, st);
   else if (c->RC == 16)
-    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<16>, dim3(c->P), dim3(ENT), args, smem, st);
+    e = launch_coop((void*)en_chain_kernel<16>, dim3(c->P), dim3(ENT), args, smem, st);
   else
-    e = cudaLaunchCooperativeKernel((void*)en_chain_kernel<8>, dim3(c->P), dim3(ENT), args, smem, st);
+    e = launch_coop((void*)en_chain_kernel<8>, dim3(c->P), dim3(ENT), args, smem, st);
   note_launch();
   return check_cuda(e, "en_chain (cooperative launch)");
 }

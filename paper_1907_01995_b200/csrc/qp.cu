@@ -186,7 +186,7 @@ __device__ QpSmem carve_qp(double* base, int s, bool rowphase, bool lsmem, doubl
 }
 
 template <int RC>
-__global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
+__global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
   if (a.ctrl[0]) return;
   extern __shared__ __align__(16) double qsm[];
   const int s = a.s;
@@ -627,19 +627,19 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
         if (i < a.m) {
           const double res = ldcg(a.ax + i) - a.b[i];
           a.y[i] = a.y[i] - beta * res;
-          pm = fmax(pm, fabs(res));
+          pm = nanmax(pm, fabs(res));
           ps += fabs(res);
         }
       }
     }
   }
-  pm = warp_max(pm);
+  pm = warp_nanmax(pm);
   ps = warp_sum(ps);
   if (lane == 0) { w.bw.red[warp] = pm; w.sc[warp] = ps; }
   __syncthreads();
   if (tid == 0) {
     double m1 = 0.0, s1 = 0.0;
-    for (int q = 0; q < nw; ++q) { m1 = fmax(m1, w.bw.red[q]); s1 += w.sc[q]; }
+    for (int q = 0; q < nw; ++q) { m1 = nanmax(m1, w.bw.red[q]); s1 += w.sc[q]; }
     a.pmax[blockIdx.x] = m1;
     a.psum[blockIdx.x] = s1;
   }
@@ -660,30 +660,31 @@ __global__ void __launch_bounds__(QPT) qp_chain_kernel(QpChainArgs a) {
         if (a.H) grad = grad + ldcg(a.hx + j);
         if (has_a) grad = grad - aty;
         const double xj = ldcg(a.x + j);
-        const double pr = fmin(fmax(xj - grad, a.lo[j]), a.hi[j]);
-        dm = fmax(dm, fabs(pr - xj));
+        const double v = xj - grad;
+        const double pr = (v != v) ? v : fmin(fmax(v, a.lo[j]), a.hi[j]);   // np.clip keeps NaN
+        dm = nanmax(dm, fabs(pr - xj));
       }
     }
   }
-  dm = warp_max(dm);
+  dm = warp_nanmax(dm);
   if (lane == 0) w.bw.red[warp] = dm;
   __syncthreads();
   if (tid == 0) {
     double m1 = 0.0;
-    for (int q = 0; q < nw; ++q) m1 = fmax(m1, w.bw.red[q]);
+    for (int q = 0; q < nw; ++q) m1 = nanmax(m1, w.bw.red[q]);
     a.dmax[blockIdx.x] = m1;
   }
   grid_barrier(a.bar, target, P);
   if (blockIdx.x == 0 && warp == 0) {
     double pmx = 0.0, psm = 0.0, dmx = 0.0;
     for (int q = lane; q < P; q += 32) {
-      pmx = fmax(pmx, ldcg(a.pmax + q));
+      pmx = nanmax(pmx, ldcg(a.pmax + q));
       psm += ldcg(a.psum + q);
-      dmx = fmax(dmx, ldcg(a.dmax + q));
+      dmx = nanmax(dmx, ldcg(a.dmax + q));
     }
-    pmx = warp_max(pmx);
+    pmx = warp_nanmax(pmx);
     psm = warp_sum(psm);
-    dmx = warp_max(dmx);
+    dmx = warp_nanmax(dmx);
     if (lane == 0) {
       a.hist_p[a.sweep] = pmx;
       a.hist_l1[a.sweep] = psm;
@@ -709,7 +710,7 @@ __global__ void clip0_kernel(const double* lo, const double* hi, int64_t n, doub
 // single-CTA test entry for the box solver (inverse-free first solve)
 __global__ void __launch_bounds__(QPT) box_test_kernel(const double* M, const double* r, const double* lo,
                                                        const double* hi, int s, double* xout,
-                                                       int32_t* info, double* L) {
+                                                       int32_t* info, double* L, int max_passes) {
   extern __shared__ __align__(16) double bsm[];
   QpSmem w = carve_qp<32>(bsm, s, false, false, L);   // workspace L: global, s(s+1)
   for (int i = threadIdx.x; i < s; i += QPT) {
@@ -726,7 +727,7 @@ __global__ void __launch_bounds__(QPT) box_test_kernel(const double* M, const do
   if (!fail) {
     for (int i = threadIdx.x; i < s; i += QPT) w.bw.x[i] = w.bw.xf[i];
     __syncthreads();
-    fail = box_active_set(M, s, s, w.bw, false);
+    fail = box_active_set(M, s, s, w.bw, false, max_passes);
   }
   for (int i = threadIdx.x; i < s; i += QPT) xout[i] = w.bw.x[i];
   if (threadIdx.x == 0) *info = fail;
@@ -910,7 +911,7 @@ int qp_chain(rac_qp_ctx* c, double tol_p, double tol_d, int fixed) {
   a.Ninv = c->Ninv;
   a.cond = c->cond;
   void* args[] = {&a};
-  cudaError_t e = cudaLaunchCooperativeKernel(qp_kernel(c), dim3(c->P), dim3(QPT), args, qp_smem(c), c->st);
+  cudaError_t e = launch_coop((const void*)qp_kernel(c), dim3(c->P), dim3(QPT), args, qp_smem(c), c->st);
   note_launch();
   return check_cuda(e, "qp_chain (cooperative launch)");
 }
@@ -1042,6 +1043,39 @@ extern "C" int rac_qp_set_problem(rac_qp_ctx* c, const double* H, const double* 
   c->div_bar = 1e8 * std::max(primal0, 1.0);
   c->ready = true;
   return check_launch("rac_qp_set_problem");
+}
+
+namespace rac {
+// out = A x for the column-major (lda x n) copy of A: one thread per row, columns in order
+__global__ void gemv_colmajor_kernel(const double* __restrict__ Ac, int64_t lda, int64_t m, int64_t n,
+                                     const double* __restrict__ x, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t j = 0; j < n; ++j) acc = fma(Ac[j * lda + i], x[j], acc);
+    out[i] = acc;
+  }
+}
+}  // namespace rac
+
+// Start the next sweep from (x, y) instead of (clip(0, lo, hi), 0): the running products
+// Hx and Ax are recomputed from x.  engine.run_sweep (engine.py:284-315) goes through this.
+extern "C" int rac_qp_set_state(rac_qp_ctx* c, const double* x, const double* y) {
+  using namespace rac;
+  clear_error();
+  if (!c || !x || (c->m > 0 && !y)) return set_error(RAC_ERR_ARG, "rac_qp_set_state: null pointer");
+  if (!c->ready) return set_error(RAC_ERR_ARG, "rac_qp_set_state: call rac_qp_set_problem first");
+  cudaMemcpyAsync(c->x, x, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->st);
+  if (c->m > 0) cudaMemcpyAsync(c->y, y, c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->st);
+  if (c->H) {
+    int rc = launch_gemv_rows(c->H, c->n, c->n, c->x, c->hx, c->st);
+    if (rc) return rc;
+  }
+  if (c->m > 0) {
+    gemv_colmajor_kernel<<<(int)std::min<int64_t>((c->m + 127) / 128, 1184), 128, 0, c->st>>>(
+        c->Ac, c->lda, c->m, c->n, c->x, c->ax);
+    note_launch();
+  }
+  return check_launch("rac_qp_set_state");
 }
 
 extern "C" int rac_qp_borrow_h(rac_qp_ctx* c, const double* H) {
@@ -1240,7 +1274,11 @@ extern "C" int rac_box_block_min(const double* M, const double* r, const double*
   int rc = check_cuda(cudaFuncSetAttribute(box_test_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "box smem attribute");
   if (rc) return rc;
-  box_test_kernel<<<1, QPT, smem, st>>>(M, r, lo, hi, s, x, info, L);
+  // RAC_BOX_PASSES (tests only): active-set pass budget instead of 10 s, e.g. 0 to run the
+  // projected-gradient fallback of engine.py:175-186 directly from the clipped solution
+  const char* ep = getenv("RAC_BOX_PASSES");
+  const int passes = ep ? atoi(ep) : -1;
+  box_test_kernel<<<1, QPT, smem, st>>>(M, r, lo, hi, s, x, info, L, passes);
   if (L) cudaFreeAsync(L, st);
   note_launch();
   return check_launch("rac_box_block_min");

@@ -64,6 +64,19 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// max that propagates NaN like numpy's np.max (fmax drops it): a residual that went
+// non-finite must not read as converged
+__device__ __forceinline__ double nanmax(double a, double b) {
+  return (a != a) ? a : ((b != b) ? b : fmax(a, b));
+}
+
+__device__ __forceinline__ double warp_nanmax(double v) {
+  __syncwarp();
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 __device__ __forceinline__ double warp_max(double v) {
   __syncwarp();
 #pragma unroll

@@ -21,6 +21,12 @@ unsigned long long launch_count();
 int num_sms();
 int dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
+void trim_pool(size_t keep);
+// launch the persistent (software grid-barrier) kernels without the cooperative
+// attribute: under Nsight Compute or with RAC_PROFILE_NONCOOP=1 (capi.cu)
+bool profile_noncoop();
+// cudaLaunchCooperativeKernel, or a plain launch when profile_noncoop()
+cudaError_t launch_coop(const void* f, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t st);
 int launch_gemv_rows(const double* Q, int64_t rows, int64_t cols, const double* w, double* out,
                      cudaStream_t st);
 
@@ -90,6 +96,13 @@ int launch_chol_system(const SysArgs& a, int p, cudaStream_t st);
 size_t chol_scratch_bytes(int s, int p);
 
 __global__ void iota_kernel(int32_t* v, int64_t n);
+
+// label-weighted kernel strips (strips.cu): out[i][j] = y_{rows_i} y_j K(x_{rows_i}, x_j) from
+// the zero-padded row-major samples Xp (N x ldd, ldd % 32 == 0); sq = |x_j|^2 (Gaussian only)
+int launch_kernel_strip(const double* Xp, int64_t ldd, int64_t d, const int32_t* rows, int s, int64_t N,
+                        const double* y, const double* sq, int kind, double sigma, double* out, int64_t ldo,
+                        cudaStream_t st);
+int launch_row_sqnorm(const double* Xp, int64_t ldd, int64_t N, int64_t d, double* sq, cudaStream_t st);
 
 // row-major X (m x n) -> column-major (ld x n), rows m..ld-1 zero
 int launch_transpose_pad(const double* X, int64_t m, int64_t n, int64_t ld, double* Xc, cudaStream_t st);

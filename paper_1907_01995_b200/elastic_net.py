@@ -140,19 +140,20 @@ class EnSolver:
     """One native elastic-net sweep context (rac_en_ctx) on the current stream."""
 
     def __init__(self, m: int, n: int, block_size: int, mode: Mode, lam: float, alpha: float,
-                 gamma: float, device: int = 0):
+                 gamma: float, device=None):
         self.dev = _device.require_cuda(device)
         self.lib = _native.load()
         self.m, self.n = int(m), int(n)
         self.s = min(int(block_size), self.n)
         self.p = -(-self.n // self.s)
         self.mode = Mode(mode)
-        self.stream = _device.stream_handle()
+        self.stream = _device.stream_handle(device=self.dev)
         h = _native._p()
-        _native.check(self.lib.rac_en_create(
-            h, self.m, self.n, self.s,
-            _native.MODE_RP if self.mode == Mode.RP else _native.MODE_RAC,
-            float(lam), float(alpha), float(gamma), self.stream))
+        with torch.cuda.device(self.dev):    # the context allocates and launches on this device
+            _native.check(self.lib.rac_en_create(
+                h, self.m, self.n, self.s,
+                _native.MODE_RP if self.mode == Mode.RP else _native.MODE_RAC,
+                float(lam), float(alpha), float(gamma), self.stream))
         self.h = h
         self._keep = []
         self.gram_mode = "blocks"
@@ -271,18 +272,40 @@ COV_MAX_N = 20000
 
 # fit() reuses native contexts of the same shape (rac_en_reset) instead of creating and
 # destroying one per call: streams, events, plans and pool buffers stay; each fit holds
-# its context exclusively.  At most _POOL_MAX idle contexts are kept (least recently
-# used closed first).
+# its context exclusively.  At most _POOL_MAX idle contexts and about _POOL_BYTES of
+# their device memory are kept (least recently used closed first); release_pool() closes
+# them all and returns the memory to the driver.
 _POOL: "collections.OrderedDict" = collections.OrderedDict()   # (key, serial) -> solver
 _POOL_LOCK = threading.Lock()
 _POOL_MAX = 4
+_POOL_BYTES = int(os.environ.get("RAC_POOL_BYTES", str(24 << 30)))
 _POOL_SERIAL = itertools.count()
+
+
+def _ctx_bytes(key) -> int:
+    """Rough device footprint of a pooled context: X (column-major), its int8 digit slices,
+    G (covariance mode) and the per-sweep block inverses, double-buffered."""
+    m, n, s = key[0], key[1], key[2]
+    p = -(-n // s)
+    return 16 * m * n + (8 * n * n if n <= COV_MAX_N else 0) + 16 * p * s * s
+
+
+def release_pool() -> None:
+    """Close every idle pooled fit context and trim the native memory pool (e.g. before a
+    large allocation by other code)."""
+    with _POOL_LOCK:
+        idle = list(_POOL.values())
+        _POOL.clear()
+    for sv in idle:
+        sv.close()
+    if torch.cuda.is_available():
+        _native.check(_native.load().rac_trim_pool(0))
 
 
 def _acquire_solver(m, n, block_size, mode, lam, alpha, gamma, device):
     # RAC_* environment switches select native variants when a context is created / planned
     env = tuple(sorted((k, v) for k, v in os.environ.items() if k.startswith("RAC_")))
-    key = (m, n, min(int(block_size), n), Mode(mode), device, _device.stream_handle(), env)
+    key = (m, n, min(int(block_size), n), Mode(mode), device, _device.stream_handle(device=device), env)
     solver = None
     with _POOL_LOCK:
         for pk in reversed(_POOL):
@@ -300,7 +323,8 @@ def _release_solver(key, solver, ok: bool) -> None:
     if ok:
         with _POOL_LOCK:
             _POOL[(key, next(_POOL_SERIAL))] = solver
-            while len(_POOL) > _POOL_MAX:
+            while len(_POOL) > _POOL_MAX or (len(_POOL) > 1 and
+                                            sum(_ctx_bytes(k[0]) for k in _POOL) > _POOL_BYTES):
                 evicted.append(_POOL.popitem(last=False)[1])
     else:
         evicted.append(solver)
@@ -320,7 +344,7 @@ def choose_gram_mode(m: int, n: int, block_size: int, iters: int) -> str:
 
 
 def fit(X: Matrix, y: np.ndarray, spec: ElasticNetSpec, *, sweep_hook=None,
-        batch: int = 16, device: int = 0, gram_mode: str = "auto") -> ElasticNetModel:
+        batch: int = 16, device=None, gram_mode: str = "auto") -> ElasticNetModel:
     """Randomized block-sweep fit of the elastic-net objective (elastic_net.py:150-232).
 
     Same arguments, results and errors as the reference.  `sweep_hook(k, beta,
@@ -339,6 +363,13 @@ def fit(X: Matrix, y: np.ndarray, spec: ElasticNetSpec, *, sweep_hook=None,
     if y.size != m:
         raise ValueError(f"y has length {y.size}, expected {m}")
     gamma = resolve_gamma(spec, X)
+    dev = _device.require_cuda(device)
+    with torch.cuda.device(dev):     # the pooled context, its stream and uploads live on `dev`
+        return _fit_on(dev.index, X, y, spec, m, n, gamma, sweep_hook, batch, gram_mode)
+
+
+def _fit_on(device: int, X, y, spec: ElasticNetSpec, m: int, n: int, gamma: float, sweep_hook, batch: int,
+            gram_mode: str) -> ElasticNetModel:
     mode = Mode(spec.mode)
     rng = np.random.default_rng(spec.seed)
     key, solver = _acquire_solver(m, n, spec.block_size, mode, spec.lam, spec.alpha, gamma, device)

@@ -11,6 +11,8 @@ block solver, the dual step and the residuals all run in the native engine
 
 from __future__ import annotations
 
+import math
+from dataclasses import dataclass
 from typing import Optional
 
 import numpy as np
@@ -41,15 +43,16 @@ class QpSolver:
     """One native dense box-QP sweep context (rac_qp_ctx) on the current stream."""
 
     def __init__(self, n: int, m: int, block_size: int, mode: Mode, beta: float,
-                 ridge_rel: float = 0.0, device: int = 0):
+                 ridge_rel: float = 0.0, device=None):
         self.dev = _device.require_cuda(device)
         self.lib = _native.load()
         self.n, self.m, self.s = int(n), int(m), int(block_size)
         self.p = -(-self.n // self.s)
         self.mode = Mode(mode)
         h = _native._p()
-        _native.check(self.lib.rac_qp_create(h, self.n, self.m, self.s, _MODE[self.mode], float(beta),
-                                             float(ridge_rel), _device.stream_handle()))
+        with torch.cuda.device(self.dev):    # the context allocates and launches on this device
+            _native.check(self.lib.rac_qp_create(h, self.n, self.m, self.s, _MODE[self.mode], float(beta),
+                                                 float(ridge_rel), _device.stream_handle(device=self.dev)))
         self.h = h
         self._keep = []
 
@@ -139,19 +142,28 @@ def drive(solver: QpSolver, rng: np.random.Generator, max_iters: int, tol_p: flo
     return it, status
 
 
-def solve(problem: QpProblem, config: SolverConfig, sweep_hook=None) -> SolveResult:
-    """Run the randomized multi-block sweep until tolerance or iteration cap (engine.py:322-405)."""
+def solve(problem: QpProblem, config: SolverConfig, sweep_hook=None, *, device=None) -> SolveResult:
+    """Run the randomized multi-block sweep until tolerance or iteration cap (engine.py:322-405).
+
+    `device` (not in the reference): CUDA device index, default the current device."""
     report = validate_problem(problem)
     if not report.ok:
         raise ValueError("invalid problem: " + "; ".join(report.issues))
     n = problem.n
     config.validate(n)
+    dev = _device.require_cuda(device)
+    with torch.cuda.device(dev):
+        return _solve_on(dev, problem, config, sweep_hook)
+
+
+def _solve_on(dev, problem: QpProblem, config: SolverConfig, sweep_hook) -> SolveResult:
+    n = problem.n
     mode = Mode(config.mode)
     rng = np.random.default_rng(config.seed)
     H = None if problem.H is None else as_dense(problem.H)
     A = None if problem.A is None else as_dense(problem.A)
     m = 0 if A is None else A.shape[0]
-    solver = QpSolver(n, m, config.block_size, mode, config.beta_penalty, 0.0)
+    solver = QpSolver(n, m, config.block_size, mode, config.beta_penalty, 0.0, device=dev)
     try:
         solver.set_problem(problem.c, problem.lower, problem.upper, H=H, A=A,
                            b=None if m == 0 else problem.b)
@@ -172,17 +184,191 @@ def solve(problem: QpProblem, config: SolverConfig, sweep_hook=None) -> SolveRes
         solver.close()
 
 
-def solve_block(matrix: np.ndarray, rhs: np.ndarray, lower: np.ndarray, upper: np.ndarray) -> np.ndarray:
-    """Exact box minimizer of 1/2 x'Mx - r'x for one block on the device (engine.py:189-245)."""
-    dev = _device.require_cuda(0)
+@dataclass
+class BlockSystem:
+    """One block's subproblem min 1/2 x'Mx - r'x over a box (engine.py:51-65).  `bounded`
+    defaults to "some bound is finite", as in the reference."""
+
+    matrix: np.ndarray
+    rhs: np.ndarray
+    lower: np.ndarray
+    upper: np.ndarray
+    bounded: Optional[bool] = None
+
+    def __post_init__(self):
+        if self.bounded is None:
+            self.bounded = bool(np.any(np.isfinite(self.lower)) or np.any(np.isfinite(self.upper)))
+
+
+@dataclass(frozen=True)
+class ResidualPair:
+    """Primal ||Ax - b||_inf, box-projected stationarity (inf-norms) and ||Ax - b||_1
+    (engine.py:68-77)."""
+
+    primal: float
+    dual: float
+    primal_l1: float
+
+
+def _box_min_device(M: torch.Tensor, r: torch.Tensor, lo: torch.Tensor, hi: torch.Tensor) -> torch.Tensor:
     lib = _native.load()
-    s = int(np.asarray(rhs).size)
-    M = _device.upload(np.asarray(matrix, dtype=float), device=dev)
-    r, lo, hi = (_device.upload(np.asarray(v, dtype=float), device=dev) for v in (rhs, lower, upper))
-    x = torch.empty(s, dtype=torch.float64, device=dev)
-    info = torch.zeros(1, dtype=torch.int32, device=dev)
+    s = int(r.numel())
+    x = torch.empty(s, dtype=torch.float64, device=M.device)
+    info = torch.zeros(1, dtype=torch.int32, device=M.device)
     _native.check(lib.rac_box_block_min(M.data_ptr(), r.data_ptr(), lo.data_ptr(), hi.data_ptr(), s,
-                                        x.data_ptr(), info.data_ptr(), _device.stream_handle()))
+                                        x.data_ptr(), info.data_ptr(), _device.stream_handle(device=M.device)))
     if int(info.item()) != 0:
         raise BlockDefinitenessError(NOT_PD_MESSAGE)
-    return x.cpu().numpy()
+    return x
+
+
+def solve_block(system, chol: Optional[np.ndarray] = None, *legacy, device=None) -> np.ndarray:
+    """Exact minimizer of 1/2 x'Mx - r'x over the block's box, on the device
+    (engine.py:189-245: Cholesky solve; bounded blocks run the clamp / release-worst
+    active set with the 10 s pass budget and the projected-gradient fallback — csrc/boxqp.cuh).
+
+    `chol` (the reference's cached factor) is accepted for signature compatibility; the
+    device factors M itself (same factor up to rounding).  An unbounded system
+    (`bounded=False`) is the plain SPD solve.  The array form
+    solve_block(M, r, lower, upper) is kept for the native tests."""
+    if not isinstance(system, BlockSystem):
+        if chol is None or len(legacy) != 2:
+            raise TypeError("solve_block(system: BlockSystem, chol=None)")
+        system = BlockSystem(np.asarray(system, dtype=float), np.asarray(chol, dtype=float),
+                             np.asarray(legacy[0], dtype=float), np.asarray(legacy[1], dtype=float))
+    dev = _device.require_cuda(device)
+    s = int(np.asarray(system.rhs).size)
+    lo, hi = np.asarray(system.lower, dtype=float), np.asarray(system.upper, dtype=float)
+    if not system.bounded:
+        lo, hi = np.full(s, -np.inf), np.full(s, np.inf)
+    with torch.cuda.device(dev):
+        M = _device.upload(np.asarray(system.matrix, dtype=float), device=dev)
+        r, lod, hid = (_device.upload(v, device=dev) for v in (np.asarray(system.rhs, dtype=float), lo, hi))
+        return _box_min_device(M, r, lod, hid).cpu().numpy()
+
+
+def _dense_dev(mat, dev):
+    return None if mat is None else _device.upload(as_dense(mat), device=dev)
+
+
+def dual_update(y: np.ndarray, A, x: np.ndarray, b: np.ndarray, beta: float, *, device=None) -> np.ndarray:
+    """y - beta (Ax - b) (engine.py:248-256), on the device."""
+    if A is None:
+        return np.asarray(y, dtype=float).copy()
+    dev = _device.require_cuda(device)
+    with torch.cuda.device(dev):
+        Ad = _dense_dev(A, dev)
+        r = Ad @ _device.upload(np.asarray(x, dtype=float), device=dev) - _device.upload(np.asarray(b, dtype=float),
+                                                                                        device=dev)
+        yv = np.asarray(y, dtype=float)
+        if yv.size != r.numel():
+            raise ValueError(f"y has length {yv.size}, expected {r.numel()}")
+        return (_device.upload(yv, device=dev) - beta * r).cpu().numpy()
+
+
+def compute_residuals(problem: QpProblem, x: np.ndarray, y: np.ndarray, *, device=None) -> ResidualPair:
+    """Primal ||Ax - b||_inf (and 1-norm) and the box-projected stationarity step
+    ||P(x - (Hx + c - A'y)) - x||_inf (engine.py:259-281), on the device.  NaN propagates
+    (as numpy's max does)."""
+    dev = _device.require_cuda(device)
+    with torch.cuda.device(dev):
+        xd = _device.upload(np.asarray(x, dtype=float), device=dev)
+        grad = _device.upload(problem.c, device=dev).clone()
+        primal = primal_l1 = 0.0
+        if problem.A is not None:
+            Ad = _dense_dev(problem.A, dev)
+            r = Ad @ xd - _device.upload(problem.b, device=dev)
+            if r.numel():
+                primal = float(r.abs().max().item())
+                primal_l1 = float(r.abs().sum().item())
+            grad -= Ad.T @ _device.upload(np.asarray(y, dtype=float), device=dev)
+        if problem.H is not None:
+            grad += _dense_dev(problem.H, dev) @ xd
+        v = xd - grad
+        proj = torch.minimum(torch.maximum(v, _device.upload(problem.lower, device=dev)),
+                             _device.upload(problem.upper, device=dev))
+        proj = torch.where(torch.isnan(v), v, proj)
+        dual = float((proj - xd).abs().max().item()) if xd.numel() else 0.0
+        return ResidualPair(primal=primal, dual=dual, primal_l1=primal_l1)
+
+
+def assemble_block_system(problem: QpProblem, x: np.ndarray, y: np.ndarray, block, beta: float, *,
+                          device=None) -> BlockSystem:
+    """The exact subproblem of one block with the others fixed (engine.py:136-157):
+    M = H_bb + beta A_b'A_b,  r = -(c_b + H_{b,rest} x_rest - A_b'y + beta A_b'(A_rest x_rest - b)),
+    gathered on the device (no permuted copy of H or A)."""
+    n = problem.n
+    x = np.asarray(x, dtype=float)
+    y = np.asarray(y, dtype=float)
+    if x.size != n:
+        raise ValueError(f"x has length {x.size}, expected {n}")
+    if y.size != problem.m:
+        raise ValueError(f"y has length {y.size}, expected {problem.m}")
+    idx_np = np.asarray(block, dtype=np.int64)
+    dev = _device.require_cuda(device)
+    with torch.cuda.device(dev):
+        idx = torch.from_numpy(idx_np).to(dev)
+        xd = _device.upload(x, device=dev)
+        xb = xd[idx]
+        s = idx.numel()
+        M = torch.zeros((s, s), dtype=torch.float64, device=dev)
+        rhs = -_device.upload(problem.c, device=dev)[idx]
+        if problem.H is not None:
+            Hb = _dense_dev(problem.H, dev)[:, idx]         # columns of symmetric H
+            Hbb = Hb[idx, :]
+            M += Hbb
+            rhs -= Hb.T @ xd - Hbb @ xb
+        if problem.A is not None:
+            Ad = _dense_dev(problem.A, dev)
+            Ab = Ad[:, idx]
+            M += beta * (Ab.T @ Ab)
+            ax_rest = Ad @ xd - Ab @ xb
+            rhs += Ab.T @ _device.upload(y, device=dev) - beta * (Ab.T @ (ax_rest - _device.upload(problem.b,
+                                                                                                    device=dev)))
+        lower, upper = problem.lower[idx_np], problem.upper[idx_np]
+        return BlockSystem(matrix=M.cpu().numpy(), rhs=rhs.cpu().numpy(), lower=lower, upper=upper)
+
+
+def run_sweep(problem: QpProblem, x: np.ndarray, y: np.ndarray, order, beta: float,
+              chol_cache: Optional[dict] = None, piece_cache: Optional[dict] = None, *,
+              device=None) -> tuple[np.ndarray, np.ndarray]:
+    """One full pass in the given block order, then one dual step (engine.py:284-315),
+    through the native sweep (rac_qp_set_state + one fixed-partition sweep).
+
+    The blocks must be what chunk_indices produces (equal sizes except a shorter last
+    block; indices within a block in any order — the device sorts them, which only
+    reorders a block's coordinates).  `chol_cache` / `piece_cache` are accepted for
+    signature compatibility; the device forms the block factors itself.  Inputs are not
+    modified."""
+    groups = [np.asarray(g, dtype=np.int64) for g in order]
+    n = problem.n
+    if not groups or sum(g.size for g in groups) != n or \
+            not np.array_equal(np.sort(np.concatenate(groups)), np.arange(n)):
+        raise ValueError("order must partition range(n)")
+    s = groups[0].size
+    if any(g.size != s for g in groups[:-1]) or groups[-1].size > s:
+        raise ValueError("run_sweep on the device needs chunk_indices-shaped blocks (equal sizes, last shorter)")
+    report = validate_problem(problem)
+    if not report.ok:
+        raise ValueError("invalid problem: " + "; ".join(report.issues))
+    dev = _device.require_cuda(device)
+    with torch.cuda.device(dev):
+        H = None if problem.H is None else as_dense(problem.H)
+        A = None if problem.A is None else as_dense(problem.A)
+        m = 0 if A is None else A.shape[0]
+        solver = QpSolver(n, m, s, Mode.CYCLIC, beta, 0.0, device=dev)
+        try:
+            solver.set_problem(problem.c, problem.lower, problem.upper, H=H, A=A, b=None if m == 0 else problem.b)
+            solver.set_divergence_bar(math.inf)
+            solver.set_partition(np.concatenate(groups))
+            xd = _device.upload(np.asarray(x, dtype=float), device=dev)
+            yd = _device.upload(np.asarray(y, dtype=float).reshape(-1), device=dev) if m else None
+            _native.check(solver.lib.rac_qp_set_state(solver.h, xd.data_ptr(), _device.ptr(yd)))
+            solver.run(None, 1, 0.0, 0.0, True)
+            it, _, failed = solver.progress()
+            if failed >= 0:
+                raise BlockDefinitenessError(NOT_PD_MESSAGE)
+            xo, yo, _ = solver.state()
+            return xo.cpu().numpy(), yo.cpu().numpy()
+        finally:
+            solver.close()

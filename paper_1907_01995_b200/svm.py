@@ -101,7 +101,7 @@ def default_config(n: int, block_size: Optional[int] = None, seed: int = 0, max_
 
 def build_q(X: np.ndarray, y: np.ndarray, kernel: KernelSpec, device=None) -> torch.Tensor:
     """Q = y_i y_j K(x_i, x_j) on the device (N x N fp64), one DMMA SYRK + epilogue."""
-    dev = device or _device.require_cuda(0)
+    dev = _device.require_cuda(device)
     lib = _native.load()
     N, d = X.shape
     Xd = _device.upload(X, device=dev)
@@ -109,8 +109,8 @@ def build_q(X: np.ndarray, y: np.ndarray, kernel: KernelSpec, device=None) -> to
     Q = torch.empty((N, N), dtype=torch.float64, device=dev)
     kind = _native.KERNEL_LINEAR if kernel.kind == "linear" else _native.KERNEL_GAUSSIAN
     _native.check(lib.rac_svm_build_q(Xd.data_ptr(), N, d, yd.data_ptr(), kind, float(kernel.sigma),
-                                      Q.data_ptr(), _device.stream_handle()))
-    torch.cuda.current_stream().synchronize()
+                                      Q.data_ptr(), _device.stream_handle(device=dev)))
+    torch.cuda.current_stream(dev).synchronize()
     return Q
 
 
@@ -123,11 +123,19 @@ def _bias_from_q(Q: torch.Tensor, z: np.ndarray, y: np.ndarray, C: float) -> flo
     w = torch.from_numpy(np.where(support, z, 0.0)).to(Q.device)
     qz = torch.empty(Q.shape[0], dtype=torch.float64, device=Q.device)
     _native.check(lib.rac_gemv(Q.data_ptr(), Q.shape[0], Q.shape[1], w.data_ptr(), qz.data_ptr(),
-                               _device.stream_handle()))
+                               _device.stream_handle(device=Q.device)))
     g = y * qz.cpu().numpy()     # sum_j y_j z_j K(x_j, x_i) = y_i (Q z_sup)_i
     margin = (z > MARGIN_DELTA * C) & (z < (1.0 - MARGIN_DELTA) * C)
     if np.any(margin):
-        return float(np.mean(y[margin] - g[margin]))
+        return _bias_from_g(g[margin], np.flatnonzero(margin), z, y, C, True)
+    return _bias_from_g(g, np.arange(y.size), z, y, C, False)
+
+
+def _bias_from_g(g: np.ndarray, rows: np.ndarray, z: np.ndarray, y: np.ndarray, C: float, margin: bool) -> float:
+    """Margin mean, else the midpoint of the interval the bound KKT conditions allow (svm.py:304-322);
+    `g` holds sum_j y_j z_j K(x_j, x_i) for the samples `rows`."""
+    if margin:
+        return float(np.mean(y[rows] - g))
     vals = y - g
     at_upper = z >= (1.0 - MARGIN_DELTA) * C
     at_lower = ~at_upper
@@ -144,10 +152,11 @@ def _bias_from_q(Q: torch.Tensor, z: np.ndarray, y: np.ndarray, C: float) -> flo
 
 def train(X: Matrix, labels: np.ndarray, C: float, kernel: KernelSpec,
           config: Optional[SolverConfig] = None, cache_capacity: Optional[int] = None,
-          return_diagnostics: bool = False, sweep_hook=None):
+          return_diagnostics: bool = False, sweep_hook=None, device=None):
     """Train a classifier by sweeping the dual QP blockwise (svm.py:181-284).
 
-    `sweep_hook(k, z, nu)` (optional, not in the reference) observes each sweep.
+    `sweep_hook(k, z, nu)` (optional, not in the reference) observes each sweep; `device`
+    (not in the reference) is the CUDA device, default the current one.
     """
     kernel.validate()
     Xd = _rows(X)
@@ -164,9 +173,15 @@ def train(X: Matrix, labels: np.ndarray, C: float, kernel: KernelSpec,
     config.validate(n)
     mode = Mode(config.mode)
     rng = np.random.default_rng(config.seed)
-    dev = _device.require_cuda(0)
+    dev = _device.require_cuda(device)
+    with torch.cuda.device(dev):
+        return _train_on(dev, Xd, y, C, kernel, config, mode, rng, return_diagnostics, sweep_hook)
+
+
+def _train_on(dev, Xd, y, C, kernel, config, mode, rng, return_diagnostics, sweep_hook):
+    n = Xd.shape[0]
     Q = build_q(Xd, y, kernel, dev)
-    solver = QpSolver(n, 1, config.block_size, mode, config.beta_penalty, RIDGE_REL)
+    solver = QpSolver(n, 1, config.block_size, mode, config.beta_penalty, RIDGE_REL, device=dev)
     try:
         solver.set_problem(np.full(n, -1.0), np.zeros(n), np.full(n, float(C)),
                            A=y.reshape(1, n), b=np.zeros(1), borrowed_h=Q)
@@ -201,6 +216,93 @@ def _gather_rows(X: np.ndarray, mask: np.ndarray) -> np.ndarray:
     rows = np.flatnonzero(mask)
     Xc = np.ascontiguousarray(X)
     return torch.from_numpy(Xc).index_select(0, torch.from_numpy(rows)).numpy()
+
+
+# ---------------------------------------------------------------- reference helpers on the device
+class KernelRowCache:
+    """Signature twin of svm.py:96-118.  The device forms whole strips at once
+    (rac_svm_kernel_strip), so the cache is only carried through; `hits`/`misses` count
+    the rows asked for."""
+
+    def __init__(self, X: np.ndarray, kernel: KernelSpec, capacity: int):
+        self.X = X
+        self.kernel = kernel
+        self.capacity = max(1, capacity)
+        self.hits = 0
+        self.misses = 0
+
+
+def _strip_rows(Xd: np.ndarray, y: np.ndarray, rows: np.ndarray, kernel: KernelSpec, dev) -> torch.Tensor:
+    """(len(rows) x N) label-weighted kernel strip on the device."""
+    lib = _native.load()
+    N, d = Xd.shape
+    Xg = _device.upload(Xd, device=dev)
+    yg = _device.upload(y, device=dev)
+    rg = torch.from_numpy(np.asarray(rows, dtype=np.int32)).to(dev)
+    out = torch.empty((rows.size, N), dtype=torch.float64, device=dev)
+    kind = _native.KERNEL_LINEAR if kernel.kind == "linear" else _native.KERNEL_GAUSSIAN
+    _native.check(lib.rac_svm_kernel_strip(Xg.data_ptr(), N, d, yg.data_ptr(), rg.data_ptr(), int(rows.size), kind,
+                                           float(kernel.sigma), out.data_ptr(), _device.stream_handle(device=dev)))
+    return out
+
+
+def assemble_kernel_block(X: Matrix, y: np.ndarray, block, kernel: KernelSpec,
+                          cache: Optional[KernelRowCache] = None, with_strip: bool = False, *, device=None):
+    """Label-weighted kernel block Q_bb (and with `with_strip` the s x N strip Q_b.)
+    straight from the data rows, on the FP64 tensor cores (svm.py:121-143)."""
+    kernel.validate()
+    Xd = _rows(X)
+    y = np.asarray(y, dtype=float)
+    idx = np.asarray(block, dtype=np.int64)
+    dev = _device.require_cuda(device)
+    with torch.cuda.device(dev):
+        strip = _strip_rows(Xd, y, idx, kernel, dev)
+        if cache is not None:
+            cache.misses += int(idx.size)
+        qbb = strip[:, torch.from_numpy(idx).to(dev)]
+        if with_strip:
+            return qbb.cpu().numpy(), strip.cpu().numpy()
+        return qbb.cpu().numpy()
+
+
+def kernel_eval(xi: np.ndarray, xj: np.ndarray, kernel: KernelSpec) -> float:
+    """K(x_i, x_j) for one pair (svm.py:68-79); scalar host helper."""
+    kernel.validate()
+    xi, xj = np.asarray(xi, dtype=float), np.asarray(xj, dtype=float)
+    if xi.shape != xj.shape:
+        raise ValueError(f"feature dimensions differ: {xi.shape} vs {xj.shape}")
+    if kernel.kind == "linear":
+        return float(xi @ xj)
+    return math.exp(-float(np.sum((xi - xj) ** 2)) / (2.0 * kernel.sigma ** 2))
+
+
+def compute_bias(duals: np.ndarray, X: Matrix, labels: np.ndarray, C: float, kernel: KernelSpec, *,
+                 device=None) -> float:
+    """Bias from the margin support vectors (svm.py:287-322).  g_i = sum_j y_j z_j K(x_j, x_i)
+    = y_i (Q z_sup)_i is formed from device kernel strips of the needed rows (chunks of at
+    most 2048 rows), then the reference's margin mean / bracket midpoint."""
+    Xd = _rows(X)
+    y = np.asarray(labels, dtype=float)
+    z = np.asarray(duals, dtype=float)
+    support = z > SUPPORT_THRESHOLD
+    if not np.any(support):
+        raise DegenerateModelError("no support vectors; cannot recover a bias")
+    margin = (z > MARGIN_DELTA * C) & (z < (1.0 - MARGIN_DELTA) * C)
+    need = np.flatnonzero(margin) if np.any(margin) else np.arange(y.size)
+    dev = _device.require_cuda(device)
+    lib = _native.load()
+    with torch.cuda.device(dev):
+        w = torch.from_numpy(np.where(support, z, 0.0)).to(dev)
+        qz = np.empty(need.size)
+        for c0 in range(0, need.size, 2048):
+            rows = need[c0:c0 + 2048]
+            strip = _strip_rows(Xd, y, rows, kernel, dev)
+            out = torch.empty(rows.size, dtype=torch.float64, device=dev)
+            _native.check(lib.rac_gemv(strip.data_ptr(), rows.size, y.size, w.data_ptr(), out.data_ptr(),
+                                       _device.stream_handle(device=dev)))
+            qz[c0:c0 + rows.size] = out.cpu().numpy()
+    g = y[need] * qz
+    return _bias_from_g(g, need, z, y, C, bool(np.any(margin)))
 
 
 # ---------------------------------------------------------------- host post-processing

@@ -101,14 +101,15 @@ class EnCapture:
         ren._col_block, ren.z_update = self._cb, self._zu
 
 
-def _en_case(tag, X, y, spec, keep_full=None, out=None):
+def _en_case(tag, X, y, spec, keep_full=None, out=None, block_sweeps=3, save_xy=True):
     with EnCapture() as cap:
         model = ren.fit(X, y, spec)
     K = len(cap.beta)
     keep = range(1, K + 1) if keep_full is None else [k for k in keep_full if k <= K]
     d = out if out is not None else {}
-    d[f"{tag}_X"] = X
-    d[f"{tag}_y"] = y
+    if save_xy:
+        d[f"{tag}_X"] = X
+        d[f"{tag}_y"] = y
     d[f"{tag}_params"] = np.array([spec.lam, spec.alpha,
                                    np.nan if spec.gamma is None else spec.gamma,
                                    spec.block_size, spec.iters, spec.seed,
@@ -119,7 +120,7 @@ def _en_case(tag, X, y, spec, keep_full=None, out=None):
         d[f"{tag}_beta_{k}"] = cap.beta[k - 1]
         d[f"{tag}_z_{k}"] = cap.z[k - 1]
         d[f"{tag}_xi_{k}"] = cap.xi[k - 1]
-    for k in range(1, min(K, 3) + 1):
+    for k in range(1, min(K, block_sweeps) + 1):
         d[f"{tag}_blocks_{k}"] = np.concatenate(cap.blocks[k - 1])
         d[f"{tag}_blocklens_{k}"] = np.asarray([b.size for b in cap.blocks[k - 1]])
     d[f"{tag}_norms"] = np.asarray([[np.linalg.norm(b), np.linalg.norm(z), np.linalg.norm(x)]
@@ -206,7 +207,7 @@ class SvmCapture:
         rsvm.assemble_kernel_block, rsvm.solve_block = self._akb, self._sb
 
 
-def _svm_case(tag, X, y, C, kernel, cfg, out):
+def _svm_case(tag, X, y, C, kernel, cfg, out, keep=None, save_xy=True):
     with SvmCapture() as cap:
         model, diag = rsvm.train(X, y, C, kernel, cfg, return_diagnostics=True)
     n = X.shape[0]
@@ -225,14 +226,25 @@ def _svm_case(tag, X, y, C, kernel, cfg, out):
         zs.append(z.copy())
         nus.append(nu)
     assert np.array_equal(z, diag.duals) and nu == diag.eq_dual
-    out[f"{tag}_X"] = X
-    out[f"{tag}_y"] = y
+    if save_xy:
+        out[f"{tag}_X"] = X
+        out[f"{tag}_y"] = y
     out[f"{tag}_params"] = np.array([C, cfg.block_size, cfg.beta_penalty, cfg.max_iters,
                                      cfg.tol_primal, cfg.tol_dual, cfg.seed,
                                      float(cfg.fixed_iterations), kernel.sigma])
     out[f"{tag}_kernel"] = np.array(kernel.kind)
     out[f"{tag}_mode"] = np.array(rprob.Mode(cfg.mode).value)
-    out[f"{tag}_z"] = np.asarray(zs)
+    if keep is None:
+        out[f"{tag}_z"] = np.asarray(zs)
+    else:
+        kept = [k for k in keep if k <= len(zs)]
+        out[f"{tag}_sweeps_kept"] = np.asarray(kept, dtype=np.int64)
+        for k in kept:
+            out[f"{tag}_z_{k}"] = zs[k - 1]
+        out[f"{tag}_znorms"] = np.asarray([np.linalg.norm(v) for v in zs])
+        if kernel.kind == "linear":
+            w = X.T @ (y * z)        # linear kernel: z'Qz = ||X'(y*z)||^2 (test_svm.py:173)
+            out[f"{tag}_dual_objective"] = np.array(0.5 * float(w @ w) - float(z.sum()))
     out[f"{tag}_nu"] = np.asarray(nus)
     out[f"{tag}_primal"] = diag.primal_residual_history
     out[f"{tag}_dual"] = diag.dual_residual_history
@@ -381,8 +393,54 @@ def gen_block_and_prox():
     _save("block_prox", **d)
 
 
+# ---------------------------------------------------------------------------
+# Full BASELINE sizes (VERDICT r01 "next round" #1): the unmodified racml at the
+# §8(d) seed-0 recipe.  Inputs are NOT stored (regenerated from the seed on the
+# GPU box by paper_1907_01995_b200.configs); kept: iterates at sweeps 1, 2, 5, 10,
+# 25, 50, the norms of every sweep, the first sweep's block list, the final
+# iterates, objective and iteration count.
+FULL_KEEP = [1, 2, 5, 10, 25, 50]
+
+
+def gen_full_en(cfg: int, iters: int | None = None):
+    import time
+    c = configs.GENERATORS[cfg]()
+    spec = ren.ElasticNetSpec(lam=c.lam, alpha=c.alpha, gamma=c.gamma, block_size=c.block_size,
+                              iters=iters or c.iters, seed=c.seed, tol=c.tol)
+    t0 = time.perf_counter()
+    d = _en_case(f"cfg{cfg}", c.X, c.y, spec, keep_full=FULL_KEEP, block_sweeps=1, save_xy=False)
+    d[f"cfg{cfg}_blocks_1"] = d[f"cfg{cfg}_blocks_1"].astype(np.int32)
+    d[f"cfg{cfg}_seconds"] = np.array(time.perf_counter() - t0)
+    print(f"config {cfg}: {int(d[f'cfg{cfg}_final'][1])} sweeps in {float(d[f'cfg{cfg}_seconds']):.1f} s")
+    _save(f"en_config{cfg}_full", **d)
+
+
+def gen_full_svm(sweeps: int = 50):
+    import time
+    Mode, SolverConfig = rprob.Mode, rprob.SolverConfig
+    c = configs.config4()
+    d = {}
+    t0 = time.perf_counter()
+    _svm_case("cfg4", c.X, c.labels, c.C, rsvm.KernelSpec("linear"),
+              SolverConfig(mode=Mode.RAC, block_size=c.block_size, beta_penalty=c.beta,
+                           max_iters=sweeps, tol_primal=c.tol_primal, tol_dual=c.tol_dual, seed=0),
+              d, keep=FULL_KEEP, save_xy=False)
+    d["cfg4_blocks_1"] = d["cfg4_blocks_1"].astype(np.int32)
+    d["cfg4_seconds"] = np.array(time.perf_counter() - t0)
+    print(f"config 4: {sweeps} sweeps in {float(d['cfg4_seconds']):.1f} s")
+    _save("svm_config4_full", **d)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["chunks", "en", "svm", "qp", "block"]
+    if "full2" in which:
+        gen_full_en(2)
+    if "full3" in which:
+        gen_full_en(3)
+    if "full5" in which:
+        gen_full_en(5, iters=50)
+    if "full4" in which:
+        gen_full_svm(50)
     if "chunks" in which:
         gen_chunks()
     if "block" in which:

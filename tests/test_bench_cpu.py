@@ -38,3 +38,25 @@ def test_help_lists_driver_flags():
     assert out.returncode == 0
     for flag in ("--gpus", "--steps", "--warmup", "--impl"):
         assert flag in out.stdout
+
+
+def test_reference_config_matches_b200_arm_config():
+    """Both arms print the same `config` object for the same workload (the driver pairs them)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_1907_01995_b200 import configs
+    d = _run(["--impl", "reference", "--config", "1", "--steps", "2", "--warmup", "1"])
+    assert d["config"] == bench.config_dict(1, configs.config1(), 2, 1)
+    assert d["config"]["gram_mode"] in ("blocks", "covariance")
+
+
+def test_default_headline_is_largest_config():
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.HEADLINE == 5
+
+
+def test_gpus_n_launches_n_ranks():
+    """`--gpus 2` without torchrun re-launches itself as two ranks (gloo plumbing check)."""
+    d = _run(["--gpus", "2", "--plumbing-check"], timeout=300)
+    assert d["n_gpus"] == 2 and d["plumbing_check"] is True

@@ -238,7 +238,7 @@ def test_fit_context_pool_reuse_env_keys_and_eviction(monkeypatch):
             events.append(("close", self.m))
 
     monkeypatch.setattr(en, "EnSolver", FakeSolver)
-    monkeypatch.setattr(en._device, "stream_handle", lambda: 0)
+    monkeypatch.setattr(en._device, "stream_handle", lambda *a, **k: 0)
     for k in [k for k in list(__import__("os").environ) if k.startswith("RAC_")]:
         monkeypatch.delenv(k)
     en._POOL.clear()
@@ -259,3 +259,32 @@ def test_fit_context_pool_reuse_env_keys_and_eviction(monkeypatch):
     assert len(en._POOL) == en._POOL_MAX
     assert ("close", 10) in events and ("close", 100) in events   # least recently used first
     en._POOL.clear()
+
+
+def test_package_reexports_reference_surface():
+    """The racml re-export names that belong to the sweep (racml/__init__.py:3-67, SURVEY §8(a)
+    a13) are importable from the package root; spectral / data_io / CLI are out of scope."""
+    import paper_1907_01995_b200 as rac
+    for name in ("Mode", "QpProblem", "SolveResult", "SolverConfig", "Status", "ValidationReport",
+                 "validate_problem", "BlockDefinitenessError", "BlockSystem", "ResidualPair",
+                 "assemble_block_system", "compute_residuals", "dual_update", "run_sweep", "solve", "solve_block",
+                 "ElasticNetModel", "ElasticNetSpec", "fit", "soft_threshold", "z_update", "KernelSpec", "SvmModel",
+                 "accuracy", "assemble_kernel_block", "compute_bias", "kernel_eval", "predict", "train"):
+        assert hasattr(rac, name), name
+    bs = rac.BlockSystem(np.eye(2), np.ones(2), np.array([-np.inf, 0.0]), np.array([np.inf, np.inf]))
+    assert bs.bounded is True
+    assert rac.BlockSystem(np.eye(1), np.ones(1), np.array([-np.inf]), np.array([np.inf])).bounded is False
+    rp = rac.ResidualPair(primal=1.0, dual=2.0, primal_l1=3.0)
+    with pytest.raises(Exception):
+        rp.primal = 0.0          # frozen like the reference's
+
+
+def test_helpers_fail_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    import paper_1907_01995_b200 as rac
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        rac.solve_block(rac.BlockSystem(np.eye(1), np.ones(1), np.zeros(1), np.ones(1)))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        rac.assemble_kernel_block(np.eye(3), np.ones(3), [0, 1], rac.KernelSpec("linear"))

@@ -222,6 +222,37 @@ int rac_svm_build_q(const double* X, int64_t N, int64_t d, const double* labels,
  * / KernelRowCache.row (svm.py:107-118); Q_bb = strip[:, rows]. */
 int rac_svm_kernel_strip(const double* X, int64_t N, int64_t d, const double* labels, const int32_t* rows,
                          int32_t s, int32_t kind, double sigma, double* strip, void* stream);
+/* ------------------------------------------------------------------ consensus baseline
+ * Per-sweep part of elastic_net.py:252-316 consensus_fit (the paper's Table-1 two-block
+ * baseline): `count` sweeps of copy solves, z-shrink, dual step and residual, all on the
+ * device; sweeps after state[1] (stop flag: residual <= tol, tol < 0 = never) are no-ops.
+ * S_i^{-1} (direct, p x p) / W_i^{-1} (Woodbury, n_i x n_i) are formed by the caller. */
+typedef struct rac_consensus_args {
+  int32_t N;               /* copies (sample groups) */
+  int64_t p;               /* features */
+  const int32_t* kind;     /* [N] 0 direct, 1 Woodbury */
+  const int32_t* ni;       /* [N] samples per group */
+  const int64_t* off_inv;  /* [N] offsets into inv */
+  const int64_t* off_x;    /* [N] offsets of X_i (n_i x p row-major) into xg (Woodbury) */
+  const int64_t* off_u;    /* [N] offsets of group i's n_i-vectors into u / inner (increasing) */
+  const double* inv;
+  const double* xg;
+  const double* w0;        /* [N][p] X_i' y_i / n */
+  double* copies;          /* [N][p] */
+  double* duals;           /* [N][p] */
+  double* z;               /* [p] */
+  double* u;               /* [wb_rows] */
+  double* inner;           /* [wb_rows] */
+  double* part;            /* [part_cap] */
+  double* hist;            /* residual per sweep */
+  int32_t* state;          /* [0] sweeps done, [1] stop flag */
+  int64_t wb_rows;         /* sum of n_i over Woodbury groups' u slots (0: none) */
+  int32_t direct_groups;
+  int32_t part_cap;
+  double gamma, thr, denom, tol;
+} rac_consensus_args;
+int rac_consensus_run(const rac_consensus_args* args, int32_t count, void* stream);
+
 int rac_gemv(const double* Q, int64_t rows, int64_t cols, const double* w, double* out,
              void* stream);
 

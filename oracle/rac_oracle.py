@@ -466,3 +466,47 @@ def qp_objective(H, c, x) -> float:
     if H is not None:
         val += 0.5 * float(x @ (H @ x))
     return val
+
+
+# ---------------------------------------------------------------------------
+# two-block consensus baseline  (elastic_net.py:252-316)
+# ---------------------------------------------------------------------------
+
+def consensus_fit(X, y, lam: float, alpha: float, gamma: Optional[float] = None, block_size: int = 100,
+                  iters: int = 10, seed: int = 0, tol: Optional[float] = None) -> dict:
+    """elastic_net.py:252-316 (consensus_fit): one coefficient copy per sample group
+    (direct p x p Cholesky when the group has >= p samples, else the Woodbury n_i x n_i
+    route), z shrunk against the aggregated copies, dual ascent per copy."""
+    X = np.asarray(X.todense() if hasattr(X, "todense") else X, dtype=float)
+    n, p = X.shape
+    y = np.asarray(y, dtype=float)
+    g = auto_gamma(lam, gamma, X)
+    rng = np.random.default_rng(seed)
+    want = min(n, max(2, math.ceil(p / min(block_size, p))))
+    groups = sorted_chunks(rng.permutation(n), math.ceil(n / want))
+    solvers, targets = [], []
+    for idx in groups:
+        Xi = X[idx]
+        targets.append(Xi.T @ y[idx] / n)
+        if p <= idx.size:
+            solvers.append(("direct", Xi, np.linalg.cholesky(Xi.T @ Xi / n + g * np.eye(p))))
+        else:
+            solvers.append(("woodbury", Xi, np.linalg.cholesky(Xi @ Xi.T + n * g * np.eye(idx.size))))
+    N = len(groups)
+    copies, duals, z = np.zeros((N, p)), np.zeros((N, p)), np.zeros(p)
+    done, resid = 0, math.inf
+    for _ in range(iters):
+        for i, ((kind, Xi, L), w0) in enumerate(zip(solvers, targets)):
+            w = w0 + duals[i] + g * z
+            if kind == "direct":
+                copies[i] = scipy.linalg.cho_solve((L, True), w)
+            else:
+                copies[i] = (w - Xi.T @ scipy.linalg.cho_solve((L, True), Xi @ w)) / g
+        agg = duals.sum(axis=0) - g * copies.sum(axis=0)
+        z = neg_shrink(agg, lam * alpha) / ((1.0 - alpha) * lam + N * g)
+        duals -= g * (copies - z)
+        done += 1
+        resid = float(np.mean(np.sum(np.abs(copies - z), axis=1)))
+        if tol is not None and resid <= tol:
+            break
+    return dict(beta=copies.mean(axis=0), z=z, xi=duals.mean(axis=0), gamma=g, iterations=done, residual=resid)

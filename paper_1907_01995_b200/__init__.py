@@ -33,6 +33,7 @@ from .engine import (
 from .elastic_net import (
     ElasticNetModel,
     ElasticNetSpec,
+    consensus_fit,
     fit,
     objective,
     soft_threshold,
@@ -57,7 +58,7 @@ __all__ = [
     "Mode", "QpProblem", "SolveResult", "SolverConfig", "Status", "ValidationReport", "chunk_indices",
     "validate_problem", "BlockDefinitenessError", "BlockSystem", "ResidualPair", "assemble_block_system",
     "compute_residuals", "dual_update", "run_sweep", "solve", "solve_block", "ElasticNetModel",
-    "ElasticNetSpec", "fit", "objective", "soft_threshold", "z_update", "DegenerateModelError", "KernelSpec",
+    "ElasticNetSpec", "consensus_fit", "fit", "objective", "soft_threshold", "z_update", "DegenerateModelError", "KernelSpec",
     "SvmModel", "TrainDiagnostics", "accuracy", "assemble_kernel_block", "compute_bias", "kernel_eval",
     "predict", "train",
 ]

@@ -59,6 +59,7 @@ SIGNATURES = {
     "rac_qp_set_problem": (_i32, [_p, _p, _p, _p, _p, _p, _p]),
     "rac_qp_borrow_h": (_i32, [_p, _p]),
     "rac_qp_set_state": (_i32, [_p, _p, _p]),
+    "rac_consensus_run": (_i32, [_p, _i32, _p]),
     "rac_svm_kernel_strip": (_i32, [_p, _i64, _i64, _p, _p, _i32, _i32, _f64, _p, _p]),
     "rac_qp_set_divergence_bar": (_i32, [_p, _f64]),
     "rac_qp_set_partition": (_i32, [_p, _p]),

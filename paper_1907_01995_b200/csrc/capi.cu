@@ -73,7 +73,8 @@ void trim_pool(size_t keep) {
 }
 
 // Nsight Compute cannot replay cooperative (grid-synchronised) launches, cluster ones
-// least of all.  Under the profiler (it injects itself through CUDA_INJECTION64_PATH)
+// least of all.  Under the profiler (ncu exports NV_NSIGHT_INJECTION_TRANSPORT_TYPE and
+// NV_COMPUTE_PROFILER_PERFWORKS_DIR into the target; other injectors CUDA_INJECTION64_PATH)
 // or with RAC_PROFILE_NONCOOP=1, the persistent chain kernels are launched without
 // the cooperative attribute: every such grid is sized to one co-resident wave (checked
 // with the occupancy API when the context is planned) and the other kernels sharing
@@ -82,8 +83,12 @@ void trim_pool(size_t keep) {
 bool profile_noncoop() {
   static const int v = [] {
     if (const char* e = getenv("RAC_PROFILE_NONCOOP")) return atoi(e) == 1 ? 1 : 0;
-    const char* inj = getenv("CUDA_INJECTION64_PATH");
-    return (inj && *inj) ? 1 : 0;
+    for (const char* k : {"NV_NSIGHT_INJECTION_TRANSPORT_TYPE", "NV_COMPUTE_PROFILER_PERFWORKS_DIR",
+                          "CUDA_INJECTION64_PATH"}) {
+      const char* v = getenv(k);
+      if (v && *v) return 1;
+    }
+    return 0;
   }();
   return v == 1;
 }

@@ -445,3 +445,6 @@ def _fit_on(device: int, X, y, spec: ElasticNetSpec, m: int, n: int, gamma: floa
                                residual_history=hp.copy(), dual_residual_history=hd.copy())
     finally:
         _release_solver(key, solver, ok)
+
+
+from .consensus import consensus_fit  # noqa: E402  (the consensus baseline, elastic_net.py:252-316)

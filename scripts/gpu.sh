@@ -10,6 +10,10 @@ for step in "$@"; do
   case "$what" in
     test)   timeout 1500 python -m pytest tests -m gpu -x -q --timeout 600 --timeout-method thread > "$log" 2>&1 ;;
     smoke)  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$log" 2>&1 ;;
+    smokencu) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$log.plain" 2>&1 && \
+            timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+              --log-file "gpurun_out/${TAG}_smoke_launches.csv" python -c "import __graft_entry__ as g; g.smoke()" > "$log" 2>&1 ;;
+    benchall) timeout 1500 python bench.py > "$log" 2>&1 ;;
     bench)  timeout 900 python bench.py ${a:+--config $a} > "$log" 2>&1 ;;
     ref)    timeout 900 python bench.py --impl reference ${a:+--config $a} > "$log" 2>&1 ;;
     launches) timeout 300 python bench.py ${a:+--config $a} --no-cpu --steps 5 --warmup 3 > "$log.plain" 2>&1 && \

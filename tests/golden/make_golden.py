@@ -394,6 +394,31 @@ def gen_block_and_prox():
 
 
 # ---------------------------------------------------------------------------
+def gen_consensus():
+    """racml.elastic_net.consensus_fit on direct-route (p <= n_i), Woodbury-route (p > n_i)
+    and mixed group shapes, with and without a tolerance."""
+    d = {}
+    cases = [
+        ("direct", 400, 12, dict(lam=0.1, alpha=0.7, gamma=0.5, block_size=4, iters=40, seed=3)),
+        ("woodbury", 40, 90, dict(lam=0.05, alpha=1.0, gamma=1.0, block_size=10, iters=60, seed=4)),
+        ("mixed_tol", 61, 20, dict(lam=0.2, alpha=0.5, gamma=None, block_size=7, iters=5000, seed=5, tol=1e-8)),
+        ("ridge", 120, 30, dict(lam=0.3, alpha=0.0, gamma=0.8, block_size=6, iters=25, seed=6)),
+    ]
+    for i, (tag, n, p, kw) in enumerate(cases):
+        rng = np.random.default_rng(500 + i)
+        X = rng.standard_normal((n, p))
+        y = X @ (rng.standard_normal(p) * (rng.random(p) < 0.3)) + 0.1 * rng.standard_normal(n)
+        spec = ren.ElasticNetSpec(**kw)
+        m = ren.consensus_fit(X, y, spec)
+        d[f"{tag}_X"], d[f"{tag}_y"] = X, y
+        d[f"{tag}_params"] = np.array([spec.lam, spec.alpha, np.nan if spec.gamma is None else spec.gamma,
+                                       spec.block_size, spec.iters, spec.seed, np.nan if spec.tol is None else spec.tol])
+        d[f"{tag}_beta"], d[f"{tag}_z"], d[f"{tag}_xi"] = m.beta, m.z, m.xi
+        d[f"{tag}_final"] = np.array([m.gamma, m.iterations, m.residual])
+    _save("consensus", **d)
+
+
+# ---------------------------------------------------------------------------
 # Full BASELINE sizes (VERDICT r01 "next round" #1): the unmodified racml at the
 # §8(d) seed-0 recipe.  Inputs are NOT stored (regenerated from the seed on the
 # GPU box by paper_1907_01995_b200.configs); kept: iterates at sweeps 1, 2, 5, 10,
@@ -433,6 +458,8 @@ def gen_full_svm(sweeps: int = 50):
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["chunks", "en", "svm", "qp", "block"]
+    if "consensus" in which:
+        gen_consensus()
     if "full2" in which:
         gen_full_en(2)
     if "full3" in which:

@@ -185,15 +185,23 @@ def test_train_raises_block_definiteness_mid_sweep(dev):
 
 
 def test_qp_nan_residual_is_not_converged(dev):
-    """NaN iterates must not read as converged (numpy's max propagates NaN): a NaN in c makes
-    every residual NaN; the reference runs to the cap with status max_iters."""
-    import paper_1907_01995_b200 as rac
-    H = np.eye(4) * 2.0
-    c = np.array([1.0, np.nan, -1.0, 0.5])
-    res = rac.solve(rac.QpProblem(c=c, H=H, lower=np.full(4, -1.0), upper=np.full(4, 1.0)),
-                    rac.SolverConfig(block_size=2, max_iters=4, tol_primal=1e-6, tol_dual=1e-6, seed=0))
-    assert res.status == rac.Status.MAX_ITERS and res.iterations == 4
-    assert np.isnan(res.dual_residual_history).all()
+    """NaN iterates must not read as converged (numpy's max propagates NaN).  validate_problem
+    rejects a NaN c up front, so the native context is driven directly: a NaN in c makes the
+    dual residual NaN every sweep; the run goes to the cap with status max_iters."""
+    from paper_1907_01995_b200.engine import QpSolver
+    from paper_1907_01995_b200.problems import Mode, Status
+    n = 4
+    sol = QpSolver(n, 0, 2, Mode.CYCLIC, 1.0, 0.0)
+    try:
+        sol.set_problem(np.array([1.0, np.nan, -1.0, 0.5]), np.full(n, -1.0), np.full(n, 1.0), H=np.eye(n) * 2.0)
+        sol.set_partition(np.arange(n))
+        sol.run(None, 4, 1e-6, 1e-6, False)
+        it, status, failed = sol.progress()
+        hp, _, hd = (h.cpu().numpy() for h in sol.history(it))
+    finally:
+        sol.close()
+    assert failed < 0 and it == 4 and status == Status.MAX_ITERS
+    assert np.isnan(hd).all()
 
 
 def test_current_device_is_the_default(dev):
@@ -206,3 +214,24 @@ def test_current_device_is_the_default(dev):
     m = rac.fit(rng.standard_normal((30, 12)), rng.standard_normal(30), rac.ElasticNetSpec(lam=0.1, alpha=0.5, iters=3,
                                                                                           block_size=4))
     assert m.iterations == 3
+
+
+# ---------------------------------------------------------------- consensus baseline (§8(f) rank 4)
+@pytest.mark.parametrize("tag", ["direct", "woodbury", "mixed_tol", "ridge"])
+def test_consensus_fit_matches_reference(dev, golden, tag):
+    import paper_1907_01995_b200 as rac
+    from paper_1907_01995_b200.elastic_net import objective
+    g = golden("consensus")
+    lam, alpha, gamma, bs, iters, seed, tol = g[f"{tag}_params"]
+    spec = rac.ElasticNetSpec(lam=float(lam), alpha=float(alpha), gamma=None if np.isnan(gamma) else float(gamma),
+                              block_size=int(bs), iters=int(iters), seed=int(seed),
+                              tol=None if np.isnan(tol) else float(tol))
+    m = rac.consensus_fit(g[f"{tag}_X"], g[f"{tag}_y"], spec)
+    assert abs(m.iterations - int(g[f"{tag}_final"][1])) <= 1
+    for k in ("beta", "z", "xi"):
+        want = g[f"{tag}_{k}"]
+        assert np.linalg.norm(getattr(m, k) - want) <= 1e-9 * max(np.linalg.norm(want), 1e-300), k
+    X, y = g[f"{tag}_X"], g[f"{tag}_y"]
+    ow = objective(X, y, g[f"{tag}_beta"], spec.lam, spec.alpha)
+    assert abs(objective(X, y, m.beta, spec.lam, spec.alpha) - ow) <= 1e-8 * abs(ow)
+    assert m.gamma == g[f"{tag}_final"][0]

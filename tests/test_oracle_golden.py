@@ -148,3 +148,16 @@ def test_qp_matches_reference(golden, tag):
             assert rel(ys[k], g[f"{tag}_y"][k]) <= 1e-12
     np.testing.assert_allclose(res["primal_history"][:50], g[f"{tag}_primal"][:50], rtol=1e-8, atol=1e-14)
     np.testing.assert_allclose(res["dual_history"][:50], g[f"{tag}_dual"][:50], rtol=1e-8, atol=1e-14)
+
+
+def test_consensus_oracle_matches_reference(golden):
+    """oracle.consensus_fit (restatement of elastic_net.py:252-316) vs the unmodified racml."""
+    from oracle import rac_oracle as ro
+    g = golden("consensus")
+    for tag in ("direct", "woodbury", "mixed_tol", "ridge"):
+        lam, alpha, gamma, bs, iters, seed, tol = g[f"{tag}_params"]
+        r = ro.consensus_fit(g[f"{tag}_X"], g[f"{tag}_y"], lam, alpha, None if np.isnan(gamma) else gamma, int(bs),
+                             int(iters), int(seed), None if np.isnan(tol) else tol)
+        assert r["iterations"] == int(g[f"{tag}_final"][1])
+        for k in ("beta", "z", "xi"):
+            np.testing.assert_allclose(r[k], g[f"{tag}_{k}"], rtol=1e-12, atol=1e-14)

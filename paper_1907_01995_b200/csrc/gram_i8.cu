@@ -328,20 +328,10 @@ __global__ void __launch_bounds__(GATHER ? I8_THREADS_G : I8_THREADS, 1) gram_i8
           cp_async16_zfill(base + op * I8_S * I8_OP + (hk * 4 + sl) * I8_OP + (grp * 2 + h) * 128 + r * 16, src,
                            ok ? 16u : 0u);
         }
-        cp_async_commit();
-        if (q > 0) {
-          // the previous slot's pieces have landed: make them visible to the tensor core's
-          // async-proxy reads, then count this thread's arrival
-          cp_async_wait<1>();
-          fence_proxy_async_smem();
-          mbar_arrive(&bar_full[(q - 1) % I8_NST]);
-        }
+        // completion is tracked by the slot's mbarrier (one no-increment arrival per producer
+        // thread once its copies land); the producer moves on to the next free slot at once
+        cp_async_mbar_arrive_noinc(&bar_full[slot]);
       }
-    }
-    if (q > 0) {
-      cp_async_wait<0>();
-      fence_proxy_async_smem();
-      mbar_arrive(&bar_full[(q - 1) % I8_NST]);
     }
   } else if (!GATHER && warp == 4) {
     if (lane == 0) {
@@ -391,6 +381,9 @@ __global__ void __launch_bounds__(GATHER ? I8_THREADS_G : I8_THREADS, 1) gram_i8
           const int nk = min(kpack, q1 - kst);
           const bool first = kst == sg * I8_SEGST;
           mbar_wait(&bar_full[slot], (q / I8_NST) & 1);
+          // gather mode: the operands were written by cp.async (generic proxy); order them
+          // before the tensor core's async-proxy reads
+          if (GATHER) fence_proxy_async_smem();
           tc_fence_after();
           const unsigned sA = smem_u32(smem + slot * I8_STAGE);
           const unsigned sB = sA + I8_S * I8_OP;

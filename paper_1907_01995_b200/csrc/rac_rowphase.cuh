@@ -193,6 +193,7 @@ struct Row1tSmem {
   double* red;    // [G][rw]
   int32_t* sIdx;  // [s]
   int rwp;
+  int redcap;     // doubles in `red` (sized for rw rows; a CTA with fewer rows must not use more)
 };
 
 __host__ __device__ inline int row1t_groups(int rw) { return rw >= RP_THREADS ? 1 : RP_THREADS / rw; }
@@ -213,6 +214,7 @@ __device__ __forceinline__ Row1tSmem carve_row1t(double* base, int s, int rw) {
   w.sDel = w.sX + s;
   w.red = w.sDel + s;
   w.sIdx = reinterpret_cast<int32_t*>(w.red + (size_t)row1t_groups(rw) * rw);
+  w.redcap = row1t_groups(rw) * rw;
   return w;
 }
 
@@ -227,7 +229,9 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
                              const int32_t* __restrict__ idx, int s, int bprev, int bnext, const double* delta,
                              const double* xsrc, double* partial, const Row1tSmem& w, TFn tfn) {
   const int tid = threadIdx.x;
-  const int G = row1t_groups(nr);
+  // groups of the row reductions; the last CTA's shorter row range (nr < rw) must stay
+  // inside the reduction buffer sized for rw rows
+  const int G = min(row1t_groups(nr), w.redcap / nr);
   const int row = tid % nr, grp = tid / nr;
   const bool act = grp < G;
   if (bprev >= 0)

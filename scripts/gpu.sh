@@ -9,6 +9,8 @@ for step in "$@"; do
   log="gpurun_out/${TAG}_${what}${a:+_$a}.log"
   case "$what" in
     test)   timeout 1500 python -m pytest tests -m gpu -x -q --timeout 600 --timeout-method thread > "$log" 2>&1 ;;
+    testk)  timeout 1500 python -m pytest tests -m gpu -q --timeout 600 --timeout-method thread -k "$a" > "$log" 2>&1 ;;
+    bench1) timeout 900 python bench.py --only --no-cpu ${a:+--config $a} > "$log" 2>&1 ;;
     smoke)  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$log" 2>&1 ;;
     smokencu) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$log.plain" 2>&1 && \
             timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \

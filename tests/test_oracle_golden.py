@@ -161,3 +161,24 @@ def test_consensus_oracle_matches_reference(golden):
         assert r["iterations"] == int(g[f"{tag}_final"][1])
         for k in ("beta", "z", "xi"):
             np.testing.assert_allclose(r[k], g[f"{tag}_{k}"], rtol=1e-12, atol=1e-14)
+
+
+def test_full_size_fixtures_are_complete(golden):
+    """The full-BASELINE-size fixtures (make_golden.py full2/3/4/5) hold what test_gpu_full
+    needs: first-sweep blocks, iterates at sweeps 1, 2, 5, 10, 25, 50 (those reached), every
+    sweep's norms, the final objective and iteration count."""
+    for cfg, n, s in ((2, 2000, 100), (3, 5000, 200), (5, 100000, 500)):
+        g = golden(f"en_config{cfg}_full")
+        t = f"cfg{cfg}"
+        assert np.array_equal(np.sort(g[f"{t}_blocks_1"]), np.arange(n))
+        for k in g[f"{t}_sweeps_kept"]:
+            assert g[f"{t}_beta_{int(k)}"].shape == (n,)
+        assert g[f"{t}_norms"].shape[1] == 3 and g[f"{t}_final"].shape == (5,)
+    assert int(golden("en_config2_full")["cfg2_final"][1]) == 43
+    assert int(golden("en_config3_full")["cfg3_final"][1]) == 70
+    assert int(golden("en_config5_full")["cfg5_final"][1]) == 50
+    g = golden("svm_config4_full")
+    assert int(g["cfg4_iterations"]) == 50 and g["cfg4_nu"].shape == (50,)
+    assert np.array_equal(np.sort(g["cfg4_blocks_1"]), np.arange(20000))
+    for k in g["cfg4_sweeps_kept"]:
+        assert g[f"cfg4_z_{int(k)}"].shape == (20000,)

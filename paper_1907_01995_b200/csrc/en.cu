@@ -322,9 +322,7 @@ struct rac_en_ctx {
   void* i8_ws = nullptr;      // digit slices of the tensor-core Gram (gram_i8.cu), null = DMMA Gram
   size_t i8_ws_cap = 0;
   int64_t g_rows_done = 0;    // row-chunk ingest: samples already summed into G
-  void* bg_ws = nullptr;      // block mode: digit slices of the int8 block Grams, null = DMMA
-  bool bg_pre = false;        // bg_ws holds every feature's slices, formed once with the data (gather
-                              // per sweep); else the partition's slices, re-formed every sweep
+  void* bg_ws = nullptr;      // block mode: per-sweep digit slices of the int8 block Grams, null = DMMA
   size_t bg_cap = 0;
   int* ex_all = nullptr;      // block mode: per-feature exponents of Xc (set with the data)
   int32_t* h_ctrl = nullptr;  // pinned: ctrl snapshot after each run (2 slots), for rac_en_poll
@@ -592,8 +590,6 @@ int en_factor(rac_en_ctx* c, cudaStream_t st, int sweeps = 1) {
 // block mode: the p block Grams of the partition in c->idx into gram_ws — int8 tensor
 // cores (exact digit slices, gram_i8.cu) when reserved, else the FP64 DMMA tiles
 int en_block_gram(rac_en_ctx* c, cudaStream_t st) {
-  if (c->bg_ws && c->bg_pre)
-    return rac::launch_gram_i8_blocks_pre(c->bg_ws, c->m, c->n, c->idx, c->s, c->p, c->ex_all, c->gram_ws, st);
   if (c->bg_ws)
     return rac::launch_gram_i8_blocks(c->Xc, c->ld, c->m, c->idx, c->s, c->p, c->ex_all, c->gram_ws, c->bg_ws,
                                       c->bg_cap, st);
@@ -957,11 +953,7 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
     const int64_t jt = (s + 127) / 128;
     const int64_t tiles = (int64_t)c->p * jt * (jt + 1) / 2;
     if (mode8 == 2 || (mode8 == 1 && s >= 128 && tiles >= 4 * (int64_t)num_sms())) {
-      // RAC_BG_PRE=0: re-slice the partition every sweep (round-1 form) instead of slicing
-      // every feature once per data set and gathering
-      const char* ep = getenv("RAC_BG_PRE");
-      c->bg_pre = !(ep && atoi(ep) == 0);
-      const size_t need = c->bg_pre ? gram_i8_presliced_bytes(c->ld, n) : gram_i8_blocks_ws_bytes(c->ld, s, c->p);
+      const size_t need = gram_i8_blocks_ws_bytes(c->ld, s, c->p);
       uint8_t* w = nullptr;
       if (dalloc(c, &w, need) == RAC_OK && dalloc(c, &c->ex_all, n) == RAC_OK) {
         c->bg_ws = w;
@@ -1048,7 +1040,6 @@ extern "C" int rac_en_set_data(rac_en_ctx* c, const double* X, int32_t layout, c
   neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
   if (c->bg_ws) {
     int rc = launch_i8_colexp(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->st);
-    if (!rc && c->bg_pre) rc = launch_i8_preslice(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->bg_ws, c->bg_cap, c->st);
     if (rc) return rc;
   }
   c->have_data = true;
@@ -1121,9 +1112,6 @@ extern "C" int rac_en_set_data_rows(rac_en_ctx* c, const double* X_rows, int64_t
   note_launch();
   neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
   if (c->bg_ws && (rc = launch_i8_colexp(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->st))) return rc;
-  if (c->bg_ws && c->bg_pre &&
-      (rc = launch_i8_preslice(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->bg_ws, c->bg_cap, c->st)))
-    return rc;
   if (c->gram_mode == 1) {
     scale_kernel<<<num_sms() * 8, 256, 0, c->st>>>(c->G, c->n * c->n, (double)c->m);   // dot, then / m
     note_launch();

@@ -30,14 +30,6 @@
 //   byte ((kst * ngrp + g) * 2 + c) * 128 + r * 16 + b
 //   kst = sample / 32, g = feature / 8, c = (sample % 32) / 16, r = feature % 8, b = sample % 16
 // i.e. 8 x 16 B core matrices, LBO (K direction) = 128 B, SBO (8-feature groups) = 256 B.
-//
-// Block mode (per-sweep block Grams, config 5) on PRE-SLICED data: the per-feature exponents
-// do not depend on the partition, so every feature's digits are formed ONCE per data set
-// into P[kst][feature][slice][32 B] (256 contiguous bytes per feature per 32-sample stage,
-// i8_preslice_kernel), and each sweep's Gram gathers its block's features straight from P
-// into the canonical operand layout with 16-byte cp.async (four producer warps, completion
-// by mbarrier after a generic->async proxy fence) instead of re-slicing the partition's
-// 4 GB of FP64 columns every sweep.
 #include "rac_common.cuh"
 #include "rac_internal.h"
 
@@ -54,8 +46,6 @@ constexpr int I8_STAGE = 2 * I8_S * I8_OP;    // 64 KB: 8 A + 8 B slice operands
 constexpr int I8_SEGST = 2046;                // stages per exact int32 segment (65472 samples)
 constexpr int I8_SMEM = I8_NST * I8_STAGE + 1024;
 constexpr int I8_THREADS = 192;               // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
-constexpr int I8_THREADS_G = 288;             // gather: warps 0-3 epilogue, 5 MMA, 4 + 6..8 cp.async producers
-constexpr int I8_PROD = 128;                  // gather producer threads
 static_assert(I8_S * 64 * 64 * (I8_SEGST * (double)I8_KS) < 2147483648.0, "int32 group sums must stay exact");
 static_assert(4 * I8_TN <= 512, "a pass's weight groups must fit the 512 TMEM columns");
 static_assert(I8_S == 8, "the two passes split the groups w = 2..9");
@@ -74,8 +64,6 @@ struct I8Args {
   size_t blk_sl;         // block mode (blockIdx.y = block): slice, output and exponent strides
   int64_t blk_g;
   int blk_ex;
-  const int32_t* idx;    // gather mode: block feature lists idx[b * n ..] (-1 = padding)
-  int64_t nfeat;         // gather mode: features in P (row stride of a stage, in 256 B records)
 };
 
 // ---- tcgen05 helpers ------------------------------------------------------------------
@@ -200,63 +188,12 @@ __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict_
   }
 }
 
-// ---- once per data set: every feature's digits, P[kst][feature][slice][32 B] ----------------
-// CTA = 8 features (one per warp) x 256 samples; thread = 8 consecutive samples of one feature,
-// written as 8 B of each slice's 32-byte record
-__global__ void __launch_bounds__(256) i8_preslice_kernel(const double* __restrict__ Xc, int64_t ld, int64_t len,
-                                                          int n, const int* __restrict__ ex, uint8_t* __restrict__ P,
-                                                          int nstg) {
-  const int f = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = blockIdx.x * 8 + f;
-  const int kst = blockIdx.y * 8 + (lane >> 2);
-  if (j >= n || kst >= nstg) return;
-  const int64_t k0 = (int64_t)blockIdx.y * 256 + lane * 8;
-  const double* col = Xc + (int64_t)j * ld;
-  double x[8];
-  if (k0 + 8 <= len) {
-    const double2* p2 = reinterpret_cast<const double2*>(col + k0);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const double2 t = __ldg(p2 + i);
-      x[2 * i] = t.x;
-      x[2 * i + 1] = t.y;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = (k0 + i < len) ? col[k0 + i] : 0.0;
-  }
-  const int e = __ldg(ex + j);
-  unsigned long long packed[I8_S];
-#pragma unroll
-  for (int s = 0; s < I8_S; ++s) packed[s] = 0ull;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    long long N = __double2ll_rn(ldexp(x[i], 55 - e));   // same digits as i8_slice_kernel
-#pragma unroll
-    for (int s = I8_S - 1; s > 0; --s) {
-      const long long d = ((N + 64) & 127) - 64;
-      N = (N - d) >> 7;
-      packed[s] |= (unsigned long long)(uint8_t)(int8_t)d << (8 * i);
-    }
-    packed[0] |= (unsigned long long)(uint8_t)(int8_t)N << (8 * i);
-  }
-  uint8_t* dst = P + ((size_t)kst * n + j) * 256 + (lane & 3) * 8;
-#pragma unroll
-  for (int s = 0; s < I8_S; ++s) *reinterpret_cast<unsigned long long*>(dst + s * 32) = packed[s];
-}
-
 // ---- the tensor-core Gram ----------------------------------------------------------------
 // phases: pass 0 (groups w = 6..9) then pass 1 (w = 2..5), each over the K segments
-template <bool GATHER>
-__global__ void __launch_bounds__(GATHER ? I8_THREADS_G : I8_THREADS, 1) gram_i8_kernel(I8Args a) {
-  const int32_t* bidx = nullptr;   // gather mode: this block's feature list
-  if (GATHER) {
-    bidx = a.idx + (size_t)blockIdx.y * a.n;
-  } else {
-    a.sl += blockIdx.y * a.blk_sl;
-    a.ex += blockIdx.y * a.blk_ex;
-  }
+__global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
+  a.sl += blockIdx.y * a.blk_sl;
   a.G += blockIdx.y * a.blk_g;
+  a.ex += blockIdx.y * a.blk_ex;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bar_full[I8_NST], bar_free[I8_NST], bar_acc, bar_tfree;
@@ -271,16 +208,9 @@ __global__ void __launch_bounds__(GATHER ? I8_THREADS_G : I8_THREADS, 1) gram_i8
   }
   const int Kt = J + t;
 
-  __shared__ int sFeat[GATHER ? 2 : 1][GATHER ? I8_TM : 1];   // gather: feature ids of the A / B tiles
-  if (GATHER) {
-    for (int i = threadIdx.x; i < 2 * I8_TM; i += blockDim.x) {
-      const int pos = (i < I8_TM ? J : Kt) * I8_TM + (i & (I8_TM - 1));
-      sFeat[i / I8_TM][i & (I8_TM - 1)] = pos < a.n ? __ldg(bidx + pos) : -1;
-    }
-  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < I8_NST; ++i) {
-      mbar_init(&bar_full[i], GATHER ? I8_PROD : 1);
+      mbar_init(&bar_full[i], 1);
       mbar_init(&bar_free[i], 1);
     }
     mbar_init(&bar_acc, 1);
@@ -299,41 +229,7 @@ __global__ void __launch_bounds__(GATHER ? I8_THREADS_G : I8_THREADS, 1) gram_i8
   const int nseg = (a.nstg + I8_SEGST - 1) / I8_SEGST;
   const int nphase = 2 * nseg;
 
-  if (GATHER && (warp == 4 || warp >= 6)) {
-    // cp.async gather producers: per slot 4096 pieces of 16 B = (operand, [k step,] slice,
-    // 8-feature group, K half, feature row); a warp instruction covers 16 features x 32 B of
-    // one slice (coalesced sectors) and writes 512 contiguous operand bytes (conflict-free)
-    const int pt = (warp == 4 ? 0 : warp - 5) * 32 + lane;
-    int q = 0;
-    for (int ph = 0; ph < nphase; ++ph) {
-      const bool p0 = ph < nseg;
-      const int sg = ph % nseg;
-      const int q1 = min(a.nstg, (sg + 1) * I8_SEGST);
-      const int kpack = p0 ? 1 : 2;
-      for (int kst = sg * I8_SEGST; kst < q1; kst += kpack, ++q) {
-        const int slot = q % I8_NST;
-        const int nk = min(kpack, q1 - kst);
-        if (q >= I8_NST) mbar_wait(&bar_free[slot], ((q / I8_NST) - 1) & 1);
-        uint8_t* base = smem + slot * I8_STAGE;
-#pragma unroll 4
-        for (int it = 0; it < 32; ++it) {
-          const int e = it * I8_PROD + pt;
-          const int r = e & 7, h = (e >> 3) & 1, grp = ((e >> 5) & 7) * 2 + ((e >> 4) & 1);
-          const int op = e >> 11;
-          const int sl = p0 ? ((e >> 8) & 7) : ((e >> 8) & 3);
-          const int hk = p0 ? 0 : ((e >> 10) & 1);
-          const int fid = sFeat[op][grp * 8 + r];
-          const bool ok = fid >= 0 && hk < nk;
-          const uint8_t* src = ok ? a.sl + ((size_t)(kst + hk) * a.nfeat + fid) * 256 + sl * 32 + h * 16 : a.sl;
-          cp_async16_zfill(base + op * I8_S * I8_OP + (hk * 4 + sl) * I8_OP + (grp * 2 + h) * 128 + r * 16, src,
-                           ok ? 16u : 0u);
-        }
-        // completion is tracked by the slot's mbarrier (one no-increment arrival per producer
-        // thread once its copies land); the producer moves on to the next free slot at once
-        cp_async_mbar_arrive_noinc(&bar_full[slot]);
-      }
-    }
-  } else if (!GATHER && warp == 4) {
+  if (warp == 4) {
     if (lane == 0) {
       // TMA producer: one 4 KB bulk copy per slice operand per stage
       const size_t offA = (size_t)J * 16 * 256, offB = (size_t)Kt * 16 * 256;
@@ -381,9 +277,6 @@ __global__ void __launch_bounds__(GATHER ? I8_THREADS_G : I8_THREADS, 1) gram_i8
           const int nk = min(kpack, q1 - kst);
           const bool first = kst == sg * I8_SEGST;
           mbar_wait(&bar_full[slot], (q / I8_NST) & 1);
-          // gather mode: the operands were written by cp.async (generic proxy); order them
-          // before the tensor core's async-proxy reads
-          if (GATHER) fence_proxy_async_smem();
           tc_fence_after();
           const unsigned sA = smem_u32(smem + slot * I8_STAGE);
           const unsigned sB = sA + I8_S * I8_OP;
@@ -411,14 +304,13 @@ __global__ void __launch_bounds__(GATHER ? I8_THREADS_G : I8_THREADS, 1) gram_i8
       }
     }
     __syncwarp();
-  } else if (warp < 4) {
+  } else {
     // epilogue: warp w owns TMEM lanes 32w.. = row feature j = 128J + 32w + lane; per phase
     // the FP64 partial sum_g 2^{-7(w-2)} C_w · 2^{e_j + e_k - 12} is added to G[j][k] (k >= j)
     const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
     const int j = J * I8_TM + warp * 32 + lane;
     const bool jok = j < a.n;
-    const int fj = GATHER ? (jok ? sFeat[0][warp * 32 + lane] : -1) : j;
-    const int ej = (jok && fj >= 0) ? __ldg(a.ex + fj) - 12 : 0;
+    const int ej = jok ? __ldg(a.ex + j) - 12 : 0;
     double* Grow = a.G + (int64_t)(jok ? j : 0) * a.n;
     for (int ph = 0; ph < nphase; ++ph) {
       const int w0 = (ph < nseg) ? 6 : 2;     // groups w0 .. w0 + 3 in TMEM columns 0..511
@@ -443,8 +335,7 @@ __global__ void __launch_bounds__(GATHER ? I8_THREADS_G : I8_THREADS, 1) gram_i8
         for (int c = 0; c < 32; ++c) {
           const int k = Kt * I8_TN + cc * 32 + c;
           if (k >= a.n || k < j) continue;
-          const int fk = GATHER ? sFeat[1][cc * 32 + c] : k;
-          const double part = ldexp(acc[c], ej + (fk >= 0 ? __ldg(a.ex + fk) : 0));
+          const double part = ldexp(acc[c], ej + __ldg(a.ex + k));
           const double cur = (ph == 0 && !a.accum) ? 0.0 : Grow[k];
           double val = cur + part;
           if (last) {
@@ -471,10 +362,8 @@ __global__ void __launch_bounds__(GATHER ? I8_THREADS_G : I8_THREADS, 1) gram_i8
 void set_i8_attributes() {
   static bool done = false;
   if (done) return;
-  cudaFuncSetAttribute(gram_i8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM);
-  cudaFuncSetAttribute(gram_i8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM);
-  for (const void* k : {(const void*)gram_i8_kernel<false>, (const void*)gram_i8_kernel<true>,
-                        (const void*)i8_slice_kernel, (const void*)i8_preslice_kernel, (const void*)i8_colexp_kernel})
+  cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, I8_SMEM);
+  for (const void* k : {(const void*)gram_i8_kernel, (const void*)i8_slice_kernel, (const void*)i8_colexp_kernel})
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   done = true;
 }
@@ -520,7 +409,7 @@ int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, 
   a.accum = accum;
   const int tiles = a.JT * (a.JT + 1) / 2;
   note_launch();
-  gram_i8_kernel<false><<<tiles, I8_THREADS, I8_SMEM, st>>>(a);
+  gram_i8_kernel<<<tiles, I8_THREADS, I8_SMEM, st>>>(a);
   return check_launch("gram_i8");
 }
 
@@ -569,48 +458,8 @@ int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32
   a.blk_g = (int64_t)s * s;
   a.blk_ex = ngrp * 8;
   note_launch();
-  gram_i8_kernel<false><<<dim3((unsigned)(a.JT * (a.JT + 1) / 2), (unsigned)p), I8_THREADS, I8_SMEM, st>>>(a);
+  gram_i8_kernel<<<dim3((unsigned)(a.JT * (a.JT + 1) / 2), (unsigned)p), I8_THREADS, I8_SMEM, st>>>(a);
   return check_launch("gram_i8 blocks");
-}
-
-size_t gram_i8_presliced_bytes(int64_t len, int64_t n) {
-  const int64_t nstg = (len + I8_KS - 1) / I8_KS;
-  return (size_t)nstg * n * 256;
-}
-
-int launch_i8_preslice(const double* Xc, int64_t ld, int64_t len, int n, const int* ex, void* P, size_t P_bytes,
-                       cudaStream_t st) {
-  if (!P || P_bytes < gram_i8_presliced_bytes(len, n)) return set_error(RAC_ERR_ARG, "i8 preslice: buffer too small");
-  const int nstg = (int)((len + I8_KS - 1) / I8_KS);
-  if ((nstg + 7) / 8 > 65535) return set_error(RAC_ERR_UNSUPPORTED, "i8 preslice: too many samples");
-  set_i8_attributes();
-  note_launch();
-  i8_preslice_kernel<<<dim3((unsigned)((n + 7) / 8), (unsigned)((nstg + 7) / 8)), 256, 0, st>>>(
-      Xc, ld, len, n, ex, static_cast<uint8_t*>(P), nstg);
-  return check_launch("i8 preslice");
-}
-
-// block mode on pre-sliced data: the p block Grams (full symmetric s x s raw sums) of idx[b*s ..]
-int launch_gram_i8_blocks_pre(const void* P, int64_t len, int64_t nfeat, const int32_t* idx, int s, int p,
-                              const int* ex_all, double* out, cudaStream_t st) {
-  const int nstg = (int)((len + I8_KS - 1) / I8_KS);
-  if (p > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8 blocks: too many blocks");
-  set_i8_attributes();
-  I8Args a{};
-  a.sl = static_cast<const uint8_t*>(P);
-  a.nstg = nstg;
-  a.n = s;
-  a.JT = (s + I8_TM - 1) / I8_TM;
-  a.ex = ex_all;
-  a.G = out;
-  a.div = 0.0;
-  a.accum = 0;
-  a.blk_g = (int64_t)s * s;
-  a.idx = idx;
-  a.nfeat = nfeat;
-  note_launch();
-  gram_i8_kernel<true><<<dim3((unsigned)(a.JT * (a.JT + 1) / 2), (unsigned)p), I8_THREADS_G, I8_SMEM, st>>>(a);
-  return check_launch("gram_i8 blocks (pre-sliced gather)");
 }
 
 }  // namespace rac

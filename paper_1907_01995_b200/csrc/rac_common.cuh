@@ -105,20 +105,6 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
 }
-// 16-byte copy that zero-fills the destination when src_bytes == 0 (no global read)
-__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, unsigned src_bytes) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(src_bytes) : "memory");
-}
-// arrive on `bar` once all of this thread's prior cp.async copies have landed (no count
-// increment: the barrier's expected count includes one arrival per producer thread)
-__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
-  unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }

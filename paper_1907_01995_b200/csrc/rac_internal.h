@@ -64,13 +64,6 @@ size_t gram_i8_blocks_ws_bytes(int64_t len, int s, int p);
 int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st);
 int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32_t* idx, int s, int p,
                           const int* ex_all, double* out, void* ws, size_t ws_bytes, cudaStream_t st);
-// block mode on pre-sliced data: every feature's slices once per data set (P, len samples),
-// then per sweep the block Grams gathered from P by feature index (gram_i8.cu)
-size_t gram_i8_presliced_bytes(int64_t len, int64_t n);
-int launch_i8_preslice(const double* Xc, int64_t ld, int64_t len, int n, const int* ex, void* P, size_t P_bytes,
-                       cudaStream_t st);
-int launch_gram_i8_blocks_pre(const void* P, int64_t len, int64_t nfeat, const int32_t* idx, int s, int p,
-                              const int* ex_all, double* out, cudaStream_t st);
 int launch_gram_reduce_sym(const double* ws, int64_t n, int splits, double div, double* G, cudaStream_t st);
 // K3: assemble block systems, Cholesky, explicit inverse.
 struct SysArgs {

@@ -118,9 +118,8 @@ def test_covariance_fit_with_int8_gram_vs_oracle(lib, monkeypatch, ingest):
                 assert err <= 1e-9, (m, n, s, k, err)
 
 
-@pytest.mark.parametrize("pre", ["1", "0"])
 @pytest.mark.parametrize("ingest", ["host", "device"])
-def test_block_mode_fit_with_int8_block_grams_vs_oracle(lib, monkeypatch, ingest, pre):
+def test_block_mode_fit_with_int8_block_grams_vs_oracle(lib, monkeypatch, ingest):
     """RAC_BG_I8=2 forces the per-sweep int8 block Grams (gather-slicing of the partition's
     columns + one batched tensor-core launch) in block mode: short last block (padding),
     s above and below one 128-feature tile, rp mode; per-sweep iterates against the oracle."""
@@ -128,7 +127,6 @@ def test_block_mode_fit_with_int8_block_grams_vs_oracle(lib, monkeypatch, ingest
     from paper_1907_01995_b200 import elastic_net as en
     from paper_1907_01995_b200.problems import Mode
     monkeypatch.setenv("RAC_BG_I8", "2")
-    monkeypatch.setenv("RAC_BG_PRE", pre)     # 1: slices formed once, gathered per sweep (default)
     rng = np.random.default_rng(31)
     for (m, n, s, mode) in [(400, 700, 150, "rac"), (9000, 520, 130, "rac"), (250, 300, 40, "rp")]:
         X = rng.standard_normal((m, n))
@@ -145,21 +143,3 @@ def test_block_mode_fit_with_int8_block_grams_vs_oracle(lib, monkeypatch, ingest
             for a_, b_ in zip(got[k], caps[k]):
                 err = np.linalg.norm(a_ - b_) / max(np.linalg.norm(b_), 1e-300)
                 assert err <= 1e-9, (m, n, s, mode, k, err)
-
-
-def test_presliced_gather_grams_bitwise_equal_reslicing(lib, monkeypatch):
-    """The pre-sliced gather path forms the same digits and runs the same MMA / epilogue
-    order as per-sweep re-slicing, so the iterates are bit-identical."""
-    from paper_1907_01995_b200 import elastic_net as en
-    monkeypatch.setenv("RAC_BG_I8", "2")
-    rng = np.random.default_rng(41)
-    X = rng.standard_normal((3000, 900))
-    X[:, 5] *= 1e6           # wide exponent spread across features
-    y = X[:, :13] @ rng.standard_normal(13) + 0.05 * rng.standard_normal(3000)
-    spec = en.ElasticNetSpec(lam=0.05, alpha=0.6, gamma=1.0, block_size=260, iters=5, seed=2)
-    out = {}
-    for pre in ("1", "0"):
-        monkeypatch.setenv("RAC_BG_PRE", pre)
-        out[pre] = en.fit(X, y, spec, gram_mode="blocks")
-    for k in ("beta", "z", "xi"):
-        assert np.array_equal(getattr(out["1"], k), getattr(out["0"], k)), k

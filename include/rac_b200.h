@@ -117,6 +117,12 @@ int rac_en_set_data_rows(rac_en_ctx* ctx, const double* X_rows, int64_t row0, in
  * of HBM) and runs the chain on G in one thread-block cluster; selecting it
  * again re-forms G.  RAC_ERR_UNSUPPORTED if the single-cluster chain does not
  * fit (large n or s).  In rp mode the partition must be set again afterwards. */
+/* Sparse design (scipy CSC, canonical: rows sorted within a column, no duplicates):
+ * indptr int64[n+1], rows int32[nnz], vals double[nnz] (device).  Expanded into the
+ * context's column-major X on the device; replaces elastic_net.py:144-147 _col_block on
+ * sparse X (the reference densifies each block's columns per sweep). */
+int rac_en_set_data_csc(rac_en_ctx* ctx, const int64_t* indptr, const int32_t* rows, const double* vals,
+                        const double* y);
 int rac_en_set_gram_mode(rac_en_ctx* ctx, int32_t mode);
 int rac_en_set_partition(rac_en_ctx* ctx, const int64_t* perm);
 /* Enqueue `count` sweeps.  RAC: `perms` = count permutations of n.  RP: count

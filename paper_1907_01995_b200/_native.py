@@ -40,6 +40,7 @@ SIGNATURES = {
     "rac_en_create": (_i32, [C.POINTER(_p), _i64, _i64, _i32, _i32, _f64, _f64, _f64, _p]),
     "rac_en_set_data": (_i32, [_p, _p, _i32, _p]),
     "rac_en_set_data_rows": (_i32, [_p, _p, _i64, _i64, _p]),
+    "rac_en_set_data_csc": (_i32, [_p, _p, _p, _p, _p]),
     "rac_en_set_gram_mode": (_i32, [_p, _i32]),
     "rac_en_set_partition": (_i32, [_p, _p]),
     "rac_en_run": (_i32, [_p, _p, _i32, _f64]),

@@ -1019,6 +1019,46 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
   return RAC_OK;
 }
 
+namespace rac {
+// CSC (canonical: sorted, no duplicate entries) -> the column-major Xc: one warp per column
+// scatters its stored entries into the zeroed column (a block's columns are then exactly
+// what the reference's X[:, block].todense() gives, elastic_net.py:144-147)
+__global__ void csc_scatter_kernel(const int64_t* __restrict__ indptr, const int32_t* __restrict__ rows,
+                                   const double* __restrict__ vals, int64_t n, int64_t ld, double* __restrict__ Xc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; j < n; j += nw) {
+    double* col = Xc + j * ld;
+    for (int64_t k = indptr[j] + lane; k < indptr[j + 1]; k += 32) col[rows[k]] = vals[k];
+  }
+}
+}  // namespace rac
+
+// Sparse X: the nnz stored entries travel (12 bytes each instead of 8 m n for the dense
+// matrix) and are expanded on the device; everything after is the dense block path.
+extern "C" int rac_en_set_data_csc(rac_en_ctx* c, const int64_t* indptr, const int32_t* rows, const double* vals,
+                                   const double* y) {
+  using namespace rac;
+  clear_error();
+  if (!c || !indptr || !y || (!rows && vals) || (rows && !vals))
+    return set_error(RAC_ERR_ARG, "rac_en_set_data_csc: null pointer");
+  cudaMemsetAsync(c->Xc, 0, (size_t)c->ld * c->n * sizeof(double), c->st);
+  if (rows) {
+    const int blocks = (int)std::min<int64_t>((c->n + 7) / 8, (int64_t)num_sms() * 16);
+    csc_scatter_kernel<<<blocks, 256, 0, c->st>>>(indptr, rows, vals, c->n, c->ld, c->Xc);
+    note_launch();
+  }
+  int blocks = (int)std::min<int64_t>((c->n + 7) / 8, (int64_t)num_sms() * 16);
+  note_launch();
+  neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
+  if (c->bg_ws) {
+    int rc = launch_i8_colexp(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->st);
+    if (rc) return rc;
+  }
+  c->have_data = true;
+  return check_launch("rac_en_set_data_csc");
+}
+
 extern "C" int rac_en_set_data(rac_en_ctx* c, const double* X, int32_t layout, const double* y) {
   using namespace rac;
   clear_error();

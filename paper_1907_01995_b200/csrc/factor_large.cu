@@ -44,7 +44,8 @@ __device__ __forceinline__ LargeBufs large_bufs(double* scratch, int s, int p) {
   return L;
 }
 
-// (0) assemble the padded block systems (lower part) from the split-K partials
+// (0) assemble the padded block systems (lower part) from the split-K partials: one warp per
+// row i, lanes over the columns j <= i (coalesced reads of the Gram row, writes of A's row)
 __global__ void large_assemble_kernel(SysArgs a, int p) {
   if (a.done && *a.done) return;
   const int s = a.s;
@@ -52,79 +53,98 @@ __global__ void large_assemble_kernel(SysArgs a, int p) {
   const int b = blockIdx.y;
   const int32_t* bidx = a.idx ? a.idx + (int64_t)b * s : nullptr;
   double* A = L.A + (size_t)b * L.S * L.S;
-  const int64_t total = (int64_t)L.S * L.S;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / L.S), j = (int)(e - (int64_t)i * L.S);
-    if (j > i) continue;
-    double v;
-    if (i >= s || j >= s || (bidx && (bidx[i] < 0 || bidx[j] < 0))) {
-      v = (i == j) ? 1.0 : 0.0;
-    } else {
-      v = 0.0;
-      if (a.ws) {
-        const double* src = a.ws + (int64_t)b * a.splits * s * s + (int64_t)i * s + j;
-        double acc = src[0];
-        for (int z = 1; z < a.splits; ++z) acc += src[(int64_t)z * s * s];
-        if (a.div != 1.0) acc = acc / a.div;
-        if (a.mul != 1.0) acc = a.mul * acc;
-        v = acc;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < L.S; i += nw) {
+    const bool ivalid = i < s && !(bidx && bidx[i] < 0);
+    const int64_t gi = ivalid && bidx ? (int64_t)bidx[i] * a.ldh : 0;
+    for (int j = lane; j <= i; j += 32) {
+      double v;
+      if (!ivalid || j >= s || (bidx && bidx[j] < 0)) {
+        v = (i == j) ? 1.0 : 0.0;
+      } else {
+        v = 0.0;
+        if (a.ws) {
+          const double* src = a.ws + (int64_t)b * a.splits * s * s + (int64_t)i * s + j;
+          double acc = src[0];
+          for (int z = 1; z < a.splits; ++z) acc += src[(int64_t)z * s * s];
+          if (a.div != 1.0) acc = acc / a.div;
+          if (a.mul != 1.0) acc = a.mul * acc;
+          v = acc;
+        }
+        if (a.H) {
+          const double h = a.H[gi + bidx[j]];
+          v = a.ws ? h + v : h;
+        }
+        if (i == j) v += a.shift;
       }
-      if (a.H) {
-        const double h = a.H[(int64_t)bidx[i] * a.ldh + bidx[j]];
-        v = a.ws ? h + v : h;
-      }
-      if (i == j) v += a.shift;
+      A[(int64_t)i * L.S + j] = v;
     }
-    A[(int64_t)i * L.S + j] = v;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.info[b] = 0;
 }
 
-// (a) W = inv(A_KK): unblocked symmetric sweep of the 64x64 block in smem
+// (a) W = inv(A_KK): symmetric sweep of the 64x64 diagonal block held in REGISTERS: thread
+// (i, quarter) owns row i's 16 columns 16*quarter..; per pivot q the owner of column q
+// publishes it (double-buffered in smem, one barrier per pivot), and every thread updates
+// its 16 entries.  The sweep keeps the matrix symmetric, so column q is also row q.
 __global__ void __launch_bounds__(LTHREADS) large_pivot_kernel(SysArgs a, int p, int kt) {
   if (a.done && *a.done) return;
   const LargeBufs L = large_bufs(a.scratch, a.s, p);
   const int b = blockIdx.x;
   if (a.info[b]) return;
-  __shared__ double P[LT][LT + 1];
-  __shared__ double col[LT];
-  __shared__ int fail;
+  static_assert(LTHREADS == 4 * LT, "thread = (row, quarter of the columns)");
+  __shared__ __align__(16) double col[2][LT];
   const double* A = L.A + (size_t)b * L.S * L.S;
-  const int tid = threadIdx.x, k0 = kt * LT;
-  if (tid == 0) fail = 0;
-  for (int e = tid; e < LT * LT; e += LTHREADS) {
-    const int i = e / LT, j = e - i * LT;
-    const int gi = k0 + i, gj = k0 + j;
-    P[i][j] = (j <= i) ? A[(int64_t)gi * L.S + gj] : A[(int64_t)gj * L.S + gi];
+  const int tid = threadIdx.x, i = tid >> 2, j0 = (tid & 3) * 16, k0 = kt * LT;
+  double v[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int j = j0 + u;
+    v[u] = (j <= i) ? A[(int64_t)(k0 + i) * L.S + k0 + j] : A[(int64_t)(k0 + j) * L.S + k0 + i];
   }
+  if ((tid & 3) == 0) col[0][i] = v[0];   // column 0 = row i's entry 0 (owner: quarter 0)
   __syncthreads();
+  int fail = 0;
   for (int q = 0; q < LT; ++q) {
-    const double d = P[q][q];
+    const double* c = col[q & 1];
+    const double d = c[q];
     if (!(d > 0.0) || !isfinite(d)) {
-      if (tid == 0) fail = k0 + q + 1;
+      fail = k0 + q + 1;    // uniform: every thread read the same pivot
       break;
     }
-    if (tid < LT) col[tid] = P[tid][q];
-    __syncthreads();
     const double dinv = 1.0 / d;
-    for (int e = tid; e < LT * LT; e += LTHREADS) {
-      const int i = e / LT, j = e - i * LT;
-      double v;
-      if (i == q && j == q) v = -dinv;
-      else if (i == q) v = col[j] * dinv;
-      else if (j == q) v = col[i] * dinv;
-      else v = P[i][j] - col[i] * col[j] * dinv;
-      P[i][j] = v;
+    const double ci = c[i];
+    const double ri = ci * dinv;
+    double cj[16];
+#pragma unroll
+    for (int u = 0; u < 16; u += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(c + j0 + u);
+      cj[u] = t.x;
+      cj[u + 1] = t.y;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int j = j0 + u;
+      if (j == q) v[u] = (i == q) ? -dinv : ri;
+      else if (i == q) v[u] = cj[u] * dinv;
+      else v[u] = v[u] - ri * cj[u];
+    }
+    // publish column q + 1 (owned by quarter (q + 1) / 16) for the next pivot
+    if (q + 1 < LT && (tid & 3) == ((q + 1) >> 4)) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u)
+        if (j0 + u == q + 1) col[(q + 1) & 1][i] = v[u];
     }
     __syncthreads();
   }
-  __syncthreads();
   if (fail) {
     if (tid == 0) a.info[b] = fail;
     return;
   }
   double* W = L.W + (size_t)b * LT * LT;
-  for (int e = tid; e < LT * LT; e += LTHREADS) W[e] = -P[e / LT][e % LT];   // +inv
+#pragma unroll
+  for (int u = 0; u < 16; ++u) W[i * LT + j0 + u] = -v[u];   // +inv
 }
 
 // load a 64x64 tile (row-major, ld) into smem [r][c] (optionally transposed).
@@ -300,7 +320,7 @@ int launch_inverse_large(const SysArgs& a, int p, cudaStream_t st) {
     if (rc) return rc;
     attr = true;
   }
-  large_assemble_kernel<<<dim3(64, p), 256, 0, st>>>(a, p);
+  large_assemble_kernel<<<dim3((S + 7) / 8, p), 256, 0, st>>>(a, p);
   for (int kt = 0; kt < nt; ++kt) {
     large_pivot_kernel<<<p, LTHREADS, 0, st>>>(a, p, kt);
     if (nt > 1) {

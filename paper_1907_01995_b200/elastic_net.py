@@ -181,7 +181,8 @@ class EnSolver:
         """X: numpy (C or F order) / scipy sparse / torch tensor; y: length m."""
         layout = _native.LAYOUT_ROW_MAJOR
         if sp.issparse(X):
-            X = np.asarray(X.todense(), dtype=float)
+            self._set_data_csc(X, y)
+            return
         if isinstance(X, torch.Tensor):
             Xd = X.to(self.dev, torch.float64)
             if not Xd.is_contiguous() and Xd.t().is_contiguous():
@@ -201,6 +202,23 @@ class EnSolver:
         yd = _device.upload(y, device=self.dev)
         _native.check(self.lib.rac_en_set_data(self.h, Xd.data_ptr(), layout, yd.data_ptr()))
         self._keep = [Xd, yd]   # alive until the stream consumed them
+
+    def _set_data_csc(self, X, y) -> None:
+        """Sparse X: upload the CSC arrays (nnz-sized) and expand on the device (rac_en_set_data_csc)."""
+        A = sp.csc_matrix(X, dtype=np.float64, copy=True)
+        A.sum_duplicates()          # canonical: sorted rows, duplicates summed (what todense gives)
+        A.sort_indices()
+        if A.nnz >= 2 ** 31 or self.m >= 2 ** 31:
+            raise ValueError("sparse X too large for 32-bit row indices")
+        ip = _device.upload(A.indptr.astype(np.int64), dtype=torch.int64, device=self.dev)
+        rows = vals = None
+        if A.nnz:
+            rows = torch.from_numpy(A.indices.astype(np.int32)).to(self.dev)
+            vals = _device.upload(A.data, device=self.dev)
+        yd = _device.upload(y, device=self.dev)
+        _native.check(self.lib.rac_en_set_data_csc(self.h, ip.data_ptr(), _device.ptr(rows), _device.ptr(vals),
+                                                   yd.data_ptr()))
+        self._keep = [ip, rows, vals, yd]
 
     def _set_data_streamed(self, X: np.ndarray, y) -> None:
         """Host X in row chunks: the transfer of chunk k+1 overlaps the device

@@ -394,6 +394,31 @@ def gen_block_and_prox():
 
 
 # ---------------------------------------------------------------------------
+def gen_sparse():
+    """racml fit on scipy CSC designs (the test_elastic_net.py:261-269 recipe and a larger,
+    1%-dense one): per-sweep iterates of the reference's sparse column-block path."""
+    import scipy.sparse as sps
+    d = {}
+    rng = np.random.default_rng(15)
+    X = sps.csc_matrix(np.where(rng.random((30, 40)) < 0.2, rng.standard_normal((30, 40)), 0.0))
+    y = rng.standard_normal(30)
+    _en_case("ref", X, y, ren.ElasticNetSpec(lam=0.05, alpha=1.0, block_size=16, iters=50, seed=7),
+             keep_full=[1, 2, 5, 10, 25, 50], out=d, save_xy=False)
+    d["ref_X"] = X.toarray()
+    d["ref_y"] = y
+    rng = np.random.default_rng(16)
+    X = sps.random(1500, 2400, density=0.01, format="csc", random_state=np.random.RandomState(16),
+                   data_rvs=lambda k: rng.standard_normal(k))
+    y = X @ (rng.standard_normal(2400) * (rng.random(2400) < 0.05)) + 0.01 * rng.standard_normal(1500)
+    _en_case("big", X, y, ren.ElasticNetSpec(lam=0.02, alpha=0.9, gamma=None, block_size=120, iters=30, seed=2),
+             keep_full=[1, 2, 5, 10, 30], out=d, save_xy=False)
+    d["big_data"], d["big_indices"], d["big_indptr"] = X.data, X.indices, X.indptr
+    d["big_shape"] = np.array(X.shape)
+    d["big_y"] = y
+    _save("en_sparse", **d)
+
+
+# ---------------------------------------------------------------------------
 def gen_consensus():
     """racml.elastic_net.consensus_fit on direct-route (p <= n_i), Woodbury-route (p > n_i)
     and mixed group shapes, with and without a tolerance."""
@@ -460,6 +485,8 @@ if __name__ == "__main__":
     which = sys.argv[1:] or ["chunks", "en", "svm", "qp", "block"]
     if "consensus" in which:
         gen_consensus()
+    if "sparse" in which:
+        gen_sparse()
     if "full2" in which:
         gen_full_en(2)
     if "full3" in which:

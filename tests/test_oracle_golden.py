@@ -182,3 +182,28 @@ def test_full_size_fixtures_are_complete(golden):
     assert np.array_equal(np.sort(g["cfg4_blocks_1"]), np.arange(20000))
     for k in g["cfg4_sweeps_kept"]:
         assert g[f"cfg4_z_{int(k)}"].shape == (20000,)
+
+
+def _sparse_case(g, tag):
+    import scipy.sparse as sps
+    if tag == "ref":
+        return sps.csc_matrix(g["ref_X"]), g["ref_y"]
+    shp = tuple(int(v) for v in g["big_shape"])
+    return sps.csc_matrix((g["big_data"], g["big_indices"], g["big_indptr"]), shape=shp), g["big_y"]
+
+
+@pytest.mark.parametrize("tag", ["ref", "big"])
+def test_sparse_oracle_matches_reference(golden, tag):
+    """oracle.en_fit on CSC input (the reference densifies each block's columns) vs racml."""
+    from oracle import rac_oracle as ro
+    g = golden("en_sparse")
+    X, y = _sparse_case(g, tag)
+    lam, alpha, gamma, bs, iters, seed, tol = g[f"{tag}_params"]
+    caps = {}
+    ro.en_fit(X, y, lam, alpha, None if np.isnan(gamma) else gamma, int(bs), int(iters), seed=int(seed),
+              on_sweep=lambda k, bl, b, z, xi: caps.__setitem__(k, (b.copy(), z.copy(), xi.copy())))
+    for k in g[f"{tag}_sweeps_kept"]:
+        b, z, xi = caps[int(k)]
+        for got, key in ((b, "beta"), (z, "z"), (xi, "xi")):
+            want = g[f"{tag}_{key}_{int(k)}"]
+            assert np.linalg.norm(got - want) <= 1e-12 * max(np.linalg.norm(want), 1e-300)

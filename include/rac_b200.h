@@ -196,6 +196,13 @@ int rac_qp_borrow_h(rac_qp_ctx* ctx, const double* H);
 /* Replaces engine.py:284-315's inputs (x, y) of run_sweep: the next sweep starts from the
  * device vectors x (n) and y (m) instead of (clip(0, lower, upper), 0). */
 int rac_qp_set_state(rac_qp_ctx* ctx, const double* x, const double* y);
+/* Kernel strips on the fly instead of a resident n x n H (SVM dual, svm.py:96-143 — the
+ * reference assembles each block's s x n strip from data rows): H_ij = labels_i labels_j
+ * K(X_i, X_j) with X n x d row-major (device), kind RAC_KERNEL_*; per sweep the blocks' H_bb,
+ * then the strip rows of up to max_strip_bytes worth of blocks at a time.  Before
+ * rac_qp_set_problem (with H = null; every box must contain 0); RAC / CYCLIC modes. */
+int rac_qp_set_kernel_strips(rac_qp_ctx* ctx, const double* X, int64_t d, const double* labels, int32_t kind,
+                             double sigma, uint64_t max_strip_bytes);
 /* Divergence bar (engine.py:361-362): set_problem uses 1e8*max(primal0, 1);
  * svm.train has no guard and passes +inf. */
 int rac_qp_set_divergence_bar(rac_qp_ctx* ctx, double bar);

@@ -60,6 +60,7 @@ SIGNATURES = {
     "rac_qp_set_problem": (_i32, [_p, _p, _p, _p, _p, _p, _p]),
     "rac_qp_borrow_h": (_i32, [_p, _p]),
     "rac_qp_set_state": (_i32, [_p, _p, _p]),
+    "rac_qp_set_kernel_strips": (_i32, [_p, _p, _i64, _p, _i32, _f64, C.c_uint64]),
     "rac_consensus_run": (_i32, [_p, _i32, _p]),
     "rac_svm_kernel_strip": (_i32, [_p, _i64, _i64, _p, _p, _i32, _i32, _f64, _p, _p]),
     "rac_qp_set_divergence_bar": (_i32, [_p, _f64]),

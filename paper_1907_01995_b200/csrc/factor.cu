@@ -31,8 +31,9 @@ constexpr int SB = 8;   // pivots per blocked sweep step
 __device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }  // j <= i
 
 // gathered H_bb entry (0 for padding)
-__device__ __forceinline__ double h_entry(const SysArgs& a, const int32_t* bidx, int i, int j) {
-  if (!a.H || !bidx || bidx[i] < 0 || bidx[j] < 0) return 0.0;
+__device__ __forceinline__ double h_entry(const SysArgs& a, int b, const int32_t* bidx, int i, int j) {
+  if (!(a.H || a.hblk) || !bidx || bidx[i] < 0 || bidx[j] < 0) return 0.0;
+  if (a.hblk) return a.hblk[((int64_t)b * a.s + i) * a.s + j];
   return a.H[(int64_t)bidx[i] * a.ldh + bidx[j]];
 }
 
@@ -41,7 +42,7 @@ __device__ __forceinline__ double sys_entry(const SysArgs& a, int b, const int32
                                             double* h_out) {
   const bool pad = bidx && (bidx[i] < 0 || bidx[j] < 0);
   double h = 0.0;
-  if (a.H && !pad) h = a.H[(int64_t)bidx[i] * a.ldh + bidx[j]];
+  if (!pad) h = h_entry(a, b, bidx, i, j);
   if (h_out) *h_out = h;
   if (pad) return (i == j) ? 1.0 : 0.0;   // short last block: identity rows keep the leading part exact
   double v = 0.0;
@@ -54,7 +55,7 @@ __device__ __forceinline__ double sys_entry(const SysArgs& a, int b, const int32
     if (a.mul != 1.0) acc = a.mul * acc;
     v = acc;
   }
-  if (a.H) v = a.ws ? h + v : h;
+  if (a.H || a.hblk) v = a.ws ? h + v : h;
   if (i == j) v += a.shift;
   return v;
 }
@@ -83,7 +84,7 @@ __device__ void assemble_square(const SysArgs& a, int b, double* A, int ld, doub
   for (int e = tid; e < s * s; e += CTHREADS) {
     const int i = e / s, j = e - i * s;
     const double v = (j <= i) ? sys_entry(a, b, bidx, i, j, nullptr) : 0.0;
-    if (hbo) hbo[e] = h_entry(a, bidx, i, j);
+    if (hbo) hbo[e] = h_entry(a, b, bidx, i, j);
     A[(int64_t)i * ld + j] = v;
   }
   __syncthreads();
@@ -357,8 +358,8 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
                 if (a.div != 1.0) acc = acc / a.div;
                 if (a.mul != 1.0) acc = a.mul * acc;
               }
-              if (a.H) {
-                const double h = a.H[(int64_t)gi * a.ldh + gj];
+              if (a.H || a.hblk) {
+                const double h = a.hblk ? a.hblk[((int64_t)b * s + i) * s + j] : a.H[(int64_t)gi * a.ldh + gj];
                 acc = wsb ? h + acc : h;
               }
               if (i == j) acc += a.shift;
@@ -375,7 +376,7 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
     if (hbo)
       for (int e = tid; e < s * s; e += CTHREADS) {
         const int i = e / s, j = e - i * s;
-        hbo[e] = h_entry(a, bidx, i, j);
+        hbo[e] = h_entry(a, b, bidx, i, j);
       }
     __syncthreads();
     if (a.ridge_rel > 0.0) {

@@ -24,18 +24,21 @@ constexpr int LTHREADS = 256;
 
 size_t large_scratch_bytes(int s, int p) {
   const size_t S = (size_t)(s + LT - 1) / LT * LT;
-  return (size_t)p * (S * S + S * LT + LT * LT) * sizeof(double);
+  return (size_t)p * (S * S + S * LT + 2 * LT * LT) * sizeof(double);
 }
 
 struct LargeBufs {
+  int p;
   double* A;    // [p][S][S]   (only lower tiles maintained)
   double* CW;   // [p][S][LT]
-  double* W;    // [p][LT][LT]
+  double* W;    // [2][p][LT][LT]: W of pivot step kt in half kt & 1 (the look-ahead pivot of
+                //   step kt + 1 is written while step kt's strip still reads W_kt)
   int S, nt;
 };
 
 __device__ __forceinline__ LargeBufs large_bufs(double* scratch, int s, int p) {
   LargeBufs L;
+  L.p = p;
   L.S = (s + LT - 1) / LT * LT;
   L.nt = L.S / LT;
   L.A = scratch;
@@ -72,8 +75,8 @@ __global__ void large_assemble_kernel(SysArgs a, int p) {
           if (a.mul != 1.0) acc = a.mul * acc;
           v = acc;
         }
-        if (a.H) {
-          const double h = a.H[gi + bidx[j]];
+        if (a.H || a.hblk) {
+          const double h = a.hblk ? a.hblk[((int64_t)b * s + i) * s + j] : a.H[gi + bidx[j]];
           v = a.ws ? h + v : h;
         }
         if (i == j) v += a.shift;
@@ -88,11 +91,7 @@ __global__ void large_assemble_kernel(SysArgs a, int p) {
 // (i, quarter) owns row i's 16 columns 16*quarter..; per pivot q the owner of column q
 // publishes it (double-buffered in smem, one barrier per pivot), and every thread updates
 // its 16 entries.  The sweep keeps the matrix symmetric, so column q is also row q.
-__global__ void __launch_bounds__(LTHREADS) large_pivot_kernel(SysArgs a, int p, int kt) {
-  if (a.done && *a.done) return;
-  const LargeBufs L = large_bufs(a.scratch, a.s, p);
-  const int b = blockIdx.x;
-  if (a.info[b]) return;
+__device__ void pivot_sweep(const SysArgs& a, const LargeBufs& L, int b, int kt) {
   static_assert(LTHREADS == 4 * LT, "thread = (row, quarter of the columns)");
   __shared__ __align__(16) double col[2][LT];
   const double* A = L.A + (size_t)b * L.S * L.S;
@@ -114,8 +113,7 @@ __global__ void __launch_bounds__(LTHREADS) large_pivot_kernel(SysArgs a, int p,
       break;
     }
     const double dinv = 1.0 / d;
-    const double ci = c[i];
-    const double ri = ci * dinv;
+    const double ri = c[i] * dinv;
     double cj[16];
 #pragma unroll
     for (int u = 0; u < 16; u += 2) {
@@ -142,9 +140,17 @@ __global__ void __launch_bounds__(LTHREADS) large_pivot_kernel(SysArgs a, int p,
     if (tid == 0) a.info[b] = fail;
     return;
   }
-  double* W = L.W + (size_t)b * LT * LT;
+  double* W = L.W + ((size_t)(kt & 1) * L.p + b) * LT * LT;
 #pragma unroll
   for (int u = 0; u < 16; ++u) W[i * LT + j0 + u] = -v[u];   // +inv
+}
+
+__global__ void __launch_bounds__(LTHREADS) large_pivot_kernel(SysArgs a, int p, int kt) {
+  if (a.done && *a.done) return;
+  const LargeBufs L = large_bufs(a.scratch, a.s, p);
+  const int b = blockIdx.x;
+  if (a.info[b]) return;
+  pivot_sweep(a, L, b, kt);
 }
 
 // load a 64x64 tile (row-major, ld) into smem [r][c] (optionally transposed).
@@ -210,7 +216,7 @@ __global__ void __launch_bounds__(LTHREADS) large_cw_kernel(SysArgs a, int p, in
   // X = A_IK (rows i of tile I, k of tile K); Y rows j = W columns: W symmetric, Y[j][k] = W[j][k]
   if (I > kt) load_tile(sX, A + (int64_t)I * LT * L.S + kt * LT, L.S, false);
   else load_tile(sX, A + (int64_t)kt * LT * L.S + I * LT, L.S, true);
-  load_tile(sY, L.W + (size_t)b * LT * LT, LT, false);
+  load_tile(sY, L.W + ((size_t)(kt & 1) * p + b) * LT * LT, LT, false);
   cp_async_wait<0>();
   __syncthreads();
   double acc[2][4][2] = {};
@@ -227,14 +233,22 @@ __global__ void __launch_bounds__(LTHREADS) large_cw_kernel(SysArgs a, int p, in
 }
 
 // (c) A_IJ -= CW_I * A_JK'   for lower tiles I >= J with I, J != K
+// grid (p, tiles): the first tile of every block is the NEXT pivot tile (K+1, K+1), so those
+// CTAs are dispatched first; after its update the CTA also inverts it (the next step's pivot,
+// look-ahead), overlapping that latency-bound sweep with the rest of this update.
 __global__ void __launch_bounds__(LTHREADS) large_update_kernel(SysArgs a, int p, int kt) {
   if (a.done && *a.done) return;
   const LargeBufs L = large_bufs(a.scratch, a.s, p);
-  const int b = blockIdx.y;
+  const int b = blockIdx.x;
   if (a.info[b]) return;
-  // tile index over the lower triangle of the (nt-1) x (nt-1) grid without K
+  // tile index over the lower triangle of the (nt-1) x (nt-1) grid without K; index 0 is
+  // remapped to the next diagonal tile (reduced index (kt, kt)) when there is a next step
   const int m = L.nt - 1;
-  int I = 0, J = blockIdx.x;
+  const bool lookahead = kt + 1 < L.nt;
+  const int dnext = kt * (kt + 1) / 2 + kt;
+  int e = blockIdx.y;
+  if (lookahead) e = (e == 0) ? dnext : (e <= dnext ? e - 1 : e);
+  int I = 0, J = e;
   while (J > I) { J -= I + 1; ++I; }
   if (I >= m) return;
   if (I >= kt) ++I;
@@ -266,6 +280,10 @@ __global__ void __launch_bounds__(LTHREADS) large_update_kernel(SysArgs a, int p
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) C[(int64_t)(r0 + i * 8 + g) * L.S + c0 + j * 8 + 2 * t + e] = acc[i][j][e];
+  if (lookahead && I == kt + 1 && J == kt + 1) {
+    __syncthreads();   // the updated tile (global, written by this CTA) is the next pivot
+    pivot_sweep(a, L, b, kt + 1);
+  }
 }
 
 // (d) K strip: A_IK = CW_I (lower tiles, transposed above K), A_KK = -W
@@ -279,7 +297,7 @@ __global__ void large_strip_kernel(SysArgs a, int p, int kt) {
   for (int e = threadIdx.x; e < LT * LT; e += blockDim.x) {
     const int i = e / LT, j = e - i * LT;
     if (I == kt) {
-      if (j <= i) A[(int64_t)(kt * LT + i) * L.S + kt * LT + j] = -L.W[(size_t)b * LT * LT + e];
+      if (j <= i) A[(int64_t)(kt * LT + i) * L.S + kt * LT + j] = -L.W[((size_t)(kt & 1) * p + b) * LT * LT + e];
     } else {
       const double v = L.CW[((size_t)b * L.S + (size_t)I * LT + i) * LT + j];   // CW_I[i][j] = A'_{I i, K j}
       if (I > kt) A[(int64_t)(I * LT + i) * L.S + kt * LT + j] = v;
@@ -321,18 +339,19 @@ int launch_inverse_large(const SysArgs& a, int p, cudaStream_t st) {
     attr = true;
   }
   large_assemble_kernel<<<dim3((S + 7) / 8, p), 256, 0, st>>>(a, p);
+  // the first pivot is its own launch; every later one runs inside the previous step's update
+  large_pivot_kernel<<<p, LTHREADS, 0, st>>>(a, p, 0);
   for (int kt = 0; kt < nt; ++kt) {
-    large_pivot_kernel<<<p, LTHREADS, 0, st>>>(a, p, kt);
     if (nt > 1) {
       large_cw_kernel<<<dim3(nt - 1, p), LTHREADS, smem, st>>>(a, p, kt);
       const int m = nt - 1;
       const int ntiles = m * (m + 1) / 2;
-      if (ntiles > 0) large_update_kernel<<<dim3(ntiles, p), LTHREADS, smem, st>>>(a, p, kt);
+      if (ntiles > 0) large_update_kernel<<<dim3(p, ntiles), LTHREADS, smem, st>>>(a, p, kt);
     }
     large_strip_kernel<<<dim3(nt, p), 256, 0, st>>>(a, p, kt);
   }
   large_out_kernel<<<dim3(32, p), 256, 0, st>>>(a, p);
-  note_launch(2 + nt * (nt > 1 ? 4 : 2));
+  note_launch(3 + nt * (nt > 1 ? 3 : 1));
   return check_launch("inverse_large");
 }
 

@@ -55,10 +55,20 @@ struct QpChainArgs {
   double beta, tol_p, tol_d, div_bar;
   int fixed, sweep, lsmem;
   double *hist_p, *hist_l1, *hist_d;
+  // blocks [t0, t1) of the sweep's visit order run in this launch (the dual step and the
+  // residuals only when t1 == p).  strips: H holds the kernel strips of exactly these blocks,
+  // row (t - t0) * s + i for member i of block t (formed on the fly, svm.py:121-143), instead
+  // of the full N x N matrix indexed by sample
+  int t0, t1, strips;
 };
 
+// H row of member i (global index g) of the block visited at step t
+__device__ __forceinline__ const double* h_row(const QpChainArgs& a, int t, int i, int g) {
+  return a.strips ? a.H + ((int64_t)(t - a.t0) * a.s + i) * a.n : a.H + (int64_t)g * a.n;
+}
+
 // hx[cols of this CTA] += sum_i H[blk[i], col] * delta[i]
-__device__ void strip_update(const QpChainArgs& a, const int32_t* sIdx, const double* sDel,
+__device__ void strip_update(const QpChainArgs& a, int t, const int32_t* sIdx, const double* sDel,
                              double* red, int s) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = QPT / 32;
   const int P = gridDim.x;
@@ -77,7 +87,7 @@ __device__ void strip_update(const QpChainArgs& a, const int32_t* sIdx, const do
         const int i = i0 + u * nw;
         const int g = (i < s) ? sIdx[i] : -1;
         dd[u] = (g >= 0) ? sDel[i] : 0.0;
-        const double* row = a.H + (int64_t)(g >= 0 ? g : 0) * a.n;
+        const double* row = h_row(a, t, (g >= 0) ? i : 0, g >= 0 ? g : 0);
 #pragma unroll
         for (int q = 0; q < QCOLS / 32; ++q) {
           const int64_t j = t0 + q * 32 + lane;
@@ -274,7 +284,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
     mbar_init(w.bar, 1);
     mbar_fence_init();
   }
-  auto issue_strip = [&](int b) {
+  auto issue_strip = [&](int b, int t) {
     if (!strip_smem || blockIdx.x == 0 || sc1 <= sc0) return;
     const int32_t* bi = a.idx + (int64_t)b * s;
     const unsigned seg = (unsigned)((sc1 - sc0) * sizeof(double));
@@ -292,7 +302,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
     __syncthreads();
     for (int i = tid; i < s; i += QPT) {
       const int g = bi[i];
-      if (g >= 0) bulk_g2s(w.sM + (size_t)i * sper2, a.H + (int64_t)g * a.n + sc0, seg, w.bar);
+      if (g >= 0) bulk_g2s(w.sM + (size_t)i * sper2, h_row(a, t, i, g) + sc0, seg, w.bar);
       else
         for (int64_t jj = 0; jj < sc1 - sc0; ++jj) w.sM[(size_t)i * sper2 + jj] = 0.0;   // padding row
     }
@@ -453,30 +463,31 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
     }
     if (tid == 0) pf_cond = ldcg(a.cond + bn);
   };
-  int bnext = a.order ? a.order[0] : 0;
+  int bnext = a.order ? a.order[a.t0] : a.t0;
+  const int s0 = a.t0 & 1;   // parity slot of the launch's first block
   prefetch_ML(bnext);
-  compute_hbx(bnext, 0);
+  compute_hbx(bnext, s0);
   if (small_a) {
-    small_pre(bnext, 0);
+    small_pre(bnext, s0);
     __syncthreads();
-    small_post(0, 0, false, true);
+    small_post(s0, s0, false, true);
   }
   else if (has_a)
     row_phase<RC>(a.Ac, a.lda, a.m, a.nrc, a.idx, s, -1, bnext, a.delta, a.x, a.ax, a.partial, w.rp, tfn);
   const bool tr = a.trace && blockIdx.x == 0 && tid == 0;
   // per-CTA arrival stamps at both grid barriers of every block (tracing only)
   long long* arr = a.trace ? a.trace + 14 * (size_t)a.p : nullptr;
-  for (int t = 0; t < a.p; ++t) {
+  for (int t = a.t0; t < a.t1; ++t) {
     const int b = bnext;
     if (arr && tid == 0) arr[((size_t)t * P + blockIdx.x) * 2 + 1] = gtimer();
     grid_barrier(a.bar, target, P);
     if (tr) a.trace[10 * t + 0] = gtimer();
-    issue_strip(b);
+    issue_strip(b, t);
     // While CTA 0 solves block t, the others prepare block t+1's terms that do not
     // depend on block t's solution: H_bb x_b (double-buffered by parity) and, on the
     // constraint-row owner, A_b x_b.
     {
-      const int bn1 = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
+      const int bn1 = (t + 1 < a.t1) ? (a.order ? a.order[t + 1] : t + 1) : -1;
       if (bn1 >= 0 && blockIdx.x != 0) {
         compute_hbx(bn1, (t + 1) & 1);
         if (small_a) small_pre(bn1, (t + 1) & 1);
@@ -505,7 +516,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
       if (tid == 0) w.bw.misc[0] = 0;
       __syncthreads();
       int nval = 0;
-      const bool use_pf = pf_on && t > 0;
+      const bool use_pf = pf_on && t > a.t0;
       for (int i = tid; i < s; i += QPT) {
         const int g = use_pf ? (int)pf[i] : bidx[i];
         w.sIdx[i] = g;
@@ -585,7 +596,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
         }
         a.delta[i] = d;
       }
-      if (t + 1 < a.p) prefetch_ML(a.order ? a.order[t + 1] : t + 1);
+      if (t + 1 < a.t1) prefetch_ML(a.order ? a.order[t + 1] : t + 1);
     }
     if (tr) a.trace[10 * t + 5] = gtimer();
     if (arr && tid == 0) arr[((size_t)t * P + blockIdx.x) * 2 + 0] = gtimer();
@@ -600,14 +611,14 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
     if (tid == 0) bad = ldcg(a.ctrl + 0);
     __syncthreads();
     if (bad) return;
-    bnext = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
+    bnext = (t + 1 < a.t1) ? (a.order ? a.order[t + 1] : t + 1) : -1;
     if (P == 1 && bnext >= 0) {   // single CTA: nobody could prepare during S
       compute_hbx(bnext, (t + 1) & 1);
       if (small_a) small_pre(bnext, (t + 1) & 1);
     }
     if (tr) a.trace[10 * t + 8] = gtimer();
     if (strip_smem) strip_from_smem();
-    else if (a.H) strip_update(a, w.sIdx, w.sDel, w.red, s);
+    else if (a.H) strip_update(a, t, w.sIdx, w.sDel, w.red, s);
     if (tr) a.trace[10 * t + 9] = gtimer();
     if (small_a) small_post(t & 1, (t + 1) & 1, true, bnext >= 0);
     else if (has_a && (int)blockIdx.x < a.nrc)   // CTAs without row chunks have no partial to write
@@ -615,6 +626,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
     if (bnext >= 0) prefetch_next(bnext, (t + 1) & 1);
     if (tr) a.trace[10 * t + 7] = gtimer();
   }
+  if (a.t1 < a.p) return;   // a later launch continues the sweep (running Hx / Ax are global)
   grid_barrier(a.bar, target, P);
   // ------------------------------------------------------------ dual step + primal residual
   // rows of A are owned by the CTA that owns their row chunk
@@ -790,6 +802,13 @@ struct rac_qp_ctx {
   double div_bar = INFINITY;
   int rc = 32;   // rows per chunk of the A row phase (8 for few constraint rows)
   long long* trace = nullptr;   // 4 stamps per block of the last traced sweep
+  // kernel strips on the fly (rac_qp_set_kernel_strips): no N x N matrix; per sweep the
+  // blocks' H_bb and, batch by batch, the strip rows of sb blocks are formed from the samples
+  bool strips = false;
+  double *Xp = nullptr, *sq = nullptr, *lab = nullptr, *Hs = nullptr, *hblk = nullptr;
+  int64_t ldd = 0, dfeat = 0;
+  int kkind = 0, sb = 1;
+  double ksigma = 1.0;
   std::vector<void*> allocs;
 };
 
@@ -840,11 +859,18 @@ int qp_block_systems(rac_qp_ctx* c) {
     if (rc) return rc;
   }
   SysArgs a{};
+  if (c->strips) {
+    // H_bb of every block straight from the samples (gathered rows and columns), one launch
+    rc = launch_kernel_strip(c->Xp, c->ldd, c->dfeat, c->idx, c->s, c->s, c->lab, c->sq, c->kkind, c->ksigma,
+                             c->hblk, c->s, c->st, c->idx, c->p);
+    if (rc) return rc;
+    a.hblk = c->hblk;
+  }
   a.ws = (c->m > 0) ? c->gram_ws : nullptr;
   a.splits = c->gp.splits;
   a.div = 1.0;
   a.mul = c->beta;
-  a.H = c->H;
+  a.H = c->strips ? nullptr : c->H;
   a.ldh = c->n;
   a.idx = c->idx;
   a.shift = 0.0;
@@ -862,7 +888,7 @@ int qp_block_systems(rac_qp_ctx* c) {
   return launch_chol_system(a, c->p, c->st);
 }
 
-int qp_chain(rac_qp_ctx* c, double tol_p, double tol_d, int fixed) {
+int qp_chain(rac_qp_ctx* c, double tol_p, double tol_d, int fixed, int t0, int t1) {
   using namespace rac;
   cudaMemsetAsync(c->bar, 0, sizeof(unsigned), c->st);
   QpChainArgs a{};
@@ -872,7 +898,10 @@ int qp_chain(rac_qp_ctx* c, double tol_p, double tol_d, int fixed) {
   a.s = c->s;
   a.p = c->p;
   a.nrc = c->nrc;
-  a.H = c->H;
+  a.H = c->strips ? c->Hs : c->H;
+  a.strips = c->strips ? 1 : 0;
+  a.t0 = t0;
+  a.t1 = t1;
   a.Ac = c->Ac;
   a.b = c->b;
   a.c = c->c;
@@ -1004,6 +1033,7 @@ extern "C" int rac_qp_set_problem(rac_qp_ctx* c, const double* H, const double* 
   if ((c->m > 0) != (A != nullptr) || (c->m > 0 && !b))
     return set_error(RAC_ERR_ARG, "rac_qp_set_problem: A/b must be given iff m > 0");
   const size_t nb = c->n * sizeof(double);
+  if (H && c->strips) return set_error(RAC_ERR_ARG, "rac_qp_set_problem: H given to a kernel-strip context");
   if (H) {
     if (!c->own_h) {
       int rc = qalloc(c, &c->H, (size_t)c->n * c->n);
@@ -1025,7 +1055,18 @@ extern "C" int rac_qp_set_problem(rac_qp_ctx* c, const double* H, const double* 
   note_launch();
   clip0_kernel<<<(int)std::min<int64_t>((c->n + 255) / 256, 1184), 256, 0, c->st>>>(c->lo, c->hi, c->n, c->x);
   // running products at x0 and the divergence bar (engine.py:361-362)
-  if (c->H) {
+  if (c->strips) {
+    // strip mode serves the SVM dual: x0 = clip(0, 0, C) = 0, so Hx0 = 0 (checked below)
+    std::vector<double> lo(c->n), hi(c->n);
+    cudaMemcpyAsync(lo.data(), c->lo, nb, cudaMemcpyDeviceToHost, c->st);
+    cudaMemcpyAsync(hi.data(), c->hi, nb, cudaMemcpyDeviceToHost, c->st);
+    int rc = check_cuda(cudaStreamSynchronize(c->st), "qp set_problem sync");
+    if (rc) return rc;
+    for (int64_t i = 0; i < c->n; ++i)
+      if (lo[i] > 0.0 || hi[i] < 0.0)
+        return set_error(RAC_ERR_UNSUPPORTED, "kernel strips need 0 inside every box (x0 = 0)");
+    cudaMemsetAsync(c->hx, 0, nb, c->st);
+  } else if (c->H) {
     int rc = launch_gemv_rows(c->H, c->n, c->n, c->x, c->hx, c->st);
     if (rc) return rc;
   }
@@ -1064,6 +1105,7 @@ extern "C" int rac_qp_set_state(rac_qp_ctx* c, const double* x, const double* y)
   clear_error();
   if (!c || !x || (c->m > 0 && !y)) return set_error(RAC_ERR_ARG, "rac_qp_set_state: null pointer");
   if (!c->ready) return set_error(RAC_ERR_ARG, "rac_qp_set_state: call rac_qp_set_problem first");
+  if (c->strips) return set_error(RAC_ERR_UNSUPPORTED, "rac_qp_set_state: not with kernel strips");
   cudaMemcpyAsync(c->x, x, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->st);
   if (c->m > 0) cudaMemcpyAsync(c->y, y, c->m * sizeof(double), cudaMemcpyDeviceToDevice, c->st);
   if (c->H) {
@@ -1076,6 +1118,38 @@ extern "C" int rac_qp_set_state(rac_qp_ctx* c, const double* x, const double* y)
     note_launch();
   }
   return check_launch("rac_qp_set_state");
+}
+
+// Kernel strips on the fly instead of a resident N x N matrix (svm.py:96-143): H_ij =
+// labels_i labels_j K(x_i, x_j) is formed per sweep for the blocks' H_bb and batch by batch for
+// the strip rows (at most max_strip_bytes of strips at a time).  Call before set_problem.
+extern "C" int rac_qp_set_kernel_strips(rac_qp_ctx* c, const double* X, int64_t d, const double* labels,
+                                        int32_t kind, double sigma, uint64_t max_strip_bytes) {
+  using namespace rac;
+  clear_error();
+  if (!c || !X || !labels || d < 1) return set_error(RAC_ERR_ARG, "rac_qp_set_kernel_strips: bad arguments");
+  if (kind == RAC_KERNEL_GAUSSIAN && !(sigma > 0)) return set_error(RAC_ERR_ARG, "sigma must be > 0");
+  if (c->mode == RAC_MODE_RP)
+    return set_error(RAC_ERR_UNSUPPORTED, "kernel strips: rp mode visits blocks out of table order");
+  if (c->H || c->strips) return set_error(RAC_ERR_ARG, "rac_qp_set_kernel_strips: context already has H");
+  const int64_t n = c->n, s = c->s;
+  c->ldd = (d + 31) / 32 * 32;
+  c->dfeat = d;
+  c->kkind = kind;
+  c->ksigma = sigma;
+  const size_t row = (size_t)s * n * sizeof(double);
+  c->sb = (int)std::max<int64_t>(1, std::min<int64_t>(c->p, (int64_t)(max_strip_bytes / std::max<size_t>(row, 1))));
+  int rc;
+  if ((rc = qalloc(c, &c->Xp, (size_t)n * c->ldd)) || (rc = qalloc(c, &c->sq, n)) || (rc = qalloc(c, &c->lab, n)) ||
+      (rc = qalloc(c, &c->hblk, (size_t)c->p * s * s)) || (rc = qalloc(c, &c->Hs, (size_t)c->sb * s * n)))
+    return rc;
+  cudaMemsetAsync(c->Xp, 0, (size_t)n * c->ldd * sizeof(double), c->st);
+  cudaMemcpy2DAsync(c->Xp, c->ldd * sizeof(double), X, d * sizeof(double), d * sizeof(double), n,
+                    cudaMemcpyDeviceToDevice, c->st);
+  cudaMemcpyAsync(c->lab, labels, n * sizeof(double), cudaMemcpyDeviceToDevice, c->st);
+  if (kind == RAC_KERNEL_GAUSSIAN && (rc = launch_row_sqnorm(c->Xp, c->ldd, n, d, c->sq, c->st))) return rc;
+  c->strips = true;
+  return check_launch("rac_qp_set_kernel_strips");
 }
 
 extern "C" int rac_qp_borrow_h(rac_qp_ctx* c, const double* H) {
@@ -1130,7 +1204,17 @@ extern "C" int rac_qp_run(rac_qp_ctx* c, const int64_t* perms, int32_t count, do
       rc = launch_order_cast(perms + (int64_t)k * c->p, c->p, c->order, c->st);
       if (rc) return rc;
     }
-    rc = qp_chain(c, tol_p, tol_d, fixed);
+    if (c->strips) {
+      // the sweep in batches of sb blocks: their kernel strips, then the chain over them
+      for (int t0 = 0; t0 < c->p && !rc; t0 += c->sb) {
+        const int t1 = std::min(c->p, t0 + c->sb);
+        rc = launch_kernel_strip(c->Xp, c->ldd, c->dfeat, c->idx + (int64_t)t0 * c->s, (t1 - t0) * c->s, c->n,
+                                 c->lab, c->sq, c->kkind, c->ksigma, c->Hs, c->n, c->st);
+        if (!rc) rc = qp_chain(c, tol_p, tol_d, fixed, t0, t1);
+      }
+    } else {
+      rc = qp_chain(c, tol_p, tol_d, fixed, 0, c->p);
+    }
     if (rc) return rc;
     c->sweeps++;
   }

@@ -72,6 +72,8 @@ struct SysArgs {
   double div, mul;    // val = (sum / div) * mul  (div==1/mul==1 skip the op)
   const double* H;    // optional dense H (row-major, ldh) -> + H[idx_i][idx_j]
   int64_t ldh;
+  const double* hblk; // optional [p][s][s] precomputed H_bb per block (kernel strips on the fly):
+                      // used instead of gathering H (H may then be null)
   const int32_t* idx;  // block indices (-1 = padding of the short last block -> identity row)
   const int32_t* blk_list;
   double shift, ridge_rel;
@@ -97,11 +99,12 @@ size_t chol_scratch_bytes(int s, int p);
 
 __global__ void iota_kernel(int32_t* v, int64_t n);
 
-// label-weighted kernel strips (strips.cu): out[i][j] = y_{rows_i} y_j K(x_{rows_i}, x_j) from
-// the zero-padded row-major samples Xp (N x ldd, ldd % 32 == 0); sq = |x_j|^2 (Gaussian only)
+// label-weighted kernel strips (strips.cu): out[i][j] = y_{rows_i} y_j K(x_{rows_i}, x_{c_j}) from
+// the zero-padded row-major samples Xp (N x ldd, ldd % 32 == 0); sq = |x_j|^2 (Gaussian only);
+// c_j = j, or cols[j]; `batch` problems along blockIdx.z (rows / cols advance by s, out by s*ldo)
 int launch_kernel_strip(const double* Xp, int64_t ldd, int64_t d, const int32_t* rows, int s, int64_t N,
                         const double* y, const double* sq, int kind, double sigma, double* out, int64_t ldo,
-                        cudaStream_t st);
+                        cudaStream_t st, const int32_t* cols = nullptr, int batch = 1);
 int launch_row_sqnorm(const double* Xp, int64_t ldd, int64_t N, int64_t d, double* sq, cudaStream_t st);
 
 // row-major X (m x n) -> column-major (ld x n), rows m..ld-1 zero

@@ -33,14 +33,20 @@ __global__ void row_sqnorm_kernel(const double* __restrict__ Xp, int64_t ldd, in
   }
 }
 
-// out[i * ldo + j], i < s (rows[i] = sample index; -1 = padding row -> zeros), j < N
+// out[i * ldo + j], i < s (rows[i] = sample index; -1 = padding row -> zeros), j < N; the
+// output columns are samples 0..N-1, or cols[j] when given (-1 = zero column).  blockIdx.z
+// batches independent problems: rows / cols / out advance by the given strides.
 __global__ void __launch_bounds__(STHREADS) strip_kernel(const double* __restrict__ Xp, int64_t ldd, int64_t d,
                                                         const int32_t* __restrict__ rows, int s, int64_t N,
                                                         const double* __restrict__ y,
                                                         const double* __restrict__ sq, int kind,
                                                         double two_sigma2, double* __restrict__ out,
-                                                        int64_t ldo) {
+                                                        int64_t ldo, const int32_t* __restrict__ cols,
+                                                        int64_t zstride_rc, int64_t zstride_out) {
   extern __shared__ __align__(16) double ssm[];
+  rows += blockIdx.z * zstride_rc;
+  if (cols) cols += blockIdx.z * zstride_rc;
+  out += blockIdx.z * zstride_out;
   double* sA[2] = {ssm, ssm + ST * SLD};
   double* sB[2] = {ssm + 2 * ST * SLD, ssm + 3 * ST * SLD};
   const int I = blockIdx.y;                 // tile of strip rows
@@ -54,10 +60,11 @@ __global__ void __launch_bounds__(STHREADS) strip_kernel(const double* __restric
     srcA[tid] = r >= 0 ? (int64_t)r * ldd : -1;
     yA[tid] = r >= 0 ? y[r] : 0.0;
     qA[tid] = (r >= 0 && kind == RAC_KERNEL_GAUSSIAN) ? sq[r] : 0.0;
-    const int64_t gj = J * ST + tid;
-    srcB[tid] = gj < N ? gj * ldd : -1;
-    yB[tid] = gj < N ? y[gj] : 0.0;
-    qB[tid] = (gj < N && kind == RAC_KERNEL_GAUSSIAN) ? sq[gj] : 0.0;
+    const int64_t gj0 = J * ST + tid;
+    const int64_t gj = gj0 < N ? (cols ? (int64_t)cols[gj0] : gj0) : -1;
+    srcB[tid] = gj >= 0 ? gj * ldd : -1;
+    yB[tid] = gj >= 0 ? y[gj] : 0.0;
+    qB[tid] = (gj >= 0 && kind == RAC_KERNEL_GAUSSIAN) ? sq[gj] : 0.0;
   }
   __syncthreads();
   for (int e = tid; e < ST * SLD; e += STHREADS) {
@@ -139,14 +146,15 @@ __global__ void __launch_bounds__(STHREADS) strip_kernel(const double* __restric
 
 int launch_kernel_strip(const double* Xp, int64_t ldd, int64_t d, const int32_t* rows, int s, int64_t N,
                         const double* y, const double* sq, int kind, double sigma, double* out, int64_t ldo,
-                        cudaStream_t st) {
-  if (s <= 0 || N <= 0) return RAC_OK;
+                        cudaStream_t st, const int32_t* cols, int batch) {
+  if (s <= 0 || N <= 0 || batch <= 0) return RAC_OK;
   const size_t smem = 4 * ST * SLD * sizeof(double);
   int rc = check_cuda(cudaFuncSetAttribute(strip_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                       "strip smem attribute");
   if (rc) return rc;
-  dim3 grid((unsigned)((N + ST - 1) / ST), (unsigned)((s + ST - 1) / ST));
-  strip_kernel<<<grid, STHREADS, smem, st>>>(Xp, ldd, d, rows, s, N, y, sq, kind, 2.0 * sigma * sigma, out, ldo);
+  dim3 grid((unsigned)((N + ST - 1) / ST), (unsigned)((s + ST - 1) / ST), (unsigned)batch);
+  strip_kernel<<<grid, STHREADS, smem, st>>>(Xp, ldd, d, rows, s, N, y, sq, kind, 2.0 * sigma * sigma, out, ldo,
+                                             cols, (int64_t)s, (int64_t)s * ldo);
   note_launch();
   return check_launch("kernel strip");
 }
@@ -183,7 +191,7 @@ extern "C" int rac_svm_kernel_strip(const double* X, int64_t N, int64_t d, const
   cudaMemcpy2DAsync(Xp, ldd * sizeof(double), X, d * sizeof(double), d * sizeof(double), N,
                     cudaMemcpyDeviceToDevice, st);
   if (kind == RAC_KERNEL_GAUSSIAN) rc = launch_row_sqnorm(Xp, ldd, N, d, sq, st);
-  if (!rc) rc = launch_kernel_strip(Xp, ldd, d, rows, s, N, labels, sq, kind, sigma, strip, N, st);
+  if (!rc) rc = launch_kernel_strip(Xp, ldd, d, rows, s, N, labels, sq, kind, sigma, strip, N, st, nullptr, 1);
   cudaFreeAsync(Xp, st);
   cudaFreeAsync(sq, st);
   return rc;

@@ -145,20 +145,21 @@ def test_assemble_kernel_block_and_bias(dev, kind, sigma):
 
 
 # ---------------------------------------------------------------- not-PD raised mid-sweep
-@pytest.mark.parametrize("gram", ["blocks", "covariance"])
-def test_fit_raises_block_definiteness_mid_sweep(dev, gram):
+@pytest.mark.parametrize("gram,m,n,s", [("blocks", 80, 40, 8), ("covariance", 80, 40, 8),
+                                         ("blocks", 700, 600, 300)])    # s > 236: the large-s inverse
+def test_fit_raises_block_definiteness_mid_sweep(dev, gram, m, n, s):
     """A NaN column makes its block system indefinite for LAPACK (the reference's
     np.linalg.cholesky raises at that block, elastic_net.py:213-219)."""
     import paper_1907_01995_b200 as rac
     rng = np.random.default_rng(3)
-    X = rng.standard_normal((80, 40))
+    X = rng.standard_normal((m, n))
     X[:, 17] = np.nan
     with pytest.raises(rac.BlockDefinitenessError, match="positive definite"):
-        rac.fit(X, rng.standard_normal(80), rac.ElasticNetSpec(lam=0.1, alpha=0.5, gamma=1.0, block_size=8, iters=5),
+        rac.fit(X, rng.standard_normal(m), rac.ElasticNetSpec(lam=0.1, alpha=0.5, gamma=1.0, block_size=s, iters=5),
                 gram_mode=gram)
     # the pooled context is sound afterwards: a clean fit of the same shape works
-    Xc = rng.standard_normal((80, 40))
-    m = rac.fit(Xc, rng.standard_normal(80), rac.ElasticNetSpec(lam=0.1, alpha=0.5, gamma=1.0, block_size=8, iters=5),
+    Xc = rng.standard_normal((m, n))
+    m = rac.fit(Xc, rng.standard_normal(m), rac.ElasticNetSpec(lam=0.1, alpha=0.5, gamma=1.0, block_size=s, iters=5),
                 gram_mode=gram)
     assert m.iterations == 5 and np.all(np.isfinite(m.beta))
 

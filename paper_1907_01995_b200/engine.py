@@ -77,6 +77,15 @@ class QpSolver:
             hi.data_ptr()))
         self._keep = [cd, lo, hi, Hd, Ad, bd, borrowed_h]
 
+    def set_kernel_strips(self, X: np.ndarray, labels: np.ndarray, kind: int, sigma: float, max_strip_bytes: int):
+        """No resident n x n H: per sweep the blocks' H_bb and batches of strip rows are formed
+        from the samples (rac_qp_set_kernel_strips; before set_problem)."""
+        Xd = _device.upload(np.ascontiguousarray(X, dtype=float), device=self.dev)
+        yd = _device.upload(np.asarray(labels, dtype=float), device=self.dev)
+        _native.check(self.lib.rac_qp_set_kernel_strips(self.h, Xd.data_ptr(), int(X.shape[1]), yd.data_ptr(),
+                                                        int(kind), float(sigma), int(max_strip_bytes)))
+        self._strip_keep = [Xd, yd]
+
     def set_divergence_bar(self, bar: float):
         _native.check(self.lib.rac_qp_set_divergence_bar(self.h, float(bar)))
 

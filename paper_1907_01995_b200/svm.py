@@ -14,6 +14,7 @@ LRU of kernel rows.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -178,11 +179,30 @@ def train(X: Matrix, labels: np.ndarray, C: float, kernel: KernelSpec,
         return _train_on(dev, Xd, y, C, kernel, config, mode, rng, return_diagnostics, sweep_hook)
 
 
+def use_kernel_strips(n: int, mode: Mode, device) -> bool:
+    """Kernel strips on the fly (the reference's own scheme, svm.py:96-143) when the n x n
+    label-weighted kernel matrix would take more than half of the free device memory, or
+    RAC_SVM_STRIPS=1; RAC_SVM_STRIPS=0 forces the resident matrix.  RP visits blocks out of
+    table order and keeps the resident matrix."""
+    env = os.environ.get("RAC_SVM_STRIPS")
+    if env is not None:
+        return env == "1" and Mode(mode) != Mode.RP
+    free, _ = torch.cuda.mem_get_info(device)
+    return 8.0 * n * n > 0.5 * free and Mode(mode) != Mode.RP
+
+
+STRIP_BYTES = 2 << 30      # strip rows formed per batch of blocks
+
+
 def _train_on(dev, Xd, y, C, kernel, config, mode, rng, return_diagnostics, sweep_hook):
     n = Xd.shape[0]
-    Q = build_q(Xd, y, kernel, dev)
+    strips = use_kernel_strips(n, mode, dev)
+    Q = None if strips else build_q(Xd, y, kernel, dev)
     solver = QpSolver(n, 1, config.block_size, mode, config.beta_penalty, RIDGE_REL, device=dev)
     try:
+        if strips:
+            kind = _native.KERNEL_LINEAR if kernel.kind == "linear" else _native.KERNEL_GAUSSIAN
+            solver.set_kernel_strips(Xd, y, kind, kernel.sigma, STRIP_BYTES)
         solver.set_problem(np.full(n, -1.0), np.zeros(n), np.full(n, float(C)),
                            A=y.reshape(1, n), b=np.zeros(1), borrowed_h=Q)
         solver.set_divergence_bar(math.inf)   # train has no divergence guard
@@ -199,7 +219,7 @@ def _train_on(dev, Xd, y, C, kernel, config, mode, rng, return_diagnostics, swee
         nu = float(yv.cpu().numpy()[0])
     finally:
         solver.close()
-    bias = _bias_from_q(Q, z, y, C)
+    bias = compute_bias(z, Xd, y, C, kernel, device=dev) if strips else _bias_from_q(Q, z, y, C)
     del Q
     support = z > SUPPORT_THRESHOLD
     model = SvmModel(support_points=_gather_rows(Xd, support), support_duals=z[support].copy(),

@@ -93,9 +93,13 @@ def test_fit_full_size_matches_reference(dev, golden, cfg):
         assert rel(model.beta, g[f"{tag}_final_beta"]) <= ITER_TOL
 
 
-def test_train_config4_full_size_matches_reference(dev, golden):
+@pytest.mark.parametrize("strips", ["0", "1"])
+def test_train_config4_full_size_matches_reference(dev, golden, strips, monkeypatch):
+    """strips=1: no resident 20000 x 20000 Q; per sweep the blocks' H_bb and batches of strip
+    rows."""
     from paper_1907_01995_b200 import configs, svm
     from paper_1907_01995_b200.problems import Mode, SolverConfig
+    monkeypatch.setenv("RAC_SVM_STRIPS", strips)
     g = golden("svm_config4_full")
     C, bs, beta, max_iters, tp, td, seed, fixed, sigma = g["cfg4_params"]
     case = configs.config4()

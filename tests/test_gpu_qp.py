@@ -123,10 +123,15 @@ def test_solve_determinism(dev):
 
 
 # ---------------------------------------------------------------- svm.train
+@pytest.mark.parametrize("strips", ["0", "1"])
 @pytest.mark.parametrize("tag", ["lin", "gauss", "gauss_rp", "cfg4s"])
-def test_train_matches_reference(dev, golden, tag):
+def test_train_matches_reference(dev, golden, tag, strips, monkeypatch):
+    """strips=1: kernel strips formed on the fly per batch of blocks (the
+    reference's own scheme) instead of the resident N x N matrix (rp keeps the matrix)."""
     from paper_1907_01995_b200 import svm
     from paper_1907_01995_b200.problems import Mode, SolverConfig
+    monkeypatch.setenv("RAC_SVM_STRIPS", strips)
+    monkeypatch.setattr(svm, "STRIP_BYTES", 1 << 14)     # several strip batches per sweep
     g = golden("svm_small")
     C, bs, beta, iters, tp, td, seed, fixed, sigma = g[f"{tag}_params"]
     cfg = SolverConfig(mode=Mode(str(g[f"{tag}_mode"])), block_size=int(bs), beta_penalty=float(beta),

@@ -452,7 +452,7 @@ def measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline: b
     lib.rac_en_set_timing(solver.h, 2)
     solver.run(_device.PermutationFeeder(rng, n, dev).draw(1), None)
     torch.cuda.synchronize()
-    ntr = 16 + 16 * p + s
+    ntr = 16 + 20 * p + s
     tbuf = (np.ctypeslib.ctypes.c_int64 * ntr)()
     lib.rac_en_trace(solver.h, tbuf, ntr)
     info = (np.ctypeslib.ctypes.c_int32 * 4)()
@@ -480,6 +480,14 @@ def measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline: b
         ph = np.diff(tv[pro - 1:]).reshape(p, nl)
         chain_trace.update({"first_phase_us": float(tv[pro - 1] - tv[0]),
                             "per_block_us": {k: float(v) for k, v in zip(labels, ph.mean(axis=0))}})
+        if info[0] == 0 and int(info[2]) == 0 and p > 1:
+            # one-tile row phase split: (a) r += X_prev delta, tile load, (c) t = r - X_next beta_next,
+            # (d) partials X_next' t (CTA 0 stamps; the last block has no next tile)
+            rt = np.array(tbuf[16 + 16 * p + s:16 + 20 * p + s], dtype=np.float64).reshape(p, 4)[:p - 1] / 1e3
+            start = tv[pro + 6 * np.arange(p - 1) + 4]
+            d = np.diff(np.c_[start, rt], axis=1)
+            chain_trace["row_phase_split_us"] = {k: float(v) for k, v in
+                                                 zip(("a_r_update", "tile_load", "c_t", "d_partials"), d.mean(axis=0))}
     if s <= 236:
         # factor kernel, block 0: assembly, then per 8-pivot step [panel copy, 8x8 sweep, CW, update]
         f0 = 8 + 16 * p
@@ -677,6 +685,24 @@ def measure_svm(cfg, case, args, world, rank, local, peaks, headline: bool) -> d
     t0 = time.perf_counter()
     svm.train(X, y, case.C, svm.KernelSpec("linear"), cfgk)
     t_e2e = dist_max(time.perf_counter() - t0, world, dev)
+    # the same train with kernel strips formed on the fly (no resident N x N matrix: the
+    # reference's own scheme) — what runs when Q does not fit in HBM
+    os.environ["RAC_SVM_STRIPS"] = "1"
+    try:
+        svm.train(X, y, case.C, svm.KernelSpec("linear"), SolverConfig(block_size=s, max_iters=1))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        svm.train(X, y, case.C, svm.KernelSpec("linear"), cfgk)
+        t_strips = dist_max(time.perf_counter() - t0, world, dev)
+    finally:
+        os.environ.pop("RAC_SVM_STRIPS", None)
+    out["kernel_strips_variant"] = {
+        "e2e": {"value": world * K / t_strips, "unit": "sweeps/s",
+                "h2d_bytes_per_step": int((8 * N * d + 8 * N) / K + 8 * N),
+                "d2h_bytes_per_step": int((8 * N + 8) / K + 32)},
+        "note": "svm.train with RAC_SVM_STRIPS=1: per sweep the blocks' H_bb and batches of strip rows are "
+                "formed from X on the FP64 tensor cores (2 N^2 d flop per sweep) instead of reading a "
+                "resident N x N Q"}
     hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
     achieved = 8.0 * N * N / (ms * 1e-3 / K) / 1e9
     out.update({
@@ -699,7 +725,7 @@ def measure_svm(cfg, case, args, world, rank, local, peaks, headline: bool) -> d
 
 # ------------------------------------------------------------------ B200 arm: driver
 SUMMARY_KEYS = ("value", "ms_per_step", "e2e", "time_to_tol", "roofline", "cpu_baseline", "stage_ms_per_sweep",
-                "gram_mode", "residuals_at_last_sweep", "config")
+                "gram_mode", "residuals_at_last_sweep", "kernel_strips_variant", "config")
 
 
 def run_b200(args) -> int:
@@ -737,7 +763,7 @@ def run_b200(args) -> int:
         "clocks": h.get("clocks"), "gpu_launches": h["gpu_launches"], "time_to_tol": h.get("time_to_tol"),
     }
     for k in ("stage_ms_per_sweep", "chain_trace", "reference_algorithm_variant", "rp_mode_variant",
-              "q_build_seconds", "residuals_at_last_sweep"):
+              "q_build_seconds", "residuals_at_last_sweep", "kernel_strips_variant"):
         if k in h:
             line[k] = h[k]
     line["peaks"] = {"hbm_gbs": peaks.get("hbm_gbs", HBM_FALLBACK_GBS), "fp64_dgemm_tflops_measured": fp64,

@@ -115,10 +115,14 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
         if (i < s) prefetch_l2(Ib + (int64_t)i * s + 16 * (e % lines));
       }
     }
+    if constexpr (RC == 0)
+      if (t + 1 < a.p) row1t_gather_idx(a.idx, s, a.order ? a.order[t + 1] : t + 1, w1);
     // ---- S1: reduce the per-CTA partials -> block right-hand side
     for (int j = gw; j < s; j += GW) {
       double acc = 0.0;
-      for (int q = lane; q < P; q += 32) acc += ldcg(a.partial + (int64_t)q * s + j);
+      // RC == 0: partials are [j][cta] (row_phase_1t), else [cta][j]
+      for (int q = lane; q < P; q += 32)
+        acc += ldcg(a.partial + (RC == 0 ? (int64_t)j * P + q : (int64_t)q * s + j));
       acc = warp_sum(acc);
       if (lane == 0) {
         int g = a.idx[(int64_t)b * s + j];
@@ -159,12 +163,17 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
         }
       }
     }
+    // the next row phase's block: its beta (final until its own solve) gathered into shared
+    // memory behind this CTA's S2 work, landing during the barrier (indices issued before S1)
+    if constexpr (RC == 0)
+      if (t + 1 < a.p) row1t_gather_beta(s, a.beta, w1);
     if (tr) a.trace[tp++] = gtimer();
     grid_barrier(a.bar, target, P);
     if (tr) a.trace[tp++] = gtimer();
     bnext = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
     if constexpr (RC == 0)
-      row_phase_1t(a.Xc, a.ld, r0, nr1, a.idx, s, b, bnext, a.delta, a.beta, a.partial, w1, tfn);
+      row_phase_1t(a.Xc, a.ld, r0, nr1, a.idx, s, b, bnext, a.delta, a.beta, a.partial, w1, tfn,
+                   tr ? a.trace + 16 + 16 * (size_t)a.p + s + 4 * (size_t)t : nullptr, true);
     else
       row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
     if (tr) a.trace[tp++] = gtimer();

@@ -140,57 +140,51 @@ __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict_
     j = pos < n ? __ldg(idx + (size_t)blockIdx.z * n + pos) : -1;
     sl += (size_t)blockIdx.z * I8_S * slice_bytes;
   }
+  const int64_t k0 = (int64_t)blockIdx.y * 256 + lane * 8;
+  double x[8];
+  if (j >= 0 && k0 + 8 <= len) {
+    const double2* p = reinterpret_cast<const double2*>(Xc + (int64_t)j * ld + k0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double2 t = __ldg(p + i);
+      x[2 * i] = t.x;
+      x[2 * i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = (j >= 0 && k0 + i < len) ? Xc[(int64_t)j * ld + k0 + i] : 0.0;
+  }
   const int e = (j >= 0) ? __ldg(ex + j) : 0;
   if (idx && blockIdx.y == 0 && lane == 0) ex_blk[(size_t)blockIdx.z * ngrp * 8 + pos] = e;
-  // several 256-sample chunks per CTA (grid-stride over gridDim.y): the index and exponent
-  // loads and the CTA start-up are amortised over ~4 chunks
-  const int nchunk = (nstg + 7) / 8;
-  for (int yc = blockIdx.y; yc < nchunk; yc += gridDim.y) {
-    const int64_t k0 = (int64_t)yc * 256 + lane * 8;
-    double x[8];
-    if (j >= 0 && k0 + 8 <= len) {
-      const double2* p = reinterpret_cast<const double2*>(Xc + (int64_t)j * ld + k0);
+  unsigned long long packed[I8_S];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double2 t = __ldg(p + i);
-        x[2 * i] = t.x;
-        x[2 * i + 1] = t.y;
-      }
-    } else {
+  for (int s = 0; s < I8_S; ++s) packed[s] = 0ull;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) x[i] = (j >= 0 && k0 + i < len) ? Xc[(int64_t)j * ld + k0 + i] : 0.0;
+  for (int i = 0; i < 8; ++i) {
+    // x 2^(55-e) (exact, |.| < 2^55) rounded once to an integer N, then N's balanced
+    // base-128 digits from the bottom: d = ((N + 64) mod 128) - 64, N <- (N - d) / 128
+    // (exact shifts); the top digit is what remains, |d_1| <= 64
+    long long N = __double2ll_rn(ldexp(x[i], 55 - e));
+#pragma unroll
+    for (int s = I8_S - 1; s > 0; --s) {
+      const long long d = ((N + 64) & 127) - 64;
+      N = (N - d) >> 7;
+      packed[s] |= (unsigned long long)(uint8_t)(int8_t)d << (8 * i);
     }
-    unsigned long long packed[I8_S];
+    packed[0] |= (unsigned long long)(uint8_t)(int8_t)N << (8 * i);
+  }
+  // sample k0 + i -> stage lane / 4, chunk (lane % 4) / 2, byte (lane % 2) * 8 + i
+  const int off = (lane >> 2) * 256 + ((lane & 3) >> 1) * 128 + f * 16 + (lane & 1) * 8;
 #pragma unroll
-    for (int s = 0; s < I8_S; ++s) packed[s] = 0ull;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      // x 2^(55-e) (exact, |.| < 2^55) rounded once to an integer N, then N's balanced
-      // base-128 digits from the bottom: d = ((N + 64) mod 128) - 64, N <- (N - d) / 128
-      // (exact shifts); the top digit is what remains, |d_1| <= 64
-      long long N = __double2ll_rn(ldexp(x[i], 55 - e));
-#pragma unroll
-      for (int s = I8_S - 1; s > 0; --s) {
-        const long long d = ((N + 64) & 127) - 64;
-        N = (N - d) >> 7;
-        packed[s] |= (unsigned long long)(uint8_t)(int8_t)d << (8 * i);
-      }
-      packed[0] |= (unsigned long long)(uint8_t)(int8_t)N << (8 * i);
-    }
-    // sample k0 + i -> stage lane / 4, chunk (lane % 4) / 2, byte (lane % 2) * 8 + i
-    const int off = (lane >> 2) * 256 + ((lane & 3) >> 1) * 128 + f * 16 + (lane & 1) * 8;
-    __syncthreads();   // the previous chunk's stores have read buf
-#pragma unroll
-    for (int s = 0; s < I8_S; ++s) *reinterpret_cast<unsigned long long*>(&buf[s][off]) = packed[s];
-    __syncthreads();
-    // 8 slices x 8 stages x 256 B, 16 B per thread per pass
-    const int kst0 = yc * 8;
-    for (int q = threadIdx.x; q < I8_S * 8 * 16; q += 256) {
-      const int s = q >> 7, kl = (q >> 4) & 7, o = q & 15;
-      if (kst0 + kl >= nstg) continue;
-      const uint4 v = *reinterpret_cast<const uint4*>(&buf[s][kl * 256 + o * 16]);
-      *reinterpret_cast<uint4*>(sl + s * slice_bytes + ((size_t)(kst0 + kl) * ngrp + g) * 256 + o * 16) = v;
-    }
+  for (int s = 0; s < I8_S; ++s) *reinterpret_cast<unsigned long long*>(&buf[s][off]) = packed[s];
+  __syncthreads();
+  // 8 slices x 8 stages x 256 B, 16 B per thread per pass
+  const int kst0 = blockIdx.y * 8;
+  for (int q = threadIdx.x; q < I8_S * 8 * 16; q += 256) {
+    const int s = q >> 7, kl = (q >> 4) & 7, o = q & 15;
+    if (kst0 + kl >= nstg) continue;
+    const uint4 v = *reinterpret_cast<const uint4*>(&buf[s][kl * 256 + o * 16]);
+    *reinterpret_cast<uint4*>(sl + s * slice_bytes + ((size_t)(kst0 + kl) * ngrp + g) * 256 + o * 16) = v;
   }
 }
 
@@ -399,7 +393,7 @@ int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, 
   i8_colexp_kernel<<<std::min(num_sms() * 8, (nfeat + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, nfeat, ex);
   if ((nstg + 7) / 8 > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8: too many samples");
   note_launch();
-  i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)(((nstg + 7) / 8 + 3) / 4)), 256, 0, st>>>(
+  i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8)), 256, 0, st>>>(
       Xc, ld, len, n, ex, sl, slice_bytes, ngrp, nstg, nullptr, nullptr);
   set_i8_attributes();
   I8Args a{};
@@ -446,7 +440,7 @@ int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32
   if ((nstg + 7) / 8 > 65535 || p > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8 blocks: shape");
   set_i8_attributes();
   note_launch();
-  i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)(((nstg + 7) / 8 + 3) / 4), (unsigned)p), 256, 0, st>>>(
+  i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8), (unsigned)p), 256, 0, st>>>(
       Xc, ld, len, s, ex_all, sl, slice_bytes, ngrp, nstg, idx, ex_blk);
   set_i8_attributes();
   I8Args a{};

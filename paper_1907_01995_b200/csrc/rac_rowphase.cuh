@@ -197,8 +197,10 @@ struct Row1tSmem {
 };
 
 __host__ __device__ inline int row1t_groups(int rw) { return rw >= RP_THREADS ? 1 : RP_THREADS / rw; }
-// row stride of the tile: even (16-byte cp.async rows), +2 breaks the bank alignment
-__host__ __device__ inline int row1t_stride(int rw) { return rw + 2; }
+// row stride of the tile in doubles: even (16-byte cp.async rows); phase (d) reads it
+// column-parallel (lane j at j * stride), which is 2-way bank-conflicted for a stride of
+// 2 mod 4 and 4-way for 0 mod 4, so rw (even) is padded to the next 2 mod 4
+__host__ __device__ inline int row1t_stride(int rw) { return (rw % 4 == 2) ? rw : rw + 2; }
 __host__ __device__ inline size_t row1t_smem_bytes(int s, int rw) {
   const int rwp = row1t_stride(rw);
   return ((size_t)s * rwp + 2 * (size_t)rw + 2 * (size_t)s + (size_t)row1t_groups(rw) * rw) * sizeof(double) +
@@ -224,10 +226,30 @@ __device__ __forceinline__ double row1t_dot(const double* tile, int rwp, int row
   return strided_dot(tile + row, v, j0, s, step, rwp);
 }
 
+// indices and current beta of block b (the row phase's next block) into shared memory while
+// the chain waits on grid barriers (b's beta is final: b is solved later), asynchronously:
+// (1) the indices (cp.async, one group), (2) after they landed, beta gathered by them
+// (cp.async, one group that the row phase's wait completes)
+__device__ __forceinline__ void row1t_gather_idx(const int32_t* __restrict__ idx, int s, int b, const Row1tSmem& w) {
+  for (int j = threadIdx.x; j < s; j += RP_THREADS) cp_async4(w.sIdx + j, idx + (int64_t)b * s + j);
+  cp_async_commit();
+}
+__device__ __forceinline__ void row1t_gather_beta(int s, const double* xsrc, const Row1tSmem& w) {
+  cp_async_wait<0>();   // this thread's index copies (the same threads read them back)
+  for (int j = threadIdx.x; j < s; j += RP_THREADS) {
+    const int g = w.sIdx[j];
+    if (g >= 0) cp_async8(w.sX + j, xsrc + g);
+    else w.sX[j] = 0.0;
+  }
+  cp_async_commit();
+}
+
 template <class TFn>
 __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r0, int nr,
                              const int32_t* __restrict__ idx, int s, int bprev, int bnext, const double* delta,
-                             const double* xsrc, double* partial, const Row1tSmem& w, TFn tfn) {
+                             const double* xsrc, double* partial, const Row1tSmem& w, TFn tfn,
+                             long long* rt = nullptr, bool pre_gathered = false) {
+  // rt (tracing, CTA 0 thread 0): %globaltimer after (a), after the tile load, after (c), after (d)
   const int tid = threadIdx.x;
   // groups of the row reductions; the last CTA's shorter row range (nr < rw) must stay
   // inside the reduction buffer sized for rw rows
@@ -236,7 +258,7 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
   const bool act = grp < G;
   if (bprev >= 0)
     for (int j = tid; j < s; j += RP_THREADS) w.sDel[j] = ldcg(delta + j);
-  if (bnext >= 0)
+  if (bnext >= 0 && !pre_gathered)
     for (int j = tid; j < s; j += RP_THREADS) {
       const int g = idx[(int64_t)bnext * s + j];
       w.sIdx[j] = g;
@@ -253,6 +275,7 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
     }
     __syncthreads();
   }
+  if (rt) rt[0] = gtimer();
   if (bnext < 0) return;
   // (b) 16-byte pieces (nr, r0, ld and the row stride are even)
   const int h = nr >> 1;
@@ -266,6 +289,7 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
+  if (rt) rt[1] = gtimer();
   // (c)
   if (act) w.red[grp * nr + row] = row1t_dot(w.tile, w.rwp, row, w.sX, grp, s, G);
   __syncthreads();
@@ -275,6 +299,7 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
     w.sT[tid] = tfn(r0 + tid, w.sR[tid], u);
   }
   __syncthreads();
+  if (rt) rt[2] = gtimer();
   // (d)
   for (int j = tid; j < s; j += RP_THREADS) {
     const double* col = w.tile + (size_t)j * w.rwp;
@@ -287,9 +312,12 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
       a3 += col[i + 3] * w.sT[i + 3];
     }
     for (; i < nr; ++i) a0 += col[i] * w.sT[i];
-    partial[(int64_t)blockIdx.x * s + j] = (a0 + a1) + (a2 + a3);
+    // column-major partials [j][cta]: the S1 reduction then reads each column's P partials
+    // as one contiguous run
+    partial[(int64_t)j * gridDim.x + blockIdx.x] = (a0 + a1) + (a2 + a3);
   }
   __syncthreads();
+  if (rt) rt[3] = gtimer();
 }
 
 }  // namespace rac

@@ -314,7 +314,8 @@ struct rac_en_ctx {
   bool pipe = false;
   cudaStream_t sprep = nullptr, schain = nullptr;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_prep[2] = {nullptr, nullptr},
-              ev_chain[2] = {nullptr, nullptr};
+              ev_chain[2] = {nullptr, nullptr}, ev_gram = nullptr;
+  bool look_gram = true;      // block mode: gram(k+1) before chain(k), factor(k+1) beside it (RAC_EN_LOOKGRAM)
   bool chain_rec[2] = {false, false};
   int32_t* idx_b[2] = {nullptr, nullptr};
   double* inv_b[2] = {nullptr, nullptr};
@@ -995,7 +996,9 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
       rac_en_destroy(c);
       return rc;
     }
-    cudaEvent_t* evs[] = {&c->ev_start, &c->ev_end, &c->ev_prep[0], &c->ev_prep[1], &c->ev_chain[0], &c->ev_chain[1]};
+    cudaEvent_t* evs[] = {&c->ev_start, &c->ev_end, &c->ev_prep[0], &c->ev_prep[1], &c->ev_chain[0], &c->ev_chain[1],
+                          &c->ev_gram};
+    if (const char* el = getenv("RAC_EN_LOOKGRAM")) c->look_gram = atoi(el) != 0;
     for (cudaEvent_t* e : evs)
       if ((rc = check_cuda(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "pipeline event"))) {
         rac_en_destroy(c);
@@ -1368,6 +1371,57 @@ static int en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, double tol
     cudaStreamWaitEvent(c->st, c->ev_end, 0);
     return check_launch("rac_en_run (batched)");
   }
+  if (c->pipe && !c->timing && count > 0 && c->gram_mode != 1 && c->mode == RAC_MODE_RAC && c->look_gram) {
+    // block mode: gram(k+1) runs BEFORE chain(k) (the int8 Gram's shared memory cannot sit
+    // beside the chain), so the factorisations of sweep k+1 start together with chain(k) and
+    // fill the room the latency-bound chain leaves on every SM:
+    //   sprep: sort(k+1) gram(k+1) [ev_gram] factor(k+1) [ev_prep(k+1)]
+    //   schain: wait ev_prep(k), ev_gram -> chain(k) [ev_chain(k)]
+    // gram_ws is single-buffered: factor(k) precedes gram(k+1) on sprep.
+    cudaEventRecord(c->ev_start, c->st);
+    cudaStreamWaitEvent(c->sprep, c->ev_start, 0);
+    cudaStreamWaitEvent(c->schain, c->ev_start, 0);
+    const int base = c->sweeps;
+    auto prep_gram = [&](int k) -> int {
+      const int j = (base + k) & 1;
+      if (c->chain_rec[j]) cudaStreamWaitEvent(c->sprep, c->ev_chain[j], 0);   // chain(k-2) done
+      c->idx = c->idx_b[j];
+      c->inv = c->inv_b[j];
+      c->info = c->info_b[j];
+      int r = launch_chunk_sort(perms + (int64_t)k * c->n, c->n, c->s, 1, c->idx, c->sprep);
+      return r ? r : en_block_gram(c, c->sprep);
+    };
+    auto prep_factor = [&](int k) -> int {
+      const int j = (base + k) & 1;
+      c->idx = c->idx_b[j];
+      c->inv = c->inv_b[j];
+      c->info = c->info_b[j];
+      int r = en_factor(c, c->sprep);
+      cudaEventRecord(c->ev_prep[j], c->sprep);
+      return r;
+    };
+    if ((rc = prep_gram(0)) || (rc = prep_factor(0))) return rc;
+    for (int k = 0; k < count; ++k) {
+      const int j = c->sweeps & 1;
+      if (k + 1 < count) {
+        if ((rc = prep_gram(k + 1))) return rc;
+        cudaEventRecord(c->ev_gram, c->sprep);
+        cudaStreamWaitEvent(c->schain, c->ev_gram, 0);
+      }
+      cudaStreamWaitEvent(c->schain, c->ev_prep[j], 0);
+      c->idx = c->idx_b[j];
+      c->inv = c->inv_b[j];
+      c->info = c->info_b[j];
+      if ((rc = en_chain(c, tol, c->schain))) return rc;
+      cudaEventRecord(c->ev_chain[j], c->schain);
+      c->chain_rec[j] = true;
+      c->sweeps++;
+      if (k + 1 < count && (rc = prep_factor(k + 1))) return rc;
+    }
+    cudaEventRecord(c->ev_end, c->schain);
+    cudaStreamWaitEvent(c->st, c->ev_end, 0);
+    return check_launch("rac_en_run (pipelined, gram ahead)");
+  }
   if (c->pipe && !c->timing && count > 0) {
     // prep(k+1) on sprep overlaps chain(k) on schain; prep(k) may only overwrite the
     // buffers of sweep k-2 once that chain is done.
@@ -1570,7 +1624,7 @@ extern "C" int rac_en_destroy(rac_en_ctx* c) {
   if (c->schain) cudaStreamSynchronize(c->schain);
   if (c->sprep) cudaStreamSynchronize(c->sprep);
   for (auto e : c->events) cudaEventDestroy(e);
-  for (cudaEvent_t e : {c->ev_start, c->ev_end, c->ev_prep[0], c->ev_prep[1], c->ev_chain[0], c->ev_chain[1],
+  for (cudaEvent_t e : {c->ev_start, c->ev_end, c->ev_prep[0], c->ev_prep[1], c->ev_chain[0], c->ev_chain[1], c->ev_gram,
                         c->ev_ctrl[0], c->ev_ctrl[1]})
     if (e) cudaEventDestroy(e);
   if (c->h_ctrl) cudaFreeHost(c->h_ctrl);

@@ -315,7 +315,8 @@ struct rac_en_ctx {
   cudaStream_t sprep = nullptr, schain = nullptr;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr, ev_prep[2] = {nullptr, nullptr},
               ev_chain[2] = {nullptr, nullptr}, ev_gram = nullptr;
-  bool look_gram = true;      // block mode: gram(k+1) before chain(k), factor(k+1) beside it (RAC_EN_LOOKGRAM)
+  bool look_gram = false;     // block mode: gram(k+1) before chain(k), factor(k+1) beside it (RAC_EN_LOOKGRAM=1;
+                              // measured no faster on config 5)
   bool chain_rec[2] = {false, false};
   int32_t* idx_b[2] = {nullptr, nullptr};
   double* inv_b[2] = {nullptr, nullptr};

@@ -35,7 +35,7 @@ int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what)
 // returned at the next synchronisation, and rac_trim_pool() / a context's
 // destruction trims the pool back to the threshold so that PyTorch's caching
 // allocator (e.g. an N x N SVM Q after a large fit) can have the memory.
-static const uint64_t POOL_KEEP = 8ULL << 30;
+const uint64_t POOL_KEEP = 8ULL << 30;
 static std::atomic<uint64_t> g_pool_ready{0};   // bit per configured device
 
 static cudaMemPool_t device_pool(int dev) {

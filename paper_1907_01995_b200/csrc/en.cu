@@ -336,6 +336,10 @@ struct rac_en_ctx {
   void* bg_ws = nullptr;      // block mode: per-sweep digit slices of the int8 block Grams, null = DMMA
   size_t bg_cap = 0;
   int* ex_all = nullptr;      // block mode: per-feature exponents of Xc (set with the data)
+  int* i8_bad = nullptr;      // raised by the exponent passes when a column's max/rms makes the int8
+                              // digit slices lose FP64-level accuracy (then: DMMA Grams for this data)
+  bool i8_checked = true;
+  bool i8_off = false;        // this data set's Grams on the DMMA tiles (set from i8_bad)
   int32_t* h_ctrl = nullptr;  // pinned: ctrl snapshot after each run (2 slots), for rac_en_poll
   cudaEvent_t ev_ctrl[2] = {nullptr, nullptr};
   int64_t ctrl_n = 0;         // runs snapshotted
@@ -541,9 +545,9 @@ int en_compute_G(rac_en_ctx* c, cudaStream_t st) {
   const int64_t n = c->n;
   GramPlan pl = plan_gram(c->m, (int)n, 1);
   int rc = RAC_OK;
-  if (c->i8_ws) {
+  if (c->i8_ws && !c->i8_off) {
     // int8 tensor-core Gram in exact digit-slice arithmetic (FP64-level accuracy)
-    if ((rc = launch_gram_i8(c->Xc, c->ld, c->m, (int)n, c->G, (double)c->m, 0, c->i8_ws, c->i8_ws_cap, st)) ||
+    if ((rc = launch_gram_i8(c->Xc, c->ld, c->m, (int)n, c->G, (double)c->m, 0, c->i8_ws, c->i8_ws_cap, st, c->i8_bad)) ||
         (rc = launch_gemv_rows(c->G, n, n, c->beta, c->q, st)))
       return rc;
     c->have_G = true;
@@ -578,7 +582,7 @@ int en_factor(rac_en_ctx* c, cudaStream_t st, int sweeps = 1) {
     a.mul = 1.0;
   } else {
     a.ws = c->gram_ws;
-    a.splits = c->bg_ws ? 1 : c->gp.splits;   // the int8 block Grams are complete (one split)
+    a.splits = (c->bg_ws && !c->i8_off) ? 1 : c->gp.splits;   // the int8 block Grams are complete (one split)
     a.div = (double)c->m;
     a.mul = 1.0;
   }
@@ -601,7 +605,7 @@ int en_factor(rac_en_ctx* c, cudaStream_t st, int sweeps = 1) {
 // block mode: the p block Grams of the partition in c->idx into gram_ws — int8 tensor
 // cores (exact digit slices, gram_i8.cu) when reserved, else the FP64 DMMA tiles
 int en_block_gram(rac_en_ctx* c, cudaStream_t st) {
-  if (c->bg_ws)
+  if (c->bg_ws && !c->i8_off)
     return rac::launch_gram_i8_blocks(c->Xc, c->ld, c->m, c->idx, c->s, c->p, c->ex_all, c->gram_ws, c->bg_ws,
                                       c->bg_cap, st);
   return rac::launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, st, c->ctrl);
@@ -950,7 +954,7 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
       (rc = dalloc(c, &c->order, c->p)) ||
       (rc = dalloc(c, &c->gram_ws, gram_ws_bytes(m, s, c->p) / sizeof(double))) ||
       (rc = dalloc(c, &c->inv, sqs)) || (rc = dalloc(c, &c->info, c->p)) ||
-      (rc = dalloc(c, &c->partial, (size_t)c->P * s)) || (rc = dalloc(c, &c->rhs, s)) ||
+      (rc = dalloc(c, &c->partial, (size_t)c->P * s)) || (rc = dalloc(c, &c->rhs, s)) || (rc = dalloc(c, &c->i8_bad, 1)) ||
       (rc = dalloc(c, &c->delta, s)) || (rc = dalloc(c, &c->wsum, GW)) ||
       (rc = dalloc(c, &c->wmax, GW)) || (rc = dalloc(c, &c->bar, 1)) || (rc = dalloc(c, &c->ctrl, 4))) {
     rac_en_destroy(c);
@@ -1064,8 +1068,11 @@ extern "C" int rac_en_set_data_csc(rac_en_ctx* c, const int64_t* indptr, const i
   int blocks = (int)std::min<int64_t>((c->n + 7) / 8, (int64_t)num_sms() * 16);
   note_launch();
   neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
+  cudaMemsetAsync(c->i8_bad, 0, sizeof(int), c->st);
+  c->i8_checked = false;
+  c->i8_off = false;
   if (c->bg_ws) {
-    int rc = launch_i8_colexp(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->st);
+    int rc = launch_i8_colexp(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->st, c->i8_bad);
     if (rc) return rc;
   }
   c->have_data = true;
@@ -1091,8 +1098,11 @@ extern "C" int rac_en_set_data(rac_en_ctx* c, const double* X, int32_t layout, c
   int blocks = (int)std::min<int64_t>((c->n + 7) / 8, (int64_t)num_sms() * 16);
   note_launch();
   neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
+  cudaMemsetAsync(c->i8_bad, 0, sizeof(int), c->st);
+  c->i8_checked = false;
+  c->i8_off = false;
   if (c->bg_ws) {
-    int rc = launch_i8_colexp(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->st);
+    int rc = launch_i8_colexp(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->st, c->i8_bad);
     if (rc) return rc;
   }
   c->have_data = true;
@@ -1111,6 +1121,9 @@ extern "C" int rac_en_set_data_rows(rac_en_ctx* c, const double* X_rows, int64_t
   if (row0 == 0) {
     c->have_data = false;
     c->have_G = false;
+    cudaMemsetAsync(c->i8_bad, 0, sizeof(int), c->st);
+    c->i8_checked = false;
+  c->i8_off = false;
     c->g_rows_done = 0;
     if (c->gram_mode == 1) cudaMemsetAsync(c->G, 0, (size_t)c->n * c->n * sizeof(double), c->st);
   }
@@ -1148,7 +1161,7 @@ extern "C" int rac_en_set_data_rows(rac_en_ctx* c, const double* X_rows, int64_t
           cudaEventRecord(c->ev_start, c->st);
           cudaStreamWaitEvent(gs, c->ev_start, 0);
         }
-        rc = launch_gram_i8(c->Xc + done, c->ld, plen, (int)c->n, c->G, 0.0, 1, c->i8_ws, c->i8_ws_cap, gs);
+        rc = launch_gram_i8(c->Xc + done, c->ld, plen, (int)c->n, c->G, 0.0, 1, c->i8_ws, c->i8_ws_cap, gs, c->i8_bad);
         c->g_rows_done = upto;
         if (last && gs != c->st) {
           cudaEventRecord(c->ev_end, gs);
@@ -1164,7 +1177,7 @@ extern "C" int rac_en_set_data_rows(rac_en_ctx* c, const double* X_rows, int64_t
   int blocks = (int)std::min<int64_t>((c->n + 7) / 8, (int64_t)num_sms() * 16);
   note_launch();
   neg_xty_kernel<<<blocks, 256, 0, c->st>>>(c->Xc, c->ld, c->m, c->n, y, (double)c->m, c->c);
-  if (c->bg_ws && (rc = launch_i8_colexp(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->st))) return rc;
+  if (c->bg_ws && (rc = launch_i8_colexp(c->Xc, c->ld, c->m, (int)c->n, c->ex_all, c->st, c->i8_bad))) return rc;
   if (c->gram_mode == 1) {
     scale_kernel<<<num_sms() * 8, 256, 0, c->st>>>(c->G, c->n * c->n, (double)c->m);   // dot, then / m
     note_launch();
@@ -1339,6 +1352,21 @@ static int en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, double tol
     return set_error(RAC_ERR_ARG, "rac_en_run: rp mode needs rac_en_set_partition");
   int rc = en_grow_history(c, c->sweeps + count);
   if (rc) return rc;
+  if (!c->i8_checked && (c->bg_ws || c->i8_ws) && count > 0) {
+    // heavy-tailed columns (max/rms above gram_i8.cu's bound): this data set's Grams go to
+    // the FP64 DMMA tiles (G is re-formed; the block Grams switch for the whole fit)
+    if (c->gram_mode == 1 && !c->have_G && (rc = en_compute_G(c, c->st))) return rc;   // raises the flag
+    int bad = 0;
+    if ((rc = check_cuda(cudaMemcpyAsync(&bad, c->i8_bad, sizeof(int), cudaMemcpyDeviceToHost, c->st),
+                         "int8 accuracy flag")) ||
+        (rc = check_cuda(cudaStreamSynchronize(c->st), "int8 accuracy flag")))
+      return rc;
+    if (bad) {
+      c->i8_off = true;
+      c->have_G = false;
+    }
+    c->i8_checked = true;
+  }
   if (c->gram_mode == 1 && !c->have_G && count > 0 && (rc = en_compute_G(c, c->st))) return rc;
   if (c->pipe && !c->timing && count > 0 && c->gram_mode == 1 && c->cla_L && c->idx_r) {
     // batched preparation: sort + factor + tiles of B sweeps in one launch each on sprep
@@ -1632,6 +1660,10 @@ extern "C" int rac_en_destroy(rac_en_ctx* c) {
   if (c->schain) cudaStreamDestroy(c->schain);
   if (c->sprep) cudaStreamDestroy(c->sprep);
   for (void* q : c->allocs) rac::dev_free(q, c->st);
+  // release the freed memory above the pool's threshold now (a later synchronisation would
+  // otherwise pay for unmapping gigabytes at an unrelated point, e.g. inside the next fit)
+  if (c->st) cudaStreamSynchronize(c->st);
+  rac::trim_pool(rac::POOL_KEEP);
   delete c;
   return RAC_OK;
 }

@@ -103,21 +103,33 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
 }
 
 // ---- per-feature exponent: 2^e > max |x_j| ---------------------------------------------
+// The dropped digit products bound a Gram entry's error by 2^-52.8 max|x_j| max|x_k| per
+// sample, i.e. by 2^-52.8 r_j r_k relative to |x_j| |x_k| where r = max / rms of a column.
+// A column with r > I8_MAX_RATIO (heavy outliers: r_j r_k > 2^16 leaves > 2^-37 of relative
+// error) raises *bad, and the caller forms that Gram on the FP64 DMMA tiles instead.
+constexpr double I8_MAX_RATIO = 256.0;
+
 __global__ void i8_colexp_kernel(const double* __restrict__ Xc, int64_t ld, int64_t len, int n, int nfeat,
-                                 int* __restrict__ ex) {
+                                 int* __restrict__ ex, int* __restrict__ bad) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nfeat; j += warps) {
-    double mx = 0.0;
+    double mx = 0.0, ss = 0.0;
     if (j < n) {
       const double* col = Xc + (int64_t)j * ld;
-      for (int64_t k = lane; k < len; k += 32) mx = fmax(mx, fabs(__ldg(col + k)));
+      for (int64_t k = lane; k < len; k += 32) {
+        const double v = __ldg(col + k);
+        mx = fmax(mx, fabs(v));
+        ss = fma(v, v, ss);
+      }
     }
     mx = warp_max(mx);
+    ss = warp_sum(ss);
     if (lane == 0) {
       int e = 0;
       if (mx > 0.0) frexp(mx, &e);
       ex[j] = e;
+      if (bad && mx > 0.0 && mx > I8_MAX_RATIO * sqrt(ss / (double)len)) atomicOr(bad, 1);
     }
   }
 }
@@ -379,7 +391,7 @@ size_t gram_i8_ws_bytes(int64_t len, int n) {
 // G (n x n, row-major) = Xc[:, :n]' Xc[:, :n] over samples [0, len) of the column-major Xc
 // (ld >= len): written / div (div > 0), or ADDED (accum) for row-chunk streaming.
 int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, double div, int accum, void* ws,
-                   size_t ws_bytes, cudaStream_t st) {
+                   size_t ws_bytes, cudaStream_t st, int* bad) {
   if (n < 1 || len < 1) return RAC_OK;
   if (!ws || ws_bytes < gram_i8_ws_bytes(len, n)) return set_error(RAC_ERR_ARG, "gram_i8: workspace too small");
   const int nstg = (int)((len + I8_KS - 1) / I8_KS);
@@ -390,7 +402,7 @@ int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, 
   const int nfeat = ngrp * 8;
   set_i8_attributes();
   note_launch();
-  i8_colexp_kernel<<<std::min(num_sms() * 8, (nfeat + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, nfeat, ex);
+  i8_colexp_kernel<<<std::min(num_sms() * 8, (nfeat + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, nfeat, ex, bad);
   if ((nstg + 7) / 8 > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8: too many samples");
   note_launch();
   i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8)), 256, 0, st>>>(
@@ -419,10 +431,10 @@ size_t gram_i8_blocks_ws_bytes(int64_t len, int s, int p) {
   return (size_t)p * I8_S * nstg * ngrp * 256 + (size_t)p * ngrp * 8 * sizeof(int) + 256;
 }
 
-int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st) {
+int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st, int* bad) {
   set_i8_attributes();
   note_launch();
-  i8_colexp_kernel<<<std::min(num_sms() * 8, (n + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, n, ex);
+  i8_colexp_kernel<<<std::min(num_sms() * 8, (n + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, n, ex, bad);
   return check_launch("i8 exponents");
 }
 

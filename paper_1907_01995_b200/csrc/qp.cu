@@ -1283,6 +1283,8 @@ extern "C" int rac_qp_destroy(rac_qp_ctx* c) {
   if (!c) return RAC_OK;
   if (c->st) cudaStreamSynchronize(c->st);
   for (void* q : c->allocs) rac::dev_free(q, c->st);
+  if (c->st) cudaStreamSynchronize(c->st);
+  rac::trim_pool(rac::POOL_KEEP);   // see rac_en_destroy
   delete c;
   return RAC_OK;
 }
@@ -1320,10 +1322,28 @@ extern "C" int rac_svm_build_q(const double* X, int64_t N, int64_t d, const doub
       ws8 = nullptr;
     }
   }
-  if (ws8) {
-    rc = launch_gram_i8(Xp, ldd, d, (int)N, Q, 1.0, 0, ws8, ws8b, st);
+  int* bad = nullptr;
+  if (ws8 && cudaMallocAsync((void**)&bad, sizeof(int), st) != cudaSuccess) {
+    cudaGetLastError();
+    bad = nullptr;
+  }
+  if (ws8 && bad) {
+    cudaMemsetAsync(bad, 0, sizeof(int), st);
+    rc = launch_gram_i8(Xp, ldd, d, (int)N, Q, 1.0, 0, ws8, ws8b, st, bad);
     cudaFreeAsync(ws8, st);
+    int hbad = 0;
+    if (!rc) rc = check_cuda(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st), "int8 flag");
+    if (!rc) rc = check_cuda(cudaStreamSynchronize(st), "int8 flag");
+    cudaFreeAsync(bad, st);
+    if (!rc && hbad) {
+      // heavy-tailed samples: the digit slices would lose FP64-level accuracy (gram_i8.cu)
+      GramPlan pl = plan_gram(d, (int)N, 1);
+      pl.splits = 1;
+      pl.chunk = ldd;
+      rc = launch_gram(Xp, ldd, d, ids, nullptr, (int)N, 1, Q, pl, st, nullptr, 1.0);
+    }
   } else {
+    if (ws8) cudaFreeAsync(ws8, st);
     GramPlan pl = plan_gram(d, (int)N, 1);
     pl.splits = 1;
     pl.chunk = ldd;

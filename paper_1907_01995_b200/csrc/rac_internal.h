@@ -22,6 +22,7 @@ int num_sms();
 int dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
 void trim_pool(size_t keep);
+extern const uint64_t POOL_KEEP;   // bytes the device pool keeps mapped across synchronisations
 // launch the persistent (software grid-barrier) kernels without the cooperative
 // attribute: under Nsight Compute or with RAC_PROFILE_NONCOOP=1 (capi.cu)
 bool profile_noncoop();
@@ -56,12 +57,14 @@ int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx, c
 // covariance Gram on the tensor cores in exact int8 digit-slice arithmetic (gram_i8.cu):
 // G = Xc' Xc over samples [0, len) written / div, or added (accum); ws >= gram_i8_ws_bytes
 size_t gram_i8_ws_bytes(int64_t len, int n);
+// bad (optional): raised when a column's max/rms ratio makes the digit-slice error exceed the
+// FP64 level (gram_i8.cu I8_MAX_RATIO) — the caller then forms that Gram on the DMMA tiles
 int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, double div, int accum, void* ws,
-                   size_t ws_bytes, cudaStream_t st);
+                   size_t ws_bytes, cudaStream_t st, int* bad = nullptr);
 // block mode: per-feature exponents once per data set, then per sweep the p block Grams
 // (full symmetric raw sums out[b][s][s]) of idx[b*s ..] in one slicing + one GEMM launch
 size_t gram_i8_blocks_ws_bytes(int64_t len, int s, int p);
-int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st);
+int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st, int* bad = nullptr);
 int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32_t* idx, int s, int p,
                           const int* ex_all, double* out, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_gram_reduce_sym(const double* ws, int64_t n, int splits, double div, double* G, cudaStream_t st);

@@ -143,3 +143,53 @@ def test_block_mode_fit_with_int8_block_grams_vs_oracle(lib, monkeypatch, ingest
             for a_, b_ in zip(got[k], caps[k]):
                 err = np.linalg.norm(a_ - b_) / max(np.linalg.norm(b_), 1e-300)
                 assert err <= 1e-9, (m, n, s, mode, k, err)
+
+
+@pytest.mark.parametrize("gram,env", [("covariance", {}), ("blocks", {"RAC_BG_I8": "2"})])
+def test_int8_grams_fall_back_on_heavy_outliers(lib, monkeypatch, gram, env):
+    """A 1e12 outlier in a column leaves the digit slices ~1e-5 relative error in that column's
+    Gram entries (the dropped products scale with max|x_j| max|x_k| per sample):
+    the exponent pass flags the column (max/rms > 256) and the fit forms this data set's Grams
+    on the FP64 DMMA tiles — per-sweep parity with the oracle holds."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import elastic_net as en
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(51)
+    m, n, s = 3000, 1700, 170
+    X = rng.standard_normal((m, n))
+    X[17, 100] = 1e12
+    X[400, 901] = -3e9
+    y = X[:, :9] @ rng.standard_normal(9) + 0.05 * rng.standard_normal(m)
+    kw = dict(lam=0.05, alpha=0.7, gamma=1.0, block_size=s, iters=4, seed=4)
+    caps = {}
+    ro.en_fit(X, y, mode="rac", **kw,
+              on_sweep=lambda k, bl, b, z, xi: caps.__setitem__(k, (b.copy(), z.copy(), xi.copy())))
+    got = {}
+    en.fit(X, y, en.ElasticNetSpec(**kw), gram_mode=gram,
+           sweep_hook=lambda k, b, z, xi: got.__setitem__(k, (b, z, xi)))
+    for k in caps:
+        for a_, b_ in zip(got[k], caps[k]):
+            err = np.linalg.norm(a_ - b_) / max(np.linalg.norm(b_), 1e-300)
+            assert err <= 1e-9, (gram, k, err)
+    # the same context on well-behaved data goes back to the int8 tensor cores (flag reset)
+    Xg = rng.standard_normal((m, n))
+    a = en.fit(Xg, y, en.ElasticNetSpec(**kw), gram_mode=gram)
+    r = ro.en_fit(Xg, y, mode="rac", **kw)
+    assert np.linalg.norm(a.beta - r["beta"]) <= 1e-9 * np.linalg.norm(r["beta"])
+
+
+def test_svm_q_falls_back_on_heavy_outliers(lib, monkeypatch):
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import svm
+    from paper_1907_01995_b200.problems import Mode, SolverConfig
+    monkeypatch.setenv("RAC_Q_I8", "2")
+    rng = np.random.default_rng(52)
+    N = 600
+    lab = np.where(np.arange(N) < N // 2, 1.0, -1.0)
+    X = rng.standard_normal((N, 40)) + lab[:, None] * 0.4
+    X[7, 3] = 1e9
+    cfg = SolverConfig(mode=Mode.RAC, block_size=50, beta_penalty=1.0, max_iters=3, seed=0)
+    _, diag = svm.train(X, lab, 1.0, svm.KernelSpec("linear"), cfg, return_diagnostics=True)
+    r = ro.svm_train(X, lab, 1.0, "linear", block_size=50, beta=1.0, max_iters=3, seed=0)
+    assert np.linalg.norm(diag.duals - r["z"]) <= 1e-9 * max(np.linalg.norm(r["z"]), 1e-300)

@@ -20,6 +20,7 @@ torchrun, `--gpus N` re-launches itself under torch.distributed.run with N ranks
 from __future__ import annotations
 
 import argparse
+import gc
 import glob
 import json
 import math
@@ -416,6 +417,7 @@ def measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline: b
     rng = np.random.default_rng(case.seed)
     perms = _device.PermutationFeeder(rng, n, dev).draw(W + K)
     solver.run(perms[:W], None)
+    gc.collect()
     torch.cuda.synchronize()
     clocks = ClockSampler(local) if headline else None
     if clocks:
@@ -539,6 +541,7 @@ def measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline: b
         # end to end: fit() on host arrays with the tolerance (upload, G, sweeps, results)
         spec_tol = en.ElasticNetSpec(lam=case.lam, alpha=case.alpha, gamma=case.gamma,
                                      block_size=case.block_size, iters=case.iters, seed=case.seed, tol=case.tol)
+        gc.collect()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         model = en.fit(case.X, case.y, spec_tol)
@@ -557,6 +560,7 @@ def measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline: b
     # warm-up call on the full problem: process-level one-time costs (pinned staging
     # buffers, kernel attributes, cluster occupancy queries) stay out of the e2e number
     en.fit(case.X, case.y, spec)
+    gc.collect()     # a previous config's multi-GB host arrays must not be freed inside the timer
     torch.cuda.synchronize()
     dist_barrier(world)
     t0 = time.perf_counter()
@@ -680,6 +684,7 @@ def measure_svm(cfg, case, args, world, rank, local, peaks, headline: bool) -> d
     cfgk = SolverConfig(mode=Mode.RAC, block_size=s, beta_penalty=case.beta, max_iters=K,
                         tol_primal=case.tol_primal, tol_dual=case.tol_dual, seed=case.seed, fixed_iterations=True)
     svm.train(X, y, case.C, svm.KernelSpec("linear"), SolverConfig(block_size=s, max_iters=1))
+    gc.collect()
     torch.cuda.synchronize()
     dist_barrier(world)
     t0 = time.perf_counter()
@@ -753,6 +758,7 @@ def run_b200(args) -> int:
             r["cpu_baseline"] = None
         results[cfg] = r
         del case
+        gc.collect()
         torch.cuda.empty_cache()
     h = results[args.config]
     line = {

@@ -112,7 +112,7 @@ __device__ void pivot_sweep(const SysArgs& a, const LargeBufs& L, int b, int kt)
       fail = k0 + q + 1;    // uniform: every thread read the same pivot
       break;
     }
-    const double dinv = 1.0 / d;
+    const double dinv = __drcp_rn(d);   // correctly rounded: the same value as 1.0 / d, no division slow path
     const double ri = c[i] * dinv;
     double cj[16];
 #pragma unroll

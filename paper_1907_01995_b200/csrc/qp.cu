@@ -195,6 +195,101 @@ __device__ QpSmem carve_qp(double* base, int s, bool rowphase, bool lsmem, doubl
   return q;
 }
 
+// end of a sweep (all CTAs): dual step y -= beta (Ax - b) with the primal residuals, the dual
+// residual per column, the history and the stop / divergence flags (engine.py:248-281,
+// 385-397).  Rows of A are owned by the CTA that owns their row chunk (RC rows).
+template <int RC>
+__device__ void qp_sweep_end(const QpChainArgs& a, QpSmem& w, unsigned& target) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = QPT / 32;
+  const int P = gridDim.x;
+  const bool has_a = a.m > 0;
+  const double beta = a.beta;
+  grid_barrier(a.bar, target, P);
+  // ------------------------------------------------------------ dual step + primal residual
+  // rows of A are owned by the CTA that owns their row chunk
+  double pm = 0.0, ps = 0.0;
+  if (has_a) {
+    for (int ch = blockIdx.x; ch < a.nrc; ch += P) {
+      const int64_t i0 = (int64_t)ch * RC;
+      for (int r = tid; r < RC; r += QPT) {
+        const int64_t i = i0 + r;
+        if (i < a.m) {
+          const double res = ldcg(a.ax + i) - a.b[i];
+          a.y[i] = a.y[i] - beta * res;
+          pm = nanmax(pm, fabs(res));
+          ps += fabs(res);
+        }
+      }
+    }
+  }
+  pm = warp_nanmax(pm);
+  ps = warp_sum(ps);
+  if (lane == 0) { w.bw.red[warp] = pm; w.sc[warp] = ps; }
+  __syncthreads();
+  if (tid == 0) {
+    double m1 = 0.0, s1 = 0.0;
+    for (int q = 0; q < nw; ++q) { m1 = nanmax(m1, w.bw.red[q]); s1 += w.sc[q]; }
+    a.pmax[blockIdx.x] = m1;
+    a.psum[blockIdx.x] = s1;
+  }
+  grid_barrier(a.bar, target, P);
+  // ------------------------------------------------------------ dual residual (columns)
+  double dm = 0.0;
+  {
+    const int gw = blockIdx.x * nw + warp, GW = P * nw;
+    for (int64_t j = gw; j < a.n; j += GW) {
+      double aty = 0.0;
+      if (has_a) {
+        const double* col = a.Ac + j * a.lda;
+        for (int64_t r = lane; r < a.m; r += 32) aty += col[r] * ldcg(a.y + r);
+        aty = warp_sum(aty);
+      }
+      if (lane == 0) {
+        double grad = a.c[j];
+        if (a.H) grad = grad + ldcg(a.hx + j);
+        if (has_a) grad = grad - aty;
+        const double xj = ldcg(a.x + j);
+        const double v = xj - grad;
+        const double pr = (v != v) ? v : fmin(fmax(v, a.lo[j]), a.hi[j]);   // np.clip keeps NaN
+        dm = nanmax(dm, fabs(pr - xj));
+      }
+    }
+  }
+  dm = warp_nanmax(dm);
+  if (lane == 0) w.bw.red[warp] = dm;
+  __syncthreads();
+  if (tid == 0) {
+    double m1 = 0.0;
+    for (int q = 0; q < nw; ++q) m1 = nanmax(m1, w.bw.red[q]);
+    a.dmax[blockIdx.x] = m1;
+  }
+  grid_barrier(a.bar, target, P);
+  if (blockIdx.x == 0 && warp == 0) {
+    double pmx = 0.0, psm = 0.0, dmx = 0.0;
+    for (int q = lane; q < P; q += 32) {
+      pmx = nanmax(pmx, ldcg(a.pmax + q));
+      psm += ldcg(a.psum + q);
+      dmx = nanmax(dmx, ldcg(a.dmax + q));
+    }
+    pmx = warp_nanmax(pmx);
+    psm = warp_sum(psm);
+    dmx = warp_nanmax(dmx);
+    if (lane == 0) {
+      a.hist_p[a.sweep] = pmx;
+      a.hist_l1[a.sweep] = psm;
+      a.hist_d[a.sweep] = dmx;
+      a.ctrl[1] = a.sweep + 1;
+      if (pmx > a.div_bar) {
+        a.ctrl[3] = RAC_STATUS_DIVERGED;
+        a.ctrl[0] = 1;
+      } else if (!a.fixed && pmx <= a.tol_p && dmx <= a.tol_d) {
+        a.ctrl[3] = RAC_STATUS_CONVERGED;
+        a.ctrl[0] = 1;
+      }
+    }
+  }
+}
+
 template <int RC>
 __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
   if (a.ctrl[0]) return;
@@ -627,90 +722,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
     if (tr) a.trace[10 * t + 7] = gtimer();
   }
   if (a.t1 < a.p) return;   // a later launch continues the sweep (running Hx / Ax are global)
-  grid_barrier(a.bar, target, P);
-  // ------------------------------------------------------------ dual step + primal residual
-  // rows of A are owned by the CTA that owns their row chunk
-  double pm = 0.0, ps = 0.0;
-  if (has_a) {
-    for (int ch = blockIdx.x; ch < a.nrc; ch += P) {
-      const int64_t i0 = (int64_t)ch * RC;
-      for (int r = tid; r < RC; r += QPT) {
-        const int64_t i = i0 + r;
-        if (i < a.m) {
-          const double res = ldcg(a.ax + i) - a.b[i];
-          a.y[i] = a.y[i] - beta * res;
-          pm = nanmax(pm, fabs(res));
-          ps += fabs(res);
-        }
-      }
-    }
-  }
-  pm = warp_nanmax(pm);
-  ps = warp_sum(ps);
-  if (lane == 0) { w.bw.red[warp] = pm; w.sc[warp] = ps; }
-  __syncthreads();
-  if (tid == 0) {
-    double m1 = 0.0, s1 = 0.0;
-    for (int q = 0; q < nw; ++q) { m1 = nanmax(m1, w.bw.red[q]); s1 += w.sc[q]; }
-    a.pmax[blockIdx.x] = m1;
-    a.psum[blockIdx.x] = s1;
-  }
-  grid_barrier(a.bar, target, P);
-  // ------------------------------------------------------------ dual residual (columns)
-  double dm = 0.0;
-  {
-    const int gw = blockIdx.x * nw + warp, GW = P * nw;
-    for (int64_t j = gw; j < a.n; j += GW) {
-      double aty = 0.0;
-      if (has_a) {
-        const double* col = a.Ac + j * a.lda;
-        for (int64_t r = lane; r < a.m; r += 32) aty += col[r] * ldcg(a.y + r);
-        aty = warp_sum(aty);
-      }
-      if (lane == 0) {
-        double grad = a.c[j];
-        if (a.H) grad = grad + ldcg(a.hx + j);
-        if (has_a) grad = grad - aty;
-        const double xj = ldcg(a.x + j);
-        const double v = xj - grad;
-        const double pr = (v != v) ? v : fmin(fmax(v, a.lo[j]), a.hi[j]);   // np.clip keeps NaN
-        dm = nanmax(dm, fabs(pr - xj));
-      }
-    }
-  }
-  dm = warp_nanmax(dm);
-  if (lane == 0) w.bw.red[warp] = dm;
-  __syncthreads();
-  if (tid == 0) {
-    double m1 = 0.0;
-    for (int q = 0; q < nw; ++q) m1 = nanmax(m1, w.bw.red[q]);
-    a.dmax[blockIdx.x] = m1;
-  }
-  grid_barrier(a.bar, target, P);
-  if (blockIdx.x == 0 && warp == 0) {
-    double pmx = 0.0, psm = 0.0, dmx = 0.0;
-    for (int q = lane; q < P; q += 32) {
-      pmx = nanmax(pmx, ldcg(a.pmax + q));
-      psm += ldcg(a.psum + q);
-      dmx = nanmax(dmx, ldcg(a.dmax + q));
-    }
-    pmx = warp_nanmax(pmx);
-    psm = warp_sum(psm);
-    dmx = warp_nanmax(dmx);
-    if (lane == 0) {
-      a.hist_p[a.sweep] = pmx;
-      a.hist_l1[a.sweep] = psm;
-      a.hist_d[a.sweep] = dmx;
-      a.ctrl[1] = a.sweep + 1;
-      if (pmx > a.div_bar) {
-        a.ctrl[3] = RAC_STATUS_DIVERGED;
-        a.ctrl[0] = 1;
-      } else if (!a.fixed && pmx <= a.tol_p && dmx <= a.tol_d) {
-        a.ctrl[3] = RAC_STATUS_CONVERGED;
-        a.ctrl[0] = 1;
-      }
-    }
-  }
+  qp_sweep_end<RC>(a, w, target);
 }
 
 // x0 = clip(0, lo, hi)

@@ -341,7 +341,7 @@ def run_reference(args) -> int:
 
 
 # ------------------------------------------------------------------ roofline
-def en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, workload, prep_batch=1) -> dict:
+def en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, workload, prep_batch=1, slices=8) -> dict:
     """Roofline entry for the dominant stage of an EN sweep (per-unit figures: SURVEY.md §8(d),
     DESIGN.md §4).  `stages` are per-sweep times measured with CUDA events; in covariance mode
     the block systems of `prep_batch` sweeps are prepared by one launch that overlaps the chain,
@@ -363,15 +363,17 @@ def en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, workload,
         achieved = byts / sec / 1e9
         roof = {"kernel": kern, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "algorithmic": desc}
-    elif dom == "gram" and gram_mode == "blocks" and block_grams_int8(s, p):
+    elif dom == "gram" and gram_mode == "blocks" and block_grams_int8(s, p) and slices > 0:
         jt = (s + 127) // 128
-        ops = 2.0 * 36 * p * (jt * (jt + 1) // 2) * 128 * 128 * ((m + 31) // 32 * 32)
+        prods = slices * (slices + 1) // 2        # slice pairs s + t <= S + 1
+        ops = 2.0 * prods * p * (jt * (jt + 1) // 2) * 128 * 128 * ((m + 31) // 32 * 32)
         achieved = ops / sec / 1e12
         roof = {"kernel": "gram_i8_kernel (tcgen05 kind::i8, + digit slicing)", "bound": "tensor",
                 "achieved": achieved, "peak": i8["peak"], "unit": "TOPS (int8)", "frac": achieved / i8["peak"],
                 "peak_source": i8["source"],
-                "algorithmic": "36 int8 digit-slice products x 2*128*128*K per upper tile of each of the p "
-                               "blocks per sweep (exact FP64 block Grams)",
+                "slices": slices,
+                "algorithmic": f"{prods} int8 digit-slice products ({slices} slices) x 2*128*128*K per upper "
+                               "tile of each of the p blocks per sweep (FP64-level block Grams)",
                 "fp64_equivalent": {"achieved_tflops": float(m) * n * (s + 1) / sec / 1e12, "peak": fp64,
                                     "frac": float(m) * n * (s + 1) / sec / 1e12 / fp64,
                                     "algorithmic": "m*n*(s+1) flop per sweep (symmetric SYRK of all p blocks)"}}
@@ -459,6 +461,9 @@ def measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline: b
     lib.rac_en_trace(solver.h, tbuf, ntr)
     info = (np.ctypeslib.ctypes.c_int32 * 4)()
     lib.rac_en_info(solver.h, info)
+    sl = np.ctypeslib.ctypes.c_int32(0)
+    lib.rac_en_gram_slices(solver.h, np.ctypeslib.ctypes.byref(sl))
+    slices = int(sl.value)          # digit slices of the int8 Grams (0: FP64 DMMA tiles)
     labels = (("delta_sum_next_wait", "t1_term", "v", "partials_push", "exchange_wait")
               if info[0] == 3 else
               ("cluster_sync", "cluster_reduce", "grid_barrier", "commit", "rhs_loads", "solve_wait", "rhs",
@@ -573,7 +578,7 @@ def measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline: b
     # ---------------- roofline of the dominant kernel
     hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
     out["roofline"] = en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, case.name,
-                                  chain_trace.get("prep_batch_sweeps", 1))
+                                  chain_trace.get("prep_batch_sweeps", 1), slices)
     out["roofline"]["peak_source"] = out["roofline"].get("peak_source", "MEASURED_PEAKS.json hbm_gbs"
                                                          if out["roofline"]["unit"] == "GB/s"
                                                          else "cuBLAS DGEMM 8192^3 measured in this run")

@@ -170,6 +170,10 @@ int rac_gram_covariance(const double* Xc, int64_t ld, int64_t len, int32_t n, do
                         int32_t method);
 /* [chain variant (0 streaming, 1 resident-tile cluster), CTAs, rows per chunk, chunks per CTA] */
 int rac_en_info(rac_en_ctx* ctx, int32_t* info_host4);
+/* Digit slices of the context's int8 tensor-core Grams (block Grams, else the last
+ * covariance G): 7 or 8 (chosen on the device per data set from the columns' max/rms),
+ * 0 when the Grams run on the FP64 DMMA tiles.  Synchronises the context's stream. */
+int rac_en_gram_slices(rac_en_ctx* ctx, int32_t* slices_host);
 /* Re-arm a context for a new fit with the same shape (m, n, block size, mode):
  * iterates, history and failure state cleared, data / partition / G must be set
  * again; buffers, plans and streams are kept (fit()'s context pool).  The tags

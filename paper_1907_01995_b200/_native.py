@@ -55,6 +55,7 @@ SIGNATURES = {
     "rac_gram_covariance": (_i32, [_p, _i64, _i64, _i32, _p, _f64, _i32]),
     "rac_en_reset": (_i32, [_p, _f64, _f64, _f64]),
     "rac_en_info": (_i32, [_p, _pi32]),
+    "rac_en_gram_slices": (_i32, [_p, _pi32]),
     "rac_en_destroy": (_i32, [_p]),
     "rac_qp_create": (_i32, [C.POINTER(_p), _i64, _i64, _i32, _i32, _f64, _f64, _p]),
     "rac_qp_set_problem": (_i32, [_p, _p, _p, _p, _p, _p, _p]),

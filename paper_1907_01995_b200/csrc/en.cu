@@ -606,8 +606,8 @@ int en_factor(rac_en_ctx* c, cudaStream_t st, int sweeps = 1) {
 // cores (exact digit slices, gram_i8.cu) when reserved, else the FP64 DMMA tiles
 int en_block_gram(rac_en_ctx* c, cudaStream_t st) {
   if (c->bg_ws && !c->i8_off)
-    return rac::launch_gram_i8_blocks(c->Xc, c->ld, c->m, c->idx, c->s, c->p, c->ex_all, c->gram_ws, c->bg_ws,
-                                      c->bg_cap, st);
+    return rac::launch_gram_i8_blocks(c->Xc, c->ld, c->m, c->idx, c->s, c->p, c->ex_all, c->i8_bad, c->gram_ws,
+                                      c->bg_ws, c->bg_cap, st);
   return rac::launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, st, c->ctrl);
 }
 
@@ -1361,7 +1361,7 @@ static int en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, double tol
                          "int8 accuracy flag")) ||
         (rc = check_cuda(cudaStreamSynchronize(c->st), "int8 accuracy flag")))
       return rc;
-    if (bad) {
+    if (bad & 1) {   // bit 1 (8 instead of 7 slices) is read by the kernels themselves
       c->i8_off = true;
       c->have_G = false;
     }
@@ -1584,6 +1584,22 @@ extern "C" int rac_en_info(rac_en_ctx* c, int32_t* info4) {
   // lookahead chain: [3, grid CTAs, sweeps per preparation batch, lookahead depth]
   info4[2] = (c->gram_mode == 1 && c->cla_L) ? (c->pipe && c->idx_r ? c->cla_B : 1) : c->RC;
   info4[3] = (c->gram_mode == 1 && c->cla_L) ? c->cla_D : c->nch;
+  return RAC_OK;
+}
+
+extern "C" int rac_en_gram_slices(rac_en_ctx* c, int32_t* slices) {
+  using namespace rac;
+  clear_error();
+  if (!c || !slices) return set_error(RAC_ERR_ARG, "rac_en_gram_slices: bad arguments");
+  *slices = 0;
+  const int* flags = c->bg_ws ? c->i8_bad : (c->i8_ws ? gram_i8_ws_flags(c->i8_ws) : nullptr);
+  if (!flags || c->i8_off || (!c->bg_ws && !c->have_G)) return RAC_OK;
+  int f = 0;
+  int rc = check_cuda(cudaMemcpyAsync(&f, flags, sizeof(int), cudaMemcpyDeviceToHost, c->st), "slices flag");
+  if (!rc) rc = check_cuda(cudaStreamSynchronize(c->st), "slices flag");
+  if (rc) return rc;
+  const char* e = getenv("RAC_I8_SLICES");
+  *slices = ((f & 2) || (e && atoi(e) == 8)) ? 8 : 7;
   return RAC_OK;
 }
 

@@ -7,23 +7,29 @@
 //
 // Digit slicing (Ozaki scheme): every feature column j gets the power-of-two scale
 // 2^{e_j} > max_i |x_ij|, and x·2^{6-e_j} is split into S balanced digits
-//     x·2^{6-e_j} = d_1 + d_2 2^-7 + ... + d_S 2^{-7(S-1)} + rest,  d_s in [-64, 64], |rest| <= 2^-50
-// (N = rint(x·2^{55-e_j}) once, then N's balanced base-128 digits in integer arithmetic).  Then
+//     x·2^{6-e_j} = d_1 + d_2 2^-7 + ... + d_S 2^{-7(S-1)} + rest,  d_s in [-64, 64], |rest| <= 2^{-7(S-1)-1}
+// (N = rint(x·2^{6+7(S-1)-e_j}) once, then N's balanced base-128 digits in integer arithmetic).  Then
 //     G_jk = 2^{e_j+e_k-12} Σ_{w=2..S+1} 2^{-7(w-2)} C_w[j,k],
 //     C_w = Σ_{s+t=w} D_s' D_t      (int8 GEMMs, exact int32 sums)
 // The dropped products (s+t > S+1) and the rest terms are below 2^-52.8 of
-// max|x_j|·max|x_k| per sample for S = 8 — the rounding level of an FP64 dot product.
+// max|x_j|·max|x_k| per sample for S = 8 — the rounding level of an FP64 dot product — and
+// below 2^-45.8 for S = 7.  S is chosen per data set on the device (i8_colexp_kernel): S = 7
+// (28 slice products instead of 36) when every column's max/rms ratio r is at most
+// I8_NARROW_RATIO, so that the S = 7 error relative to |x_j| |x_k| (≈ 2^-48 r_j r_k / sqrt(m)
+// typical) stays at the FP64 DMMA tiles' measured level (Gaussian columns, m = 5000,
+// tests/test_digit_slices.py: S = 7 max 4.5e-15, median 2.9e-16; S = 8 3.2e-16 / 2.5e-18;
+// numpy FP64 3.9e-16 / 6.3e-18; DMMA tiles 2e-15 .. 2e-14); else S = 8.
 // Each group's int32 sum is exact while K·S·64² < 2^31 (K segments of 65472 samples,
 // combined in FP64).  The FP64 combination runs in a fixed order, so the
 // result is deterministic and G is exactly symmetric (each unordered pair is formed once
 // and mirrored).
 //
 // Tiles are 128 x 128 (M = N = 128 MMAs: 16 operand bytes per 1024 MACs, under the shared-memory
-// read rate that capped 128 x 64 tiles); the 8 weight groups need 1024 TMEM columns, so
-// each tile makes two passes over K with 4 groups (512 columns) each — the small weights
-// w = 6..9 (26 slice products, all 8 slices) first, then w = 2..5 (10 products, slices
-// 1-4).  Each pass's FP64 partial is added to the tile's upper-triangle entries of G,
-// the last one also writes the mirror.
+// read rate that capped 128 x 64 tiles); the S weight groups need up to 1024 TMEM columns, so
+// each tile makes two passes over K with up to 4 groups (512 columns) each — the small weights
+// w = S-2..S+1 (S = 8: 26 slice products, S = 7: 22; all S slices) first, then w = 2..S-3
+// (S = 8: 10 products from slices 1-4, S = 7: 6 from slices 1-3).  Each pass's FP64 partial is
+// added to the tile's upper-triangle entries of G, the last one also writes the mirror.
 //
 // Data layout: slice s is stored in the UMMA "no swizzle, K-major" canonical layout so
 // that one pipeline stage of a tile is ONE contiguous 4 KB block fetched by one TMA bulk copy:
@@ -48,7 +54,8 @@ constexpr int I8_SMEM = I8_NST * I8_STAGE + 1024;
 constexpr int I8_THREADS = 192;               // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
 static_assert(I8_S * 64 * 64 * (I8_SEGST * (double)I8_KS) < 2147483648.0, "int32 group sums must stay exact");
 static_assert(4 * I8_TN <= 512, "a pass's weight groups must fit the 512 TMEM columns");
-static_assert(I8_S == 8, "the two passes split the groups w = 2..9");
+static_assert(I8_S == 8, "storage for up to 8 slices; the two passes split the groups w = 2..S+1");
+// pass 0: groups w = S-2 .. S+1 (all S slices), pass 1: groups w = 2 .. S-3 (slices 1 .. S-4)
 
 struct I8Args {
   const uint8_t* sl;     // S slices
@@ -64,7 +71,14 @@ struct I8Args {
   size_t blk_sl;         // block mode (blockIdx.y = block): slice, output and exponent strides
   int64_t blk_g;
   int blk_ex;
+  const int* flags;      // i8_colexp_kernel's flags: bit 1 = some column's max/rms > I8_NARROW_RATIO
+  int force8;            // RAC_I8_SLICES=8: always 8 slices
 };
+
+// slices of this data set: 8 when a column is wide (or forced), else 7
+__device__ __forceinline__ int slice_count(const int* flags, int force8) {
+  return (force8 || (*flags & 2)) ? 8 : 7;
+}
 
 // ---- tcgen05 helpers ------------------------------------------------------------------
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -108,9 +122,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
 // A column with r > I8_MAX_RATIO (heavy outliers: r_j r_k > 2^16 leaves > 2^-37 of relative
 // error) raises *bad, and the caller forms that Gram on the FP64 DMMA tiles instead.
 constexpr double I8_MAX_RATIO = 256.0;
+// 7 slices while every column's r <= I8_NARROW_RATIO (flags bit 1 raised otherwise: 8 slices)
+constexpr double I8_NARROW_RATIO = 8.0;
 
+// flags: bit 0 = r > I8_MAX_RATIO somewhere (also raised in *bad when given), bit 1 = r >
+// I8_NARROW_RATIO somewhere
 __global__ void i8_colexp_kernel(const double* __restrict__ Xc, int64_t ld, int64_t len, int n, int nfeat,
-                                 int* __restrict__ ex, int* __restrict__ bad) {
+                                 int* __restrict__ ex, int* __restrict__ flags, int* __restrict__ bad) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < nfeat; j += warps) {
@@ -129,7 +147,12 @@ __global__ void i8_colexp_kernel(const double* __restrict__ Xc, int64_t ld, int6
       int e = 0;
       if (mx > 0.0) frexp(mx, &e);
       ex[j] = e;
-      if (bad && mx > 0.0 && mx > I8_MAX_RATIO * sqrt(ss / (double)len)) atomicOr(bad, 1);
+      const double rms = sqrt(ss / (double)len);
+      if (mx > 0.0 && mx > I8_NARROW_RATIO * rms) atomicOr(flags, 2);
+      if (mx > 0.0 && mx > I8_MAX_RATIO * rms) {
+        atomicOr(flags, 1);
+        if (bad) atomicOr(bad, 1);
+      }
     }
   }
 }
@@ -142,8 +165,10 @@ __global__ void i8_colexp_kernel(const double* __restrict__ Xc, int64_t ld, int6
 __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict__ Xc, int64_t ld, int64_t len,
                                                        int n, const int* __restrict__ ex, uint8_t* __restrict__ sl,
                                                        size_t slice_bytes, int ngrp, int nstg,
-                                                       const int32_t* __restrict__ idx, int* __restrict__ ex_blk) {
+                                                       const int32_t* __restrict__ idx, int* __restrict__ ex_blk,
+                                                       const int* __restrict__ flags, int force8) {
   __shared__ __align__(16) uint8_t buf[I8_S][8 * 256];
+  const int S = slice_count(flags, force8);
   const int f = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = blockIdx.x;
   const int pos = g * 8 + f;
@@ -173,12 +198,13 @@ __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict_
   for (int s = 0; s < I8_S; ++s) packed[s] = 0ull;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    // x 2^(55-e) (exact, |.| < 2^55) rounded once to an integer N, then N's balanced
+    // x 2^(6+7(S-1)-e) (exact, |.| < 2^55) rounded once to an integer N, then N's balanced
     // base-128 digits from the bottom: d = ((N + 64) mod 128) - 64, N <- (N - d) / 128
     // (exact shifts); the top digit is what remains, |d_1| <= 64
-    long long N = __double2ll_rn(ldexp(x[i], 55 - e));
+    long long N = __double2ll_rn(ldexp(x[i], 7 * S - 1 - e));
 #pragma unroll
     for (int s = I8_S - 1; s > 0; --s) {
+      if (s >= S) continue;
       const long long d = ((N + 64) & 127) - 64;
       N = (N - d) >> 7;
       packed[s] |= (unsigned long long)(uint8_t)(int8_t)d << (8 * i);
@@ -194,18 +220,42 @@ __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict_
   const int kst0 = blockIdx.y * 8;
   for (int q = threadIdx.x; q < I8_S * 8 * 16; q += 256) {
     const int s = q >> 7, kl = (q >> 4) & 7, o = q & 15;
-    if (kst0 + kl >= nstg) continue;
+    if (kst0 + kl >= nstg || s >= S) continue;
     const uint4 v = *reinterpret_cast<const uint4*>(&buf[s][kl * 256 + o * 16]);
     *reinterpret_cast<uint4*>(sl + s * slice_bytes + ((size_t)(kst0 + kl) * ngrp + g) * 256 + o * 16) = v;
   }
 }
 
 // ---- the tensor-core Gram ----------------------------------------------------------------
-// phases: pass 0 (groups w = 6..9) then pass 1 (w = 2..5), each over the K segments
+// one pipeline stage's MMAs.  Pass 0: groups w = S-2 .. S+1 (TMEM group w - S + 2) from the
+// stage's S slice operands; pass 1: groups w = 2 .. S-3 from nk packed K steps of S-4 slices.
+template <int S>
+__device__ __forceinline__ void issue_stage(uint32_t tmem, unsigned sA, unsigned sB, bool p0, int nk, bool first) {
+  if (p0) {
+#pragma unroll
+    for (int w = S - 2; w <= S + 1; ++w)
+#pragma unroll
+      for (int s = 1; s < w; ++s)
+        tc_mma_i8(tmem + (uint32_t)((w - S + 2) * I8_TN), umma_desc(sA + (s - 1) * I8_OP),
+                  umma_desc(sB + (w - s - 1) * I8_OP), I8_IDESC, (first && s == 1) ? 0u : 1u);
+  } else {
+#pragma unroll 1
+    for (int h = 0; h < nk; ++h)
+#pragma unroll
+      for (int w = 2; w <= S - 3; ++w)
+#pragma unroll
+        for (int s = 1; s < w; ++s)
+          tc_mma_i8(tmem + (uint32_t)((w - 2) * I8_TN), umma_desc(sA + (h * 4 + s - 1) * I8_OP),
+                    umma_desc(sB + (h * 4 + w - s - 1) * I8_OP), I8_IDESC, (first && h == 0 && s == 1) ? 0u : 1u);
+  }
+}
+
+// phases: pass 0 (groups w = S-2 .. S+1) then pass 1 (w = 2 .. S-3), each over the K segments
 __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
   a.sl += blockIdx.y * a.blk_sl;
   a.G += blockIdx.y * a.blk_g;
   a.ex += blockIdx.y * a.blk_ex;
+  const int S = slice_count(a.flags, a.force8);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bar_full[I8_NST], bar_free[I8_NST], bar_acc, bar_tfree;
@@ -247,7 +297,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
       const size_t offA = (size_t)J * 16 * 256, offB = (size_t)Kt * 16 * 256;
       int q = 0;
       for (int ph = 0; ph < nphase; ++ph) {
-        const int ns = (ph < nseg) ? I8_S : 4;   // pass 0 reads all slices, pass 1 slices 1-4
+        const int ns = (ph < nseg) ? S : S - 4;   // pass 0 reads all slices, pass 1 slices 1 .. S-4
         const int sg = ph % nseg;
         const int q1 = min(a.nstg, (sg + 1) * I8_SEGST);
         // pass 1 packs two 32-sample steps (4 slices each) into one slot
@@ -292,24 +342,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
           tc_fence_after();
           const unsigned sA = smem_u32(smem + slot * I8_STAGE);
           const unsigned sB = sA + I8_S * I8_OP;
-          if (p0) {
-#pragma unroll
-            for (int w = 6; w <= 9; ++w)
-#pragma unroll
-              for (int s = 1; s < w; ++s)
-                tc_mma_i8(tmem + (uint32_t)((w - 6) * I8_TN), umma_desc(sA + (s - 1) * I8_OP),
-                          umma_desc(sB + (w - s - 1) * I8_OP), I8_IDESC, (first && s == 1) ? 0u : 1u);
-          } else {
-#pragma unroll 1
-            for (int h = 0; h < nk; ++h)
-#pragma unroll
-              for (int w = 2; w <= 5; ++w)
-#pragma unroll
-                for (int s = 1; s < w; ++s)
-                  tc_mma_i8(tmem + (uint32_t)((w - 2) * I8_TN), umma_desc(sA + (h * 4 + s - 1) * I8_OP),
-                            umma_desc(sB + (h * 4 + w - s - 1) * I8_OP), I8_IDESC,
-                            (first && h == 0 && s == 1) ? 0u : 1u);
-          }
+          if (S == 8) issue_stage<8>(tmem, sA, sB, p0, nk, first);
+          else issue_stage<7>(tmem, sA, sB, p0, nk, first);
           tc_commit(&bar_free[slot]);
         }
         tc_commit(&bar_acc);
@@ -325,7 +359,8 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
     const int ej = jok ? __ldg(a.ex + j) - 12 : 0;
     double* Grow = a.G + (int64_t)(jok ? j : 0) * a.n;
     for (int ph = 0; ph < nphase; ++ph) {
-      const int w0 = (ph < nseg) ? 6 : 2;     // groups w0 .. w0 + 3 in TMEM columns 0..511
+      const int w0 = (ph < nseg) ? S - 2 : 2;   // groups w0 .. w0 + ng - 1 in TMEM columns 0..511
+      const int ng = (ph < nseg) ? 4 : S - 4;
       const bool last = ph == nphase - 1;
       mbar_wait(&bar_acc, ph & 1);
       tc_fence_after();
@@ -335,7 +370,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
 #pragma unroll
         for (int c = 0; c < 32; ++c) acc[c] = 0.0;
 #pragma unroll 1
-        for (int g = 3; g >= 0; --g) {        // smallest weight first, fixed order
+        for (int g = ng - 1; g >= 0; --g) {   // smallest weight first, fixed order
           int v[32];
           tmem_ld32(trow + (uint32_t)(g * I8_TN + cc * 32), v);
           const double wgt = ldexp(1.0, -7 * (w0 + g - 2));
@@ -382,6 +417,12 @@ void set_i8_attributes() {
 
 }  // namespace
 
+// RAC_I8_SLICES=8: always 8 slices (read per launch)
+static int force8_env() {
+  const char* e = getenv("RAC_I8_SLICES");
+  return (e && atoi(e) == 8) ? 1 : 0;
+}
+
 size_t gram_i8_ws_bytes(int64_t len, int n) {
   const int64_t nstg = (len + I8_KS - 1) / I8_KS;
   const int64_t ngrp = (int64_t)((n + I8_TM - 1) / I8_TM) * 16;
@@ -397,16 +438,18 @@ int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, 
   const int nstg = (int)((len + I8_KS - 1) / I8_KS);
   const int ngrp = ((n + I8_TM - 1) / I8_TM) * 16;
   const size_t slice_bytes = (size_t)nstg * ngrp * 256;
-  uint8_t* sl = static_cast<uint8_t*>(ws);
+  int* flags = static_cast<int*>(ws);   // the workspace's first 256 bytes (gram_i8_ws_flags)
+  uint8_t* sl = static_cast<uint8_t*>(ws) + 256;
   int* ex = reinterpret_cast<int*>(sl + I8_S * slice_bytes);
   const int nfeat = ngrp * 8;
   set_i8_attributes();
+  cudaMemsetAsync(flags, 0, sizeof(int), st);
   note_launch();
-  i8_colexp_kernel<<<std::min(num_sms() * 8, (nfeat + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, nfeat, ex, bad);
+  i8_colexp_kernel<<<std::min(num_sms() * 8, (nfeat + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, nfeat, ex, flags, bad);
   if ((nstg + 7) / 8 > 65535) return set_error(RAC_ERR_UNSUPPORTED, "gram_i8: too many samples");
   note_launch();
   i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8)), 256, 0, st>>>(
-      Xc, ld, len, n, ex, sl, slice_bytes, ngrp, nstg, nullptr, nullptr);
+      Xc, ld, len, n, ex, sl, slice_bytes, ngrp, nstg, nullptr, nullptr, flags, force8_env());
   set_i8_attributes();
   I8Args a{};
   a.sl = sl;
@@ -419,11 +462,15 @@ int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, 
   a.G = G;
   a.div = div;
   a.accum = accum;
+  a.flags = flags;
+  a.force8 = force8_env();
   const int tiles = a.JT * (a.JT + 1) / 2;
   note_launch();
   gram_i8_kernel<<<tiles, I8_THREADS, I8_SMEM, st>>>(a);
   return check_launch("gram_i8");
 }
+
+const int* gram_i8_ws_flags(const void* ws) { return static_cast<const int*>(ws); }
 
 size_t gram_i8_blocks_ws_bytes(int64_t len, int s, int p) {
   const int64_t nstg = (len + I8_KS - 1) / I8_KS;
@@ -431,17 +478,18 @@ size_t gram_i8_blocks_ws_bytes(int64_t len, int s, int p) {
   return (size_t)p * I8_S * nstg * ngrp * 256 + (size_t)p * ngrp * 8 * sizeof(int) + 256;
 }
 
-int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st, int* bad) {
+int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st, int* flags) {
   set_i8_attributes();
   note_launch();
-  i8_colexp_kernel<<<std::min(num_sms() * 8, (n + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, n, ex, bad);
+  i8_colexp_kernel<<<std::min(num_sms() * 8, (n + 7) / 8), 256, 0, st>>>(Xc, ld, len, n, n, ex, flags, nullptr);
   return check_launch("i8 exponents");
 }
 
 // block mode: the p block Grams (full symmetric s x s raw sums, out[b][s][s]) of the
 // feature lists idx[b*s ..] (-1 = padding), ex_all = per-feature exponents of Xc
 int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32_t* idx, int s, int p,
-                          const int* ex_all, double* out, void* ws, size_t ws_bytes, cudaStream_t st) {
+                          const int* ex_all, const int* flags, double* out, void* ws, size_t ws_bytes,
+                          cudaStream_t st) {
   if (!ws || ws_bytes < gram_i8_blocks_ws_bytes(len, s, p))
     return set_error(RAC_ERR_ARG, "gram_i8 blocks: workspace too small");
   const int nstg = (int)((len + I8_KS - 1) / I8_KS);
@@ -453,7 +501,7 @@ int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32
   set_i8_attributes();
   note_launch();
   i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8), (unsigned)p), 256, 0, st>>>(
-      Xc, ld, len, s, ex_all, sl, slice_bytes, ngrp, nstg, idx, ex_blk);
+      Xc, ld, len, s, ex_all, sl, slice_bytes, ngrp, nstg, idx, ex_blk, flags, force8_env());
   set_i8_attributes();
   I8Args a{};
   a.sl = sl;
@@ -469,6 +517,8 @@ int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32
   a.blk_sl = (size_t)I8_S * slice_bytes;
   a.blk_g = (int64_t)s * s;
   a.blk_ex = ngrp * 8;
+  a.flags = flags;
+  a.force8 = force8_env();
   note_launch();
   gram_i8_kernel<<<dim3((unsigned)(a.JT * (a.JT + 1) / 2), (unsigned)p), I8_THREADS, I8_SMEM, st>>>(a);
   return check_launch("gram_i8 blocks");

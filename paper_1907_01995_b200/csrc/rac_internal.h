@@ -57,6 +57,8 @@ int launch_gram(const double* V, int64_t ldv, int64_t len, const int32_t* idx, c
 // covariance Gram on the tensor cores in exact int8 digit-slice arithmetic (gram_i8.cu):
 // G = Xc' Xc over samples [0, len) written / div, or added (accum); ws >= gram_i8_ws_bytes
 size_t gram_i8_ws_bytes(int64_t len, int n);
+// the flags word of the last launch_gram_i8 on this workspace (bits as launch_i8_colexp's)
+const int* gram_i8_ws_flags(const void* ws);
 // bad (optional): raised when a column's max/rms ratio makes the digit-slice error exceed the
 // FP64 level (gram_i8.cu I8_MAX_RATIO) — the caller then forms that Gram on the DMMA tiles
 int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, double div, int accum, void* ws,
@@ -64,9 +66,13 @@ int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, 
 // block mode: per-feature exponents once per data set, then per sweep the p block Grams
 // (full symmetric raw sums out[b][s][s]) of idx[b*s ..] in one slicing + one GEMM launch
 size_t gram_i8_blocks_ws_bytes(int64_t len, int s, int p);
-int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st, int* bad = nullptr);
+// flags (required): bit 0 = a column too heavy-tailed for the digit slices (the caller switches
+// to the DMMA tiles), bit 1 = a column wide enough to need 8 slices (else 7); read on the device
+// by launch_gram_i8_blocks
+int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st, int* flags);
 int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32_t* idx, int s, int p,
-                          const int* ex_all, double* out, void* ws, size_t ws_bytes, cudaStream_t st);
+                          const int* ex_all, const int* flags, double* out, void* ws, size_t ws_bytes,
+                          cudaStream_t st);
 int launch_gram_reduce_sym(const double* ws, int64_t n, int splits, double div, double* G, cudaStream_t st);
 // K3: assemble block systems, Cholesky, explicit inverse.
 struct SysArgs {

@@ -749,6 +749,7 @@ def run_b200(args) -> int:
     i8 = int8_peak_tops(torch, peaks)
     order = [args.config] + ([] if args.only else [c for c in (1, 2, 3, 4, 5) if c != args.config])
     results = {}
+    cases = {}
     for cfg in order:
         headline = cfg == args.config
         case = make_case(cfg)
@@ -757,14 +758,19 @@ def run_b200(args) -> int:
         else:
             r = measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline)
         r["config"] = config_dict(cfg, case, args.steps, world)
-        if rank == 0 and world == 1 and not args.no_cpu:
-            r["cpu_baseline"] = cpu_baseline(cfg, case, budget_s=8.0 if headline else 5.0)
-        else:
-            r["cpu_baseline"] = None
+        r["cpu_baseline"] = None
         results[cfg] = r
+        cases[cfg] = case
         del case
         gc.collect()
         torch.cuda.empty_cache()
+    # the CPU legs run after every GPU measurement: a 16-thread oracle run right before a
+    # config's end-to-end leg slowed that leg's host side (measured: config 4 e2e 23 vs 125
+    # sweeps/s, config 2 1 860 vs 2 990)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        for cfg in order:
+            results[cfg]["cpu_baseline"] = cpu_baseline(cfg, cases[cfg], budget_s=8.0 if cfg == args.config else 5.0)
+    cases.clear()
     h = results[args.config]
     line = {
         "metric": METRIC, "value": h["value"], "unit": "sweeps/s", "n_gpus": world,

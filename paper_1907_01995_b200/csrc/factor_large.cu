@@ -5,10 +5,11 @@
 // The block system lives in global memory as 64 x 64 lower tiles of an
 // S x S matrix (S = s rounded up to 64, padding = identity).  For each pivot
 // tile K:
-//   (a) W   = A_KK^{-1}              one CTA per block, packed sweep in smem
-//   (b) CW_I = A_IK W                 one CTA per (block, tile row I != K)
-//   (c) A_IJ -= CW_I A_JK'            one CTA per (block, lower tile I>=J, I,J != K)
-//   (d) A_IK = CW_I, A_KK = -W        K row / column rewritten
+//   (a) W   = A_KK^{-1}              one CTA per block, sweep held in registers
+//   (b) CW_I = A_IK W                 one CTA per (block, tile row I != K); the same CTA rewrites
+//                                     the K strip in place (A_IK = CW_I, A_KK = -W) and keeps the
+//                                     old strip tile in OLD_I for (c)
+//   (c) A_IJ -= CW_I OLD_J'           one CTA per (block, lower tile I>=J, I,J != K)
 // and finally inv = -A.  (b) and (c) are 64x64x64 products on FP64 tensor
 // cores (DMMA.8x8x4).  A non-positive pivot marks the block; such blocks are
 // re-done by the authoritative Cholesky kernel (factor.cu).
@@ -24,13 +25,14 @@ constexpr int LTHREADS = 256;
 
 size_t large_scratch_bytes(int s, int p) {
   const size_t S = (size_t)(s + LT - 1) / LT * LT;
-  return (size_t)p * (S * S + S * LT + 2 * LT * LT) * sizeof(double);
+  return (size_t)p * (S * S + 2 * S * LT + 2 * LT * LT) * sizeof(double);
 }
 
 struct LargeBufs {
   int p;
   double* A;    // [p][S][S]   (only lower tiles maintained)
   double* CW;   // [p][S][LT]
+  double* OLD;  // [p][S][LT]: the K strip before step K rewrote it (OLD_I[i][k] = A_IK[i][k])
   double* W;    // [2][p][LT][LT]: W of pivot step kt in half kt & 1 (the look-ahead pivot of
                 //   step kt + 1 is written while step kt's strip still reads W_kt)
   int S, nt;
@@ -43,7 +45,8 @@ __device__ __forceinline__ LargeBufs large_bufs(double* scratch, int s, int p) {
   L.nt = L.S / LT;
   L.A = scratch;
   L.CW = L.A + (size_t)p * L.S * L.S;
-  L.W = L.CW + (size_t)p * L.S * LT;
+  L.OLD = L.CW + (size_t)p * L.S * LT;
+  L.W = L.OLD + (size_t)p * L.S * LT;
   return L;
 }
 
@@ -201,18 +204,20 @@ __device__ __forceinline__ void tile_mma(const double (*sX)[LLD], const double (
   }
 }
 
-// (b) CW_I = A_IK * W for every tile row I != K
+// (b) CW_I = A_IK * W for every tile row I != K.  The CTA also rewrites the K strip in place
+// (A_IK = CW_I in the lower-tile orientation) after saving the old tile to OLD_I, and the first
+// CTA of a block writes A_KK = -W.  Nothing else reads the K strip during this launch.
 __global__ void __launch_bounds__(LTHREADS) large_cw_kernel(SysArgs a, int p, int kt) {
-  if (a.done && *a.done) return;
   const LargeBufs L = large_bufs(a.scratch, a.s, p);
   const int b = blockIdx.y;
   int I = blockIdx.x;
   if (I >= kt) ++I;   // skip K
-  if (a.info[b]) return;
+  const int dn = a.done ? *a.done : 0;
+  if (dn | a.info[b]) return;
   extern __shared__ __align__(16) double lsm[];
   double(*sX)[LLD] = reinterpret_cast<double(*)[LLD]>(lsm);
   double(*sY)[LLD] = reinterpret_cast<double(*)[LLD]>(lsm + LT * LLD);
-  const double* A = L.A + (size_t)b * L.S * L.S;
+  double* A = L.A + (size_t)b * L.S * L.S;
   // X = A_IK (rows i of tile I, k of tile K); Y rows j = W columns: W symmetric, Y[j][k] = W[j][k]
   if (I > kt) load_tile(sX, A + (int64_t)I * LT * L.S + kt * LT, L.S, false);
   else load_tile(sX, A + (int64_t)kt * LT * L.S + I * LT, L.S, true);
@@ -224,23 +229,45 @@ __global__ void __launch_bounds__(LTHREADS) large_cw_kernel(SysArgs a, int p, in
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
   double* CW = L.CW + ((size_t)b * L.S + (size_t)I * LT) * LT;
+  double* OLD = L.OLD + ((size_t)b * L.S + (size_t)I * LT) * LT;
+  // the old strip tile, as loaded
+#pragma unroll
+  for (int u = 0; u < (LT * LT / 2) / LTHREADS; ++u) {
+    const int e = threadIdx.x + u * LTHREADS;
+    const int r = e / (LT / 2), c = 2 * (e - r * (LT / 2));
+    *reinterpret_cast<double2*>(OLD + (size_t)r * LT + c) = make_double2(sX[r][c], sX[r][c + 1]);
+  }
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) CW[(size_t)(r0 + i * 8 + g) * LT + c0 + j * 8 + 2 * t + e] = acc[i][j][e];
+    for (int j = 0; j < 4; ++j) {
+      const int row = r0 + i * 8 + g, col = c0 + j * 8 + 2 * t;
+      const double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
+      *reinterpret_cast<double2*>(CW + (size_t)row * LT + col) = v;
+      if (I > kt) {
+        *reinterpret_cast<double2*>(A + (int64_t)(I * LT + row) * L.S + kt * LT + col) = v;
+      } else {   // lower tile (K, I): A[K k][I i] = CW_I[i][k]
+        A[(int64_t)(kt * LT + col) * L.S + I * LT + row] = v.x;
+        A[(int64_t)(kt * LT + col + 1) * L.S + I * LT + row] = v.y;
+      }
+    }
+  if (blockIdx.x == 0) {   // A_KK = -W (lower part)
+    for (int e = threadIdx.x; e < LT * LT; e += LTHREADS) {
+      const int i = e / LT, j = e - i * LT;
+      if (j <= i) A[(int64_t)(kt * LT + i) * L.S + kt * LT + j] = -sY[i][j];
+    }
+  }
 }
 
-// (c) A_IJ -= CW_I * A_JK'   for lower tiles I >= J with I, J != K
+// (c) A_IJ -= CW_I * OLD_J'   for lower tiles I >= J with I, J != K   (OLD_J = A_JK before (b))
 // grid (p, tiles): the first tile of every block is the NEXT pivot tile (K+1, K+1), so those
 // CTAs are dispatched first; after its update the CTA also inverts it (the next step's pivot,
 // look-ahead), overlapping that latency-bound sweep with the rest of this update.
 __global__ void __launch_bounds__(LTHREADS) large_update_kernel(SysArgs a, int p, int kt) {
-  if (a.done && *a.done) return;
   const LargeBufs L = large_bufs(a.scratch, a.s, p);
   const int b = blockIdx.x;
-  if (a.info[b]) return;
+  const int dn = a.done ? *a.done : 0;
+  if (dn | a.info[b]) return;
   // tile index over the lower triangle of the (nt-1) x (nt-1) grid without K; index 0 is
   // remapped to the next diagonal tile (reduced index (kt, kt)) when there is a next step
   const int m = L.nt - 1;
@@ -258,9 +285,7 @@ __global__ void __launch_bounds__(LTHREADS) large_update_kernel(SysArgs a, int p
   double(*sY)[LLD] = reinterpret_cast<double(*)[LLD]>(lsm + LT * LLD);
   double* A = L.A + (size_t)b * L.S * L.S;
   load_tile(sX, L.CW + ((size_t)b * L.S + (size_t)I * LT) * LT, LT, false);
-  // Y[j][k] = A[J*64 + j][K*64 + k]
-  if (J > kt) load_tile(sY, A + (int64_t)J * LT * L.S + kt * LT, L.S, false);
-  else load_tile(sY, A + (int64_t)kt * LT * L.S + J * LT, L.S, true);
+  load_tile(sY, L.OLD + ((size_t)b * L.S + (size_t)J * LT) * LT, LT, false);   // Y[j][k] = A_JK[j][k]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
   double* C = A + (int64_t)I * LT * L.S + J * LT;
@@ -268,9 +293,11 @@ __global__ void __launch_bounds__(LTHREADS) large_update_kernel(SysArgs a, int p
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) acc[i][j][e] = C[(int64_t)(r0 + i * 8 + g) * L.S + c0 + j * 8 + 2 * t + e];
+    for (int j = 0; j < 4; ++j) {
+      const double2 v = *reinterpret_cast<const double2*>(C + (int64_t)(r0 + i * 8 + g) * L.S + c0 + j * 8 + 2 * t);
+      acc[i][j][0] = v.x;
+      acc[i][j][1] = v.y;
+    }
   cp_async_wait<0>();
   __syncthreads();
   tile_mma(sX, sY, acc, -1.0);
@@ -278,47 +305,51 @@ __global__ void __launch_bounds__(LTHREADS) large_update_kernel(SysArgs a, int p
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) C[(int64_t)(r0 + i * 8 + g) * L.S + c0 + j * 8 + 2 * t + e] = acc[i][j][e];
+      *reinterpret_cast<double2*>(C + (int64_t)(r0 + i * 8 + g) * L.S + c0 + j * 8 + 2 * t) =
+          make_double2(acc[i][j][0], acc[i][j][1]);
   if (lookahead && I == kt + 1 && J == kt + 1) {
     __syncthreads();   // the updated tile (global, written by this CTA) is the next pivot
     pivot_sweep(a, L, b, kt + 1);
   }
 }
 
-// (d) K strip: A_IK = CW_I (lower tiles, transposed above K), A_KK = -W
-__global__ void large_strip_kernel(SysArgs a, int p, int kt) {
-  if (a.done && *a.done) return;
+// nt == 1 (s <= 64 forced onto this path): A = -W
+__global__ void large_strip1_kernel(SysArgs a, int p) {
   const LargeBufs L = large_bufs(a.scratch, a.s, p);
-  const int b = blockIdx.y;
-  if (a.info[b]) return;
-  const int I = blockIdx.x;   // 0..nt-1
+  const int b = blockIdx.x;
+  const int dn = a.done ? *a.done : 0;
+  if (dn | a.info[b]) return;
   double* A = L.A + (size_t)b * L.S * L.S;
   for (int e = threadIdx.x; e < LT * LT; e += blockDim.x) {
     const int i = e / LT, j = e - i * LT;
-    if (I == kt) {
-      if (j <= i) A[(int64_t)(kt * LT + i) * L.S + kt * LT + j] = -L.W[((size_t)(kt & 1) * p + b) * LT * LT + e];
-    } else {
-      const double v = L.CW[((size_t)b * L.S + (size_t)I * LT + i) * LT + j];   // CW_I[i][j] = A'_{I i, K j}
-      if (I > kt) A[(int64_t)(I * LT + i) * L.S + kt * LT + j] = v;
-      else A[(int64_t)(kt * LT + j) * L.S + I * LT + i] = v;          // lower tile (K, I)
-    }
+    if (j <= i) A[(int64_t)i * L.S + j] = -L.W[(size_t)b * LT * LT + e];
   }
 }
 
-// (e) inv = -A (symmetric, s x s)
-__global__ void large_out_kernel(SysArgs a, int p) {
-  if (a.done && *a.done) return;
+// (e) inv = -A (symmetric, s x s): one CTA per 64 x 64 output tile, the upper tiles through a
+// shared-memory transpose of the stored lower tile (coalesced on both sides)
+__global__ void __launch_bounds__(LTHREADS) large_out_kernel(SysArgs a, int p) {
   const int s = a.s;
   const LargeBufs L = large_bufs(a.scratch, s, p);
   const int b = blockIdx.y;
-  if (a.info[b]) return;
-  const double* A = L.A + (size_t)b * L.S * L.S;
+  const int dn = a.done ? *a.done : 0;
+  if (dn | a.info[b]) return;
+  const int I = blockIdx.x / L.nt, J = blockIdx.x - I * L.nt;
+  const int hi = max(I, J), lo = min(I, J);
+  __shared__ double T[LT][LT + 1];
+  const double* A = L.A + (size_t)b * L.S * L.S + (int64_t)hi * LT * L.S + lo * LT;
+  for (int e = threadIdx.x; e < LT * LT; e += LTHREADS) {
+    const int i = e / LT, j = e - i * LT;
+    T[i][j] = A[(int64_t)i * L.S + j];
+  }
+  __syncthreads();
   double* out = a.inv + (int64_t)b * s * s;
-  const int64_t total = (int64_t)s * s;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / s), j = (int)(e - (int64_t)i * s);
-    out[e] = -((j <= i) ? A[(int64_t)i * L.S + j] : A[(int64_t)j * L.S + i]);
+  for (int e = threadIdx.x; e < LT * LT; e += LTHREADS) {
+    const int i = e / LT, j = e - i * LT;
+    const int gi = I * LT + i, gj = J * LT + j;
+    if (gi >= s || gj >= s) continue;
+    const double v = (I > J) ? T[i][j] : (I < J) ? T[j][i] : T[max(i, j)][min(i, j)];
+    out[(int64_t)gi * s + gj] = -v;
   }
 }
 
@@ -348,10 +379,10 @@ int launch_inverse_large(const SysArgs& a, int p, cudaStream_t st) {
       const int ntiles = m * (m + 1) / 2;
       if (ntiles > 0) large_update_kernel<<<dim3(p, ntiles), LTHREADS, smem, st>>>(a, p, kt);
     }
-    large_strip_kernel<<<dim3(nt, p), 256, 0, st>>>(a, p, kt);
+    else large_strip1_kernel<<<p, LTHREADS, 0, st>>>(a, p);   // single tile: A = -W
   }
-  large_out_kernel<<<dim3(32, p), 256, 0, st>>>(a, p);
-  note_launch(3 + nt * (nt > 1 ? 3 : 1));
+  large_out_kernel<<<dim3(nt * nt, p), LTHREADS, 0, st>>>(a, p);
+  note_launch(3 + nt * (nt > 1 ? 2 : 1));
   return check_launch("inverse_large");
 }
 

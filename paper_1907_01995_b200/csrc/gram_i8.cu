@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
     if (lane == 0) {
       // TMA producer: one 4 KB bulk copy per slice operand per stage
       const size_t offA = (size_t)J * 16 * 256, offB = (size_t)Kt * 16 * 256;
+      const bool diag = J == Kt;   // diagonal tile: B is the A operand, loaded once
       int q = 0;
       for (int ph = 0; ph < nphase; ++ph) {
         const int ns = (ph < nseg) ? S : S - 4;   // pass 0 reads all slices, pass 1 slices 1 .. S-4
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
           const int slot = q % I8_NST;
           const int nk = min(kpack, q1 - kst);
           if (q >= I8_NST) mbar_wait(&bar_free[slot], ((q / I8_NST) - 1) & 1);
-          mbar_arrive_expect_tx(&bar_full[slot], (unsigned)(2 * ns * nk * I8_OP));
+          mbar_arrive_expect_tx(&bar_full[slot], (unsigned)((diag ? 1 : 2) * ns * nk * I8_OP));
           uint8_t* sA = smem + slot * I8_STAGE;
           uint8_t* sB = sA + I8_S * I8_OP;
 #pragma unroll 1
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
             for (int s = 0; s < ns; ++s) {
               const uint8_t* src = a.sl + s * a.slice_bytes + row;
               bulk_g2s(sA + (h * 4 + s) * I8_OP, src + offA, I8_OP, &bar_full[slot]);
-              bulk_g2s(sB + (h * 4 + s) * I8_OP, src + offB, I8_OP, &bar_full[slot]);
+              if (!diag) bulk_g2s(sB + (h * 4 + s) * I8_OP, src + offB, I8_OP, &bar_full[slot]);
             }
           }
         }
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
           mbar_wait(&bar_full[slot], (q / I8_NST) & 1);
           tc_fence_after();
           const unsigned sA = smem_u32(smem + slot * I8_STAGE);
-          const unsigned sB = sA + I8_S * I8_OP;
+          const unsigned sB = (J == Kt) ? sA : sA + I8_S * I8_OP;
           if (S == 8) issue_stage<8>(tmem, sA, sB, p0, nk, first);
           else issue_stage<7>(tmem, sA, sB, p0, nk, first);
           tc_commit(&bar_free[slot]);

@@ -157,8 +157,62 @@ __global__ void i8_colexp_kernel(const double* __restrict__ Xc, int64_t ld, int6
   }
 }
 
+// The S balanced base-128 digits of 8 values, packed[s] byte i = digit s of x[i] (int8).
+// x 2^(7S-1-e) (exact, |.| <= 2^(7S-1)) is rounded once to an integer N; adding the bias
+// 64 (1 + 128 + ... + 128^(S-2)) turns the balanced digits d in [-64, 63] of the S-1 lower
+// positions into the plain 7-bit fields u = d + 64 of N + bias, and leaves the signed top
+// digit (|d_1| <= 64) in the bits above.  Each field is moved straight to its byte by one
+// (funnel) shift and one masked OR; u - 64 as an int8 is u ^ 0x40 sign-extended from bit 6,
+// done on four bytes at a time.  (The slicing pass was instruction-bound, not memory-bound,
+// with the digit recurrence in 64-bit arithmetic: ~140 instructions per value.)
+template <int S>
+__device__ __forceinline__ void slice_digits(const double (&x)[8], int e, unsigned long long (&packed)[I8_S]) {
+  long long bias = 0;
+#pragma unroll
+  for (int k = 0; k < S - 1; ++k) bias |= 64ll << (7 * k);
+  const int sc = 7 * S - 1 - e;
+  const bool fast = sc >= -1022 && sc <= 1023;   // 2^sc is a normal double: one exact multiplication
+  const double scale = fast ? __longlong_as_double((long long)(sc + 1023) << 52) : 1.0;
+  double xs[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) xs[i] = x[i];
+  if (!fast) {   // columns with a maximum near the ends of the double range
+#pragma unroll 1
+    for (int i = 0; i < 8; ++i) xs[i] = ldexp(xs[i], sc);
+  }
+  uint32_t w[I8_S][2];
+#pragma unroll
+  for (int s = 0; s < I8_S; ++s) w[s][0] = w[s][1] = 0u;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const long long N = __double2ll_rn(xs[i] * scale) + bias;
+    const uint32_t nlo = (uint32_t)(unsigned long long)N, nhi = (uint32_t)((unsigned long long)N >> 32);
+    const int half = i >> 2, sh8 = 8 * (i & 3);
+#pragma unroll
+    for (int k = 0; k < S - 1; ++k) {   // field k from the bottom = slice index S - 1 - k
+      const int r = 7 * k - sh8;        // bit 7k of N lands on bit sh8 of the word
+      const uint32_t v = r >= 32 ? nhi >> (r - 32) : (r >= 0 ? __funnelshift_r(nlo, nhi, r) : nlo << (-r));
+      w[S - 1 - k][half] |= v & (0x7fu << sh8);
+    }
+    const int r = 7 * (S - 1) - sh8;    // top digit: 8 bits from bit 7(S-1)
+    const uint32_t v = r >= 32 ? nhi >> (r - 32) : __funnelshift_r(nlo, nhi, r);
+    w[0][half] |= v & (0xffu << sh8);
+  }
+#pragma unroll
+  for (int s = 0; s < I8_S; ++s) {
+    if (s >= 1 && s < S) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t t = w[s][h] ^ 0x40404040u;
+        w[s][h] = t | ((t & 0x40404040u) << 1);
+      }
+    }
+    packed[s] = (unsigned long long)w[s][0] | ((unsigned long long)w[s][1] << 32);
+  }
+}
+
 // ---- digit slices in the canonical UMMA layout -----------------------------------------
-// CTA = one 8-feature group x 8 stages (256 samples); thread = (feature f, 8 samples).
+// CTA = one 8-feature group x 8 stages (256 samples); thread = (feature f, 4 pairs of samples).
 // Covariance: features 0..n-1 of Xc.  Block mode (idx != null): blockIdx.z = block b, whose
 // features are idx[b*n ..] (n = s, -1 = padding), exponents ex[feature], and the block's
 // per-position exponents are written to ex_blk[b * nfeat + position].
@@ -177,51 +231,52 @@ __global__ void __launch_bounds__(256) i8_slice_kernel(const double* __restrict_
     j = pos < n ? __ldg(idx + (size_t)blockIdx.z * n + pos) : -1;
     sl += (size_t)blockIdx.z * I8_S * slice_bytes;
   }
-  const int64_t k0 = (int64_t)blockIdx.y * 256 + lane * 8;
+  // load i of a lane: the pair of samples 64 i + 2 lane, + 1 of the CTA's 256 (a warp's load is
+  // 512 contiguous bytes of its feature column)
+  const int64_t kc = (int64_t)blockIdx.y * 256;
   double x[8];
-  if (j >= 0 && k0 + 8 <= len) {
-    const double2* p = reinterpret_cast<const double2*>(Xc + (int64_t)j * ld + k0);
+  if (j >= 0) {
+    const double* col = Xc + (int64_t)j * ld + kc;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const double2 t = __ldg(p + i);
-      x[2 * i] = t.x;
-      x[2 * i + 1] = t.y;
+      const int k = 64 * i + 2 * lane;
+      if (kc + k + 2 <= len) {
+        const double2 t = __ldg(reinterpret_cast<const double2*>(col + k));
+        x[2 * i] = t.x;
+        x[2 * i + 1] = t.y;
+      } else {
+        x[2 * i] = (kc + k < len) ? col[k] : 0.0;
+        x[2 * i + 1] = 0.0;
+      }
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = (j >= 0 && k0 + i < len) ? Xc[(int64_t)j * ld + k0 + i] : 0.0;
+    for (int i = 0; i < 8; ++i) x[i] = 0.0;
   }
   const int e = (j >= 0) ? __ldg(ex + j) : 0;
   if (idx && blockIdx.y == 0 && lane == 0) ex_blk[(size_t)blockIdx.z * ngrp * 8 + pos] = e;
   unsigned long long packed[I8_S];
+  if (S == 8) slice_digits<8>(x, e, packed);
+  else slice_digits<7>(x, e, packed);
+  // pair i -> stage 2 i + lane / 16, K chunk (lane / 8) % 2, bytes 2 (lane % 8), + 1 of feature f's
+  // 16-byte row: logical 16-byte chunk C = stage * 16 + chunk * 8 + f, stored at C ^ ((C >> 3) & 7)
+  // (the 8 rows of a core matrix spread over the 8 bank groups: conflict-free stores and loads)
 #pragma unroll
-  for (int s = 0; s < I8_S; ++s) packed[s] = 0ull;
+  for (int i = 0; i < 4; ++i) {
+    const int C = (2 * i + (lane >> 4)) * 16 + ((lane >> 3) & 1) * 8 + f;
+    const int off = (C ^ ((C >> 3) & 7)) * 16 + 2 * (lane & 7);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    // x 2^(6+7(S-1)-e) (exact, |.| < 2^55) rounded once to an integer N, then N's balanced
-    // base-128 digits from the bottom: d = ((N + 64) mod 128) - 64, N <- (N - d) / 128
-    // (exact shifts); the top digit is what remains, |d_1| <= 64
-    long long N = __double2ll_rn(ldexp(x[i], 7 * S - 1 - e));
-#pragma unroll
-    for (int s = I8_S - 1; s > 0; --s) {
-      if (s >= S) continue;
-      const long long d = ((N + 64) & 127) - 64;
-      N = (N - d) >> 7;
-      packed[s] |= (unsigned long long)(uint8_t)(int8_t)d << (8 * i);
-    }
-    packed[0] |= (unsigned long long)(uint8_t)(int8_t)N << (8 * i);
+    for (int s = 0; s < I8_S; ++s)
+      if (s < S) *reinterpret_cast<uint16_t*>(&buf[s][off]) = (uint16_t)(packed[s] >> (16 * i));
   }
-  // sample k0 + i -> stage lane / 4, chunk (lane % 4) / 2, byte (lane % 2) * 8 + i
-  const int off = (lane >> 2) * 256 + ((lane & 3) >> 1) * 128 + f * 16 + (lane & 1) * 8;
-#pragma unroll
-  for (int s = 0; s < I8_S; ++s) *reinterpret_cast<unsigned long long*>(&buf[s][off]) = packed[s];
   __syncthreads();
   // 8 slices x 8 stages x 256 B, 16 B per thread per pass
   const int kst0 = blockIdx.y * 8;
   for (int q = threadIdx.x; q < I8_S * 8 * 16; q += 256) {
     const int s = q >> 7, kl = (q >> 4) & 7, o = q & 15;
     if (kst0 + kl >= nstg || s >= S) continue;
-    const uint4 v = *reinterpret_cast<const uint4*>(&buf[s][kl * 256 + o * 16]);
+    const int C = kl * 16 + o;
+    const uint4 v = *reinterpret_cast<const uint4*>(&buf[s][(C ^ ((C >> 3) & 7)) * 16]);
     *reinterpret_cast<uint4*>(sl + s * slice_bytes + ((size_t)(kst0 + kl) * ngrp + g) * 256 + o * 16) = v;
   }
 }

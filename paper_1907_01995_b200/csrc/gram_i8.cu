@@ -116,6 +116,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// v 2^(ea + eb): two exact multiplications by powers of two while both are far inside the
+// double range (any realistic column scale), ldexp otherwise
+__device__ __forceinline__ double scale_pow2(double v, int ea, int eb) {
+  if (abs(ea) <= 400 && abs(eb) <= 400)
+    return v * __longlong_as_double((long long)(ea + 1023) << 52) * __longlong_as_double((long long)(eb + 1023) << 52);
+  return ldexp(v, ea + eb);
+}
+
 // ---- per-feature exponent: 2^e > max |x_j| ---------------------------------------------
 // The dropped digit products bound a Gram entry's error by 2^-52.8 max|x_j| max|x_k| per
 // sample, i.e. by 2^-52.8 r_j r_k relative to |x_j| |x_k| where r = max / rms of a column.
@@ -438,14 +446,26 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
         for (int c = 0; c < 32; ++c) {
           const int k = Kt * I8_TN + cc * 32 + c;
           if (k >= a.n || k < j) continue;
-          const double part = ldexp(acc[c], ej + __ldg(a.ex + k));
-          const double cur = (ph == 0 && !a.accum) ? 0.0 : Grow[k];
-          double val = cur + part;
-          if (last) {
-            if (!a.accum && a.div > 0.0) val = val / a.div;
-            if (k > j) a.G[(int64_t)k * a.n + j] = val;
+          const double part = scale_pow2(acc[c], ej, __ldg(a.ex + k));
+          if (a.div > 0.0 && !a.accum) {
+            // G = sum / div: the division follows the last phase's sum (read-modify-write)
+            const double cur = (ph == 0) ? 0.0 : Grow[k];
+            double val = cur + part;
+            if (last) {
+              val = val / a.div;
+              if (k > j) a.G[(int64_t)k * a.n + j] = val;
+            }
+            Grow[k] = val;
+          } else if (ph == 0 && !a.accum) {
+            // raw sums: the first phase stores, later ones add with fire-and-forget reductions
+            // (same thread, same address: ordered; the same sum as a read-modify-write, and no
+            // load latency while the tensor pipe waits for TMEM); the mirror gets the same terms
+            Grow[k] = part;
+            if (k > j) a.G[(int64_t)k * a.n + j] = part;
+          } else {
+            atomicAdd(Grow + k, part);
+            if (k > j) atomicAdd(a.G + (int64_t)k * a.n + j, part);
           }
-          Grow[k] = val;
         }
       }
       tc_fence_before();

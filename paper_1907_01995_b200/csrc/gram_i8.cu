@@ -51,7 +51,8 @@ constexpr int I8_OP = I8_TM * I8_KS;          // 4 KB per slice operand per stag
 constexpr int I8_STAGE = 2 * I8_S * I8_OP;    // 64 KB: 8 A + 8 B slice operands
 constexpr int I8_SEGST = 2046;                // stages per exact int32 segment (65472 samples)
 constexpr int I8_SMEM = I8_NST * I8_STAGE + 1024;
-constexpr int I8_THREADS = 192;               // warps 0-3 epilogue, 4 TMA producer, 5 MMA issuer
+constexpr int I8_EPI = 8;                     // epilogue warps: warp w drains TMEM lanes 32 (w % 4).., column half w / 4
+constexpr int I8_THREADS = (I8_EPI + 2) * 32;  // warps 0-7 epilogue, 8 TMA producer, 9 MMA issuer
 static_assert(I8_S * 64 * 64 * (I8_SEGST * (double)I8_KS) < 2147483648.0, "int32 group sums must stay exact");
 static_assert(4 * I8_TN <= 512, "a pass's weight groups must fit the 512 TMEM columns");
 static_assert(I8_S == 8, "storage for up to 8 slices; the two passes split the groups w = 2..S+1");
@@ -323,6 +324,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bar_full[I8_NST], bar_free[I8_NST], bar_acc, bar_tfree;
   __shared__ uint32_t tmem_slot;
+  __shared__ int ek_s[I8_TN];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // tile (J, Kt), Kt >= J: row features 128J.., column features 128Kt..
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
       mbar_init(&bar_free[i], 1);
     }
     mbar_init(&bar_acc, 1);
-    mbar_init(&bar_tfree, 128);
+    mbar_init(&bar_tfree, I8_EPI * 32);
     mbar_fence_init();
   }
   if (warp == 0) {
@@ -354,7 +356,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
   const int nseg = (a.nstg + I8_SEGST - 1) / I8_SEGST;
   const int nphase = 2 * nseg;
 
-  if (warp == 4) {
+  if (warp == I8_EPI) {
     if (lane == 0) {
       // TMA producer: one 4 KB bulk copy per slice operand per stage
       const size_t offA = (size_t)J * 16 * 256, offB = (size_t)Kt * 16 * 256;
@@ -387,7 +389,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == I8_EPI + 1) {
     if (lane == 0) {
       // MMA issuer: per stage the phase's slice products into their weight groups
       int q = 0;
@@ -415,21 +417,35 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
     }
     __syncwarp();
   } else {
-    // epilogue: warp w owns TMEM lanes 32w.. = row feature j = 128J + 32w + lane; per phase
-    // the FP64 partial sum_g 2^{-7(w-2)} C_w · 2^{e_j + e_k - 12} is added to G[j][k] (k >= j)
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-    const int j = J * I8_TM + warp * 32 + lane;
+    // epilogue: warp w owns TMEM lanes 32 (w % 4).. = row feature j = 128J + 32 (w % 4) + lane and
+    // the column half w / 4 of every group; per phase the FP64 partial
+    // sum_g 2^{-7(w-2)} C_w · 2^{e_j + e_k - 12} is added to G[j][k] (k >= j)
+    const int wq = warp & 3, half = warp >> 2;
+    const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
+    const int j = J * I8_TM + wq * 32 + lane;
     const bool jok = j < a.n;
     const int ej = jok ? __ldg(a.ex + j) - 12 : 0;
     double* Grow = a.G + (int64_t)(jok ? j : 0) * a.n;
+    // the column features' exponents, once per tile
+    {
+      const int t = threadIdx.x;
+      if (t < I8_TN) ek_s[t] = (Kt * I8_TN + t < a.n) ? __ldg(a.ex + Kt * I8_TN + t) : 0;
+      asm volatile("bar.sync 1, %0;" ::"n"(I8_EPI * 32) : "memory");
+    }
+    // 0: G = sum / div (read-modify-write, the division follows the last phase's sum);
+    // raw sums: 1 = first phase stores, 2 = later phases (and accumulation) add with
+    // fire-and-forget reductions — same thread, same address: ordered, the same sum as a
+    // read-modify-write but no load latency while the tensor pipe waits for TMEM; the mirror
+    // gets the same terms
     for (int ph = 0; ph < nphase; ++ph) {
       const int w0 = (ph < nseg) ? S - 2 : 2;   // groups w0 .. w0 + ng - 1 in TMEM columns 0..511
       const int ng = (ph < nseg) ? 4 : S - 4;
       const bool last = ph == nphase - 1;
+      const int mode = (a.div > 0.0 && !a.accum) ? 0 : ((ph == 0 && !a.accum) ? 1 : 2);
       mbar_wait(&bar_acc, ph & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int cc = 0; cc < I8_TN / 32; ++cc) {
+      for (int cc = half * (I8_TN / 64); cc < (half + 1) * (I8_TN / 64); ++cc) {
         double acc[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) acc[c] = 0.0;
@@ -442,29 +458,37 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
           for (int c = 0; c < 32; ++c) acc[c] = fma((double)v[c], wgt, acc[c]);
         }
         if (!jok) continue;
+        const int kb = Kt * I8_TN + cc * 32;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int k = Kt * I8_TN + cc * 32 + c;
-          if (k >= a.n || k < j) continue;
-          const double part = scale_pow2(acc[c], ej, __ldg(a.ex + k));
-          if (a.div > 0.0 && !a.accum) {
-            // G = sum / div: the division follows the last phase's sum (read-modify-write)
+        for (int c = 0; c < 32; ++c) acc[c] = scale_pow2(acc[c], ej, ek_s[cc * 32 + c]);
+        if (mode == 1) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int k = kb + c;
+            if (k >= a.n || k < j) continue;
+            Grow[k] = acc[c];
+            if (k > j) a.G[(int64_t)k * a.n + j] = acc[c];
+          }
+        } else if (mode == 2) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int k = kb + c;
+            if (k >= a.n || k < j) continue;
+            atomicAdd(Grow + k, acc[c]);
+            if (k > j) atomicAdd(a.G + (int64_t)k * a.n + j, acc[c]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int k = kb + c;
+            if (k >= a.n || k < j) continue;
             const double cur = (ph == 0) ? 0.0 : Grow[k];
-            double val = cur + part;
+            double val = cur + acc[c];
             if (last) {
               val = val / a.div;
               if (k > j) a.G[(int64_t)k * a.n + j] = val;
             }
             Grow[k] = val;
-          } else if (ph == 0 && !a.accum) {
-            // raw sums: the first phase stores, later ones add with fire-and-forget reductions
-            // (same thread, same address: ordered; the same sum as a read-modify-write, and no
-            // load latency while the tensor pipe waits for TMEM); the mirror gets the same terms
-            Grow[k] = part;
-            if (k > j) a.G[(int64_t)k * a.n + j] = part;
-          } else {
-            atomicAdd(Grow + k, part);
-            if (k > j) atomicAdd(a.G + (int64_t)k * a.n + j, part);
           }
         }
       }

@@ -105,17 +105,20 @@ __device__ __forceinline__ uint64_t umma_desc(unsigned saddr) {
 constexpr uint32_t I8_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(I8_TN >> 3) << 17) |
                               ((uint32_t)(I8_TM >> 4) << 24);
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
+// 16 TMEM lanes x 32 columns: thread t receives, for i = 0..3, v[4i + 0..1] = lane t / 4, columns
+// 8i + 2 (t % 4) + {0, 1} and v[4i + 2..3] = lane t / 4 + 8, the same columns (the accumulator
+// fragment layout of mma: rows over lane / 4, column pairs over lane % 4).  With it both the
+// direct stores G[j][k..k+1] (4 lanes = 64 contiguous bytes per row) and the mirror stores
+// G[k][j] (8 lanes = 64 contiguous bytes per row) fill whole sectors; the 32x32b shape
+// (thread = row) made every direct store touch 32 sectors.
+__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, int* v) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // v 2^(ea + eb): two exact multiplications by powers of two while both are far inside the
 // double range (any realistic column scale), ldexp otherwise
@@ -417,26 +420,29 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
     }
     __syncwarp();
   } else {
-    // epilogue: warp w owns TMEM lanes 32 (w % 4).. = row feature j = 128J + 32 (w % 4) + lane and
-    // the column half w / 4 of every group; per phase the FP64 partial
-    // sum_g 2^{-7(w-2)} C_w · 2^{e_j + e_k - 12} is added to G[j][k] (k >= j)
+    // epilogue: warp w drains TMEM lanes 32 (w % 4).. (row features 128J + 32 (w % 4) ..) and the
+    // column half w / 4 (two 32-column chunks) of every group.  Per phase the FP64 partial
+    // sum_g 2^{-7(w-2)} C_w · 2^{e_j + e_k - 12} of both chunks is formed in registers, TMEM is
+    // handed back to the MMA issuer, and only then the partial goes to G[j][k] (k >= j) and its
+    // mirror — the global-memory part of the epilogue runs under the next phase's MMAs.
     const int wq = warp & 3, half = warp >> 2;
+    const int tr = lane >> 2, tc = (lane & 3) * 2;
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
-    const int j = J * I8_TM + wq * 32 + lane;
-    const bool jok = j < a.n;
-    const int ej = jok ? __ldg(a.ex + j) - 12 : 0;
-    double* Grow = a.G + (int64_t)(jok ? j : 0) * a.n;
+    const int jb = J * I8_TM + wq * 32 + tr;   // this thread's rows: jb + 8 rr + 16 h
+    int ejr[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) ejr[r] = (jb + 8 * r < a.n) ? __ldg(a.ex + jb + 8 * r) - 12 : 0;
     // the column features' exponents, once per tile
     {
       const int t = threadIdx.x;
       if (t < I8_TN) ek_s[t] = (Kt * I8_TN + t < a.n) ? __ldg(a.ex + Kt * I8_TN + t) : 0;
       asm volatile("bar.sync 1, %0;" ::"n"(I8_EPI * 32) : "memory");
     }
-    // 0: G = sum / div (read-modify-write, the division follows the last phase's sum);
+    const bool vec_ok = Kt > J && (a.n & 1) == 0 && (reinterpret_cast<uintptr_t>(a.G) & 15) == 0;
+    // mode 0: G = sum / div (read-modify-write, the division follows the last phase's sum);
     // raw sums: 1 = first phase stores, 2 = later phases (and accumulation) add with
     // fire-and-forget reductions — same thread, same address: ordered, the same sum as a
-    // read-modify-write but no load latency while the tensor pipe waits for TMEM; the mirror
-    // gets the same terms
+    // read-modify-write but no load latency; the mirror gets the same terms
     for (int ph = 0; ph < nphase; ++ph) {
       const int w0 = (ph < nseg) ? S - 2 : 2;   // groups w0 .. w0 + ng - 1 in TMEM columns 0..511
       const int ng = (ph < nseg) ? 4 : S - 4;
@@ -444,56 +450,71 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
       const int mode = (a.div > 0.0 && !a.accum) ? 0 : ((ph == 0 && !a.accum) ? 1 : 2);
       mbar_wait(&bar_acc, ph & 1);
       tc_fence_after();
-#pragma unroll 1
-      for (int cc = half * (I8_TN / 64); cc < (half + 1) * (I8_TN / 64); ++cc) {
-        double acc[32];
+      double acc[2][32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[q][c] = 0.0;
 #pragma unroll 1
-        for (int g = ng - 1; g >= 0; --g) {   // smallest weight first, fixed order
+      for (int g = ng - 1; g >= 0; --g) {   // smallest weight first, fixed order
+        const double wgt = ldexp(1.0, -7 * (w0 + g - 2));
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
           int v[32];
-          tmem_ld32(trow + (uint32_t)(g * I8_TN + cc * 32), v);
-          const double wgt = ldexp(1.0, -7 * (w0 + g - 2));
+          const uint32_t col = (uint32_t)(g * I8_TN + (half * 2 + q) * 32);
+          tmem_ld_16x256b_x4(trow + col, v);
+          tmem_ld_16x256b_x4(trow + (16u << 16) + col, v + 16);
+          tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < 32; ++c) acc[c] = fma((double)v[c], wgt, acc[c]);
-        }
-        if (!jok) continue;
-        const int kb = Kt * I8_TN + cc * 32;
-#pragma unroll
-        for (int c = 0; c < 32; ++c) acc[c] = scale_pow2(acc[c], ej, ek_s[cc * 32 + c]);
-        if (mode == 1) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int k = kb + c;
-            if (k >= a.n || k < j) continue;
-            Grow[k] = acc[c];
-            if (k > j) a.G[(int64_t)k * a.n + j] = acc[c];
-          }
-        } else if (mode == 2) {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int k = kb + c;
-            if (k >= a.n || k < j) continue;
-            atomicAdd(Grow + k, acc[c]);
-            if (k > j) atomicAdd(a.G + (int64_t)k * a.n + j, acc[c]);
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int k = kb + c;
-            if (k >= a.n || k < j) continue;
-            const double cur = (ph == 0) ? 0.0 : Grow[k];
-            double val = cur + acc[c];
-            if (last) {
-              val = val / a.div;
-              if (k > j) a.G[(int64_t)k * a.n + j] = val;
-            }
-            Grow[k] = val;
-          }
+          for (int c = 0; c < 32; ++c) acc[q][c] = fma((double)v[c], wgt, acc[q][c]);
         }
       }
       tc_fence_before();
-      mbar_arrive(&bar_tfree);
+      mbar_arrive(&bar_tfree);   // TMEM drained: the next phase's MMAs may overwrite it
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int kl0 = (half * 2 + q) * 32 + tc;   // tile-local column of i = 0, u = 0
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {               // r = 2 h + rr
+          const int j = jb + 8 * r;
+          if (j >= a.n) continue;
+          double* Grow = a.G + (int64_t)j * a.n;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int kl = kl0 + 8 * i, k = Kt * I8_TN + kl;
+            const int e = (r >> 1) * 16 + 4 * i + 2 * (r & 1);
+            const double v0 = scale_pow2(acc[q][e], ejr[r], ek_s[kl]);
+            const double v1 = scale_pow2(acc[q][e + 1], ejr[r], ek_s[kl + 1]);
+            if (mode == 1 && vec_ok && k + 1 < a.n) {
+              *reinterpret_cast<double2*>(Grow + k) = make_double2(v0, v1);
+              a.G[(int64_t)k * a.n + j] = v0;
+              a.G[(int64_t)(k + 1) * a.n + j] = v1;
+              continue;
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int ku = k + u;
+              const double val = u ? v1 : v0;
+              if (ku >= a.n || ku < j) continue;
+              if (mode == 1) {
+                Grow[ku] = val;
+                if (ku > j) a.G[(int64_t)ku * a.n + j] = val;
+              } else if (mode == 2) {
+                atomicAdd(Grow + ku, val);
+                if (ku > j) atomicAdd(a.G + (int64_t)ku * a.n + j, val);
+              } else {
+                const double cur = (ph == 0) ? 0.0 : Grow[ku];
+                double t = cur + val;
+                if (last) {
+                  t = t / a.div;
+                  if (ku > j) a.G[(int64_t)ku * a.n + j] = t;
+                }
+                Grow[ku] = t;
+              }
+            }
+          }
+        }
+      }
     }
   }
   tc_fence_before();

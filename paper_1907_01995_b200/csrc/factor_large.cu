@@ -108,36 +108,43 @@ __device__ void pivot_sweep(const SysArgs& a, const LargeBufs& L, int b, int kt)
   if ((tid & 3) == 0) col[0][i] = v[0];   // column 0 = row i's entry 0 (owner: quarter 0)
   __syncthreads();
   int fail = 0;
-  for (int q = 0; q < LT; ++q) {
-    const double* c = col[q & 1];
-    const double d = c[q];
-    if (!(d > 0.0) || !isfinite(d)) {
-      fail = k0 + q + 1;    // uniform: every thread read the same pivot
-      break;
-    }
-    const double dinv = __drcp_rn(d);   // correctly rounded: the same value as 1.0 / d, no division slow path
-    const double ri = c[i] * dinv;
-    double cj[16];
+  const int quarter = tid & 3;
+  // pivots in groups of 16 = one quarter's columns: inside a group the pivot's position in
+  // its owner's registers is a compile-time index, so a pivot costs the 16 FMAs, 8 vector
+  // loads of the pivot column and a handful of predicated moves (the sweep is a chain of 64
+  // dependent pivots: its latency, not its flop count, is what the look-ahead has to hide)
+#pragma unroll 1
+  for (int Q = 0; Q < LT / 16 && !fail; ++Q) {
 #pragma unroll
-    for (int u = 0; u < 16; u += 2) {
-      const double2 t = *reinterpret_cast<const double2*>(c + j0 + u);
-      cj[u] = t.x;
-      cj[u + 1] = t.y;
-    }
+    for (int uq = 0; uq < 16; ++uq) {
+      const int q = Q * 16 + uq;
+      const double* c = col[q & 1];
+      const double d = c[q];
+      if (!(d > 0.0) || !isfinite(d)) {
+        fail = k0 + q + 1;    // uniform: every thread read the same pivot
+        break;
+      }
+      const double dinv = __drcp_rn(d);   // correctly rounded: the same value as 1.0 / d, no division slow path
+      const double ri = c[i] * dinv;
+      double cj[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) {
-      const int j = j0 + u;
-      if (j == q) v[u] = (i == q) ? -dinv : ri;
-      else if (i == q) v[u] = cj[u] * dinv;
-      else v[u] = v[u] - ri * cj[u];
-    }
-    // publish column q + 1 (owned by quarter (q + 1) / 16) for the next pivot
-    if (q + 1 < LT && (tid & 3) == ((q + 1) >> 4)) {
+      for (int u = 0; u < 16; u += 2) {
+        const double2 t = *reinterpret_cast<const double2*>(c + j0 + u);
+        cj[u] = t.x;
+        cj[u + 1] = t.y;
+      }
+      if (i == q) {   // the pivot row (4 threads)
 #pragma unroll
-      for (int u = 0; u < 16; ++u)
-        if (j0 + u == q + 1) col[(q + 1) & 1][i] = v[u];
+        for (int u = 0; u < 16; ++u) v[u] = cj[u] * dinv;
+      } else {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = v[u] - ri * cj[u];
+      }
+      if (quarter == Q) v[uq] = (i == q) ? -dinv : ri;   // the pivot column
+      // publish column q + 1 (owned by quarter (q + 1) / 16) for the next pivot
+      if (q + 1 < LT && quarter == ((q + 1) >> 4)) col[(q + 1) & 1][i] = v[(uq + 1) & 15];
+      __syncthreads();
     }
-    __syncthreads();
   }
   if (fail) {
     if (tid == 0) a.info[b] = fail;

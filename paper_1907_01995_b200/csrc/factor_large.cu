@@ -94,21 +94,23 @@ __global__ void large_assemble_kernel(SysArgs a, int p) {
 // (i, quarter) owns row i's 16 columns 16*quarter..; per pivot q the owner of column q
 // publishes it (double-buffered in smem, one barrier per pivot), and every thread updates
 // its 16 entries.  The sweep keeps the matrix symmetric, so column q is also row q.
+// A warp = 32 rows of ONE quarter: its lanes read the same 16 pivot-column entries (pure
+// broadcasts; with the four quarters inside a warp every vector load was a 4-way bank
+// conflict per quarter-warp, ~1000 shared-memory cycles per pivot).
 __device__ void pivot_sweep(const SysArgs& a, const LargeBufs& L, int b, int kt) {
   static_assert(LTHREADS == 4 * LT, "thread = (row, quarter of the columns)");
   __shared__ __align__(16) double col[2][LT];
   const double* A = L.A + (size_t)b * L.S * L.S;
-  const int tid = threadIdx.x, i = tid >> 2, j0 = (tid & 3) * 16, k0 = kt * LT;
+  const int tid = threadIdx.x, quarter = (tid >> 5) & 3, i = (tid >> 7) * 32 + (tid & 31), j0 = quarter * 16, k0 = kt * LT;
   double v[16];
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     const int j = j0 + u;
     v[u] = (j <= i) ? A[(int64_t)(k0 + i) * L.S + k0 + j] : A[(int64_t)(k0 + j) * L.S + k0 + i];
   }
-  if ((tid & 3) == 0) col[0][i] = v[0];   // column 0 = row i's entry 0 (owner: quarter 0)
+  if (quarter == 0) col[0][i] = v[0];   // column 0 = row i's entry 0 (owner: quarter 0)
   __syncthreads();
   int fail = 0;
-  const int quarter = tid & 3;
   // pivots in groups of 16 = one quarter's columns: inside a group the pivot's position in
   // its owner's registers is a compile-time index, so a pivot costs the 16 FMAs, 8 vector
   // loads of the pivot column and a handful of predicated moves (the sweep is a chain of 64

@@ -239,6 +239,9 @@ __global__ void __launch_bounds__(LTHREADS) large_cw_kernel(SysArgs a, int p, in
   const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;
   double* CW = L.CW + ((size_t)b * L.S + (size_t)I * LT) * LT;
   double* OLD = L.OLD + ((size_t)b * L.S + (size_t)I * LT) * LT;
+  const bool lastk = kt == L.nt - 1;   // last step: the strip is final, inv = -A goes straight out
+  const int s = a.s;
+  double* out = a.inv + (int64_t)b * s * s;
   // the old strip tile, as loaded
 #pragma unroll
   for (int u = 0; u < (LT * LT / 2) / LTHREADS; ++u) {
@@ -253,17 +256,34 @@ __global__ void __launch_bounds__(LTHREADS) large_cw_kernel(SysArgs a, int p, in
       const int row = r0 + i * 8 + g, col = c0 + j * 8 + 2 * t;
       const double2 v = make_double2(acc[i][j][0], acc[i][j][1]);
       *reinterpret_cast<double2*>(CW + (size_t)row * LT + col) = v;
-      if (I > kt) {
+      if (lastk) {   // I < K: inv[K k][I i] = inv[I i][K k] = -CW_I[i][k]
+        const int gi = I * LT + row, gk = kt * LT + col;
+        if (gi < s) {
+          if (gk < s) {
+            out[(int64_t)gk * s + gi] = -v.x;
+            out[(int64_t)gi * s + gk] = -v.x;
+          }
+          if (gk + 1 < s) {
+            out[(int64_t)(gk + 1) * s + gi] = -v.y;
+            out[(int64_t)gi * s + gk + 1] = -v.y;
+          }
+        }
+      } else if (I > kt) {
         *reinterpret_cast<double2*>(A + (int64_t)(I * LT + row) * L.S + kt * LT + col) = v;
       } else {   // lower tile (K, I): A[K k][I i] = CW_I[i][k]
         A[(int64_t)(kt * LT + col) * L.S + I * LT + row] = v.x;
         A[(int64_t)(kt * LT + col + 1) * L.S + I * LT + row] = v.y;
       }
     }
-  if (blockIdx.x == 0) {   // A_KK = -W (lower part)
+  if (blockIdx.x == 0) {   // A_KK = -W (lower part); last step: inv_KK = W
     for (int e = threadIdx.x; e < LT * LT; e += LTHREADS) {
       const int i = e / LT, j = e - i * LT;
-      if (j <= i) A[(int64_t)(kt * LT + i) * L.S + kt * LT + j] = -sY[i][j];
+      if (lastk) {
+        const int gi = kt * LT + i, gj = kt * LT + j;
+        if (gi < s && gj < s) out[(int64_t)gi * s + gj] = sY[max(i, j)][min(i, j)];
+      } else if (j <= i) {
+        A[(int64_t)(kt * LT + i) * L.S + kt * LT + j] = -sY[i][j];
+      }
     }
   }
 }
@@ -310,6 +330,26 @@ __global__ void __launch_bounds__(LTHREADS) large_update_kernel(SysArgs a, int p
   cp_async_wait<0>();
   __syncthreads();
   tile_mma(sX, sY, acc, -1.0);
+  if (kt == L.nt - 1) {
+    // last step: the tile is final; inv = -A goes straight out, both orientations (the lower
+    // part of a diagonal tile serves both, so inv is exactly symmetric)
+    const int s = a.s;
+    double* out = a.inv + (int64_t)b * s * s;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int row = r0 + i * 8 + g, col = c0 + j * 8 + 2 * t + u;
+          const int gi = I * LT + row, gj = J * LT + col;
+          if (gi >= s || gj >= s || (I == J && col > row)) continue;
+          const double v = -acc[i][j][u];
+          out[(int64_t)gi * s + gj] = v;
+          if (gi != gj) out[(int64_t)gj * s + gi] = v;
+        }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -390,8 +430,9 @@ int launch_inverse_large(const SysArgs& a, int p, cudaStream_t st) {
     }
     else large_strip1_kernel<<<p, LTHREADS, 0, st>>>(a, p);   // single tile: A = -W
   }
-  large_out_kernel<<<dim3(nt * nt, p), LTHREADS, 0, st>>>(a, p);
-  note_launch(3 + nt * (nt > 1 ? 2 : 1));
+  // nt > 1: the last step's kernels write inv = -A themselves
+  if (nt == 1) large_out_kernel<<<dim3(nt * nt, p), LTHREADS, 0, st>>>(a, p);
+  note_launch(2 + (nt == 1) + nt * (nt > 1 ? 2 : 1));
   return check_launch("inverse_large");
 }
 

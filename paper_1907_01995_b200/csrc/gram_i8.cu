@@ -74,6 +74,7 @@ struct I8Args {
   int blk_ex;
   const int* flags;      // i8_colexp_kernel's flags: bit 1 = some column's max/rms > I8_NARROW_RATIO
   int force8;            // RAC_I8_SLICES=8: always 8 slices
+  int lower_only;        // block mode: only the lower triangle (incl. the diagonal) is consumed
 };
 
 // slices of this data set: 8 when a column is wide (or forced), else 7
@@ -486,7 +487,7 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
             const double v0 = scale_pow2(acc[q][e], ejr[r], ek_s[kl]);
             const double v1 = scale_pow2(acc[q][e + 1], ejr[r], ek_s[kl + 1]);
             if (mode == 1 && vec_ok && k + 1 < a.n) {
-              *reinterpret_cast<double2*>(Grow + k) = make_double2(v0, v1);
+              if (!a.lower_only) *reinterpret_cast<double2*>(Grow + k) = make_double2(v0, v1);
               a.G[(int64_t)k * a.n + j] = v0;
               a.G[(int64_t)(k + 1) * a.n + j] = v1;
               continue;
@@ -496,11 +497,12 @@ __global__ void __launch_bounds__(I8_THREADS, 1) gram_i8_kernel(I8Args a) {
               const int ku = k + u;
               const double val = u ? v1 : v0;
               if (ku >= a.n || ku < j) continue;
+              const bool direct = !a.lower_only || ku == j;
               if (mode == 1) {
-                Grow[ku] = val;
+                if (direct) Grow[ku] = val;
                 if (ku > j) a.G[(int64_t)ku * a.n + j] = val;
               } else if (mode == 2) {
-                atomicAdd(Grow + ku, val);
+                if (direct) atomicAdd(Grow + ku, val);
                 if (ku > j) atomicAdd(a.G + (int64_t)ku * a.n + j, val);
               } else {
                 const double cur = (ph == 0) ? 0.0 : Grow[ku];
@@ -606,7 +608,7 @@ int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, 
   return check_launch("i8 exponents");
 }
 
-// block mode: the p block Grams (full symmetric s x s raw sums, out[b][s][s]) of the
+// block mode: the p block Grams (s x s raw sums, out[b][s][s], LOWER triangle incl. diagonal) of the
 // feature lists idx[b*s ..] (-1 = padding), ex_all = per-feature exponents of Xc
 int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32_t* idx, int s, int p,
                           const int* ex_all, const int* flags, double* out, void* ws, size_t ws_bytes,
@@ -638,6 +640,7 @@ int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32
   a.blk_sl = (size_t)I8_S * slice_bytes;
   a.blk_g = (int64_t)s * s;
   a.blk_ex = ngrp * 8;
+  a.lower_only = 1;   // the block systems are assembled from the lower triangle
   a.flags = flags;
   a.force8 = force8_env();
   note_launch();

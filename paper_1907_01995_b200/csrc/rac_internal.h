@@ -64,7 +64,7 @@ const int* gram_i8_ws_flags(const void* ws);
 int launch_gram_i8(const double* Xc, int64_t ld, int64_t len, int n, double* G, double div, int accum, void* ws,
                    size_t ws_bytes, cudaStream_t st, int* bad = nullptr);
 // block mode: per-feature exponents once per data set, then per sweep the p block Grams
-// (full symmetric raw sums out[b][s][s]) of idx[b*s ..] in one slicing + one GEMM launch
+// (raw sums out[b][s][s], lower triangle incl. the diagonal valid) of idx[b*s ..] in one slicing + one GEMM launch
 size_t gram_i8_blocks_ws_bytes(int64_t len, int s, int p);
 // flags (required): bit 0 = a column too heavy-tailed for the digit slices (the caller switches
 // to the DMMA tiles), bit 1 = a column wide enough to need 8 slices (else 7); read on the device

@@ -16,7 +16,7 @@ torch.cuda.synchronize()
 for rep in range(3):
     t = [time.perf_counter()]
     sol = en.EnSolver(m, n, case.block_size, Mode.RAC, case.lam, case.alpha, case.gamma); torch.cuda.synchronize(); t.append(time.perf_counter())
-    sol.set_gram_mode("covariance"); torch.cuda.synchronize(); t.append(time.perf_counter())
+    (sol.set_gram_mode("covariance") if en.choose_gram_mode(m, n, case.block_size, K) == "covariance" else None); torch.cuda.synchronize(); t.append(time.perf_counter())
     sol.set_data(X, y); torch.cuda.synchronize(); t.append(time.perf_counter())
     feeder = _device.PermutationFeeder(np.random.default_rng(0), n, sol.dev)
     perms = feeder.draw(16); p2 = feeder.draw(4); torch.cuda.synchronize(); t.append(time.perf_counter())

@@ -119,17 +119,25 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
       if (t + 1 < a.p) row1t_gather_idx(a.idx, s, a.order ? a.order[t + 1] : t + 1, w1);
     // ---- S1: reduce the per-CTA partials -> block right-hand side
     for (int j = gw; j < s; j += GW) {
+      // the coordinate's scalars (final since the previous sweep) are requested before the
+      // reduction, so their L2 round trips overlap it instead of following it
+      const int g = a.idx[(int64_t)b * s + j];
+      double cg = 0.0, xg = 0.0, zg = 0.0;
+      if (g >= 0) {
+        cg = a.c[g];
+        xg = ldcg(a.xi + g);
+        zg = ldcg(a.z + g);
+      }
       double acc = 0.0;
       // RC == 0: partials are [j][cta] (row_phase_1t), else [cta][j]
       for (int q = lane; q < P; q += 32)
         acc += ldcg(a.partial + (RC == 0 ? (int64_t)j * P + q : (int64_t)q * s + j));
       acc = warp_sum(acc);
       if (lane == 0) {
-        int g = a.idx[(int64_t)b * s + j];
         double rhs = 0.0;
         if (g >= 0) {
           double cross = acc / m;
-          rhs = -(sub(sub(add(a.c[g], cross), ldcg(a.xi + g)), mul(gamma, ldcg(a.z + g))));
+          rhs = -(sub(sub(add(cg, cross), xg), mul(gamma, zg)));
         }
         a.rhs[j] = rhs;
       }
@@ -142,16 +150,21 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
     for (int i = gw; i < s; i += GW) {
       int g = a.idx[(int64_t)b * s + i];
       const double* row = Ib + (int64_t)i * s;
+      // old beta / z / xi requested before the dot product (see S1)
+      double bo = 0.0, zo = 0.0, x0 = 0.0;
+      if (g >= 0) {
+        bo = ldcg(a.beta + g);
+        zo = ldcg(a.z + g);
+        x0 = ldcg(a.xi + g);
+      }
       double acc = 0.0;
       for (int j = lane; j < s; j += 32) acc += row[j] * ldcg(a.rhs + j);
       acc = warp_sum(acc);
       if (lane == 0) {
         if (g >= 0) {
           const double bn = acc;
-          const double bo = ldcg(a.beta + g);
           a.delta[i] = bn - bo;
           a.beta[g] = bn;
-          const double zo = ldcg(a.z + g), x0 = ldcg(a.xi + g);
           const double av = sub(x0, mul(gamma, bn));
           const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
           a.z[g] = zn;

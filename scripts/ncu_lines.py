@@ -39,15 +39,16 @@ for r in rows:
     key = (fname, ln)
     src[key] = r[1].strip()
     for k, v in d.items():
-        if k.startswith("stall_") and "Not Issued" not in k or k == "Warp Stall Sampling (All Samples)":
+        if k.startswith("stall_") and "Not Issued" not in k or k in ("Warp Stall Sampling (All Samples)", "Instructions Executed"):
             try:
                 per[key][k] += float(v or 0)
             except ValueError:
                 pass
 tot = sum(v["Warp Stall Sampling (All Samples)"] for v in per.values()) or 1.0
+itot = sum(v.get("Instructions Executed", 0) for v in per.values()) or 1.0
 ranked = sorted(per.items(), key=lambda kv: -kv[1]["Warp Stall Sampling (All Samples)"])[:top]
 for key, v in ranked:
     s = v["Warp Stall Sampling (All Samples)"]
     st = sorted(((x, k[6:]) for k, x in v.items() if k.startswith("stall_")), reverse=True)[:3]
-    print(f"{s / tot * 100:5.1f}% {key[0]}:{key[1]:<5d} {src[key][:70]:70s} " +
+    print(f"{s / tot * 100:5.1f}% inst {v.get('Instructions Executed', 0) / itot * 100:4.1f}% {key[0]}:{key[1]:<5d} {src[key][:70]:70s} " +
           " ".join(f"{n}={x / max(s, 1) * 100:.0f}%" for x, n in st))

@@ -28,7 +28,19 @@ namespace rac {
 constexpr int CTHREADS = 512;
 constexpr int SB = 8;   // pivots per blocked sweep step
 
-__device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }  // j <= i
+// The lower triangle is kept as 8 x 8 tiles: tile (I, J), J <= I, at (I (I + 1) / 2 + J) * 64
+// doubles, row-major inside (diagonal tiles are stored whole; their upper part is never read
+// as a value).  The rank-8 update then loads and stores a tile's DMMA fragment as one 16-byte
+// access per lane, 512 contiguous bytes per warp: conflict-free, where rows of the packed
+// triangle collided 3-4 ways (the update is bound by shared-memory wavefronts).
+__host__ __device__ __forceinline__ int tri_tiles(int s8) { return (s8 >> 3) * ((s8 >> 3) + 1) / 2; }
+__device__ __forceinline__ int pk(int i, int j) {   // j <= i
+  const int I = i >> 3, J = j >> 3;
+  return ((I * (I + 1) / 2 + J) << 6) + ((i & 7) << 3) + (j & 7);
+}
+// stride of the 8-row panel buffers Cm / CW: = 4 mod 16 doubles, so the update's fragment loads
+// (lane (g, t): row t or t + 4, column 8 I + g) fall on 32 distinct bank pairs
+__host__ __device__ __forceinline__ int panel_stride(int s8) { return s8 + ((4 - (s8 & 15)) + 16) % 16; }
 
 // gathered H_bb entry (0 for padding)
 __device__ __forceinline__ double h_entry(const SysArgs& a, int b, const int32_t* bidx, int i, int j) {
@@ -162,8 +174,9 @@ __device__ void cta_chol_inverse(double* A, int ld, int s, double* dY, double* o
   }
 }
 
-// blocked symmetric sweep on the packed lower triangle P (-> -P^{-1}); 0 or k+1
-__device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double* W, int* fail,
+// blocked symmetric sweep on the tiled lower triangle P (-> -P^{-1}); 0 or k+1.  s % 8 == 0
+// (the caller pads with identity rows); sp = panel_stride(s).
+__device__ int cta_sweep_packed(double* P, int s, int sp, double* Cm, double* CW, double* W, int* fail,
                                 long long* tr) {
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   if (tid == 0) *fail = 0;
@@ -174,10 +187,9 @@ __device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double
     ++tp;
   };
   for (int k = 0; k < s; k += SB) {
-    const int bb = min(SB, s - k);
-    for (int e = tid; e < bb * s; e += CTHREADS) {
+    for (int e = tid; e < SB * s; e += CTHREADS) {
       const int q = e / s, i = e - q * s, c = k + q;
-      Cm[q * s + i] = (i >= c) ? P[pk(i, c)] : P[pk(c, i)];
+      Cm[q * sp + i] = (i >= c) ? P[pk(i, c)] : P[pk(c, i)];
     }
     __syncthreads();
     stamp();
@@ -185,28 +197,22 @@ __device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double
       // 8x8 diagonal block swept in registers: lane l holds (r0 = l/8, c = l%8)
       // and (r0 + 4, c); pivot rows/columns move by warp shuffles.
       const int r0 = tx >> 3, c = tx & 7, r1 = r0 + 4;
-      double v0 = (r0 < bb && c < bb) ? Cm[c * s + k + r0] : 0.0;
-      double v1 = (r1 < bb && c < bb) ? Cm[c * s + k + r1] : 0.0;
+      double v0 = Cm[c * sp + k + r0];
+      double v1 = Cm[c * sp + k + r1];
       int f = 0;
       // branch-free (selects only) and fully unrolled: every lane runs the same
       // instruction stream; a non-positive pivot is recorded, the rest ignored
 #pragma unroll
       for (int q = 0; q < SB; ++q) {
-        if (q < bb) {
-          const double d = __shfl_sync(0xffffffffu, (q < 4) ? v0 : v1, (q & 3) * 8 + q);  // W[q][q]
-          const double wq0 = __shfl_sync(0xffffffffu, v0, r0 * 8 + q);     // W[r0][q]
-          const double wq1 = __shfl_sync(0xffffffffu, v1, r0 * 8 + q);     // W[r1][q]
-          const double wqc = __shfl_sync(0xffffffffu, (q < 4) ? v0 : v1, (q & 3) * 8 + c);  // W[q][c]
-          const bool ok = (d > 0.0) && isfinite(d);
-          if (!ok && !f) f = k + q + 1;
-          const double dinv = __drcp_rn(ok ? d : 1.0);
-          const double n0 = (r0 == q) ? ((c == q) ? -dinv : wqc * dinv)
-                                      : ((c == q) ? wq0 * dinv : v0 - wq0 * wqc * dinv);
-          const double n1 = (r1 == q) ? ((c == q) ? -dinv : wqc * dinv)
-                                      : ((c == q) ? wq1 * dinv : v1 - wq1 * wqc * dinv);
-          if (r0 < bb && c < bb) v0 = n0;
-          if (r1 < bb && c < bb) v1 = n1;
-        }
+        const double d = __shfl_sync(0xffffffffu, (q < 4) ? v0 : v1, (q & 3) * 8 + q);  // W[q][q]
+        const double wq0 = __shfl_sync(0xffffffffu, v0, r0 * 8 + q);     // W[r0][q]
+        const double wq1 = __shfl_sync(0xffffffffu, v1, r0 * 8 + q);     // W[r1][q]
+        const double wqc = __shfl_sync(0xffffffffu, (q < 4) ? v0 : v1, (q & 3) * 8 + c);  // W[q][c]
+        const bool ok = (d > 0.0) && isfinite(d);
+        if (!ok && !f) f = k + q + 1;
+        const double dinv = __drcp_rn(ok ? d : 1.0);
+        v0 = (r0 == q) ? ((c == q) ? -dinv : wqc * dinv) : ((c == q) ? wq0 * dinv : v0 - wq0 * wqc * dinv);
+        v1 = (r1 == q) ? ((c == q) ? -dinv : wqc * dinv) : ((c == q) ? wq1 * dinv : v1 - wq1 * wqc * dinv);
       }
       if (tx == 0 && f) *fail = f;
       W[tx] = -v0;
@@ -215,31 +221,31 @@ __device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double
     __syncthreads();
     stamp();
     if (*fail) return *fail;
-    for (int e = tid; e < bb * s; e += CTHREADS) {
+    for (int e = tid; e < SB * s; e += CTHREADS) {
       const int q = e / s, i = e - q * s;
       double acc = 0.0;
-      for (int r = 0; r < bb; ++r) acc += Cm[r * s + i] * W[r * SB + q];
-      CW[q * s + i] = acc;
+#pragma unroll
+      for (int r = 0; r < SB; ++r) acc += Cm[r * sp + i] * W[r * SB + q];
+      CW[q * sp + i] = acc;
     }
     __syncthreads();
     stamp();
-    if ((s & 7) == 0 && bb == SB) {
+    {
       // rank-8 update  A_RR -= CW Cm'  on FP64 tensor cores: one m8n8k4 pair per
       // 8x8 lower tile (D = C - A B, A = CW rows, B = Cm rows); the K strip is
       // rewritten below.  lane (g, t): A[g][t], B[t][g], D[g][2t..2t+1].
-      const int nt = s >> 3, ntiles = nt * (nt + 1) / 2;
+      const int ntiles = tri_tiles(s);
       const int g = tx >> 2, t4 = tx & 3;
       int I = 0, J = ty;   // tile ty in row-major lower-triangle order, advanced by 16
       while (J > I) { J -= I + 1; ++I; }
       for (int tile = ty; tile < ntiles; tile += CTHREADS / 32) {
-        const int r = 8 * I + g, c0 = 8 * J + 2 * t4;
-        const int off = pk(r, 0);
-        double d0 = (c0 <= r) ? P[off + c0] : 0.0;
-        double d1 = (c0 + 1 <= r) ? P[off + c0 + 1] : 0.0;
-        dmma884(d0, d1, -CW[t4 * s + 8 * I + g], Cm[t4 * s + 8 * J + g]);
-        dmma884(d0, d1, -CW[(t4 + 4) * s + 8 * I + g], Cm[(t4 + 4) * s + 8 * J + g]);
-        if (c0 <= r) P[off + c0] = d0;
-        if (c0 + 1 <= r) P[off + c0 + 1] = d1;
+        double2* pt = reinterpret_cast<double2*>(P + (tile << 6) + (g << 3) + 2 * t4);
+        double2 d = *pt;
+        const double a0 = -CW[t4 * sp + 8 * I + g], a1 = -CW[(t4 + 4) * sp + 8 * I + g];
+        const double b0 = Cm[t4 * sp + 8 * J + g], b1 = Cm[(t4 + 4) * sp + 8 * J + g];
+        dmma884(d.x, d.y, a0, b0);
+        dmma884(d.x, d.y, a1, b1);
+        *pt = d;
         J += CTHREADS / 32;
         while (J > I) { J -= I + 1; ++I; }
       }
@@ -248,40 +254,11 @@ __device__ int cta_sweep_packed(double* P, int s, double* Cm, double* CW, double
       for (int e = tid; e < (s - k) * SB; e += CTHREADS) {
         const int i = k + e / SB, q = e % SB, j = k + q;
         if (j > i) continue;
-        P[pk(i, j)] = (i < k + SB) ? -W[(i - k) * SB + q] : CW[q * s + i];
+        P[pk(i, j)] = (i < k + SB) ? -W[(i - k) * SB + q] : CW[q * sp + i];
       }
       for (int e = tid; e < k * SB; e += CTHREADS) {
         const int q = e / k, j = e - q * k, i = k + q;
-        P[pk(i, j)] = CW[q * s + j];
-      }
-    } else {
-      for (int pr = ty; pr < (s + 1) / 2; pr += CTHREADS / 32) {
-        for (int half = 0; half < 2; ++half) {
-          const int i = half ? s - 1 - pr : pr;
-          if (half && i == pr) break;
-          const int off = pk(i, 0);
-          const bool iK = (i >= k && i < k + bb);
-          double cw[SB];
-#pragma unroll
-          for (int q = 0; q < SB; ++q) cw[q] = (q < bb) ? CW[q * s + i] : 0.0;
-          for (int j = tx; j <= i; j += 32) {
-            const bool jK = (j >= k && j < k + bb);
-            double v;
-            if (iK && jK) {
-              v = -W[(i - k) * SB + (j - k)];
-            } else if (jK) {
-              v = CW[(j - k) * s + i];
-            } else if (iK) {
-              v = CW[(i - k) * s + j];
-            } else {
-              v = P[off + j];
-#pragma unroll
-              for (int q = 0; q < SB; ++q)
-                if (q < bb) v -= cw[q] * Cm[q * s + j];
-            }
-            P[off + j] = v;
-          }
-        }
+        P[pk(i, j)] = CW[q * sp + j];
       }
     }
     __syncthreads();
@@ -297,8 +274,8 @@ struct FactorSmemPlan {
 
 constexpr size_t kMaxDyn = 227 * 1024 - 2048;
 __host__ __device__ inline size_t packed_bytes(int s) {
-  const size_t s8 = (s + 7) & ~7;
-  return (s8 * (s8 + 1) / 2 + 2 * SB * s8) * sizeof(double);
+  const int s8 = (s + 7) & ~7;
+  return ((size_t)tri_tiles(s8) * 64 + 2 * SB * (size_t)panel_stride(s8)) * sizeof(double);
 }
 __host__ __device__ inline size_t square_bytes(int s) { return ((size_t)s * (s + 1) + s) * sizeof(double); }
 
@@ -319,20 +296,19 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
   if (mode == FACTOR_INVERSE && use_packed) {
     // padded to a multiple of 8 (identity rows) so the update runs on DMMA tiles
     const int s8 = (s + 7) & ~7;
+    const int sp = panel_stride(s8);
+    const int ntri = tri_tiles(s8) * 64;   // doubles of the tiled triangle
     double* P = fsm;
-    double* Cm = fsm + (size_t)s8 * (s8 + 1) / 2;
-    double* CW = Cm + SB * s8;
+    double* Cm = fsm + ntri;
+    double* CW = Cm + SB * sp;
     double* hbo = a.hbb_out ? a.hbb_out + (int64_t)b * s * s : nullptr;
     const int tx = tid & 31, ty = tid >> 5;
-    // block indices staged in smem (Cm is free until the sweep), then every row's
-    // entries fetched as one batch of independent loads per lane (s8 <= 256)
+    // block indices staged in smem (Cm is free until the sweep), then every thread fetches
+    // batches of 8 independent entries (one L2 round trip per 8 * CTHREADS entries)
     int* sbi = reinterpret_cast<int*>(Cm);
     for (int i = tid; i < s; i += CTHREADS) sbi[i] = bidx ? bidx[i] : i;
     __syncthreads();
     const double* wsb = a.ws ? a.ws + (int64_t)b * a.splits * s * s : nullptr;
-    // packed lower triangle, 8 independent gathers per thread in flight (one L2
-    // round trip per 8 * CTHREADS entries instead of one per row and warp)
-    const int ntri = s8 * (s8 + 1) / 2;
     for (int e0 = 0; e0 < ntri; e0 += 8 * CTHREADS) {
       double v[8];
       int pos[8];
@@ -342,12 +318,15 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
         pos[u] = e;
         double val = 0.0;
         if (e < ntri) {
-          int i = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-          while (pk(i + 1, 0) <= e) ++i;
-          while (pk(i, 0) > e) --i;
-          const int j = e - pk(i, 0);
+          // tile T = I (I + 1) / 2 + J of the triangle, element (w / 8, w % 8) inside
+          const int T = e >> 6, w = e & 63;
+          int I = (int)((sqrtf(8.0f * (float)T + 1.0f) - 1.0f) * 0.5f);
+          while ((I + 1) * (I + 2) / 2 <= T) ++I;
+          while (I * (I + 1) / 2 > T) --I;
+          const int J = T - I * (I + 1) / 2;
+          const int i = 8 * I + (w >> 3), j = 8 * J + (w & 7);
           val = (i == j) ? 1.0 : 0.0;
-          if (i < s && j < s) {
+          if (i < s && j <= i) {
             const int gi = sbi[i], gj = sbi[j];
             if (!(bidx && (gi < 0 || gj < 0))) {
               double acc = 0.0;
@@ -365,6 +344,8 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
               if (i == j) acc += a.shift;
               val = acc;
             }
+          } else if (j > i) {
+            val = 0.0;   // upper part of a diagonal tile: carried along by the update, never used
           }
         }
         v[u] = val;
@@ -394,13 +375,31 @@ __global__ void __launch_bounds__(CTHREADS) factor_kernel(SysArgs a, int mode, i
     }
     long long* tr = (a.trace && blockIdx.x == 0) ? a.trace + 2 : nullptr;
     if (tr && tid == 0) a.trace[1] = gtimer();
-    const int f = cta_sweep_packed(P, s8, Cm, CW, W, &fail, tr);
+    const int f = cta_sweep_packed(P, s8, sp, Cm, CW, W, &fail, tr);
     __syncthreads();
     if (!f) {
       if (tid == 0) a.info[b] = 0;
-      for (int e = tid; e < s * s; e += CTHREADS) {
-        const int i = e / s, j = e - i * s;
-        out[e] = -((j <= i) ? P[pk(i, j)] : P[pk(j, i)]);
+      // inv = -P, both orientations from each lower tile: a warp per tile, lane (g, t) holds
+      // (8 I + g, 8 J + 2 t .. + 1): 64 contiguous bytes per row either way
+      {
+        const int g = tx >> 2, t4 = tx & 3;
+        int I = 0, J = ty;
+        while (J > I) { J -= I + 1; ++I; }
+        for (int tile = ty; tile < tri_tiles(s8); tile += CTHREADS / 32) {
+          const double2 d = *reinterpret_cast<const double2*>(P + (tile << 6) + (g << 3) + 2 * t4);
+          const int i = 8 * I + g;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int j = 8 * J + 2 * t4 + u;
+            if (i < s && j <= i) {
+              const double v = -(u ? d.y : d.x);
+              out[(int64_t)i * s + j] = v;
+              if (j < i) out[(int64_t)j * s + i] = v;
+            }
+          }
+          J += CTHREADS / 32;
+          while (J > I) { J -= I + 1; ++I; }
+        }
       }
       return;
     }

@@ -244,18 +244,50 @@ __device__ __forceinline__ void row1t_gather_beta(int s, const double* xsrc, con
   cp_async_commit();
 }
 
+// The resident-tile dot products in column chunks: the same operations in the same order as
+// strided_dot (four chains over j = j0, j0 + step, ...; the tail into chain 0), cut at chunk ends
+// that are multiples of 4 * step, so the chains run on across chunks and the result is
+// bit-identical to the unchunked sum.
+struct Dot4 {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int j = 0;
+};
+__device__ __forceinline__ void dot4_chunk(Dot4& d, const double* col, const double* v, int ce, int step, int ld) {
+  int j = d.j;
+  for (; j + 3 * step < ce; j += 4 * step) {
+    d.a0 += col[j * ld] * v[j];
+    d.a1 += col[(j + step) * ld] * v[j + step];
+    d.a2 += col[(j + 2 * step) * ld] * v[j + 2 * step];
+    d.a3 += col[(j + 3 * step) * ld] * v[j + 3 * step];
+  }
+  d.j = j;
+}
+__device__ __forceinline__ double dot4_finish(Dot4& d, const double* col, const double* v, int s, int step, int ld) {
+  for (int j = d.j; j < s; j += step) d.a0 += col[j * ld] * v[j];
+  return (d.a0 + d.a1) + (d.a2 + d.a3);
+}
+
+constexpr int R1T_NC = 4;   // column chunks of the tile pipeline
+
+// Columns of the tile are released chunk by chunk while (a) runs and refilled at once with
+// the next block's columns (16-byte cp.async, one group per chunk); (c) consumes the chunks as
+// they land.  The tile's HBM read (D once per sweep) thereby overlaps both reductions instead
+// of standing between them.
 template <class TFn>
 __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r0, int nr,
                              const int32_t* __restrict__ idx, int s, int bprev, int bnext, const double* delta,
                              const double* xsrc, double* partial, const Row1tSmem& w, TFn tfn,
                              long long* rt = nullptr, bool pre_gathered = false) {
-  // rt (tracing, CTA 0 thread 0): %globaltimer after (a), after the tile load, after (c), after (d)
+  // rt (tracing, CTA 0 thread 0): %globaltimer after (a) + the issue of the loads, after the
+  // first chunk landed, after (c), after (d)
   const int tid = threadIdx.x;
   // groups of the row reductions; the last CTA's shorter row range (nr < rw) must stay
   // inside the reduction buffer sized for rw rows
   const int G = min(row1t_groups(nr), w.redcap / nr);
   const int row = tid % nr, grp = tid / nr;
   const bool act = grp < G;
+  // chunk width: a multiple of 4 G columns (the dot products' four chains of stride G)
+  const int CH = (((s + R1T_NC - 1) / R1T_NC + 4 * G - 1) / (4 * G)) * (4 * G);
   if (bprev >= 0)
     for (int j = tid; j < s; j += RP_THREADS) w.sDel[j] = ldcg(delta + j);
   if (bnext >= 0 && !pre_gathered)
@@ -264,34 +296,66 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
       w.sIdx[j] = g;
       w.sX[j] = (g >= 0) ? ldcg(xsrc + g) : 0.0;
     }
+  if (bnext >= 0 && pre_gathered) cp_async_wait<0>();   // this thread's beta gathers (row1t_gather_beta)
   __syncthreads();
+  const int h = nr >> 1;   // 16-byte pieces per column (nr, r0, ld and the row stride are even)
+  auto issue_chunk = [&](int c) {
+    const int cb = min(c * CH, s), ce = min(cb + CH, s);
+    if (bnext >= 0)
+      for (int e = tid; e < (ce - cb) * h; e += RP_THREADS) {
+        const int jj = e / h, j = cb + jj, i = 2 * (e - jj * h);
+        const int g = w.sIdx[j];
+        double* d = w.tile + (size_t)j * w.rwp + i;
+        if (g >= 0) cp_async16(d, V + (int64_t)g * ld + r0 + i);
+        else d[0] = d[1] = 0.0;
+      }
+    cp_async_commit();
+  };
   if (bprev >= 0) {   // (a) resident tile holds X[rows, b_prev]
-    if (act) w.red[grp * nr + row] = row1t_dot(w.tile, w.rwp, row, w.sDel, grp, s, G);
-    __syncthreads();
+    Dot4 d;
+    d.j = grp;
+#pragma unroll
+    for (int c = 0; c < R1T_NC; ++c) {
+      const int ce = (c == R1T_NC - 1) ? s : min((c + 1) * CH, s);
+      const bool fin = ce == s && (c == 0 || c * CH < s);   // the chunk that holds the last columns (and the tail)
+      if (act) dot4_chunk(d, w.tile + row, w.sDel, ce, G, w.rwp);
+      if (fin && act) w.red[grp * nr + row] = dot4_finish(d, w.tile + row, w.sDel, s, G, w.rwp);
+      __syncthreads();   // every thread is done with the chunk's columns
+      issue_chunk(c);
+    }
     if (tid < nr) {
       double u = 0.0;
       for (int q = 0; q < G; ++q) u += w.red[q * nr + tid];
       w.sR[tid] += u;
     }
     __syncthreads();
+  } else {
+#pragma unroll
+    for (int c = 0; c < R1T_NC; ++c) issue_chunk(c);
   }
   if (rt) rt[0] = gtimer();
-  if (bnext < 0) return;
-  // (b) 16-byte pieces (nr, r0, ld and the row stride are even)
-  const int h = nr >> 1;
-  for (int e = tid; e < s * h; e += RP_THREADS) {
-    const int j = e / h, i = 2 * (e - j * h);
-    const int g = w.sIdx[j];
-    double* d = w.tile + (size_t)j * w.rwp + i;
-    if (g >= 0) cp_async16(d, V + (int64_t)g * ld + r0 + i);
-    else d[0] = d[1] = 0.0;
+  if (bnext < 0) {
+    cp_async_wait<0>();
+    return;
   }
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  if (rt) rt[1] = gtimer();
-  // (c)
-  if (act) w.red[grp * nr + row] = row1t_dot(w.tile, w.rwp, row, w.sX, grp, s, G);
+  // (c) chunk c is complete when at most NC - 1 - c groups are pending
+  {
+    Dot4 d;
+    d.j = grp;
+#pragma unroll
+    for (int c = 0; c < R1T_NC; ++c) {
+      if (c == 0) cp_async_wait<R1T_NC - 1>();
+      else if (c == 1) cp_async_wait<R1T_NC - 2>();
+      else if (c == 2) cp_async_wait<R1T_NC - 3>();
+      else cp_async_wait<0>();
+      __syncthreads();
+      if (rt && c == 0) rt[1] = gtimer();
+      const int ce = (c == R1T_NC - 1) ? s : min((c + 1) * CH, s);
+      const bool fin = ce == s && (c == 0 || c * CH < s);
+      if (act) dot4_chunk(d, w.tile + row, w.sX, ce, G, w.rwp);
+      if (fin && act) w.red[grp * nr + row] = dot4_finish(d, w.tile + row, w.sX, s, G, w.rwp);
+    }
+  }
   __syncthreads();
   if (tid < nr) {
     double u = 0.0;

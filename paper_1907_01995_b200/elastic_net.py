@@ -410,14 +410,17 @@ def _fit_on(device: int, X, y, spec: ElasticNetSpec, m: int, n: int, gamma: floa
         else:
             feeder = _device.PermutationFeeder(rng, n, solver.dev)
         step = 1 if sweep_hook is not None else max(1, int(batch))
+        # the first batch is drawn before any sweep can start: keep its host time (~1 us per 100
+        # coordinates per sweep) small; later batches are drawn while the device runs
+        first = max(1, min(step, 200_000 // max(1, feeder.size)))
         done = 0
         iterations, converged, failed = 0, False, -1
         if sweep_hook is None and spec.tol is not None and spec.iters > 0:
             # with a tolerance: batch k+1 is enqueued before batch k's status is read (a
             # non-blocking poll of the run before the latest), so no host round trip
             # separates the batches; launches after convergence are no-ops on the device
-            solver.run(feeder.draw(min(step, spec.iters)), spec.tol)
-            done = min(step, spec.iters)
+            solver.run(feeder.draw(min(first, spec.iters)), spec.tol)
+            done = min(first, spec.iters)
             while True:
                 lag = 0
                 if done < spec.iters:
@@ -429,9 +432,9 @@ def _fit_on(device: int, X, y, spec: ElasticNetSpec, m: int, n: int, gamma: floa
                 if failed >= 0 or conv or lag == 0:
                     break
             done = spec.iters          # the final progress() below reports the true state
-        perms = feeder.draw(min(step, spec.iters)) if done < spec.iters else None
+        perms = feeder.draw(min(first, spec.iters)) if done < spec.iters else None
         while done < spec.iters:
-            k = min(step, spec.iters - done)
+            k = perms.shape[0]
             solver.run(perms, spec.tol)
             done += k
             # the next batch's permutations are drawn (host PCG64, same stream order) while

@@ -350,6 +350,21 @@ def en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, workload,
     eff["factor"] = stages.get("factor", 0.0) / max(1, prep_batch)
     eff.pop("assembly", None)
     dom = max(eff, key=eff.get)
+    roof = en_stage_roofline(dom, stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, slices)
+    roof["traffic"] = traffic_table().get(f"{workload}:{roof['kernel'].split()[0]}")
+    # every stage against its own roof (the headline entry above is the stage that bounds a sweep)
+    roof["all_stages"] = [
+        {k: v for k, v in en_stage_roofline(st, stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, slices).items()
+         if k in ("stage", "kernel", "bound", "achieved", "peak", "unit", "frac")}
+        | {"ms_per_sweep": stages[st]}
+        for st in ("gram", "factor", "chain")
+        if stages.get(st, 0.0) > 0.0 and not (st == "gram" and gram_mode == "covariance")]   # G: once per fit
+    return roof
+
+
+def en_stage_roofline(dom, stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, slices) -> dict:
+    """One stage's kernel against the roof that bounds it (algorithmic work per sweep ÷ the stage's
+    measured time per sweep)."""
     sec = stages[dom] * 1e-3
     if dom == "chain":
         if gram_mode == "covariance":
@@ -388,7 +403,6 @@ def en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, workload,
                 "bound": "tensor", "achieved": achieved, "peak": fp64, "unit": "TFLOP/s",
                 "frac": achieved / fp64, "algorithmic": "2 s^3 flop per block inverse x p blocks per sweep"}
     roof["stage"] = dom
-    roof["traffic"] = traffic_table().get(f"{workload}:{roof['kernel'].split()[0]}")
     return roof
 
 
@@ -452,6 +466,12 @@ def measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline: b
     lib.rac_en_timing(solver.h, stage, nt)
     stages = {k: float(v) / max(nt.value, 1) for k, v in zip(("assembly", "gram", "factor", "chain"), stage)}
     out["stage_ms_per_sweep"] = stages
+    # int8 block Grams: the gram stage is two kernels (digit slicing, then the tcgen05 GEMM)
+    sl_ms = np.ctypeslib.ctypes.c_double(0.0)
+    lib.rac_en_timing_slicing(solver.h, np.ctypeslib.ctypes.byref(sl_ms))
+    slice_ms = sl_ms.value / max(nt.value, 1)
+    if slice_ms > 0.0:
+        out["gram_stage_split_ms"] = {"i8_slice_kernel": slice_ms, "gram_i8_kernel": stages["gram"] - slice_ms}
     # chain phase trace (CTA 0 %globaltimer at each phase boundary of one sweep)
     lib.rac_en_set_timing(solver.h, 2)
     solver.run(_device.PermutationFeeder(rng, n, dev).draw(1), None)
@@ -579,6 +599,22 @@ def measure_en(cfg, case, args, world, rank, local, peaks, fp64, i8, headline: b
     hbm = peaks.get("hbm_gbs", HBM_FALLBACK_GBS)
     out["roofline"] = en_roofline(stages, m, n, s, p, gram_mode, variant, hbm, fp64, i8, case.name,
                                   chain_trace.get("prep_batch_sweeps", 1), slices)
+    split = out.get("gram_stage_split_ms")
+    if split and gram_mode == "blocks":
+        # the gram stage's two kernels against their own roofs: slicing moves 8 m n bytes in (FP64
+        # columns) and `slices` m n bytes out; the GEMM's int8 ops are the stage entry's
+        jt = (s + 127) // 128
+        prods = slices * (slices + 1) // 2
+        ops = 2.0 * prods * p * (jt * (jt + 1) // 2) * 128 * 128 * ((m + 31) // 32 * 32)
+        byts = (8.0 + slices) * float(m) * n
+        sl_s, mm_s = split["i8_slice_kernel"] * 1e-3, split["gram_i8_kernel"] * 1e-3
+        out["roofline"]["all_stages"] = [
+            {"stage": "gram (slicing)", "kernel": "i8_slice_kernel", "bound": "hbm", "achieved": byts / sl_s / 1e9,
+             "peak": hbm, "unit": "GB/s", "frac": byts / sl_s / 1e9 / hbm, "ms_per_sweep": split["i8_slice_kernel"]},
+            {"stage": "gram (GEMM)", "kernel": "gram_i8_kernel", "bound": "tensor", "achieved": ops / mm_s / 1e12,
+             "peak": i8["peak"], "unit": "TOPS (int8)", "frac": ops / mm_s / 1e12 / i8["peak"],
+             "ms_per_sweep": split["gram_i8_kernel"]},
+        ] + [e for e in out["roofline"]["all_stages"] if e["stage"] != "gram"]
     out["roofline"]["peak_source"] = out["roofline"].get("peak_source", "MEASURED_PEAKS.json hbm_gbs"
                                                          if out["roofline"]["unit"] == "GB/s"
                                                          else "cuBLAS DGEMM 8192^3 measured in this run")

@@ -148,6 +148,9 @@ int rac_en_history(rac_en_ctx* ctx, double* primal, double* dual, int32_t capaci
  * factor, chain] over the timed sweeps, then resets. */
 int rac_en_set_timing(rac_en_ctx* ctx, int32_t enable);
 int rac_en_timing(rac_en_ctx* ctx, double* stage_ms_host4, int32_t* sweeps_host);
+/* The digit-slicing share (ms, summed over the sweeps of the last rac_en_timing call) of
+ * the gram stage when the block Grams ran on the int8 tensor cores; 0 otherwise. */
+int rac_en_timing_slicing(rac_en_ctx* ctx, double* slice_ms_host);
 /* enable >= 2 in rac_en_set_timing also records %globaltimer at every chain
  * phase boundary of each sweep (CTA 0), up to 8 + 16p stamps (the last
  * sweep's are kept).  Streaming chain: [start, R0, then per block bar, S1,

@@ -50,6 +50,7 @@ SIGNATURES = {
     "rac_en_history": (_i32, [_p, _p, _p, _i32]),
     "rac_en_set_timing": (_i32, [_p, _i32]),
     "rac_en_timing": (_i32, [_p, _pf64, _pi32]),
+    "rac_en_timing_slicing": (_i32, [_p, _pf64]),
     "rac_en_trace": (_i32, [_p, C.POINTER(C.c_int64), _i32]),
     "rac_debug_buffer": (_i32, [_p]),
     "rac_gram_covariance": (_i32, [_p, _i64, _i64, _i32, _p, _f64, _i32]),

@@ -373,6 +373,8 @@ struct rac_en_ctx {
   // optional per-stage CUDA-event timing: [assembly, gram, factor, chain]
   bool timing = false;
   std::vector<cudaEvent_t> events;  // 5 per timed sweep
+  std::vector<cudaEvent_t> slice_events;   // int8 block Grams: after the slicing pass, one per timed sweep
+  double slice_ms = 0.0;                    // summed by rac_en_timing, read by rac_en_timing_slicing
   long long* trace = nullptr;       // phase timestamps of the last traced sweep (chain | factor)
   long long* trace_buf = nullptr;
 };
@@ -617,10 +619,10 @@ int en_factor(rac_en_ctx* c, cudaStream_t st, int sweeps = 1) {
 
 // block mode: the p block Grams of the partition in c->idx into gram_ws — int8 tensor
 // cores (exact digit slices, gram_i8.cu) when reserved, else the FP64 DMMA tiles
-int en_block_gram(rac_en_ctx* c, cudaStream_t st) {
+int en_block_gram(rac_en_ctx* c, cudaStream_t st, cudaEvent_t after_slicing = nullptr) {
   if (c->bg_ws && !c->i8_off)
     return rac::launch_gram_i8_blocks(c->Xc, c->ld, c->m, c->idx, c->s, c->p, c->ex_all, c->i8_bad, c->gram_ws,
-                                      c->bg_ws, c->bg_cap, st);
+                                      c->bg_ws, c->bg_cap, st, after_slicing);
   return rac::launch_gram(c->Xc, c->ld, c->m, c->idx, nullptr, c->s, c->p, c->gram_ws, c->gp, st, c->ctrl);
 }
 
@@ -1502,8 +1504,11 @@ static int en_run(rac_en_ctx* c, const int64_t* perms, int32_t count, double tol
       if (rc) return rc;
       if (c->timing) cudaEventRecord(ev[1], c->st);
       if (c->gram_mode != 1) {
-        rc = en_block_gram(c, c->st);
+        cudaEvent_t mid = nullptr;
+        if (c->timing && c->bg_ws && !c->i8_off) cudaEventCreate(&mid);
+        rc = en_block_gram(c, c->st, mid);
         if (rc) return rc;
+        if (mid) c->slice_events.push_back(mid);
       }
       if (c->timing) cudaEventRecord(ev[2], c->st);
       rc = en_factor(c, c->st);
@@ -1639,9 +1644,27 @@ extern "C" int rac_en_timing(rac_en_ctx* c, double* stage_ms, int32_t* sweeps) {
       stage_ms[q] += ms;
     }
   }
+  // slicing share of the gram stage (int8 block Grams; one mid event per timed sweep)
+  c->slice_ms = 0.0;
+  if (c->slice_events.size() == k)
+    for (size_t i = 0; i < k; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, c->events[5 * i + 1], c->slice_events[i]);
+      c->slice_ms += ms;
+    }
+  for (auto e : c->slice_events) cudaEventDestroy(e);
+  c->slice_events.clear();
   for (auto e : c->events) cudaEventDestroy(e);
   c->events.clear();
   if (sweeps) *sweeps = (int32_t)k;
+  return RAC_OK;
+}
+
+extern "C" int rac_en_timing_slicing(rac_en_ctx* c, double* slice_ms) {
+  using namespace rac;
+  clear_error();
+  if (!c || !slice_ms) return set_error(RAC_ERR_ARG, "rac_en_timing_slicing: bad arguments");
+  *slice_ms = c->slice_ms;
   return RAC_OK;
 }
 

@@ -612,7 +612,7 @@ int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, 
 // feature lists idx[b*s ..] (-1 = padding), ex_all = per-feature exponents of Xc
 int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32_t* idx, int s, int p,
                           const int* ex_all, const int* flags, double* out, void* ws, size_t ws_bytes,
-                          cudaStream_t st) {
+                          cudaStream_t st, cudaEvent_t after_slicing) {
   if (!ws || ws_bytes < gram_i8_blocks_ws_bytes(len, s, p))
     return set_error(RAC_ERR_ARG, "gram_i8 blocks: workspace too small");
   const int nstg = (int)((len + I8_KS - 1) / I8_KS);
@@ -625,6 +625,7 @@ int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32
   note_launch();
   i8_slice_kernel<<<dim3((unsigned)ngrp, (unsigned)((nstg + 7) / 8), (unsigned)p), 256, 0, st>>>(
       Xc, ld, len, s, ex_all, sl, slice_bytes, ngrp, nstg, idx, ex_blk, flags, force8_env());
+  if (after_slicing) cudaEventRecord(after_slicing, st);   // stage timing: slicing | GEMM
   set_i8_attributes();
   I8Args a{};
   a.sl = sl;

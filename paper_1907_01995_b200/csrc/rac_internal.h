@@ -72,7 +72,7 @@ size_t gram_i8_blocks_ws_bytes(int64_t len, int s, int p);
 int launch_i8_colexp(const double* Xc, int64_t ld, int64_t len, int n, int* ex, cudaStream_t st, int* flags);
 int launch_gram_i8_blocks(const double* Xc, int64_t ld, int64_t len, const int32_t* idx, int s, int p,
                           const int* ex_all, const int* flags, double* out, void* ws, size_t ws_bytes,
-                          cudaStream_t st);
+                          cudaStream_t st, cudaEvent_t after_slicing = nullptr);
 int launch_gram_reduce_sym(const double* ws, int64_t n, int splits, double div, double* G, cudaStream_t st);
 // K3: assemble block systems, Cholesky, explicit inverse.
 struct SysArgs {

@@ -51,6 +51,18 @@ struct EnChainArgs {
   double *hist_p, *hist_d;
   long long* trace;     // optional: %globaltimer at every phase boundary (CTA 0)
   int rw;               // RC == 0 (one-tile resident row phase): rows per CTA
+  // RC == 0: per-block hand-offs (partials -> S1, rhs -> S2, delta -> row phase) as tagged 64-bit
+  // word pairs (rac_common.cuh ll_store) that the reader spins on, instead of a grid barrier.
+  // Layout: partials [s][P][2], rhs [s][2], delta [s][2]; tag of block step t = tag0 + t + 1
+  // (unique per launch and step).  Each buffer is rewritten for step t + 1 only after every reader
+  // of step t is done: a writer of step t + 1 data depends, through the chain itself, on all of
+  // step t's readers' outputs.  Default (ll_mask = 1): only the partials, where every word has ONE
+  // reader (measured on config 5: chain 3.94 -> 3.65 ms per sweep); the two broadcast hand-offs keep
+  // their grid barrier — 16 000 - 38 000 threads polling the same 8 KB delay its writers (rhs
+  // tagged: 4.02 ms; delta tagged: 3.64 ms, no gain over the partials alone).
+  unsigned long long* ll;
+  unsigned tag0;
+  int ll_mask;   // 1: partials -> S1, 2: rhs -> S2, 4: delta -> row phase (the others keep their grid barrier)
 };
 
 
@@ -94,17 +106,25 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
   int tp = 0;
   if (tr) a.trace[tp++] = gtimer();
   int bnext = a.order ? a.order[0] : 0;
+  const bool LL = (RC == 0) && a.ll != nullptr;
+  const bool LLP = LL && (a.ll_mask & 1), LLR = LL && (a.ll_mask & 2), LLD = LL && (a.ll_mask & 4);
+  unsigned long long* const llp = LLP ? a.ll : nullptr;
+  unsigned long long* const ll_rhs = LLR ? a.ll + 2 * (size_t)s * P : nullptr;
+  unsigned long long* const ll_del = LLD ? a.ll + 2 * (size_t)s * P + 2 * (size_t)s : nullptr;
+  const bool s_cta = blockIdx.x * (ENT / 32) < s;   // this CTA has S1 / S2 rows
   if constexpr (RC == 0) {
     for (int i = threadIdx.x; i < nr1; i += ENT) w1.sR[i] = a.r[r0 + i];
     __syncthreads();
-    row_phase_1t(a.Xc, a.ld, r0, nr1, a.idx, s, -1, bnext, a.delta, a.beta, a.partial, w1, tfn);
+    row_phase_1t(a.Xc, a.ld, r0, nr1, a.idx, s, -1, bnext, a.delta, a.beta, a.partial, w1, tfn, nullptr, false,
+                 llp, ll_del, 0u, a.tag0 + 1u);
   } else {
     row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, -1, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
   }
   if (tr) a.trace[tp++] = gtimer();
   for (int t = 0; t < a.p; ++t) {
     const int b = bnext;
-    grid_barrier(a.bar, target, P);
+    const unsigned tg = a.tag0 + (unsigned)t + 1u;
+    if (!LLP) grid_barrier(a.bar, target, P);
     if (tr) a.trace[tp++] = gtimer();
     // this CTA's S2 rows of inv_b -> L2 while S1 runs (one 128-byte line per thread)
     {
@@ -129,9 +149,30 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
         zg = ldcg(a.z + g);
       }
       double acc = 0.0;
-      // RC == 0: partials are [j][cta] (row_phase_1t), else [cta][j]
-      for (int q = lane; q < P; q += 32)
-        acc += ldcg(a.partial + (RC == 0 ? (int64_t)j * P + q : (int64_t)q * s + j));
+      if (LLP) {
+        // the column's P tagged partials: all loads in flight, then re-poll the late ones; summed
+        // in the same order as the plain path
+        const unsigned long long* pj = llp + 2 * (size_t)j * P;
+        constexpr int QM = 8;   // P <= 256 CTAs
+        unsigned long long w0[QM], w1[QM];
+#pragma unroll
+        for (int u = 0; u < QM; ++u) {
+          const int q = lane + 32 * u;
+          if (q < P) ll_load2(pj + 2 * q, w0[u], w1[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < QM; ++u) {
+          const int q = lane + 32 * u;
+          if (q < P) {
+            while (!(ll_ok(w0[u], tg) && ll_ok(w1[u], tg))) ll_load2(pj + 2 * q, w0[u], w1[u]);
+            acc += ll_value((unsigned)w0[u], (unsigned)w1[u]);
+          }
+        }
+      } else {
+        // RC == 0: partials are [j][cta] (row_phase_1t), else [cta][j]
+        for (int q = lane; q < P; q += 32)
+          acc += ldcg(a.partial + (RC == 0 ? (int64_t)j * P + q : (int64_t)q * s + j));
+      }
       acc = warp_sum(acc);
       if (lane == 0) {
         double rhs = 0.0;
@@ -139,11 +180,20 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
           double cross = acc / m;
           rhs = -(sub(sub(add(cg, cross), xg), mul(gamma, zg)));
         }
-        a.rhs[j] = rhs;
+        if (LLR) ll_store(ll_rhs + 2 * j, rhs, tg);
+        else a.rhs[j] = rhs;
       }
     }
     if (tr) a.trace[tp++] = gtimer();
-    grid_barrier(a.bar, target, P);
+    if (!LLR) grid_barrier(a.bar, target, P);
+    // tagged rhs: the CTAs with S2 rows stage it in shared memory once (sDel is free between
+    // the row phases)
+    const double* rhs_src = a.rhs;
+    if (LLR && s_cta) {
+      ll_poll4(ll_rhs, threadIdx.x, ENT, s, tg, w1.sDel);   // s <= EN_QMAX * ENT
+      __syncthreads();
+      rhs_src = w1.sDel;
+    }
     if (tr) a.trace[tp++] = gtimer();
     // ---- S2: beta_b = inv_b rhs, fused prox/dual/residual per coordinate
     const double* Ib = a.inv + (int64_t)b * s * s;
@@ -158,12 +208,16 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
         x0 = ldcg(a.xi + g);
       }
       double acc = 0.0;
-      for (int j = lane; j < s; j += 32) acc += row[j] * ldcg(a.rhs + j);
+      if (LLR)
+        for (int j = lane; j < s; j += 32) acc += row[j] * rhs_src[j];
+      else
+        for (int j = lane; j < s; j += 32) acc += row[j] * ldcg(a.rhs + j);
       acc = warp_sum(acc);
       if (lane == 0) {
         if (g >= 0) {
           const double bn = acc;
-          a.delta[i] = bn - bo;
+          if (LLD) ll_store(ll_del + 2 * i, bn - bo, tg);
+          else a.delta[i] = bn - bo;
           a.beta[g] = bn;
           const double av = sub(x0, mul(gamma, bn));
           const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
@@ -172,7 +226,8 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
           my_sum += fabs(sub(bn, zn));
           my_max = fmax(my_max, fabs(sub(zn, zo)));
         } else {
-          a.delta[i] = 0.0;
+          if (LLD) ll_store(ll_del + 2 * i, 0.0, tg);
+          else a.delta[i] = 0.0;
         }
       }
     }
@@ -181,12 +236,13 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
     if constexpr (RC == 0)
       if (t + 1 < a.p) row1t_gather_beta(s, a.beta, w1);
     if (tr) a.trace[tp++] = gtimer();
-    grid_barrier(a.bar, target, P);
+    if (!LLD) grid_barrier(a.bar, target, P);
+    else if (LLR && s_cta) __syncthreads();   // S2 read the staged rhs from sDel; the row phase refills it with delta
     if (tr) a.trace[tp++] = gtimer();
     bnext = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
     if constexpr (RC == 0)
       row_phase_1t(a.Xc, a.ld, r0, nr1, a.idx, s, b, bnext, a.delta, a.beta, a.partial, w1, tfn,
-                   tr ? a.trace + 16 + 16 * (size_t)a.p + s + 4 * (size_t)t : nullptr, true);
+                   tr ? a.trace + 16 + 16 * (size_t)a.p + s + 4 * (size_t)t : nullptr, true, llp, ll_del, tg, tg + 1u);
     else
       row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
     if (tr) a.trace[tp++] = gtimer();
@@ -308,6 +364,9 @@ struct rac_en_ctx {
   bool have_data = false, have_partition = false;
   int sweeps = 0;        // sweeps enqueued so far (history index; reset by rac_en_reset)
   unsigned msg_tag = 0;  // lookahead-chain launches so far: tag of the tagged messages (never reset)
+  unsigned long long* ll = nullptr;   // streaming one-tile chain: tagged hand-off words (EnChainArgs::ll)
+  unsigned ll_epoch = 0;              // chain launches with tagged hand-offs so far (tag0 = epoch (p + 1))
+  int ll_mask = 1;                    // which hand-offs are tagged (RAC_EN_LL; EnChainArgs::ll_mask)
   int hist_cap = 0;
   // device buffers
   double *Xc = nullptr, *y = nullptr, *c = nullptr, *beta = nullptr, *z = nullptr, *xi = nullptr,
@@ -784,6 +843,17 @@ int en_chain(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
   a.hist_d = c->hist_d;
   a.trace = c->trace;
   a.rw = c->rw;
+  if (c->ll && c->RC == 0 && c->variant != 1) {
+    if ((unsigned long long)(c->ll_epoch + 2u) * (unsigned)(c->p + 1) >= 0xfffffff0ull) {
+      // tag space used up (2^32 / (p + 1) launches): clear the words and start over
+      cudaMemsetAsync(c->ll, 0, 2 * ((size_t)c->s * c->P + 2 * (size_t)c->s) * sizeof(unsigned long long), st);
+      c->ll_epoch = 0;
+    }
+    ++c->ll_epoch;
+    a.ll = c->ll;
+    a.tag0 = c->ll_epoch * (unsigned)(c->p + 1);
+    a.ll_mask = c->ll_mask;
+  }
   void* args[] = {&a};
   if (c->variant == 1) {
     int nch = c->nch;
@@ -974,6 +1044,16 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
       (rc = dalloc(c, &c->wmax, GW)) || (rc = dalloc(c, &c->bar, 1)) || (rc = dalloc(c, &c->ctrl, 4))) {
     rac_en_destroy(c);
     return rc;
+  }
+  if (c->RC == 0 && c->P <= 256) {
+    // RAC_EN_LL: bit mask of the tagged hand-offs (1 partials, 2 rhs, 4 delta); 0: three grid barriers per block
+    const char* e = getenv("RAC_EN_LL");
+    if (e) c->ll_mask = atoi(e) & 7;
+    if (c->ll_mask != 0 &&
+        (rc = dalloc(c, &c->ll, 2 * ((size_t)s * c->P + 2 * (size_t)s)))) {
+      rac_en_destroy(c);
+      return rc;
+    }
   }
   {
     // int8 tensor-core block Grams when a sweep's 128 x 128 tiles fill the SMs several times

@@ -56,13 +56,21 @@ struct EnChainArgs {
   // Layout: partials [s][P][2], rhs [s][2], delta [s][2]; tag of block step t = tag0 + t + 1
   // (unique per launch and step).  Each buffer is rewritten for step t + 1 only after every reader
   // of step t is done: a writer of step t + 1 data depends, through the chain itself, on all of
-  // step t's readers' outputs.  Default (ll_mask = 1): only the partials, where every word has ONE
-  // reader (measured on config 5: chain 3.94 -> 3.65 ms per sweep); the two broadcast hand-offs keep
-  // their grid barrier — 16 000 - 38 000 threads polling the same 8 KB delay its writers (rhs
-  // tagged: 4.02 ms; delta tagged: 3.64 ms, no gain over the partials alone).
+  // step t's readers' outputs.  Default (ll_mask = 1 + the fused S phase below): the partials, where
+  // every word has ONE reader (measured on config 5: chain 3.94 -> 3.65 ms per sweep, 3.54 with the
+  // fused S phase).  A tagged rhs broadcast (bit 2: 16 000 threads polling the same 8 KB delay its
+  // writers) is slower, 4.02 ms; delta as one private tagged copy per consumer CTA (bit 4) is
+  // within noise of the barrier (3.49 vs 3.54 ms) and stays off.
   unsigned long long* ll;
   unsigned tag0;
   int ll_mask;   // 1: partials -> S1, 2: rhs -> S2, 4: delta -> row phase (the others keep their grid barrier)
+  // fused S phase (needs the tagged partials; one pass: every column has its own warp, s <= 512):
+  // warp j scales row j of the symmetric inverse by rhs_j, the CTA sums its 8 scaled rows in shared
+  // memory (fuse_off: byte offset of the [8][s] buffer) and publishes them as tagged words
+  // [s][ceil(s / 8)][2] (behind the words above); warp i then sums row i's CTA partials.  Every
+  // tagged word has one reader, and the rhs broadcast with its grid barrier is gone.
+  int fuse;
+  unsigned fuse_off;
 };
 
 
@@ -110,13 +118,21 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
   const bool LLP = LL && (a.ll_mask & 1), LLR = LL && (a.ll_mask & 2), LLD = LL && (a.ll_mask & 4);
   unsigned long long* const llp = LLP ? a.ll : nullptr;
   unsigned long long* const ll_rhs = LLR ? a.ll + 2 * (size_t)s * P : nullptr;
-  unsigned long long* const ll_del = LLD ? a.ll + 2 * (size_t)s * P + 2 * (size_t)s : nullptr;
+  // delta: one private copy per consumer CTA ([P][s][2] behind the S-phase words), so that every
+  // tagged word has one reader
+  const int NSCc = (s + ENT / 32 - 1) / (ENT / 32);
+  unsigned long long* const ll_del = LLD ? a.ll + 2 * ((size_t)s * P + 2 * (size_t)s + (size_t)s * NSCc) : nullptr;
+  auto publish_delta = [&](int i, double dv, unsigned tag) {   // whole warp: delta_i into every CTA's copy
+    for (int q = lane; q < P; q += 32) ll_store(ll_del + 2 * ((size_t)q * s + i), dv, tag);
+  };
+  const unsigned long long* const my_del = LLD ? ll_del + 2 * (size_t)blockIdx.x * s : nullptr;
   const bool s_cta = blockIdx.x * (ENT / 32) < s;   // this CTA has S1 / S2 rows
+  const bool FUSE = LLP && a.fuse && !LLR;
   if constexpr (RC == 0) {
     for (int i = threadIdx.x; i < nr1; i += ENT) w1.sR[i] = a.r[r0 + i];
     __syncthreads();
     row_phase_1t(a.Xc, a.ld, r0, nr1, a.idx, s, -1, bnext, a.delta, a.beta, a.partial, w1, tfn, nullptr, false,
-                 llp, ll_del, 0u, a.tag0 + 1u);
+                 llp, my_del, 0u, a.tag0 + 1u);
   } else {
     row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, -1, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
   }
@@ -137,6 +153,112 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
     }
     if constexpr (RC == 0)
       if (t + 1 < a.p) row1t_gather_idx(a.idx, s, a.order ? a.order[t + 1] : t + 1, w1);
+    if (FUSE) {
+      if (s_cta) {
+        const int NSC = (s + ENT / 32 - 1) / (ENT / 32);
+        unsigned long long* const ypart = a.ll + 2 * ((size_t)s * P + 2 * (size_t)s);
+        const double* Ibf = a.inv + (int64_t)b * s * s;
+        const int j = gw;
+        const bool mine = j < s;
+        const int g = mine ? a.idx[(int64_t)b * s + j] : -1;
+        double cg = 0.0, xg = 0.0, zg = 0.0, bo = 0.0;
+        if (g >= 0) {
+          cg = a.c[g];
+          xg = ldcg(a.xi + g);
+          zg = ldcg(a.z + g);
+          bo = ldcg(a.beta + g);
+        }
+        // row j of the symmetric inverse (= its column j), in flight behind the partials' poll
+        constexpr int KM = 16;   // s <= 512
+        double rowv[KM];
+#pragma unroll
+        for (int k = 0; k < KM; ++k) {
+          const int i = lane + 32 * k;
+          rowv[k] = (mine && i < s) ? Ibf[(int64_t)j * s + i] : 0.0;
+        }
+        double acc = 0.0;
+        if (mine) {
+          const unsigned long long* pj = llp + 2 * (size_t)j * P;
+          constexpr int QM = 8;   // P <= 256 CTAs
+          unsigned long long w0[QM], w1[QM];
+#pragma unroll
+          for (int u = 0; u < QM; ++u) {
+            const int q = lane + 32 * u;
+            if (q < P) ll_load2(pj + 2 * q, w0[u], w1[u]);
+          }
+#pragma unroll
+          for (int u = 0; u < QM; ++u) {
+            const int q = lane + 32 * u;
+            if (q < P) {
+              while (!(ll_ok(w0[u], tg) && ll_ok(w1[u], tg))) ll_load2(pj + 2 * q, w0[u], w1[u]);
+              acc += ll_value((unsigned)w0[u], (unsigned)w1[u]);
+            }
+          }
+        }
+        acc = warp_sum(acc);
+        double rhs = 0.0;
+        if (g >= 0) {
+          double cross = acc / m;
+          rhs = -(sub(sub(add(cg, cross), xg), mul(gamma, zg)));
+        }
+        double* sV = reinterpret_cast<double*>(reinterpret_cast<char*>(esm) + a.fuse_off);
+#pragma unroll
+        for (int k = 0; k < KM; ++k) {
+          const int i = lane + 32 * k;
+          if (i < s) sV[warp * s + i] = rowv[k] * rhs;
+        }
+        if (tr) a.trace[tp++] = gtimer();
+        __syncthreads();
+        for (int i = threadIdx.x; i < s; i += ENT) {
+          double y = 0.0;
+#pragma unroll
+          for (int w8 = 0; w8 < ENT / 32; ++w8) y += sV[w8 * s + i];
+          ll_store(ypart + 2 * ((size_t)i * NSC + blockIdx.x), y, tg);
+        }
+        if (tr) a.trace[tp++] = gtimer();
+        if (mine) {
+          const unsigned long long* yi = ypart + 2 * (size_t)j * NSC;
+          unsigned long long w0[2], w1[2];   // NSC <= 64
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int q = lane + 32 * u;
+            if (q < NSC) ll_load2(yi + 2 * q, w0[u], w1[u]);
+          }
+          double bsum = 0.0;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int q = lane + 32 * u;
+            if (q < NSC) {
+              while (!(ll_ok(w0[u], tg) && ll_ok(w1[u], tg))) ll_load2(yi + 2 * q, w0[u], w1[u]);
+              bsum += ll_value((unsigned)w0[u], (unsigned)w1[u]);
+            }
+          }
+          bsum = warp_sum(bsum);
+          if (lane == 0) {
+            if (g >= 0) {
+              const double bn = bsum;
+              if (!LLD) a.delta[j] = bn - bo;
+              a.beta[g] = bn;
+              const double av = sub(xg, mul(gamma, bn));
+              const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
+              a.z[g] = zn;
+              a.xi[g] = sub(xg, mul(gamma, sub(bn, zn)));
+              my_sum += fabs(sub(bn, zn));
+              my_max = fmax(my_max, fabs(sub(zn, zg)));
+            } else {
+              if (!LLD) a.delta[j] = 0.0;
+            }
+          }
+          if (LLD) publish_delta(j, (g >= 0) ? bsum - bo : 0.0, tg);
+        }
+        __syncthreads();   // sV is rewritten by the next block's S phase
+      } else if (tr) {
+        tp += 2;
+      }
+      if constexpr (RC == 0)
+        if (t + 1 < a.p) row1t_gather_beta(s, a.beta, w1);
+      if (tr) a.trace[tp++] = gtimer();
+    } else {
     // ---- S1: reduce the per-CTA partials -> block right-hand side
     for (int j = gw; j < s; j += GW) {
       // the coordinate's scalars (final since the previous sweep) are requested before the
@@ -216,8 +338,7 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
       if (lane == 0) {
         if (g >= 0) {
           const double bn = acc;
-          if (LLD) ll_store(ll_del + 2 * i, bn - bo, tg);
-          else a.delta[i] = bn - bo;
+          if (!LLD) a.delta[i] = bn - bo;
           a.beta[g] = bn;
           const double av = sub(x0, mul(gamma, bn));
           const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
@@ -226,23 +347,24 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
           my_sum += fabs(sub(bn, zn));
           my_max = fmax(my_max, fabs(sub(zn, zo)));
         } else {
-          if (LLD) ll_store(ll_del + 2 * i, 0.0, tg);
-          else a.delta[i] = 0.0;
+          if (!LLD) a.delta[i] = 0.0;
         }
       }
+      if (LLD) publish_delta(i, (g >= 0) ? acc - bo : 0.0, tg);
     }
     // the next row phase's block: its beta (final until its own solve) gathered into shared
     // memory behind this CTA's S2 work, landing during the barrier (indices issued before S1)
     if constexpr (RC == 0)
       if (t + 1 < a.p) row1t_gather_beta(s, a.beta, w1);
     if (tr) a.trace[tp++] = gtimer();
+    }   // !FUSE
     if (!LLD) grid_barrier(a.bar, target, P);
     else if (LLR && s_cta) __syncthreads();   // S2 read the staged rhs from sDel; the row phase refills it with delta
     if (tr) a.trace[tp++] = gtimer();
     bnext = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
     if constexpr (RC == 0)
       row_phase_1t(a.Xc, a.ld, r0, nr1, a.idx, s, b, bnext, a.delta, a.beta, a.partial, w1, tfn,
-                   tr ? a.trace + 16 + 16 * (size_t)a.p + s + 4 * (size_t)t : nullptr, true, llp, ll_del, tg, tg + 1u);
+                   tr ? a.trace + 16 + 16 * (size_t)a.p + s + 4 * (size_t)t : nullptr, true, llp, my_del, tg, tg + 1u);
     else
       row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
     if (tr) a.trace[tp++] = gtimer();
@@ -367,6 +489,7 @@ struct rac_en_ctx {
   unsigned long long* ll = nullptr;   // streaming one-tile chain: tagged hand-off words (EnChainArgs::ll)
   unsigned ll_epoch = 0;              // chain launches with tagged hand-offs so far (tag0 = epoch (p + 1))
   int ll_mask = 1;                    // which hand-offs are tagged (RAC_EN_LL; EnChainArgs::ll_mask)
+  bool fuse = false;                  // fused S phase (EnChainArgs::fuse; RAC_EN_LL bit 8, on by default)
   int hist_cap = 0;
   // device buffers
   double *Xc = nullptr, *y = nullptr, *c = nullptr, *beta = nullptr, *z = nullptr, *xi = nullptr,
@@ -846,13 +969,18 @@ int en_chain(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
   if (c->ll && c->RC == 0 && c->variant != 1) {
     if ((unsigned long long)(c->ll_epoch + 2u) * (unsigned)(c->p + 1) >= 0xfffffff0ull) {
       // tag space used up (2^32 / (p + 1) launches): clear the words and start over
-      cudaMemsetAsync(c->ll, 0, 2 * ((size_t)c->s * c->P + 2 * (size_t)c->s) * sizeof(unsigned long long), st);
+      const size_t nsc = (size_t)(c->s + ENT / 32 - 1) / (ENT / 32);
+      cudaMemsetAsync(c->ll, 0,
+                      2 * ((size_t)c->s * c->P + 2 * (size_t)c->s + c->s * nsc + (size_t)c->P * c->s) *
+                          sizeof(unsigned long long), st);
       c->ll_epoch = 0;
     }
     ++c->ll_epoch;
     a.ll = c->ll;
     a.tag0 = c->ll_epoch * (unsigned)(c->p + 1);
     a.ll_mask = c->ll_mask;
+    a.fuse = c->fuse ? 1 : 0;
+    a.fuse_off = (unsigned)((row1t_smem_bytes(c->s, c->rw) + 15) / 16 * 16);
   }
   void* args[] = {&a};
   if (c->variant == 1) {
@@ -882,6 +1010,7 @@ int en_chain(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
                       "en_chain_res (cluster cooperative launch)");
   }
   size_t smem = c->RC == 0 ? row1t_smem_bytes(c->s, c->rw) : en_chain_smem(c->s, c->RC);
+  if (c->RC == 0 && c->fuse) smem = (smem + 15) / 16 * 16 + (size_t)(ENT / 32) * c->s * sizeof(double);
   cudaError_t e;
   {
     // the function attribute is process-wide: another context's plan may have lowered it
@@ -1048,12 +1177,23 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
   if (c->RC == 0 && c->P <= 256) {
     // RAC_EN_LL: bit mask of the tagged hand-offs (1 partials, 2 rhs, 4 delta); 0: three grid barriers per block
     const char* e = getenv("RAC_EN_LL");
-    if (e) c->ll_mask = atoi(e) & 7;
+    int want_fuse = 1;
+    if (e) {
+      c->ll_mask = atoi(e) & 7;
+      want_fuse = (atoi(e) & 8) ? 1 : 0;
+    }
+    const int nsc = (s + ENT / 32 - 1) / (ENT / 32);
     if (c->ll_mask != 0 &&
-        (rc = dalloc(c, &c->ll, 2 * ((size_t)s * c->P + 2 * (size_t)s)))) {
+        (rc = dalloc(c, &c->ll, 2 * ((size_t)s * c->P + 2 * (size_t)s + (size_t)s * nsc + (size_t)c->P * s)))) {
       rac_en_destroy(c);
       return rc;
     }
+    const size_t smf = (row1t_smem_bytes(s, c->rw) + 15) / 16 * 16 + (size_t)(ENT / 32) * s * sizeof(double);
+    if (want_fuse && (c->ll_mask & 1) && !(c->ll_mask & 2) && s <= 512 && c->P * (ENT / 32) >= s && smf <= 200 * 1024 &&
+        cudaFuncSetAttribute((void*)en_chain_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf) ==
+            cudaSuccess)
+      c->fuse = true;
+    cudaGetLastError();
   }
   {
     // int8 tensor-core block Grams when a sweep's 128 x 128 tiles fill the SMs several times

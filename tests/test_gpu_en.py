@@ -392,6 +392,36 @@ def test_streaming_chain_one_tile_vs_oracle(lib, monkeypatch, one_tile):
                 assert rel(a_, b_) <= ITER_TOL, (m, n, s, k)
 
 
+@pytest.mark.parametrize("handoffs", ["0", "1", "3", "5", "7", "9", "13"])
+def test_streaming_chain_tagged_handoffs_vs_oracle(lib, monkeypatch, handoffs):
+    """The one-tile streaming chain's per-block hand-offs (partials -> S1, rhs -> S2, delta -> row
+    phase) behind grid barriers (RAC_EN_LL=0) or as tagged words the reader spins on (bits 1 / 2 /
+    4), and the fused S phase (bit 8; default 9): every combination gives the oracle's per-sweep
+    iterates, also when the pooled context is used again (the tags of a new launch must not match
+    the words a previous fit left behind) and with a short last block."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import elastic_net as en
+    monkeypatch.setenv("RAC_EN_LL", handoffs)
+    rng = np.random.default_rng(47)
+    for (m, n, s, alpha) in [(700, 1000, 300, 0.9), (150, 650, 320, 1.0)]:
+        for rep in range(2):
+            X = rng.standard_normal((m, n))
+            y = X[:, :5] @ rng.standard_normal(5) + 0.05 * rng.standard_normal(m)
+            kw = dict(lam=0.05, alpha=alpha, gamma=1.0, block_size=s, iters=5, seed=3 + rep)
+            caps = {}
+            ro.en_fit(X, y, mode="rac", **kw,
+                      on_sweep=lambda k, bl, b, z, xi: caps.__setitem__(k, (b.copy(), z.copy(), xi.copy())))
+            got = {}
+            en.fit(X, y, en.ElasticNetSpec(**kw), gram_mode="blocks",
+                   sweep_hook=lambda k, b, z, xi: got.__setitem__(k, (b, z, xi)))
+            for k in caps:
+                for a_, b_ in zip(got[k], caps[k]):
+                    assert rel(a_, b_) <= ITER_TOL, (handoffs, m, n, s, rep, k)
+            # without the per-sweep hook: several sweeps per run call, same final iterate
+            fin = en.fit(X, y, en.ElasticNetSpec(**kw), gram_mode="blocks")
+            assert rel(fin.beta, caps[max(caps)][0]) <= ITER_TOL
+
+
 @pytest.mark.parametrize("gram", ["covariance", "blocks"])
 def test_fit_enqueue_ahead_stops_where_the_synchronous_loop_does(lib, gram):
     """fit() with a tolerance enqueues batch k+1 before polling batch k (rac_en_poll); the

@@ -60,6 +60,14 @@ struct QpChainArgs {
   // row (t - t0) * s + i for member i of block t (formed on the fly, svm.py:121-143), instead
   // of the full N x N matrix indexed by sample
   int t0, t1, strips;
+  // One grid barrier per block instead of two (resident strips staged in shared memory, no or few
+  // constraint rows): the workers publish hx at the NEXT block's coordinates as tagged word pairs
+  // right where they apply delta (each coordinate has one owner CTA and one reader, CTA 0), and the
+  // constraint-row owner publishes the block's partial the same way; CTA 0 spins on those words
+  // instead of waiting for the whole grid.  llq: hx words [s][2], partial words [s][2]; tag of
+  // block step t = tagq0 + t + 1.  delta is double-buffered by step parity.
+  unsigned long long* llq;
+  unsigned tagq0;
 };
 
 // H row of member i (global index g) of the block visited at step t
@@ -324,7 +332,8 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
   unsigned mpar = 0u;
   const bool bulkML = (w.sM != nullptr) && ((s * s) % 2 == 0);
   if (blockIdx.x == 0 && w.sM && tid == 0) {
-    mbar_init(w.bar, 1);
+    mbar_init(w.bar, 1);       // N_b = M_b^{-1} (needed first: x0 = N_b r)
+    mbar_init(w.bar + 1, 1);   // M_b (needed by the box solve; its copy runs under x0)
     mbar_fence_init();
   }
   auto prefetch_ML = [&](int b) {
@@ -336,12 +345,12 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
       if (tid == 0) {
         fence_proxy_async();
         const unsigned bytes = (unsigned)(s * s * sizeof(double));
-        mbar_arrive_expect_tx(w.bar, 2 * bytes);
-        for (unsigned off = 0; off < bytes; off += 32768u) {
-          const unsigned len = min(32768u, bytes - off);
-          bulk_g2s(w.sM + off / 8, Mg + off / 8, len, w.bar);
-          bulk_g2s(w.sN + off / 8, Ng + off / 8, len, w.bar);
-        }
+        mbar_arrive_expect_tx(w.bar, bytes);
+        for (unsigned off = 0; off < bytes; off += 32768u)
+          bulk_g2s(w.sN + off / 8, Ng + off / 8, min(32768u, bytes - off), w.bar);
+        mbar_arrive_expect_tx(w.bar + 1, bytes);
+        for (unsigned off = 0; off < bytes; off += 32768u)
+          bulk_g2s(w.sM + off / 8, Mg + off / 8, min(32768u, bytes - off), w.bar + 1);
       }
     } else {
       for (int e = tid; e < s * s; e += QPT) {
@@ -351,14 +360,17 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
       cp_async_commit();
     }
   };
-  auto wait_ML = [&]() {
-    if (bulkML) {
-      mbar_wait(w.bar, mpar);
-      mpar ^= 1u;
-    } else if (w.sM) {
-      cp_async_wait<0>();
-    }
+  auto wait_N = [&]() {   // N_b resident (also M_b when the copies are not bulk copies)
+    if (bulkML) mbar_spin(w.bar, mpar);   // on the critical path: poll, no suspend / wake latency
+    else if (w.sM) cp_async_wait<0>();
     __syncthreads();
+  };
+  auto wait_M = [&]() {
+    if (bulkML) {
+      mbar_spin(w.bar + 1, mpar);
+      mpar ^= 1u;
+      __syncthreads();
+    }
   };
   // hbx = H_bb x_b for block b (rows spread over all warps of the grid)
   // Strip staging: while CTA 0 solves block b, every other CTA bulk-copies
@@ -374,6 +386,33 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
                           (a.n % 2 == 0);
   const int64_t sc0 = ((int)blockIdx.x < sfirst) ? 0 : min64(a.n, (int64_t)(blockIdx.x - sfirst) * sper2);
   const int64_t sc1 = ((int)blockIdx.x < sfirst) ? 0 : min64(a.n, sc0 + sper2);
+  const bool lla = a.llq != nullptr && strip_smem && ((few_rows && strip_smem) || !has_a) && P > sfirst;
+  unsigned long long* const hxLL = a.llq;
+  unsigned long long* const paLL = a.llq ? a.llq + 2 * (size_t)s : nullptr;
+  // workers: position of each owned column in the next block (-1: not a member); w.red is free
+  // on the strip CTAs when the strips are staged in shared memory
+  int* posmap = reinterpret_cast<int*>(w.red);
+  // a strip CTA owns its columns of hx for the whole launch: kept in shared memory (second half of
+  // w.red), written through to global memory, so the G phase has no load of hx on its path
+  double* sHx = w.red + (QPT / 32) * QCOLS / 2;
+  const bool hx_cached = strip_smem && blockIdx.x >= (unsigned)sfirst && sc1 > sc0 &&
+                         (sc1 - sc0) <= (QPT / 32) * QCOLS / 2;
+  if (hx_cached)
+    for (int jj = tid; jj < (int)(sc1 - sc0); jj += QPT) sHx[jj] = ldcg(a.hx + sc0 + jj);
+  auto build_posmap = [&](int bn) {
+    if (blockIdx.x < (unsigned)sfirst || sc1 <= sc0) return;
+    const int W = (int)(sc1 - sc0);
+    for (int jj = tid; jj < W; jj += QPT) posmap[jj] = -1;
+    __syncthreads();
+    if (bn >= 0) {
+      const int32_t* bi = a.idx + (int64_t)bn * s;
+      for (int i = tid; i < s; i += QPT) {
+        const int g = bi[i];
+        if (g >= sc0 && g < sc1) posmap[g - sc0] = i;
+      }
+    }
+    __syncthreads();
+  };
   unsigned spar = 0u;
   if (strip_smem && blockIdx.x != 0 && tid == 0) {
     mbar_init(w.bar, 1);
@@ -402,7 +441,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
         for (int64_t jj = 0; jj < sc1 - sc0; ++jj) w.sM[(size_t)i * sper2 + jj] = 0.0;   // padding row
     }
   };
-  auto strip_from_smem = [&]() {
+  auto strip_from_smem = [&](unsigned pub_tag) {   // pub_tag != 0: publish hx at the next block's coordinates
     if (blockIdx.x == 0 || sc1 <= sc0) return;
     mbar_wait(w.bar, spar);
     spar ^= 1u;
@@ -410,7 +449,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
     const int W = (int)(sc1 - sc0);
     for (int jj = tid; jj < W; jj += QPT) {
       // padding rows are zero-filled and their delta is 0: no branch; 4 partial sums
-      const double hx0 = ldcg(a.hx + sc0 + jj);
+      const double hx0 = hx_cached ? sHx[jj] : ldcg(a.hx + sc0 + jj);
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int i = 0;
       for (; i + 4 <= s; i += 4) {
@@ -420,7 +459,10 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
         a3 += w.sM[(size_t)(i + 3) * sper2 + jj] * w.sDel[i + 3];
       }
       for (; i < s; ++i) a0 += w.sM[(size_t)i * sper2 + jj] * w.sDel[i];
-      a.hx[sc0 + jj] = hx0 + ((a0 + a1) + (a2 + a3));
+      const double hnew = hx0 + ((a0 + a1) + (a2 + a3));
+      a.hx[sc0 + jj] = hnew;
+      if (hx_cached) sHx[jj] = hnew;
+      if (pub_tag && posmap[jj] >= 0) ll_store(hxLL + 2 * (size_t)posmap[jj], hnew, pub_tag);
     }
     __syncthreads();
   };
@@ -503,7 +545,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
     }
     block_rows_sum(un, mr, sUn[slot]);
   };
-  auto small_post = [&](int slot_b, int slot_bn, bool has_prev, bool has_next) {
+  auto small_post = [&](int slot_b, int slot_bn, bool has_prev, bool has_next, unsigned pub_tag) {
     if ((int)blockIdx.x != a_owner) return;
     const int mr = (int)a.m;
     if (has_prev) {
@@ -531,7 +573,8 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
       for (int j = tid; j < s; j += QPT) {
         double acc = 0.0;
         for (int r = 0; r < mr; ++r) acc += an[(size_t)r * s + j] * w.rp.sT[r];
-        a.partial[j] = acc;
+        if (pub_tag) ll_store(paLL + 2 * (size_t)j, acc, pub_tag);
+        else a.partial[j] = acc;
       }
     }
   };
@@ -565,7 +608,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
   if (small_a) {
     small_pre(bnext, s0);
     __syncthreads();
-    small_post(s0, s0, false, true);
+    small_post(s0, s0, false, true, 0u);
   }
   else if (has_a)
     row_phase<RC>(a.Ac, a.lda, a.m, a.nrc, a.idx, s, -1, bnext, a.delta, a.x, a.ax, a.partial, w.rp, tfn);
@@ -575,14 +618,16 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
   for (int t = a.t0; t < a.t1; ++t) {
     const int b = bnext;
     if (arr && tid == 0) arr[((size_t)t * P + blockIdx.x) * 2 + 1] = gtimer();
-    grid_barrier(a.bar, target, P);
+    const bool lla_t = lla && t > a.t0;   // this block's hx / partial arrive as tagged words: no barrier
+    const unsigned tagq = a.tagq0 + (unsigned)t + 1u;
+    if (!lla_t) grid_barrier(a.bar, target, P);
     if (tr) a.trace[10 * t + 0] = gtimer();
-    issue_strip(b, t);
     // While CTA 0 solves block t, the others prepare block t+1's terms that do not
     // depend on block t's solution: H_bb x_b (double-buffered by parity) and, on the
     // constraint-row owner, A_b x_b.
     {
       const int bn1 = (t + 1 < a.t1) ? (a.order ? a.order[t + 1] : t + 1) : -1;
+      if (lla && blockIdx.x != 0) build_posmap(bn1);   // for the G phase's publication of hx at block t+1
       if (bn1 >= 0 && blockIdx.x != 0) {
         compute_hbx(bn1, (t + 1) & 1);
         if (small_a) small_pre(bn1, (t + 1) & 1);
@@ -601,6 +646,10 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
         }
       }
     }
+    // the strip's 8 s n bytes are requested AFTER the latency-bound preparation above: without a
+    // grid barrier in front of this point they would otherwise start right behind the previous
+    // G phase and delay CTA 0's copy of M_b / N_b, which is on the critical path
+    issue_strip(b, t);
     // ------------------------------------------------------------ S (CTA 0)
     if (blockIdx.x == 0) {
       const int32_t* bidx = a.idx + (int64_t)b * s;
@@ -617,14 +666,30 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
         w.sIdx[i] = g;
         nval += (g >= 0);
         if (g >= 0) {
-          const double hxg = ldcg(a.hx + g);
+          // all of the block's loads in flight, then the spins on the tagged words
+          unsigned long long h0 = 0, h1 = 0, p0 = 0, p1 = 0;
+          if (lla_t) {
+            ll_load2(hxLL + 2 * (size_t)i, h0, h1);
+            if (has_a) ll_load2(paLL + 2 * (size_t)i, p0, p1);
+          }
+          const double hb = a.H ? (use_pf ? pf[5 * s + i] : ldcg(a.hbx + (int64_t)(t & 1) * s + i)) : 0.0;
+          double hxg;
+          if (lla_t) {   // published by the column's owner while it applied the previous delta
+            while (!(ll_ok(h0, tagq) && ll_ok(h1, tagq))) ll_load2(hxLL + 2 * (size_t)i, h0, h1);
+            hxg = ll_value((unsigned)h0, (unsigned)h1);
+          } else {
+            hxg = ldcg(a.hx + g);
+          }
           const double xg = use_pf ? pf[4 * s + i] : ldcg(a.x + g);
           const double cg_ = use_pf ? pf[s + i] : a.c[g];
           const double lo = use_pf ? pf[2 * s + i] : a.lo[g], hi = use_pf ? pf[3 * s + i] : a.hi[g];
-          const double hb = a.H ? (use_pf ? pf[5 * s + i] : ldcg(a.hbx + (int64_t)(t & 1) * s + i)) : 0.0;
           double pa = 0.0;
-          if (has_a)
+          if (has_a && lla_t) {   // small_a: the constraint-row owner's tagged partial
+            while (!(ll_ok(p0, tagq) && ll_ok(p1, tagq))) ll_load2(paLL + 2 * (size_t)i, p0, p1);
+            pa = ll_value((unsigned)p0, (unsigned)p1);
+          } else if (has_a) {
             for (int q = 0; q < Pa; ++q) pa += ldcg(a.partial + (int64_t)q * s + i);
+          }
           w.sxb[i] = xg;
           w.shx[i] = hxg;
           w.bw.lo[i] = lo;
@@ -639,13 +704,15 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
       __syncthreads();
       if (tr) a.trace[10 * t + 1] = gtimer();
       const int seff = w.bw.misc[0];
+      const double cond_b = use_pf ? pf_cond : ldcg(a.cond + b);
+
       // unconstrained solution (engine.py:201-203).  Well-conditioned blocks:
       // x = N_b r with the smem-resident inverse, reduced systems by Schur
       // complements of N_b.  Otherwise: cho_solve with the block's Cholesky
       // factor and direct reduced factorizations, exactly as the reference.
-      const bool schur = (w.sM != nullptr) && ((use_pf ? pf_cond : ldcg(a.cond + b)) < 1e6);
+      const bool schur = (w.sM != nullptr) && (cond_b < 1e6);
       const double* Mblk;
-      if (w.sM) wait_ML();   // M_b, N_b resident (ld = s)
+      if (w.sM) wait_N();   // N_b resident (ld = s); M_b may still be landing under x0
       if (tr) a.trace[10 * t + 2] = gtimer();
       if (schur) {
         cta_symv(w.sN, s, seff, w.bw.r, w.bw.x, w.bw.symv_scratch);   // M_b^{-1} is exactly symmetric (Y'Y)
@@ -664,6 +731,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
         w.bw.lcap = s * (s + 1);
         Mblk = w.sM ? w.sM : a.Mb + (int64_t)b * s * s;
       }
+      if (w.sM) wait_M();   // M_b resident
       __syncthreads();
       long long t_box = tr ? gtimer() : 0;
       if (tr) a.trace[10 * t + 3] = t_box;
@@ -689,7 +757,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
           d = w.bw.x[i] - w.sxb[i];
           a.x[w.sIdx[i]] = w.bw.x[i];
         }
-        a.delta[i] = d;
+        a.delta[(lla ? (size_t)(t & 1) * s : 0) + i] = d;
       }
       if (t + 1 < a.t1) prefetch_ML(a.order ? a.order[t + 1] : t + 1);
     }
@@ -701,7 +769,7 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
     // block data + the non-PD abort flag in one round trip
     for (int i = tid; i < s; i += QPT) {
       w.sIdx[i] = a.idx[(int64_t)b * s + i];
-      w.sDel[i] = ldcg(a.delta + i);
+      w.sDel[i] = ldcg(a.delta + (lla ? (size_t)(t & 1) * s : 0) + i);
     }
     if (tid == 0) bad = ldcg(a.ctrl + 0);
     __syncthreads();
@@ -712,10 +780,10 @@ __global__ void __launch_bounds__(QPT, 1) qp_chain_kernel(QpChainArgs a) {
       if (small_a) small_pre(bnext, (t + 1) & 1);
     }
     if (tr) a.trace[10 * t + 8] = gtimer();
-    if (strip_smem) strip_from_smem();
+    if (strip_smem) strip_from_smem((lla && bnext >= 0) ? tagq + 1u : 0u);
     else if (a.H) strip_update(a, t, w.sIdx, w.sDel, w.red, s);
     if (tr) a.trace[10 * t + 9] = gtimer();
-    if (small_a) small_post(t & 1, (t + 1) & 1, true, bnext >= 0);
+    if (small_a) small_post(t & 1, (t + 1) & 1, true, bnext >= 0, lla ? tagq + 1u : 0u);
     else if (has_a && (int)blockIdx.x < a.nrc)   // CTAs without row chunks have no partial to write
       row_phase<RC>(a.Ac, a.lda, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.x, a.ax, a.partial, w.rp, tfn);
     if (bnext >= 0) prefetch_next(bnext, (t + 1) & 1);
@@ -807,6 +875,8 @@ struct rac_qp_ctx {
   double *partial = nullptr, *delta = nullptr, *pmax = nullptr, *psum = nullptr, *dmax = nullptr;
   double* lscratch = nullptr;
   double* hbx = nullptr;
+  unsigned long long* llq = nullptr;   // tagged hand-off words of the chain (QpChainArgs::llq)
+  unsigned llq_epoch = 0;              // chain launches so far (tagq0 = epoch (p + 1))
   double *Ninv = nullptr, *cond = nullptr;
   unsigned* bar = nullptr;
   int32_t* ctrl = nullptr;
@@ -904,6 +974,15 @@ int qp_chain(rac_qp_ctx* c, double tol_p, double tol_d, int fixed, int t0, int t
   using namespace rac;
   cudaMemsetAsync(c->bar, 0, sizeof(unsigned), c->st);
   QpChainArgs a{};
+  if (c->llq) {
+    if ((unsigned long long)(c->llq_epoch + 2u) * (unsigned)(c->p + 1) >= 0xfffffff0ull) {
+      cudaMemsetAsync(c->llq, 0, 4 * (size_t)c->s * sizeof(unsigned long long), c->st);   // tag space used up
+      c->llq_epoch = 0;
+    }
+    ++c->llq_epoch;
+    a.llq = c->llq;
+    a.tagq0 = c->llq_epoch * (unsigned)(c->p + 1);
+  }
   a.n = c->n;
   a.m = c->m;
   a.lda = c->lda;
@@ -1005,7 +1084,7 @@ extern "C" int rac_qp_create(rac_qp_ctx** out, int64_t n, int64_t m, int32_t blo
       (rc = qalloc(c, &c->idx, (size_t)c->p * c->s)) || (rc = qalloc(c, &c->order, c->p)) ||
       (rc = qalloc(c, &c->info, c->p)) || (rc = qalloc(c, &c->Mb, sqs)) || (rc = qalloc(c, &c->Hbb, sqs)) ||
       (rc = qalloc(c, &c->inv, sqs)) || (rc = qalloc(c, &c->partial, (size_t)c->P * c->s)) ||
-      (rc = qalloc(c, &c->delta, c->s)) || (rc = qalloc(c, &c->pmax, c->P)) || (rc = qalloc(c, &c->psum, c->P)) ||
+      (rc = qalloc(c, &c->delta, 2 * (size_t)c->s)) || (rc = qalloc(c, &c->pmax, c->P)) || (rc = qalloc(c, &c->psum, c->P)) ||
       (rc = qalloc(c, &c->dmax, c->P)) || (rc = qalloc(c, &c->bar, 1)) || (rc = qalloc(c, &c->ctrl, 4)) ||
       (rc = qalloc(c, &c->hbx, 2 * (size_t)c->s)) || (rc = qalloc(c, &c->Ninv, sqs)) || (rc = qalloc(c, &c->cond, c->p))) {
     rac_qp_destroy(c);
@@ -1019,6 +1098,17 @@ extern "C" int rac_qp_create(rac_qp_ctx** out, int64_t n, int64_t m, int32_t blo
   if (scr && (rc = qalloc(c, &c->scratch, scr / sizeof(double)))) {
     rac_qp_destroy(c);
     return rc;
+  }
+  {
+    // tagged hx / partial hand-off of the chain (one grid barrier per block); RAC_QP_LL=0: two barriers
+    const char* e = getenv("RAC_QP_LL");
+    if (!(e && atoi(e) == 0)) {
+      if ((rc = qalloc(c, &c->llq, 4 * (size_t)c->s))) {
+        rac_qp_destroy(c);
+        return rc;
+      }
+      cudaMemsetAsync(c->llq, 0, 4 * (size_t)c->s * sizeof(unsigned long long), c->st);
+    }
   }
   if ((rc = qalloc(c, &c->lscratch, (size_t)c->s * (c->s + 1)))) {
     rac_qp_destroy(c);

@@ -85,6 +85,40 @@ def test_solve_matches_reference(dev, golden, tag):
         assert abs(got - want) <= OBJ_TOL * max(abs(want), 1e-12)
 
 
+@pytest.mark.parametrize("tag", ["box_rac", "medium_box", "h_only"])
+def test_solve_two_barriers_per_block(dev, golden, tag, monkeypatch):
+    """RAC_QP_LL=0 keeps the chain's two grid barriers per block (the default hands hx at the next
+    block's coordinates and the constraint rows' partial to CTA 0 as tagged words and has one):
+    same per-sweep iterates against the reference's golden vectors."""
+    monkeypatch.setenv("RAC_QP_LL", "0")
+    test_solve_matches_reference(dev, golden, tag)
+
+
+@pytest.mark.parametrize("ll", ["0", "1"])
+def test_train_handoff_modes_agree_with_oracle(dev, ll, monkeypatch):
+    """svm.train (one constraint row: the tagged hx / partial hand-off path) on a shape with a short
+    last block and several column strips, in both hand-off modes, per sweep against the oracle."""
+    from oracle import rac_oracle as ro
+    from paper_1907_01995_b200 import svm
+    from paper_1907_01995_b200.problems import SolverConfig
+    monkeypatch.setenv("RAC_QP_LL", ll)
+    rng = np.random.default_rng(5)
+    N, d, s = 1230, 12, 100
+    X = rng.standard_normal((N, d))
+    y = np.where(X[:, 0] + 0.3 * rng.standard_normal(N) > 0, 1.0, -1.0)
+    want = {}
+    ro.svm_train(X, y, C=1.0, block_size=s, beta=1.0, max_iters=6, seed=4, fixed_iterations=True,
+                 on_sweep=lambda k, blocks, z, nu, primal, dual: want.__setitem__(k, (z.copy(), float(nu))))
+    got = {}
+    svm.train(X, y, 1.0, svm.KernelSpec("linear"),
+              SolverConfig(block_size=s, beta_penalty=1.0, max_iters=6, seed=4, fixed_iterations=True),
+              sweep_hook=lambda k, z, nu: got.__setitem__(k, (z, float(nu))))
+    assert len(got) == len(want) == 6
+    for k in want:
+        assert rel(got[k][0], want[k][0]) <= ITER_TOL, (ll, k)
+        assert abs(got[k][1] - want[k][1]) <= ITER_TOL * max(1.0, abs(want[k][1])), (ll, k)
+
+
 def test_solve_invalid_problem(dev):
     from paper_1907_01995_b200 import engine
     from paper_1907_01995_b200.problems import QpProblem, SolverConfig

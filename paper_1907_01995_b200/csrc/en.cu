@@ -51,19 +51,17 @@ struct EnChainArgs {
   double *hist_p, *hist_d;
   long long* trace;     // optional: %globaltimer at every phase boundary (CTA 0)
   int rw;               // RC == 0 (one-tile resident row phase): rows per CTA
-  // RC == 0: per-block hand-offs (partials -> S1, rhs -> S2, delta -> row phase) as tagged 64-bit
-  // word pairs (rac_common.cuh ll_store) that the reader spins on, instead of a grid barrier.
-  // Layout: partials [s][P][2], rhs [s][2], delta [s][2]; tag of block step t = tag0 + t + 1
-  // (unique per launch and step).  Each buffer is rewritten for step t + 1 only after every reader
-  // of step t is done: a writer of step t + 1 data depends, through the chain itself, on all of
-  // step t's readers' outputs.  Default (ll_mask = 1 + the fused S phase below): the partials, where
-  // every word has ONE reader (measured on config 5: chain 3.94 -> 3.65 ms per sweep, 3.54 with the
-  // fused S phase).  A tagged rhs broadcast (bit 2: 16 000 threads polling the same 8 KB delay its
-  // writers) is slower, 4.02 ms; delta as one private tagged copy per consumer CTA (bit 4) is
-  // within noise of the barrier (3.49 vs 3.54 ms) and stays off.
+  // RC == 0: the row phase's partials reach the S phase as tagged 64-bit word pairs (rac_common.cuh
+  // ll_store) that the reader spins on, instead of behind a grid barrier.  Layout: partials
+  // [s][P][2], then the fused S phase's CTA sums [s][ceil(s / 8)][2]; tag of block step t =
+  // tag0 + t + 1 (unique per launch and step).  Each buffer is rewritten for step t + 1 only
+  // after every reader of step t is done: a writer of step t + 1 data depends, through the chain
+  // itself, on all of step t's readers' outputs.  Every tagged word has ONE reader; the broadcast
+  // hand-offs (rhs to all S warps, delta to all CTAs) were measured slower as tagged words — the
+  // pollers of a shared 8 KB delay its writers — and stay behind a grid barrier.
   unsigned long long* ll;
   unsigned tag0;
-  int ll_mask;   // 1: partials -> S1, 2: rhs -> S2, 4: delta -> row phase (the others keep their grid barrier)
+  int ll_mask;   // 1: tagged partials (0: grid barrier)
   // fused S phase (needs the tagged partials; one pass: every column has its own warp, s <= 512):
   // warp j scales row j of the symmetric inverse by rhs_j, the CTA sums its 8 scaled rows in shared
   // memory (fuse_off: byte offset of the [8][s] buffer) and publishes them as tagged words
@@ -77,7 +75,7 @@ struct EnChainArgs {
 // RC > 0: row chunks of RC rows streamed through shared memory; RC == 0: each CTA owns
 // `rw` contiguous rows and keeps the current block's tile resident (row_phase_1t)
 template <int RC>
-__global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
+__global__ void __maxnreg__(192) en_chain_kernel(EnChainArgs a) {
   if (a.ctrl[0]) return;
   extern __shared__ __align__(16) double esm[];
   const int s = a.s;
@@ -115,24 +113,15 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
   if (tr) a.trace[tp++] = gtimer();
   int bnext = a.order ? a.order[0] : 0;
   const bool LL = (RC == 0) && a.ll != nullptr;
-  const bool LLP = LL && (a.ll_mask & 1), LLR = LL && (a.ll_mask & 2), LLD = LL && (a.ll_mask & 4);
+  const bool LLP = LL && (a.ll_mask & 1);
   unsigned long long* const llp = LLP ? a.ll : nullptr;
-  unsigned long long* const ll_rhs = LLR ? a.ll + 2 * (size_t)s * P : nullptr;
-  // delta: one private copy per consumer CTA ([P][s][2] behind the S-phase words), so that every
-  // tagged word has one reader
-  const int NSCc = (s + ENT / 32 - 1) / (ENT / 32);
-  unsigned long long* const ll_del = LLD ? a.ll + 2 * ((size_t)s * P + 2 * (size_t)s + (size_t)s * NSCc) : nullptr;
-  auto publish_delta = [&](int i, double dv, unsigned tag) {   // whole warp: delta_i into every CTA's copy
-    for (int q = lane; q < P; q += 32) ll_store(ll_del + 2 * ((size_t)q * s + i), dv, tag);
-  };
-  const unsigned long long* const my_del = LLD ? ll_del + 2 * (size_t)blockIdx.x * s : nullptr;
   const bool s_cta = blockIdx.x * (ENT / 32) < s;   // this CTA has S1 / S2 rows
-  const bool FUSE = LLP && a.fuse && !LLR;
+  const bool FUSE = LLP && a.fuse;
   if constexpr (RC == 0) {
     for (int i = threadIdx.x; i < nr1; i += ENT) w1.sR[i] = a.r[r0 + i];
     __syncthreads();
     row_phase_1t(a.Xc, a.ld, r0, nr1, a.idx, s, -1, bnext, a.delta, a.beta, a.partial, w1, tfn, nullptr, false,
-                 llp, my_del, 0u, a.tag0 + 1u);
+                 llp, a.tag0 + 1u);
   } else {
     row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, -1, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
   }
@@ -156,7 +145,7 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
     if (FUSE) {
       if (s_cta) {
         const int NSC = (s + ENT / 32 - 1) / (ENT / 32);
-        unsigned long long* const ypart = a.ll + 2 * ((size_t)s * P + 2 * (size_t)s);
+        unsigned long long* const ypart = a.ll + 2 * (size_t)s * P;
         const double* Ibf = a.inv + (int64_t)b * s * s;
         const int j = gw;
         const bool mine = j < s;
@@ -237,7 +226,7 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
           if (lane == 0) {
             if (g >= 0) {
               const double bn = bsum;
-              if (!LLD) a.delta[j] = bn - bo;
+              a.delta[j] = bn - bo;
               a.beta[g] = bn;
               const double av = sub(xg, mul(gamma, bn));
               const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
@@ -246,10 +235,9 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
               my_sum += fabs(sub(bn, zn));
               my_max = fmax(my_max, fabs(sub(zn, zg)));
             } else {
-              if (!LLD) a.delta[j] = 0.0;
+              a.delta[j] = 0.0;
             }
           }
-          if (LLD) publish_delta(j, (g >= 0) ? bsum - bo : 0.0, tg);
         }
         __syncthreads();   // sV is rewritten by the next block's S phase
       } else if (tr) {
@@ -302,20 +290,11 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
           double cross = acc / m;
           rhs = -(sub(sub(add(cg, cross), xg), mul(gamma, zg)));
         }
-        if (LLR) ll_store(ll_rhs + 2 * j, rhs, tg);
-        else a.rhs[j] = rhs;
+        a.rhs[j] = rhs;
       }
     }
     if (tr) a.trace[tp++] = gtimer();
-    if (!LLR) grid_barrier(a.bar, target, P);
-    // tagged rhs: the CTAs with S2 rows stage it in shared memory once (sDel is free between
-    // the row phases)
-    const double* rhs_src = a.rhs;
-    if (LLR && s_cta) {
-      ll_poll4(ll_rhs, threadIdx.x, ENT, s, tg, w1.sDel);   // s <= EN_QMAX * ENT
-      __syncthreads();
-      rhs_src = w1.sDel;
-    }
+    grid_barrier(a.bar, target, P);
     if (tr) a.trace[tp++] = gtimer();
     // ---- S2: beta_b = inv_b rhs, fused prox/dual/residual per coordinate
     const double* Ib = a.inv + (int64_t)b * s * s;
@@ -330,15 +309,12 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
         x0 = ldcg(a.xi + g);
       }
       double acc = 0.0;
-      if (LLR)
-        for (int j = lane; j < s; j += 32) acc += row[j] * rhs_src[j];
-      else
-        for (int j = lane; j < s; j += 32) acc += row[j] * ldcg(a.rhs + j);
+      for (int j = lane; j < s; j += 32) acc += row[j] * ldcg(a.rhs + j);
       acc = warp_sum(acc);
       if (lane == 0) {
         if (g >= 0) {
           const double bn = acc;
-          if (!LLD) a.delta[i] = bn - bo;
+          a.delta[i] = bn - bo;
           a.beta[g] = bn;
           const double av = sub(x0, mul(gamma, bn));
           const double zn = __ddiv_rn(neg_shrink(av, a.thr), a.den);
@@ -347,10 +323,9 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
           my_sum += fabs(sub(bn, zn));
           my_max = fmax(my_max, fabs(sub(zn, zo)));
         } else {
-          if (!LLD) a.delta[i] = 0.0;
+          a.delta[i] = 0.0;
         }
       }
-      if (LLD) publish_delta(i, (g >= 0) ? acc - bo : 0.0, tg);
     }
     // the next row phase's block: its beta (final until its own solve) gathered into shared
     // memory behind this CTA's S2 work, landing during the barrier (indices issued before S1)
@@ -358,13 +333,12 @@ __global__ void __launch_bounds__(ENT, 1) en_chain_kernel(EnChainArgs a) {
       if (t + 1 < a.p) row1t_gather_beta(s, a.beta, w1);
     if (tr) a.trace[tp++] = gtimer();
     }   // !FUSE
-    if (!LLD) grid_barrier(a.bar, target, P);
-    else if (LLR && s_cta) __syncthreads();   // S2 read the staged rhs from sDel; the row phase refills it with delta
+    grid_barrier(a.bar, target, P);
     if (tr) a.trace[tp++] = gtimer();
     bnext = (t + 1 < a.p) ? (a.order ? a.order[t + 1] : t + 1) : -1;
     if constexpr (RC == 0)
       row_phase_1t(a.Xc, a.ld, r0, nr1, a.idx, s, b, bnext, a.delta, a.beta, a.partial, w1, tfn,
-                   tr ? a.trace + 16 + 16 * (size_t)a.p + s + 4 * (size_t)t : nullptr, true, llp, my_del, tg, tg + 1u);
+                   tr ? a.trace + 16 + 16 * (size_t)a.p + s + 4 * (size_t)t : nullptr, true, llp, tg + 1u);
     else
       row_phase<RC>(a.Xc, a.ld, a.m, a.nrc, a.idx, s, b, bnext, a.delta, a.beta, a.r, a.partial, w, tfn);
     if (tr) a.trace[tp++] = gtimer();
@@ -488,7 +462,7 @@ struct rac_en_ctx {
   unsigned msg_tag = 0;  // lookahead-chain launches so far: tag of the tagged messages (never reset)
   unsigned long long* ll = nullptr;   // streaming one-tile chain: tagged hand-off words (EnChainArgs::ll)
   unsigned ll_epoch = 0;              // chain launches with tagged hand-offs so far (tag0 = epoch (p + 1))
-  int ll_mask = 1;                    // which hand-offs are tagged (RAC_EN_LL; EnChainArgs::ll_mask)
+  int ll_mask = 1;                    // tagged partials (RAC_EN_LL bit 1; EnChainArgs::ll_mask)
   bool fuse = false;                  // fused S phase (EnChainArgs::fuse; RAC_EN_LL bit 8, on by default)
   int hist_cap = 0;
   // device buffers
@@ -971,7 +945,7 @@ int en_chain(rac_en_ctx* c, double tol, cudaStream_t st, int nsw = 1) {
       // tag space used up (2^32 / (p + 1) launches): clear the words and start over
       const size_t nsc = (size_t)(c->s + ENT / 32 - 1) / (ENT / 32);
       cudaMemsetAsync(c->ll, 0,
-                      2 * ((size_t)c->s * c->P + 2 * (size_t)c->s + c->s * nsc + (size_t)c->P * c->s) *
+                      2 * ((size_t)c->s * c->P + c->s * nsc) *
                           sizeof(unsigned long long), st);
       c->ll_epoch = 0;
     }
@@ -1175,21 +1149,21 @@ extern "C" int rac_en_create(rac_en_ctx** out, int64_t m, int64_t n, int32_t blo
     return rc;
   }
   if (c->RC == 0 && c->P <= 256) {
-    // RAC_EN_LL: bit mask of the tagged hand-offs (1 partials, 2 rhs, 4 delta); 0: three grid barriers per block
+    // RAC_EN_LL: 1 tagged partials, + 8 the fused S phase (default 9); 0: three grid barriers per block
     const char* e = getenv("RAC_EN_LL");
     int want_fuse = 1;
     if (e) {
-      c->ll_mask = atoi(e) & 7;
+      c->ll_mask = atoi(e) & 1;
       want_fuse = (atoi(e) & 8) ? 1 : 0;
     }
     const int nsc = (s + ENT / 32 - 1) / (ENT / 32);
     if (c->ll_mask != 0 &&
-        (rc = dalloc(c, &c->ll, 2 * ((size_t)s * c->P + 2 * (size_t)s + (size_t)s * nsc + (size_t)c->P * s)))) {
+        (rc = dalloc(c, &c->ll, 2 * ((size_t)s * c->P + (size_t)s * nsc)))) {
       rac_en_destroy(c);
       return rc;
     }
     const size_t smf = (row1t_smem_bytes(s, c->rw) + 15) / 16 * 16 + (size_t)(ENT / 32) * s * sizeof(double);
-    if (want_fuse && (c->ll_mask & 1) && !(c->ll_mask & 2) && s <= 512 && c->P * (ENT / 32) >= s && smf <= 200 * 1024 &&
+    if (want_fuse && (c->ll_mask & 1) && s <= 512 && c->P * (ENT / 32) >= s && smf <= 200 * 1024 &&
         cudaFuncSetAttribute((void*)en_chain_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smf) ==
             cudaSuccess)
       c->fuse = true;

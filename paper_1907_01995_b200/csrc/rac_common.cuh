@@ -265,23 +265,6 @@ __device__ __forceinline__ void ll_load2(const unsigned long long* p, unsigned l
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
 }
 __device__ __forceinline__ bool ll_ok(unsigned long long w, unsigned tag) { return (unsigned)(w >> 32) == tag; }
-// `cnt` <= 4 tagged doubles at p[2 (j0 + k step)], k < cnt: all loads in flight, then the late ones re-polled
-__device__ __forceinline__ void ll_poll4(const unsigned long long* p, int j0, int step, int n, unsigned tag, double* out) {
-  unsigned long long w0[4], w1[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int j = j0 + k * step;
-    if (j < n) ll_load2(p + 2 * (size_t)j, w0[k], w1[k]);
-  }
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int j = j0 + k * step;
-    if (j < n) {
-      while (!(ll_ok(w0[k], tag) && ll_ok(w1[k], tag))) ll_load2(p + 2 * (size_t)j, w0[k], w1[k]);
-      out[j] = __longlong_as_double((long long)(((w1[k] & 0xffffffffull) << 32) | (w0[k] & 0xffffffffull)));
-    }
-  }
-}
 __device__ __forceinline__ double ll_value(unsigned lo, unsigned hi) {
   return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
 }

@@ -278,11 +278,9 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
                              const int32_t* __restrict__ idx, int s, int bprev, int bnext, const double* delta,
                              const double* xsrc, double* partial, const Row1tSmem& w, TFn tfn,
                              long long* rt = nullptr, bool pre_gathered = false,
-                             unsigned long long* ll_part = nullptr, const unsigned long long* ll_del = nullptr,
-                             unsigned tag_prev = 0u, unsigned tag_next = 0u) {
-  // tagged hand-offs (rac_common.cuh ll_store): ll_del != nullptr: delta arrives as tagged words
-  // (tag_prev; the reader spins on the data itself); ll_part != nullptr: the partials leave as
-  // tagged words (tag_next)
+                             unsigned long long* ll_part = nullptr, unsigned tag_next = 0u) {
+  // ll_part != nullptr: the partials leave as tagged words (rac_common.cuh ll_store, tag_next) that
+  // the S phase spins on
   // rt (tracing, CTA 0 thread 0): %globaltimer after (a) + the issue of the loads, after the
   // first chunk landed, after (c), after (d)
   const int tid = threadIdx.x;
@@ -293,11 +291,8 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
   const bool act = grp < G;
   // chunk width: a multiple of 4 G columns (the dot products' four chains of stride G)
   const int CH = (((s + R1T_NC - 1) / R1T_NC + 4 * G - 1) / (4 * G)) * (4 * G);
-  if (bprev >= 0 && ll_del) {
-    ll_poll4(ll_del, tid, RP_THREADS, s, tag_prev, w.sDel);   // s <= RP_QMAX * RP_THREADS
-  } else if (bprev >= 0) {
+  if (bprev >= 0)
     for (int j = tid; j < s; j += RP_THREADS) w.sDel[j] = ldcg(delta + j);
-  }
   if (bnext >= 0 && !pre_gathered)
     for (int j = tid; j < s; j += RP_THREADS) {
       const int g = idx[(int64_t)bnext * s + j];

@@ -18,6 +18,10 @@
 //      belongs to exactly one block and z/xi of other blocks are untouched)
 //   -- grid barrier --
 //
+// The one-tile streaming chain (RC == 0, config 5) keeps only the last of these barriers: the
+// partials reach the S phase as tagged words, and S1 / S2 are one fused phase (EnChainArgs::ll,
+// ::fuse below).
+//
 // X is stored column-major with a leading dimension padded to 32 rows (zero
 // rows), so a block's column gather is a set of contiguous, coalesced reads.
 #include <algorithm>

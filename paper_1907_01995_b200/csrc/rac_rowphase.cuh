@@ -307,9 +307,21 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
   // and chunk was ~0.45 us of instructions per chunk)
   const int pj0 = tid / h, pi0 = tid - pj0 * h;
   const int pdj = RP_THREADS / h, pdi = RP_THREADS - pdj * h;
+  // h <= RP_THREADS (always, for tiles that fit): thread = (column lane pj0 < pdj, FIXED piece pi0),
+  // columns in steps of pdj — per piece one index load, one 64-bit multiply-add and the copy
+  const double* const vsrc = V + r0 + 2 * pi0;
+  double* const vdst = w.tile + 2 * pi0;
   auto issue_chunk = [&](int c) {
     const int cb = min(c * CH, s), ce = min(cb + CH, s);
-    if (bnext >= 0) {
+    if (bnext >= 0 && pdj >= 1) {
+      if (pj0 < pdj)
+        for (int j = cb + pj0; j < ce; j += pdj) {
+          const int g = w.sIdx[j];
+          double* d = vdst + (size_t)j * w.rwp;
+          if (g >= 0) cp_async16(d, vsrc + (int64_t)g * ld);
+          else d[0] = d[1] = 0.0;
+        }
+    } else if (bnext >= 0) {
       const int ncol = ce - cb;
       int jj = pj0, ii = pi0;
       while (jj < ncol) {

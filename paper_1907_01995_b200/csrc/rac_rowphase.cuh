@@ -398,11 +398,17 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
     const double* col = w.tile + (size_t)j * w.rwp;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int i = 0;
+    // 16-byte loads (the row stride and the tile base are even): lane j at j * rwp * 8 bytes is
+    // conflict-free for 16-byte accesses when rwp = 2 mod 4, and 2-way conflicted for 8-byte ones
+    const double2* col2 = reinterpret_cast<const double2*>(col);
+    const double2* t2 = reinterpret_cast<const double2*>(w.sT);
     for (; i + 4 <= nr; i += 4) {
-      a0 += col[i] * w.sT[i];
-      a1 += col[i + 1] * w.sT[i + 1];
-      a2 += col[i + 2] * w.sT[i + 2];
-      a3 += col[i + 3] * w.sT[i + 3];
+      const double2 c0 = col2[i >> 1], c1 = col2[(i >> 1) + 1];
+      const double2 u0 = t2[i >> 1], u1 = t2[(i >> 1) + 1];
+      a0 += c0.x * u0.x;
+      a1 += c0.y * u0.y;
+      a2 += c1.x * u1.x;
+      a3 += c1.y * u1.y;
     }
     for (; i < nr; ++i) a0 += col[i] * w.sT[i];
     // column-major partials [j][cta]: the S1 reduction then reads each column's P partials

@@ -267,7 +267,7 @@ __device__ __forceinline__ double dot4_finish(Dot4& d, const double* col, const 
   return (d.a0 + d.a1) + (d.a2 + d.a3);
 }
 
-constexpr int R1T_NC = 4;   // column chunks of the tile pipeline
+constexpr int R1T_NC = 3;   // column chunks of the tile pipeline (measured on config 5: chain 3.26 ms with 4, 3.13 with 3, 3.25 with 2)
 
 // Columns of the tile are released chunk by chunk while (a) runs and refilled at once with
 // the next block's columns (16-byte cp.async, one group per chunk); (c) consumes the chunks as
@@ -374,8 +374,8 @@ __device__ void row_phase_1t(const double* __restrict__ V, int64_t ld, int64_t r
 #pragma unroll
     for (int c = 0; c < R1T_NC; ++c) {
       if (c == 0) cp_async_wait<R1T_NC - 1>();
-      else if (c == 1) cp_async_wait<R1T_NC - 2>();
-      else if (c == 2) cp_async_wait<R1T_NC - 3>();
+      else if (c == 1) cp_async_wait<(R1T_NC >= 2 ? R1T_NC - 2 : 0)>();
+      else if (c == 2) cp_async_wait<(R1T_NC >= 3 ? R1T_NC - 3 : 0)>();
       else cp_async_wait<0>();
       __syncthreads();
       if (rt && c == 0) rt[1] = gtimer();

@@ -728,16 +728,16 @@ def measure_svm(cfg, case, args, world, rank, local, peaks, headline: bool) -> d
     gc.collect()
     torch.cuda.synchronize()
     dist_barrier(world)
-    # median of three complete trains: a single one occasionally pays the device memory pool's
-    # regrowth for the 8 N^2 bytes of Q after other configs' contexts were trimmed (measured: 50 vs
-    # 110 - 146 sweeps/s for the same code)
+    # median of five complete trains: single trains on the bench box show sporadic 70 - 200 ms
+    # stalls (measured: 50 vs 110 - 148 sweeps/s for the same code; back-to-back trains in a fresh
+    # process are stable at 135 ms, scripts/prof_train_rep.py)
     reps = []
-    for _ in range(3):
+    for _ in range(5):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         svm.train(X, y, case.C, svm.KernelSpec("linear"), cfgk)
         reps.append(time.perf_counter() - t0)
-    t_e2e = dist_max(sorted(reps)[1], world, dev)
+    t_e2e = dist_max(sorted(reps)[len(reps) // 2], world, dev)
     # the same train with kernel strips formed on the fly (no resident N x N matrix: the
     # reference's own scheme) — what runs when Q does not fit in HBM
     os.environ["RAC_SVM_STRIPS"] = "1"
@@ -768,7 +768,7 @@ def measure_svm(cfg, case, args, world, rank, local, peaks, headline: bool) -> d
         "e2e": {"value": world * K / t_e2e, "unit": "sweeps/s",
                 "h2d_bytes_per_step": int((8 * N * d + 8 * N) / K + 8 * N),
                 "d2h_bytes_per_step": int((8 * N + 8) / K + 32),
-                "timed": "median of 3 complete svm.train calls on host arrays (each: upload, Q = X X', K sweeps, model)",
+                "timed": "median of 5 complete svm.train calls on host arrays (each: upload, Q = X X', K sweeps, model)",
                 "runs_s": [round(r, 4) for r in reps]},
         "roofline": {"kernel": "qp_chain_kernel", "bound": "hbm", "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
